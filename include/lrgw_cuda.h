@@ -1,0 +1,199 @@
+/* lrgw_cuda.h — C-ABI of liblrgw_cuda.so, the B200 (sm_100a) implementation of
+ * the low-rank epsilon^-1 hot path of arXiv 2403.12340 (reference: the
+ * header-only C++ library `lrgw`, /root/reference/proj/include/lrgw).
+ *
+ * Plain C: pointers, sizes, int status codes; no C++ or torch types. Every
+ * matrix is column-major float64 with an explicit leading dimension.
+ * The reference's C++ API (include/lrgw/*.hpp in this repo) is a thin layer
+ * over these entry points; INTEGRATION.md shows how a caller binds them.
+ *
+ * Status codes map 1:1 onto the reference exception taxonomy
+ * (errors.hpp:10-36, contour.hpp:92-96). A failing call leaves a message in
+ * lrgw_ctx_last_error(); LRGW_ERR_SINGULAR also sets lrgw_ctx_last_pivot().
+ * Calls are synchronous at the ABI (results are complete on return) unless
+ * the name carries `_async`. A context is single-threaded; concurrent
+ * contexts are allowed.
+ */
+#ifndef LRGW_CUDA_H_
+#define LRGW_CUDA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LRGW_ABI_VERSION 1
+
+enum lrgw_status {
+  LRGW_OK = 0,
+  LRGW_ERR_INVALID_INPUT = 1,        /* invalid_input   (errors.hpp:10-12) */
+  LRGW_ERR_GUARD_EXCEEDED = 2,       /* guard_exceeded  (errors.hpp:21-23) */
+  LRGW_ERR_NUMERIC = 3,              /* numeric_error   (errors.hpp:26-28) */
+  LRGW_ERR_SINGULAR = 4,             /* singular_matrix (errors.hpp:31-36) */
+  LRGW_ERR_CONTOUR_CONVERGENCE = 5,  /* contour_convergence_error (contour.hpp:92-96) */
+  LRGW_ERR_IO = 6,                   /* io_error        (errors.hpp:15-17) */
+  LRGW_ERR_CUDA = 7,                 /* device / library failure (no reference analogue) */
+  LRGW_ERR_UNSUPPORTED = 8,          /* reported as invalid_input by the C++ layer */
+  LRGW_ERR_INTERNAL = 9
+};
+
+/* PointSelector (isdf.hpp:28) */
+enum lrgw_point_selector { LRGW_QRCP_DIRECT = 0, LRGW_QRCP_SKETCHED = 1 };
+
+/* Build stages timed by lrgw_build (device time, CUDA events). */
+enum lrgw_stage {
+  LRGW_STAGE_SELECT = 0,  /* ISDF point selection                */
+  LRGW_STAGE_FIT = 1,     /* Theta = (Z C^T)(C C^T)^-1           */
+  LRGW_STAGE_FIT_SOLVE = 2, /* cuSOLVER leaf: G_mumu factor+inverse (inside FIT) */
+  LRGW_STAGE_CONTOUR = 3, /* Cauchy quadrature of the core T     */
+  LRGW_STAGE_FFT = 4,     /* cuFFT leaf: batched D2Z of Theta    */
+  LRGW_STAGE_PVP = 5,     /* Theta^T V Theta G-space SYRK        */
+  LRGW_STAGE_SMW = 6,     /* cuSOLVER leaf: SMW core K           */
+  LRGW_STAGE_TOTAL = 7,
+  LRGW_NUM_STAGES = 8
+};
+
+typedef struct lrgw_ctx_s* lrgw_ctx;
+typedef struct lrgw_eps_s* lrgw_eps; /* device-resident factored eps^-1 (smw.hpp:77-82) */
+
+int lrgw_abi_version(void);
+
+/* ---- context ------------------------------------------------------------- */
+int lrgw_ctx_create(int device, lrgw_ctx* out);
+int lrgw_ctx_destroy(lrgw_ctx ctx);
+int lrgw_ctx_set_stream(lrgw_ctx ctx, void* cuda_stream); /* NULL = context-owned stream */
+void* lrgw_ctx_stream(lrgw_ctx ctx);
+int lrgw_ctx_synchronize(lrgw_ctx ctx);
+const char* lrgw_ctx_last_error(lrgw_ctx ctx);
+int lrgw_ctx_last_pivot(lrgw_ctx ctx);
+/* Per-stage device milliseconds of the last lrgw_build (LRGW_NUM_STAGES). */
+int lrgw_ctx_stage_ms(lrgw_ctx ctx, double* ms, int n);
+/* Kernel launches issued by this context since creation (own kernels only). */
+long long lrgw_ctx_kernel_launches(lrgw_ctx ctx);
+/* Candidate-set size of the batched greedy point selection (default 64). */
+int lrgw_ctx_set_select_batch(lrgw_ctx ctx, int s);
+
+/* ---- host-scalar contour geometry ----------------------------------------- */
+int lrgw_num_aux(double k_mu, int n1, int n2, int* out);                 /* isdf.hpp:42-46 */
+int lrgw_elliptic_k(double k, double* out);                              /* elliptic.hpp:28-33 */
+int lrgw_jacobi_sn_cn_dn(double u, double k, double* out3);              /* elliptic.hpp:48-85 */
+int lrgw_jacobi_complex(double x, double y, double k, double* out6);     /* elliptic.hpp:97-118 */
+/* spec7 = {q, Q, r, R, L, e_shift, bypass}                                  contour.hpp:35-71 */
+int lrgw_elliptic_params(const double* energies, int n_e, int n_v, int n_c, double delta_rel,
+                         int max_nodes, double* spec7);
+int lrgw_cauchy_error_bound(const double* spec7, int n_lambda, double* out); /* contour.hpp:75-80 */
+
+/* ---- host-buffer API: drop-in bodies of the reference free functions ------ */
+/* select_interpolation_points (isdf.hpp:95-112); pts sorted ascending. */
+int lrgw_select_interpolation_points(lrgw_ctx ctx, const double* psi_a, const double* psi_b,
+                                     int n_r, int n1, int n2, int n_mu, int method, int32_t* pts);
+/* fit_auxiliary_basis (isdf.hpp:118-163): theta is n_r x n_mu. */
+int lrgw_fit_auxiliary_basis(lrgw_ctx ctx, const double* psi_a, const double* psi_b, int n_r,
+                             int n1, int n2, const int32_t* pts, int n_mu, double* theta);
+/* coupled_coefficients_direct (contour.hpp:114-137). */
+int lrgw_coupled_coefficients_direct(lrgw_ctx ctx, const double* psi_v_pts,
+                                     const double* psi_c_pts, int n_mu, int n_v, int n_c,
+                                     const double* energies, int n_e, double* t);
+/* detail::sum_node_terms (contour.hpp:185-222): acc = sum_k w_k term_k. */
+int lrgw_sum_node_terms(lrgw_ctx ctx, const double* psi_v_pts, const double* psi_c_pts, int n_mu,
+                        int n_v, int n_c, const double* energies, int n_e, const double* spec7,
+                        const double* nodes, const double* weights, int n_nodes, double* acc);
+/* Fixed closed trapezoid of n_lambda intervals (n_lambda + 1 nodes), times the
+ * prefactor and symmetrised — the BASELINE configs' quadrature. */
+int lrgw_coupled_coefficients_fixed(lrgw_ctx ctx, const double* psi_v_pts,
+                                    const double* psi_c_pts, int n_mu, int n_v, int n_c,
+                                    const double* energies, int n_e, int n_lambda, double* t);
+/* coupled_coefficients_contour (contour.hpp:298-329). On
+ * LRGW_ERR_CONTOUR_CONVERGENCE `t`, nodes_used and est_rel hold the best estimate. */
+int lrgw_coupled_coefficients_contour(lrgw_ctx ctx, const double* psi_v_pts,
+                                      const double* psi_c_pts, int n_mu, int n_v, int n_c,
+                                      const double* energies, int n_e, double delta_rel,
+                                      int max_nodes, double* t, int* nodes_used, double* est_rel);
+/* contour_refinement_levels (contour.hpp:282-294): up to max_levels estimates. */
+int lrgw_contour_refinement_levels(lrgw_ctx ctx, const double* psi_v_pts,
+                                   const double* psi_c_pts, int n_mu, int n_v, int n_c,
+                                   const double* energies, int n_e, int max_level_nodes,
+                                   int max_levels, double* out, int* counts, int* n_levels);
+/* build_coulomb kernel (model.hpp:165-195), length n_r. */
+int lrgw_coulomb_kernel(const int* dims, const double* cell, double* kernel);
+/* apply_coulomb (model.hpp:208-223); zero_kernel selects zero_coulomb (198-204). */
+int lrgw_apply_coulomb(lrgw_ctx ctx, const int* dims, const double* cell, int zero_kernel,
+                       const double* x, int m, double* y);
+/* assemble_K (smw.hpp:42-73). */
+int lrgw_assemble_K(lrgw_ctx ctx, const double* t, const double* p, int n_r, int n_mu,
+                    const int* dims, const double* cell, int zero_kernel, double* k);
+/* build_epsilon_inverse (smw.hpp:84-94): uploads P, keeps P and K on device. */
+int lrgw_build_epsilon_inverse(lrgw_ctx ctx, const double* t, const double* p, int n_r, int n_mu,
+                               const int* dims, const double* cell, int zero_kernel,
+                               lrgw_eps* out);
+/* An eps handle from host P and a caller-supplied K (e.g. the K = 0 identity). */
+int lrgw_eps_from_parts(lrgw_ctx ctx, const double* p, const double* k, int n_r, int n_mu,
+                        const int* dims, const double* cell, int zero_kernel, lrgw_eps* out);
+/* epsilon_inverse_apply (smw.hpp:97-103): Y = X + V P (K (P^T X)), X n_r x m. */
+int lrgw_epsilon_inverse_apply(lrgw_ctx ctx, lrgw_eps e, const double* x, int m, double* y);
+/* Host copies of the factors (any pointer may be NULL). vp = V P is formed on demand. */
+int lrgw_eps_get(lrgw_ctx ctx, lrgw_eps e, double* k, double* p, double* vp, double* t,
+                 int32_t* pts);
+int lrgw_eps_shape(lrgw_eps e, int* n_r, int* n_mu);
+int lrgw_eps_destroy(lrgw_eps e);
+
+/* ---- device-pointer API (the hot path; all pointers in device memory) ----- */
+typedef struct {
+  int n_r, n_v, n_c;
+  int dims[3];
+  double cell[3];
+  double k_mu;       /* N_mu = clamp(llround(k_mu sqrt(N_v N_c)), 1, N_r) (isdf.hpp:42-46, 180) */
+  int n_lambda;      /* > 0: fixed trapezoid of n_lambda intervals; 0: adaptive (delta_rel) */
+  double delta_rel;  /* adaptive stopping rule (contour.hpp:313-320) */
+  int max_nodes;     /* adaptive node cap (contour.hpp:31) */
+  int zero_kernel;   /* 1: V = 0 (zero_coulomb) */
+} lrgw_build_params;
+
+/* The factored eps^-1 build, stages 1-5, from device-resident orbitals
+ * phi_v (n_r x n_v, ld ldv) and phi_c (n_r x n_c, ld ldc) and host energies
+ * (ascending, n_v + n_c). Stage device times: lrgw_ctx_stage_ms. */
+int lrgw_build(lrgw_ctx ctx, const lrgw_build_params* prm, const double* phi_v, long long ldv,
+               const double* phi_c, long long ldc, const double* energies, lrgw_eps* out);
+/* Device pointers owned by the handle (n_r x n_mu Theta, n_mu^2 K and T). */
+int lrgw_eps_device_ptrs(lrgw_eps e, double** theta, double** k, double** t);
+/* eps^-1 applied to a device block: y = x + V Theta (K (Theta^T x)). */
+int lrgw_eps_apply_dev(lrgw_ctx ctx, lrgw_eps e, const double* x, long long ldx, int m, double* y,
+                       long long ldy);
+
+/* Stage-level device entry points (multi-rank orchestration composes these). */
+int lrgw_dev_select(lrgw_ctx ctx, const double* a, long long lda, int n1, const double* b,
+                    long long ldb, int n2, int n_r, int n_mu, int32_t* pts_host,
+                    double* min_margin);
+int lrgw_dev_fit(lrgw_ctx ctx, const double* a, long long lda, int n1, const double* b,
+                 long long ldb, int n2, int n_r, const int32_t* pts_host, int n_mu,
+                 double* theta, long long ldt);
+/* Fit for a row panel [row0, row0 + rows) of Theta given the full point-row
+ * factors a_mu (n_mu x n1) and b_mu (n_mu x n2): rank-local, no exchange. */
+int lrgw_dev_fit_panel(lrgw_ctx ctx, const double* a, long long lda, int n1, const double* b,
+                       long long ldb, int n2, int rows, const double* a_mu, const double* b_mu,
+                       const double* g_inv, int n_mu, double* theta, long long ldt);
+/* Partial node sum over nodes [node0, node0 + count) of an n_lambda-interval
+ * trapezoid, unscaled (acc = sum w_k term_k, lower triangle mirrored). */
+int lrgw_dev_contour_partial(lrgw_ctx ctx, const double* pv, long long ldv, const double* pc,
+                             long long ldpc, int n_mu, int n_v, int n_c, const double* energies,
+                             int n_e, int n_lambda, int node0, int count, double* acc);
+int lrgw_dev_contour_fixed(lrgw_ctx ctx, const double* pv, long long ldv, const double* pc,
+                           long long ldpc, int n_mu, int n_v, int n_c, const double* energies,
+                           int n_e, int n_lambda, double* t, long long ldt);
+int lrgw_dev_pvp(lrgw_ctx ctx, const int* dims, const double* cell, int zero_kernel,
+                 const double* theta, long long ldt, int n_mu, double* pvp);
+int lrgw_dev_smw_core(lrgw_ctx ctx, const double* t, const double* pvp, int n_mu, double* k);
+int lrgw_dev_coulomb_apply(lrgw_ctx ctx, const int* dims, const double* cell, int zero_kernel,
+                           const double* x, long long ldx, int m, double* y, long long ldy);
+/* Plain FP64 GEMM through the path's DMMA engine: C = alpha op(A) op(B) + beta C,
+ * trans = 'N' | 'T' (BLAS semantics). Exposed for tests and benchmarking. */
+int lrgw_dev_dgemm(lrgw_ctx ctx, char trans_a, char trans_b, int m, int n, int k, double alpha,
+                   const double* a, long long lda, const double* b, long long ldb, double beta,
+                   double* c, long long ldc);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LRGW_CUDA_H_ */

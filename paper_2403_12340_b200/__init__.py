@@ -1,0 +1,12 @@
+"""paper_2403_12340_b200 — B200-native (sm_100a) low-rank dielectric-matrix
+inversion of arXiv 2403.12340 behind the reference `lrgw` interface.
+
+    csrc/      hand-written CUDA kernels + the C-ABI (include/lrgw_cuda.h)
+    lib/       liblrgw_cuda.so (built in-tree)
+    lrgw.py    Python mirror of the reference hot-path API over the C-ABI
+    synth.py   seeded synthetic Si-like / C60-like workloads (BASELINE configs)
+    dist.py    multi-rank orchestration (node / row-panel sharding)
+"""
+from . import lrgw  # noqa: F401  (raises ImportError when the extension is missing)
+
+__all__ = ["lrgw"]

@@ -1,0 +1,1253 @@
+// capi.cu — the C-ABI of liblrgw_cuda.so (include/lrgw_cuda.h).
+//
+// Host orchestration of the B200 hot path: context (stream, cuSOLVER handle,
+// cuFFT plan cache), device scratch through the stream-ordered allocator,
+// stage timing with CUDA events, and the mapping of every failure onto the
+// reference exception taxonomy (errors.hpp:10-36). Stage math lives in the
+// kernels (gemm.cu, quadrature.cu, select.cu, coulomb.cu, misc.cu); cuFFT
+// and cuSOLVER are used only as leaf calls (3-D FFT, N_mu x N_mu factors).
+#include <cufft.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "elliptic.h"
+#include "kernels.h"
+#include "lrgw_cuda.h"
+#include "select.h"
+
+namespace lrgw_dev {
+static std::atomic<long long> g_launches{0};
+long long launch_count() { return g_launches.load(); }
+void count_launches(int n) { g_launches += n; }
+}  // namespace lrgw_dev
+
+using namespace lrgw_dev;
+
+namespace {
+
+struct Fail {
+  int code;
+  std::string msg;
+  int pivot;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg, int pivot = -1) { throw Fail{code, msg, pivot}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(LRGW_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void ckf(cufftResult r, const char* what) {
+  if (r != CUFFT_SUCCESS) fail(LRGW_ERR_CUDA, std::string(what) + ": cufft error " + std::to_string((int)r));
+}
+void cks(cusolverStatus_t r, const char* what) {
+  if (r != CUSOLVER_STATUS_SUCCESS)
+    fail(LRGW_ERR_CUDA, std::string(what) + ": cusolver error " + std::to_string((int)r));
+}
+void host_status(int st, const char* what) {
+  if (st != lrgw_host::kOk) fail(st, what);
+}
+
+}  // namespace
+
+struct lrgw_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  int sm_count = 148;
+  cusolverDnHandle_t solver = nullptr;
+  std::map<std::tuple<int, int, int, int, long long, long long, int>, cufftHandle> plans;
+  std::string err;
+  int pivot = -1;
+  double stage_ms[LRGW_NUM_STAGES] = {};
+  long long launches0 = 0;
+  int select_batch = 64;
+};
+
+struct lrgw_eps_s {
+  lrgw_ctx ctx = nullptr;
+  int n_r = 0, n_mu = 0;
+  int dims[3] = {0, 0, 0};
+  double cell[3] = {0, 0, 0};
+  int zero = 0;
+  double* theta = nullptr;
+  double* k = nullptr;
+  double* t = nullptr;
+  std::vector<int32_t> pts;
+};
+
+namespace {
+
+// Device buffer from the stream-ordered pool (freed on scope exit).
+struct DBuf {
+  lrgw_ctx ctx = nullptr;
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  DBuf(lrgw_ctx c, size_t b) : ctx(c), bytes(b) {
+    if (b) ck(cudaMallocAsync(&p, b, c->stream), "cudaMallocAsync");
+  }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : ctx(o.ctx), p(o.p), bytes(o.bytes) { o.p = nullptr; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    release();
+    ctx = o.ctx;
+    p = o.p;
+    bytes = o.bytes;
+    o.p = nullptr;
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, ctx->stream);
+    p = nullptr;
+  }
+  double* d() const { return static_cast<double*>(p); }
+  int* i() const { return static_cast<int*>(p); }
+  void* take() {
+    void* q = p;
+    p = nullptr;
+    return q;
+  }
+};
+
+DBuf dalloc(lrgw_ctx c, size_t n) { return DBuf(c, n * sizeof(double)); }
+DBuf ialloc(lrgw_ctx c, size_t n) { return DBuf(c, n * sizeof(int)); }
+
+DBuf upload(lrgw_ctx c, const double* h, size_t n) {
+  DBuf b = dalloc(c, n);
+  if (n) ck(cudaMemcpyAsync(b.p, h, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
+  return b;
+}
+
+DBuf upload_i(lrgw_ctx c, const int32_t* h, size_t n) {
+  DBuf b = ialloc(c, n);
+  if (n) ck(cudaMemcpyAsync(b.p, h, n * sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D");
+  return b;
+}
+
+void download(lrgw_ctx c, void* h, const void* d, size_t bytes) {
+  if (bytes) ck(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+}
+
+void use_device(lrgw_ctx c) { ck(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+// The ABI wrapper: run the body, map failures onto status codes.
+template <class F>
+int guarded(lrgw_ctx c, F&& f) {
+  if (!c) return LRGW_ERR_INVALID_INPUT;
+  try {
+    use_device(c);
+    c->pivot = -1;
+    f();
+    return LRGW_OK;
+  } catch (const Fail& e) {
+    c->err = e.msg;
+    if (e.code == LRGW_ERR_SINGULAR) c->pivot = e.pivot;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    c->err = "host allocation failure";
+    return LRGW_ERR_INTERNAL;
+  } catch (...) {
+    c->err = "unknown failure";
+    return LRGW_ERR_INTERNAL;
+  }
+}
+
+template <class F>
+int guarded_host(F&& f) {
+  try {
+    f();
+    return LRGW_OK;
+  } catch (const Fail& e) {
+    return e.code;
+  } catch (...) {
+    return LRGW_ERR_INTERNAL;
+  }
+}
+
+lrgw_host::Spec spec_from7(const double* s7) {
+  lrgw_host::Spec s;
+  s.q = s7[0];
+  s.big_q = s7[1];
+  s.r = s7[2];
+  s.big_r = s7[3];
+  s.l = s7[4];
+  s.e_shift = s7[5];
+  s.bypass = s7[6] != 0.0;
+  return s;
+}
+
+void spec_to7(const lrgw_host::Spec& s, double* o) {
+  o[0] = s.q;
+  o[1] = s.big_q;
+  o[2] = s.r;
+  o[3] = s.big_r;
+  o[4] = s.l;
+  o[5] = s.e_shift;
+  o[6] = s.bypass ? 1.0 : 0.0;
+}
+
+void check_grid(const int* dims, const double* cell) {
+  for (int i = 0; i < 3; ++i) {
+    if (dims[i] < 2) fail(LRGW_ERR_INVALID_INPUT, "Grid: all dims must be >= 2");
+    if (!(cell[i] > 0.0)) fail(LRGW_ERR_INVALID_INPUT, "Grid: cell lengths must be > 0");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// cuFFT plans (leaf): batched 3-D D2Z / Z2D over columns, dims {n3, n2, n1}
+// row-major = the grid's linear index i1 + n1 (i2 + n2 i3) (grid.hpp:11).
+// ---------------------------------------------------------------------------
+cufftHandle get_plan(lrgw_ctx c, const int* dims, int batch, long long rdist, long long cdist,
+                     bool forward) {
+  const auto key = std::make_tuple(dims[0], dims[1], dims[2], batch, rdist, cdist, forward ? 1 : 0);
+  auto it = c->plans.find(key);
+  if (it != c->plans.end()) return it->second;
+  cufftHandle plan;
+  long long n[3] = {dims[2], dims[1], dims[0]};
+  long long rembed[3] = {dims[2], dims[1], dims[0]};
+  long long cembed[3] = {dims[2], dims[1], dims[0] / 2 + 1};
+  ckf(cufftCreate(&plan), "cufftCreate");
+  size_t work = 0;
+  if (forward)
+    ckf(cufftMakePlanMany64(plan, 3, n, rembed, 1, rdist, cembed, 1, cdist, CUFFT_D2Z, batch, &work),
+        "cufftMakePlanMany64(D2Z)");
+  else
+    ckf(cufftMakePlanMany64(plan, 3, n, cembed, 1, cdist, rembed, 1, rdist, CUFFT_Z2D, batch, &work),
+        "cufftMakePlanMany64(Z2D)");
+  ckf(cufftSetStream(plan, c->stream), "cufftSetStream");
+  c->plans[key] = plan;
+  return plan;
+}
+
+long long half_len(const int* dims) { return (long long)(dims[0] / 2 + 1) * dims[1] * dims[2]; }
+
+// xhat (complex, half spectrum, column stride half_len) = D2Z(x)
+void fft_forward(lrgw_ctx c, const int* dims, const double* x, long long ldx, int m, double* xhat) {
+  if (m <= 0) return;
+  cufftHandle plan = get_plan(c, dims, m, ldx, half_len(dims), true);
+  ckf(cufftExecD2Z(plan, const_cast<double*>(x), reinterpret_cast<cufftDoubleComplex*>(xhat)),
+      "cufftExecD2Z");
+}
+
+void fft_inverse(lrgw_ctx c, const int* dims, double* xhat, int m, double* y, long long ldy) {
+  if (m <= 0) return;
+  cufftHandle plan = get_plan(c, dims, m, ldy, half_len(dims), false);
+  ckf(cufftExecZ2D(plan, reinterpret_cast<cufftDoubleComplex*>(xhat), y), "cufftExecZ2D");
+}
+
+// y = V x = Re(F^-1 diag(v) F x) (model.hpp:208-223)
+void coulomb_apply(lrgw_ctx c, const int* dims, const double* cell, int zero, const double* x,
+                   long long ldx, int m, double* y, long long ldy) {
+  if (m <= 0) return;
+  const long long nh = half_len(dims);
+  DBuf xh = dalloc(c, (size_t)2 * nh * m);
+  fft_forward(c, dims, x, ldx, m, xh.d());
+  ck(coulomb_scale_half(c->stream, dims[0], dims[1], dims[2], cell[0], cell[1], cell[2], zero, xh.d(), m),
+     "coulomb_scale_half");
+  fft_inverse(c, dims, xh.d(), m, y, ldy);
+}
+
+// Split-K scratch for the skinny / symmetric GEMMs.
+struct Work {
+  DBuf buf;
+  size_t elems = 0;
+};
+
+Work make_work(lrgw_ctx c, size_t elems) {
+  Work w;
+  w.buf = dalloc(c, elems);
+  w.elems = elems;
+  return w;
+}
+
+void gemm(lrgw_ctx c, int M, int N, int K, const double* A, long long lda, Lay la, const double* B,
+          long long ldb, Lay lb, double* C, long long ldc, double alpha, double beta,
+          const double* scale = nullptr, bool lower = false, Work* w = nullptr) {
+  ck(dgemm(c->stream, M, N, K, A, lda, la, B, ldb, lb, C, ldc, alpha, beta, scale, lower, c->sm_count,
+           w ? w->buf.d() : nullptr, w ? w->elems : 0),
+     "dgemm");
+}
+
+// pvp = Theta^T V Theta via the half-spectrum G-space SYRK (smw.hpp:61-62):
+// one batched D2Z of Theta (cuFFT leaf), then a lower-triangle DMMA GEMM over
+// K = 2 * half_len interleaved reals with w_G v(G)/N_r fused as the scale.
+void pvp_impl(lrgw_ctx c, const int* dims, const double* cell, int zero, const double* theta,
+              long long ldt, int n_mu, double* pvp, cudaEvent_t ev_fft_end) {
+  const long long nh = half_len(dims);
+  DBuf xh = dalloc(c, (size_t)2 * nh * n_mu);
+  fft_forward(c, dims, theta, ldt, n_mu, xh.d());
+  if (ev_fft_end) ck(cudaEventRecord(ev_fft_end, c->stream), "event");
+  DBuf wts = dalloc(c, (size_t)2 * nh);
+  ck(coulomb_half_weights(c->stream, dims[0], dims[1], dims[2], cell[0], cell[1], cell[2], zero, wts.d()),
+     "coulomb_half_weights");
+  Work w = make_work(c, (size_t)8 * n_mu * n_mu);
+  gemm(c, n_mu, n_mu, (int)(2 * nh), xh.d(), 2 * nh, Lay::K, xh.d(), 2 * nh, Lay::K, pvp, n_mu, 1.0, 0.0,
+       wts.d(), true, &w);
+  ck(mirror_lower(c->stream, pvp, n_mu, n_mu, false), "mirror");
+}
+
+// ---------------------------------------------------------------------------
+// Dense N_mu x N_mu leaf factorisations (cuSOLVER).
+// ---------------------------------------------------------------------------
+double dev_max_abs(lrgw_ctx c, const double* x, size_t n) {
+  DBuf r = dalloc(c, 512);
+  ck(max_abs(c->stream, x, n, r.d()), "max_abs");
+  double h = 0;
+  download(c, &h, r.d() + 296, sizeof(double));
+  return h;
+}
+
+// In-place Cholesky of an SPD matrix (lower). Returns info (0 = ok).
+int potrf_lower(lrgw_ctx c, double* a, int n) {
+  int lwork = 0;
+  cks(cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, n, a, n, &lwork), "potrf_bufferSize");
+  DBuf work = dalloc(c, (size_t)std::max(lwork, 1));
+  DBuf info = ialloc(c, 1);
+  cks(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, n, a, n, work.d(), lwork, info.i()), "potrf");
+  int h = 0;
+  download(c, &h, info.p, sizeof(int));
+  return h;
+}
+
+void potri_lower(lrgw_ctx c, double* a, int n) {
+  int lwork = 0;
+  cks(cusolverDnDpotri_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, n, a, n, &lwork), "potri_bufferSize");
+  DBuf work = dalloc(c, (size_t)std::max(lwork, 1));
+  DBuf info = ialloc(c, 1);
+  cks(cusolverDnDpotri(c->solver, CUBLAS_FILL_MODE_LOWER, n, a, n, work.d(), lwork, info.i()), "potri");
+  int h = 0;
+  download(c, &h, info.p, sizeof(int));
+  if (h != 0) fail(LRGW_ERR_SINGULAR, "potri: singular factor", h - 1);
+  ck(mirror_lower(c->stream, a, n, n, false), "mirror");
+}
+
+// Smallest |L_kk|^2 of a Cholesky factor against the LU threshold
+// 1e-14 * max|A| (linalg.hpp:128, 137). Returns the offending index or -1.
+int tiny_pivot(lrgw_ctx c, const double* chol, int n, double max_abs_a) {
+  std::vector<double> diag(n);
+  // n is N_mu (<= a few thousand): one D2H of the factor's diagonal via a strided copy
+  ck(cudaMemcpy2DAsync(diag.data(), sizeof(double), chol, (size_t)(n + 1) * sizeof(double), sizeof(double),
+                       n, cudaMemcpyDeviceToHost, c->stream),
+     "D2H diag");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  const double tiny = 1e-14 * (max_abs_a > 0.0 ? max_abs_a : 1.0);
+  for (int i = 0; i < n; ++i)
+    if (diag[i] * diag[i] < tiny) return i;
+  return -1;
+}
+
+// Inverse of the symmetric ISDF Gram via LU with the reference singularity
+// rule (linalg.hpp:123-150); on a tiny pivot, the truncated-eigenvalue
+// pseudo-inverse of isdf.hpp:144-161. ginv is overwritten (n x n).
+void gram_inverse(lrgw_ctx c, const double* gram, int n, double* ginv) {
+  const double mx = dev_max_abs(c, gram, (size_t)n * n);
+  const double tiny = 1e-14 * (mx > 0.0 ? mx : 1.0);
+  DBuf lu = dalloc(c, (size_t)n * n);
+  ck(cudaMemcpyAsync(lu.p, gram, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, c->stream), "D2D");
+  int lwork = 0;
+  cks(cusolverDnDgetrf_bufferSize(c->solver, n, n, lu.d(), n, &lwork), "getrf_bufferSize");
+  DBuf work = dalloc(c, (size_t)std::max(lwork, 1));
+  DBuf ipiv = ialloc(c, n);
+  DBuf info = ialloc(c, 1);
+  cks(cusolverDnDgetrf(c->solver, n, n, lu.d(), n, work.d(), ipiv.i(), info.i()), "getrf");
+  std::vector<double> diag(n);
+  ck(cudaMemcpy2DAsync(diag.data(), sizeof(double), lu.d(), (size_t)(n + 1) * sizeof(double), sizeof(double), n,
+                       cudaMemcpyDeviceToHost, c->stream),
+     "D2H diag");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  bool singular = false;
+  for (int i = 0; i < n; ++i)
+    if (!(std::abs(diag[i]) >= tiny)) singular = true;
+  if (!singular) {
+    ck(fill(c->stream, ginv, (size_t)n * n, 0.0), "fill");
+    ck(add_diag(c->stream, ginv, n, n, 1.0), "add_diag");
+    cks(cusolverDnDgetrs(c->solver, CUBLAS_OP_N, n, n, lu.d(), n, ipiv.i(), ginv, n, info.i()), "getrs");
+    ck(mirror_lower(c->stream, ginv, n, n, true), "symmetrize");
+    return;
+  }
+  // pseudo-inverse fallback (isdf.hpp:144-161)
+  DBuf q = dalloc(c, (size_t)n * n);
+  ck(cudaMemcpyAsync(q.p, gram, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, c->stream), "D2D");
+  DBuf w = dalloc(c, n);
+  int lw2 = 0;
+  cks(cusolverDnDsyevd_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, q.d(), n, w.d(),
+                                  &lw2),
+      "syevd_bufferSize");
+  DBuf work2 = dalloc(c, (size_t)std::max(lw2, 1));
+  cks(cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, q.d(), n, w.d(), work2.d(),
+                       lw2, info.i()),
+      "syevd");
+  std::vector<double> hw(n);
+  int hinfo = 0;
+  ck(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  download(c, hw.data(), w.p, sizeof(double) * n);
+  if (hinfo != 0) fail(LRGW_ERR_NUMERIC, "fit_auxiliary_basis: eigensolver failed");
+  double lam_max = 0.0;
+  for (double v : hw) lam_max = std::max(lam_max, std::abs(v));
+  if (lam_max <= 0.0) fail(LRGW_ERR_NUMERIC, "fit_auxiliary_basis: degenerate Gram matrix");
+  std::vector<double> inv(n, 0.0);
+  int kept = 0;
+  for (int i = 0; i < n; ++i)
+    if (std::abs(hw[i]) > 1e-12 * lam_max) {
+      inv[i] = 1.0 / hw[i];
+      ++kept;
+    }
+  if (kept == 0) fail(LRGW_ERR_NUMERIC, "fit_auxiliary_basis: degenerate Gram matrix");
+  DBuf dinv = upload(c, inv.data(), n);
+  // pinv = Q diag(inv) Q^T  (A = Q: MN, B = Q: MN, scale on k)
+  gemm(c, n, n, n, q.d(), n, Lay::MN, q.d(), n, Lay::MN, ginv, n, 1.0, 0.0, dinv.d());
+}
+
+// K = (T^-1/2 - P^T V P)^-1 (smw.hpp:42-73) with Cholesky leaves: T must be
+// negative definite (the reference's sym_eig check, smw.hpp:47-51), then
+// 1/2 T^-1 = -1/2 (-T)^-1 and K = -(-M)^-1 with -M = 1/2 (-T)^-1 + pvp SPD.
+void smw_core(lrgw_ctx c, const double* t, const double* pvp, int n, double* k) {
+  const size_t nn = (size_t)n * n;
+  const double mx = dev_max_abs(c, t, nn);
+  DBuf negt = dalloc(c, nn);
+  ck(scale_copy(c->stream, t, negt.d(), nn, -1.0), "scale_copy");
+  if (potrf_lower(c, negt.d(), n) != 0)
+    fail(LRGW_ERR_NUMERIC, "assemble_K: T is not negative definite (gapless or rank-deficient input)");
+  const int tp = tiny_pivot(c, negt.d(), n, mx);
+  if (tp >= 0) fail(LRGW_ERR_SINGULAR, "assemble_K: T singular", tp);
+  potri_lower(c, negt.d(), n);  // (-T)^-1, full
+  // -M = 1/2 (-T)^-1 + pvp
+  DBuf negm = dalloc(c, nn);
+  ck(cudaMemcpyAsync(negm.p, pvp, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+  ck(axpby(c->stream, n, n, 0.5, negt.d(), n, 1.0, negm.d(), n), "axpby");
+  const double mx2 = dev_max_abs(c, negm.d(), nn);
+  if (potrf_lower(c, negm.d(), n) != 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", 0);
+  const int tp2 = tiny_pivot(c, negm.d(), n, mx2);
+  if (tp2 >= 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", tp2);
+  potri_lower(c, negm.d(), n);
+  ck(scale_copy(c->stream, negm.d(), k, nn, -1.0), "scale_copy");
+}
+
+// ---------------------------------------------------------------------------
+// Stage 1: ISDF point selection (isdf.hpp:95-112) — see select.cu.
+// ---------------------------------------------------------------------------
+std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int n1, const double* b,
+                                 long long ldb, int n2, int n_r, int n_mu, double* min_margin) {
+  if (n_mu > n_r) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: N_mu > N_r");
+  if (n_mu < 1) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: N_mu < 1");
+  if (n1 < 1 || n2 < 1) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: empty orbital set");
+  const long long m = (long long)n1 * n2;
+  const int kmax = (int)std::min<long long>(m, n_r);
+  const int steps = std::min(n_mu, kmax);
+  const int s = std::max(1, std::min({c->select_batch, select_max_candidates(), n_r}));
+  const int grid_blocks = select_grid_blocks(c->sm_count);
+
+  DBuf d = dalloc(c, n_r), pos = ialloc(c, n_r), perm = ialloc(c, n_r);
+  DBuf L = dalloc(c, (size_t)n_r * std::max(steps, 1));
+  DBuf W = dalloc(c, (size_t)n_r * s);
+  DBuf amu = dalloc(c, (size_t)s * n1), bmu = dalloc(c, (size_t)s * n2);
+  DBuf lc = dalloc(c, (size_t)s * std::max(steps, 1));
+  const size_t tk = select_topk_tmp_elems(n_r, s);
+  DBuf tv = dalloc(c, tk), tpp = ialloc(c, tk), tg = ialloc(c, tk);
+  DBuf cand = ialloc(c, s), ncand = ialloc(c, 1);
+  DBuf part(c, select_part_bytes(grid_blocks));
+  DBuf order = ialloc(c, std::max(steps, 1)), margin = dalloc(c, std::max(steps, 1));
+  DBuf kout = ialloc(c, 1);
+  Work w = make_work(c, (size_t)8 * s * 1024);
+
+  ck(select_init(c->stream, a, lda, n1, b, ldb, n2, n_r, d.d(), pos.i()), "select_init");
+  int k = 0;
+  while (k < steps) {
+    const int sc = std::min(s, n_r - k);
+    ck(select_topk(c->stream, d.d(), pos.i(), n_r, k, sc, tv.d(), tpp.i(), tg.i(), cand.i(), ncand.i()),
+       "select_topk");
+    ck(gather_rows(c->stream, a, lda, n1, cand.i(), sc, amu.d(), sc), "gather");
+    ck(gather_rows(c->stream, b, ldb, n2, cand.i(), sc, bmu.d(), sc), "gather");
+    ck(hadamard_gemm(c->stream, n_r, sc, a, lda, amu.d(), sc, n1, b, ldb, bmu.d(), sc, n2, W.d(), n_r, 1.0, 0.0),
+       "hadamard_gemm");
+    if (k > 0) {
+      ck(gather_rows(c->stream, L.d(), n_r, k, cand.i(), sc, lc.d(), sc), "gather");
+      gemm(c, n_r, sc, k, L.d(), n_r, Lay::MN, lc.d(), sc, Lay::MN, W.d(), n_r, -1.0, 1.0);
+    }
+    ck(select_steps(c->stream, grid_blocks, n_r, steps, k, d.d(), pos.i(), L.d(), W.d(), cand.i(), sc, part.p,
+                    order.i(), margin.d(), kout.i()),
+       "select_steps");
+    int knew = 0;
+    download(c, &knew, kout.p, sizeof(int));
+    if (knew <= k) fail(LRGW_ERR_INTERNAL, "select: no progress (non-finite residuals?)");
+    k = knew;
+  }
+  ck(select_scatter_perm(c->stream, pos.i(), n_r, perm.i()), "scatter_perm");
+  std::vector<int32_t> pts(n_mu);
+  download(c, pts.data(), perm.p, sizeof(int) * n_mu);
+  std::sort(pts.begin(), pts.end());
+  if (min_margin) {
+    std::vector<double> mg(std::max(steps, 1));
+    download(c, mg.data(), margin.p, sizeof(double) * std::max(steps, 1));
+    double mn = 1.0;
+    for (int i = 0; i < steps; ++i) mn = std::min(mn, mg[i]);
+    *min_margin = mn;
+  }
+  return pts;
+}
+
+// ---------------------------------------------------------------------------
+// Stage 2: Theta = lhs G^-1 with lhs = (A A_mu^T) o (B B_mu^T) (isdf.hpp:118-163).
+// ---------------------------------------------------------------------------
+void check_points(const int32_t* pts, int n_mu, int n_r) {
+  if (n_mu < 1) fail(LRGW_ERR_INVALID_INPUT, "fit_auxiliary_basis: empty point set");
+  for (int i = 0; i < n_mu; ++i) {
+    if (pts[i] < 0 || pts[i] >= n_r) fail(LRGW_ERR_INVALID_INPUT, "rows_at: index out of range");
+    if (i > 0 && pts[i] <= pts[i - 1])
+      fail(LRGW_ERR_INVALID_INPUT, "fit_auxiliary_basis: points must be distinct and sorted");
+  }
+}
+
+void fit_impl(lrgw_ctx c, const double* a, long long lda, int n1, const double* b, long long ldb, int n2,
+              int n_r, const int32_t* pts, int n_mu, double* theta, long long ldt, cudaEvent_t ev_solve0,
+              cudaEvent_t ev_solve1) {
+  check_points(pts, n_mu, n_r);
+  DBuf dp = upload_i(c, pts, n_mu);
+  DBuf amu = dalloc(c, (size_t)n_mu * n1), bmu = dalloc(c, (size_t)n_mu * n2);
+  ck(gather_rows(c->stream, a, lda, n1, dp.i(), n_mu, amu.d(), n_mu), "gather");
+  ck(gather_rows(c->stream, b, ldb, n2, dp.i(), n_mu, bmu.d(), n_mu), "gather");
+  DBuf lhs = dalloc(c, (size_t)n_r * n_mu);
+  ck(hadamard_gemm(c->stream, n_r, n_mu, a, lda, amu.d(), n_mu, n1, b, ldb, bmu.d(), n_mu, n2, lhs.d(), n_r, 1.0,
+                   0.0),
+     "hadamard_gemm");
+  DBuf gram = dalloc(c, (size_t)n_mu * n_mu);
+  ck(gather_rows(c->stream, lhs.d(), n_r, n_mu, dp.i(), n_mu, gram.d(), n_mu), "gather");
+  ck(mirror_lower(c->stream, gram.d(), n_mu, n_mu, true), "symmetrize");
+  DBuf ginv = dalloc(c, (size_t)n_mu * n_mu);
+  if (ev_solve0) ck(cudaEventRecord(ev_solve0, c->stream), "event");
+  gram_inverse(c, gram.d(), n_mu, ginv.d());
+  if (ev_solve1) ck(cudaEventRecord(ev_solve1, c->stream), "event");
+  gemm(c, n_r, n_mu, n_mu, lhs.d(), n_r, Lay::MN, ginv.d(), n_mu, Lay::MN, theta, ldt, 1.0, 0.0);
+}
+
+// ---------------------------------------------------------------------------
+// Stage 3: quadrature (K3, quadrature.cu).
+// ---------------------------------------------------------------------------
+struct NodeSet {
+  std::vector<double> nodes, weights;
+};
+
+NodeSet trapezoid(const lrgw_host::Spec& s, int n_intervals) {
+  NodeSet ns;
+  const double h = 2.0 * s.big_r / n_intervals;
+  for (int k = 0; k <= n_intervals; ++k) {
+    ns.nodes.push_back(-s.big_r + k * h);
+    ns.weights.push_back((k == 0 || k == n_intervals) ? 0.5 * h : h);
+  }
+  return ns;
+}
+
+// out (n_mu^2, mirrored) = pref * (beta * running + sum_k w_k term_k); running updated if given.
+void quad_run(lrgw_ctx c, const double* pv, long long ldv, const double* pc, long long ldpc, int n_mu, int n_v,
+              int n_c, const std::vector<double>& dv, const std::vector<double>& dc, const std::vector<double>& gw,
+              int n_nodes, double* running, double beta, double pref, double* out, long long ldo) {
+  if (n_nodes <= 0) {
+    ck(fill(c->stream, out, (size_t)n_mu * n_mu, 0.0), "fill");
+    return;
+  }
+  DBuf ddv = upload(c, dv.data(), dv.size()), ddc = upload(c, dc.data(), dc.size());
+  DBuf dgw = upload(c, gw.data(), gw.size());
+  const int groups = quad_partial_groups(n_mu, n_nodes, c->sm_count);
+  DBuf partial = dalloc(c, (size_t)groups * n_mu * n_mu);
+  ck(quad_nodes(c->stream, n_mu, n_v, n_c, pv, ldv, pc, ldpc, n_nodes, ddv.d(), ddc.d(), dgw.d(), groups,
+                partial.d(), running, beta, pref, out, ldo),
+     "quad_nodes");
+}
+
+void node_tables_or_fail(const lrgw_host::Spec& s, const double* e, int n_v, int n_c, const NodeSet& ns,
+                         std::vector<double>* dv, std::vector<double>* dc, std::vector<double>* gw) {
+  const int st = lrgw_host::node_tables(s, e, n_v, n_c, ns.nodes.data(), ns.weights.data(),
+                                        (int)ns.nodes.size(), dv, dc, gw);
+  if (st == lrgw_host::kNumeric) fail(LRGW_ERR_NUMERIC, "jacobi_complex: argument too close to a pole");
+  if (st != lrgw_host::kOk) fail(st, "contour node geometry");
+}
+
+void check_coupled(int n_mu, int n_v, int n_c, int n_e) {
+  if (n_mu < 1 || n_v < 1 || n_c < 1) fail(LRGW_ERR_INVALID_INPUT, "coupled_coefficients: empty input");
+  if (n_v + n_c > n_e) fail(LRGW_ERR_INVALID_INPUT, "coupled_coefficients: not enough energies");
+}
+
+// T = sum_i (v_i v_i^T) o (Pc diag(1/(e_i - e_c)) Pc^T), symmetrised
+// (contour.hpp:114-137) through the K3 kernel with one-hot valence diagonals.
+void direct_impl(lrgw_ctx c, const double* pv, long long ldv, const double* pc, long long ldpc, int n_mu, int n_v,
+                 int n_c, const double* e, double* t, long long ldt) {
+  std::vector<double> dv((size_t)2 * n_v * n_v, 0.0), dc((size_t)2 * n_v * n_c, 0.0), gw((size_t)2 * n_v, 0.0);
+  for (int i = 0; i < n_v; ++i) {
+    dv[2 * ((size_t)i * n_v + i)] = 1.0;
+    for (int j = 0; j < n_c; ++j) dc[2 * ((size_t)i * n_c + j)] = 1.0 / (e[i] - e[n_v + j]);
+    gw[2 * i + 1] = 1.0;  // term = g_im * Re(Jv o Jc) with real J's
+  }
+  quad_run(c, pv, ldv, pc, ldpc, n_mu, n_v, n_c, dv, dc, gw, n_v, nullptr, 0.0, 1.0, t, ldt);
+}
+
+void fixed_impl(lrgw_ctx c, const double* pv, long long ldv, const double* pc, long long ldpc, int n_mu, int n_v,
+                int n_c, const double* e, int n_e, int n_lambda, double* t, long long ldt) {
+  if (n_lambda < 1) fail(LRGW_ERR_INVALID_INPUT, "contour quadrature: N_lambda < 1");
+  lrgw_host::Spec s;
+  host_status(lrgw_host::elliptic_params(e, n_e, n_v, n_c, 1e-7, 1025, &s), "elliptic_params");
+  if (s.bypass) {  // single energy denominator: the mandated direct sum (driver.hpp:239-240)
+    direct_impl(c, pv, ldv, pc, ldpc, n_mu, n_v, n_c, e, t, ldt);
+    return;
+  }
+  NodeSet ns = trapezoid(s, n_lambda);
+  std::vector<double> dv, dc, gw;
+  node_tables_or_fail(s, e, n_v, n_c, ns, &dv, &dc, &gw);
+  quad_run(c, pv, ldv, pc, ldpc, n_mu, n_v, n_c, dv, dc, gw, (int)ns.nodes.size(), nullptr, 0.0,
+           lrgw_host::prefactor(s), t, ldt);
+}
+
+// Nested 2^m+1 levels (contour.hpp:235-279); visit(n_nodes, T_dev) -> continue?
+template <class Visit>
+void levels_impl(lrgw_ctx c, const double* pv, long long ldv, const double* pc, long long ldpc, int n_mu, int n_v,
+                 int n_c, const double* e, const lrgw_host::Spec& s, int max_level_nodes, Visit&& visit) {
+  if (s.bypass) fail(LRGW_ERR_INVALID_INPUT, "contour quadrature: spec is bypass-flagged; use the direct sum");
+  if ((1 << 4) + 1 > max_level_nodes) fail(LRGW_ERR_INVALID_INPUT, "contour quadrature: node cap below one level");
+  const double pref = lrgw_host::prefactor(s);
+  DBuf running = dalloc(c, (size_t)n_mu * n_mu);
+  DBuf tl = dalloc(c, (size_t)n_mu * n_mu);
+  bool first = true;
+  for (int m = 4;; ++m) {
+    const int n_nodes = (1 << m) + 1;
+    if (n_nodes > max_level_nodes) break;
+    const double h = 2.0 * s.big_r / (n_nodes - 1);
+    NodeSet ns;
+    if (first) {
+      for (int k = 0; k < n_nodes; ++k) {
+        ns.nodes.push_back(-s.big_r + k * h);
+        ns.weights.push_back((k == 0 || k == n_nodes - 1) ? 0.5 * h : h);
+      }
+    } else {
+      for (int k = 1; k < n_nodes; k += 2) {
+        ns.nodes.push_back(-s.big_r + k * h);
+        ns.weights.push_back(h);
+      }
+    }
+    std::vector<double> dv, dc, gw;
+    node_tables_or_fail(s, e, n_v, n_c, ns, &dv, &dc, &gw);
+    quad_run(c, pv, ldv, pc, ldpc, n_mu, n_v, n_c, dv, dc, gw, (int)ns.nodes.size(), running.d(),
+             first ? 0.0 : 0.5, pref, tl.d(), n_mu);
+    first = false;
+    if (!visit(n_nodes, tl.d())) break;
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+int lrgw_abi_version(void) { return LRGW_ABI_VERSION; }
+
+int lrgw_ctx_create(int device, lrgw_ctx* out) {
+  if (!out) return LRGW_ERR_INVALID_INPUT;
+  *out = nullptr;
+  auto* c = new (std::nothrow) lrgw_ctx_s;
+  if (!c) return LRGW_ERR_INTERNAL;
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return LRGW_ERR_CUDA;
+  }
+  c->stream = c->own_stream;
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) {
+    cudaStreamDestroy(c->own_stream);
+    delete c;
+    return LRGW_ERR_CUDA;
+  }
+  cusolverDnSetStream(c->solver, c->stream);
+  // keep freed pool memory cached across calls (stream-ordered allocator)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  c->launches0 = launch_count();
+  *out = c;
+  return LRGW_OK;
+}
+
+int lrgw_ctx_destroy(lrgw_ctx c) {
+  if (!c) return LRGW_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->plans) cufftDestroy(kv.second);
+  if (c->solver) cusolverDnDestroy(c->solver);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+  return LRGW_OK;
+}
+
+int lrgw_ctx_set_stream(lrgw_ctx c, void* stream) {
+  return guarded(c, [&] {
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    cusolverDnSetStream(c->solver, c->stream);
+    for (auto& kv : c->plans) cufftSetStream(kv.second, c->stream);
+  });
+}
+
+void* lrgw_ctx_stream(lrgw_ctx c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int lrgw_ctx_synchronize(lrgw_ctx c) {
+  return guarded(c, [&] { ck(cudaStreamSynchronize(c->stream), "sync"); });
+}
+
+const char* lrgw_ctx_last_error(lrgw_ctx c) { return c ? c->err.c_str() : "null context"; }
+int lrgw_ctx_last_pivot(lrgw_ctx c) { return c ? c->pivot : -1; }
+
+int lrgw_ctx_stage_ms(lrgw_ctx c, double* ms, int n) {
+  if (!c || !ms) return LRGW_ERR_INVALID_INPUT;
+  for (int i = 0; i < n && i < LRGW_NUM_STAGES; ++i) ms[i] = c->stage_ms[i];
+  return LRGW_OK;
+}
+
+long long lrgw_ctx_kernel_launches(lrgw_ctx c) { return c ? launch_count() - c->launches0 : 0; }
+
+int lrgw_ctx_set_select_batch(lrgw_ctx c, int s) {
+  if (!c || s < 1 || s > select_max_candidates()) return LRGW_ERR_INVALID_INPUT;
+  c->select_batch = s;
+  return LRGW_OK;
+}
+
+// ---- host scalars ---------------------------------------------------------
+int lrgw_num_aux(double k_mu, int n1, int n2, int* out) {
+  if (!(k_mu > 0.0) || !out) return LRGW_ERR_INVALID_INPUT;
+  *out = static_cast<int>(std::llround(k_mu * std::sqrt(static_cast<double>(n1) * n2)));
+  return LRGW_OK;
+}
+
+int lrgw_elliptic_k(double k, double* out) { return lrgw_host::elliptic_k(k, out); }
+
+int lrgw_jacobi_sn_cn_dn(double u, double k, double* o) {
+  return lrgw_host::jacobi_sn_cn_dn(u, k, o, o + 1, o + 2);
+}
+
+int lrgw_jacobi_complex(double x, double y, double k, double* o) {
+  std::complex<double> sn, cn, dn;
+  const int st = lrgw_host::jacobi_complex(x, y, k, &sn, &cn, &dn);
+  if (st != lrgw_host::kOk) return st;
+  o[0] = sn.real();
+  o[1] = sn.imag();
+  o[2] = cn.real();
+  o[3] = cn.imag();
+  o[4] = dn.real();
+  o[5] = dn.imag();
+  return LRGW_OK;
+}
+
+int lrgw_elliptic_params(const double* e, int n_e, int n_v, int n_c, double delta_rel, int max_nodes,
+                         double* spec7) {
+  lrgw_host::Spec s;
+  const int st = lrgw_host::elliptic_params(e, n_e, n_v, n_c, delta_rel, max_nodes, &s);
+  if (st == lrgw_host::kOk) spec_to7(s, spec7);
+  return st;
+}
+
+int lrgw_cauchy_error_bound(const double* spec7, int n_lambda, double* out) {
+  return lrgw_host::cauchy_error_bound(spec_from7(spec7), n_lambda, out);
+}
+
+int lrgw_coulomb_kernel(const int* dims, const double* cell, double* kernel) {
+  return guarded_host([&] {
+    check_grid(dims, cell);
+    const double two_pi = 6.283185307179586476925286766559;
+    const int n1 = dims[0], n2 = dims[1], n3 = dims[2];
+    for (long long idx = 0; idx < (long long)n1 * n2 * n3; ++idx) {
+      const int i1 = (int)(idx % n1), i2 = (int)((idx / n1) % n2), i3 = (int)(idx / ((long long)n1 * n2));
+      const int f1 = i1 <= n1 / 2 ? i1 : i1 - n1, f2 = i2 <= n2 / 2 ? i2 : i2 - n2, f3 = i3 <= n3 / 2 ? i3 : i3 - n3;
+      const double g1 = two_pi * f1 / cell[0], g2 = two_pi * f2 / cell[1], g3 = two_pi * f3 / cell[2];
+      const double g = g1 * g1 + g2 * g2 + g3 * g3;
+      kernel[idx] = g > 0.0 ? 12.566370614359172953850573533118 / g : 0.0;
+    }
+  });
+}
+
+// ---- host-buffer API --------------------------------------------------------
+int lrgw_select_interpolation_points(lrgw_ctx c, const double* psi_a, const double* psi_b, int n_r, int n1,
+                                     int n2, int n_mu, int method, int32_t* pts) {
+  return guarded(c, [&] {
+    if (method == LRGW_QRCP_SKETCHED)
+      fail(LRGW_ERR_UNSUPPORTED, "select_interpolation_points: qrcp_sketched is not implemented on B200");
+    if (n_mu > n_r) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: N_mu > N_r");
+    if (n_mu < 1) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: N_mu < 1");
+    DBuf a = upload(c, psi_a, (size_t)n_r * n1), b = upload(c, psi_b, (size_t)n_r * n2);
+    std::vector<int32_t> p = select_impl(c, a.d(), n_r, n1, b.d(), n_r, n2, n_r, n_mu, nullptr);
+    std::copy(p.begin(), p.end(), pts);
+  });
+}
+
+int lrgw_fit_auxiliary_basis(lrgw_ctx c, const double* psi_a, const double* psi_b, int n_r, int n1, int n2,
+                             const int32_t* pts, int n_mu, double* theta) {
+  return guarded(c, [&] {
+    check_points(pts, n_mu, n_r);
+    DBuf a = upload(c, psi_a, (size_t)n_r * n1), b = upload(c, psi_b, (size_t)n_r * n2);
+    DBuf th = dalloc(c, (size_t)n_r * n_mu);
+    fit_impl(c, a.d(), n_r, n1, b.d(), n_r, n2, n_r, pts, n_mu, th.d(), n_r, nullptr, nullptr);
+    download(c, theta, th.p, sizeof(double) * n_r * n_mu);
+  });
+}
+
+int lrgw_coupled_coefficients_direct(lrgw_ctx c, const double* pv, const double* pc, int n_mu, int n_v, int n_c,
+                                     const double* e, int n_e, double* t) {
+  return guarded(c, [&] {
+    check_coupled(n_mu, n_v, n_c, n_e);
+    DBuf dv = upload(c, pv, (size_t)n_mu * n_v), dc = upload(c, pc, (size_t)n_mu * n_c);
+    DBuf dt = dalloc(c, (size_t)n_mu * n_mu);
+    direct_impl(c, dv.d(), n_mu, dc.d(), n_mu, n_mu, n_v, n_c, e, dt.d(), n_mu);
+    download(c, t, dt.p, sizeof(double) * n_mu * n_mu);
+  });
+}
+
+int lrgw_sum_node_terms(lrgw_ctx c, const double* pv, const double* pc, int n_mu, int n_v, int n_c, const double* e,
+                        int n_e, const double* spec7, const double* nodes, const double* weights, int n_nodes,
+                        double* acc) {
+  return guarded(c, [&] {
+    check_coupled(n_mu, n_v, n_c, n_e);
+    lrgw_host::Spec s = spec_from7(spec7);
+    NodeSet ns;
+    ns.nodes.assign(nodes, nodes + n_nodes);
+    ns.weights.assign(weights, weights + n_nodes);
+    std::vector<double> dv, dc, gw;
+    node_tables_or_fail(s, e, n_v, n_c, ns, &dv, &dc, &gw);
+    DBuf dpv = upload(c, pv, (size_t)n_mu * n_v), dpc = upload(c, pc, (size_t)n_mu * n_c);
+    DBuf dt = dalloc(c, (size_t)n_mu * n_mu);
+    quad_run(c, dpv.d(), n_mu, dpc.d(), n_mu, n_mu, n_v, n_c, dv, dc, gw, n_nodes, nullptr, 0.0, 1.0, dt.d(), n_mu);
+    download(c, acc, dt.p, sizeof(double) * n_mu * n_mu);
+  });
+}
+
+int lrgw_coupled_coefficients_fixed(lrgw_ctx c, const double* pv, const double* pc, int n_mu, int n_v, int n_c,
+                                    const double* e, int n_e, int n_lambda, double* t) {
+  return guarded(c, [&] {
+    check_coupled(n_mu, n_v, n_c, n_e);
+    DBuf dpv = upload(c, pv, (size_t)n_mu * n_v), dpc = upload(c, pc, (size_t)n_mu * n_c);
+    DBuf dt = dalloc(c, (size_t)n_mu * n_mu);
+    fixed_impl(c, dpv.d(), n_mu, dpc.d(), n_mu, n_mu, n_v, n_c, e, n_e, n_lambda, dt.d(), n_mu);
+    download(c, t, dt.p, sizeof(double) * n_mu * n_mu);
+  });
+}
+
+int lrgw_coupled_coefficients_contour(lrgw_ctx c, const double* pv, const double* pc, int n_mu, int n_v, int n_c,
+                                      const double* e, int n_e, double delta_rel, int max_nodes, double* t,
+                                      int* nodes_used, double* est_rel) {
+  return guarded(c, [&] {
+    check_coupled(n_mu, n_v, n_c, n_e);
+    lrgw_host::Spec s;
+    host_status(lrgw_host::elliptic_params(e, n_e, n_v, n_c, delta_rel, max_nodes, &s), "elliptic_params");
+    DBuf dpv = upload(c, pv, (size_t)n_mu * n_v), dpc = upload(c, pc, (size_t)n_mu * n_c);
+    const size_t nn = (size_t)n_mu * n_mu;
+    DBuf prev = dalloc(c, nn), best = dalloc(c, nn), red = dalloc(c, 512);
+    bool have_prev = false, converged = false;
+    int best_nodes = 0;
+    double best_rel = 1.0;
+    levels_impl(c, dpv.d(), n_mu, dpc.d(), n_mu, n_mu, n_v, n_c, e, s, s.max_nodes, [&](int n_nodes, double* tl) {
+      ck(cudaMemcpyAsync(best.p, tl, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+      best_nodes = n_nodes;
+      if (!have_prev) {
+        best_rel = 1.0;
+        have_prev = true;
+        ck(cudaMemcpyAsync(prev.p, tl, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+        return true;
+      }
+      double h[2];
+      ck(frob_diff(c->stream, tl, prev.d(), nn, red.d()), "frob");
+      ck(cudaMemcpyAsync(&h[0], red.d() + 296, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+      ck(frob_diff(c->stream, tl, nullptr, nn, red.d()), "frob");
+      download(c, &h[1], red.d() + 296, sizeof(double));
+      const double scale = std::max(std::sqrt(h[1]), 1e-300);
+      best_rel = std::sqrt(h[0]) / scale;
+      ck(cudaMemcpyAsync(prev.p, tl, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+      if (best_rel <= s.delta_rel) {
+        converged = true;
+        return false;
+      }
+      return true;
+    });
+    download(c, t, best.p, nn * sizeof(double));
+    if (nodes_used) *nodes_used = best_nodes;
+    if (est_rel) *est_rel = best_rel;
+    if (!converged)
+      fail(LRGW_ERR_CONTOUR_CONVERGENCE, "coupled_coefficients_contour: did not reach delta_rel within max_nodes");
+  });
+}
+
+int lrgw_contour_refinement_levels(lrgw_ctx c, const double* pv, const double* pc, int n_mu, int n_v, int n_c,
+                                   const double* e, int n_e, int max_level_nodes, int max_levels, double* out,
+                                   int* counts, int* n_levels) {
+  return guarded(c, [&] {
+    check_coupled(n_mu, n_v, n_c, n_e);
+    lrgw_host::Spec s;
+    host_status(lrgw_host::elliptic_params(e, n_e, n_v, n_c, 1e-7, 1025, &s), "elliptic_params");
+    DBuf dpv = upload(c, pv, (size_t)n_mu * n_v), dpc = upload(c, pc, (size_t)n_mu * n_c);
+    const size_t nn = (size_t)n_mu * n_mu;
+    int n = 0;
+    levels_impl(c, dpv.d(), n_mu, dpc.d(), n_mu, n_mu, n_v, n_c, e, s, max_level_nodes, [&](int nodes, double* tl) {
+      if (n >= max_levels) return false;
+      counts[n] = nodes;
+      download(c, out + n * nn, tl, nn * sizeof(double));
+      ++n;
+      return true;
+    });
+    *n_levels = n;
+  });
+}
+
+int lrgw_apply_coulomb(lrgw_ctx c, const int* dims, const double* cell, int zero, const double* x, int m, double* y) {
+  return guarded(c, [&] {
+    check_grid(dims, cell);
+    const long long n_r = (long long)dims[0] * dims[1] * dims[2];
+    DBuf dx = upload(c, x, (size_t)n_r * m), dy = dalloc(c, (size_t)n_r * m);
+    coulomb_apply(c, dims, cell, zero, dx.d(), n_r, m, dy.d(), n_r);
+    download(c, y, dy.p, sizeof(double) * n_r * m);
+  });
+}
+
+int lrgw_assemble_K(lrgw_ctx c, const double* t, const double* p, int n_r, int n_mu, const int* dims,
+                    const double* cell, int zero, double* k) {
+  return guarded(c, [&] {
+    check_grid(dims, cell);
+    if ((long long)dims[0] * dims[1] * dims[2] != n_r || n_mu < 1)
+      fail(LRGW_ERR_INVALID_INPUT, "assemble_K: T / P_vc shape mismatch");
+    DBuf dt = upload(c, t, (size_t)n_mu * n_mu), dp = upload(c, p, (size_t)n_r * n_mu);
+    DBuf pvp = dalloc(c, (size_t)n_mu * n_mu), dk = dalloc(c, (size_t)n_mu * n_mu);
+    pvp_impl(c, dims, cell, zero, dp.d(), n_r, n_mu, pvp.d(), nullptr);
+    smw_core(c, dt.d(), pvp.d(), n_mu, dk.d());
+    download(c, k, dk.p, sizeof(double) * n_mu * n_mu);
+  });
+}
+
+int lrgw_eps_from_parts(lrgw_ctx c, const double* p, const double* k, int n_r, int n_mu, const int* dims,
+                        const double* cell, int zero, lrgw_eps* out) {
+  return guarded(c, [&] {
+    check_grid(dims, cell);
+    if ((long long)dims[0] * dims[1] * dims[2] != n_r) fail(LRGW_ERR_INVALID_INPUT, "eps: grid / N_r mismatch");
+    auto* e = new lrgw_eps_s;
+    e->ctx = c;
+    e->n_r = n_r;
+    e->n_mu = n_mu;
+    std::memcpy(e->dims, dims, sizeof(e->dims));
+    std::memcpy(e->cell, cell, sizeof(e->cell));
+    e->zero = zero;
+    DBuf dp = upload(c, p, (size_t)n_r * n_mu), dk = upload(c, k, (size_t)n_mu * n_mu);
+    e->theta = static_cast<double*>(dp.take());
+    e->k = static_cast<double*>(dk.take());
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    *out = e;
+  });
+}
+
+int lrgw_build_epsilon_inverse(lrgw_ctx c, const double* t, const double* p, int n_r, int n_mu, const int* dims,
+                               const double* cell, int zero, lrgw_eps* out) {
+  return guarded(c, [&] {
+    check_grid(dims, cell);
+    if ((long long)dims[0] * dims[1] * dims[2] != n_r || n_mu < 1)
+      fail(LRGW_ERR_INVALID_INPUT, "assemble_K: T / P_vc shape mismatch");
+    DBuf dt = upload(c, t, (size_t)n_mu * n_mu), dp = upload(c, p, (size_t)n_r * n_mu);
+    DBuf pvp = dalloc(c, (size_t)n_mu * n_mu), dk = dalloc(c, (size_t)n_mu * n_mu);
+    pvp_impl(c, dims, cell, zero, dp.d(), n_r, n_mu, pvp.d(), nullptr);
+    smw_core(c, dt.d(), pvp.d(), n_mu, dk.d());
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    auto* e = new lrgw_eps_s;
+    e->ctx = c;
+    e->n_r = n_r;
+    e->n_mu = n_mu;
+    std::memcpy(e->dims, dims, sizeof(e->dims));
+    std::memcpy(e->cell, cell, sizeof(e->cell));
+    e->zero = zero;
+    e->theta = static_cast<double*>(dp.take());
+    e->k = static_cast<double*>(dk.take());
+    e->t = static_cast<double*>(dt.take());
+    *out = e;
+  });
+}
+
+static void eps_apply_impl(lrgw_ctx c, lrgw_eps e, const double* x, long long ldx, int m, double* y, long long ldy) {
+  const int n_r = e->n_r, n_mu = e->n_mu;
+  DBuf u = dalloc(c, (size_t)n_mu * m), w = dalloc(c, (size_t)n_mu * m), z = dalloc(c, (size_t)n_r * m);
+  Work wk = make_work(c, (size_t)64 * n_mu * m);
+  // u = Theta^T x ; w = K u ; z = Theta w ; y = x + V z   (smw.hpp:101-102)
+  gemm(c, n_mu, m, n_r, e->theta, n_r, Lay::K, x, ldx, Lay::K, u.d(), n_mu, 1.0, 0.0, nullptr, false, &wk);
+  gemm(c, n_mu, m, n_mu, e->k, n_mu, Lay::MN, u.d(), n_mu, Lay::K, w.d(), n_mu, 1.0, 0.0);
+  gemm(c, n_r, m, n_mu, e->theta, n_r, Lay::MN, w.d(), n_mu, Lay::K, z.d(), n_r, 1.0, 0.0);
+  coulomb_apply(c, e->dims, e->cell, e->zero, z.d(), n_r, m, y, ldy);
+  ck(axpby(c->stream, n_r, m, 1.0, x, ldx, 1.0, y, ldy), "axpby");
+}
+
+int lrgw_epsilon_inverse_apply(lrgw_ctx c, lrgw_eps e, const double* x, int m, double* y) {
+  return guarded(c, [&] {
+    if (!e) fail(LRGW_ERR_INVALID_INPUT, "epsilon_inverse_apply: null handle");
+    const size_t n = (size_t)e->n_r * m;
+    DBuf dx = upload(c, x, n), dy = dalloc(c, n);
+    eps_apply_impl(c, e, dx.d(), e->n_r, m, dy.d(), e->n_r);
+    download(c, y, dy.p, n * sizeof(double));
+  });
+}
+
+int lrgw_eps_apply_dev(lrgw_ctx c, lrgw_eps e, const double* x, long long ldx, int m, double* y, long long ldy) {
+  return guarded(c, [&] {
+    if (!e) fail(LRGW_ERR_INVALID_INPUT, "epsilon_inverse_apply: null handle");
+    if (ldx < e->n_r || ldy < e->n_r) fail(LRGW_ERR_INVALID_INPUT, "epsilon_inverse_apply: row mismatch");
+    eps_apply_impl(c, e, x, ldx, m, y, ldy);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int lrgw_eps_get(lrgw_ctx c, lrgw_eps e, double* k, double* p, double* vp, double* t, int32_t* pts) {
+  return guarded(c, [&] {
+    if (!e) fail(LRGW_ERR_INVALID_INPUT, "eps: null handle");
+    const size_t nn = (size_t)e->n_mu * e->n_mu, np = (size_t)e->n_r * e->n_mu;
+    if (k) download(c, k, e->k, nn * sizeof(double));
+    if (p) download(c, p, e->theta, np * sizeof(double));
+    if (t && e->t) download(c, t, e->t, nn * sizeof(double));
+    if (pts && !e->pts.empty()) std::copy(e->pts.begin(), e->pts.end(), pts);
+    if (vp) {
+      DBuf dvp = dalloc(c, np);
+      coulomb_apply(c, e->dims, e->cell, e->zero, e->theta, e->n_r, e->n_mu, dvp.d(), e->n_r);
+      download(c, vp, dvp.p, np * sizeof(double));
+    }
+  });
+}
+
+int lrgw_eps_shape(lrgw_eps e, int* n_r, int* n_mu) {
+  if (!e) return LRGW_ERR_INVALID_INPUT;
+  if (n_r) *n_r = e->n_r;
+  if (n_mu) *n_mu = e->n_mu;
+  return LRGW_OK;
+}
+
+int lrgw_eps_destroy(lrgw_eps e) {
+  if (!e) return LRGW_OK;
+  cudaSetDevice(e->ctx->device);
+  cudaStreamSynchronize(e->ctx->stream);
+  cudaFree(e->theta);
+  cudaFree(e->k);
+  cudaFree(e->t);
+  delete e;
+  return LRGW_OK;
+}
+
+int lrgw_eps_device_ptrs(lrgw_eps e, double** theta, double** k, double** t) {
+  if (!e) return LRGW_ERR_INVALID_INPUT;
+  if (theta) *theta = e->theta;
+  if (k) *k = e->k;
+  if (t) *t = e->t;
+  return LRGW_OK;
+}
+
+// ---- the whole build --------------------------------------------------------
+int lrgw_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, long long ldv, const double* phi_c,
+               long long ldc, const double* energies, lrgw_eps* out) {
+  return guarded(c, [&] {
+    if (!prm || !out) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: null argument");
+    const lrgw_build_params& P = *prm;
+    check_grid(P.dims, P.cell);
+    const int n_r = P.n_r, n_v = P.n_v, n_c = P.n_c;
+    if ((long long)P.dims[0] * P.dims[1] * P.dims[2] != n_r) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: grid / N_r mismatch");
+    if (n_v < 1 || n_c < 1) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: need n_v >= 1 and n_c >= 1");
+    int n_mu = 0;
+    if (lrgw_num_aux(P.k_mu, n_v, n_c, &n_mu) != LRGW_OK) fail(LRGW_ERR_INVALID_INPUT, "num_aux: k_mu must be > 0");
+    n_mu = std::clamp(n_mu, 1, n_r);
+    const int n_e = n_v + n_c;
+    lrgw_host::Spec spec;
+    host_status(lrgw_host::elliptic_params(energies, n_e, n_v, n_c, P.delta_rel > 0 ? P.delta_rel : 1e-7,
+                                           P.max_nodes > 0 ? P.max_nodes : 1025, &spec),
+                "elliptic_params");
+    cudaEvent_t ev[10];
+    for (auto& x : ev) ck(cudaEventCreate(&x), "event");
+    struct EvGuard {
+      cudaEvent_t* e;
+      ~EvGuard() {
+        for (int i = 0; i < 10; ++i) cudaEventDestroy(e[i]);
+      }
+    } eg{ev};
+    ck(cudaEventRecord(ev[0], c->stream), "event");
+    // stage 1
+    std::vector<int32_t> pts = select_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, n_mu, nullptr);
+    ck(cudaEventRecord(ev[1], c->stream), "event");
+    // stage 2
+    DBuf theta = dalloc(c, (size_t)n_r * n_mu);
+    fit_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, pts.data(), n_mu, theta.d(), n_r, ev[8], ev[9]);
+    ck(cudaEventRecord(ev[2], c->stream), "event");
+    // stage 3
+    DBuf dpts = upload_i(c, pts.data(), n_mu);
+    DBuf pv = dalloc(c, (size_t)n_mu * n_v), pc = dalloc(c, (size_t)n_mu * n_c);
+    ck(gather_rows(c->stream, phi_v, ldv, n_v, dpts.i(), n_mu, pv.d(), n_mu), "gather");
+    ck(gather_rows(c->stream, phi_c, ldc, n_c, dpts.i(), n_mu, pc.d(), n_mu), "gather");
+    DBuf t = dalloc(c, (size_t)n_mu * n_mu);
+    if (spec.bypass) {
+      direct_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, t.d(), n_mu);
+    } else if (P.n_lambda > 0) {
+      fixed_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, n_e, P.n_lambda, t.d(), n_mu);
+    } else {
+      const size_t nn = (size_t)n_mu * n_mu;
+      DBuf prev = dalloc(c, nn), red = dalloc(c, 512);
+      bool have = false, conv = false;
+      levels_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, spec, spec.max_nodes,
+                  [&](int, double* tl) {
+                    ck(cudaMemcpyAsync(t.p, tl, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+                    if (!have) {
+                      have = true;
+                      ck(cudaMemcpyAsync(prev.p, tl, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+                      return true;
+                    }
+                    double h[2];
+                    ck(frob_diff(c->stream, tl, prev.d(), nn, red.d()), "frob");
+                    ck(cudaMemcpyAsync(&h[0], red.d() + 296, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+                    ck(frob_diff(c->stream, tl, nullptr, nn, red.d()), "frob");
+                    download(c, &h[1], red.d() + 296, sizeof(double));
+                    ck(cudaMemcpyAsync(prev.p, tl, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+                    if (std::sqrt(h[0]) / std::max(std::sqrt(h[1]), 1e-300) <= spec.delta_rel) {
+                      conv = true;
+                      return false;
+                    }
+                    return true;
+                  });
+      if (!conv) fail(LRGW_ERR_CONTOUR_CONVERGENCE, "coupled_coefficients_contour: did not reach delta_rel within max_nodes");
+    }
+    ck(cudaEventRecord(ev[3], c->stream), "event");
+    // stages 4-5
+    DBuf pvp = dalloc(c, (size_t)n_mu * n_mu), k = dalloc(c, (size_t)n_mu * n_mu);
+    pvp_impl(c, P.dims, P.cell, P.zero_kernel, theta.d(), n_r, n_mu, pvp.d(), ev[4]);
+    ck(cudaEventRecord(ev[5], c->stream), "event");
+    smw_core(c, t.d(), pvp.d(), n_mu, k.d());
+    ck(cudaEventRecord(ev[6], c->stream), "event");
+    ck(cudaEventSynchronize(ev[6]), "sync");
+    float ms;
+    auto el = [&](int a, int b) {
+      cudaEventElapsedTime(&ms, ev[a], ev[b]);
+      return (double)ms;
+    };
+    c->stage_ms[LRGW_STAGE_SELECT] = el(0, 1);
+    c->stage_ms[LRGW_STAGE_FIT] = el(1, 2);
+    c->stage_ms[LRGW_STAGE_FIT_SOLVE] = el(8, 9);
+    c->stage_ms[LRGW_STAGE_CONTOUR] = el(2, 3);
+    c->stage_ms[LRGW_STAGE_FFT] = el(3, 4);
+    c->stage_ms[LRGW_STAGE_PVP] = el(4, 5);
+    c->stage_ms[LRGW_STAGE_SMW] = el(5, 6);
+    c->stage_ms[LRGW_STAGE_TOTAL] = el(0, 6);
+    auto* e = new lrgw_eps_s;
+    e->ctx = c;
+    e->n_r = n_r;
+    e->n_mu = n_mu;
+    std::memcpy(e->dims, P.dims, sizeof(e->dims));
+    std::memcpy(e->cell, P.cell, sizeof(e->cell));
+    e->zero = P.zero_kernel;
+    e->theta = static_cast<double*>(theta.take());
+    e->k = static_cast<double*>(k.take());
+    e->t = static_cast<double*>(t.take());
+    e->pts = pts;
+    *out = e;
+  });
+}
+
+// ---- stage-level device API -------------------------------------------------
+int lrgw_dev_select(lrgw_ctx c, const double* a, long long lda, int n1, const double* b, long long ldb, int n2,
+                    int n_r, int n_mu, int32_t* pts_host, double* min_margin) {
+  return guarded(c, [&] {
+    std::vector<int32_t> p = select_impl(c, a, lda, n1, b, ldb, n2, n_r, n_mu, min_margin);
+    std::copy(p.begin(), p.end(), pts_host);
+  });
+}
+
+int lrgw_dev_fit(lrgw_ctx c, const double* a, long long lda, int n1, const double* b, long long ldb, int n2, int n_r,
+                 const int32_t* pts_host, int n_mu, double* theta, long long ldt) {
+  return guarded(c, [&] {
+    fit_impl(c, a, lda, n1, b, ldb, n2, n_r, pts_host, n_mu, theta, ldt, nullptr, nullptr);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int lrgw_dev_fit_panel(lrgw_ctx c, const double* a, long long lda, int n1, const double* b, long long ldb, int n2,
+                       int rows, const double* a_mu, const double* b_mu, const double* g_inv, int n_mu, double* theta,
+                       long long ldt) {
+  return guarded(c, [&] {
+    DBuf lhs = dalloc(c, (size_t)rows * n_mu);
+    ck(hadamard_gemm(c->stream, rows, n_mu, a, lda, a_mu, n_mu, n1, b, ldb, b_mu, n_mu, n2, lhs.d(), rows, 1.0, 0.0),
+       "hadamard_gemm");
+    gemm(c, rows, n_mu, n_mu, lhs.d(), rows, Lay::MN, g_inv, n_mu, Lay::MN, theta, ldt, 1.0, 0.0);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int lrgw_dev_contour_partial(lrgw_ctx c, const double* pv, long long ldv, const double* pc, long long ldpc, int n_mu,
+                             int n_v, int n_c, const double* e, int n_e, int n_lambda, int node0, int count,
+                             double* acc) {
+  return guarded(c, [&] {
+    check_coupled(n_mu, n_v, n_c, n_e);
+    lrgw_host::Spec s;
+    host_status(lrgw_host::elliptic_params(e, n_e, n_v, n_c, 1e-7, 1025, &s), "elliptic_params");
+    if (s.bypass) fail(LRGW_ERR_INVALID_INPUT, "contour quadrature: spec is bypass-flagged; use the direct sum");
+    NodeSet all = trapezoid(s, n_lambda), ns;
+    for (int k = node0; k < node0 + count && k < (int)all.nodes.size(); ++k) {
+      ns.nodes.push_back(all.nodes[k]);
+      ns.weights.push_back(all.weights[k]);
+    }
+    std::vector<double> dv, dc, gw;
+    node_tables_or_fail(s, e, n_v, n_c, ns, &dv, &dc, &gw);
+    quad_run(c, pv, ldv, pc, ldpc, n_mu, n_v, n_c, dv, dc, gw, (int)ns.nodes.size(), nullptr, 0.0, 1.0, acc, n_mu);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int lrgw_dev_contour_fixed(lrgw_ctx c, const double* pv, long long ldv, const double* pc, long long ldpc, int n_mu,
+                           int n_v, int n_c, const double* e, int n_e, int n_lambda, double* t, long long ldt) {
+  return guarded(c, [&] {
+    check_coupled(n_mu, n_v, n_c, n_e);
+    fixed_impl(c, pv, ldv, pc, ldpc, n_mu, n_v, n_c, e, n_e, n_lambda, t, ldt);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int lrgw_dev_pvp(lrgw_ctx c, const int* dims, const double* cell, int zero, const double* theta, long long ldt,
+                 int n_mu, double* pvp) {
+  return guarded(c, [&] {
+    check_grid(dims, cell);
+    pvp_impl(c, dims, cell, zero, theta, ldt, n_mu, pvp, nullptr);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int lrgw_dev_smw_core(lrgw_ctx c, const double* t, const double* pvp, int n_mu, double* k) {
+  return guarded(c, [&] {
+    smw_core(c, t, pvp, n_mu, k);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int lrgw_dev_coulomb_apply(lrgw_ctx c, const int* dims, const double* cell, int zero, const double* x, long long ldx,
+                           int m, double* y, long long ldy) {
+  return guarded(c, [&] {
+    check_grid(dims, cell);
+    coulomb_apply(c, dims, cell, zero, x, ldx, m, y, ldy);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int lrgw_dev_dgemm(lrgw_ctx c, char ta, char tb, int m, int n, int k, double alpha, const double* a, long long lda,
+                   const double* b, long long ldb, double beta, double* cm, long long ldc) {
+  return guarded(c, [&] {
+    const bool at = ta == 'T' || ta == 't', bt = tb == 'T' || tb == 't';
+    Work w = make_work(c, (size_t)8 * m * n);
+    gemm(c, m, n, k, a, lda, at ? Lay::K : Lay::MN, b, ldb, bt ? Lay::MN : Lay::K, cm, ldc, alpha, beta, nullptr,
+         false, &w);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+}  // extern "C"

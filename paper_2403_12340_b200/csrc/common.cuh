@@ -1,0 +1,61 @@
+// common.cuh — shared device primitives for the lrgw B200 kernels (sm_100a).
+//
+// FP64 on B200: tcgen05 has no kind::f64, so the FP64 tensor path is the
+// warp-level DMMA (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4). Measured on this
+// pool (profiles/fp64_peaks_r01.txt): DMMA 37.2 TFLOP/s vs DFMA 34.2 TFLOP/s,
+// so every FP64 contraction here is DMMA fed from shared memory that is
+// filled by a multi-stage cp.async pipeline.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lrgw_dev {
+
+// D(8x8) += A(8x4) * B(4x8). Fragment ownership (PTX ISA, m8n8k4 .f64):
+//   g = lane >> 2, t = lane & 3
+//   a  = A[g][t]            b  = B[t][g]  (i.e. B^T[g][t])
+//   c0 = C[g][2t], c1 = C[g][2t+1]
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 16-byte async copy global->shared, zero-filled when !pred.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(n));
+}
+
+// 8-byte async copy (ca path), zero-filled when !pred.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  const int n = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(n));
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Map a linear block index onto the lower-triangle tile (i >= j) of a
+// T x T tile grid, row-major over the triangle: idx = i(i+1)/2 + j.
+__device__ __forceinline__ void lower_tile(int idx, int& ti, int& tj) {
+  int i = static_cast<int>((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
+  while ((i + 1) * (i + 2) / 2 <= idx) ++i;
+  while (i * (i + 1) / 2 > idx) --i;
+  ti = i;
+  tj = idx - i * (i + 1) / 2;
+}
+
+}  // namespace lrgw_dev

@@ -1,0 +1,180 @@
+// gemm.cu — dispatch for the FP64 DMMA GEMM engine (gemm.cuh) plus the small
+// elementwise kernels the path needs (split-K reduction, symmetric mirror,
+// row gather).
+#include <algorithm>
+
+#include "gemm.cuh"
+#include "kernels.h"
+
+namespace lrgw_dev {
+
+namespace {
+
+// Large tiles: 128x64 CTA, 8 warps of 32x32, 3 stages (~90 KB smem, 2 CTA/SM).
+// Small tiles: 64x64 CTA, 4 warps of 32x32, 4 stages (~80 KB smem, 2 CTA/SM).
+template <bool AK, bool BK, int VA, int VB>
+using CfgL = GemmCfg<128, 64, 32, 32, 3, AK, BK, VA, VB>;
+template <bool AK, bool BK, int VA, int VB>
+using CfgS = GemmCfg<64, 64, 32, 32, 4, AK, BK, VA, VB>;
+
+template <class Cfg>
+cudaError_t launch_cfg(cudaStream_t st, const DgemmParams& p, int splits) {
+  dim3 grid;
+  if (p.lower) {
+    const int t = (p.M + Cfg::BM - 1) / Cfg::BM;
+    grid = dim3(t * (t + 1) / 2, 1, splits);
+  } else {
+    grid = dim3((p.M + Cfg::BM - 1) / Cfg::BM, (p.N + Cfg::BN - 1) / Cfg::BN, splits);
+  }
+  if (grid.x == 0 || grid.y == 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(dgemm_kernel<Cfg>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  dgemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(p); count_launches(1);
+  return cudaGetLastError();
+}
+
+template <bool AK, bool BK>
+cudaError_t launch_layout(cudaStream_t st, const DgemmParams& p, bool big, bool va, bool vb,
+                          int splits) {
+  if (big) {
+    if (va && vb) return launch_cfg<CfgL<AK, BK, 2, 2>>(st, p, splits);
+    return launch_cfg<CfgL<AK, BK, 1, 1>>(st, p, splits);
+  }
+  if (va && vb) return launch_cfg<CfgS<AK, BK, 2, 2>>(st, p, splits);
+  return launch_cfg<CfgS<AK, BK, 1, 1>>(st, p, splits);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+__global__ void splitk_reduce_kernel(const double* partial, int splits, long long stride, int M,
+                                     int N, double* C, long long ldc, double beta, int lower,
+                                     int tile) {
+  const long long total = (long long)M * N;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int m = static_cast<int>(idx % M), n = static_cast<int>(idx / M);
+    if (lower && (n / tile) > (m / tile)) continue;
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += partial[z * stride + idx];
+    double* c = C + m + (long long)n * ldc;
+    *c = (beta == 0.0) ? s : s + beta * (*c);
+  }
+}
+
+__global__ void mirror_lower_kernel(double* a, int n, long long lda, int average) {
+  const long long total = (long long)n * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = static_cast<int>(idx % n), j = static_cast<int>(idx / n);
+    if (i <= j) continue;  // (i, j) strictly lower
+    double* lo = a + i + (long long)j * lda;
+    double* up = a + j + (long long)i * lda;
+    const double v = average ? 0.5 * (*lo + *up) : *lo;
+    *lo = v;
+    *up = v;
+  }
+}
+
+__global__ void gather_rows_kernel(const double* src, long long lds, int cols, const int* rows,
+                                   int n_rows, double* dst, long long ldd) {
+  const long long total = (long long)n_rows * cols;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(idx % n_rows), c = static_cast<int>(idx / n_rows);
+    dst[r + c * ldd] = src[rows[r] + c * lds];
+  }
+}
+
+}  // namespace
+
+cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long long lda, Lay la,
+                  const double* B, long long ldb, Lay lb, double* C, long long ldc, double alpha,
+                  double beta, const double* scale, bool lower, int sm_count, double* work,
+                  size_t work_elems) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  DgemmParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.A = A;
+  p.lda = lda;
+  p.B = B;
+  p.ldb = ldb;
+  p.C = C;
+  p.ldc = ldc;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.scale = scale;
+  p.lower = lower ? 1 : 0;
+  const bool ak = la == Lay::K, bk = lb == Lay::K;
+  // 16-byte cp.async needs aligned bases, even leading dims and even extents
+  // along the contiguous axis.
+  const bool va = aligned16(A) && lda % 2 == 0 && (ak ? K % 2 == 0 : M % 2 == 0);
+  const bool vb = aligned16(B) && ldb % 2 == 0 && (bk ? K % 2 == 0 : N % 2 == 0);
+  bool big = (long long)((M + 127) / 128) * ((N + 63) / 64) >= 2LL * sm_count && !lower;
+  const int BMt = big ? 128 : 64, BNt = 64;
+  long long tiles = lower ? (long long)((M + 63) / 64) * ((M + 63) / 64 + 1) / 2
+                          : (long long)((M + BMt - 1) / BMt) * ((N + BNt - 1) / BNt);
+  // split-K when the output tile grid cannot fill the chip and K is long
+  int splits = 1;
+  const int ktiles = (K + 15) / 16;
+  if (tiles < 2LL * sm_count && ktiles >= 32 && work) {
+    splits = static_cast<int>(std::min<long long>((2LL * sm_count + tiles - 1) / tiles, ktiles / 16));
+    while (splits > 1 && (size_t)splits * M * N > work_elems) --splits;
+  }
+  if (lower && M != N) return cudaErrorInvalidValue;
+  if (splits > 1) {
+    const int kc = ((ktiles + splits - 1) / splits) * 16;
+    splits = (K + kc - 1) / kc;
+    p.k_chunk = kc;
+    p.partial = work;
+    p.part_stride = (long long)M * N;
+  }
+  cudaError_t e;
+  if (!ak && !bk) e = launch_layout<false, false>(st, p, big, va, vb, splits);
+  else if (!ak && bk) e = launch_layout<false, true>(st, p, big, va, vb, splits);
+  else if (ak && !bk) e = launch_layout<true, false>(st, p, big, va, vb, splits);
+  else e = launch_layout<true, true>(st, p, big, va, vb, splits);
+  if (e != cudaSuccess || splits <= 1) return e;
+  splitk_reduce_kernel<<<1184, 256, 0, st>>>(work, splits, (long long)M * N, M, N, C, ldc, beta,
+                                             lower ? 1 : 0, 64); count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long long lda1,
+                          const double* b1, long long ldb1, int k1, const double* a2,
+                          long long lda2, const double* b2, long long ldb2, int k2, double* C,
+                          long long ldc, double alpha, double beta) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  HadamardParams p{M, N, k1, k2, a1, b1, a2, b2, lda1, ldb1, lda2, ldb2, C, ldc, alpha, beta};
+  const bool vec = aligned16(a1) && aligned16(b1) && aligned16(a2) && aligned16(b2) &&
+                   lda1 % 2 == 0 && ldb1 % 2 == 0 && lda2 % 2 == 0 && ldb2 % 2 == 0 &&
+                   M % 2 == 0 && N % 2 == 0;
+  auto go = [&](auto cfg) -> cudaError_t {
+    using Cfg = decltype(cfg);
+    dim3 grid((M + Cfg::BM - 1) / Cfg::BM, (N + Cfg::BN - 1) / Cfg::BN);
+    cudaError_t e = cudaFuncSetAttribute(hadamard_kernel<Cfg>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    hadamard_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(p); count_launches(1);
+    return cudaGetLastError();
+  };
+  if (vec) return go(CfgL<false, false, 2, 2>{});
+  return go(CfgL<false, false, 1, 1>{});
+}
+
+cudaError_t mirror_lower(cudaStream_t st, double* a, int n, long long lda, bool average) {
+  if (n <= 1) return cudaSuccess;
+  mirror_lower_kernel<<<592, 256, 0, st>>>(a, n, lda, average ? 1 : 0); count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t gather_rows(cudaStream_t st, const double* src, long long lds, int cols, const int* rows,
+                        int n_rows, double* dst, long long ldd) {
+  if (n_rows <= 0 || cols <= 0) return cudaSuccess;
+  gather_rows_kernel<<<592, 256, 0, st>>>(src, lds, cols, rows, n_rows, dst, ldd); count_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace lrgw_dev

@@ -1,0 +1,63 @@
+// kernels.h — internal device-side entry points of liblrgw_cuda (not the C-ABI;
+// see include/lrgw_cuda.h for that). All matrices column-major FP64.
+#pragma once
+
+#include <cstddef>
+#include <cuda_runtime.h>
+
+namespace lrgw_dev {
+
+// Kernel launches issued by this library (all launcher sites bump it).
+long long launch_count();
+void count_launches(int n);
+
+enum class Lay { MN, K };  // operand stored MN-contiguous (col-major) or K-contiguous
+
+// C = alpha * A diag(scale) B^T + beta * C with A: M x K, B: N x K (see gemm.cuh).
+// lower: only lower-triangle 64x64 tiles (M == N). `work` enables split-K.
+cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long long lda, Lay la,
+                  const double* B, long long ldb, Lay lb, double* C, long long ldc, double alpha,
+                  double beta, const double* scale, bool lower, int sm_count, double* work,
+                  size_t work_elems);
+
+// C = alpha * (A1 B1^T) o (A2 B2^T) + beta * C; A1: M x K1, B1: N x K1, A2: M x K2,
+// B2: N x K2, all MN-contiguous (isdf.hpp:132 fit GEMM pair + Hadamard).
+cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long long lda1,
+                          const double* b1, long long ldb1, int k1, const double* a2,
+                          long long lda2, const double* b2, long long ldb2, int k2, double* C,
+                          long long ldc, double alpha, double beta);
+
+// a(j,i) = a(i,j) for i > j (average = 0) or both = (a(i,j) + a(j,i))/2.
+cudaError_t mirror_lower(cudaStream_t st, double* a, int n, long long lda, bool average);
+
+// dst(r, c) = src(rows[r], c), rows on device.
+cudaError_t gather_rows(cudaStream_t st, const double* src, long long lds, int cols, const int* rows,
+                        int n_rows, double* dst, long long ldd);
+
+// K3 quadrature (quadrature.cu).
+int quad_partial_groups(int n_mu, int n_nodes, int sm_count);
+cudaError_t quad_nodes(cudaStream_t st, int n_mu, int n_v, int n_c, const double* pv, long long ldv,
+                       const double* pc, long long ldc, int n_nodes, const double* dv,
+                       const double* dc, const double* gw, int groups, double* partial,
+                       double* running, double beta, double pref, double* t, long long ldt);
+
+// Coulomb (coulomb.cu): G-space half-spectrum weights c(G) = w_G v(G) / N_r
+// (w_G = 2 off the self-conjugate i1 planes, 1 on them) laid out to match a
+// D2Z output column of 2*n3*n2*(n1/2+1) interleaved reals.
+cudaError_t coulomb_half_weights(cudaStream_t st, int n1, int n2, int n3, double c1, double c2,
+                                 double c3, int zero_kernel, double* w);
+// y(r) = x_hat(G) * v(G) / N_r over the half spectrum (in place, complex).
+cudaError_t coulomb_scale_half(cudaStream_t st, int n1, int n2, int n3, double c1, double c2,
+                               double c3, int zero_kernel, double* xhat, int cols);
+
+
+// scalar helpers (misc.cu)
+cudaError_t scale_copy(cudaStream_t st, const double* src, double* dst, size_t n, double alpha);
+cudaError_t fill(cudaStream_t st, double* dst, size_t n, double v);
+cudaError_t add_diag(cudaStream_t st, double* a, int n, long long lda, double v);
+cudaError_t axpby(cudaStream_t st, int rows, int cols, double alpha, const double* x, long long ldx,
+                  double beta, double* y, long long ldy);
+cudaError_t max_abs(cudaStream_t st, const double* x, size_t n, double* d_out);
+cudaError_t frob_diff(cudaStream_t st, const double* a, const double* b, size_t n, double* d_out2);
+
+}  // namespace lrgw_dev

@@ -1,0 +1,117 @@
+// misc.cu — small elementwise / reduction kernels used around the hot path.
+#include "kernels.h"
+
+namespace lrgw_dev {
+
+namespace {
+
+__global__ void scale_copy_kernel(const double* src, double* dst, size_t n, double alpha) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = alpha * src[i];
+}
+
+__global__ void fill_kernel(double* dst, size_t n, double v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = v;
+}
+
+__global__ void add_diag_kernel(double* a, int n, long long lda, double v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    a[i + i * lda] += v;
+}
+
+__global__ void axpby_kernel(int rows, int cols, double alpha, const double* x, long long ldx,
+                             double beta, double* y, long long ldy) {
+  const long long total = (long long)rows * cols;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(idx % rows), c = static_cast<int>(idx / rows);
+    double* yy = y + r + c * ldy;
+    *yy = alpha * x[r + c * ldx] + (beta == 0.0 ? 0.0 : beta * *yy);
+  }
+}
+
+// Deterministic two-level reductions: fixed grid, per-block partials, one
+// final block (no atomics on doubles).
+__global__ void max_abs_kernel(const double* x, size_t n, double* partial) {
+  __shared__ double s[256];
+  double m = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(x[i]));
+  s[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] = fmax(s[threadIdx.x], s[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = s[0];
+}
+
+__global__ void sum_sq_diff_kernel(const double* a, const double* b, size_t n, double* partial) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double d = b ? a[i] - b[i] : a[i];
+    acc = fma(d, d, acc);
+  }
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = s[0];
+}
+
+__global__ void finish_kernel(const double* partial, int n, double* out, int is_max) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = is_max ? fmax(r, partial[i]) : r + partial[i];
+    *out = r;
+  }
+}
+
+constexpr int kRedBlocks = 296;
+
+}  // namespace
+
+cudaError_t scale_copy(cudaStream_t st, const double* src, double* dst, size_t n, double alpha) {
+  if (n == 0) return cudaSuccess;
+  scale_copy_kernel<<<1184, 256, 0, st>>>(src, dst, n, alpha); count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t fill(cudaStream_t st, double* dst, size_t n, double v) {
+  if (n == 0) return cudaSuccess;
+  fill_kernel<<<1184, 256, 0, st>>>(dst, n, v); count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t add_diag(cudaStream_t st, double* a, int n, long long lda, double v) {
+  if (n <= 0) return cudaSuccess;
+  add_diag_kernel<<<(n + 255) / 256, 256, 0, st>>>(a, n, lda, v); count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t axpby(cudaStream_t st, int rows, int cols, double alpha, const double* x, long long ldx,
+                  double beta, double* y, long long ldy) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  axpby_kernel<<<1184, 256, 0, st>>>(rows, cols, alpha, x, ldx, beta, y, ldy); count_launches(1);
+  return cudaGetLastError();
+}
+
+// d_out must hold kRedBlocks + 1 doubles; the result lands in d_out[kRedBlocks].
+cudaError_t max_abs(cudaStream_t st, const double* x, size_t n, double* d_out) {
+  max_abs_kernel<<<kRedBlocks, 256, 0, st>>>(x, n, d_out); count_launches(1);
+  finish_kernel<<<1, 32, 0, st>>>(d_out, kRedBlocks, d_out + kRedBlocks, 1); count_launches(1);
+  return cudaGetLastError();
+}
+
+// sum (a - b)^2 (b may be null) -> d_out2[kRedBlocks]
+cudaError_t frob_diff(cudaStream_t st, const double* a, const double* b, size_t n, double* d_out2) {
+  sum_sq_diff_kernel<<<kRedBlocks, 256, 0, st>>>(a, b, n, d_out2); count_launches(1);
+  finish_kernel<<<1, 32, 0, st>>>(d_out2, kRedBlocks, d_out2 + kRedBlocks, 0); count_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace lrgw_dev

@@ -1,0 +1,590 @@
+"""Python mirror of the reference `lrgw` hot-path interface over liblrgw_cuda.so.
+
+Names, argument meaning and error behaviour follow the reference C++ API
+(/root/reference/proj/include/lrgw): host arrays in, host arrays out, the
+reference exception taxonomy (errors.hpp:10-36) raised as Python exceptions.
+Every call runs on the GPU through the C-ABI (include/lrgw_cuda.h); there is no
+CPU path. The device-resident build (`build`) takes torch CUDA tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+# ---------------------------------------------------------------------------
+# exception taxonomy (errors.hpp:10-36, contour.hpp:92-96)
+# ---------------------------------------------------------------------------
+
+
+class LrgwError(Exception):
+    code = 9
+
+
+class InvalidInput(LrgwError, ValueError):
+    code = 1
+
+
+class GuardExceeded(LrgwError):
+    code = 2
+
+
+class NumericError(LrgwError):
+    code = 3
+
+
+class SingularMatrix(NumericError):
+    code = 4
+
+    def __init__(self, msg, pivot_index=-1):
+        super().__init__(f"{msg} (pivot index {pivot_index})")
+        self.pivot_index = pivot_index
+
+
+class ContourConvergenceError(NumericError):
+    code = 5
+
+    def __init__(self, msg, best=None):
+        super().__init__(msg)
+        self.best = best
+
+
+class IoError(LrgwError):
+    code = 6
+
+
+class CudaError(LrgwError):
+    code = 7
+
+
+class Unsupported(InvalidInput):
+    code = 8
+
+
+_EXC = {1: InvalidInput, 2: GuardExceeded, 3: NumericError, 6: IoError, 7: CudaError, 8: Unsupported}
+
+
+def _raise(rc, ctx_handle=None, what=""):
+    lib = L.load()
+    msg = what
+    if ctx_handle is not None:
+        m = lib.lrgw_ctx_last_error(ctx_handle)
+        if m:
+            msg = f"{what}: {m.decode()}" if what else m.decode()
+    if rc == 4:
+        piv = lib.lrgw_ctx_last_pivot(ctx_handle) if ctx_handle is not None else -1
+        raise SingularMatrix(msg, piv)
+    if rc == 5:
+        raise ContourConvergenceError(msg)
+    raise _EXC.get(rc, LrgwError)(msg)
+
+
+def _check(rc, ctx_handle=None, what=""):
+    if rc != 0:
+        _raise(rc, ctx_handle, what)
+
+
+# ---------------------------------------------------------------------------
+# context
+# ---------------------------------------------------------------------------
+
+
+class Context:
+    """One lrgw_ctx (stream, cuSOLVER handle, cuFFT plan cache) on one device."""
+
+    def __init__(self, device: int = 0):
+        self._lib = L.load()
+        h = L.ctx_t()
+        rc = self._lib.lrgw_ctx_create(device, ctypes.byref(h))
+        if rc != 0:
+            raise CudaError(f"lrgw_ctx_create(device={device}) failed with status {rc}")
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.lrgw_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stage_ms(self):
+        out = np.zeros(8)
+        self._lib.lrgw_ctx_stage_ms(self.handle, out.ctypes.data_as(L.c_double_p), 8)
+        names = ["select", "fit", "fit_solve", "contour", "fft", "pvp", "smw", "total"]
+        return dict(zip(names, out.tolist()))
+
+    def kernel_launches(self) -> int:
+        return int(self._lib.lrgw_ctx_kernel_launches(self.handle))
+
+    def set_select_batch(self, s: int):
+        _check(self._lib.lrgw_ctx_set_select_batch(self.handle, int(s)), self.handle, "set_select_batch")
+
+    def set_stream(self, stream_ptr: int | None):
+        _check(self._lib.lrgw_ctx_set_stream(self.handle, ctypes.c_void_p(stream_ptr or 0)), self.handle,
+               "set_stream")
+
+    def synchronize(self):
+        _check(self._lib.lrgw_ctx_synchronize(self.handle), self.handle, "synchronize")
+
+
+_default = {}
+_default_lock = threading.Lock()
+
+
+def default_context(device: int = 0) -> Context:
+    with _default_lock:
+        if device not in _default:
+            _default[device] = Context(device)
+        return _default[device]
+
+
+def _ctx(ctx):
+    return ctx if ctx is not None else default_context()
+
+
+def _f(a):
+    return np.asfortranarray(a, dtype=np.float64)
+
+
+def _dp(a):
+    return a.ctypes.data_as(L.c_double_p)
+
+
+def _ip(a):
+    return a.ctypes.data_as(L.c_int32_p)
+
+
+def _grid(dims, cell):
+    d = np.ascontiguousarray(dims, dtype=np.int32)
+    c = np.ascontiguousarray(cell, dtype=np.float64)
+    if d.size != 3 or c.size != 3:
+        raise InvalidInput("Grid: dims and cell need 3 entries")
+    return d, c
+
+
+# ---------------------------------------------------------------------------
+# ISDF (isdf.hpp)
+# ---------------------------------------------------------------------------
+
+
+def num_aux(k_mu: float, n1: int, n2: int) -> int:
+    """isdf.hpp:42-46."""
+    out = ctypes.c_int(0)
+    _check(L.load().lrgw_num_aux(float(k_mu), int(n1), int(n2), ctypes.byref(out)), None,
+           "num_aux: k_mu must be > 0")
+    return out.value
+
+
+def select_interpolation_points(psi_a, psi_b, n_mu: int, method: str = "qrcp_direct", ctx=None) -> np.ndarray:
+    """isdf.hpp:95-112 — N_mu grid indices, sorted ascending (int32)."""
+    c = _ctx(ctx)
+    a, b = _f(psi_a), _f(psi_b)
+    if a.shape[0] != b.shape[0]:
+        raise InvalidInput("pair_matrix_transposed: row mismatch")
+    meth = {"qrcp_direct": 0, "qrcp_sketched": 1}[method]
+    pts = np.zeros(max(int(n_mu), 0), dtype=np.int32)
+    rc = c._lib.lrgw_select_interpolation_points(c.handle, _dp(a), _dp(b), a.shape[0], a.shape[1], b.shape[1],
+                                                 int(n_mu), meth, _ip(pts) if pts.size else None)
+    _check(rc, c.handle, "select_interpolation_points")
+    return pts
+
+
+def fit_auxiliary_basis(psi_a, psi_b, points, ctx=None) -> np.ndarray:
+    """isdf.hpp:118-163 — Theta (N_r x N_mu, Fortran order)."""
+    c = _ctx(ctx)
+    a, b = _f(psi_a), _f(psi_b)
+    pts = np.ascontiguousarray(points, dtype=np.int32)
+    theta = np.zeros((a.shape[0], pts.size), order="F")
+    rc = c._lib.lrgw_fit_auxiliary_basis(c.handle, _dp(a), _dp(b), a.shape[0], a.shape[1], b.shape[1],
+                                         _ip(pts) if pts.size else None, pts.size, _dp(theta))
+    _check(rc, c.handle, "fit_auxiliary_basis")
+    return theta
+
+
+@dataclass
+class IsdfDecomposition:
+    """isdf.hpp:33-39."""
+    label: str
+    k_mu: float
+    n_mu: int
+    point_indices: np.ndarray
+    p: np.ndarray
+
+
+def build_isdf(psi, n_v, n_c, k_mu, ctx=None) -> IsdfDecomposition:
+    """isdf.hpp:176-183 for the vc pair set."""
+    a, b = psi[:, :n_v], psi[:, n_v:n_v + n_c]
+    n_mu = min(max(num_aux(k_mu, n_v, n_c), 1), psi.shape[0])
+    pts = select_interpolation_points(a, b, n_mu, ctx=ctx)
+    return IsdfDecomposition("vc", k_mu, n_mu, pts, fit_auxiliary_basis(a, b, pts, ctx=ctx))
+
+
+# ---------------------------------------------------------------------------
+# contour (elliptic.hpp, contour.hpp)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class ContourSpec:
+    """contour.hpp:23-33."""
+    q: float = 0.0
+    big_q: float = 0.0
+    r: float = 0.0
+    big_r: float = 0.0
+    l: float = 0.0
+    e_shift: float = 0.0
+    delta_rel: float = 1e-7
+    max_nodes: int = 1025
+    bypass: bool = False
+
+    def as7(self):
+        return np.array([self.q, self.big_q, self.r, self.big_r, self.l, self.e_shift, float(self.bypass)])
+
+
+@dataclass
+class CoupledCoefficients:
+    """contour.hpp:86-90."""
+    t: np.ndarray
+    nodes_used: int = 0
+    est_rel_error: float = 0.0
+
+
+def elliptic_k(k: float) -> float:
+    out = ctypes.c_double(0)
+    _check(L.load().lrgw_elliptic_k(float(k), ctypes.byref(out)), None, "elliptic_k: modulus must be in [0, 1)")
+    return out.value
+
+
+def jacobi_sn_cn_dn(u: float, k: float):
+    out = np.zeros(3)
+    _check(L.load().lrgw_jacobi_sn_cn_dn(float(u), float(k), _dp(out)), None, "jacobi_sn_cn_dn")
+    return tuple(out.tolist())
+
+
+def jacobi_complex(x: float, y: float, k: float):
+    out = np.zeros(6)
+    _check(L.load().lrgw_jacobi_complex(float(x), float(y), float(k), _dp(out)), None, "jacobi_complex")
+    return complex(out[0], out[1]), complex(out[2], out[3]), complex(out[4], out[5])
+
+
+def elliptic_params(energies, n_v: int, n_c: int, delta_rel: float, max_nodes: int = 1025) -> ContourSpec:
+    e = np.ascontiguousarray(energies, dtype=np.float64)
+    out = np.zeros(7)
+    _check(L.load().lrgw_elliptic_params(_dp(e), e.size, int(n_v), int(n_c), float(delta_rel), int(max_nodes),
+                                         _dp(out)), None, "elliptic_params")
+    return ContourSpec(*out[:6].tolist(), delta_rel=delta_rel, max_nodes=max_nodes, bypass=bool(out[6]))
+
+
+def cauchy_error_bound(spec: ContourSpec, n_lambda: int) -> float:
+    s = spec.as7()
+    out = ctypes.c_double(0)
+    _check(L.load().lrgw_cauchy_error_bound(_dp(s), int(n_lambda), ctypes.byref(out)), None,
+           "cauchy_error_bound: N_lambda < 1")
+    return out.value
+
+
+def _pts_args(psi_v_pts, psi_c_pts, energies):
+    pv, pc = _f(psi_v_pts), _f(psi_c_pts)
+    if pv.shape[0] != pc.shape[0]:
+        raise InvalidInput("coupled_coefficients: point-row mismatch")
+    e = np.ascontiguousarray(energies, dtype=np.float64)
+    return pv, pc, e
+
+
+def coupled_coefficients_direct(psi_v_pts, psi_c_pts, energies, ctx=None) -> CoupledCoefficients:
+    c = _ctx(ctx)
+    pv, pc, e = _pts_args(psi_v_pts, psi_c_pts, energies)
+    t = np.zeros((pv.shape[0], pv.shape[0]), order="F")
+    _check(c._lib.lrgw_coupled_coefficients_direct(c.handle, _dp(pv), _dp(pc), pv.shape[0], pv.shape[1],
+                                                   pc.shape[1], _dp(e), e.size, _dp(t)), c.handle,
+           "coupled_coefficients_direct")
+    return CoupledCoefficients(t, 0, 0.0)
+
+
+def sum_node_terms(psi_v_pts, psi_c_pts, energies, spec: ContourSpec, nodes, weights, ctx=None) -> np.ndarray:
+    c = _ctx(ctx)
+    pv, pc, e = _pts_args(psi_v_pts, psi_c_pts, energies)
+    nd = np.ascontiguousarray(nodes, dtype=np.float64)
+    wt = np.ascontiguousarray(weights, dtype=np.float64)
+    s = spec.as7()
+    acc = np.zeros((pv.shape[0], pv.shape[0]), order="F")
+    _check(c._lib.lrgw_sum_node_terms(c.handle, _dp(pv), _dp(pc), pv.shape[0], pv.shape[1], pc.shape[1], _dp(e),
+                                      e.size, _dp(s), _dp(nd), _dp(wt), nd.size, _dp(acc)), c.handle,
+           "sum_node_terms")
+    return acc
+
+
+def coupled_coefficients_fixed(psi_v_pts, psi_c_pts, energies, n_lambda: int, ctx=None) -> CoupledCoefficients:
+    c = _ctx(ctx)
+    pv, pc, e = _pts_args(psi_v_pts, psi_c_pts, energies)
+    t = np.zeros((pv.shape[0], pv.shape[0]), order="F")
+    _check(c._lib.lrgw_coupled_coefficients_fixed(c.handle, _dp(pv), _dp(pc), pv.shape[0], pv.shape[1],
+                                                  pc.shape[1], _dp(e), e.size, int(n_lambda), _dp(t)), c.handle,
+           "coupled_coefficients_fixed")
+    return CoupledCoefficients(t, int(n_lambda) + 1, 0.0)
+
+
+def coupled_coefficients_contour(psi_v_pts, psi_c_pts, energies, spec: ContourSpec, threads: int = 1,
+                                 ctx=None) -> CoupledCoefficients:
+    """contour.hpp:298-329 (`threads` kept for signature parity; host-only)."""
+    c = _ctx(ctx)
+    pv, pc, e = _pts_args(psi_v_pts, psi_c_pts, energies)
+    t = np.zeros((pv.shape[0], pv.shape[0]), order="F")
+    nu = ctypes.c_int(0)
+    est = ctypes.c_double(0)
+    rc = c._lib.lrgw_coupled_coefficients_contour(c.handle, _dp(pv), _dp(pc), pv.shape[0], pv.shape[1],
+                                                  pc.shape[1], _dp(e), e.size, float(spec.delta_rel),
+                                                  int(spec.max_nodes), _dp(t), ctypes.byref(nu), ctypes.byref(est))
+    if rc == 5:
+        raise ContourConvergenceError(
+            "coupled_coefficients_contour: did not reach delta_rel within max_nodes",
+            CoupledCoefficients(t, nu.value, est.value))
+    _check(rc, c.handle, "coupled_coefficients_contour")
+    return CoupledCoefficients(t, nu.value, est.value)
+
+
+def contour_refinement_levels(psi_v_pts, psi_c_pts, energies, spec: ContourSpec, max_level_nodes: int,
+                              threads: int = 1, ctx=None):
+    c = _ctx(ctx)
+    pv, pc, e = _pts_args(psi_v_pts, psi_c_pts, energies)
+    n_mu = pv.shape[0]
+    max_levels = 16
+    out = np.zeros((max_levels, n_mu, n_mu))
+    counts = np.zeros(max_levels, dtype=np.int32)
+    nl = ctypes.c_int(0)
+    _check(c._lib.lrgw_contour_refinement_levels(c.handle, _dp(pv), _dp(pc), n_mu, pv.shape[1], pc.shape[1],
+                                                 _dp(e), e.size, int(max_level_nodes), max_levels, _dp(out),
+                                                 counts.ctypes.data_as(L.c_int_p), ctypes.byref(nl)), c.handle,
+           "contour_refinement_levels")
+    # each level was written column-major into a C-order slab: transpose back
+    return [(int(counts[i]), np.asfortranarray(out[i].T)) for i in range(nl.value)]
+
+
+# ---------------------------------------------------------------------------
+# Coulomb + SMW (model.hpp, smw.hpp)
+# ---------------------------------------------------------------------------
+
+
+def coulomb_kernel(dims, cell) -> np.ndarray:
+    d, c = _grid(dims, cell)
+    out = np.zeros(int(np.prod(d)))
+    _check(L.load().lrgw_coulomb_kernel(d.ctypes.data_as(L.c_int_p), _dp(c), _dp(out)), None, "build_coulomb")
+    return out
+
+
+def apply_coulomb(dims, cell, x, zero_kernel: bool = False, ctx=None) -> np.ndarray:
+    c = _ctx(ctx)
+    d, cl = _grid(dims, cell)
+    xx = _f(x)
+    if xx.ndim == 1:
+        xx = xx.reshape(-1, 1, order="F")
+    if xx.shape[0] != int(np.prod(d)):
+        raise InvalidInput("apply_coulomb: row count != N_r")
+    y = np.zeros_like(xx, order="F")
+    _check(c._lib.lrgw_apply_coulomb(c.handle, d.ctypes.data_as(L.c_int_p), _dp(cl), int(zero_kernel), _dp(xx),
+                                     xx.shape[1], _dp(y)), c.handle, "apply_coulomb")
+    return y
+
+
+def assemble_K(t, p, dims, cell, zero_kernel: bool = False, ctx=None) -> np.ndarray:
+    c = _ctx(ctx)
+    d, cl = _grid(dims, cell)
+    tt, pp = _f(t), _f(p)
+    if tt.shape[0] != tt.shape[1] or tt.shape[0] != pp.shape[1]:
+        raise InvalidInput("assemble_K: T / P_vc shape mismatch")
+    k = np.zeros_like(tt, order="F")
+    _check(c._lib.lrgw_assemble_K(c.handle, _dp(tt), _dp(pp), pp.shape[0], pp.shape[1],
+                                  d.ctypes.data_as(L.c_int_p), _dp(cl), int(zero_kernel), _dp(k)), c.handle,
+           "assemble_K")
+    return k
+
+
+class EpsilonInverseLowRank:
+    """Device-resident factored eps^-1 (smw.hpp:77-82): Theta, K (and T) stay
+    in HBM; host copies on demand (`k`, `p_vc`, `vp`)."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx = ctx
+        self.handle = handle
+        n_r, n_mu = ctypes.c_int(0), ctypes.c_int(0)
+        ctx._lib.lrgw_eps_shape(handle, ctypes.byref(n_r), ctypes.byref(n_mu))
+        self.n_r, self.n_mu = n_r.value, n_mu.value
+
+    def _get(self, which):
+        out = np.zeros((self.n_mu, self.n_mu) if which in ("k", "t") else (self.n_r, self.n_mu), order="F")
+        args = {"k": None, "p": None, "vp": None, "t": None}
+        args[which] = _dp(out)
+        _check(self.ctx._lib.lrgw_eps_get(self.ctx.handle, self.handle, args["k"], args["p"], args["vp"],
+                                          args["t"], None), self.ctx.handle, "eps_get")
+        return out
+
+    @property
+    def k(self):
+        return self._get("k")
+
+    @property
+    def p_vc(self):
+        return self._get("p")
+
+    @property
+    def vp(self):
+        return self._get("vp")
+
+    @property
+    def t(self):
+        return self._get("t")
+
+    @property
+    def point_indices(self):
+        pts = np.zeros(self.n_mu, dtype=np.int32)
+        _check(self.ctx._lib.lrgw_eps_get(self.ctx.handle, self.handle, None, None, None, None, _ip(pts)),
+               self.ctx.handle, "eps_get")
+        return pts
+
+    def device_ptrs(self):
+        th, k, t = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        self.ctx._lib.lrgw_eps_device_ptrs(self.handle, ctypes.byref(th), ctypes.byref(k), ctypes.byref(t))
+        return th.value, k.value, t.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.ctx._lib.lrgw_eps_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_epsilon_inverse(t, p, dims, cell, threads: int = 1, zero_kernel: bool = False,
+                          ctx=None) -> EpsilonInverseLowRank:
+    """smw.hpp:84-94."""
+    c = _ctx(ctx)
+    d, cl = _grid(dims, cell)
+    tt, pp = _f(t), _f(p)
+    h = L.eps_t()
+    _check(c._lib.lrgw_build_epsilon_inverse(c.handle, _dp(tt), _dp(pp), pp.shape[0], pp.shape[1],
+                                             d.ctypes.data_as(L.c_int_p), _dp(cl), int(zero_kernel),
+                                             ctypes.byref(h)), c.handle, "build_epsilon_inverse")
+    return EpsilonInverseLowRank(c, h)
+
+
+def epsilon_inverse_from_parts(p, k, dims, cell, ctx=None) -> EpsilonInverseLowRank:
+    c = _ctx(ctx)
+    d, cl = _grid(dims, cell)
+    pp, kk = _f(p), _f(k)
+    h = L.eps_t()
+    _check(c._lib.lrgw_eps_from_parts(c.handle, _dp(pp), _dp(kk), pp.shape[0], pp.shape[1],
+                                      d.ctypes.data_as(L.c_int_p), _dp(cl), 0, ctypes.byref(h)), c.handle,
+           "eps_from_parts")
+    return EpsilonInverseLowRank(c, h)
+
+
+def epsilon_inverse_apply(e: EpsilonInverseLowRank, x) -> np.ndarray:
+    """smw.hpp:97-103: X + V P (K (P^T X))."""
+    xx = _f(x)
+    if xx.ndim == 1:
+        xx = xx.reshape(-1, 1, order="F")
+    if xx.shape[0] != e.n_r:
+        raise InvalidInput("epsilon_inverse_apply: row mismatch")
+    y = np.zeros_like(xx, order="F")
+    _check(e.ctx._lib.lrgw_epsilon_inverse_apply(e.ctx.handle, e.handle, _dp(xx), xx.shape[1], _dp(y)),
+           e.ctx.handle, "epsilon_inverse_apply")
+    return y
+
+
+# ---------------------------------------------------------------------------
+# device-resident build (stages 1-5) over torch CUDA tensors
+# ---------------------------------------------------------------------------
+
+
+def _dev_ptr_cm(t):
+    """Device pointer and leading dim of a column-major view of a 2-D CUDA tensor."""
+    import torch
+
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64):
+        raise InvalidInput("expected a float64 CUDA tensor")
+    if t.dim() != 2 or t.stride(0) != 1:
+        raise InvalidInput("expected a column-major (stride(0) == 1) 2-D tensor")
+    return t.data_ptr(), max(t.stride(1), t.shape[0])
+
+
+def build(phi_v, phi_c, energies, dims, cell, k_mu: float = 8.0, n_lambda: int = 16, delta_rel: float = 1e-7,
+          max_nodes: int = 1025, zero_kernel: bool = False, ctx=None) -> EpsilonInverseLowRank:
+    """Stages 1-5 from device-resident orbitals (column-major float64 CUDA
+    tensors, N_r x N_v and N_r x N_c) and host energies: point selection,
+    Theta fit, Cauchy quadrature core, G-space Theta^T V Theta, SMW core K."""
+    c = _ctx(ctx)
+    pv, ldv = _dev_ptr_cm(phi_v)
+    pc, ldc = _dev_ptr_cm(phi_c)
+    e = np.ascontiguousarray(energies, dtype=np.float64)
+    prm = L.BuildParams()
+    prm.n_r, prm.n_v, prm.n_c = phi_v.shape[0], phi_v.shape[1], phi_c.shape[1]
+    prm.dims[:] = [int(x) for x in dims]
+    prm.cell[:] = [float(x) for x in cell]
+    prm.k_mu = float(k_mu)
+    prm.n_lambda = int(n_lambda)
+    prm.delta_rel = float(delta_rel)
+    prm.max_nodes = int(max_nodes)
+    prm.zero_kernel = int(zero_kernel)
+    _sync_torch(phi_v)
+    h = L.eps_t()
+    _check(c._lib.lrgw_build(c.handle, ctypes.byref(prm), ctypes.c_void_p(pv), ldv, ctypes.c_void_p(pc), ldc,
+                             _dp(e), ctypes.byref(h)), c.handle, "build")
+    return EpsilonInverseLowRank(c, h)
+
+
+def _sync_torch(t):
+    import torch
+
+    torch.cuda.current_stream(t.device).synchronize()
+
+
+def eps_apply_dev(e: EpsilonInverseLowRank, x, y):
+    """y = eps^-1 x for column-major float64 CUDA tensors (N_r x m)."""
+    px, ldx = _dev_ptr_cm(x)
+    py, ldy = _dev_ptr_cm(y)
+    _sync_torch(x)
+    _check(e.ctx._lib.lrgw_eps_apply_dev(e.ctx.handle, e.handle, ctypes.c_void_p(px), ldx, x.shape[1],
+                                         ctypes.c_void_p(py), ldy), e.ctx.handle, "eps_apply_dev")
+    return y
+
+
+def dgemm_dev(trans_a: str, trans_b: str, alpha: float, a, b, beta: float, c, ctx=None):
+    """C = alpha op(A) op(B) + beta C on column-major float64 CUDA tensors
+    through the path's DMMA GEMM engine (BLAS argument semantics)."""
+    cx = _ctx(ctx)
+    pa, lda = _dev_ptr_cm(a)
+    pb, ldb = _dev_ptr_cm(b)
+    pc, ldc = _dev_ptr_cm(c)
+    m, n = c.shape
+    k = a.shape[1] if trans_a.upper() == "N" else a.shape[0]
+    _sync_torch(a)
+    _check(cx._lib.lrgw_dev_dgemm(cx.handle, trans_a.upper().encode(), trans_b.upper().encode(), m, n, k,
+                                  float(alpha), ctypes.c_void_p(pa), lda, ctypes.c_void_p(pb), ldb, float(beta),
+                                  ctypes.c_void_p(pc), ldc), cx.handle, "dgemm")
+    return c
+
+
+def coulomb_apply_dev(dims, cell, x, y, zero_kernel: bool = False, ctx=None):
+    """y = V x for column-major float64 CUDA tensors (N_r x m)."""
+    cx = _ctx(ctx)
+    d, cl = _grid(dims, cell)
+    px, ldx = _dev_ptr_cm(x)
+    py, ldy = _dev_ptr_cm(y)
+    _sync_torch(x)
+    _check(cx._lib.lrgw_dev_coulomb_apply(cx.handle, d.ctypes.data_as(L.c_int_p), _dp(cl), int(zero_kernel),
+                                          ctypes.c_void_p(px), ldx, x.shape[1], ctypes.c_void_p(py), ldy),
+           cx.handle, "coulomb_apply")
+    return y

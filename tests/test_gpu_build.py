@@ -1,0 +1,116 @@
+"""GPU: the whole device-resident build (lrgw_build, stages 1-5) at BASELINE
+configs — against the reference at Si8 and through size-independent
+properties (plus the oracle's bit-exact pivot sequence) at Si64."""
+import numpy as np
+import pytest
+
+from helpers import rel
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def _cm(t):
+    return t.t().contiguous().t()
+
+
+def _eps_residual(L, ctx, ep, cfg, x):
+    """||eps (eps^-1 x) - x|| / ||x|| with eps = I - V (2 Theta T Theta^T)
+    applied matrix-free on the device (smw.hpp:116-169 definition)."""
+    import torch
+
+    th_p, k_p, t_p = ep.device_ptrs()
+    theta = L_tensor(th_p, (ep.n_r, ep.n_mu))
+    tmat = L_tensor(t_p, (ep.n_mu, ep.n_mu))
+    y = torch.empty_like(x)
+    L.eps_apply_dev(ep, x, y)
+    u = _cm(torch.empty(ep.n_mu, x.shape[1], dtype=torch.float64, device="cuda"))
+    L.dgemm_dev("T", "N", 1.0, theta, y, 0.0, u, ctx=ctx)
+    w = _cm(torch.empty_like(u))
+    L.dgemm_dev("N", "N", 2.0, tmat, u, 0.0, w, ctx=ctx)
+    z = _cm(torch.empty_like(x))
+    L.dgemm_dev("N", "N", 1.0, theta, w, 0.0, z, ctx=ctx)
+    vz = _cm(torch.empty_like(x))
+    L.coulomb_apply_dev(cfg.dims, cfg.cell3, z, vz, ctx=ctx)
+    r = y - vz - x
+    return float(torch.linalg.norm(r) / torch.linalg.norm(x))
+
+
+def L_tensor(ptr, shape):
+    """Zero-copy column-major torch view of a device buffer owned by an eps handle."""
+    import torch
+
+    n = shape[0] * shape[1]
+
+    class _Holder:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3,
+                                    "strides": None}
+
+    flat = torch.as_tensor(_Holder(), device="cuda")
+    return flat.view(shape[1], shape[0]).t()
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2403_12340_b200 import lrgw
+
+    return lrgw
+
+
+def test_si8_build_matches_reference(L, ctx, ref):
+    import torch
+
+    from paper_2403_12340_b200 import synth
+
+    cfg = synth.CONFIGS["si8"]
+    psi = synth.orbitals_host(cfg)
+    e = synth.energies(cfg)
+    a, b = psi[:, :16], psi[:, 16:]
+    dpsi = _cm(torch.from_numpy(np.ascontiguousarray(psi.T)).t().cuda())
+    ep = L.build(dpsi[:, :16], dpsi[:, 16:], e, cfg.dims, cfg.cell3, k_mu=cfg.k_mu, n_lambda=cfg.n_lambda, ctx=ctx)
+    pts_ref = ref.select_points(a, b, 128)
+    assert np.array_equal(ep.point_indices, pts_ref)
+    th_ref = ref.fit(a, b, pts_ref)
+    assert rel(ep.p_vc, th_ref) <= TOL
+    s7 = ref.elliptic_params(e, 16, 16)
+    h = 2 * s7[3] / cfg.n_lambda
+    nodes = [-s7[3] + i * h for i in range(cfg.n_lambda + 1)]
+    w = [0.5 * h if i in (0, cfg.n_lambda) else h for i in range(cfg.n_lambda + 1)]
+    acc = 2 * np.sqrt(s7[0] * s7[1]) / (np.pi * s7[2]) * ref.sum_node_terms(a[pts_ref], b[pts_ref], e, s7, nodes, w)
+    t_ref = 0.5 * (acc + acc.T)
+    assert rel(ep.t, t_ref) <= TOL
+    x = synth.probe_host(cfg.n_r)
+    y_ref, k_ref, _ = ref.build_and_apply(t_ref, th_ref, cfg.dims, cfg.cell3, x, threads=8)
+    assert rel(ep.k, k_ref) <= TOL
+    assert rel(L.epsilon_inverse_apply(ep, x), y_ref) <= TOL
+    st = ctx.stage_ms()
+    assert st["total"] > 0 and st["select"] > 0
+
+
+def test_si64_build_properties_and_pivots(L, ctx):
+    import torch
+
+    from oracle import restate as R
+    from paper_2403_12340_b200 import synth
+
+    cfg = synth.CONFIGS["si64"]
+    psi = synth.orbitals_device(cfg)
+    e = synth.energies(cfg)
+    ep = L.build(psi[:, :128], psi[:, 128:], e, cfg.dims, cfg.cell3, k_mu=cfg.k_mu, n_lambda=cfg.n_lambda,
+                 ctx=ctx)
+    assert ep.n_mu == 1024
+    pts = ep.point_indices
+    assert np.all(np.diff(pts) > 0)
+    # bit-exact pivots against the oracle restatement (oracle/select.c)
+    hpsi = psi.cpu().numpy()
+    pts_or, diag = R.select_points(hpsi[:, :128], hpsi[:, 128:], 1024, return_diag=True)
+    assert np.array_equal(pts, pts_or)
+    assert diag["recompute_events"] == 0
+    k = torch.from_numpy(ep.k)
+    assert float(torch.linalg.norm(k - k.T) / torch.linalg.norm(k)) <= 1e-12
+    assert float(torch.linalg.eigvalsh(k).max()) < 0
+    t = torch.from_numpy(ep.t)
+    assert float(torch.linalg.eigvalsh(t).max()) < 0
+    x = _cm(torch.randn(cfg.n_r, 8, dtype=torch.float64, device="cuda",
+                        generator=torch.Generator(device="cuda").manual_seed(7)))
+    assert _eps_residual(L, ctx, ep, cfg, x) <= 1e-9

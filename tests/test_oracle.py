@@ -1,0 +1,177 @@
+"""CPU: pin the oracle restatement (oracle/restate.py, oracle/select.c) against
+the compiled reference (oracle/_ref) and the reference's own known-answer
+tests, and against the committed golden fixtures (tests/golden/)."""
+import glob
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import restate as R
+from helpers import rel
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ---- reference KATs restated (proj/tests/*.cpp) ---------------------------
+
+def test_num_aux_kats():
+    # test_isdf.cpp:21-34
+    assert R.num_aux(8.0, 16, 16) == 128
+    assert R.num_aux(8.0, 128, 128) == 1024
+    assert R.num_aux(1.0, 1, 1) == 1
+    with pytest.raises(R.InvalidInput):
+        R.num_aux(0.0, 4, 4)
+    prev = 0
+    for k in np.arange(1.0, 12.01, 0.5):
+        n = R.num_aux(k, 7, 9)
+        assert n >= prev
+        prev = n
+
+
+def test_elliptic_kats():
+    # test_elliptic.cpp:12-62
+    for r in (0.0, 1 / 3, 0.5, 0.9, 0.99):
+        by_quad = R.integrate_adaptive(lambda th: 1.0 / math.sqrt(1.0 - r * r * math.sin(th) ** 2), 0.0,
+                                       1.57079632679489661923)
+        assert abs(R.elliptic_k(r) - by_quad) <= 1e-10 * by_quad
+    with pytest.raises(R.InvalidInput):
+        R.elliptic_k(1.0)
+    sn, cn, dn = R.jacobi_sn_cn_dn(R.elliptic_k(1 / 3), 1 / 3)
+    assert abs(sn - 1.0) <= 1e-10 and abs(cn) <= 1e-8
+    rng = np.random.default_rng(77)
+    for _ in range(200):
+        r, u = rng.uniform(0, 0.97), rng.uniform(-4, 4)
+        sn, cn, dn = R.jacobi_sn_cn_dn(u, r)
+        assert abs(sn * sn + cn * cn - 1) <= 1e-12
+        assert abs(dn * dn + r * r * sn * sn - 1) <= 1e-12
+
+
+def test_elliptic_params_kats():
+    # test_contour.cpp:35-65
+    s = R.elliptic_params([0.0, 1.0, 4.0], 1, 2, 1e-7)
+    assert abs(s.r - 1 / 3) <= 1e-15 and s.l > 0 and not s.bypass
+    assert abs(s.big_r - R.elliptic_k(1 / 3)) <= 1e-14 * s.big_r
+    s = R.elliptic_params([0.0, 2.0], 1, 1, 1e-7)
+    assert s.r == 0.0 and s.bypass
+    with pytest.raises(R.InvalidInput):
+        R.elliptic_params([0.0, 0.0, 1.0], 1, 2, 1e-7)
+
+
+def test_contour_toy_pins_constant():
+    # test_contour.cpp:84-95: energies (0, 2, 4), T = -0.75
+    v = np.ones((1, 1))
+    c = np.ones((1, 2))
+    e = [0.0, 2.0, 4.0]
+    spec = R.elliptic_params(e, 1, 2, 1e-10)
+    t, n, est = R.coupled_coefficients_contour(v, c, e, spec)
+    assert abs(t[0, 0] + 0.75) <= 0.75e-9 and n >= 17 and est <= 1e-10
+    assert abs(R.coupled_coefficients_direct(np.ones((1, 1)), np.ones((1, 1)), [0.0, 2.0])[0, 0] + 0.5) < 1e-15
+
+
+def test_cauchy_bound_kats():
+    # test_contour.cpp:152-170
+    assert abs(R.cauchy_error_bound(1.0, math.exp(2.0), 10) - math.exp(-math.pi ** 2)) <= 1e-12
+    b1, b2 = R.cauchy_error_bound(1.0, math.exp(2.0), 7), R.cauchy_error_bound(1.0, math.exp(2.0), 14)
+    assert abs(b2 - b1 * b1) <= 1e-12 * b2
+
+
+def test_coulomb_kats():
+    # test_model.cpp:68-80: kernel >= 0, v(0) = 0, kills constants
+    dims, cell = (4, 4, 4), (5.0, 5.0, 5.0)
+    v = R.coulomb_kernel(dims, cell)
+    assert np.all(v >= 0) and v[0] == 0.0
+    y = R.apply_coulomb(dims, cell, np.ones((64, 1)))
+    assert np.max(np.abs(y)) <= 1e-12
+
+
+# ---- restatement vs the compiled reference ---------------------------------
+
+def _desk(ref, seed=1, dims=(8, 8, 8), n=16, gap=1.0, bw=4.0):
+    psi, e = ref.build_synthetic(seed, dims, (6.0, 6.0, 6.0), n, n, gap, bw)
+    return psi[:, :n], psi[:, n:], e
+
+
+def test_restatement_matches_reference_isdf(ref):
+    a, b, e = _desk(ref)
+    p_ref = ref.select_points(a, b, 128)
+    p_or, diag = R.select_points(a, b, 128, return_diag=True)
+    assert np.array_equal(p_ref, p_or)
+    assert diag["recompute_events"] == 0
+    assert rel(R.fit_auxiliary_basis(a, b, p_or), ref.fit(a, b, p_ref)) <= 1e-12
+
+
+def test_restatement_matches_reference_selection_shapes(ref):
+    # N_mu = N_r selects all indices (test_isdf.cpp:36-44); N_mu > rank keeps the
+    # swapped tail (assemble_K rank-deficient fixture, test_smw.cpp:74-85)
+    psi, _ = ref.build_synthetic(3, (2, 2, 2), (4.0, 4.0, 4.0), 2, 2, 1.0, 2.0)
+    a, b = psi[:, :2], psi[:, 2:]
+    assert np.array_equal(R.select_points(a, b, 8), np.arange(8))
+    psi, _ = ref.build_synthetic(2, (4, 4, 4), (6.0, 6.0, 6.0), 2, 2, 1.0, 2.0)
+    a, b = psi[:, :2], psi[:, 2:]
+    assert np.array_equal(R.select_points(a, b, 8), ref.select_points(a, b, 8))
+    for seed, dims, n, nmu in [(6, (4, 4, 4), 4, 12), (5, (8, 4, 4), 6, 24), (3, (8, 8, 8), 8, 48)]:
+        psi, _ = ref.build_synthetic(seed, dims, (6.0, 6.0, 6.0), n, n, 1.0, 4.0)
+        a, b = psi[:, :n], psi[:, n:]
+        assert np.array_equal(R.select_points(a, b, nmu), ref.select_points(a, b, nmu))
+
+
+def test_restatement_matches_reference_contour(ref):
+    a, b, e = _desk(ref, seed=11)
+    pts = ref.select_points(a, b, 128)
+    pv, pc = a[pts], b[pts]
+    spec = R.elliptic_params(e, 16, 16, 1e-7)
+    assert np.allclose(spec.as7(), ref.elliptic_params(e, 16, 16), rtol=1e-14, atol=0)
+    nodes, w = R.trapezoid_nodes(spec, 24)
+    assert rel(R.sum_node_terms(pv, pc, e, spec, nodes, w), ref.sum_node_terms(pv, pc, e, spec.as7(), nodes, w)) < 1e-13
+    assert rel(R.coupled_coefficients_direct(pv, pc, e), ref.coupled_direct(pv, pc, e)) < 1e-13
+    t_r, n_r, est_r, st = ref.coupled_contour(pv, pc, e)
+    t_o, n_o, est_o = R.coupled_coefficients_contour(pv, pc, e, spec)
+    assert st == 0 and n_r == n_o and rel(t_o, t_r) < 1e-13
+    for t_node in (-spec.big_r, 0.1, spec.big_r):
+        assert rel(R.node_term(pv, pc, e, spec, t_node), ref.node_term(pv, pc, e, spec.as7(), t_node)) < 1e-13
+
+
+def test_restatement_matches_reference_smw(ref):
+    dims, cell = (8, 8, 8), (6.0, 6.0, 6.0)
+    a, b, e = _desk(ref, seed=7)
+    pts = ref.select_points(a, b, 128)
+    th = ref.fit(a, b, pts)
+    t = ref.coupled_direct(a[pts], b[pts], e)
+    x = ref.gaussian(19, 512, 4)
+    assert rel(R.apply_coulomb(dims, cell, x), ref.apply_coulomb(dims, cell, x)) < 1e-13
+    k_o = R.assemble_K(t, th, dims, cell)
+    y_r, k_r, _ = ref.build_and_apply(t, th, dims, cell, x)
+    assert rel(k_o, k_r) < 1e-12
+    assert rel(R.epsilon_inverse_apply(th, k_o, dims, cell, x), y_r) < 1e-13
+
+
+def test_restatement_error_behaviour(ref):
+    # degenerate Gram (test_isdf.cpp:228-231) and rank-deficient T (test_smw.cpp:74-85)
+    with pytest.raises(R.NumericError):
+        R.fit_auxiliary_basis(np.zeros((8, 2)), np.zeros((8, 2)), [1, 3])
+    with pytest.raises(R.NumericError):
+        ref.fit(np.zeros((8, 2)), np.zeros((8, 2)), [1, 3])
+    with pytest.raises(R.InvalidInput):
+        R.fit_auxiliary_basis(np.ones((8, 2)), np.ones((8, 2)), [3, 1])
+
+
+# ---- golden fixtures (generated by tests/golden/make_golden.py from _ref) --
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "*.npz"))))
+def test_oracle_against_golden(path):
+    g = np.load(path)
+    n_v, n_c = int(g["n_v"]), int(g["n_c"])
+    dims, cell = tuple(g["dims"]), tuple(g["cell"])
+    a, b = g["psi"][:, :n_v], g["psi"][:, n_v:n_v + n_c]
+    pts = R.select_points(a, b, int(g["n_mu"]))
+    assert np.array_equal(pts, g["pts"])
+    assert rel(R.fit_auxiliary_basis(a, b, pts), g["theta"]) <= 1e-10
+    pv, pc = a[pts], b[pts]
+    assert rel(R.coupled_coefficients_direct(pv, pc, g["energies"]), g["t_direct"]) <= 1e-12
+    spec = R.elliptic_params(g["energies"], n_v, n_c, 1e-7)
+    if not spec.bypass:
+        assert rel(R.coupled_coefficients_fixed(pv, pc, g["energies"], spec, int(g["n_lambda"])), g["t_fixed"]) <= 1e-12
+    assert rel(R.assemble_K(g["t_direct"], g["theta"], dims, cell), g["k"]) <= 1e-10
+    assert rel(R.epsilon_inverse_apply(g["theta"], g["k"], dims, cell, g["x"]), g["y"]) <= 1e-12

@@ -1,0 +1,126 @@
+// FP64 peak microbenchmarks for B200 (sm_100a): DFMA pipe vs DMMA (mma.sync f64).
+// Used once to fix the FP64 roofline denominator (MEASURED_PEAKS.json has none)
+// and to choose between DFMA and DMMA for the hot GEMMs.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_peaks fp64_peaks.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
+
+template <int CHAINS>
+__global__ void dfma_loop(double* out, int iters, double a, double b) {
+  double acc[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) acc[c] = threadIdx.x * 1e-9 + c;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) acc[c] = fma(acc[c], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += acc[c];
+  if (s == 12345.678) out[0] = s;
+}
+
+template <int CHAINS>
+__global__ void dmma_loop(double* out, int iters) {
+  const int lane = threadIdx.x & 31;
+  double a = 1.0 + lane * 1e-6, b = 1.0 - lane * 1e-6;
+  double c[CHAINS][2];
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i) { c[i][0] = 0; c[i][1] = 0; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < CHAINS; ++i) {
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[0] = s;
+}
+
+template <int CHAINS>
+__global__ void dmma16_loop(double* out, int iters) {
+  const int lane = threadIdx.x & 31;
+  double a[8], b[4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = 1.0 + (lane + i) * 1e-6;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = 1.0 - (lane + i) * 1e-6;
+  double c[CHAINS][4];
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i) { c[i][0] = c[i][1] = c[i][2] = c[i][3] = 0; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < CHAINS; ++i) {
+      asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+                   "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
+                   : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                     "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+  if (s == 12345.678) out[0] = s;
+}
+
+int main() {
+  double* d;
+  CK(cudaMalloc(&d, 64));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float ms;
+  const int iters = 20000;
+  for (int wpb : {4, 8, 16}) {
+    for (int bps : {1, 2, 4}) {
+      int blocks = sms * bps, threads = 32 * wpb;
+      dfma_loop<8><<<blocks, threads>>>(d, 100, 1.0000001, 1e-9);
+      CK(cudaDeviceSynchronize());
+      cudaEventRecord(e0);
+      dfma_loop<8><<<blocks, threads>>>(d, iters, 1.0000001, 1e-9);
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1));
+      cudaEventElapsedTime(&ms, e0, e1);
+      double fl = 2.0 * 8 * iters * (double)blocks * threads;
+      printf("DFMA   warps/blk=%2d blk/SM=%d : %8.2f TFLOP/s (%.3f ms)\n", wpb, bps, fl / ms / 1e9, ms);
+    }
+  }
+  for (int wpb : {4, 8, 16}) {
+    for (int bps : {1, 2, 4}) {
+      int blocks = sms * bps, threads = 32 * wpb;
+      dmma_loop<8><<<blocks, threads>>>(d, 100);
+      CK(cudaDeviceSynchronize());
+      cudaEventRecord(e0);
+      dmma_loop<8><<<blocks, threads>>>(d, iters);
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1));
+      cudaEventElapsedTime(&ms, e0, e1);
+      double fl = 2.0 * 256 * 8 * iters * (double)blocks * wpb;
+      printf("DMMA884 warps/blk=%2d blk/SM=%d : %8.2f TFLOP/s (%.3f ms)\n", wpb, bps, fl / ms / 1e9, ms);
+    }
+  }
+  for (int wpb : {4, 8}) {
+    for (int bps : {1, 2}) {
+      int blocks = sms * bps, threads = 32 * wpb;
+      dmma16_loop<4><<<blocks, threads>>>(d, 100);
+      CK(cudaDeviceSynchronize());
+      cudaEventRecord(e0);
+      dmma16_loop<4><<<blocks, threads>>>(d, iters / 4);
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1));
+      cudaEventElapsedTime(&ms, e0, e1);
+      double fl = 2.0 * 16 * 8 * 16 * 4 * (iters / 4) * (double)blocks * wpb;
+      printf("DMMA16816 warps/blk=%2d blk/SM=%d : %8.2f TFLOP/s (%.3f ms)\n", wpb, bps, fl / ms / 1e9, ms);
+    }
+  }
+  return 0;
+}
