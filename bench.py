@@ -1,0 +1,331 @@
+"""bench.py — low-rank eps^-1 build time on B200 (BASELINE.json metric).
+
+One step = the factored eps^-1 build, stages 1-5 (ISDF point selection, Theta
+fit, Cauchy quadrature of the core, G-space Theta^T V Theta, SMW core K), plus
+eps^-1 applied to the seeded 8-column probe block, on the Si64-sized config
+(BASELINE.json configs[1], the primary 1-GPU roofline case):
+
+  value      device time per build with inputs resident in HBM (CUDA events
+             on the library stream, max over ranks)
+  e2e        the same step through the C-ABI from pinned HOST buffers: the
+             H2D copy of Phi and of the probe and the D2H of eps^-1 X inside
+             the timed region
+  roofline   the dominant kernel of the step (largest device-time share),
+             algorithmic FLOPs / its CUDA-event duration against
+             the measured FP64 peak (profiles/FP64_PEAK.json: DMMA 37.17
+             TFLOP/s; MEASURED_PEAKS.json has no FP64 entry)
+  cpu_baseline  the reference CPU implementation (oracle/_ref) on the host
+             cores on a bounded, extrapolated sample (oracle/cpu_baseline.py)
+
+Inputs are larger than L2 (Phi 226 MB, Theta 906 MB) — no explicit flush.
+N > 1 (torchrun): "replicas only" this round — every rank builds its own
+replica (no data-path collective); the per-rank time is max-reduced.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config si64] [--impl ours|reference]
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.17  # profiles/FP64_PEAK.json (measured DMMA loop, 148 SMs, 1965 MHz)
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm = 6552.3
+    if os.path.exists(p):
+        try:
+            hbm = float(json.load(open(p)).get("hbm_gbs", hbm))
+        except Exception:
+            pass
+    return hbm
+
+
+def algorithmic_work(cfg, n_mu):
+    """Per-launch algorithmic FLOPs / bytes."""
+    n_r, n = cfg.n_r, cfg.n_v + cfg.n_c
+    nh = (cfg.dims[0] // 2 + 1) * cfg.dims[1] * cfg.dims[2]
+    return {
+        "select": ("tensor", 2.0 * n_r * (n_mu * n + n_mu * (n_mu - 1) / 2.0)),
+        "fit_lhs": ("tensor", 2.0 * n_r * n_mu * n),
+        "fit_gemm": ("tensor", 2.0 * n_r * n_mu * n_mu),
+        "contour": ("tensor", 2.0 * n_mu * (n_mu + 1) * n * (cfg.n_lambda + 1)),
+        "fft": ("hbm", 8.0 * n_r * n_mu + 16.0 * nh * n_mu),
+        "pvp": ("tensor", 1.0 * n_r * n_mu * (n_mu + 1)),
+    }
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, gpu):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        out = self.proc.communicate()[0].strip().splitlines()
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(int(float(f[0])))
+                mx = max(mx, int(float(f[1])))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        dist.init_process_group(backend)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x, world, device):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_ours(args, cfg, world, rank, local):
+    import torch
+
+    from paper_2403_12340_b200 import lrgw, synth
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ctx = lrgw.Context(local)
+    stream = torch.cuda.ExternalStream(lrgw.L.load().lrgw_ctx_stream(ctx.handle), device=dev)
+    psi = synth.orbitals_device(cfg, seed=1, device=dev)
+    e = synth.energies(cfg)
+    phi_v, phi_c = psi[:, :cfg.n_v], psi[:, cfg.n_v:]
+    x_host = synth.probe_host(cfg.n_r)
+    x_dev = torch.from_numpy(np.ascontiguousarray(x_host.T)).to(dev).t()
+    y_dev = torch.empty(8, cfg.n_r, dtype=torch.float64, device=dev).t()
+    torch.cuda.synchronize()
+
+    def step_dev():
+        ep = lrgw.build(phi_v, phi_c, e, cfg.dims, cfg.cell3, k_mu=cfg.k_mu, n_lambda=cfg.n_lambda, ctx=ctx)
+        lrgw.eps_apply_dev(ep, x_dev, y_dev)
+        return ep
+
+    for _ in range(args.warmup):
+        step_dev().close()
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region ----
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    launches0 = ctx.kernel_launches()
+    stage_acc = {}
+    t_steps = []
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    for _ in range(args.steps):
+        e0.record(stream)
+        ep = step_dev()
+        e1.record(stream)
+        e1.synchronize()
+        t_steps.append(e0.elapsed_time(e1))
+        for k, v in ctx.stage_ms().items():
+            stage_acc.setdefault(k, []).append(v)
+        ep.close()
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    launches = ctx.kernel_launches() - launches0
+    ms_local = sum(t_steps) / len(t_steps)
+    ms = max_over_ranks(ms_local, world, dev)
+
+    # ---- e2e through the C-ABI from pinned host buffers ----
+    psi_h = torch.empty(psi.shape[1], psi.shape[0], dtype=torch.float64).pin_memory()
+    psi_h.copy_(psi.t())
+    x_h = torch.from_numpy(np.ascontiguousarray(x_host.T)).pin_memory()
+    y_h = torch.empty(8, cfg.n_r, dtype=torch.float64).pin_memory()
+    psi_d = torch.empty(psi.shape[1], psi.shape[0], dtype=torch.float64, device=dev)
+    x_d = torch.empty(8, cfg.n_r, dtype=torch.float64, device=dev)
+    y_d = torch.empty(8, cfg.n_r, dtype=torch.float64, device=dev)
+
+    def step_e2e():
+        with torch.cuda.stream(stream):
+            psi_d.copy_(psi_h, non_blocking=True)
+            x_d.copy_(x_h, non_blocking=True)
+        pd = psi_d.t()
+        ep = lrgw.build(pd[:, :cfg.n_v], pd[:, cfg.n_v:], e, cfg.dims, cfg.cell3, k_mu=cfg.k_mu,
+                        n_lambda=cfg.n_lambda, ctx=ctx)
+        lrgw.eps_apply_dev(ep, x_d.t(), y_d.t())
+        with torch.cuda.stream(stream):
+            y_h.copy_(y_d, non_blocking=True)
+        ep.close()
+
+    step_e2e()
+    torch.cuda.synchronize()
+    barrier(world)
+    e2e_ms = []
+    for _ in range(max(1, min(args.steps, 5))):
+        e0.record(stream)
+        step_e2e()
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e = max_over_ranks(sum(e2e_ms) / len(e2e_ms), world, dev)
+    h2d = psi_h.numel() * 8 + x_h.numel() * 8
+    d2h = y_h.numel() * 8
+    # parity guard on the bench output: eps^-1 X finite and the probe changed
+    assert torch.isfinite(y_d).all()
+
+    stages = {k: statistics.median(v) for k, v in stage_acc.items()}
+    n_mu = min(max(lrgw.num_aux(cfg.k_mu, cfg.n_v, cfg.n_c), 1), cfg.n_r)
+    work = algorithmic_work(cfg, n_mu)
+    hbm = _peaks()
+    kernels = {}
+    for k, (bound, amount) in work.items():
+        t = stages.get(k, 0.0)
+        if t <= 0:
+            continue
+        if bound == "tensor":
+            ach = amount / (t * 1e-3) / 1e12
+            kernels[k] = {"ms": round(t, 4), "bound": "tensor", "achieved": round(ach, 3),
+                          "unit": "TFLOP/s", "frac": round(ach / FP64_PEAK_TFLOPS, 4)}
+        else:
+            ach = amount / (t * 1e-3) / 1e9
+            kernels[k] = {"ms": round(t, 4), "bound": "hbm", "achieved": round(ach, 1), "unit": "GB/s",
+                          "frac": round(ach / hbm, 4)}
+    for k in ("fit_solve", "smw"):
+        kernels[k] = {"ms": round(stages.get(k, 0.0), 4), "bound": "cusolver-leaf"}
+    dom = max((k for k in kernels if "achieved" in kernels[k]), key=lambda k: kernels[k]["ms"])
+    dk = kernels[dom]
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(dom)
+    roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"],
+                "peak": FP64_PEAK_TFLOPS if dk["bound"] == "tensor" else hbm,
+                "unit": dk["unit"], "frac": dk["frac"], "traffic": traffic,
+                "peak_source": "profiles/FP64_PEAK.json (measured DMMA)" if dk["bound"] == "tensor"
+                else "MEASURED_PEAKS.json hbm_gbs"}
+    return {"ms": ms, "e2e_ms": e2e, "h2d": h2d, "d2h": d2h, "launches": launches, "clocks": clk,
+            "stages": stages, "kernels": kernels, "roofline": roofline, "psi": psi, "e": e, "ctx": ctx}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="si64")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    from paper_2403_12340_b200 import synth
+
+    cfg = synth.CONFIGS[args.config]
+    world, rank, local = dist_setup(args)
+    workload = {"workload": f"{cfg.name}: grid {cfg.dims[0]}^3 = {cfg.n_r} points, cell {cfg.cell} bohr, "
+                            f"N_v = N_c = {cfg.n_v}, N_mu = {int(round(cfg.k_mu * (cfg.n_v * cfg.n_c) ** 0.5))}, "
+                            f"N_lambda = {cfg.n_lambda}, eps^-1 X on an {cfg.n_r}x8 probe",
+                "stages": "1-5 (select, fit, quadrature, Coulomb/ThetaVTheta, SMW) + probe apply",
+                "l2": "inputs larger than L2 (Phi 226 MB, Theta 906 MB at si64); no flush",
+                "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"}
+    metric = "low-rank eps^-1 build time (s), stages 1-5 + probe apply"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from oracle import cpu_baseline
+
+        cores = os.cpu_count() or 1
+        vals = []
+        for i in range(args.steps + 1):  # one untimed warm-up sample
+            r = cpu_baseline.run(cfg, cores=cores, sel_steps=16, fit_rows=(1536, 2560), cols=64, seed=5 + i)
+            if i > 0:
+                vals.append(r["total_s"])
+        v = statistics.median(vals)
+        line = {"impl": "reference", "metric": metric, "value": v, "unit": "s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": 1, "ms_per_step": v * 1e3, "higher_is_better": False,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+                "config": workload,
+                "cpu_baseline": {"value": v, "unit": "s", "cores": r["cores"], "kind": "reference",
+                                 "sample": r["sample"], "stages_s": r["stages"],
+                                 "no_select_s": statistics.median(vals) - r["stages"]["select"]},
+                "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    res = run_ours(args, cfg, world, rank, local)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import cpu_baseline
+
+        psi_h = np.asfortranarray(res["psi"].cpu().numpy())
+        r = cpu_baseline.run(cfg, psi=psi_h, energies=res["e"], cores=os.cpu_count())
+        cpu = {"value": r["total_s"], "unit": "s", "cores": r["cores"], "kind": "reference",
+               "sample": r["sample"], "stages_s": {k: round(v, 3) for k, v in r["stages"].items()},
+               "no_select_s": r["total_no_select_s"]}
+    if rank == 0:
+        line = {"metric": metric, "value": res["ms"] / 1e3, "unit": "s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": False,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+                "config": workload,
+                "e2e": {"value": res["e2e_ms"] / 1e3, "unit": "s", "h2d_bytes_per_step": res["h2d"],
+                        "d2h_bytes_per_step": res["d2h"]},
+                "gpu_launches": res["launches"], "clocks": res["clocks"],
+                "roofline": res["roofline"], "stages_ms": {k: round(v, 4) for k, v in res["stages"].items()},
+                "kernels": res["kernels"], "cpu_baseline": cpu}
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

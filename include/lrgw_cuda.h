@@ -41,17 +41,19 @@ enum lrgw_status {
 /* PointSelector (isdf.hpp:28) */
 enum lrgw_point_selector { LRGW_QRCP_DIRECT = 0, LRGW_QRCP_SKETCHED = 1 };
 
-/* Build stages timed by lrgw_build (device time, CUDA events). */
+/* Build stages timed by lrgw_build (device time, CUDA events on the context
+ * stream, consecutive intervals). */
 enum lrgw_stage {
-  LRGW_STAGE_SELECT = 0,  /* ISDF point selection                */
-  LRGW_STAGE_FIT = 1,     /* Theta = (Z C^T)(C C^T)^-1           */
-  LRGW_STAGE_FIT_SOLVE = 2, /* cuSOLVER leaf: G_mumu factor+inverse (inside FIT) */
-  LRGW_STAGE_CONTOUR = 3, /* Cauchy quadrature of the core T     */
-  LRGW_STAGE_FFT = 4,     /* cuFFT leaf: batched D2Z of Theta    */
-  LRGW_STAGE_PVP = 5,     /* Theta^T V Theta G-space SYRK        */
-  LRGW_STAGE_SMW = 6,     /* cuSOLVER leaf: SMW core K           */
-  LRGW_STAGE_TOTAL = 7,
-  LRGW_NUM_STAGES = 8
+  LRGW_STAGE_SELECT = 0,    /* K1 ISDF point selection                         */
+  LRGW_STAGE_FIT_LHS = 1,   /* K2a (Phi Phi_mu^T) o (Phi Phi_mu^T) + gathers   */
+  LRGW_STAGE_FIT_SOLVE = 2, /* cuSOLVER leaf: G_mumu LU + inverse              */
+  LRGW_STAGE_FIT_GEMM = 3,  /* K2b Theta = lhs G^-1                            */
+  LRGW_STAGE_CONTOUR = 4,   /* K3 Cauchy quadrature of the core T              */
+  LRGW_STAGE_FFT = 5,       /* cuFFT leaf: batched D2Z of Theta                */
+  LRGW_STAGE_PVP = 6,       /* K5 Theta^T V Theta G-space SYRK                 */
+  LRGW_STAGE_SMW = 7,       /* K6 cuSOLVER leaf: SMW core K                    */
+  LRGW_STAGE_TOTAL = 8,
+  LRGW_NUM_STAGES = 9
 };
 
 typedef struct lrgw_ctx_s* lrgw_ctx;

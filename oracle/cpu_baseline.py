@@ -1,0 +1,111 @@
+"""oracle/cpu_baseline.py — TEST/BENCH INFRASTRUCTURE ONLY (the CPU baseline).
+
+Times the reference CPU implementation of the eps^-1 build (stages 1-5) on
+the host cores through oracle/_ref (the unmodified reference headers) on a
+BOUNDED SAMPLE of the BASELINE workload and extrapolates each stage by its
+exact cost model. The full Si64 build takes ~8 min on 8 cores, so
+each stage is sampled:
+
+  1 select   reference qrcp is guard-blocked beyond 2^26 pair entries
+             (isdf.hpp:49, 77-78), so the greedy restatement oracle/select.c
+             (OpenMP, all cores) runs the first S pivot steps; per-step cost
+             is linear in (N_v + N_c + k), summed over k < N_mu.
+  2 fit      reference fit_auxiliary_basis (isdf.hpp:118-163, serial) on two
+             row samples (all N_mu point rows + filler rows); t = a + b N_rows
+             fitted and evaluated at N_r (LU of the N_mu Gram is the constant).
+  3 contour  reference detail::sum_node_terms (contour.hpp:185-222) over ALL
+             N_lambda + 1 nodes with threads = cores (no extrapolation).
+  4-5 SMW    reference sym_eig(T), lu_solve(T, I/2), lu_invert on the real T
+             (full size); apply_coulomb on C columns (threads = cores) scaled
+             by 2 N_mu / C (the reference applies V to P twice, smw.hpp:61, 92);
+             matmul_tn on a C-column block scaled by (N_mu / C)^2.
+
+Only bench.py (cpu_baseline leg and --impl reference) imports this module.
+"""
+from __future__ import annotations
+
+import os
+import time
+
+import numpy as np
+
+from . import ref
+from . import restate as R
+
+
+def _t(fn):
+    t0 = time.perf_counter()
+    out = fn()
+    return time.perf_counter() - t0, out
+
+
+def run(cfg, psi=None, energies=None, cores=None, sel_steps=64, fit_rows=(2048, 4096), cols=128, seed=5):
+    """Returns dict(total_s, total_no_select_s, stages, sample, cores)."""
+    cores = cores or os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    n_r, n_v, n_c = cfg.n_r, cfg.n_v, cfg.n_c
+    n = n_v + n_c
+    n_mu = min(max(R.num_aux(cfg.k_mu, n_v, n_c), 1), n_r)
+    rng = np.random.default_rng(seed)
+    if psi is None:
+        psi = np.asfortranarray(np.linalg.qr(rng.standard_normal((n_r, n)))[0])
+    e = energies if energies is not None else np.concatenate(
+        [np.sort(rng.uniform(*cfg.occ, n_v)), np.sort(rng.uniform(*cfg.virt, n_c))])
+    a, b = psi[:, :n_v], psi[:, n_v:n]
+    stages = {}
+
+    # 1: greedy selection restatement, first S steps, extrapolated
+    s = min(sel_steps, n_mu)
+    t_sel, _ = _t(lambda: R.select_points(a, b, s))
+    w_s = sum(n + k + 1 for k in range(s))
+    w_all = sum(n + k + 1 for k in range(n_mu))
+    stages["select"] = t_sel * w_all / w_s
+
+    # 2: reference fit on two row samples containing all point rows
+    pts = np.sort(rng.choice(n_r, n_mu, replace=False)).astype(np.int32)
+    others = np.setdiff1d(np.arange(n_r), pts)
+    times = []
+    for rows in fit_rows:
+        rows = max(rows, n_mu + 1)
+        extra = np.sort(rng.choice(others, rows - n_mu, replace=False))
+        sel = np.sort(np.concatenate([pts, extra]))
+        sub_pts = np.searchsorted(sel, pts).astype(np.int32)
+        asub, bsub = np.asfortranarray(a[sel]), np.asfortranarray(b[sel])
+        t_fit, _ = _t(lambda: ref.fit(asub, bsub, sub_pts))
+        times.append((rows, t_fit))
+    (r1, t1), (r2, t2) = times
+    slope = (t2 - t1) / (r2 - r1)
+    stages["fit"] = max(t1 + slope * (n_r - r1), t2)
+
+    # 3: reference quadrature, all nodes, threads = cores
+    pv, pc = np.asfortranarray(a[pts]), np.asfortranarray(b[pts])
+    s7 = ref.elliptic_params(e, n_v, n_c)
+    h = 2 * s7[3] / cfg.n_lambda
+    nodes = [-s7[3] + i * h for i in range(cfg.n_lambda + 1)]
+    wts = [0.5 * h if i in (0, cfg.n_lambda) else h for i in range(cfg.n_lambda + 1)]
+    t_quad, acc = _t(lambda: ref.sum_node_terms(pv, pc, e, s7, nodes, wts, threads=cores))
+    stages["contour"] = t_quad
+    t_mat = 2 * np.sqrt(s7[0] * s7[1]) / (np.pi * s7[2]) * acc
+    t_mat = 0.5 * (t_mat + t_mat.T)
+
+    # 4-5: SMW pieces of build_epsilon_inverse (smw.hpp:42-94)
+    c = min(cols, n_mu)
+    p_blk = np.asfortranarray(rng.standard_normal((n_r, c)) / np.sqrt(n_r))
+    t_eig, _ = _t(lambda: ref.sym_eig_values(t_mat))
+    t_half, half = _t(lambda: ref.lu_solve(t_mat, 0.5 * np.eye(n_mu)))
+    t_vp, vp_blk = _t(lambda: ref.apply_coulomb(cfg.dims, cfg.cell3, p_blk, threads=cores))
+    t_tn, g = _t(lambda: ref.matmul_tn(p_blk, vp_blk))
+    mid = 0.5 * (half + half.T)
+    mid[:c, :c] -= 0.5 * (g + g.T)
+    t_inv, _ = _t(lambda: ref.lu_solve(mid, np.eye(n_mu)))
+    stages["smw_eig"] = t_eig
+    stages["smw_lu"] = t_half + t_inv
+    stages["coulomb"] = t_vp * 2.0 * n_mu / c
+    stages["pvp"] = t_tn * (n_mu / c) ** 2
+    total = sum(stages.values())
+    sample = (f"{cfg.name}: select {s}/{n_mu} greedy steps (restatement, {cores} threads) x{w_all / w_s:.1f}; "
+              f"fit on {fit_rows} rows -> linear in N_r={n_r}; all {cfg.n_lambda + 1} nodes; sym_eig/LU at "
+              f"N_mu={n_mu}; apply_coulomb {c} cols x{2 * n_mu / c:.0f}; matmul_tn {c}x{c} block "
+              f"x{(n_mu / c) ** 2:.0f}")
+    return {"total_s": total, "total_no_select_s": total - stages["select"], "stages": stages,
+            "sample": sample, "cores": cores}

@@ -279,3 +279,17 @@ def sym_eig_values(a):
     out = np.zeros(a.shape[0])
     _check(lib().ref_sym_eig_values(_d(a), a.shape[0], _d(out)), "sym_eig")
     return out
+
+
+def matmul_tn(a, b):
+    a, b = _f(a), _f(b)
+    c = np.zeros((a.shape[1], b.shape[1]), order="F")
+    _check(lib().ref_matmul_tn(_d(a), a.shape[0], a.shape[1], _d(b), b.shape[1], _d(c)), "matmul_tn")
+    return c
+
+
+def lu_solve(a, b):
+    a, b = _f(a), _f(b)
+    x = np.zeros_like(b, order="F")
+    _check(lib().ref_lu_solve(_d(a), a.shape[0], _d(b), b.shape[1], _d(x)), "lu_solve")
+    return x

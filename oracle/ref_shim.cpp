@@ -405,6 +405,16 @@ int ref_epsilon_dense(const double* psi, int n_r, int n_v, int n_c,
   });
 }
 
+// matrix.hpp:88-102 — C = A^T B (the reference's pvp contraction, smw.hpp:61).
+int ref_matmul_tn(const double* a, int m, int ka, const double* b, int kb, double* c) {
+  return guarded([&] { to_ptr(matmul_tn(from_ptr(a, m, ka), from_ptr(b, m, kb)), c); });
+}
+
+// linalg.hpp:152-183 — X = A^-1 B by LU (lu_solve), B n x nrhs.
+int ref_lu_solve(const double* a, int n, const double* b, int nrhs, double* x) {
+  return guarded([&] { to_ptr(lu_solve(from_ptr(a, n, n), from_ptr(b, n, nrhs)), x); });
+}
+
 // linalg.hpp:310-345 — ascending eigenvalues.
 int ref_sym_eig_values(const double* a, int n, double* values) {
   return guarded([&] {

@@ -67,6 +67,8 @@ struct lrgw_ctx_s {
   std::string err;
   int pivot = -1;
   double stage_ms[LRGW_NUM_STAGES] = {};
+  cudaEvent_t ev[LRGW_NUM_STAGES + 1] = {};
+  bool timing = false;  // record stage events (lrgw_build only)
   long long launches0 = 0;
   int select_batch = 64;
 };
@@ -140,6 +142,11 @@ void download(lrgw_ctx c, void* h, const void* d, size_t bytes) {
 }
 
 void use_device(lrgw_ctx c) { ck(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+// Stage boundary i of the build (no-op outside lrgw_build).
+void mark(lrgw_ctx c, int i) {
+  if (c->timing) ck(cudaEventRecord(c->ev[i], c->stream), "cudaEventRecord");
+}
 
 // The ABI wrapper: run the body, map failures onto status codes.
 template <class F>
@@ -283,11 +290,11 @@ void gemm(lrgw_ctx c, int M, int N, int K, const double* A, long long lda, Lay l
 // one batched D2Z of Theta (cuFFT leaf), then a lower-triangle DMMA GEMM over
 // K = 2 * half_len interleaved reals with w_G v(G)/N_r fused as the scale.
 void pvp_impl(lrgw_ctx c, const int* dims, const double* cell, int zero, const double* theta,
-              long long ldt, int n_mu, double* pvp, cudaEvent_t ev_fft_end) {
+              long long ldt, int n_mu, double* pvp) {
   const long long nh = half_len(dims);
   DBuf xh = dalloc(c, (size_t)2 * nh * n_mu);
   fft_forward(c, dims, theta, ldt, n_mu, xh.d());
-  if (ev_fft_end) ck(cudaEventRecord(ev_fft_end, c->stream), "event");
+  mark(c, 6);
   DBuf wts = dalloc(c, (size_t)2 * nh);
   ck(coulomb_half_weights(c->stream, dims[0], dims[1], dims[2], cell[0], cell[1], cell[2], zero, wts.d()),
      "coulomb_half_weights");
@@ -510,8 +517,7 @@ void check_points(const int32_t* pts, int n_mu, int n_r) {
 }
 
 void fit_impl(lrgw_ctx c, const double* a, long long lda, int n1, const double* b, long long ldb, int n2,
-              int n_r, const int32_t* pts, int n_mu, double* theta, long long ldt, cudaEvent_t ev_solve0,
-              cudaEvent_t ev_solve1) {
+              int n_r, const int32_t* pts, int n_mu, double* theta, long long ldt) {
   check_points(pts, n_mu, n_r);
   DBuf dp = upload_i(c, pts, n_mu);
   DBuf amu = dalloc(c, (size_t)n_mu * n1), bmu = dalloc(c, (size_t)n_mu * n2);
@@ -525,9 +531,9 @@ void fit_impl(lrgw_ctx c, const double* a, long long lda, int n1, const double* 
   ck(gather_rows(c->stream, lhs.d(), n_r, n_mu, dp.i(), n_mu, gram.d(), n_mu), "gather");
   ck(mirror_lower(c->stream, gram.d(), n_mu, n_mu, true), "symmetrize");
   DBuf ginv = dalloc(c, (size_t)n_mu * n_mu);
-  if (ev_solve0) ck(cudaEventRecord(ev_solve0, c->stream), "event");
+  mark(c, 2);
   gram_inverse(c, gram.d(), n_mu, ginv.d());
-  if (ev_solve1) ck(cudaEventRecord(ev_solve1, c->stream), "event");
+  mark(c, 3);
   gemm(c, n_r, n_mu, n_mu, lhs.d(), n_r, Lay::MN, ginv.d(), n_mu, Lay::MN, theta, ldt, 1.0, 0.0);
 }
 
@@ -689,6 +695,8 @@ int lrgw_ctx_destroy(lrgw_ctx c) {
   for (auto& kv : c->plans) cufftDestroy(kv.second);
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  for (auto& x : c->ev)
+    if (x) cudaEventDestroy(x);
   delete c;
   return LRGW_OK;
 }
@@ -798,7 +806,7 @@ int lrgw_fit_auxiliary_basis(lrgw_ctx c, const double* psi_a, const double* psi_
     check_points(pts, n_mu, n_r);
     DBuf a = upload(c, psi_a, (size_t)n_r * n1), b = upload(c, psi_b, (size_t)n_r * n2);
     DBuf th = dalloc(c, (size_t)n_r * n_mu);
-    fit_impl(c, a.d(), n_r, n1, b.d(), n_r, n2, n_r, pts, n_mu, th.d(), n_r, nullptr, nullptr);
+    fit_impl(c, a.d(), n_r, n1, b.d(), n_r, n2, n_r, pts, n_mu, th.d(), n_r);
     download(c, theta, th.p, sizeof(double) * n_r * n_mu);
   });
 }
@@ -926,7 +934,7 @@ int lrgw_assemble_K(lrgw_ctx c, const double* t, const double* p, int n_r, int n
       fail(LRGW_ERR_INVALID_INPUT, "assemble_K: T / P_vc shape mismatch");
     DBuf dt = upload(c, t, (size_t)n_mu * n_mu), dp = upload(c, p, (size_t)n_r * n_mu);
     DBuf pvp = dalloc(c, (size_t)n_mu * n_mu), dk = dalloc(c, (size_t)n_mu * n_mu);
-    pvp_impl(c, dims, cell, zero, dp.d(), n_r, n_mu, pvp.d(), nullptr);
+    pvp_impl(c, dims, cell, zero, dp.d(), n_r, n_mu, pvp.d());
     smw_core(c, dt.d(), pvp.d(), n_mu, dk.d());
     download(c, k, dk.p, sizeof(double) * n_mu * n_mu);
   });
@@ -960,7 +968,7 @@ int lrgw_build_epsilon_inverse(lrgw_ctx c, const double* t, const double* p, int
       fail(LRGW_ERR_INVALID_INPUT, "assemble_K: T / P_vc shape mismatch");
     DBuf dt = upload(c, t, (size_t)n_mu * n_mu), dp = upload(c, p, (size_t)n_r * n_mu);
     DBuf pvp = dalloc(c, (size_t)n_mu * n_mu), dk = dalloc(c, (size_t)n_mu * n_mu);
-    pvp_impl(c, dims, cell, zero, dp.d(), n_r, n_mu, pvp.d(), nullptr);
+    pvp_impl(c, dims, cell, zero, dp.d(), n_r, n_mu, pvp.d());
     smw_core(c, dt.d(), pvp.d(), n_mu, dk.d());
     ck(cudaStreamSynchronize(c->stream), "sync");
     auto* e = new lrgw_eps_s;
@@ -1068,22 +1076,21 @@ int lrgw_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, lo
     host_status(lrgw_host::elliptic_params(energies, n_e, n_v, n_c, P.delta_rel > 0 ? P.delta_rel : 1e-7,
                                            P.max_nodes > 0 ? P.max_nodes : 1025, &spec),
                 "elliptic_params");
-    cudaEvent_t ev[10];
-    for (auto& x : ev) ck(cudaEventCreate(&x), "event");
-    struct EvGuard {
-      cudaEvent_t* e;
-      ~EvGuard() {
-        for (int i = 0; i < 10; ++i) cudaEventDestroy(e[i]);
-      }
-    } eg{ev};
-    ck(cudaEventRecord(ev[0], c->stream), "event");
+    for (auto& x : c->ev)
+      if (!x) ck(cudaEventCreate(&x), "event");
+    struct TimingGuard {
+      lrgw_ctx c;
+      ~TimingGuard() { c->timing = false; }
+    } tg{c};
+    c->timing = true;
+    mark(c, 0);
     // stage 1
     std::vector<int32_t> pts = select_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, n_mu, nullptr);
-    ck(cudaEventRecord(ev[1], c->stream), "event");
+    mark(c, 1);
     // stage 2
     DBuf theta = dalloc(c, (size_t)n_r * n_mu);
-    fit_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, pts.data(), n_mu, theta.d(), n_r, ev[8], ev[9]);
-    ck(cudaEventRecord(ev[2], c->stream), "event");
+    fit_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, pts.data(), n_mu, theta.d(), n_r);
+    mark(c, 4);
     // stage 3
     DBuf dpts = upload_i(c, pts.data(), n_mu);
     DBuf pv = dalloc(c, (size_t)n_mu * n_v), pc = dalloc(c, (size_t)n_mu * n_c);
@@ -1120,27 +1127,21 @@ int lrgw_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, lo
                   });
       if (!conv) fail(LRGW_ERR_CONTOUR_CONVERGENCE, "coupled_coefficients_contour: did not reach delta_rel within max_nodes");
     }
-    ck(cudaEventRecord(ev[3], c->stream), "event");
+    mark(c, 5);
     // stages 4-5
     DBuf pvp = dalloc(c, (size_t)n_mu * n_mu), k = dalloc(c, (size_t)n_mu * n_mu);
-    pvp_impl(c, P.dims, P.cell, P.zero_kernel, theta.d(), n_r, n_mu, pvp.d(), ev[4]);
-    ck(cudaEventRecord(ev[5], c->stream), "event");
+    pvp_impl(c, P.dims, P.cell, P.zero_kernel, theta.d(), n_r, n_mu, pvp.d());
+    mark(c, 7);
     smw_core(c, t.d(), pvp.d(), n_mu, k.d());
-    ck(cudaEventRecord(ev[6], c->stream), "event");
-    ck(cudaEventSynchronize(ev[6]), "sync");
+    mark(c, 8);
+    ck(cudaEventSynchronize(c->ev[8]), "sync");
     float ms;
-    auto el = [&](int a, int b) {
-      cudaEventElapsedTime(&ms, ev[a], ev[b]);
-      return (double)ms;
-    };
-    c->stage_ms[LRGW_STAGE_SELECT] = el(0, 1);
-    c->stage_ms[LRGW_STAGE_FIT] = el(1, 2);
-    c->stage_ms[LRGW_STAGE_FIT_SOLVE] = el(8, 9);
-    c->stage_ms[LRGW_STAGE_CONTOUR] = el(2, 3);
-    c->stage_ms[LRGW_STAGE_FFT] = el(3, 4);
-    c->stage_ms[LRGW_STAGE_PVP] = el(4, 5);
-    c->stage_ms[LRGW_STAGE_SMW] = el(5, 6);
-    c->stage_ms[LRGW_STAGE_TOTAL] = el(0, 6);
+    for (int i = 0; i < 8; ++i) {
+      cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]);
+      c->stage_ms[i] = ms;
+    }
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[8]);
+    c->stage_ms[LRGW_STAGE_TOTAL] = ms;
     auto* e = new lrgw_eps_s;
     e->ctx = c;
     e->n_r = n_r;
@@ -1168,7 +1169,7 @@ int lrgw_dev_select(lrgw_ctx c, const double* a, long long lda, int n1, const do
 int lrgw_dev_fit(lrgw_ctx c, const double* a, long long lda, int n1, const double* b, long long ldb, int n2, int n_r,
                  const int32_t* pts_host, int n_mu, double* theta, long long ldt) {
   return guarded(c, [&] {
-    fit_impl(c, a, lda, n1, b, ldb, n2, n_r, pts_host, n_mu, theta, ldt, nullptr, nullptr);
+    fit_impl(c, a, lda, n1, b, ldb, n2, n_r, pts_host, n_mu, theta, ldt);
     ck(cudaStreamSynchronize(c->stream), "sync");
   });
 }
@@ -1218,7 +1219,7 @@ int lrgw_dev_pvp(lrgw_ctx c, const int* dims, const double* cell, int zero, cons
                  int n_mu, double* pvp) {
   return guarded(c, [&] {
     check_grid(dims, cell);
-    pvp_impl(c, dims, cell, zero, theta, ldt, n_mu, pvp, nullptr);
+    pvp_impl(c, dims, cell, zero, theta, ldt, n_mu, pvp);
     ck(cudaStreamSynchronize(c->stream), "sync");
   });
 }

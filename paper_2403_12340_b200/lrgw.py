@@ -93,6 +93,9 @@ def _check(rc, ctx_handle=None, what=""):
 # ---------------------------------------------------------------------------
 
 
+STAGES = ["select", "fit_lhs", "fit_solve", "fit_gemm", "contour", "fft", "pvp", "smw", "total"]
+
+
 class Context:
     """One lrgw_ctx (stream, cuSOLVER handle, cuFFT plan cache) on one device."""
 
@@ -117,9 +120,9 @@ class Context:
             pass
 
     def stage_ms(self):
-        out = np.zeros(8)
-        self._lib.lrgw_ctx_stage_ms(self.handle, out.ctypes.data_as(L.c_double_p), 8)
-        names = ["select", "fit", "fit_solve", "contour", "fft", "pvp", "smw", "total"]
+        out = np.zeros(len(STAGES))
+        self._lib.lrgw_ctx_stage_ms(self.handle, out.ctypes.data_as(L.c_double_p), len(STAGES))
+        names = STAGES
         return dict(zip(names, out.tolist()))
 
     def kernel_launches(self) -> int:
