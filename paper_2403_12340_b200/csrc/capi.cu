@@ -70,7 +70,7 @@ struct lrgw_ctx_s {
   cudaEvent_t ev[LRGW_NUM_STAGES + 1] = {};
   bool timing = false;  // record stage events (lrgw_build only)
   long long launches0 = 0;
-  int select_batch = 64;
+  int select_batch = 128;
 };
 
 struct lrgw_eps_s {
@@ -444,53 +444,102 @@ void smw_core(lrgw_ctx c, const double* t, const double* pvp, int n, double* k) 
 // ---------------------------------------------------------------------------
 // Stage 1: ISDF point selection (isdf.hpp:95-112) — see select.cu.
 // ---------------------------------------------------------------------------
+// Host mirror of select.cu's candidate entry (d, position, grid row).
+struct HostEnt {
+  double v;
+  int pos, row;
+};
+
 std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int n1, const double* b,
                                  long long ldb, int n2, int n_r, int n_mu, double* min_margin) {
   if (n_mu > n_r) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: N_mu > N_r");
   if (n_mu < 1) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: N_mu < 1");
   if (n1 < 1 || n2 < 1) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: empty orbital set");
+  if (select_ent_bytes() != sizeof(HostEnt)) fail(LRGW_ERR_INTERNAL, "select: entry layout mismatch");
   const long long m = (long long)n1 * n2;
   const int kmax = (int)std::min<long long>(m, n_r);
   const int steps = std::min(n_mu, kmax);
   const int s = std::max(1, std::min({c->select_batch, select_max_candidates(), n_r}));
-  const int grid_blocks = select_grid_blocks(c->sm_count);
 
   DBuf d = dalloc(c, n_r), pos = ialloc(c, n_r), perm = ialloc(c, n_r);
   DBuf L = dalloc(c, (size_t)n_r * std::max(steps, 1));
-  DBuf W = dalloc(c, (size_t)n_r * s);
+  DBuf Wbuf[2] = {dalloc(c, (size_t)n_r * s), dalloc(c, (size_t)n_r * s)};
   DBuf amu = dalloc(c, (size_t)s * n1), bmu = dalloc(c, (size_t)s * n2);
-  DBuf lc = dalloc(c, (size_t)s * std::max(steps, 1));
-  const size_t tk = select_topk_tmp_elems(n_r, s);
-  DBuf tv = dalloc(c, tk), tpp = ialloc(c, tk), tg = ialloc(c, tk);
-  DBuf cand = ialloc(c, s), ncand = ialloc(c, 1);
-  DBuf part(c, select_part_bytes(grid_blocks));
+  DBuf lcg = dalloc(c, (size_t)s * std::max(steps, 1));
+  DBuf top(c, (size_t)(s + 1) * sizeof(HostEnt)), top2(c, (size_t)(s + 1) * sizeof(HostEnt));
+  DBuf tmp(c, select_topk_tmp_bytes(n_r, s + 1));
+  DBuf cand = ialloc(c, s), oldc = ialloc(c, s);
+  DBuf lcand = dalloc(c, (size_t)s * s), mprime = dalloc(c, (size_t)s * s);
   DBuf order = ialloc(c, std::max(steps, 1)), margin = dalloc(c, std::max(steps, 1));
-  DBuf kout = ialloc(c, 1);
-  Work w = make_work(c, (size_t)8 * s * 1024);
+  DBuf bout = ialloc(c, 1);
 
-  ck(select_init(c->stream, a, lda, n1, b, ldb, n2, n_r, d.d(), pos.i()), "select_init");
-  int k = 0;
+  ck(select_init(c->stream, a, lda, n1, b, ldb, n2, n_r, d.d(), pos.i(), perm.i()), "select_init");
+  // Candidate columns carried between blocks: a still-unaccepted candidate's
+  // W column only needs the previous block's b new L columns subtracted.
+  std::vector<int> col_of(n_r, -1);  // grid row -> column of the previous W
+  std::vector<int> prev_rows;
+  std::vector<HostEnt> htop(s + 1), htop2(s + 1);
+  std::vector<int> hcand(s), hold(s);
+  int k = 0, k_prev = 0, b_prev = 0, cur = 0;
   while (k < steps) {
-    const int sc = std::min(s, n_r - k);
-    ck(select_topk(c->stream, d.d(), pos.i(), n_r, k, sc, tv.d(), tpp.i(), tg.i(), cand.i(), ncand.i()),
-       "select_topk");
-    ck(gather_rows(c->stream, a, lda, n1, cand.i(), sc, amu.d(), sc), "gather");
-    ck(gather_rows(c->stream, b, ldb, n2, cand.i(), sc, bmu.d(), sc), "gather");
-    ck(hadamard_gemm(c->stream, n_r, sc, a, lda, amu.d(), sc, n1, b, ldb, bmu.d(), sc, n2, W.d(), n_r, 1.0, 0.0),
-       "hadamard_gemm");
-    if (k > 0) {
-      ck(gather_rows(c->stream, L.d(), n_r, k, cand.i(), sc, lc.d(), sc), "gather");
-      gemm(c, n_r, sc, k, L.d(), n_r, Lay::MN, lc.d(), sc, Lay::MN, W.d(), n_r, -1.0, 1.0);
+    const int se = std::min(s, n_r - k);
+    ck(select_topk(c->stream, d.d(), pos.i(), n_r, k, se + 1, tmp.p, top.p), "select_topk");
+    download(c, htop.data(), top.p, sizeof(HostEnt) * (se + 1));
+    // reorder: reused candidates first (their previous columns), new ones after
+    int n_re = 0;
+    for (int i = 0; i < se; ++i)
+      if (htop[i].row >= 0 && col_of[htop[i].row] >= 0) {
+        hold[n_re] = col_of[htop[i].row];
+        htop2[n_re++] = htop[i];
+      }
+    int n_new = 0;
+    for (int i = 0; i < se; ++i)
+      if (!(htop[i].row >= 0 && col_of[htop[i].row] >= 0)) htop2[n_re + n_new++] = htop[i];
+    htop2[se] = htop[se];
+    for (int i = 0; i < se; ++i) hcand[i] = htop2[i].row < 0 ? 0 : htop2[i].row;
+    for (int r : prev_rows) col_of[r] = -1;
+    prev_rows.assign(hcand.begin(), hcand.begin() + se);
+    for (int i = 0; i < se; ++i)
+      if (htop2[i].row >= 0) col_of[htop2[i].row] = i;
+    ck(cudaMemcpyAsync(top2.p, htop2.data(), sizeof(HostEnt) * (se + 1), cudaMemcpyHostToDevice, c->stream), "H2D");
+    ck(cudaMemcpyAsync(cand.p, hcand.data(), sizeof(int) * se, cudaMemcpyHostToDevice, c->stream), "H2D");
+    double* Wn = Wbuf[cur].d();
+    double* Wp = Wbuf[1 - cur].d();
+    if (n_re > 0) {
+      ck(cudaMemcpyAsync(oldc.p, hold.data(), sizeof(int) * n_re, cudaMemcpyHostToDevice, c->stream), "H2D");
+      ck(gather_cols(c->stream, Wp, n_r, n_r, oldc.i(), n_re, Wn, n_r), "gather_cols");
+      ck(gather_rows(c->stream, L.d() + (size_t)k_prev * n_r, n_r, b_prev, cand.i(), n_re, lcg.d(), n_re), "gather");
+      gemm(c, n_r, n_re, b_prev, L.d() + (size_t)k_prev * n_r, n_r, Lay::MN, lcg.d(), n_re, Lay::MN, Wn, n_r, -1.0,
+           1.0);
     }
-    ck(select_steps(c->stream, grid_blocks, n_r, steps, k, d.d(), pos.i(), L.d(), W.d(), cand.i(), sc, part.p,
-                    order.i(), margin.d(), kout.i()),
-       "select_steps");
-    int knew = 0;
-    download(c, &knew, kout.p, sizeof(int));
-    if (knew <= k) fail(LRGW_ERR_INTERNAL, "select: no progress (non-finite residuals?)");
-    k = knew;
+    if (n_new > 0) {
+      // W(:, new) = G(:, new) - L[:, :k] L[new, :k]^T
+      double* Wnew = Wn + (size_t)n_re * n_r;
+      const int* cn = cand.i() + n_re;
+      ck(gather_rows(c->stream, a, lda, n1, cn, n_new, amu.d(), n_new), "gather");
+      ck(gather_rows(c->stream, b, ldb, n2, cn, n_new, bmu.d(), n_new), "gather");
+      ck(hadamard_gemm(c->stream, n_r, n_new, a, lda, amu.d(), n_new, n1, b, ldb, bmu.d(), n_new, n2, Wnew, n_r, 1.0,
+                       0.0),
+         "hadamard_gemm");
+      if (k > 0) {
+        ck(gather_rows(c->stream, L.d(), n_r, k, cn, n_new, lcg.d(), n_new), "gather");
+        gemm(c, n_r, n_new, k, L.d(), n_r, Lay::MN, lcg.d(), n_new, Lay::MN, Wnew, n_r, -1.0, 1.0);
+      }
+    }
+    ck(select_cand_greedy(c->stream, n_r, se, steps, k, top2.p, Wn, pos.i(), perm.i(), lcand.d(), mprime.d(),
+                          order.i(), margin.d(), bout.i()),
+       "cand_greedy");
+    int nb = 0;
+    download(c, &nb, bout.p, sizeof(int));
+    if (nb <= 0) fail(LRGW_ERR_INTERNAL, "select: no progress (non-finite residuals?)");
+    // L[:, k:k+nb] = W M'   (M' = E L_sel^-T, s_e x nb)
+    gemm(c, n_r, nb, se, Wn, n_r, Lay::MN, mprime.d(), se, Lay::K, L.d() + (size_t)k * n_r, n_r, 1.0, 0.0);
+    ck(select_downdate(c->stream, L.d(), n_r, k, nb, pos.i(), d.d()), "downdate");
+    k_prev = k;
+    b_prev = nb;
+    k += nb;
+    cur = 1 - cur;
   }
-  ck(select_scatter_perm(c->stream, pos.i(), n_r, perm.i()), "scatter_perm");
   std::vector<int32_t> pts(n_mu);
   download(c, pts.data(), perm.p, sizeof(int) * n_mu);
   std::sort(pts.begin(), pts.end());

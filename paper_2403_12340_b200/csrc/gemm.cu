@@ -16,6 +16,32 @@ template <bool AK, bool BK, int VA, int VB>
 using CfgL = GemmCfg<128, 64, 32, 32, 3, AK, BK, VA, VB>;
 template <bool AK, bool BK, int VA, int VB>
 using CfgS = GemmCfg<64, 64, 32, 32, 4, AK, BK, VA, VB>;
+// Square 128x128 CTA, 16 warps of 32x32, 3 stages (~120 KB smem, 1 CTA/SM):
+// the symmetric (lower-tile) split-K SYRK of Theta^T V Theta.
+template <bool AK, bool BK, int VA, int VB>
+using CfgX = GemmCfg<128, 128, 32, 32, 3, AK, BK, VA, VB>;
+
+// Hadamard pair (two live accumulator sets): 128x64 CTA, 16 warps of 32x16;
+// 128x32 CTA, 8 warps of 32x16 when N would otherwise pad badly.
+template <int V>
+using CfgH = GemmCfg<128, 64, 32, 16, 3, false, false, V, V>;
+template <int V>
+using CfgH32 = GemmCfg<128, 32, 32, 16, 3, false, false, V, V>;
+// Tall-skinny outputs (N not a multiple of 64): 128x32 CTA, 4 warps of 32x32.
+template <bool AK, bool BK, int VA, int VB>
+using CfgN = GemmCfg<128, 32, 32, 32, 4, AK, BK, VA, VB>;
+// Single-column-tile widths 96 / 128 for the tall-skinny GEMMs of the
+// selection (N = new candidates, K = pivots so far): 12 / 16 warps of 32x32.
+template <bool AK, bool BK, int VA, int VB>
+using Cfg96 = GemmCfg<128, 96, 32, 32, 3, AK, BK, VA, VB>;
+
+enum class Tile { S, L, X, N, W96, W128 };
+
+// Column padding of an N-wide output under 64- vs 32-wide tiles.
+bool prefer_narrow(int N) {
+  const int p64 = (N + 63) / 64 * 64, p32 = (N + 31) / 32 * 32;
+  return p32 * 5 < p64 * 4;  // narrow tiles save > 20% padded work
+}
 
 template <class Cfg>
 cudaError_t launch_cfg(cudaStream_t st, const DgemmParams& p, int splits) {
@@ -35,14 +61,49 @@ cudaError_t launch_cfg(cudaStream_t st, const DgemmParams& p, int splits) {
 }
 
 template <bool AK, bool BK>
-cudaError_t launch_layout(cudaStream_t st, const DgemmParams& p, bool big, bool va, bool vb,
+cudaError_t launch_layout(cudaStream_t st, const DgemmParams& p, Tile tile, bool va, bool vb,
                           int splits) {
-  if (big) {
+  if (tile == Tile::L) {
     if (va && vb) return launch_cfg<CfgL<AK, BK, 2, 2>>(st, p, splits);
     return launch_cfg<CfgL<AK, BK, 1, 1>>(st, p, splits);
   }
+  if (tile == Tile::X) {
+    if (va && vb) return launch_cfg<CfgX<AK, BK, 2, 2>>(st, p, splits);
+    return launch_cfg<CfgX<AK, BK, 1, 1>>(st, p, splits);
+  }
+  if (tile == Tile::N) {
+    if (va && vb) return launch_cfg<CfgN<AK, BK, 2, 2>>(st, p, splits);
+    return launch_cfg<CfgN<AK, BK, 1, 1>>(st, p, splits);
+  }
+  if (tile == Tile::W96) {
+    if (va && vb) return launch_cfg<Cfg96<AK, BK, 2, 2>>(st, p, splits);
+    return launch_cfg<Cfg96<AK, BK, 1, 1>>(st, p, splits);
+  }
+  if (tile == Tile::W128) {
+    if (va && vb) return launch_cfg<CfgX<AK, BK, 2, 2>>(st, p, splits);
+    return launch_cfg<CfgX<AK, BK, 1, 1>>(st, p, splits);
+  }
   if (va && vb) return launch_cfg<CfgS<AK, BK, 2, 2>>(st, p, splits);
   return launch_cfg<CfgS<AK, BK, 1, 1>>(st, p, splits);
+}
+
+// Split count that fills whole waves of `slots` resident CTAs: the smallest
+// s (each split >= 16 k-tiles) whose last wave is >= 90% full, else the best.
+int choose_splits(long long tiles, int ktiles, long long slots) {
+  const int smax = std::max(1, std::min(ktiles / 16, 64));
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= smax; ++s) {
+    const long long ctas = tiles * s;
+    const long long waves = (ctas + slots - 1) / slots;
+    const double eff = (double)ctas / (double)(waves * slots);
+    if (ctas >= slots && eff >= 0.9) return s;
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -86,7 +147,24 @@ __global__ void gather_rows_kernel(const double* src, long long lds, int cols, c
   }
 }
 
+__global__ void gather_cols_kernel(const double* src, long long lds, int rows, const int* cols, int n,
+                                   double* dst, long long ldd) {
+  const long long total = (long long)rows * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(idx % rows), c = static_cast<int>(idx / rows);
+    dst[r + c * ldd] = src[r + cols[c] * lds];
+  }
+}
+
 }  // namespace
+
+cudaError_t gather_cols(cudaStream_t st, const double* src, long long lds, int rows, const int* cols, int n,
+                        double* dst, long long ldd) {
+  if (rows <= 0 || n <= 0) return cudaSuccess;
+  gather_cols_kernel<<<1184, 256, 0, st>>>(src, lds, rows, cols, n, dst, ldd); count_launches(1);
+  return cudaGetLastError();
+}
 
 cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long long lda, Lay la,
                   const double* B, long long ldb, Lay lb, double* C, long long ldc, double alpha,
@@ -112,18 +190,40 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
   // along the contiguous axis.
   const bool va = aligned16(A) && lda % 2 == 0 && (ak ? K % 2 == 0 : M % 2 == 0);
   const bool vb = aligned16(B) && ldb % 2 == 0 && (bk ? K % 2 == 0 : N % 2 == 0);
-  bool big = (long long)((M + 127) / 128) * ((N + 63) / 64) >= 2LL * sm_count && !lower;
-  const int BMt = big ? 128 : 64, BNt = 64;
-  long long tiles = lower ? (long long)((M + 63) / 64) * ((M + 63) / 64 + 1) / 2
-                          : (long long)((M + BMt - 1) / BMt) * ((N + BNt - 1) / BNt);
+  if (lower && M != N) return cudaErrorInvalidValue;
+  Tile tile;
+  long long tiles;
+  int occ;
+  if (lower) {
+    tile = Tile::X;
+    const long long t = (M + 127) / 128;
+    tiles = t * (t + 1) / 2;
+    occ = 1;
+  } else if (N > 64 && N <= 128 && (long long)((M + 127) / 128) >= 2LL * sm_count) {
+    // one column tile of width 96 or 128 (A streamed once)
+    tile = N <= 96 ? Tile::W96 : Tile::W128;
+    tiles = (M + 127) / 128;
+    occ = 1;
+  } else if ((long long)((M + 127) / 128) * ((N + 31) / 32) >= 2LL * sm_count && prefer_narrow(N)) {
+    tile = Tile::N;
+    tiles = (long long)((M + 127) / 128) * ((N + 31) / 32);
+    occ = 2;
+  } else if ((long long)((M + 127) / 128) * ((N + 63) / 64) >= 2LL * sm_count) {
+    tile = Tile::L;
+    tiles = (long long)((M + 127) / 128) * ((N + 63) / 64);
+    occ = 2;
+  } else {
+    tile = Tile::S;
+    tiles = (long long)((M + 63) / 64) * ((N + 63) / 64);
+    occ = 2;
+  }
   // split-K when the output tile grid cannot fill the chip and K is long
   int splits = 1;
   const int ktiles = (K + 15) / 16;
-  if (tiles < 2LL * sm_count && ktiles >= 32 && work) {
-    splits = static_cast<int>(std::min<long long>((2LL * sm_count + tiles - 1) / tiles, ktiles / 16));
+  if (tiles < 2LL * sm_count * occ && ktiles >= 32 && work) {
+    splits = choose_splits(tiles, ktiles, (long long)sm_count * occ);
     while (splits > 1 && (size_t)splits * M * N > work_elems) --splits;
   }
-  if (lower && M != N) return cudaErrorInvalidValue;
   if (splits > 1) {
     const int kc = ((ktiles + splits - 1) / splits) * 16;
     splits = (K + kc - 1) / kc;
@@ -132,13 +232,13 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
     p.part_stride = (long long)M * N;
   }
   cudaError_t e;
-  if (!ak && !bk) e = launch_layout<false, false>(st, p, big, va, vb, splits);
-  else if (!ak && bk) e = launch_layout<false, true>(st, p, big, va, vb, splits);
-  else if (ak && !bk) e = launch_layout<true, false>(st, p, big, va, vb, splits);
-  else e = launch_layout<true, true>(st, p, big, va, vb, splits);
+  if (!ak && !bk) e = launch_layout<false, false>(st, p, tile, va, vb, splits);
+  else if (!ak && bk) e = launch_layout<false, true>(st, p, tile, va, vb, splits);
+  else if (ak && !bk) e = launch_layout<true, false>(st, p, tile, va, vb, splits);
+  else e = launch_layout<true, true>(st, p, tile, va, vb, splits);
   if (e != cudaSuccess || splits <= 1) return e;
   splitk_reduce_kernel<<<1184, 256, 0, st>>>(work, splits, (long long)M * N, M, N, C, ldc, beta,
-                                             lower ? 1 : 0, 64); count_launches(1);
+                                             lower ? 1 : 0, 128); count_launches(1);
   return cudaGetLastError();
 }
 
@@ -160,8 +260,9 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
     hadamard_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(p); count_launches(1);
     return cudaGetLastError();
   };
-  if (vec) return go(CfgL<false, false, 2, 2>{});
-  return go(CfgL<false, false, 1, 1>{});
+  if (prefer_narrow(N)) return vec ? go(CfgH32<2>{}) : go(CfgH32<1>{});
+  if (vec) return go(CfgH<2>{});
+  return go(CfgH<1>{});
 }
 
 cudaError_t mirror_lower(cudaStream_t st, double* a, int n, long long lda, bool average) {

@@ -40,8 +40,7 @@ struct TileLoader {
   static constexpr int PITCH = KMAJOR ? (BK + 4) : (ROWS + 4);   // doubles
   static constexpr int ELEMS = KMAJOR ? ROWS * PITCH : BK * PITCH;
   static constexpr int CHUNKS = ROWS * BK / VEC;
-  static_assert(CHUNKS % THREADS == 0, "tile chunks must divide threads");
-  static constexpr int PER_THREAD = CHUNKS / THREADS;
+  static constexpr int PER_THREAD = (CHUNKS + THREADS - 1) / THREADS;
 
   // row0: first logical row of the tile; k0: first k; rows/kend: bounds.
   __device__ __forceinline__ static void load(double* s, const double* g, long long ld, int row0,
@@ -49,6 +48,7 @@ struct TileLoader {
 #pragma unroll
     for (int i = 0; i < PER_THREAD; ++i) {
       const int c = tid + i * THREADS;
+      if (CHUNKS % THREADS != 0 && c >= CHUNKS) break;
       int r, k;
       if (KMAJOR) {
         r = c / (BK / VEC);

@@ -34,6 +34,10 @@ cudaError_t mirror_lower(cudaStream_t st, double* a, int n, long long lda, bool 
 cudaError_t gather_rows(cudaStream_t st, const double* src, long long lds, int cols, const int* rows,
                         int n_rows, double* dst, long long ldd);
 
+// dst(:, c) = src(:, cols[c]), cols on device.
+cudaError_t gather_cols(cudaStream_t st, const double* src, long long lds, int rows, const int* cols, int n,
+                        double* dst, long long ldd);
+
 // K3 quadrature (quadrature.cu).
 int quad_partial_groups(int n_mu, int n_nodes, int sm_count);
 cudaError_t quad_nodes(cudaStream_t st, int n_mu, int n_v, int n_c, const double* pv, long long ldv,

@@ -3,63 +3,48 @@
 // Reference: select_interpolation_points (isdf.hpp:95-112) -> Householder QRCP
 // on the materialised pair matrix Z (linalg.hpp:26-111, guard 2^26 entries).
 // B200 design: matrix-free greedy pivoted Cholesky on the Hadamard Gram
-// G = (Phi_a Phi_a^T) o (Phi_b Phi_b^T) = Z^T Z, whose residual diagonal equals
-// QRCP's residual column norms, so the greedy pivots coincide. The pivot rule
-// is mirrored exactly: argmax over remaining positions with strict '>' (ties
-// to the lowest current position, positions following the perm swap of
-// linalg.hpp:48-53), min(N1 N2, N_r) steps, first N_mu sorted ascending.
+// G = (Phi_a Phi_a^T) o (Phi_b Phi_b^T) = Z^T Z, whose residual diagonal d
+// equals QRCP's residual column norms, so the greedy pivots coincide. The
+// pivot rule is mirrored exactly: argmax over remaining positions with strict
+// '>' (ties to the lowest current position; positions follow the
+// perm[step] <-> perm[p] swap of linalg.hpp:48-53), min(N1 N2, N_r) steps, the
+// first N_mu positions sorted ascending.
 //
-// Speculative candidate batching: each block takes the top-s
-// residuals as candidates, forms their kernel columns for all rows in one
-// GEMM pass, W = G(:, cand) - L[:, :k0] L[cand, :k0]^T (DMMA), then a single
-// cooperative kernel resolves exact greedy steps while the argmax stays inside
-// the candidate set: per step one grid barrier, the new L column
-// L[:, k] = (W[:, c_p] - L[:, kb:k] L[p, kb:k]^T) / sqrt(d_p), the residual
-// downdate d -= L[:, k]^2 and a warp-shuffle (value, position) argmax. The
-// pivot sequence is identical to the unbatched greedy; only the number of
-// passes over Phi and L shrinks.
-#include <cooperative_groups.h>
-
+// Certified candidate blocks (no grid-wide barrier per pivot):
+//   1. C = the top-s unselected rows by (d desc, position asc), tau = the
+//      (s+1)-th residual. Residuals only decrease, so every non-candidate
+//      stays <= tau for the whole block.
+//   2. W = G(:, C) - L[:, :k0] L[C, :k0]^T for all rows (two DMMA GEMM passes).
+//   3. One CTA runs the exact greedy on the s x s candidate Schur complement
+//      W[C, C] in shared memory; a step is accepted only while the best
+//      candidate beats tau strictly (the first step of a block is the exact
+//      argmax by construction of C), so every accepted pivot is the global
+//      greedy pivot.
+//   4. The block's L columns for all rows follow from one GEMM,
+//      L[:, k0:k0+b] = W L_sel^-T, and d -= rowsum(L_blk^2).
+// Block lengths are ~60-80% of s; the pivot sequence is that of the plain
+// greedy (the tests check it bit-exactly against the reference).
 #include <cfloat>
 
 #include "common.cuh"
 #include "kernels.h"
 #include "select.h"
 
-namespace cg = cooperative_groups;
-
 namespace lrgw_dev {
 
 namespace {
 
-// (value, position, grid index) ordering: larger value first, then the lower
-// position (the reference's strict '>' scan in position order).
-struct Cand {
-  double v;
-  int pos;
-  int g;
-};
-
+// (value, position) ordering: larger value first, then the lower position
+// (the reference's strict '>' scan in position order, linalg.hpp:45-47).
 __device__ __forceinline__ bool better(double v1, int p1, double v2, int p2) {
   return v1 > v2 || (v1 == v2 && p1 < p2);
 }
 
-__device__ __forceinline__ void warp_argmax(double& v, int& pos, int& g) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const double v2 = __shfl_down_sync(0xffffffffu, v, off);
-    const int p2 = __shfl_down_sync(0xffffffffu, pos, off);
-    const int g2 = __shfl_down_sync(0xffffffffu, g, off);
-    if (better(v2, p2, v, pos)) {
-      v = v2;
-      pos = p2;
-      g = g2;
-    }
-  }
-}
+// l of the pivot itself: sqrt(d_piv) = 1 / inv (0 for an exhausted pivot).
+__device__ __forceinline__ double s_bv_sqrt(double inv) { return inv > 0.0 ? 1.0 / inv : 0.0; }
 
 __global__ void init_diag_kernel(const double* a, long long lda, int n1, const double* b,
-                                 long long ldb, int n2, int n_r, double* d, int* pos) {
+                                 long long ldb, int n2, int n_r, double* d, int* pos, int* perm) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_r; r += gridDim.x * blockDim.x) {
     double sa = 0.0, sb = 0.0;
     for (int i = 0; i < n1; ++i) {
@@ -72,31 +57,32 @@ __global__ void init_diag_kernel(const double* a, long long lda, int n1, const d
     }
     d[r] = sa * sb;
     pos[r] = r;
+    perm[r] = r;
   }
 }
 
-// ---- top-s candidates: per-CTA bitonic sort of (d, pos) then a merge pass --
-constexpr int TOPK_CHUNK = 2048;  // rows per CTA in pass 1 (power of two)
+// ---- top-(s+1) by (d desc, position asc): per-CTA bitonic + merge passes ----
+constexpr int TOPK_CHUNK = 2048;
 
-__device__ void bitonic_desc(double* v, int* p, int* gi, int n) {
+struct Ent {
+  double v;
+  int pos, row;
+};
+
+__device__ __forceinline__ bool ent_better(const Ent& a, const Ent& b) { return better(a.v, a.pos, b.v, b.pos); }
+
+__device__ void bitonic_desc(Ent* e, int n) {
   for (int size = 2; size <= n; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       __syncthreads();
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const int j = i ^ stride;
         if (j > i) {
+          const Ent a = e[i], b = e[j];
           const bool desc = ((i & size) == 0);
-          const bool swap = desc ? better(v[j], p[j], v[i], p[i]) : better(v[i], p[i], v[j], p[j]);
-          if (swap) {
-            double tv = v[i];
-            v[i] = v[j];
-            v[j] = tv;
-            int tp = p[i];
-            p[i] = p[j];
-            p[j] = tp;
-            int tg = gi[i];
-            gi[i] = gi[j];
-            gi[j] = tg;
+          if (desc ? ent_better(b, a) : ent_better(a, b)) {
+            e[i] = b;
+            e[j] = a;
           }
         }
       }
@@ -105,333 +91,319 @@ __device__ void bitonic_desc(double* v, int* p, int* gi, int n) {
   __syncthreads();
 }
 
-__global__ void topk_pass1_kernel(const double* d, const int* pos, int n_r, int k, int s,
-                                  double* out_v, int* out_p, int* out_g) {
-  __shared__ double v[TOPK_CHUNK];
-  __shared__ int p[TOPK_CHUNK], gi[TOPK_CHUNK];
+__device__ __forceinline__ Ent ent_none() { return Ent{-DBL_MAX, INT_MAX, -1}; }
+
+__global__ void topk_pass1_kernel(const double* d, const int* pos, int n_r, int k, int s, Ent* out) {
+  __shared__ Ent e[TOPK_CHUNK];
   const int base = blockIdx.x * TOPK_CHUNK;
   for (int i = threadIdx.x; i < TOPK_CHUNK; i += blockDim.x) {
     const int r = base + i;
-    const bool ok = r < n_r && pos[r] >= k;
-    v[i] = ok ? d[r] : -DBL_MAX;
-    p[i] = ok ? pos[r] : INT_MAX;
-    gi[i] = ok ? r : -1;
+    const int pr = r < n_r ? pos[r] : -1;
+    e[i] = (r < n_r && pr >= k) ? Ent{d[r], pr, r} : ent_none();
   }
-  bitonic_desc(v, p, gi, TOPK_CHUNK);
-  for (int i = threadIdx.x; i < s; i += blockDim.x) {
-    out_v[blockIdx.x * s + i] = v[i];
-    out_p[blockIdx.x * s + i] = p[i];
-    out_g[blockIdx.x * s + i] = gi[i];
-  }
+  bitonic_desc(e, TOPK_CHUNK);
+  for (int i = threadIdx.x; i < s; i += blockDim.x) out[blockIdx.x * s + i] = e[i];
 }
 
-// Merge pass: each CTA sorts TOPK_CHUNK candidates of the previous pass and
-// keeps its top s; the last pass (one CTA) writes the candidate list.
-__global__ void topk_merge_kernel(const double* in_v, const int* in_p, const int* in_g, int n_in,
-                                  int s, double* out_v, int* out_p, int* out_g, int* cand,
-                                  int* n_cand) {
-  __shared__ double v[TOPK_CHUNK];
-  __shared__ int p[TOPK_CHUNK], gi[TOPK_CHUNK];
+__global__ void topk_merge_kernel(const Ent* in, int n_in, int s, Ent* out) {
+  __shared__ Ent e[TOPK_CHUNK];
   const int base = blockIdx.x * TOPK_CHUNK;
   for (int i = threadIdx.x; i < TOPK_CHUNK; i += blockDim.x) {
     const int r = base + i;
-    const bool ok = r < n_in;
-    v[i] = ok ? in_v[r] : -DBL_MAX;
-    p[i] = ok ? in_p[r] : INT_MAX;
-    gi[i] = ok ? in_g[r] : -1;
+    e[i] = r < n_in ? in[r] : ent_none();
   }
-  bitonic_desc(v, p, gi, TOPK_CHUNK);
-  if (cand) {
-    if (threadIdx.x == 0) {
-      int c = 0;
-      for (int i = 0; i < s; ++i) {
-        if (gi[i] < 0) break;
-        cand[c++] = gi[i];
-      }
-      *n_cand = c;
-    }
-    return;
-  }
-  for (int i = threadIdx.x; i < s; i += blockDim.x) {
-    out_v[blockIdx.x * s + i] = v[i];
-    out_p[blockIdx.x * s + i] = p[i];
-    out_g[blockIdx.x * s + i] = gi[i];
+  bitonic_desc(e, TOPK_CHUNK);
+  for (int i = threadIdx.x; i < s; i += blockDim.x) out[blockIdx.x * s + i] = e[i];
+}
+
+// ---- the certified candidate greedy (one CTA) -------------------------------
+constexpr int CG_THREADS = 512;
+constexpr int CG_WARPS = CG_THREADS / 32;
+constexpr int CG_ROWS = 128 / CG_WARPS;  // candidate rows per warp
+
+struct CandParams {
+  int n_r, s, steps, kb;
+  const Ent* top;       // s + 1 entries: candidates then the tau entry
+  const double* W;      // n_r x s
+  int* pos;             // grid row -> position
+  int* perm;            // position -> grid row
+  double* lc;           // s x s: l vectors of the accepted steps (column t)
+  double* mprime;       // s x s: E L_sel^-T (rows of unselected candidates zero)
+  int* piv_order;       // [steps]
+  double* margin;       // [steps]
+  int* b_out;           // number of accepted steps
+};
+
+// Register-resident candidate block: warp w owns candidate rows
+// i = CG_ROWS w + r (r < CG_ROWS) and lane l holds their columns l, l+32, l+64,
+// l+96 (s <= 128); lane r additionally carries row r's residual and position.
+// Per accepted pivot: post per-warp best (lanes 0..CG_ROWS-1), barrier, every
+// warp reduces the CG_WARPS partials redundantly and the owner publishes the
+// pivot row, barrier, every warp applies the rank-1 elimination in registers.
+__device__ __forceinline__ void argmax_xor(double& v, double& sv, int& i, int& p, int off) {
+  const double v2 = __shfl_xor_sync(0xffffffffu, v, off);
+  const double s2 = __shfl_xor_sync(0xffffffffu, sv, off);
+  const int i2 = __shfl_xor_sync(0xffffffffu, i, off);
+  const int p2 = __shfl_xor_sync(0xffffffffu, p, off);
+  if (better(v2, p2, v, p)) {
+    sv = fmax(fmax(sv, s2), v);
+    v = v2;
+    p = p2;
+    i = i2;
+  } else {
+    sv = fmax(fmax(sv, s2), v2);
   }
 }
 
-// ---- the cooperative step kernel ----------------------------------------
-struct Part {
-  double v;
-  int pos, g, occupant;
-};
+__global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p) {
+  extern __shared__ __align__(16) double sm[];
+  const int s = p.s, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double* rowbuf = sm;                             // 128: published pivot row
+  int* usedv = reinterpret_cast<int*>(rowbuf + 128);  // 128 flags
+  int* rowid = usedv + 128;                        // 128 grid rows
+  int* sel = rowid + 128;                          // 128: candidate index per accepted step
+  int* pslot = sel + 128;                          // 128: perm[kb .. kb + s)
+  __shared__ double part_v[CG_WARPS], part_s[CG_WARPS];
+  __shared__ int part_i[CG_WARPS], part_p[CG_WARPS];
+  __shared__ double s_tau;
 
-constexpr int SEL_THREADS = 512;
-constexpr int SEL_MAXS = 128;
-
-struct StepParams {
-  int n_r, steps;
-  int kb;          // block start step (columns of W are for steps >= kb)
-  double* d;
-  int* pos;
-  double* L;       // n_r x n_mu (col-major, ld n_r)
-  const double* W; // n_r x s
-  const int* cand;
-  int n_cand;
-  Part* part;      // [2][gridDim.x]
-  int* piv_order;  // [steps]
-  double* margin;  // [steps] (top-2 relative margin, optional)
-  int* k_out;
-};
-
-__global__ void __launch_bounds__(SEL_THREADS, 1) select_steps_kernel(StepParams p) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ int s_cand[SEL_MAXS];
-  __shared__ double s_lp[SEL_MAXS];
-  __shared__ double red_v[SEL_THREADS / 32];
-  __shared__ int red_p[SEL_THREADS / 32], red_g[SEL_THREADS / 32], red_o[SEL_THREADS / 32];
-  __shared__ double s_second[SEL_THREADS / 32];
-  __shared__ int s_dec[4];  // p, c_p, pos_p, occupant
-  __shared__ double s_dp;
-
-  const int nb = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
-  const int r0 = (int)((long long)p.n_r * b / nb), r1 = (int)((long long)p.n_r * (b + 1) / nb);
-  for (int i = tid; i < p.n_cand; i += blockDim.x) s_cand[i] = p.cand[i];
+  for (int i = tid; i < 128; i += blockDim.x) {
+    const Ent e = i < s ? p.top[i] : ent_none();
+    rowid[i] = e.row;
+    usedv[i] = e.row < 0 ? 1 : 0;
+    pslot[i] = (i < s && p.kb + i < p.n_r) ? p.perm[p.kb + i] : -1;
+  }
+  if (tid == 0) s_tau = p.top[s].row >= 0 ? p.top[s].v : -DBL_MAX;
   __syncthreads();
+  const double tau = s_tau;
+  const int tmax = min(s, p.steps - p.kb);
 
-  int k = p.kb;
-  int piv = -1, cpiv = -1;  // pending pivot (grid index, candidate column)
-  double dpiv = 0.0;
-  for (int iter = 0;; ++iter) {
-    // ---- phase 1: apply the pending pivot, local argmax ----
-    if (piv >= 0) {
-      const int nt = k - p.kb;  // previous in-block columns
-      for (int t = tid; t < nt; t += blockDim.x)
-        s_lp[t] = p.L[piv + (long long)(p.kb + t) * p.n_r];
-      __syncthreads();
-      const double inv = dpiv > 0.0 ? 1.0 / sqrt(dpiv) : 0.0;
-      double* Lk = p.L + (long long)k * p.n_r;
-      const double* Wc = p.W + (long long)cpiv * p.n_r;
-      for (int r = r0 + tid; r < r1; r += blockDim.x) {
-        const int pr = p.pos[r];
-        if (pr < k) {  // already a pivot: L is zero there (lower triangular)
-          Lk[r] = 0.0;
-          continue;
-        }
-        if (r == piv) {
-          Lk[r] = dpiv > 0.0 ? sqrt(dpiv) : 0.0;
-          continue;
-        }
-        double c = Wc[r];
-        for (int t = 0; t < nt; ++t) c = fma(-p.L[r + (long long)(p.kb + t) * p.n_r], s_lp[t], c);
-        const double l = dpiv > 0.0 ? c * inv : 0.0;
-        Lk[r] = l;
-        p.d[r] = fma(-l, l, p.d[r]);
-      }
-      ++k;
-      __syncthreads();
-    }
-    // local argmax over rows with pos >= k; also find the occupant of position k
-    double bv = -DBL_MAX, sv = -DBL_MAX;
-    int bp = INT_MAX, bg = -1, occ = -1;
-    for (int r = r0 + tid; r < r1; r += blockDim.x) {
-      const int pr = p.pos[r];
-      if (pr == k) occ = r;
-      if (pr < k) continue;
-      const double v = p.d[r];
-      if (better(v, pr, bv, bp)) {
-        sv = fmax(sv, bv);
-        bv = v;
-        bp = pr;
-        bg = r;
-      } else {
-        sv = fmax(sv, v);
-      }
-    }
-    {
-      // second-best: track by max of non-winners (for margin logging only)
-      double v = bv;
-      int pp = bp, gg = bg;
-      double s2 = sv;
+  const int base = CG_ROWS * wid;
+  double w[CG_ROWS][4];
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const double v2 = __shfl_down_sync(0xffffffffu, v, off);
-        const int p2 = __shfl_down_sync(0xffffffffu, pp, off);
-        const int g2 = __shfl_down_sync(0xffffffffu, gg, off);
-        const double s22 = __shfl_down_sync(0xffffffffu, s2, off);
-        const int o2 = __shfl_down_sync(0xffffffffu, occ, off);
-        if (better(v2, p2, v, pp)) {
-          s2 = fmax(fmax(s2, s22), v);
-          v = v2;
-          pp = p2;
-          gg = g2;
-        } else {
-          s2 = fmax(fmax(s2, s22), v2);
-        }
-        occ = max(occ, o2);
+  for (int r = 0; r < CG_ROWS; ++r) {
+    const int g = rowid[base + r];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = lane + 32 * c;
+      w[r][c] = (g >= 0 && j < s) ? p.W[g + (long long)j * p.n_r] : 0.0;
+    }
+  }
+  // lane r < CG_ROWS: metadata of row base + r
+  const int my_i = base + (lane < CG_ROWS ? lane : 0);
+  double my_d = -DBL_MAX;
+  int my_pos = INT_MAX;
+  if (lane < CG_ROWS && my_i < s && rowid[my_i] >= 0) {
+    my_d = p.top[my_i].v;
+    my_pos = p.top[my_i].pos;
+  }
+
+  int t = 0;
+  for (;; ++t) {
+    // ---- post this warp's best unused row ----
+    double bv = -DBL_MAX, sv = -DBL_MAX;
+    int bi = -1, bp = INT_MAX;
+    if (lane < CG_ROWS && !usedv[my_i]) {
+      bv = my_d;
+      bp = my_pos;
+      bi = my_i;
+    }
+#pragma unroll
+    for (int off = CG_ROWS / 2; off > 0; off >>= 1) argmax_xor(bv, sv, bi, bp, off);
+    if (lane == 0) {
+      part_v[wid] = bv;
+      part_s[wid] = sv;
+      part_i[wid] = bi;
+      part_p[wid] = bp;
+    }
+    __syncthreads();
+    // ---- every warp reduces the partials ----
+    double v0 = -DBL_MAX, s0 = -DBL_MAX;
+    int i0 = -1, p0 = INT_MAX;
+    if (lane < CG_WARPS) {
+      v0 = part_v[lane];
+      s0 = part_s[lane];
+      i0 = part_i[lane];
+      p0 = part_p[lane];
+    }
+#pragma unroll
+    for (int off = CG_WARPS / 2; off > 0; off >>= 1) argmax_xor(v0, s0, i0, p0, off);
+    v0 = __shfl_sync(0xffffffffu, v0, 0);
+    s0 = __shfl_sync(0xffffffffu, s0, 0);
+    i0 = __shfl_sync(0xffffffffu, i0, 0);
+    p0 = __shfl_sync(0xffffffffu, p0, 0);
+    // certified iff it beats every non-candidate (<= tau); the first step of
+    // the block is the exact argmax (C is sorted by the pivot rule)
+    const bool ok = t < tmax && i0 >= 0 && (t == 0 || v0 > tau);
+    if (!ok) break;  // uniform across the CTA
+    const int k = p.kb + t;
+    const int ppos = p0;       // pivot's position before the swap
+    const int occ = pslot[t];  // perm[k] before the swap (linalg.hpp:48-53)
+    if (wid == i0 / CG_ROWS) {
+      const int r0 = i0 % CG_ROWS;
+#pragma unroll
+      for (int r = 0; r < CG_ROWS; ++r)
+        if (r == r0)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) rowbuf[lane + 32 * c] = w[r][c];
+    }
+    __syncthreads();
+    // ---- eliminate the pivot from the register block ----
+    const double inv = v0 > 0.0 ? 1.0 / sqrt(v0) : 0.0;
+    const double lpiv = v0 > 0.0 ? sqrt(v0) : 0.0;
+    double lj[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = lane + 32 * c;
+      lj[c] = (j == i0) ? lpiv : rowbuf[j] * inv;
+    }
+    double my_l = 0.0;
+#pragma unroll
+    for (int r = 0; r < CG_ROWS; ++r) {
+      const int i = base + r;
+      const double li = (i == i0) ? lpiv : (usedv[i] ? 0.0 : rowbuf[i] * inv);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) w[r][c] = fma(-li, lj[c], w[r][c]);
+      if (lane == r) my_l = li;
+    }
+    if (lane < CG_ROWS && my_i < s) {
+      p.lc[my_i + (size_t)t * s] = my_l;
+      if (my_i == i0) {
+        usedv[my_i] = 1;
+        my_pos = k;
+      } else {
+        if (!usedv[my_i]) my_d = fma(-my_l, my_l, my_d);
+        if (rowid[my_i] == occ) my_pos = ppos;
       }
-      const int w = tid >> 5;
-      if ((tid & 31) == 0) {
-        red_v[w] = v;
-        red_p[w] = pp;
-        red_g[w] = gg;
-        red_o[w] = occ;
-        s_second[w] = s2;
+    }
+    if (tid == 0) {
+      const int gp = rowid[i0];
+      p.perm[k] = gp;
+      p.perm[ppos] = occ;
+      p.pos[gp] = k;
+      p.pos[occ] = ppos;
+      if (ppos - p.kb < s) pslot[ppos - p.kb] = occ;
+      pslot[t] = gp;
+      sel[t] = i0;
+      p.piv_order[k] = gp;
+      if (p.margin) p.margin[k] = v0 > 0.0 ? (v0 - fmax(s0, tau)) / v0 : 0.0;
+    }
+    // usedv / pslot / sel are next read after the next step's first barrier
+  }
+  __syncthreads();
+  const int b = t;
+  // M' = E L_sel^-T. L_sel[t1][t2] = lc[sel[t1] + t2 s] is lower triangular in
+  // pivot order: pack it into shared memory and invert row by row
+  // (X[i][:] = (e_i - sum_{m<i} L[i][m] X[m][:]) / L[i][i], columns in parallel).
+  double* lp = reinterpret_cast<double*>(pslot + 128);  // b (b + 1) / 2, packed lower
+  double* xp = lp + (size_t)b * (b + 1) / 2;              // b (b + 1) / 2
+  for (int idx = tid; idx < b * b; idx += blockDim.x) {
+    const int i = idx / b, m = idx % b;
+    if (m <= i) lp[(size_t)i * (i + 1) / 2 + m] = p.lc[sel[i] + (size_t)m * s];
+  }
+  for (int idx = tid; idx < s * b; idx += blockDim.x) p.mprime[idx] = 0.0;
+  __syncthreads();
+  {
+    // G = CG_THREADS / 128 threads per column j (128 >= s columns), m-sum
+    // split across them and reduced with shuffles inside the group.
+    constexpr int G = CG_THREADS / 128;
+    const int j = tid / G, q = tid % G;
+    for (int i = 0; i < b; ++i) {
+      const double* li = lp + (size_t)i * (i + 1) / 2;
+      double acc = 0.0;
+      if (j <= i)
+        for (int m = j + q; m < i; m += G) acc = fma(li[m], xp[(size_t)m * (m + 1) / 2 + j], acc);
+#pragma unroll
+      for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (j <= i && q == 0) {
+        const double lii = li[i];
+        const double x = lii != 0.0 ? (((i == j) ? 1.0 : 0.0) - acc) / lii : 0.0;
+        xp[(size_t)i * (i + 1) / 2 + j] = x;
+        p.mprime[sel[j] + (size_t)i * s] = x;  // (L_sel^-T)[j][i] = X[i][j]
       }
       __syncthreads();
-      if (tid == 0) {
-        double v0 = red_v[0], s0 = s_second[0];
-        int p0 = red_p[0], g0 = red_g[0], o0 = red_o[0];
-        for (int i = 1; i < SEL_THREADS / 32; ++i) {
-          if (better(red_v[i], red_p[i], v0, p0)) {
-            s0 = fmax(fmax(s0, s_second[i]), v0);
-            v0 = red_v[i];
-            p0 = red_p[i];
-            g0 = red_g[i];
-          } else {
-            s0 = fmax(fmax(s0, s_second[i]), red_v[i]);
-          }
-          o0 = max(o0, red_o[i]);
-        }
-        Part* out = p.part + (iter & 1) * nb + b;
-        out->v = v0;
-        out->pos = p0;
-        out->g = g0;
-        out->occupant = o0;
-        // stash the CTA-local second best in the spare slot of the other buffer
-        reinterpret_cast<double*>(p.part + 2 * nb)[(iter & 1) * nb + b] = s0;
-      }
     }
-    grid.sync();
-    // ---- phase 2: global decision (identical in every CTA) ----
-    if (tid == 0) {
-      const Part* in = p.part + (iter & 1) * nb;
-      const double* sec = reinterpret_cast<const double*>(p.part + 2 * nb) + (iter & 1) * nb;
-      double v0 = in[0].v, s0 = sec[0];
-      int p0 = in[0].pos, g0 = in[0].g, o0 = in[0].occupant;
-      for (int i = 1; i < nb; ++i) {
-        if (better(in[i].v, in[i].pos, v0, p0)) {
-          s0 = fmax(fmax(s0, sec[i]), v0);
-          v0 = in[i].v;
-          p0 = in[i].pos;
-          g0 = in[i].g;
-        } else {
-          s0 = fmax(fmax(s0, sec[i]), in[i].v);
-        }
-        o0 = max(o0, in[i].occupant);
-      }
-      int c = -1;
-      if (k < p.steps && g0 >= 0)
-        for (int i = 0; i < p.n_cand; ++i)
-          if (s_cand[i] == g0) {
-            c = i;
-            break;
-          }
-      s_dec[0] = g0;
-      s_dec[1] = c;
-      s_dec[2] = p0;
-      s_dec[3] = o0;
-      s_dp = v0;
-      if (b == 0 && c >= 0) {
-        p.piv_order[k] = g0;
-        if (p.margin) p.margin[k] = v0 > 0.0 ? (v0 - s0) / v0 : 0.0;
-      }
-    }
-    __syncthreads();
-    if (s_dec[1] < 0) break;  // miss (or done): block ends; state is consistent
-    piv = s_dec[0];
-    cpiv = s_dec[1];
-    dpiv = s_dp;
-    // mirrored swap: pivot -> position k, previous occupant -> pivot's position
-    const int occupant = s_dec[3], pos_p = s_dec[2];
-    if (tid == 0) {
-      if (piv >= r0 && piv < r1) p.pos[piv] = k;
-      if (occupant >= r0 && occupant < r1 && occupant != piv) p.pos[occupant] = pos_p;
-    }
-    __syncthreads();
   }
-  if (b == 0 && tid == 0) *p.k_out = k;
+  if (tid == 0) *p.b_out = b;
 }
 
-__global__ void scatter_perm_kernel(const int* pos, int n_r, int* perm) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_r; r += gridDim.x * blockDim.x)
-    perm[pos[r]] = r;
+__global__ void cand_rows_kernel(const Ent* top, int n, int* rows) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) rows[i] = top[i].row < 0 ? 0 : top[i].row;
+}
+
+// d[r] -= sum_t L[r, kb + t]^2 for the rows still unselected.
+__global__ void downdate_kernel(const double* L, int n_r, int kb, int b, const int* pos, double* d) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_r; r += gridDim.x * blockDim.x) {
+    if (pos[r] < kb + b) continue;
+    double v = d[r];
+    const double* lr = L + (long long)kb * n_r + r;
+    for (int t = 0; t < b; ++t) {
+      const double l = lr[(long long)t * n_r];
+      v = fma(-l, l, v);
+    }
+    d[r] = v;
+  }
 }
 
 }  // namespace
 
+size_t select_topk_tmp_bytes(int n_r, int s1) {
+  return 2 * (size_t)((n_r + TOPK_CHUNK - 1) / TOPK_CHUNK) * s1 * sizeof(Ent) + 64;
+}
+
+size_t select_ent_bytes() { return sizeof(Ent); }
+
 cudaError_t select_init(cudaStream_t st, const double* a, long long lda, int n1, const double* b,
-                        long long ldb, int n2, int n_r, double* d, int* pos) {
-  init_diag_kernel<<<592, 256, 0, st>>>(a, lda, n1, b, ldb, n2, n_r, d, pos); count_launches(1);
+                        long long ldb, int n2, int n_r, double* d, int* pos, int* perm) {
+  init_diag_kernel<<<592, 256, 0, st>>>(a, lda, n1, b, ldb, n2, n_r, d, pos, perm); count_launches(1);
   return cudaGetLastError();
 }
 
-cudaError_t select_topk(cudaStream_t st, const double* d, const int* pos, int n_r, int k, int s,
-                        double* tmp_v, int* tmp_p, int* tmp_g, int* cand, int* n_cand) {
-  // tmp arrays hold two ping-pong halves of select_topk_tmp_elems(n_r, s) / 2
-  int n = (n_r + TOPK_CHUNK - 1) / TOPK_CHUNK;
-  const size_t half = (size_t)n * s;
-  topk_pass1_kernel<<<n, 1024, 0, st>>>(d, pos, n_r, k, s, tmp_v, tmp_p, tmp_g); count_launches(1);
+cudaError_t select_topk(cudaStream_t st, const double* d, const int* pos, int n_r, int k, int s1, void* tmp,
+                        void* out) {
+  Ent* t = static_cast<Ent*>(tmp);
+  const int n = (n_r + TOPK_CHUNK - 1) / TOPK_CHUNK;
+  const size_t half = (size_t)n * s1;
+  topk_pass1_kernel<<<n, 1024, 0, st>>>(d, pos, n_r, k, s1, t); count_launches(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  int n_in = n * s, src = 0;
+  int n_in = n * s1, src = 0;
   while (true) {
     const int chunks = (n_in + TOPK_CHUNK - 1) / TOPK_CHUNK;
-    const size_t so = src * half, dst = (1 - src) * half;
-    if (chunks == 1) {
-      topk_merge_kernel<<<1, 1024, 0, st>>>(tmp_v + so, tmp_p + so, tmp_g + so, n_in, s, nullptr,
-                                            nullptr, nullptr, cand, n_cand); count_launches(1);
-      return cudaGetLastError();
-    }
-    topk_merge_kernel<<<chunks, 1024, 0, st>>>(tmp_v + so, tmp_p + so, tmp_g + so, n_in, s,
-                                               tmp_v + dst, tmp_p + dst, tmp_g + dst, nullptr,
-                                               nullptr); count_launches(1);
+    Ent* from = t + src * half;
+    Ent* to = chunks == 1 ? static_cast<Ent*>(out) : t + (1 - src) * half;
+    topk_merge_kernel<<<chunks, 1024, 0, st>>>(from, n_in, s1, to); count_launches(1);
     e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    n_in = chunks * s;
+    if (e != cudaSuccess || chunks == 1) return e;
+    n_in = chunks * s1;
     src = 1 - src;
   }
 }
 
-size_t select_topk_tmp_elems(int n_r, int s) {
-  return 2 * (size_t)((n_r + TOPK_CHUNK - 1) / TOPK_CHUNK) * s;
-}
+size_t select_cand_smem_bytes(int s) { return 128 * 8 + 4 * 128 * 4 + (size_t)s * (s + 1) * 8 + 64; }
 
-int select_grid_blocks(int sm_count) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_steps_kernel, SEL_THREADS, 0);
-  if (per_sm < 1) per_sm = 1;
-  return sm_count * (per_sm > 1 ? 1 : per_sm);
-}
+int select_max_candidates() { return 128; }
 
-cudaError_t select_steps(cudaStream_t st, int grid_blocks, int n_r, int steps, int kb, double* d,
-                         int* pos, double* L, const double* W, const int* cand, int n_cand,
-                         void* part, int* piv_order, double* margin, int* k_out) {
-  StepParams p;
-  p.n_r = n_r;
-  p.steps = steps;
-  p.kb = kb;
-  p.d = d;
-  p.pos = pos;
-  p.L = L;
-  p.W = W;
-  p.cand = cand;
-  p.n_cand = n_cand;
-  p.part = static_cast<Part*>(part);
-  p.piv_order = piv_order;
-  p.margin = margin;
-  p.k_out = k_out;
-  void* args[] = {&p};
-  count_launches(1);
-  return cudaLaunchCooperativeKernel((const void*)select_steps_kernel, dim3(grid_blocks),
-                                     dim3(SEL_THREADS), args, 0, st);
-}
-
-cudaError_t select_scatter_perm(cudaStream_t st, const int* pos, int n_r, int* perm) {
-  scatter_perm_kernel<<<592, 256, 0, st>>>(pos, n_r, perm); count_launches(1);
+cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* W,
+                               int* pos, int* perm, double* lc, double* mprime, int* piv_order, double* margin,
+                               int* b_out) {
+  CandParams p{n_r, s, steps, kb, static_cast<const Ent*>(top), W, pos, perm, lc, mprime, piv_order, margin, b_out};
+  const size_t smem = select_cand_smem_bytes(s);
+  cudaError_t e = cudaFuncSetAttribute(cand_greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cand_greedy_kernel<<<1, CG_THREADS, smem, st>>>(p); count_launches(1);
   return cudaGetLastError();
 }
 
-size_t select_part_bytes(int grid_blocks) { return (size_t)3 * grid_blocks * sizeof(Part) + 64; }
-int select_max_candidates() { return SEL_MAXS; }
+cudaError_t select_cand_rows(cudaStream_t st, const void* top, int n, int* rows) {
+  cand_rows_kernel<<<1, 256, 0, st>>>(static_cast<const Ent*>(top), n, rows); count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t select_downdate(cudaStream_t st, const double* L, int n_r, int kb, int b, const int* pos, double* d) {
+  if (b <= 0) return cudaSuccess;
+  downdate_kernel<<<592, 256, 0, st>>>(L, n_r, kb, b, pos, d); count_launches(1);
+  return cudaGetLastError();
+}
 
 }  // namespace lrgw_dev

@@ -6,20 +6,24 @@
 
 namespace lrgw_dev {
 
-// d[r] = (sum_i a_ri^2)(sum_j b_rj^2) (diag of the Hadamard Gram), pos[r] = r.
+// d[r] = (sum_i a_ri^2)(sum_j b_rj^2) (diag of the Hadamard Gram), pos = perm = identity.
 cudaError_t select_init(cudaStream_t st, const double* a, long long lda, int n1, const double* b,
-                        long long ldb, int n2, int n_r, double* d, int* pos);
-// Top-s rows by (d desc, position asc) among positions >= k -> cand[0..n_cand).
-size_t select_topk_tmp_elems(int n_r, int s);
-cudaError_t select_topk(cudaStream_t st, const double* d, const int* pos, int n_r, int k, int s,
-                        double* tmp_v, int* tmp_p, int* tmp_g, int* cand, int* n_cand);
-int select_grid_blocks(int sm_count);
-size_t select_part_bytes(int grid_blocks);
+                        long long ldb, int n2, int n_r, double* d, int* pos, int* perm);
+// Top s1 unselected rows (positions >= k) by (d desc, position asc) into `out`
+// (s1 opaque entries of select_ent_bytes()); missing entries have row -1.
+size_t select_ent_bytes();
+size_t select_topk_tmp_bytes(int n_r, int s1);
+cudaError_t select_topk(cudaStream_t st, const double* d, const int* pos, int n_r, int k, int s1, void* tmp,
+                        void* out);
+cudaError_t select_cand_rows(cudaStream_t st, const void* top, int n, int* rows);
 int select_max_candidates();
-// Exact greedy steps from kb while the argmax stays among the candidates.
-cudaError_t select_steps(cudaStream_t st, int grid_blocks, int n_r, int steps, int kb, double* d,
-                         int* pos, double* L, const double* W, const int* cand, int n_cand,
-                         void* part, int* piv_order, double* margin, int* k_out);
-cudaError_t select_scatter_perm(cudaStream_t st, const int* pos, int n_r, int* perm);
+size_t select_cand_smem_bytes(int s);
+// Certified greedy on the s candidates (one CTA): accepted steps -> *b_out,
+// pivots, margins, positions; mprime (s x b) = E L_sel^-T.
+cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* W,
+                               int* pos, int* perm, double* lc, double* mprime, int* piv_order, double* margin,
+                               int* b_out);
+// d -= rowsum(L[:, kb:kb+b]^2) over unselected rows.
+cudaError_t select_downdate(cudaStream_t st, const double* L, int n_r, int kb, int b, const int* pos, double* d);
 
 }  // namespace lrgw_dev
