@@ -298,7 +298,7 @@ void pvp_impl(lrgw_ctx c, const int* dims, const double* cell, int zero, const d
   DBuf wts = dalloc(c, (size_t)2 * nh);
   ck(coulomb_half_weights(c->stream, dims[0], dims[1], dims[2], cell[0], cell[1], cell[2], zero, wts.d()),
      "coulomb_half_weights");
-  Work w = make_work(c, (size_t)8 * n_mu * n_mu);
+  Work w = make_work(c, (size_t)16 * n_mu * n_mu);
   gemm(c, n_mu, n_mu, (int)(2 * nh), xh.d(), 2 * nh, Lay::K, xh.d(), 2 * nh, Lay::K, pvp, n_mu, 1.0, 0.0,
        wts.d(), true, &w);
   ck(mirror_lower(c->stream, pvp, n_mu, n_mu, false), "mirror");
@@ -416,29 +416,62 @@ void gram_inverse(lrgw_ctx c, const double* gram, int n, double* ginv) {
   gemm(c, n, n, n, q.d(), n, Lay::MN, q.d(), n, Lay::MN, ginv, n, 1.0, 0.0, dinv.d());
 }
 
-// K = (T^-1/2 - P^T V P)^-1 (smw.hpp:42-73) with Cholesky leaves: T must be
-// negative definite (the reference's sym_eig check, smw.hpp:47-51), then
-// 1/2 T^-1 = -1/2 (-T)^-1 and K = -(-M)^-1 with -M = 1/2 (-T)^-1 + pvp SPD.
+// In-place inverse of a lower-triangular factor (cuSOLVER trtri, leaf).
+void trtri_lower(lrgw_ctx c, double* a, int n) {
+  size_t wd = 0, wh = 0;
+  cks(cusolverDnXtrtri_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, a, n, &wd,
+                                  &wh),
+      "trtri_bufferSize");
+  DBuf wdev(c, std::max<size_t>(wd, 8));
+  std::vector<char> whost(std::max<size_t>(wh, 8));
+  DBuf info = ialloc(c, 1);
+  ck(cudaMemsetAsync(info.p, 0, sizeof(int), c->stream), "memset");
+  cks(cusolverDnXtrtri(c->solver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, a, n, wdev.p, wd,
+                       whost.data(), wh, info.i()),
+      "trtri");
+  int h = 0;
+  download(c, &h, info.p, sizeof(int));
+  if (h != 0) fail(LRGW_ERR_SINGULAR, "trtri: singular factor", h - 1);
+}
+
+// K = (T^-1/2 - P^T V P)^-1 (smw.hpp:42-73). T must be negative definite
+// (the reference's sym_eig check, smw.hpp:47-51): -T = R R^T (Cholesky leaf;
+// failure -> numeric_error, a pivot below the LU threshold -> singular). Then
+//   T^-1/2 - P = -R^-T M R^-1,  M = I/2 + R^T P R  (SPD, >= I/2)
+//   K = -R M^-1 R^T = -Z Z^T,   Z = R Q^-T,  M = Q Q^T
+// i.e. two Cholesky factorisations and one triangular inverse (cuSOLVER
+// leaves) plus four N_mu^3 DMMA GEMMs; K is symmetric by construction.
 void smw_core(lrgw_ctx c, const double* t, const double* pvp, int n, double* k) {
   const size_t nn = (size_t)n * n;
   const double mx = dev_max_abs(c, t, nn);
-  DBuf negt = dalloc(c, nn);
-  ck(scale_copy(c->stream, t, negt.d(), nn, -1.0), "scale_copy");
-  if (potrf_lower(c, negt.d(), n) != 0)
+  DBuf r = dalloc(c, nn);
+  ck(scale_copy(c->stream, t, r.d(), nn, -1.0), "scale_copy");
+  if (potrf_lower(c, r.d(), n) != 0)
     fail(LRGW_ERR_NUMERIC, "assemble_K: T is not negative definite (gapless or rank-deficient input)");
-  const int tp = tiny_pivot(c, negt.d(), n, mx);
+  const int tp = tiny_pivot(c, r.d(), n, mx);
   if (tp >= 0) fail(LRGW_ERR_SINGULAR, "assemble_K: T singular", tp);
-  potri_lower(c, negt.d(), n);  // (-T)^-1, full
-  // -M = 1/2 (-T)^-1 + pvp
-  DBuf negm = dalloc(c, nn);
-  ck(cudaMemcpyAsync(negm.p, pvp, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
-  ck(axpby(c->stream, n, n, 0.5, negt.d(), n, 1.0, negm.d(), n), "axpby");
-  const double mx2 = dev_max_abs(c, negm.d(), nn);
-  if (potrf_lower(c, negm.d(), n) != 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", 0);
-  const int tp2 = tiny_pivot(c, negm.d(), n, mx2);
+  ck(zero_strict_upper(c->stream, r.d(), n, n), "zero_upper");
+  Work w = make_work(c, 8 * nn);
+  // Y = P R   (R lower: R(k, j) = 0 for k < j)
+  DBuf y = dalloc(c, nn);
+  ck(dgemm(c->stream, n, n, n, pvp, n, Lay::MN, r.d(), n, Lay::K, y.d(), n, 1.0, 0.0, nullptr, false, c->sm_count,
+           nullptr, 0, true, nullptr),
+     "dgemm(PR)");
+  // M = R^T Y + I/2 (lower tiles, mirrored)
+  DBuf m = dalloc(c, nn);
+  gemm(c, n, n, n, r.d(), n, Lay::K, y.d(), n, Lay::K, m.d(), n, 1.0, 0.0, nullptr, true, &w);
+  ck(mirror_lower(c->stream, m.d(), n, n, false), "mirror");
+  ck(add_diag(c->stream, m.d(), n, n, 0.5), "add_diag");
+  const double mx2 = dev_max_abs(c, m.d(), nn);
+  if (potrf_lower(c, m.d(), n) != 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", 0);
+  const int tp2 = tiny_pivot(c, m.d(), n, mx2);
   if (tp2 >= 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", tp2);
-  potri_lower(c, negm.d(), n);
-  ck(scale_copy(c->stream, negm.d(), k, nn, -1.0), "scale_copy");
+  ck(zero_strict_upper(c->stream, m.d(), n, n), "zero_upper");
+  trtri_lower(c, m.d(), n);  // Q^-1
+  // Z = R Q^-T ; K = -Z Z^T (lower tiles, mirrored)
+  gemm(c, n, n, n, r.d(), n, Lay::MN, m.d(), n, Lay::MN, y.d(), n, 1.0, 0.0);
+  gemm(c, n, n, n, y.d(), n, Lay::MN, y.d(), n, Lay::MN, k, n, -1.0, 0.0, nullptr, true, &w);
+  ck(mirror_lower(c->stream, k, n, n, false), "mirror");
 }
 
 // ---------------------------------------------------------------------------
@@ -450,8 +483,17 @@ struct HostEnt {
   int pos, row;
 };
 
+// keep (optional): the pivoted-Cholesky factor L (n_r x steps, pivot order)
+// and the pivot sequence, reused by the fused fit of lrgw_build.
+struct SelectKeep {
+  DBuf L;
+  std::vector<int> order;
+  int steps = 0;
+};
+
 std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int n1, const double* b,
-                                 long long ldb, int n2, int n_r, int n_mu, double* min_margin) {
+                                 long long ldb, int n2, int n_r, int n_mu, double* min_margin,
+                                 SelectKeep* keep = nullptr) {
   if (n_mu > n_r) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: N_mu > N_r");
   if (n_mu < 1) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: N_mu < 1");
   if (n1 < 1 || n2 < 1) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: empty orbital set");
@@ -464,8 +506,8 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
   DBuf d = dalloc(c, n_r), pos = ialloc(c, n_r), perm = ialloc(c, n_r);
   DBuf L = dalloc(c, (size_t)n_r * std::max(steps, 1));
   DBuf Wbuf[2] = {dalloc(c, (size_t)n_r * s), dalloc(c, (size_t)n_r * s)};
-  DBuf amu = dalloc(c, (size_t)s * n1), bmu = dalloc(c, (size_t)s * n2);
-  DBuf lcg = dalloc(c, (size_t)s * std::max(steps, 1));
+  DBuf amu = dalloc(c, (size_t)(s + 1) * n1), bmu = dalloc(c, (size_t)(s + 1) * n2);
+  DBuf lcg = dalloc(c, (size_t)(s + 1) * std::max(steps, 1));
   DBuf top(c, (size_t)(s + 1) * sizeof(HostEnt)), top2(c, (size_t)(s + 1) * sizeof(HostEnt));
   DBuf tmp(c, select_topk_tmp_bytes(n_r, s + 1));
   DBuf cand = ialloc(c, s), oldc = ialloc(c, s);
@@ -508,22 +550,24 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
     if (n_re > 0) {
       ck(cudaMemcpyAsync(oldc.p, hold.data(), sizeof(int) * n_re, cudaMemcpyHostToDevice, c->stream), "H2D");
       ck(gather_cols(c->stream, Wp, n_r, n_r, oldc.i(), n_re, Wn, n_r), "gather_cols");
-      ck(gather_rows(c->stream, L.d() + (size_t)k_prev * n_r, n_r, b_prev, cand.i(), n_re, lcg.d(), n_re), "gather");
-      gemm(c, n_r, n_re, b_prev, L.d() + (size_t)k_prev * n_r, n_r, Lay::MN, lcg.d(), n_re, Lay::MN, Wn, n_r, -1.0,
+      const int ldr = n_re + (n_re & 1);  // even ld: 16-byte operand loads
+      ck(gather_rows(c->stream, L.d() + (size_t)k_prev * n_r, n_r, b_prev, cand.i(), n_re, lcg.d(), ldr), "gather");
+      gemm(c, n_r, n_re, b_prev, L.d() + (size_t)k_prev * n_r, n_r, Lay::MN, lcg.d(), ldr, Lay::MN, Wn, n_r, -1.0,
            1.0);
     }
     if (n_new > 0) {
       // W(:, new) = G(:, new) - L[:, :k] L[new, :k]^T
       double* Wnew = Wn + (size_t)n_re * n_r;
       const int* cn = cand.i() + n_re;
-      ck(gather_rows(c->stream, a, lda, n1, cn, n_new, amu.d(), n_new), "gather");
-      ck(gather_rows(c->stream, b, ldb, n2, cn, n_new, bmu.d(), n_new), "gather");
-      ck(hadamard_gemm(c->stream, n_r, n_new, a, lda, amu.d(), n_new, n1, b, ldb, bmu.d(), n_new, n2, Wnew, n_r, 1.0,
+      const int ldn = n_new + (n_new & 1);
+      ck(gather_rows(c->stream, a, lda, n1, cn, n_new, amu.d(), ldn), "gather");
+      ck(gather_rows(c->stream, b, ldb, n2, cn, n_new, bmu.d(), ldn), "gather");
+      ck(hadamard_gemm(c->stream, n_r, n_new, a, lda, amu.d(), ldn, n1, b, ldb, bmu.d(), ldn, n2, Wnew, n_r, 1.0,
                        0.0),
          "hadamard_gemm");
       if (k > 0) {
-        ck(gather_rows(c->stream, L.d(), n_r, k, cn, n_new, lcg.d(), n_new), "gather");
-        gemm(c, n_r, n_new, k, L.d(), n_r, Lay::MN, lcg.d(), n_new, Lay::MN, Wnew, n_r, -1.0, 1.0);
+        ck(gather_rows(c->stream, L.d(), n_r, k, cn, n_new, lcg.d(), ldn), "gather");
+        gemm(c, n_r, n_new, k, L.d(), n_r, Lay::MN, lcg.d(), ldn, Lay::MN, Wnew, n_r, -1.0, 1.0);
       }
     }
     ck(select_cand_greedy(c->stream, n_r, se, steps, k, top2.p, Wn, pos.i(), perm.i(), lcand.d(), mprime.d(),
@@ -543,6 +587,12 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
   std::vector<int32_t> pts(n_mu);
   download(c, pts.data(), perm.p, sizeof(int) * n_mu);
   std::sort(pts.begin(), pts.end());
+  if (keep) {
+    keep->steps = steps;
+    keep->order.resize(steps);
+    download(c, keep->order.data(), order.p, sizeof(int) * steps);
+    keep->L = std::move(L);
+  }
   if (min_margin) {
     std::vector<double> mg(std::max(steps, 1));
     download(c, mg.data(), margin.p, sizeof(double) * std::max(steps, 1));
@@ -584,6 +634,60 @@ void fit_impl(lrgw_ctx c, const double* a, long long lda, int n1, const double* 
   gram_inverse(c, gram.d(), n_mu, ginv.d());
   mark(c, 3);
   gemm(c, n_r, n_mu, n_mu, lhs.d(), n_r, Lay::MN, ginv.d(), n_mu, Lay::MN, theta, ldt, 1.0, 0.0);
+}
+
+// Fused fit from the selection's Cholesky factor: with the greedy pivots
+// p_0..p_{N_mu-1}, G(:, P) = L L_P^T and G(P, P) = L_P L_P^T where
+// L_P = L[P, :] is lower triangular, so
+//   Theta = (Z C^T)(C C^T)^-1 = G(:, P) G(P, P)^-1 = L L_P^-1
+// (isdf.hpp:130-143 in exact arithmetic). One triangular inverse of L_P
+// (cuSOLVER trtri, leaf) and one DMMA GEMM that skips the zero upper triangle
+// of L_P^-1 and scatters the pivot-ordered columns into sorted-point order.
+// Returns false (caller falls back to the explicit path) when L_P has a pivot
+// below the LU singularity threshold of linalg.hpp:128, 137.
+bool fused_fit(lrgw_ctx c, const SelectKeep& keep, int n_r, const std::vector<int32_t>& pts_sorted, int n_mu,
+               double* theta, long long ldt) {
+  if (keep.steps != n_mu) return false;
+  std::vector<int> order(keep.order.begin(), keep.order.end());
+  DBuf dorder = upload_i(c, order.data(), n_mu);
+  DBuf lp = dalloc(c, (size_t)n_mu * n_mu);
+  ck(gather_rows(c->stream, keep.L.d(), n_r, n_mu, dorder.i(), n_mu, lp.d(), n_mu), "gather");
+  // zero the (numerically tiny) strict upper triangle and check the diagonal
+  ck(zero_strict_upper(c->stream, lp.d(), n_mu, n_mu), "zero_upper");
+  std::vector<double> diag(n_mu);
+  ck(cudaMemcpy2DAsync(diag.data(), sizeof(double), lp.d(), (size_t)(n_mu + 1) * sizeof(double), sizeof(double),
+                       n_mu, cudaMemcpyDeviceToHost, c->stream),
+     "D2H diag");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  double gmax = 0.0;
+  for (double v : diag) gmax = std::max(gmax, v * v);  // G(p_i, p_i) >= L_ii^2; the LU scale
+  const double tiny = 1e-14 * (gmax > 0.0 ? gmax : 1.0);
+  for (double v : diag)
+    if (!(v * v >= tiny)) return false;
+  // X = L_P^-1 in place
+  size_t wd = 0, wh = 0;
+  cks(cusolverDnXtrtri_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n_mu, CUDA_R_64F,
+                                  lp.d(), n_mu, &wd, &wh),
+      "trtri_bufferSize");
+  DBuf wdev(c, std::max<size_t>(wd, 8));
+  std::vector<char> whost(std::max<size_t>(wh, 8));
+  DBuf info = ialloc(c, 1);
+  cks(cusolverDnXtrtri(c->solver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n_mu, CUDA_R_64F, lp.d(), n_mu,
+                       wdev.p, wd, whost.data(), wh, info.i()),
+      "trtri");
+  int hinfo = 0;
+  download(c, &hinfo, info.p, sizeof(int));
+  if (hinfo != 0) return false;
+  mark(c, 3);  // FIT_SOLVE = gather L_P + trtri; FIT_GEMM = L L_P^-1 below
+  // output column of pivot-ordered column q: its rank among the sorted points
+  std::vector<int> colmap(n_mu);
+  for (int q = 0; q < n_mu; ++q)
+    colmap[q] = (int)(std::lower_bound(pts_sorted.begin(), pts_sorted.end(), order[q]) - pts_sorted.begin());
+  DBuf dmap = upload_i(c, colmap.data(), n_mu);
+  ck(dgemm(c->stream, n_r, n_mu, n_mu, keep.L.d(), n_r, Lay::MN, lp.d(), n_mu, Lay::K, theta, ldt, 1.0, 0.0,
+           nullptr, false, c->sm_count, nullptr, 0, true, dmap.i()),
+     "dgemm(theta)");
+  return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -1134,11 +1238,17 @@ int lrgw_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, lo
     c->timing = true;
     mark(c, 0);
     // stage 1
-    std::vector<int32_t> pts = select_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, n_mu, nullptr);
+    SelectKeep keep;
+    std::vector<int32_t> pts = select_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, n_mu, nullptr, &keep);
     mark(c, 1);
-    // stage 2
+    // stage 2: fused fit from the selection's factor (explicit path otherwise)
     DBuf theta = dalloc(c, (size_t)n_r * n_mu);
-    fit_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, pts.data(), n_mu, theta.d(), n_r);
+    mark(c, 2);  // FIT_LHS is empty on the fused path (lhs lives in L)
+    const bool fused = fused_fit(c, keep, n_r, pts, n_mu, theta.d(), n_r);
+    keep.L.release();
+    if (!fused) {  // explicit path re-marks its own lhs / solve boundaries
+      fit_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, pts.data(), n_mu, theta.d(), n_r);
+    }
     mark(c, 4);
     // stage 3
     DBuf dpts = upload_i(c, pts.data(), n_mu);

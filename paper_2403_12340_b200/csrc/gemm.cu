@@ -19,7 +19,7 @@ using CfgS = GemmCfg<64, 64, 32, 32, 4, AK, BK, VA, VB>;
 // Square 128x128 CTA, 16 warps of 32x32, 3 stages (~120 KB smem, 1 CTA/SM):
 // the symmetric (lower-tile) split-K SYRK of Theta^T V Theta.
 template <bool AK, bool BK, int VA, int VB>
-using CfgX = GemmCfg<128, 128, 32, 32, 3, AK, BK, VA, VB>;
+using CfgX = GemmCfg<128, 128, 32, 32, 3, AK, BK, VA, VB, 32>;
 
 // Hadamard pair (two live accumulator sets): 128x64 CTA, 16 warps of 32x16;
 // 128x32 CTA, 8 warps of 32x16 when N would otherwise pad badly.
@@ -169,7 +169,7 @@ cudaError_t gather_cols(cudaStream_t st, const double* src, long long lds, int r
 cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long long lda, Lay la,
                   const double* B, long long ldb, Lay lb, double* C, long long ldc, double alpha,
                   double beta, const double* scale, bool lower, int sm_count, double* work,
-                  size_t work_elems) {
+                  size_t work_elems, bool tri_b, const int* colmap) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   DgemmParams p{};
   p.M = M;
@@ -185,20 +185,27 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
   p.beta = beta;
   p.scale = scale;
   p.lower = lower ? 1 : 0;
+  p.tri_b = tri_b ? 1 : 0;
+  p.colmap = colmap;
+  if ((tri_b || colmap) && (lower || work)) return cudaErrorInvalidValue;
   const bool ak = la == Lay::K, bk = lb == Lay::K;
   // 16-byte cp.async needs aligned bases, even leading dims and even extents
   // along the contiguous axis.
-  const bool va = aligned16(A) && lda % 2 == 0 && (ak ? K % 2 == 0 : M % 2 == 0);
-  const bool vb = aligned16(B) && ldb % 2 == 0 && (bk ? K % 2 == 0 : N % 2 == 0);
+  // (an odd M / N is fine with a padded even ld: the straddling pair only
+  // feeds output rows / columns that are never stored; an odd K is not)
+  const bool va = aligned16(A) && lda % 2 == 0 && (ak ? K % 2 == 0 : (M % 2 == 0 || lda > M));
+  const bool vb = aligned16(B) && ldb % 2 == 0 && (bk ? K % 2 == 0 : (N % 2 == 0 || ldb > N));
   if (lower && M != N) return cudaErrorInvalidValue;
   Tile tile;
   long long tiles;
   int occ;
   if (lower) {
-    tile = Tile::X;
-    const long long t = (M + 127) / 128;
+    // symmetric outputs: 64x64 lower tiles + split-K (measured faster than
+    // 128x128 tiles for the long-K SYRK of Theta^T V Theta)
+    tile = Tile::S;
+    const long long t = (M + 63) / 64;
     tiles = t * (t + 1) / 2;
-    occ = 1;
+    occ = 2;
   } else if (N > 64 && N <= 128 && (long long)((M + 127) / 128) >= 2LL * sm_count) {
     // one column tile of width 96 or 128 (A streamed once)
     tile = N <= 96 ? Tile::W96 : Tile::W128;
@@ -238,7 +245,7 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
   else e = launch_layout<true, true>(st, p, tile, va, vb, splits);
   if (e != cudaSuccess || splits <= 1) return e;
   splitk_reduce_kernel<<<1184, 256, 0, st>>>(work, splits, (long long)M * N, M, N, C, ldc, beta,
-                                             lower ? 1 : 0, 128); count_launches(1);
+                                             lower ? 1 : 0, 64); count_launches(1);
   return cudaGetLastError();
 }
 
@@ -250,7 +257,7 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
   HadamardParams p{M, N, k1, k2, a1, b1, a2, b2, lda1, ldb1, lda2, ldb2, C, ldc, alpha, beta};
   const bool vec = aligned16(a1) && aligned16(b1) && aligned16(a2) && aligned16(b2) &&
                    lda1 % 2 == 0 && ldb1 % 2 == 0 && lda2 % 2 == 0 && ldb2 % 2 == 0 &&
-                   M % 2 == 0 && N % 2 == 0;
+                   (M % 2 == 0 || (lda1 > M && lda2 > M)) && (N % 2 == 0 || (ldb1 > N && ldb2 > N));
   auto go = [&](auto cfg) -> cudaError_t {
     using Cfg = decltype(cfg);
     dim3 grid((M + Cfg::BM - 1) / Cfg::BM, (N + Cfg::BN - 1) / Cfg::BN);

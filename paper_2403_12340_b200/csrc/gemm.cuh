@@ -32,6 +32,8 @@ struct DgemmParams {
   int k_chunk;           // split-K chunk (multiple of BK) when gridDim.z > 1
   double* partial;       // split-K: raw alpha*acc to partial + z*part_stride (ld = M)
   long long part_stride;
+  int tri_b;             // B(n, k) == 0 for k < n (lower-triangular operand): K starts at n0
+  const int* colmap;     // output column n is written to column colmap[n] of C
 };
 
 // Tile loader for one operand. ROWS = BM or BN.
@@ -74,16 +76,16 @@ struct TileLoader {
   }
 };
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, bool AK_, bool BK_MAJ_, int VA_, int VB_>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, bool AK_, bool BK_MAJ_, int VA_, int VB_, int BK_ = 16>
 struct GemmCfg {
-  static constexpr int BM = BM_, BN = BN_, BK = 16, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
   static constexpr bool A_KMAJOR = AK_, B_KMAJOR = BK_MAJ_;
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
   static constexpr int FM = WM / 8, FN = WN / 8;
   using LA = TileLoader<BM, BK, A_KMAJOR, VA_, THREADS>;
   using LB = TileLoader<BN, BK, B_KMAJOR, VB_, THREADS>;
-  static constexpr int STAGE_ELEMS = LA::ELEMS + LB::ELEMS;
+  static constexpr int STAGE_ELEMS = LA::ELEMS + LB::ELEMS + BK;  // + the k-slice of the diagonal scale
   static constexpr int SMEM_BYTES = STAGES * STAGE_ELEMS * 8;
 };
 
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(Cfg::THREADS) dgemm_kernel(DgemmParams p) {
     tn = blockIdx.y;
   }
   const int m0 = tm * BM, n0 = tn * BN;
-  const int kb = p.k_chunk > 0 ? blockIdx.z * p.k_chunk : 0;
+  const int kb = p.k_chunk > 0 ? blockIdx.z * p.k_chunk : (p.tri_b ? (n0 / BK) * BK : 0);
   const int ke = p.k_chunk > 0 ? min(p.K, kb + p.k_chunk) : p.K;
   const int nkt = ke > kb ? (ke - kb + BK - 1) / BK : 0;
 
@@ -119,12 +121,21 @@ __global__ void __launch_bounds__(Cfg::THREADS) dgemm_kernel(DgemmParams p) {
 
   auto stageA = [&](int s) { return smem + s * Cfg::STAGE_ELEMS; };
   auto stageB = [&](int s) { return smem + s * Cfg::STAGE_ELEMS + LA::ELEMS; };
+  auto stageS = [&](int s) { return smem + s * Cfg::STAGE_ELEMS + LA::ELEMS + LB::ELEMS; };
+  // the diagonal scale travels with its k-tile (no global load on the MMA path)
+  auto load_scale = [&](int s, int k0) {
+    if (p.scale && tid < BK) {
+      const int gk = k0 + tid;
+      cp_async8(stageS(s) + tid, gk < ke ? p.scale + gk : p.scale, gk < ke);
+    }
+  };
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nkt) {
       LA::load(stageA(s), p.A, p.lda, m0, p.M, kb + s * BK, ke, tid);
       LB::load(stageB(s), p.B, p.ldb, n0, p.N, kb + s * BK, ke, tid);
+      load_scale(s, kb + s * BK);
     }
     cp_async_commit();
   }
@@ -138,12 +149,13 @@ __global__ void __launch_bounds__(Cfg::THREADS) dgemm_kernel(DgemmParams p) {
         const int s = nx % STAGES;
         LA::load(stageA(s), p.A, p.lda, m0, p.M, kb + nx * BK, ke, tid);
         LB::load(stageB(s), p.B, p.ldb, n0, p.N, kb + nx * BK, ke, tid);
+        load_scale(s, kb + nx * BK);
       }
       cp_async_commit();
     }
     const double* sa = stageA(kt % STAGES);
     const double* sb = stageB(kt % STAGES);
-    const int kbase = kb + kt * BK;
+    const double* ss = stageS(kt % STAGES);
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[FM], bf[FN];
@@ -152,8 +164,7 @@ __global__ void __launch_bounds__(Cfg::THREADS) dgemm_kernel(DgemmParams p) {
 #pragma unroll
       for (int j = 0; j < FN; ++j) bf[j] = LB::frag(sb, wn + j * 8 + g, kk + t);
       if (p.scale) {
-        const int gk = kbase + kk + t;
-        const double sc = gk < ke ? __ldg(p.scale + gk) : 0.0;
+        const double sc = ss[kk + t];
 #pragma unroll
         for (int j = 0; j < FN; ++j) bf[j] *= sc;
       }
@@ -191,7 +202,8 @@ __global__ void __launch_bounds__(Cfg::THREADS) dgemm_kernel(DgemmParams p) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (n + h < p.N) {
-            double* c = p.C + m + (long long)(n + h) * p.ldc;
+            const int nc = p.colmap ? __ldg(p.colmap + n + h) : n + h;
+            double* c = p.C + m + (long long)nc * p.ldc;
             const double v = p.alpha * acc[i][j][h];
             *c = (p.beta == 0.0) ? v : v + p.beta * (*c);
           }

@@ -14,11 +14,13 @@ void count_launches(int n);
 enum class Lay { MN, K };  // operand stored MN-contiguous (col-major) or K-contiguous
 
 // C = alpha * A diag(scale) B^T + beta * C with A: M x K, B: N x K (see gemm.cuh).
-// lower: only lower-triangle 64x64 tiles (M == N). `work` enables split-K.
+// lower: only lower-triangle tiles (M == N). `work` enables split-K.
+// tri_b: B(n, k) == 0 for k < n (skip those k); colmap: output column n goes
+// to column colmap[n] of C (device array).
 cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long long lda, Lay la,
                   const double* B, long long ldb, Lay lb, double* C, long long ldc, double alpha,
                   double beta, const double* scale, bool lower, int sm_count, double* work,
-                  size_t work_elems);
+                  size_t work_elems, bool tri_b = false, const int* colmap = nullptr);
 
 // C = alpha * (A1 B1^T) o (A2 B2^T) + beta * C; A1: M x K1, B1: N x K1, A2: M x K2,
 // B2: N x K2, all MN-contiguous (isdf.hpp:132 fit GEMM pair + Hadamard).
@@ -58,6 +60,7 @@ cudaError_t coulomb_scale_half(cudaStream_t st, int n1, int n2, int n3, double c
 // scalar helpers (misc.cu)
 cudaError_t scale_copy(cudaStream_t st, const double* src, double* dst, size_t n, double alpha);
 cudaError_t fill(cudaStream_t st, double* dst, size_t n, double v);
+cudaError_t zero_strict_upper(cudaStream_t st, double* a, int n, long long lda);
 cudaError_t add_diag(cudaStream_t st, double* a, int n, long long lda, double v);
 cudaError_t axpby(cudaStream_t st, int rows, int cols, double alpha, const double* x, long long ldx,
                   double beta, double* y, long long ldy);

@@ -71,6 +71,15 @@ __global__ void finish_kernel(const double* partial, int n, double* out, int is_
   }
 }
 
+__global__ void zero_strict_upper_kernel(double* a, int n, long long lda) {
+  const long long total = (long long)n * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = static_cast<int>(idx % n), j = static_cast<int>(idx / n);
+    if (i < j) a[i + j * lda] = 0.0;
+  }
+}
+
 constexpr int kRedBlocks = 296;
 
 }  // namespace
@@ -97,6 +106,12 @@ cudaError_t axpby(cudaStream_t st, int rows, int cols, double alpha, const doubl
                   double beta, double* y, long long ldy) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   axpby_kernel<<<1184, 256, 0, st>>>(rows, cols, alpha, x, ldx, beta, y, ldy); count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t zero_strict_upper(cudaStream_t st, double* a, int n, long long lda) {
+  if (n <= 1) return cudaSuccess;
+  zero_strict_upper_kernel<<<592, 256, 0, st>>>(a, n, lda); count_launches(1);
   return cudaGetLastError();
 }
 
