@@ -1141,11 +1141,20 @@ int lrgw_build_epsilon_inverse(lrgw_ctx c, const double* t, const double* p, int
 static void eps_apply_impl(lrgw_ctx c, lrgw_eps e, const double* x, long long ldx, int m, double* y, long long ldy) {
   const int n_r = e->n_r, n_mu = e->n_mu;
   DBuf u = dalloc(c, (size_t)n_mu * m), w = dalloc(c, (size_t)n_mu * m), z = dalloc(c, (size_t)n_r * m);
-  Work wk = make_work(c, (size_t)64 * n_mu * m);
+  Work wk = make_work(c, (size_t)1200 * n_mu * m);
   // u = Theta^T x ; w = K u ; z = Theta w ; y = x + V z   (smw.hpp:101-102)
-  gemm(c, n_mu, m, n_r, e->theta, n_r, Lay::K, x, ldx, Lay::K, u.d(), n_mu, 1.0, 0.0, nullptr, false, &wk);
+  if (skinny_supported(m)) {
+    ck(skinny_tn(c->stream, e->theta, n_r, n_r, n_mu, x, ldx, m, u.d(), n_mu, wk.buf.d(), wk.elems, c->sm_count),
+       "skinny_tn");
+  } else {
+    gemm(c, n_mu, m, n_r, e->theta, n_r, Lay::K, x, ldx, Lay::K, u.d(), n_mu, 1.0, 0.0, nullptr, false, &wk);
+  }
   gemm(c, n_mu, m, n_mu, e->k, n_mu, Lay::MN, u.d(), n_mu, Lay::K, w.d(), n_mu, 1.0, 0.0);
-  gemm(c, n_r, m, n_mu, e->theta, n_r, Lay::MN, w.d(), n_mu, Lay::K, z.d(), n_r, 1.0, 0.0);
+  if (skinny_supported(m) && (size_t)n_mu * m * 8 <= 200 * 1024) {
+    ck(skinny_nn(c->stream, e->theta, n_r, n_r, n_mu, w.d(), n_mu, m, z.d(), n_r, c->sm_count), "skinny_nn");
+  } else {
+    gemm(c, n_r, m, n_mu, e->theta, n_r, Lay::MN, w.d(), n_mu, Lay::K, z.d(), n_r, 1.0, 0.0);
+  }
   coulomb_apply(c, e->dims, e->cell, e->zero, z.d(), n_r, m, y, ldy);
   ck(axpby(c->stream, n_r, m, 1.0, x, ldx, 1.0, y, ldy), "axpby");
 }

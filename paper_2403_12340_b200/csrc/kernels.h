@@ -2,6 +2,7 @@
 // see include/lrgw_cuda.h for that). All matrices column-major FP64.
 #pragma once
 
+#include <algorithm>
 #include <cstddef>
 #include <cuda_runtime.h>
 
@@ -39,6 +40,13 @@ cudaError_t gather_rows(cudaStream_t st, const double* src, long long lds, int c
 // dst(:, c) = src(:, cols[c]), cols on device.
 cudaError_t gather_cols(cudaStream_t st, const double* src, long long lds, int rows, const int* cols, int n,
                         double* dst, long long ldd);
+
+// K7 probe passes over Theta (skinny.cu), m in {1, 2, 4, 8, 16}.
+bool skinny_supported(int m);
+cudaError_t skinny_tn(cudaStream_t st, const double* theta, long long ldt, int n_r, int n_mu, const double* x,
+                      long long ldx, int m, double* u, long long ldu, double* work, size_t work_elems, int sm_count);
+cudaError_t skinny_nn(cudaStream_t st, const double* theta, long long ldt, int n_r, int n_mu, const double* w,
+                      long long ldw, int m, double* z, long long ldz, int sm_count);
 
 // K3 quadrature (quadrature.cu).
 int quad_partial_groups(int n_mu, int n_nodes, int sm_count);

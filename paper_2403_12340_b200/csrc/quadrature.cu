@@ -27,7 +27,7 @@ constexpr int QTHREADS = 32 * QWARPS_M * QWARPS_N;     // 256
 constexpr int QFM = QWM / 8, QFN = QWN / 8;            // 4 x 2 fragments
 constexpr int QPITCH = QBM + 4;                        // conflict-free pitch (doubles)
 constexpr int QTILE = QBK * QPITCH;
-constexpr int QSTAGE_ELEMS = 2 * QTILE;
+constexpr int QSTAGE_ELEMS = 2 * QTILE + 2 * QBK;  // + the k-tile's complex diagonal
 constexpr int QSMEM = QSTAGES * QSTAGE_ELEMS * 8;
 
 struct QuadParams {
@@ -88,6 +88,13 @@ __global__ void __launch_bounds__(QTHREADS, 1) quad_kernel(QuadParams p) {
     const int kend = cph ? p.n_c : p.n_v;
     load_panel<VEC>(s, src, ld, m0, p.n_mu, k0, kend, tid);
     load_panel<VEC>(s + QTILE, src, ld, n0, p.n_mu, k0, kend, tid);
+    // the node's diagonal 1/(z_k - e) for this k-tile (zero-filled past the band count)
+    if (tid < QBK) {
+      const int node = node0 + j / ktt;
+      const double2* dtab = cph ? p.dc + (long long)node * p.n_c : p.dv + (long long)node * p.n_v;
+      const int gk = k0 + tid;
+      cp_async16(s + 2 * QTILE + 2 * tid, gk < kend ? dtab + gk : dtab, gk < kend);
+    }
   };
 
   double accR[QFM][QFN][2], accI[QFM][QFN][2], p1[QFM][QFN][2], p2[QFM][QFN][2], tac[QFM][QFN][2];
@@ -112,16 +119,12 @@ __global__ void __launch_bounds__(QTHREADS, 1) quad_kernel(QuadParams p) {
 
     const int node = node0 + j / ktt;
     const int kt = j % ktt;
-    const bool cph = kt < ktc;
-    const double2* dtab = cph ? p.dc + (long long)node * p.n_c : p.dv + (long long)node * p.n_v;
-    const int kcount = cph ? p.n_c : p.n_v;
-    const int k0 = (cph ? kt : kt - ktc) * QBK;
     const double* sa = smem + (j % QSTAGES) * QSTAGE_ELEMS;
     const double* sb = sa + QTILE;
+    const double2* sd = reinterpret_cast<const double2*>(sa + 2 * QTILE);
 #pragma unroll
     for (int kk = 0; kk < QBK; kk += 4) {
-      const int gk = k0 + kk + t;
-      const double2 d = gk < kcount ? __ldg(dtab + gk) : make_double2(0.0, 0.0);
+      const double2 d = sd[kk + t];
       double af[QFM], br[QFN], bi[QFN];
 #pragma unroll
       for (int i = 0; i < QFM; ++i) af[i] = sa[(kk + t) * QPITCH + wm + i * 8 + g];

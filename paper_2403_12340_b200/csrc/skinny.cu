@@ -1,0 +1,165 @@
+// skinny.cu — K7: the probe apply's two passes over Theta (smw.hpp:97-103).
+//
+//   u = Theta^T x   (N_mu x m, K = N_r)     z = Theta w   (N_r x m, K = N_mu)
+//
+// with m <= 16 probe columns. Both are HBM-bound streams over Theta
+// (N_r x N_mu FP64, 906 MB at Si64); a DMMA tile would waste >90% of its
+// columns, so these are coalesced FMA streams: one pass over Theta each,
+// the small operand (x chunk / w) staged in shared memory.
+#include "kernels.h"
+
+namespace lrgw_dev {
+
+namespace {
+
+constexpr int TN_MU = 8;         // Theta columns per CTA (accumulators: TN_MU x m per thread)
+constexpr int TN_THREADS = 256;  // 8 warps
+
+// partial[chunk][mu][c] = sum over the chunk's rows of Theta[r, mu] x[r, c]
+template <int M>
+__global__ void __launch_bounds__(TN_THREADS) tn_kernel(const double* theta, long long ldt, int n_r, int n_mu,
+                                                        const double* x, long long ldx, int rows_per_chunk,
+                                                        double* partial) {
+  const int mu0 = blockIdx.x * TN_MU;
+  const int r0 = blockIdx.y * rows_per_chunk;
+  const int r1 = min(n_r, r0 + rows_per_chunk);
+  double acc[TN_MU][M];
+#pragma unroll
+  for (int i = 0; i < TN_MU; ++i)
+#pragma unroll
+    for (int c = 0; c < M; ++c) acc[i][c] = 0.0;
+  for (int r = r0 + threadIdx.x; r < r1; r += TN_THREADS) {
+    double xv[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c) xv[c] = __ldg(x + r + (long long)c * ldx);
+#pragma unroll
+    for (int i = 0; i < TN_MU; ++i) {
+      const double th = (mu0 + i < n_mu) ? __ldg(theta + r + (long long)(mu0 + i) * ldt) : 0.0;
+#pragma unroll
+      for (int c = 0; c < M; ++c) acc[i][c] = fma(th, xv[c], acc[i][c]);
+    }
+  }
+  // block reduction: warp shuffles, then across the 8 warps through smem
+  __shared__ double red[TN_THREADS / 32][TN_MU * M];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < TN_MU; ++i)
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+      double v = acc[i][c];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) red[wid][i * M + c] = v;
+    }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < TN_MU * M; idx += TN_THREADS) {
+    double v = 0.0;
+    for (int w = 0; w < TN_THREADS / 32; ++w) v += red[w][idx];
+    const int i = idx / M, c = idx % M;
+    if (mu0 + i < n_mu) partial[((long long)blockIdx.y * n_mu + mu0 + i) * M + c] = v;
+  }
+}
+
+template <int M>
+__global__ void tn_reduce_kernel(const double* partial, int chunks, int n_mu, double* u, long long ldu) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n_mu * M; idx += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int ch = 0; ch < chunks; ++ch) v += partial[(long long)ch * n_mu * M + idx];
+    const int mu = idx / M, c = idx % M;
+    u[mu + (long long)c * ldu] = v;
+  }
+}
+
+// z[r, c] = sum_mu Theta[r, mu] w[mu, c]; w (n_mu x M) staged in shared memory.
+template <int M>
+__global__ void __launch_bounds__(256) nn_kernel(const double* theta, long long ldt, int n_r, int n_mu,
+                                                 const double* w, long long ldw, double* z, long long ldz) {
+  extern __shared__ double ws[];  // n_mu x M, row-major (ws[mu * M + c])
+  for (int idx = threadIdx.x; idx < n_mu * M; idx += blockDim.x) {
+    const int mu = idx / M, c = idx % M;
+    ws[idx] = w[mu + (long long)c * ldw];
+  }
+  __syncthreads();
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_r; r += gridDim.x * blockDim.x) {
+    double acc[M];
+#pragma unroll
+    for (int c = 0; c < M; ++c) acc[c] = 0.0;
+    int mu = 0;
+    for (; mu + 4 <= n_mu; mu += 4) {
+      double th[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) th[u] = __ldg(theta + r + (long long)(mu + u) * ldt);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < M; ++c) acc[c] = fma(th[u], ws[(mu + u) * M + c], acc[c]);
+    }
+    for (; mu < n_mu; ++mu) {
+      const double th = __ldg(theta + r + (long long)mu * ldt);
+#pragma unroll
+      for (int c = 0; c < M; ++c) acc[c] = fma(th, ws[mu * M + c], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < M; ++c) z[r + (long long)c * ldz] = acc[c];
+  }
+}
+
+template <int M>
+cudaError_t tn_launch(cudaStream_t st, const double* theta, long long ldt, int n_r, int n_mu, const double* x,
+                      long long ldx, double* u, long long ldu, double* work, size_t work_elems, int sm_count) {
+  const int mus = (n_mu + TN_MU - 1) / TN_MU;
+  // enough row chunks for ~4 waves, bounded by the workspace
+  int chunks = std::max(1, (4 * sm_count * 2 + mus - 1) / mus);
+  while (chunks > 1 && (size_t)chunks * n_mu * M > work_elems) --chunks;
+  const int rows = (n_r + chunks - 1) / chunks;
+  chunks = (n_r + rows - 1) / rows;
+  tn_kernel<M><<<dim3(mus, chunks), TN_THREADS, 0, st>>>(theta, ldt, n_r, n_mu, x, ldx, rows, work);
+  count_launches(1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  tn_reduce_kernel<M><<<(n_mu * M + 255) / 256, 256, 0, st>>>(work, chunks, n_mu, u, ldu);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+template <int M>
+cudaError_t nn_launch(cudaStream_t st, const double* theta, long long ldt, int n_r, int n_mu, const double* w,
+                      long long ldw, double* z, long long ldz, int sm_count) {
+  const size_t smem = (size_t)n_mu * M * sizeof(double);
+  if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+  cudaFuncSetAttribute(nn_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int blocks = std::min((n_r + 255) / 256, 4 * sm_count);
+  nn_kernel<M><<<blocks, 256, smem, st>>>(theta, ldt, n_r, n_mu, w, ldw, z, ldz);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool skinny_supported(int m) { return m == 1 || m == 2 || m == 4 || m == 8; }
+
+cudaError_t skinny_tn(cudaStream_t st, const double* theta, long long ldt, int n_r, int n_mu, const double* x,
+                      long long ldx, int m, double* u, long long ldu, double* work, size_t work_elems, int sm_count) {
+  switch (m) {
+    case 1: return tn_launch<1>(st, theta, ldt, n_r, n_mu, x, ldx, u, ldu, work, work_elems, sm_count);
+    case 2: return tn_launch<2>(st, theta, ldt, n_r, n_mu, x, ldx, u, ldu, work, work_elems, sm_count);
+    case 4: return tn_launch<4>(st, theta, ldt, n_r, n_mu, x, ldx, u, ldu, work, work_elems, sm_count);
+    case 8: return tn_launch<8>(st, theta, ldt, n_r, n_mu, x, ldx, u, ldu, work, work_elems, sm_count);
+    case 16: return tn_launch<16>(st, theta, ldt, n_r, n_mu, x, ldx, u, ldu, work, work_elems, sm_count);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t skinny_nn(cudaStream_t st, const double* theta, long long ldt, int n_r, int n_mu, const double* w,
+                      long long ldw, int m, double* z, long long ldz, int sm_count) {
+  switch (m) {
+    case 1: return nn_launch<1>(st, theta, ldt, n_r, n_mu, w, ldw, z, ldz, sm_count);
+    case 2: return nn_launch<2>(st, theta, ldt, n_r, n_mu, w, ldw, z, ldz, sm_count);
+    case 4: return nn_launch<4>(st, theta, ldt, n_r, n_mu, w, ldw, z, ldz, sm_count);
+    case 8: return nn_launch<8>(st, theta, ldt, n_r, n_mu, w, ldw, z, ldz, sm_count);
+    case 16: return nn_launch<16>(st, theta, ldt, n_r, n_mu, w, ldw, z, ldz, sm_count);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace lrgw_dev
