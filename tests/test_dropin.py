@@ -1,0 +1,30 @@
+"""The C++ drop-in headers (include/lrgw/*.hpp) compile against the C-ABI and
+pass the reference's own known-answer tests restated in tests/cpp/test_dropin.cpp."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+LIB = os.path.join(ROOT, "paper_2403_12340_b200", "lib")
+
+
+def _compile(out):
+    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), SRC, "-o", out, "-L", LIB,
+           "-llrgw_cuda", f"-Wl,-rpath,{LIB}"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+
+
+def test_dropin_headers_compile(tmp_path):
+    if not os.path.exists(os.path.join(LIB, "liblrgw_cuda.so")):
+        pytest.fail("liblrgw_cuda.so not built")
+    _compile(str(tmp_path / "test_dropin"))
+
+
+@pytest.mark.gpu
+def test_dropin_reference_kats(tmp_path):
+    exe = str(tmp_path / "test_dropin")
+    _compile(exe)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
