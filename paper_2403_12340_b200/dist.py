@@ -1,0 +1,314 @@
+"""Multi-rank orchestration of the eps^-1 build.
+
+One process per GPU; torch.distributed carries the few exchanges. The large
+per-rank arrays (row panels of Phi, L, W, Theta) stay with a *stage backend*
+(the device kernels on a GPU rank); this module owns the partitioning and the
+deterministic exchange logic:
+
+  stage 1  grid-row panels aligned to z-planes; per candidate block one
+           all-gather of the local top-(s+1) lists, owner-contributed rows of
+           Phi / L / W[C, :] (sum of zero-padded contributions: exact), the
+           certified candidate greedy replicated on every rank, local panel
+           updates. Pivots are the greedy pivots (reference linalg.hpp:26-111).
+  stage 2  Theta panel = L panel L_P^-1 (L_P rows owner-contributed).
+  stage 3  quadrature nodes split across ranks, all-reduce of the partial T.
+  stage 4-5a  z-slab 3-D FFT: local 2-D transforms, one all-to-all to
+           y-pencils, local z transform, local G-slab Theta^T V Theta,
+           all-reduce.
+  stage 5b SMW core replicated; probe: all-reduce of Theta_p^T x.
+
+`Backend` is the per-rank compute interface; tests inject a numpy backend
+(tests/test_dist.py) and run world sizes 2-3 over gloo on CPU.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+# ---------------------------------------------------------------------------
+# partitioning
+# ---------------------------------------------------------------------------
+
+def z_panels(dims, world):
+    """Contiguous grid-row ranges [r0, r1) per rank, on z-plane boundaries
+    (rows n = i1 + n1 (i2 + n2 i3)); every rank gets >= 1 plane when n3 >= world."""
+    n1, n2, n3 = dims
+    plane = n1 * n2
+    out = []
+    for p in range(world):
+        z0 = (n3 * p) // world
+        z1 = (n3 * (p + 1)) // world
+        out.append((z0 * plane, z1 * plane))
+    return out
+
+
+def node_ranges(n_nodes, world):
+    """Contiguous quadrature-node ranges [k0, k1) per rank."""
+    return [((n_nodes * p) // world, (n_nodes * (p + 1)) // world) for p in range(world)]
+
+
+def y_chunks(n2, world):
+    return [((n2 * p) // world, (n2 * (p + 1)) // world) for p in range(world)]
+
+
+# ---------------------------------------------------------------------------
+# collectives (torch.distributed over numpy payloads; NCCL or gloo)
+# ---------------------------------------------------------------------------
+
+class Comm:
+    """Thin wrapper: rank/world and the handful of exchanges the build needs."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def _t(self, a):
+        import torch
+
+        return torch.from_numpy(np.ascontiguousarray(a))
+
+    def allreduce_sum(self, a):
+        t = self._t(a)
+        self.dist.all_reduce(t, group=self.group)
+        return t.numpy()
+
+    def allgather(self, a):
+        t = self._t(a)
+        out = [t.clone() for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [o.numpy() for o in out]
+
+    def alltoall(self, blocks):
+        """blocks[q] goes to rank q; returns the blocks received from each rank.
+        Uses all_to_all when the backend has it, else pairwise send/recv."""
+        import torch
+
+        send = [self._t(b) for b in blocks]
+        shapes = self.allgather(np.array([b.size for b in blocks], dtype=np.int64))
+        recv = [torch.empty(int(shapes[q][self.rank]), dtype=send[0].dtype) for q in range(self.world)]
+        try:
+            self.dist.all_to_all([r for r in recv], [s.reshape(-1) for s in send], group=self.group)
+        except (RuntimeError, ValueError):
+            reqs = []
+            for q in range(self.world):
+                if q == self.rank:
+                    recv[q].copy_(send[q].reshape(-1))
+                    continue
+                reqs.append(self.dist.isend(send[q].reshape(-1).contiguous(), q, group=self.group))
+                reqs.append(self.dist.irecv(recv[q], q, group=self.group))
+            for r in reqs:
+                r.wait()
+        return [r.numpy() for r in recv]
+
+
+# ---------------------------------------------------------------------------
+# the certified candidate greedy (replicated, deterministic)
+# ---------------------------------------------------------------------------
+
+def better(v1, p1, v2, p2):
+    """Reference pivot order: larger residual, then the lower current position
+    (strict '>' scan over positions, linalg.hpp:45-48)."""
+    return v1 > v2 or (v1 == v2 and p1 < p2)
+
+
+def merge_top(entries, s1):
+    """Global top-s1 of (d, pos, row) entries by the pivot order."""
+    ent = [tuple(e) for e in entries if e[2] >= 0]
+    ent.sort(key=lambda e: (-e[0], e[1]))
+    out = ent[:s1]
+    while len(out) < s1:
+        out.append((-math.inf, 2**31 - 1, -1))
+    return out
+
+
+def cand_greedy(top, w_cc, kb, steps, pos, perm):
+    """Exact greedy steps on the candidate Schur complement (select.cu
+    cand_greedy_kernel semantics). top: s+1 entries (d, pos, row); w_cc: s x s.
+    Mutates pos/perm (replicated position bookkeeping). Returns
+    (b, pivot rows, M' = E L_sel^-T (s x b), margins)."""
+    s = len(top) - 1
+    tau = top[s][0] if top[s][2] >= 0 else -math.inf
+    d = np.array([e[0] for e in top[:s]], dtype=np.float64)
+    pc = np.array([e[1] for e in top[:s]], dtype=np.int64)
+    rows = np.array([e[2] for e in top[:s]], dtype=np.int64)
+    used = rows < 0
+    w = np.array(w_cc, dtype=np.float64, copy=True)
+    lcols, sel, pivots, margins = [], [], [], []
+    tmax = min(s, steps - kb)
+    for t in range(tmax):
+        best, second, bi = -math.inf, -math.inf, -1
+        bp = 2**62
+        for i in range(s):
+            if used[i]:
+                continue
+            if better(d[i], pc[i], best, bp):
+                second = max(second, best)
+                best, bp, bi = d[i], pc[i], i
+            else:
+                second = max(second, d[i])
+        if bi < 0 or not (t == 0 or best > tau):
+            break
+        k = kb + t
+        prow, ppos = int(rows[bi]), int(pc[bi])
+        occ = int(perm[k])
+        perm[k], perm[ppos] = prow, occ
+        pos[prow], pos[occ] = k, ppos
+        for i in range(s):
+            if rows[i] == occ and i != bi:
+                pc[i] = ppos
+        pc[bi] = k
+        inv = 1.0 / math.sqrt(best) if best > 0 else 0.0
+        lpiv = math.sqrt(best) if best > 0 else 0.0
+        l = np.where(used, 0.0, w[:, bi] * inv)
+        l[bi] = lpiv
+        d = np.where(used | (np.arange(s) == bi), d, d - l * l)
+        w -= np.outer(l, l)
+        used[bi] = True
+        lcols.append(l)
+        sel.append(bi)
+        pivots.append(prow)
+        margins.append((best - max(second, tau)) / best if best > 0 else 0.0)
+    b = len(sel)
+    mprime = np.zeros((s, b))
+    if b:
+        lsel = np.array([[lcols[t2][sel[t1]] if t2 <= t1 else 0.0 for t2 in range(b)] for t1 in range(b)])
+        x = np.zeros((b, b))
+        for j in range(b):
+            for i in range(j, b):
+                acc = (1.0 if i == j else 0.0) - float(np.dot(lsel[i, j:i], x[j:i, j]))
+                x[i, j] = acc / lsel[i, i] if lsel[i, i] != 0.0 else 0.0
+        for j in range(b):
+            mprime[sel[j], :] = x[:, j]
+    return b, pivots, mprime, margins
+
+
+# ---------------------------------------------------------------------------
+# the distributed build
+# ---------------------------------------------------------------------------
+
+@dataclass
+class RankState:
+    r0: int
+    r1: int
+    d: object = None       # residual diagonal of the panel (backend array)
+    L: object = None       # panel x steps factor (backend array)
+    theta: object = None   # panel x n_mu
+    pivots: list = field(default_factory=list)
+    margins: list = field(default_factory=list)
+
+
+class DistributedBuild:
+    """Stages 1-5 across the ranks of `comm` with per-rank `backend`."""
+
+    def __init__(self, comm, backend, dims, cell, n_v, n_c, k_mu=8.0, n_lambda=16, batch=64):
+        self.comm, self.be = comm, backend
+        self.dims, self.cell = tuple(dims), tuple(cell)
+        self.n_r = dims[0] * dims[1] * dims[2]
+        self.n_v, self.n_c = n_v, n_c
+        self.n_mu = min(max(int(math.floor(k_mu * math.sqrt(n_v * n_c) + 0.5)), 1), self.n_r)
+        self.n_lambda = n_lambda
+        self.batch = batch
+        r0, r1 = z_panels(dims, comm.world)[comm.rank]
+        self.st = RankState(r0, r1)
+
+    # ---- owner contributions: rows of a panel array at global row indices --
+    def _owned_rows(self, panel_rows_fn, rows, width):
+        out = np.zeros((len(rows), width))
+        for i, r in enumerate(rows):
+            if self.st.r0 <= r < self.st.r1:
+                out[i] = panel_rows_fn(r - self.st.r0)
+        return self.comm.allreduce_sum(out)
+
+    def select(self, phi_v_p, phi_c_p):
+        """Stage 1 over the local panels (rows [r0, r1) of Phi_v / Phi_c)."""
+        be, st = self.be, self.st
+        n_r, n1, n2 = self.n_r, self.n_v, self.n_c
+        steps = min(self.n_mu, n1 * n2, n_r)
+        s = max(1, min(self.batch, n_r))
+        pos = np.arange(n_r, dtype=np.int64)
+        perm = np.arange(n_r, dtype=np.int64)
+        st.d = be.init_diag(phi_v_p, phi_c_p)
+        st.L = be.zeros(st.r1 - st.r0, max(steps, 1))
+        k = 0
+        while k < steps:
+            se = min(s, n_r - k)
+            local = be.local_top(st.d, pos[st.r0:st.r1], st.r0, k, se + 1)
+            gathered = np.concatenate(self.comm.allgather(np.asarray(local, dtype=np.float64).reshape(-1, 3)))
+            top = merge_top([(e[0], int(e[1]), int(e[2])) for e in gathered], se + 1)
+            cand = [max(e[2], 0) for e in top[:se]]
+            amu = self._owned_rows(lambda i: be.row(phi_v_p, i), cand, n1)
+            bmu = self._owned_rows(lambda i: be.row(phi_c_p, i), cand, n2)
+            lc = self._owned_rows(lambda i: be.row(st.L, i)[:k], cand, k) if k else np.zeros((se, 0))
+            w_p = be.w_panel(phi_v_p, phi_c_p, amu, bmu, st.L, lc, k)
+            w_cc = self._owned_rows(lambda i: be.row(w_p, i), cand, se)
+            b, piv, mprime, margins = cand_greedy(top, w_cc, k, steps, pos, perm)
+            if b <= 0:
+                raise RuntimeError("distributed select: no progress")
+            be.l_update(w_p, mprime, st.L, k, b)
+            be.downdate(st.L, k, b, pos[st.r0:st.r1], st.d)
+            st.pivots += piv
+            st.margins += margins
+            k += b
+        self.pos, self.perm, self.steps = pos, perm, steps
+        return np.sort(perm[:self.n_mu]).astype(np.int32)
+
+    def fit(self, pts):
+        """Stage 2: Theta panel = L panel L_P^-1, columns in sorted-point order."""
+        be, st = self.be, self.st
+        if self.steps != self.n_mu:
+            raise NotImplementedError("distributed fit needs N_mu <= N_v N_c")
+        order = st.pivots
+        lp = self._owned_rows(lambda i: be.row(st.L, i)[:self.n_mu], order, self.n_mu)
+        lp = np.tril(lp)
+        x = be.tri_inverse(lp)
+        colmap = np.searchsorted(pts, np.asarray(order))
+        xs = np.zeros_like(x)
+        xs[:, colmap] = x
+        st.theta = be.theta_panel(st.L, xs)
+        return st.theta
+
+    def contour(self, pv, pc, energies):
+        """Stage 3: node-split quadrature + all-reduce (pv, pc replicated)."""
+        n_nodes = self.n_lambda + 1
+        k0, k1 = node_ranges(n_nodes, self.comm.world)[self.comm.rank]
+        part = self.be.contour_partial(pv, pc, energies, self.n_lambda, k0, k1 - k0)
+        acc = self.comm.allreduce_sum(part)
+        return self.be.contour_finish(acc, energies, self.n_v, self.n_c)
+
+    def pvp(self):
+        """Stages 4-5a: slab FFT + G-slab SYRK + all-reduce."""
+        n1, n2, n3 = self.dims
+        be, st = self.be, self.st
+        z0, z1 = st.r0 // (n1 * n2), st.r1 // (n1 * n2)
+        xh = be.rfft2_planes(st.theta, z1 - z0, n2, n1)          # (zl, n2, n1h, n_mu) complex
+        chunks = y_chunks(n2, self.comm.world)
+        blocks = [be.to_host(xh[:, a:b]) for (a, b) in chunks]
+        recv = self.comm.alltoall([np.ascontiguousarray(bl).view(np.float64) for bl in blocks])
+        ya, yb = chunks[self.comm.rank]
+        planes = [z1_ - z0_ for (z0_, z1_) in [(r0 // (n1 * n2), r1 // (n1 * n2))
+                                               for (r0, r1) in z_panels(self.dims, self.comm.world)]]
+        n1h = n1 // 2 + 1
+        parts = [recv[q].view(np.complex128).reshape(planes[q], yb - ya, n1h, self.n_mu) for q in range(self.comm.world)]
+        pencil = np.concatenate(parts, axis=0)                      # (n3, ny, n1h, n_mu)
+        ghat = be.fft_z(pencil)
+        part = be.pvp_slab(ghat, (ya, yb), self.dims, self.cell)
+        return self.comm.allreduce_sum(part)
+
+    def smw(self, t, pvp):
+        return self.be.smw_core(t, pvp)
+
+    def apply(self, k, x_p):
+        """eps^-1 x on the local panel rows: x_p + (V Theta (K Theta^T x))_p."""
+        be, st = self.be, self.st
+        u = self.comm.allreduce_sum(be.theta_t_x(st.theta, x_p))
+        z_p = be.theta_w(st.theta, k @ u)
+        z = np.concatenate(self.comm.allgather(be.to_host(z_p)))
+        vz = be.apply_coulomb(self.dims, self.cell, z)
+        return be.to_host(x_p) + vz[st.r0:st.r1]
