@@ -508,25 +508,31 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
   DBuf Wbuf[2] = {dalloc(c, (size_t)n_r * s), dalloc(c, (size_t)n_r * s)};
   DBuf amu = dalloc(c, (size_t)(s + 1) * n1), bmu = dalloc(c, (size_t)(s + 1) * n2);
   DBuf lcg = dalloc(c, (size_t)(s + 1) * std::max(steps, 1));
-  DBuf top(c, (size_t)(s + 1) * sizeof(HostEnt)), top2(c, (size_t)(s + 1) * sizeof(HostEnt));
+  // one device->host packet per block: {nb, k_next, pad, pad} then s+1 candidates
+  const size_t pkt_bytes = 16 + (size_t)(s + 1) * sizeof(HostEnt);
+  DBuf pkt(c, pkt_bytes);
+  int* bout = static_cast<int*>(pkt.p);
+  void* top = static_cast<char*>(pkt.p) + 16;
+  DBuf top2(c, (size_t)(s + 1) * sizeof(HostEnt));
   DBuf tmp(c, select_topk_tmp_bytes(n_r, s + 1));
   DBuf cand = ialloc(c, s), oldc = ialloc(c, s);
   DBuf lcand = dalloc(c, (size_t)s * s), mprime = dalloc(c, (size_t)s * s);
   DBuf order = ialloc(c, std::max(steps, 1)), margin = dalloc(c, std::max(steps, 1));
-  DBuf bout = ialloc(c, 1);
+  std::vector<char> hpkt(pkt_bytes);
+  const HostEnt* htop = reinterpret_cast<const HostEnt*>(hpkt.data() + 16);
 
   ck(select_init(c->stream, a, lda, n1, b, ldb, n2, n_r, d.d(), pos.i(), perm.i()), "select_init");
+  ck(select_topk(c->stream, d.d(), pos.i(), n_r, 0, s + 1, tmp.p, top), "select_topk");
+  download(c, hpkt.data(), pkt.p, pkt_bytes);
   // Candidate columns carried between blocks: a still-unaccepted candidate's
   // W column only needs the previous block's b new L columns subtracted.
   std::vector<int> col_of(n_r, -1);  // grid row -> column of the previous W
   std::vector<int> prev_rows;
-  std::vector<HostEnt> htop(s + 1), htop2(s + 1);
+  std::vector<HostEnt> htop2(s + 1);
   std::vector<int> hcand(s), hold(s);
   int k = 0, k_prev = 0, b_prev = 0, cur = 0;
   while (k < steps) {
     const int se = std::min(s, n_r - k);
-    ck(select_topk(c->stream, d.d(), pos.i(), n_r, k, se + 1, tmp.p, top.p), "select_topk");
-    download(c, htop.data(), top.p, sizeof(HostEnt) * (se + 1));
     // reorder: reused candidates first (their previous columns), new ones after
     int n_re = 0;
     for (int i = 0; i < se; ++i)
@@ -571,14 +577,19 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
       }
     }
     ck(select_cand_greedy(c->stream, n_r, se, steps, k, top2.p, Wn, pos.i(), perm.i(), lcand.d(), mprime.d(),
-                          order.i(), margin.d(), bout.i()),
+                          order.i(), margin.d(), bout),
        "cand_greedy");
-    int nb = 0;
-    download(c, &nb, bout.p, sizeof(int));
+    // L[:, k:k+nb] = W M' (M' = E L_sel^-T, s_e x nb), nb read on the device
+    const int nmax = std::min(se, steps - k);
+    ck(dgemm(c->stream, n_r, nmax, se, Wn, n_r, Lay::MN, mprime.d(), se, Lay::K, L.d() + (size_t)k * n_r, n_r, 1.0,
+             0.0, nullptr, false, c->sm_count, nullptr, 0, false, nullptr, bout),
+       "dgemm(L block)");
+    ck(select_downdate(c->stream, L.d(), n_r, k, 0, pos.i(), d.d(), bout), "downdate");
+    // next block's candidates (k_next read on the device), one sync per block
+    ck(select_topk(c->stream, d.d(), pos.i(), n_r, 0, s + 1, tmp.p, top, bout + 1), "select_topk");
+    download(c, hpkt.data(), pkt.p, pkt_bytes);
+    const int nb = reinterpret_cast<const int*>(hpkt.data())[0];
     if (nb <= 0) fail(LRGW_ERR_INTERNAL, "select: no progress (non-finite residuals?)");
-    // L[:, k:k+nb] = W M'   (M' = E L_sel^-T, s_e x nb)
-    gemm(c, n_r, nb, se, Wn, n_r, Lay::MN, mprime.d(), se, Lay::K, L.d() + (size_t)k * n_r, n_r, 1.0, 0.0);
-    ck(select_downdate(c->stream, L.d(), n_r, k, nb, pos.i(), d.d()), "downdate");
     k_prev = k;
     b_prev = nb;
     k += nb;

@@ -4,6 +4,7 @@
 #include <algorithm>
 
 #include "gemm.cuh"
+#include "gemm2.cuh"
 #include "kernels.h"
 
 namespace lrgw_dev {
@@ -50,7 +51,7 @@ cudaError_t launch_cfg(cudaStream_t st, const DgemmParams& p, int splits) {
     const int t = (p.M + Cfg::BM - 1) / Cfg::BM;
     grid = dim3(t * (t + 1) / 2, 1, splits);
   } else {
-    grid = dim3((p.M + Cfg::BM - 1) / Cfg::BM, (p.N + Cfg::BN - 1) / Cfg::BN, splits);
+    grid = dim3((p.N + Cfg::BN - 1) / Cfg::BN, (p.M + Cfg::BM - 1) / Cfg::BM, splits);
   }
   if (grid.x == 0 || grid.y == 0) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(dgemm_kernel<Cfg>,
@@ -157,6 +158,51 @@ __global__ void gather_cols_kernel(const double* src, long long lds, int rows, c
   }
 }
 
+// ---- v2 (paired-fragment) configurations ---------------------------------
+template <int V>
+using G2L = Gemm2Cfg<128, 128, 64, 32, 4, V, false>;
+template <int V>
+using G2W96 = Gemm2Cfg<128, 96, 32, 32, 4, V, false>;  // 12 warps (a multiple of 4 SMSPs)
+template <int V>
+using G2W64 = Gemm2Cfg<128, 64, 64, 32, 4, V, false>;
+template <int V>
+using G2W32 = Gemm2Cfg<128, 32, 32, 32, 4, V, false>;
+template <int V>
+using H2W64 = Gemm2Cfg<128, 64, 32, 32, 4, V, true>;
+template <int V>
+using H2W32 = Gemm2Cfg<128, 32, 32, 32, 4, V, true>;
+
+template <class Cfg>
+cudaError_t launch2(cudaStream_t st, const Dgemm2Params& p) {
+  dim3 grid((p.N + Cfg::BN - 1) / Cfg::BN, (p.M + Cfg::BM - 1) / Cfg::BM);
+  if (grid.x == 0 || grid.y == 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(dgemm2_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Cfg::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  dgemm2_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(p); count_launches(1);
+  return cudaGetLastError();
+}
+
+// Column tile width for an N-wide output: the narrowest padding, preferring wide.
+int v2_width(int N) {
+  if (N > 96) return 128;
+  if (N > 64) return 96;
+  if (N > 32) return 64;
+  return 32;
+}
+
+template <int V>
+cudaError_t dispatch2(cudaStream_t st, const Dgemm2Params& p, bool had) {
+  int w = v2_width(p.N);
+  if (had) return w <= 32 ? launch2<H2W32<V>>(st, p) : launch2<H2W64<V>>(st, p);
+  switch (w) {
+    case 32: return launch2<G2W32<V>>(st, p);
+    case 64: return launch2<G2W64<V>>(st, p);
+    case 96: return launch2<G2W96<V>>(st, p);
+    default: return launch2<G2L<V>>(st, p);
+  }
+}
+
 }  // namespace
 
 cudaError_t gather_cols(cudaStream_t st, const double* src, long long lds, int rows, const int* cols, int n,
@@ -169,7 +215,7 @@ cudaError_t gather_cols(cudaStream_t st, const double* src, long long lds, int r
 cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long long lda, Lay la,
                   const double* B, long long ldb, Lay lb, double* C, long long ldc, double alpha,
                   double beta, const double* scale, bool lower, int sm_count, double* work,
-                  size_t work_elems, bool tri_b, const int* colmap) {
+                  size_t work_elems, bool tri_b, const int* colmap, const int* n_dev) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   DgemmParams p{};
   p.M = M;
@@ -187,7 +233,8 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
   p.lower = lower ? 1 : 0;
   p.tri_b = tri_b ? 1 : 0;
   p.colmap = colmap;
-  if ((tri_b || colmap) && (lower || work)) return cudaErrorInvalidValue;
+  p.n_dev = n_dev;
+  if ((tri_b || colmap || n_dev) && (lower || work)) return cudaErrorInvalidValue;
   const bool ak = la == Lay::K, bk = lb == Lay::K;
   // 16-byte cp.async needs aligned bases, even leading dims and even extents
   // along the contiguous axis.
@@ -238,6 +285,25 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
     p.partial = work;
     p.part_stride = (long long)M * N;
   }
+  // v2 (paired fragments) wins for full-width tiles; narrow outputs stay on v1
+  if (!ak && !bk && !lower && !scale && splits <= 1 && N >= 128 && tile == Tile::L) {
+    Dgemm2Params q{};
+    q.M = M;
+    q.N = N;
+    q.K = K;
+    q.A = A;
+    q.lda = lda;
+    q.B = B;
+    q.ldb = ldb;
+    q.C = C;
+    q.ldc = ldc;
+    q.alpha = alpha;
+    q.beta = beta;
+    q.tri_b = tri_b ? 1 : 0;
+    q.colmap = colmap;
+    q.n_dev = n_dev;
+    return (va && vb) ? dispatch2<2>(st, q, false) : dispatch2<1>(st, q, false);
+  }
   cudaError_t e;
   if (!ak && !bk) e = launch_layout<false, false>(st, p, tile, va, vb, splits);
   else if (!ak && bk) e = launch_layout<false, true>(st, p, tile, va, vb, splits);
@@ -256,20 +322,39 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
   if (M <= 0 || N <= 0) return cudaSuccess;
   HadamardParams p{M, N, k1, k2, a1, b1, a2, b2, lda1, ldb1, lda2, ldb2, C, ldc, alpha, beta};
   const bool vec = aligned16(a1) && aligned16(b1) && aligned16(a2) && aligned16(b2) &&
-                   lda1 % 2 == 0 && ldb1 % 2 == 0 && lda2 % 2 == 0 && ldb2 % 2 == 0 &&
-                   (M % 2 == 0 || (lda1 > M && lda2 > M)) && (N % 2 == 0 || (ldb1 > N && ldb2 > N));
+             lda1 % 2 == 0 && ldb1 % 2 == 0 && lda2 % 2 == 0 && ldb2 % 2 == 0 &&
+             (M % 2 == 0 || (lda1 > M && lda2 > M)) && (N % 2 == 0 || (ldb1 > N && ldb2 > N));
   auto go = [&](auto cfg) -> cudaError_t {
     using Cfg = decltype(cfg);
-    dim3 grid((M + Cfg::BM - 1) / Cfg::BM, (N + Cfg::BN - 1) / Cfg::BN);
-    cudaError_t e = cudaFuncSetAttribute(hadamard_kernel<Cfg>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    dim3 grid((N + Cfg::BN - 1) / Cfg::BN, (M + Cfg::BM - 1) / Cfg::BM);
+    auto kern = hadamard_kernel<Cfg>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    hadamard_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(p); count_launches(1);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(p); count_launches(1);
     return cudaGetLastError();
   };
-  if (prefer_narrow(N)) return vec ? go(CfgH32<2>{}) : go(CfgH32<1>{});
-  if (vec) return go(CfgH<2>{});
-  return go(CfgH<1>{});
+  if (N < 128) {
+    if (prefer_narrow(N)) return vec ? go(CfgH32<2>{}) : go(CfgH32<1>{});
+    return vec ? go(CfgH<2>{}) : go(CfgH<1>{});
+  }
+  Dgemm2Params q{};
+  q.M = M;
+  q.N = N;
+  q.K = k1;
+  q.K2 = k2;
+  q.A = a1;
+  q.lda = lda1;
+  q.B = b1;
+  q.ldb = ldb1;
+  q.A2 = a2;
+  q.lda2 = lda2;
+  q.B2 = b2;
+  q.ldb2 = ldb2;
+  q.C = C;
+  q.ldc = ldc;
+  q.alpha = alpha;
+  q.beta = beta;
+  return vec ? dispatch2<2>(st, q, true) : dispatch2<1>(st, q, true);
 }
 
 cudaError_t mirror_lower(cudaStream_t st, double* a, int n, long long lda, bool average) {

@@ -34,6 +34,7 @@ struct DgemmParams {
   long long part_stride;
   int tri_b;             // B(n, k) == 0 for k < n (lower-triangular operand): K starts at n0
   const int* colmap;     // output column n is written to column colmap[n] of C
+  const int* n_dev;      // if set: N = min(N, *n_dev), read on the device (no host sync)
 };
 
 // Tile loader for one operand. ROWS = BM or BN.
@@ -101,10 +102,17 @@ __global__ void __launch_bounds__(Cfg::THREADS) dgemm_kernel(DgemmParams p) {
   if (p.lower) {
     lower_tile(blockIdx.x, tm, tn);
   } else {
-    tm = blockIdx.x;
-    tn = blockIdx.y;
+    // N tiles fastest: the CTAs sharing an A row panel run together, so A is
+    // read from HBM once (then L2) instead of once per N tile
+    tn = blockIdx.x;
+    tm = blockIdx.y;
   }
   const int m0 = tm * BM, n0 = tn * BN;
+  if (p.n_dev) {
+    const int nd = *p.n_dev;
+    if (nd < p.N) p.N = nd;
+    if (n0 >= p.N) return;
+  }
   const int kb = p.k_chunk > 0 ? blockIdx.z * p.k_chunk : (p.tri_b ? (n0 / BK) * BK : 0);
   const int ke = p.k_chunk > 0 ? min(p.K, kb + p.k_chunk) : p.K;
   const int nkt = ke > kb ? (ke - kb + BK - 1) / BK : 0;
@@ -233,8 +241,9 @@ __global__ void __launch_bounds__(Cfg::THREADS) hadamard_kernel(HadamardParams p
   constexpr int FM = Cfg::FM, FN = Cfg::FN;
   using LA = typename Cfg::LA;
   using LB = typename Cfg::LB;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const int kt1 = (p.K1 + BK - 1) / BK, kt2 = (p.K2 + BK - 1) / BK, nkt = kt1 + kt2;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;  // N tiles fastest (A panel reuse in L2)
+  const int kt1 = (p.K1 + BK - 1) / BK, kt2 = (p.K2 + BK - 1) / BK;
+  const int nkt = kt1 + kt2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp % Cfg::WARPS_M) * Cfg::WM, wn = (warp / Cfg::WARPS_M) * Cfg::WN;
   const int g = lane >> 2, t = lane & 3;
@@ -248,13 +257,13 @@ __global__ void __launch_bounds__(Cfg::THREADS) hadamard_kernel(HadamardParams p
   auto issue = [&](int kt) {
     double* sa = smem + (kt % STAGES) * Cfg::STAGE_ELEMS;
     double* sb = sa + LA::ELEMS;
-    if (kt < kt1) {
-      LA::load(sa, p.A1, p.lda1, m0, p.M, kt * BK, p.K1, tid);
-      LB::load(sb, p.B1, p.ldb1, n0, p.N, kt * BK, p.K1, tid);
-    } else {
-      LA::load(sa, p.A2, p.lda2, m0, p.M, (kt - kt1) * BK, p.K2, tid);
-      LB::load(sb, p.B2, p.ldb2, n0, p.N, (kt - kt1) * BK, p.K2, tid);
-    }
+    // pick the phase's operands first so one load sequence serves both phases
+    const double *a = p.A1, *b = p.B1;
+    long long lda = p.lda1, ldb = p.ldb1;
+    int k0 = kt * BK, kend = p.K1;
+    if (kt >= kt1) a = p.A2, b = p.B2, lda = p.lda2, ldb = p.ldb2, k0 = (kt - kt1) * BK, kend = p.K2;
+    LA::load(sa, a, lda, m0, p.M, k0, kend, tid);
+    LB::load(sb, b, ldb, n0, p.N, k0, kend, tid);
   };
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {

@@ -93,8 +93,9 @@ __device__ void bitonic_desc(Ent* e, int n) {
 
 __device__ __forceinline__ Ent ent_none() { return Ent{-DBL_MAX, INT_MAX, -1}; }
 
-__global__ void topk_pass1_kernel(const double* d, const int* pos, int n_r, int k, int s, Ent* out) {
+__global__ void topk_pass1_kernel(const double* d, const int* pos, int n_r, int k, const int* k_dev, int s, Ent* out) {
   __shared__ Ent e[TOPK_CHUNK];
+  if (k_dev) k = *k_dev;
   const int base = blockIdx.x * TOPK_CHUNK;
   for (int i = threadIdx.x; i < TOPK_CHUNK; i += blockDim.x) {
     const int r = base + i;
@@ -324,7 +325,10 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
       __syncthreads();
     }
   }
-  if (tid == 0) *p.b_out = b;
+  if (tid == 0) {
+    p.b_out[0] = b;
+    p.b_out[1] = p.kb + b;  // next block start, consumed on the device
+  }
 }
 
 __global__ void cand_rows_kernel(const Ent* top, int n, int* rows) {
@@ -332,7 +336,8 @@ __global__ void cand_rows_kernel(const Ent* top, int n, int* rows) {
 }
 
 // d[r] -= sum_t L[r, kb + t]^2 for the rows still unselected.
-__global__ void downdate_kernel(const double* L, int n_r, int kb, int b, const int* pos, double* d) {
+__global__ void downdate_kernel(const double* L, int n_r, int kb, int b, const int* b_dev, const int* pos, double* d) {
+  if (b_dev) b = *b_dev;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_r; r += gridDim.x * blockDim.x) {
     if (pos[r] < kb + b) continue;
     double v = d[r];
@@ -360,11 +365,11 @@ cudaError_t select_init(cudaStream_t st, const double* a, long long lda, int n1,
 }
 
 cudaError_t select_topk(cudaStream_t st, const double* d, const int* pos, int n_r, int k, int s1, void* tmp,
-                        void* out) {
+                        void* out, const int* k_dev) {
   Ent* t = static_cast<Ent*>(tmp);
   const int n = (n_r + TOPK_CHUNK - 1) / TOPK_CHUNK;
   const size_t half = (size_t)n * s1;
-  topk_pass1_kernel<<<n, 1024, 0, st>>>(d, pos, n_r, k, s1, t); count_launches(1);
+  topk_pass1_kernel<<<n, 1024, 0, st>>>(d, pos, n_r, k, k_dev, s1, t); count_launches(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int n_in = n * s1, src = 0;
@@ -400,9 +405,10 @@ cudaError_t select_cand_rows(cudaStream_t st, const void* top, int n, int* rows)
   return cudaGetLastError();
 }
 
-cudaError_t select_downdate(cudaStream_t st, const double* L, int n_r, int kb, int b, const int* pos, double* d) {
-  if (b <= 0) return cudaSuccess;
-  downdate_kernel<<<592, 256, 0, st>>>(L, n_r, kb, b, pos, d); count_launches(1);
+cudaError_t select_downdate(cudaStream_t st, const double* L, int n_r, int kb, int b, const int* pos, double* d,
+                            const int* b_dev) {
+  if (b <= 0 && !b_dev) return cudaSuccess;
+  downdate_kernel<<<592, 256, 0, st>>>(L, n_r, kb, b, b_dev, pos, d); count_launches(1);
   return cudaGetLastError();
 }
 

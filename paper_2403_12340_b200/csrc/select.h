@@ -14,7 +14,7 @@ cudaError_t select_init(cudaStream_t st, const double* a, long long lda, int n1,
 size_t select_ent_bytes();
 size_t select_topk_tmp_bytes(int n_r, int s1);
 cudaError_t select_topk(cudaStream_t st, const double* d, const int* pos, int n_r, int k, int s1, void* tmp,
-                        void* out);
+                        void* out, const int* k_dev = nullptr);
 cudaError_t select_cand_rows(cudaStream_t st, const void* top, int n, int* rows);
 int select_max_candidates();
 size_t select_cand_smem_bytes(int s);
@@ -24,6 +24,7 @@ cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int k
                                int* pos, int* perm, double* lc, double* mprime, int* piv_order, double* margin,
                                int* b_out);
 // d -= rowsum(L[:, kb:kb+b]^2) over unselected rows.
-cudaError_t select_downdate(cudaStream_t st, const double* L, int n_r, int kb, int b, const int* pos, double* d);
+cudaError_t select_downdate(cudaStream_t st, const double* L, int n_r, int kb, int b, const int* pos, double* d,
+                            const int* b_dev = nullptr);
 
 }  // namespace lrgw_dev

@@ -42,6 +42,7 @@ def main():
               flush=True)
 
     run("theta-like", "N", "N", 110592, 1024, 1024)
+    run("theta-like v2", "N", "T", 110592, 1024, 1024)
     run("pvp-like (full)", "T", "N", 1024, 1024, 115200)
     run("lpass-96", "N", "T", 110592, 96, 512)
     run("lpass-64", "N", "T", 110592, 64, 512)
@@ -50,6 +51,9 @@ def main():
     run("probe Theta w", "N", "N", 110592, 8, 1024)
     run("square 1024", "N", "N", 1024, 1024, 1024)
     run("square 8192", "N", "N", 8192, 8192, 8192, reps=2)
+    run("square 8192 v2", "N", "T", 8192, 8192, 8192, reps=2)
+    run("lpass-80 v2", "N", "T", 110592, 80, 700)
+    run("lpass-32 v2", "N", "T", 110592, 30, 300)
 
 
 if __name__ == "__main__":

@@ -70,6 +70,66 @@ __global__ void dmma16_loop(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+
+// GEMM-like operand pattern: FM x FN accumulator tiles, distinct A/B fragment
+// registers per MMA (as in a warp tile), optionally i-major or j-major order.
+template <int FM, int FN, bool JMAJOR>
+__global__ void dmma_tile_loop(double* out, int iters) {
+  const int lane = threadIdx.x & 31;
+  double af[FM], bf[FN], acc[FM][FN][2];
+#pragma unroll
+  for (int i = 0; i < FM; ++i) af[i] = 1.0 + (lane + i) * 1e-6;
+#pragma unroll
+  for (int j = 0; j < FN; ++j) bf[j] = 1.0 - (lane + j) * 1e-6;
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    if (JMAJOR) {
+#pragma unroll
+      for (int j = 0; j < FN; ++j)
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[i][j][0]), "+d"(acc[i][j][1]) : "d"(af[i]), "d"(bf[j]));
+    } else {
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[i][j][0]), "+d"(acc[i][j][1]) : "d"(af[i]), "d"(bf[j]));
+    }
+  }
+  double sum = 0;
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) sum += acc[i][j][0] + acc[i][j][1];
+  if (sum == 12345.678) out[0] = sum;
+}
+
+template <int FM, int FN, bool JM>
+void run_tile(double* d, int sms, int wpb, int bps) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 4000;
+  int blocks = sms * bps, threads = 32 * wpb;
+  dmma_tile_loop<FM, FN, JM><<<blocks, threads>>>(d, 10);
+  cudaDeviceSynchronize();
+  cudaEventRecord(e0);
+  dmma_tile_loop<FM, FN, JM><<<blocks, threads>>>(d, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  double fl = 2.0 * 256 * FM * FN * (double)iters * blocks * wpb;
+  printf("DMMA tile %dx%d %s warps/blk=%2d blk/SM=%d : %8.2f TFLOP/s\n", FM * 8, FN * 8, JM ? "j-major" : "i-major",
+         wpb, bps, fl / ms / 1e9);
+}
+
 int main() {
   double* d;
   CK(cudaMalloc(&d, 64));
@@ -122,5 +182,13 @@ int main() {
       printf("DMMA16816 warps/blk=%2d blk/SM=%d : %8.2f TFLOP/s (%.3f ms)\n", wpb, bps, fl / ms / 1e9, ms);
     }
   }
+  run_tile<4, 4, false>(d, sms, 8, 2);
+  run_tile<4, 4, true>(d, sms, 8, 2);
+  run_tile<4, 4, false>(d, sms, 4, 2);
+  run_tile<4, 4, false>(d, sms, 16, 1);
+  run_tile<8, 4, false>(d, sms, 8, 1);
+  run_tile<4, 2, false>(d, sms, 8, 1);
+  run_tile<4, 2, false>(d, sms, 8, 2);
+  run_tile<2, 2, false>(d, sms, 8, 2);
   return 0;
 }
