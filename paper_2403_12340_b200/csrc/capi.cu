@@ -14,6 +14,8 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -71,6 +73,16 @@ struct lrgw_ctx_s {
   bool timing = false;  // record stage events (lrgw_build only)
   long long launches0 = 0;
   int select_batch = 128;
+  // Device-memory cache of this context: freed blocks are kept (by size) and
+  // handed out again to later requests on the context's stream. A build
+  // repeats the same sizes every call, so from the second call on no
+  // allocation reaches the driver (cudaMallocAsync pools fragment under the
+  // 0.1-1 GB blocks of a build and then grow or trim, stalling the host for
+  // milliseconds).
+  std::mutex mem_mu;
+  std::multimap<size_t, void*> mem_free;
+  std::unordered_map<void*, size_t> mem_live;
+  size_t mem_cached = 0;
 };
 
 struct lrgw_eps_s {
@@ -87,14 +99,65 @@ struct lrgw_eps_s {
 
 namespace {
 
-// Device buffer from the stream-ordered pool (freed on scope exit).
+void release_cached(lrgw_ctx c) {  // caller holds mem_mu
+  if (c->mem_free.empty()) return;
+  cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->mem_free) cudaFree(kv.second);
+  c->mem_free.clear();
+  c->mem_cached = 0;
+}
+
+// Stream-ordered allocation from the context cache: a cached block of at least
+// the (rounded) size and at most 1/4 larger is reused; otherwise the driver
+// allocates, after dropping the cache if memory is short.
+void* ctx_alloc(lrgw_ctx c, size_t bytes) {
+  const size_t gran = bytes < (1u << 20) ? 512 : (2u << 20);
+  const size_t want = (bytes + gran - 1) / gran * gran;
+  std::lock_guard<std::mutex> lk(c->mem_mu);
+  auto it = c->mem_free.lower_bound(want);
+  if (it != c->mem_free.end() && it->first <= want + want / 4) {
+    void* p = it->second;
+    c->mem_live[p] = it->first;
+    c->mem_cached -= it->first;
+    c->mem_free.erase(it);
+    return p;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, want);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    release_cached(c);
+    e = cudaMalloc(&p, want);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(LRGW_ERR_CUDA, std::string("device allocation of ") + std::to_string(bytes) + " bytes: " +
+                            cudaGetErrorString(e));
+  }
+  c->mem_live[p] = want;
+  return p;
+}
+
+// Return a block to the cache. Work already queued on the context stream may
+// still use it; every later user is ordered behind that work on the same stream.
+void ctx_free(lrgw_ctx c, void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(c->mem_mu);
+  auto it = c->mem_live.find(p);
+  if (it == c->mem_live.end()) return;
+  c->mem_free.emplace(it->second, p);
+  c->mem_cached += it->second;
+  c->mem_live.erase(it);
+}
+
+// Device buffer from the context cache (returned on scope exit).
 struct DBuf {
   lrgw_ctx ctx = nullptr;
   void* p = nullptr;
   size_t bytes = 0;
   DBuf() = default;
   DBuf(lrgw_ctx c, size_t b) : ctx(c), bytes(b) {
-    if (b) ck(cudaMallocAsync(&p, b, c->stream), "cudaMallocAsync");
+    if (b) p = ctx_alloc(c, b);
   }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
@@ -109,7 +172,7 @@ struct DBuf {
   }
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFreeAsync(p, ctx->stream);
+    if (p) ctx_free(ctx, p);
     p = nullptr;
   }
   double* d() const { return static_cast<double*>(p); }
@@ -485,6 +548,11 @@ struct HostEnt {
 
 // keep (optional): the pivoted-Cholesky factor L (n_r x steps, pivot order)
 // and the pivot sequence, reused by the fused fit of lrgw_build.
+bool select_trace() {
+  static const bool on = getenv("LRGW_SELECT_TRACE") != nullptr;
+  return on;
+}
+
 struct SelectKeep {
   DBuf L;
   std::vector<int> order;
@@ -549,6 +617,8 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
     prev_rows.assign(hcand.begin(), hcand.begin() + se);
     for (int i = 0; i < se; ++i)
       if (htop2[i].row >= 0) col_of[htop2[i].row] = i;
+    if (select_trace())
+      fprintf(stderr, "select block k=%d se=%d n_re=%d n_new=%d b_prev=%d\n", k, se, n_re, n_new, b_prev);
     ck(cudaMemcpyAsync(top2.p, htop2.data(), sizeof(HostEnt) * (se + 1), cudaMemcpyHostToDevice, c->stream), "H2D");
     ck(cudaMemcpyAsync(cand.p, hcand.data(), sizeof(int) * se, cudaMemcpyHostToDevice, c->stream), "H2D");
     double* Wn = Wbuf[cur].d();
@@ -842,11 +912,6 @@ int lrgw_ctx_create(int device, lrgw_ctx* out) {
   }
   cusolverDnSetStream(c->solver, c->stream);
   // keep freed pool memory cached across calls (stream-ordered allocator)
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
   c->launches0 = launch_count();
   *out = c;
   return LRGW_OK;
@@ -856,6 +921,10 @@ int lrgw_ctx_destroy(lrgw_ctx c) {
   if (!c) return LRGW_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  {
+    std::lock_guard<std::mutex> lk(c->mem_mu);
+    release_cached(c);
+  }
   for (auto& kv : c->plans) cufftDestroy(kv.second);
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -1216,9 +1285,9 @@ int lrgw_eps_destroy(lrgw_eps e) {
   if (!e) return LRGW_OK;
   cudaSetDevice(e->ctx->device);
   cudaStreamSynchronize(e->ctx->stream);
-  cudaFree(e->theta);
-  cudaFree(e->k);
-  cudaFree(e->t);
+  ctx_free(e->ctx, e->theta);
+  ctx_free(e->ctx, e->k);
+  ctx_free(e->ctx, e->t);
   delete e;
   return LRGW_OK;
 }
