@@ -647,7 +647,7 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
       }
     }
     ck(select_cand_greedy(c->stream, n_r, se, steps, k, top2.p, Wn, pos.i(), perm.i(), lcand.d(), mprime.d(),
-                          order.i(), margin.d(), bout),
+                          order.i(), min_margin ? margin.d() : nullptr, bout),
        "cand_greedy");
     // L[:, k:k+nb] = W M' (M' = E L_sel^-T, s_e x nb), nb read on the device
     const int nmax = std::min(se, steps - k);

@@ -253,6 +253,12 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
     const long long t = (M + 63) / 64;
     tiles = t * (t + 1) / 2;
     occ = 2;
+  } else if (n_dev && (long long)((M + 127) / 128) >= 2LL * sm_count) {
+    // device-side N bound (the selection's L block): 32-wide column tiles so
+    // the CTAs past the live columns exit at once
+    tile = Tile::N;
+    tiles = (long long)((M + 127) / 128) * ((N + 31) / 32);
+    occ = 2;
   } else if (N > 64 && N <= 128 && (long long)((M + 127) / 128) >= 2LL * sm_count) {
     // one column tile of width 96 or 128 (A streamed once)
     tile = N <= 96 ? Tile::W96 : Tile::W128;

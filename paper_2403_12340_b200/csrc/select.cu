@@ -25,6 +25,8 @@
 // Block lengths are ~60-80% of s; the pivot sequence is that of the plain
 // greedy (the tests check it bit-exactly against the reference).
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -121,211 +123,318 @@ __global__ void topk_merge_kernel(const Ent* in, int n_in, int s, Ent* out) {
 constexpr int CG_THREADS = 512;
 constexpr int CG_WARPS = CG_THREADS / 32;
 constexpr int CG_ROWS = 128 / CG_WARPS;  // candidate rows per warp
+constexpr int CG_MAX = 128;              // candidates
 
 struct CandParams {
   int n_r, s, steps, kb;
   const Ent* top;       // s + 1 entries: candidates then the tau entry
-  const double* W;      // n_r x s
+  const double* wcc;    // s x s: W[C, C], row-major (wcc[j + i s] = W(row_i, j))
   int* pos;             // grid row -> position
   int* perm;            // position -> grid row
-  double* lc;           // s x s: l vectors of the accepted steps (column t)
   double* mprime;       // s x s: E L_sel^-T (rows of unselected candidates zero)
   int* piv_order;       // [steps]
-  double* margin;       // [steps]
+  double* margin;       // [steps] or nullptr
   int* b_out;           // number of accepted steps
 };
 
-// Register-resident candidate block: warp w owns candidate rows
-// i = CG_ROWS w + r (r < CG_ROWS) and lane l holds their columns l, l+32, l+64,
-// l+96 (s <= 128); lane r additionally carries row r's residual and position.
-// Per accepted pivot: post per-warp best (lanes 0..CG_ROWS-1), barrier, every
-// warp reduces the CG_WARPS partials redundantly and the owner publishes the
-// pivot row, barrier, every warp applies the rank-1 elimination in registers.
-__device__ __forceinline__ void argmax_xor(double& v, double& sv, int& i, int& p, int off) {
-  const double v2 = __shfl_xor_sync(0xffffffffu, v, off);
-  const double s2 = __shfl_xor_sync(0xffffffffu, sv, off);
-  const int i2 = __shfl_xor_sync(0xffffffffu, i, off);
-  const int p2 = __shfl_xor_sync(0xffffffffu, p, off);
-  if (better(v2, p2, v, p)) {
-    sv = fmax(fmax(sv, s2), v);
-    v = v2;
-    p = p2;
-    i = i2;
-  } else {
-    sv = fmax(fmax(sv, s2), v2);
+// wcc[j + i s] = W[row_i, j]: the candidates' Schur block, gathered once by
+// many CTAs so the greedy CTA reads it coalesced.
+__global__ void gather_cc_kernel(const double* W, int n_r, int s, const Ent* top, double* wcc) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= s * s) return;
+  const int i = idx / s, j = idx % s;
+  const int g = top[i].row;
+  wcc[idx] = g >= 0 ? W[g + (long long)j * n_r] : 0.0;
+}
+
+__device__ __forceinline__ double pick8(const double (&x)[CG_ROWS], int r) {
+  double v = x[0];
+#pragma unroll
+  for (int q = 1; q < CG_ROWS; ++q) v = (r == q) ? x[q] : v;
+  return v;
+}
+
+// Pivot of the next step, published by the controller warp.
+struct CandPivot {
+  double v0, rinv;  // residual of the pivot and 1 / v0
+  int i0, ok;
+};
+
+// Order-preserving 64-bit key of a double (larger value -> larger key).
+__device__ __forceinline__ unsigned long long dkey(double v) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// Controller-warp argmax over the unused candidates (lane l: entries l + 32 c)
+// by (d desc, position asc) — the reference's strict '>' scan — with three
+// warp reductions (key high word, low word, position). sv (largest other
+// residual) only when margins are requested.
+__device__ __forceinline__ void cand_argmax(const double (&dj)[4], const int (&pj)[4], unsigned usedl, int lane,
+                                            bool want_sv, double& v0, int& p0, int& i0, double& sv) {
+  // usedl: bit c = entry lane + 32 c is taken / absent
+  unsigned long long bk = 0;
+  int bp = INT_MAX, bc = -1;
+  double bv = -DBL_MAX;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const unsigned long long k = dkey(dj[c]);
+    const bool take = !((usedl >> c) & 1u) && (bc < 0 || k > bk || (k == bk && pj[c] < bp));
+    bk = take ? k : bk;
+    bp = take ? pj[c] : bp;
+    bv = take ? dj[c] : bv;
+    bc = take ? c : bc;
+  }
+  const unsigned khi = bc >= 0 ? static_cast<unsigned>(bk >> 32) : 0u;
+  const unsigned hi = __reduce_max_sync(0xffffffffu, khi);
+  const unsigned lo = __reduce_max_sync(0xffffffffu, (bc >= 0 && khi == hi) ? static_cast<unsigned>(bk) : 0u);
+  const bool top = bc >= 0 && bk == ((static_cast<unsigned long long>(hi) << 32) | lo);
+  const int pm = static_cast<int>(__reduce_min_sync(0xffffffffu, top ? static_cast<unsigned>(bp) : 0x7fffffffu));
+  const unsigned win = __ballot_sync(0xffffffffu, top && bp == pm);
+  const int wl = win ? __ffs(win) - 1 : 0;
+  const int wc = __shfl_sync(0xffffffffu, bc, wl);
+  v0 = win ? __shfl_sync(0xffffffffu, bv, wl) : -DBL_MAX;
+  i0 = win ? wl + 32 * wc : -1;
+  p0 = pm;
+  sv = -DBL_MAX;
+  if (want_sv) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (!((usedl >> c) & 1u) && lane + 32 * c != i0) sv = fmax(sv, dj[c]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sv = fmax(sv, __shfl_xor_sync(0xffffffffu, sv, off));
   }
 }
 
+// X = L_sel^-1 for the b accepted steps (b <= 128) and M' = E X^T, after the
+// greedy loop, in 32 x 32 blocks:
+//   L_sel[i][m] = lcs[m][sel[i]] is first packed to `lsel` (lower, packed);
+//   X (dense 128 x 128, reusing the lcs space; rows/cols >= b are identity);
+//   the diagonal blocks are inverted by one warp each (lane = column,
+//   unrolled forward substitution with reciprocal pivots), then block row I
+//   takes X_Ik = -X_II sum_{m=k}^{I-1} L_Im X_mk (k < I) — all threads.
+__device__ void cand_tri_inverse(double* lcs, double* lsel, const int* sel, int b, int s, double* mprime) {
+  __shared__ double rdiag[CG_MAX];
+  double* X = lcs;
+  auto L = [&](int i, int m) -> double {  // L_sel (identity beyond b)
+    if (i >= b || m >= b) return i == m ? 1.0 : 0.0;
+    return m <= i ? lsel[i * (i + 1) / 2 + m] : 0.0;
+  };
+  for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
+    const int i = idx / b, m = idx % b;
+    if (m <= i) lsel[i * (i + 1) / 2 + m] = lcs[m * CG_MAX + sel[i]];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < CG_MAX; i += blockDim.x) {
+    const double d = L(i, i);
+    rdiag[i] = d != 0.0 ? 1.0 / d : 0.0;
+  }
+  for (int idx = threadIdx.x; idx < CG_MAX * CG_MAX; idx += blockDim.x) X[idx] = 0.0;
+  __syncthreads();
+  const int nb = (b + 31) / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // diagonal blocks: warp I inverts block I (lane j: column 32 I + j)
+  if (wid < nb) {
+    const int o = 32 * wid;
+    double x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      double acc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+      for (int m = 0; m < i; ++m) acc = fma(-L(o + i, o + m), x[m], acc);
+      x[i] = (i >= lane) ? acc * rdiag[o + i] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) X[(o + i) * CG_MAX + o + lane] = x[i];
+  }
+  __syncthreads();
+  __shared__ double P[3 * 32 * 32];
+  for (int I = 1; I < nb; ++I) {
+    // P_k = sum_{m=32k}^{32I-1} L[32I + i][m] X[m][32k + j], k < I
+    for (int idx = threadIdx.x; idx < I * 1024; idx += blockDim.x) {
+      const int k = idx / 1024, i = (idx / 32) % 32, j = idx % 32;
+      double acc = 0.0;
+      for (int m = 32 * k + j; m < 32 * I; ++m) acc = fma(L(32 * I + i, m), X[m * CG_MAX + 32 * k + j], acc);
+      P[idx] = acc;
+    }
+    __syncthreads();
+    // X_Ik = -X_II P_k
+    for (int idx = threadIdx.x; idx < I * 1024; idx += blockDim.x) {
+      const int k = idx / 1024, i = (idx / 32) % 32, j = idx % 32;
+      double acc = 0.0;
+      for (int q = 0; q <= i; ++q) acc = fma(X[(32 * I + i) * CG_MAX + 32 * I + q], P[k * 1024 + q * 32 + j], acc);
+      X[(32 * I + i) * CG_MAX + 32 * k + j] = -acc;
+    }
+    __syncthreads();
+  }
+  // M'[sel[j]][i] = X[i][j] (i >= j); the rows of unselected candidates stay 0
+  for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
+    const int i = idx / b, j = idx % b;
+    if (j <= i) mprime[sel[j] + (size_t)i * s] = X[i * CG_MAX + j];
+  }
+}
+
+// Register-resident candidate block W[C, C]: warp w owns the rows
+// i = CG_ROWS w + r (lane l: columns l + 32 c, c < 4). Warp 0 is also the
+// controller: it alone carries the residual diagonal, positions, grid rows and
+// position slots of the candidates and picks each pivot. Per step t:
+//   (after barrier B) every warp reads the published pivot; the owner warp
+//      of row i0 publishes that row r (double-buffered);
+//   barrier A;
+//   controller: d_j -= r_j^2 / d_i0, next argmax, publish — the critical
+//      path — then its own rows and the position bookkeeping;
+//   other warps: w -= r_i (r_j / d_i0) on their rows; warp 1 records
+//      l = r / sqrt(d_i0) (row t of the step history); warps 1.. extend
+//      X = L_sel^-1 by row t (forward substitution, 4 lanes per column), so
+//      M' = E X^T is complete when the loop ends;
+//   barrier B.
 __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p) {
   extern __shared__ __align__(16) double sm[];
-  const int s = p.s, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  double* rowbuf = sm;                             // 128: published pivot row
-  int* usedv = reinterpret_cast<int*>(rowbuf + 128);  // 128 flags
-  int* rowid = usedv + 128;                        // 128 grid rows
-  int* sel = rowid + 128;                          // 128: candidate index per accepted step
-  int* pslot = sel + 128;                          // 128: perm[kb .. kb + s)
-  __shared__ double part_v[CG_WARPS], part_s[CG_WARPS];
-  __shared__ int part_i[CG_WARPS], part_p[CG_WARPS];
-  __shared__ double s_tau;
+  const int s = p.s, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool ctl = wid == 0;
+  double* rowbuf = sm;                              // 2 x 128: published pivot rows
+  double* lcs = rowbuf + 2 * CG_MAX;                // [t][j]: l of candidate j at step t; later X
+  double* lsel = lcs + CG_MAX * CG_MAX;             // packed lower L_sel (after the loop)
+  int* sel = reinterpret_cast<int*>(lsel + CG_MAX * (CG_MAX + 1) / 2);  // candidate of step t
+  __shared__ CandPivot piv[2];
+  __shared__ int rjs[CG_MAX];  // controller: candidate grid rows
+  __shared__ int pss[CG_MAX];  // controller: perm[kb + j] (position slots of the block)
+  __shared__ unsigned usedsh[4];  // candidates taken / absent before this step (bit l of word c: l + 32 c)
 
-  for (int i = tid; i < 128; i += blockDim.x) {
-    const Ent e = i < s ? p.top[i] : ent_none();
-    rowid[i] = e.row;
-    usedv[i] = e.row < 0 ? 1 : 0;
-    pslot[i] = (i < s && p.kb + i < p.n_r) ? p.perm[p.kb + i] : -1;
-  }
-  if (tid == 0) s_tau = p.top[s].row >= 0 ? p.top[s].v : -DBL_MAX;
-  __syncthreads();
-  const double tau = s_tau;
+  for (int idx = threadIdx.x; idx < s * s; idx += blockDim.x) p.mprime[idx] = 0.0;
+
+  const double tau = p.top[s].row >= 0 ? p.top[s].v : -DBL_MAX;
   const int tmax = min(s, p.steps - p.kb);
+  const bool want_sv = p.margin != nullptr;
+
+  // controller state (warp 0), entries j = lane + 32 c
+  double dj[4];
+  int pj[4];
+  unsigned usedl = 0;  // bit c: entry lane + 32 c taken / absent
+  double sv = -DBL_MAX;
+  int ppos = 0;
+  if (ctl) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = lane + 32 * c;
+      const Ent e = j < s ? p.top[j] : ent_none();
+      dj[c] = e.row >= 0 ? e.v : -DBL_MAX;
+      pj[c] = e.row >= 0 ? e.pos : INT_MAX;
+      rjs[j] = e.row;
+      pss[j] = (j < s && p.kb + j < p.n_r) ? p.perm[p.kb + j] : -1;
+      usedl |= (e.row < 0 ? 1u : 0u) << c;
+      const unsigned m = __ballot_sync(0xffffffffu, e.row < 0);
+      if (lane == 0) usedsh[c] = m;
+    }
+    double v0;
+    int i0;
+    cand_argmax(dj, pj, usedl, lane, want_sv, v0, ppos, i0, sv);
+    // the first step of a block is the exact argmax (C is sorted by the pivot rule)
+    if (lane == 0) piv[0] = CandPivot{v0, v0 > 0.0 ? 1.0 / v0 : 0.0, i0, (0 < tmax && i0 >= 0) ? 1 : 0};
+  }
 
   const int base = CG_ROWS * wid;
   double w[CG_ROWS][4];
 #pragma unroll
   for (int r = 0; r < CG_ROWS; ++r) {
-    const int g = rowid[base + r];
+    const int i = base + r;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int j = lane + 32 * c;
-      w[r][c] = (g >= 0 && j < s) ? p.W[g + (long long)j * p.n_r] : 0.0;
+      w[r][c] = (i < s && j < s) ? p.wcc[j + (size_t)i * s] : 0.0;
     }
   }
-  // lane r < CG_ROWS: metadata of row base + r
-  const int my_i = base + (lane < CG_ROWS ? lane : 0);
-  double my_d = -DBL_MAX;
-  int my_pos = INT_MAX;
-  if (lane < CG_ROWS && my_i < s && rowid[my_i] >= 0) {
-    my_d = p.top[my_i].v;
-    my_pos = p.top[my_i].pos;
-  }
+  __syncthreads();
 
   int t = 0;
   for (;; ++t) {
-    // ---- post this warp's best unused row ----
-    double bv = -DBL_MAX, sv = -DBL_MAX;
-    int bi = -1, bp = INT_MAX;
-    if (lane < CG_ROWS && !usedv[my_i]) {
-      bv = my_d;
-      bp = my_pos;
-      bi = my_i;
-    }
-#pragma unroll
-    for (int off = CG_ROWS / 2; off > 0; off >>= 1) argmax_xor(bv, sv, bi, bp, off);
-    if (lane == 0) {
-      part_v[wid] = bv;
-      part_s[wid] = sv;
-      part_i[wid] = bi;
-      part_p[wid] = bp;
-    }
-    __syncthreads();
-    // ---- every warp reduces the partials ----
-    double v0 = -DBL_MAX, s0 = -DBL_MAX;
-    int i0 = -1, p0 = INT_MAX;
-    if (lane < CG_WARPS) {
-      v0 = part_v[lane];
-      s0 = part_s[lane];
-      i0 = part_i[lane];
-      p0 = part_p[lane];
-    }
-#pragma unroll
-    for (int off = CG_WARPS / 2; off > 0; off >>= 1) argmax_xor(v0, s0, i0, p0, off);
-    v0 = __shfl_sync(0xffffffffu, v0, 0);
-    s0 = __shfl_sync(0xffffffffu, s0, 0);
-    i0 = __shfl_sync(0xffffffffu, i0, 0);
-    p0 = __shfl_sync(0xffffffffu, p0, 0);
-    // certified iff it beats every non-candidate (<= tau); the first step of
-    // the block is the exact argmax (C is sorted by the pivot rule)
-    const bool ok = t < tmax && i0 >= 0 && (t == 0 || v0 > tau);
-    if (!ok) break;  // uniform across the CTA
-    const int k = p.kb + t;
-    const int ppos = p0;       // pivot's position before the swap
-    const int occ = pslot[t];  // perm[k] before the swap (linalg.hpp:48-53)
+    const CandPivot pv = piv[t & 1];
+    if (!pv.ok) break;  // uniform
+    const int i0 = pv.i0;
+    double* rb = rowbuf + (t & 1) * CG_MAX;
     if (wid == i0 / CG_ROWS) {
       const int r0 = i0 % CG_ROWS;
 #pragma unroll
-      for (int r = 0; r < CG_ROWS; ++r)
-        if (r == r0)
+      for (int c = 0; c < 4; ++c) {
+        double x[CG_ROWS];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) rowbuf[lane + 32 * c] = w[r][c];
+        for (int r = 0; r < CG_ROWS; ++r) x[r] = w[r][c];
+        rb[lane + 32 * c] = pick8(x, r0);
+      }
     }
     __syncthreads();
-    // ---- eliminate the pivot from the register block ----
-    const double inv = v0 > 0.0 ? 1.0 / sqrt(v0) : 0.0;
-    const double lpiv = v0 > 0.0 ? sqrt(v0) : 0.0;
-    double lj[4];
+    if (ctl) {
+      // ---- critical path: downdate d, pick and publish the next pivot ----
+      const int k = p.kb + t;
+      const int occ = pss[t];  // perm[k] before the swap
+      const int piv_pos = ppos;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int j = lane + 32 * c;
-      lj[c] = (j == i0) ? lpiv : rowbuf[j] * inv;
-    }
-    double my_l = 0.0;
-#pragma unroll
-    for (int r = 0; r < CG_ROWS; ++r) {
-      const int i = base + r;
-      const double li = (i == i0) ? lpiv : (usedv[i] ? 0.0 : rowbuf[i] * inv);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) w[r][c] = fma(-li, lj[c], w[r][c]);
-      if (lane == r) my_l = li;
-    }
-    if (lane < CG_ROWS && my_i < s) {
-      p.lc[my_i + (size_t)t * s] = my_l;
-      if (my_i == i0) {
-        usedv[my_i] = 1;
-        my_pos = k;
-      } else {
-        if (!usedv[my_i]) my_d = fma(-my_l, my_l, my_d);
-        if (rowid[my_i] == occ) my_pos = ppos;
+      for (int c = 0; c < 4; ++c) {
+        const int j = lane + 32 * c;
+        const double r = rb[j];
+        const bool live = !((usedl >> c) & 1u) && j != i0;
+        dj[c] = live ? fma(-r, r * pv.rinv, dj[c]) : dj[c];
+        pj[c] = (j == i0) ? k : ((rjs[j] == occ) ? piv_pos : pj[c]);
+      }
+      usedl |= (lane == (i0 & 31) ? 1u : 0u) << (i0 >> 5);
+      const double svp = sv;
+      double v1;
+      int i1;
+      cand_argmax(dj, pj, usedl, lane, want_sv, v1, ppos, i1, sv);
+      if (lane == 0)
+        piv[(t + 1) & 1] = CandPivot{v1, v1 > 0.0 ? 1.0 / v1 : 0.0, i1,
+                                     (t + 1 < tmax && i1 >= 0 && v1 > tau) ? 1 : 0};
+      if (lane == 0) {
+        const int gp = rjs[i0];  // pivot grid row
+        p.perm[k] = gp;
+        p.perm[piv_pos] = occ;
+        p.pos[gp] = k;
+        p.pos[occ] = piv_pos;
+        sel[t] = i0;
+        // position slots: perm[ppos] = occ, then perm[k] = gp
+        if (piv_pos - p.kb < CG_MAX) pss[piv_pos - p.kb] = occ;
+        pss[t] = gp;
+        p.piv_order[k] = gp;
+        usedsh[i0 >> 5] |= 1u << (i0 & 31);  // only bit i0 changes: workers exclude it already
+        if (want_sv) p.margin[k] = pv.v0 > 0.0 ? (pv.v0 - fmax(svp, tau)) / pv.v0 : 0.0;
       }
     }
-    if (tid == 0) {
-      const int gp = rowid[i0];
-      p.perm[k] = gp;
-      p.perm[ppos] = occ;
-      p.pos[gp] = k;
-      p.pos[occ] = ppos;
-      if (ppos - p.kb < s) pslot[ppos - p.kb] = occ;
-      pslot[t] = gp;
-      sel[t] = i0;
-      p.piv_order[k] = gp;
-      if (p.margin) p.margin[k] = v0 > 0.0 ? (v0 - fmax(s0, tau)) / v0 : 0.0;
+    // ---- eliminate: w -= r_i r_j / d_i0 (row / column i0 are never read
+    // again; rows already taken only see round-off-sized entries) ----
+    {
+      const unsigned um = (usedsh[base >> 5] >> (base & 31)) | (i0 / CG_ROWS == wid ? 1u << (i0 % CG_ROWS) : 0u);
+      if ((um & ((1u << CG_ROWS) - 1)) != (1u << CG_ROWS) - 1) {
+        double gj[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int j = lane + 32 * c;
+          gj[c] = (j == i0) ? 0.0 : rb[j] * pv.rinv;
+        }
+#pragma unroll
+        for (int r = 0; r < CG_ROWS; ++r) {
+          if ((um >> r) & 1u) continue;  // taken rows are never read again (warp-uniform)
+          const double ri = rb[base + r];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) w[r][c] = fma(-ri, gj[c], w[r][c]);
+        }
+      }
     }
-    // usedv / pslot / sel are next read after the next step's first barrier
+    if (wid == 1) {
+      // step history: l_j = r_j / sqrt(d_i0), l_i0 = sqrt(d_i0) (entries of
+      // rows already taken are never read: L_sel only reads rows sel[t'], t' > t)
+      const double lpiv = pv.v0 > 0.0 ? sqrt(pv.v0) : 0.0;
+      const double inv = lpiv > 0.0 ? 1.0 / lpiv : 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = lane + 32 * c;
+        lcs[t * CG_MAX + j] = (j == i0) ? lpiv : rb[j] * inv;
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const int b = t;
-  // M' = E L_sel^-T. L_sel[t1][t2] = lc[sel[t1] + t2 s] is lower triangular in
-  // pivot order: pack it into shared memory and invert row by row
-  // (X[i][:] = (e_i - sum_{m<i} L[i][m] X[m][:]) / L[i][i], columns in parallel).
-  double* lp = reinterpret_cast<double*>(pslot + 128);  // b (b + 1) / 2, packed lower
-  double* xp = lp + (size_t)b * (b + 1) / 2;              // b (b + 1) / 2
-  for (int idx = tid; idx < b * b; idx += blockDim.x) {
-    const int i = idx / b, m = idx % b;
-    if (m <= i) lp[(size_t)i * (i + 1) / 2 + m] = p.lc[sel[i] + (size_t)m * s];
-  }
-  for (int idx = tid; idx < s * b; idx += blockDim.x) p.mprime[idx] = 0.0;
-  __syncthreads();
-  {
-    // G = CG_THREADS / 128 threads per column j (128 >= s columns), m-sum
-    // split across them and reduced with shuffles inside the group.
-    constexpr int G = CG_THREADS / 128;
-    const int j = tid / G, q = tid % G;
-    for (int i = 0; i < b; ++i) {
-      const double* li = lp + (size_t)i * (i + 1) / 2;
-      double acc = 0.0;
-      if (j <= i)
-        for (int m = j + q; m < i; m += G) acc = fma(li[m], xp[(size_t)m * (m + 1) / 2 + j], acc);
-#pragma unroll
-      for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-      if (j <= i && q == 0) {
-        const double lii = li[i];
-        const double x = lii != 0.0 ? (((i == j) ? 1.0 : 0.0) - acc) / lii : 0.0;
-        xp[(size_t)i * (i + 1) / 2 + j] = x;
-        p.mprime[sel[j] + (size_t)i * s] = x;  // (L_sel^-T)[j][i] = X[i][j]
-      }
-      __syncthreads();
-    }
-  }
-  if (tid == 0) {
+  cand_tri_inverse(lcs, lsel, sel, b, s, p.mprime);
+  if (threadIdx.x == 0) {
     p.b_out[0] = b;
     p.b_out[1] = p.kb + b;  // next block start, consumed on the device
   }
@@ -385,14 +494,18 @@ cudaError_t select_topk(cudaStream_t st, const double* d, const int* pos, int n_
   }
 }
 
-size_t select_cand_smem_bytes(int s) { return 128 * 8 + 4 * 128 * 4 + (size_t)s * (s + 1) * 8 + 64; }
+size_t select_cand_smem_bytes(int) {
+  return (2 * CG_MAX + CG_MAX * CG_MAX + CG_MAX * (CG_MAX + 1) / 2) * sizeof(double) + CG_MAX * sizeof(int) + 16;
+}
 
-int select_max_candidates() { return 128; }
+int select_max_candidates() { return CG_MAX; }
 
 cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* W,
-                               int* pos, int* perm, double* lc, double* mprime, int* piv_order, double* margin,
+                               int* pos, int* perm, double* scratch, double* mprime, int* piv_order, double* margin,
                                int* b_out) {
-  CandParams p{n_r, s, steps, kb, static_cast<const Ent*>(top), W, pos, perm, lc, mprime, piv_order, margin, b_out};
+  const Ent* tp = static_cast<const Ent*>(top);
+  gather_cc_kernel<<<(s * s + 255) / 256, 256, 0, st>>>(W, n_r, s, tp, scratch); count_launches(1);
+  CandParams p{n_r, s, steps, kb, tp, scratch, pos, perm, mprime, piv_order, margin, b_out};
   const size_t smem = select_cand_smem_bytes(s);
   cudaError_t e = cudaFuncSetAttribute(cand_greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

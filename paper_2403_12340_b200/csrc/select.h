@@ -19,9 +19,10 @@ cudaError_t select_cand_rows(cudaStream_t st, const void* top, int n, int* rows)
 int select_max_candidates();
 size_t select_cand_smem_bytes(int s);
 // Certified greedy on the s candidates (one CTA): accepted steps -> *b_out,
-// pivots, margins, positions; mprime (s x b) = E L_sel^-T.
+// pivots, margins (if margin != nullptr), positions; mprime (s x b) = E L_sel^-T.
+// scratch: s x s doubles (the gathered candidate block).
 cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* W,
-                               int* pos, int* perm, double* lc, double* mprime, int* piv_order, double* margin,
+                               int* pos, int* perm, double* scratch, double* mprime, int* piv_order, double* margin,
                                int* b_out);
 // d -= rowsum(L[:, kb:kb+b]^2) over unselected rows.
 cudaError_t select_downdate(cudaStream_t st, const double* L, int n_r, int kb, int b, const int* pos, double* d,
