@@ -194,6 +194,12 @@ int lrgw_dev_dgemm(lrgw_ctx ctx, char trans_a, char trans_b, int m, int n, int k
                    const double* a, long long lda, const double* b, long long ldb, double beta,
                    double* c, long long ldc);
 
+/* Top s1 rows by (d desc, position asc) among rows with pos[r] >= k — the
+ * candidate set of one selection block (device arrays; host outputs, rows of
+ * missing entries are -1). Exposed for tests. */
+int lrgw_dev_select_topk(lrgw_ctx ctx, const double* d, const int32_t* pos, int n_r, int k, int s1,
+                         int32_t* rows_host, double* vals_host, int32_t* pos_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -590,6 +590,7 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
   const HostEnt* htop = reinterpret_cast<const HostEnt*>(hpkt.data() + 16);
 
   ck(select_init(c->stream, a, lda, n1, b, ldb, n2, n_r, d.d(), pos.i(), perm.i()), "select_init");
+  ck(select_topk_reset(c->stream, tmp.p), "select_topk_reset");
   ck(select_topk(c->stream, d.d(), pos.i(), n_r, 0, s + 1, tmp.p, top), "select_topk");
   download(c, hpkt.data(), pkt.p, pkt_bytes);
   // Candidate columns carried between blocks: a still-unaccepted candidate's
@@ -1496,6 +1497,24 @@ int lrgw_dev_dgemm(lrgw_ctx c, char ta, char tb, int m, int n, int k, double alp
     gemm(c, m, n, k, a, lda, at ? Lay::K : Lay::MN, b, ldb, bt ? Lay::MN : Lay::K, cm, ldc, alpha, beta, nullptr,
          false, &w);
     ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int lrgw_dev_select_topk(lrgw_ctx c, const double* d, const int32_t* pos, int n_r, int k, int s1, int32_t* rows,
+                         double* vals, int32_t* poss) {
+  return guarded(c, [&] {
+    if (n_r < 1 || s1 < 1 || s1 > select_max_candidates() + 1) fail(LRGW_ERR_INVALID_INPUT, "select_topk: bad sizes");
+    DBuf tmp(c, select_topk_tmp_bytes(n_r, s1));
+    DBuf out(c, (size_t)s1 * sizeof(HostEnt));
+    ck(select_topk_reset(c->stream, tmp.p), "select_topk_reset");
+    ck(select_topk(c->stream, d, pos, n_r, k, s1, tmp.p, out.p), "select_topk");
+    std::vector<HostEnt> h(s1);
+    download(c, h.data(), out.p, sizeof(HostEnt) * s1);
+    for (int i = 0; i < s1; ++i) {
+      if (rows) rows[i] = h[i].row;
+      if (vals) vals[i] = h[i].v;
+      if (poss) poss[i] = h[i].pos;
+    }
   });
 }
 

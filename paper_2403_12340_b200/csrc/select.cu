@@ -24,6 +24,7 @@
 //      L[:, k0:k0+b] = W L_sel^-T, and d -= rowsum(L_blk^2).
 // Block lengths are ~60-80% of s; the pivot sequence is that of the plain
 // greedy (the tests check it bit-exactly against the reference).
+#include <algorithm>
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
@@ -42,8 +43,13 @@ __device__ __forceinline__ bool better(double v1, int p1, double v2, int p2) {
   return v1 > v2 || (v1 == v2 && p1 < p2);
 }
 
-// l of the pivot itself: sqrt(d_piv) = 1 / inv (0 for an exhausted pivot).
-__device__ __forceinline__ double s_bv_sqrt(double inv) { return inv > 0.0 ? 1.0 / inv : 0.0; }
+// Order-preserving 64-bit key of a double (larger value -> larger key; NaN
+// lowest, so a NaN residual is never picked).
+__device__ __forceinline__ unsigned long long dkey(double v) {
+  if (v != v) return 0ull;
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
 
 __global__ void init_diag_kernel(const double* a, long long lda, int n1, const double* b,
                                  long long ldb, int n2, int n_r, double* d, int* pos, int* perm) {
@@ -63,60 +69,231 @@ __global__ void init_diag_kernel(const double* a, long long lda, int n1, const d
   }
 }
 
-// ---- top-(s+1) by (d desc, position asc): per-CTA bitonic + merge passes ----
-constexpr int TOPK_CHUNK = 2048;
-
+// ---- top-(s+1) by (d desc, position asc): histogram select ------------------
+// Four passes over the residuals (each a few microseconds at N_r ~ 1e5):
+//   max:     the largest eligible key (eligible: position >= k);
+//   hist:    4096 log-spaced bins below the max (17 leading bits of the key:
+//            sign, exponent and 5 mantissa bits, ~3% wide);
+//   compact: every CTA finds the boundary bin b* (first bin where the
+//            cumulative count reaches s1); rows of bins < b* are in for sure,
+//            rows of bin b* go to a boundary list;
+//   final:   one CTA ranks the boundary rows by (d desc, position asc),
+//            keeps the best s1 - |sure|, sorts the s1 winners and resets the
+//            scratch for the next call. A boundary bin beyond BCAP rows
+//            (massive exact ties) is merged in chunks by the same CTA.
 struct Ent {
   double v;
   int pos, row;
 };
 
 __device__ __forceinline__ bool ent_better(const Ent& a, const Ent& b) { return better(a.v, a.pos, b.v, b.pos); }
-
-__device__ void bitonic_desc(Ent* e, int n) {
-  for (int size = 2; size <= n; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      __syncthreads();
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int j = i ^ stride;
-        if (j > i) {
-          const Ent a = e[i], b = e[j];
-          const bool desc = ((i & size) == 0);
-          if (desc ? ent_better(b, a) : ent_better(a, b)) {
-            e[i] = b;
-            e[j] = a;
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-}
-
 __device__ __forceinline__ Ent ent_none() { return Ent{-DBL_MAX, INT_MAX, -1}; }
 
-__global__ void topk_pass1_kernel(const double* d, const int* pos, int n_r, int k, const int* k_dev, int s, Ent* out) {
-  __shared__ Ent e[TOPK_CHUNK];
-  if (k_dev) k = *k_dev;
-  const int base = blockIdx.x * TOPK_CHUNK;
-  for (int i = threadIdx.x; i < TOPK_CHUNK; i += blockDim.x) {
-    const int r = base + i;
-    const int pr = r < n_r ? pos[r] : -1;
-    e[i] = (r < n_r && pr >= k) ? Ent{d[r], pr, r} : ent_none();
-  }
-  bitonic_desc(e, TOPK_CHUNK);
-  for (int i = threadIdx.x; i < s; i += blockDim.x) out[blockIdx.x * s + i] = e[i];
+constexpr int TK_BINS = 4096;
+constexpr int TK_BCAP = 4096;  // boundary rows ranked in one go
+constexpr int TK_SCAP = 256;   // >= s1
+
+struct TopkScratch {
+  unsigned long long maxkey;
+  unsigned sure_cnt, bnd_cnt;
+  unsigned hist[TK_BINS];
+  Ent sure[TK_SCAP];
+  Ent bnd[TK_BCAP];
+};
+
+__device__ __forceinline__ int tk_bin(unsigned long long key, unsigned ref) {
+  const long long b = static_cast<long long>(ref) - static_cast<long long>(key >> 47);
+  return b < 0 ? 0 : (b >= TK_BINS ? TK_BINS - 1 : static_cast<int>(b));
 }
 
-__global__ void topk_merge_kernel(const Ent* in, int n_in, int s, Ent* out) {
-  __shared__ Ent e[TOPK_CHUNK];
-  const int base = blockIdx.x * TOPK_CHUNK;
-  for (int i = threadIdx.x; i < TOPK_CHUNK; i += blockDim.x) {
-    const int r = base + i;
-    e[i] = r < n_in ? in[r] : ent_none();
+__global__ void topk_max_kernel(const double* d, const int* pos, int n_r, int k, const int* k_dev, TopkScratch* sc) {
+  if (k_dev) k = *k_dev;
+  unsigned long long m = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_r; r += gridDim.x * blockDim.x)
+    if (pos[r] >= k) m = max(m, dkey(d[r]));
+  // warp max of the 64-bit key: high words, then the low words of the lanes holding the top high word
+  const unsigned hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(m >> 32));
+  const unsigned lo = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(m >> 32) == hi ? static_cast<unsigned>(m) : 0u);
+  if ((threadIdx.x & 31) == 0) atomicMax(&sc->maxkey, (static_cast<unsigned long long>(hi) << 32) | lo);
+}
+
+__global__ void topk_hist_kernel(const double* d, const int* pos, int n_r, int k, const int* k_dev, TopkScratch* sc) {
+  __shared__ unsigned h[TK_BINS];
+  if (k_dev) k = *k_dev;
+  for (int i = threadIdx.x; i < TK_BINS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const unsigned ref = static_cast<unsigned>(sc->maxkey >> 47);
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_r; r += gridDim.x * blockDim.x)
+    if (pos[r] >= k) atomicAdd(&h[tk_bin(dkey(d[r]), ref)], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < TK_BINS; i += blockDim.x)
+    if (h[i]) atomicAdd(&sc->hist[i], h[i]);
+}
+
+// First bin whose cumulative count reaches s1 (TK_BINS if the total is smaller).
+__device__ int tk_boundary(const unsigned* hist, int s1) {
+  __shared__ unsigned part[32];
+  __shared__ int bstar;
+  constexpr int PER = TK_BINS / 256;  // blockDim.x == 256
+  const int tid = threadIdx.x;
+  unsigned loc[PER], sum = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    loc[q] = hist[tid * PER + q];
+    sum += loc[q];
   }
-  bitonic_desc(e, TOPK_CHUNK);
-  for (int i = threadIdx.x; i < s; i += blockDim.x) out[blockIdx.x * s + i] = e[i];
+  // inclusive scan of the per-thread sums
+  unsigned x = sum;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, off);
+    if ((tid & 31) >= off) x += y;
+  }
+  if ((tid & 31) == 31) part[tid >> 5] = x;
+  if (tid == 0) bstar = TK_BINS;
+  __syncthreads();
+  unsigned before = 0;
+  for (int w = 0; w < (tid >> 5); ++w) before += part[w];
+  unsigned cum = before + x - sum;  // exclusive prefix of this thread's bins
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    if (cum < static_cast<unsigned>(s1) && cum + loc[q] >= static_cast<unsigned>(s1)) bstar = tid * PER + q;
+    cum += loc[q];
+  }
+  __syncthreads();
+  return bstar;
+}
+
+__global__ void __launch_bounds__(256) topk_compact_kernel(const double* d, const int* pos, int n_r, int k,
+                                                           const int* k_dev, int s1, TopkScratch* sc) {
+  if (k_dev) k = *k_dev;
+  const int bstar = tk_boundary(sc->hist, s1);
+  const unsigned ref = static_cast<unsigned>(sc->maxkey >> 47);
+  const int lane = threadIdx.x & 31;
+  const int n_it = (n_r + gridDim.x * blockDim.x - 1) / (gridDim.x * blockDim.x);
+  for (int it = 0; it < n_it; ++it) {
+    const int r = (it * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+    int bin = TK_BINS;
+    double v = 0.0;
+    int pr = 0;
+    if (r < n_r) {
+      pr = pos[r];
+      if (pr >= k) {
+        v = d[r];
+        bin = tk_bin(dkey(v), ref);
+      }
+    }
+    const bool sure = bin < bstar, bnd = bin == bstar && bin < TK_BINS;  // (TK_BINS: not eligible)
+    const unsigned ms = __ballot_sync(0xffffffffu, sure), mb = __ballot_sync(0xffffffffu, bnd);
+    unsigned bs = 0, bb = 0;
+    if (lane == 0) {
+      if (ms) bs = atomicAdd(&sc->sure_cnt, __popc(ms));
+      if (mb) bb = atomicAdd(&sc->bnd_cnt, __popc(mb));
+    }
+    bs = __shfl_sync(0xffffffffu, bs, 0);
+    bb = __shfl_sync(0xffffffffu, bb, 0);
+    const unsigned below = (1u << lane) - 1u;
+    if (sure) {
+      const unsigned idx = bs + __popc(ms & below);
+      if (idx < TK_SCAP) sc->sure[idx] = Ent{v, pr, r};
+    }
+    if (bnd) {
+      const unsigned idx = bb + __popc(mb & below);
+      if (idx < TK_BCAP) sc->bnd[idx] = Ent{v, pr, r};
+    }
+  }
+}
+
+// One CTA (TK_FINAL threads): rank, sort, write `out` (s1 entries), reset.
+constexpr int TK_FINAL = 1024;
+__global__ void __launch_bounds__(TK_FINAL) topk_final_kernel(const double* d, const int* pos, int n_r, int k,
+                                                              const int* k_dev, int s1, TopkScratch* sc, Ent* out) {
+  extern __shared__ __align__(16) unsigned char tk_smem[];
+  Ent* cand = reinterpret_cast<Ent*>(tk_smem);  // up to TK_SCAP + TK_BCAP
+  __shared__ Ent win[TK_SCAP];
+  __shared__ int nwin_s;
+  if (k_dev) k = *k_dev;
+  const int tid = threadIdx.x;
+  const int c0 = min(static_cast<int>(sc->sure_cnt), s1);
+  const int nb = static_cast<int>(sc->bnd_cnt);
+  const int need = min(s1 - c0, nb);
+  for (int i = tid; i < c0; i += blockDim.x) win[i] = sc->sure[i];
+  if (nb <= TK_BCAP) {
+    for (int i = tid; i < nb; i += blockDim.x) cand[i] = sc->bnd[i];
+    __syncthreads();
+    for (int i = tid; i < nb; i += blockDim.x) {
+      const Ent e = cand[i];
+      int rank = 0;
+      for (int q = 0; q < nb; ++q) rank += ent_better(cand[q], e) ? 1 : 0;
+      if (rank < need) win[c0 + rank] = e;
+    }
+  } else {
+    // massive ties in the boundary bin: stream its rows in grid order, chunk
+    // by chunk (block-wide compaction), keeping the best `need` rows
+    __shared__ int wsum[TK_FINAL / 32];
+    __shared__ Ent keep[TK_SCAP];
+    const unsigned ref = static_cast<unsigned>(sc->maxkey >> 47);
+    const int bb = tk_bin(dkey(sc->bnd[0].v), ref);  // the boundary bin
+    const int lane = tid & 31, wid = tid >> 5;
+    int kept = 0;
+    for (int r0 = 0; r0 < n_r;) {
+      int fill = 0;
+      for (; r0 < n_r && fill + TK_FINAL <= TK_BCAP; r0 += TK_FINAL) {
+        const int r = r0 + tid;
+        bool f = false;
+        Ent e{};
+        if (r < n_r) {
+          const int pr = pos[r];
+          if (pr >= k) {
+            const double v = d[r];
+            f = tk_bin(dkey(v), ref) == bb;
+            e = Ent{v, pr, r};
+          }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) wsum[wid] = __popc(m);
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int w = 0; w < TK_FINAL / 32; ++w) {
+          before += (w < wid) ? wsum[w] : 0;
+          total += wsum[w];
+        }
+        if (f) cand[kept + fill + before + __popc(m & ((1u << lane) - 1u))] = e;
+        fill += total;
+        __syncthreads();
+      }
+      const int m = kept + fill;
+      for (int i = tid; i < m; i += blockDim.x) {
+        const Ent e = cand[i];
+        int rank = 0;
+        for (int q = 0; q < m; ++q) rank += ent_better(cand[q], e) ? 1 : 0;
+        if (rank < need) keep[rank] = e;
+      }
+      __syncthreads();
+      kept = min(need, m);
+      for (int i = tid; i < kept; i += blockDim.x) cand[i] = keep[i];
+      __syncthreads();
+    }
+    for (int i = tid; i < need; i += blockDim.x) win[c0 + i] = cand[i];
+  }
+  if (tid == 0) nwin_s = c0 + need;
+  __syncthreads();
+  // sort the winners by rank and pad
+  const int nw = nwin_s;
+  for (int i = tid; i < nw; i += blockDim.x) {
+    const Ent e = win[i];
+    int rank = 0;
+    for (int q = 0; q < nw; ++q) rank += ent_better(win[q], e) ? 1 : 0;
+    out[rank] = e;
+  }
+  for (int i = nw + tid; i < s1; i += blockDim.x) out[i] = ent_none();
+  // reset the scratch for the next call
+  for (int i = tid; i < TK_BINS; i += blockDim.x) sc->hist[i] = 0;
+  if (tid == 0) {
+    sc->maxkey = 0;
+    sc->sure_cnt = 0;
+    sc->bnd_cnt = 0;
+  }
 }
 
 // ---- the certified candidate greedy (one CTA) -------------------------------
@@ -159,12 +336,6 @@ struct CandPivot {
   double v0, rinv;  // residual of the pivot and 1 / v0
   int i0, ok;
 };
-
-// Order-preserving 64-bit key of a double (larger value -> larger key).
-__device__ __forceinline__ unsigned long long dkey(double v) {
-  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
-  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-}
 
 // Controller-warp argmax over the unused candidates (lane l: entries l + 32 c)
 // by (d desc, position asc) — the reference's strict '>' scan — with three
@@ -461,9 +632,7 @@ __global__ void downdate_kernel(const double* L, int n_r, int kb, int b, const i
 
 }  // namespace
 
-size_t select_topk_tmp_bytes(int n_r, int s1) {
-  return 2 * (size_t)((n_r + TOPK_CHUNK - 1) / TOPK_CHUNK) * s1 * sizeof(Ent) + 64;
-}
+size_t select_topk_tmp_bytes(int, int) { return sizeof(TopkScratch) + 64; }
 
 size_t select_ent_bytes() { return sizeof(Ent); }
 
@@ -473,25 +642,24 @@ cudaError_t select_init(cudaStream_t st, const double* a, long long lda, int n1,
   return cudaGetLastError();
 }
 
+cudaError_t select_topk_reset(cudaStream_t st, void* tmp) {
+  return cudaMemsetAsync(tmp, 0, sizeof(TopkScratch), st);
+}
+
 cudaError_t select_topk(cudaStream_t st, const double* d, const int* pos, int n_r, int k, int s1, void* tmp,
                         void* out, const int* k_dev) {
-  Ent* t = static_cast<Ent*>(tmp);
-  const int n = (n_r + TOPK_CHUNK - 1) / TOPK_CHUNK;
-  const size_t half = (size_t)n * s1;
-  topk_pass1_kernel<<<n, 1024, 0, st>>>(d, pos, n_r, k, k_dev, s1, t); count_launches(1);
-  cudaError_t e = cudaGetLastError();
+  if (s1 > TK_SCAP) return cudaErrorInvalidValue;
+  TopkScratch* sc = static_cast<TopkScratch*>(tmp);
+  const int grid = std::max(1, std::min(296, (n_r + 255) / 256));
+  topk_max_kernel<<<grid, 256, 0, st>>>(d, pos, n_r, k, k_dev, sc); count_launches(1);
+  topk_hist_kernel<<<grid, 256, 0, st>>>(d, pos, n_r, k, k_dev, sc); count_launches(1);
+  topk_compact_kernel<<<grid, 256, 0, st>>>(d, pos, n_r, k, k_dev, s1, sc); count_launches(1);
+  const size_t smem = (TK_SCAP + TK_BCAP) * sizeof(Ent);
+  cudaError_t e = cudaFuncSetAttribute(topk_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  int n_in = n * s1, src = 0;
-  while (true) {
-    const int chunks = (n_in + TOPK_CHUNK - 1) / TOPK_CHUNK;
-    Ent* from = t + src * half;
-    Ent* to = chunks == 1 ? static_cast<Ent*>(out) : t + (1 - src) * half;
-    topk_merge_kernel<<<chunks, 1024, 0, st>>>(from, n_in, s1, to); count_launches(1);
-    e = cudaGetLastError();
-    if (e != cudaSuccess || chunks == 1) return e;
-    n_in = chunks * s1;
-    src = 1 - src;
-  }
+  topk_final_kernel<<<1, TK_FINAL, smem, st>>>(d, pos, n_r, k, k_dev, s1, sc, static_cast<Ent*>(out));
+  count_launches(1);
+  return cudaGetLastError();
 }
 
 size_t select_cand_smem_bytes(int) {

@@ -13,6 +13,8 @@ cudaError_t select_init(cudaStream_t st, const double* a, long long lda, int n1,
 // (s1 opaque entries of select_ent_bytes()); missing entries have row -1.
 size_t select_ent_bytes();
 size_t select_topk_tmp_bytes(int n_r, int s1);
+// tmp must be zeroed once before the first select_topk (each call leaves it zeroed).
+cudaError_t select_topk_reset(cudaStream_t st, void* tmp);
 cudaError_t select_topk(cudaStream_t st, const double* d, const int* pos, int n_r, int k, int s1, void* tmp,
                         void* out, const int* k_dev = nullptr);
 cudaError_t select_cand_rows(cudaStream_t st, const void* top, int n, int* rows);

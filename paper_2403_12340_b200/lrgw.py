@@ -580,6 +580,24 @@ def dgemm_dev(trans_a: str, trans_b: str, alpha: float, a, b, beta: float, c, ct
     return c
 
 
+def select_topk_dev(d, pos, k: int, s1: int, ctx=None):
+    """Top s1 rows by (d desc, position asc) among rows with pos >= k (one
+    selection block's candidate set). d: float64, pos: int32 CUDA vectors.
+    Returns (rows, values, positions) numpy arrays; missing entries have row -1."""
+    import numpy as np
+
+    cx = _ctx(ctx)
+    n_r = d.shape[0]
+    rows = np.empty(s1, np.int32)
+    vals = np.empty(s1, np.float64)
+    poss = np.empty(s1, np.int32)
+    _sync_torch(d)
+    _check(cx._lib.lrgw_dev_select_topk(cx.handle, ctypes.c_void_p(d.data_ptr()), ctypes.c_void_p(pos.data_ptr()),
+                                        n_r, int(k), int(s1), rows.ctypes.data, vals.ctypes.data, poss.ctypes.data),
+           cx.handle, "select_topk")
+    return rows, vals, poss
+
+
 def coulomb_apply_dev(dims, cell, x, y, zero_kernel: bool = False, ctx=None):
     """y = V x for column-major float64 CUDA tensors (N_r x m)."""
     cx = _ctx(ctx)
