@@ -626,11 +626,12 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
     double* Wp = Wbuf[1 - cur].d();
     if (n_re > 0) {
       ck(cudaMemcpyAsync(oldc.p, hold.data(), sizeof(int) * n_re, cudaMemcpyHostToDevice, c->stream), "H2D");
-      ck(gather_cols(c->stream, Wp, n_r, n_r, oldc.i(), n_re, Wn, n_r), "gather_cols");
       const int ldr = n_re + (n_re & 1);  // even ld: 16-byte operand loads
       ck(gather_rows(c->stream, L.d() + (size_t)k_prev * n_r, n_r, b_prev, cand.i(), n_re, lcg.d(), ldr), "gather");
-      gemm(c, n_r, n_re, b_prev, L.d() + (size_t)k_prev * n_r, n_r, Lay::MN, lcg.d(), ldr, Lay::MN, Wn, n_r, -1.0,
-           1.0);
+      // W(:, reused) = Wprev(:, old columns) - L_prev_block L_prev_block[reused, :]^T (column gather in the epilogue)
+      ck(dgemm(c->stream, n_r, n_re, b_prev, L.d() + (size_t)k_prev * n_r, n_r, Lay::MN, lcg.d(), ldr, Lay::MN, Wn,
+               n_r, -1.0, 1.0, nullptr, false, c->sm_count, nullptr, 0, false, nullptr, nullptr, Wp, n_r, oldc.i()),
+         "dgemm(reuse)");
     }
     if (n_new > 0) {
       // W(:, new) = G(:, new) - L[:, :k] L[new, :k]^T

@@ -23,6 +23,15 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
       : "d"(a), "d"(b));
 }
 
+// All FM x FN DMMA.8x8x4 of one k4 step (i-major; ptxas schedules them).
+template <int FM, int FN>
+__device__ __forceinline__ void dmma_block(double (&acc)[FM][FN][2], const double (&af)[FM], const double (&bf)[FN]) {
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

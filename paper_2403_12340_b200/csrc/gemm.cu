@@ -2,6 +2,8 @@
 // elementwise kernels the path needs (split-K reduction, symmetric mirror,
 // row gather).
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 #include "gemm.cuh"
 #include "gemm2.cuh"
@@ -14,9 +16,9 @@ namespace {
 // Large tiles: 128x64 CTA, 8 warps of 32x32, 3 stages (~90 KB smem, 2 CTA/SM).
 // Small tiles: 64x64 CTA, 4 warps of 32x32, 4 stages (~80 KB smem, 2 CTA/SM).
 template <bool AK, bool BK, int VA, int VB>
-using CfgL = GemmCfg<128, 64, 32, 32, 3, AK, BK, VA, VB>;
+using CfgL = GemmCfg<128, 64, 32, 32, 3, AK, BK, VA, VB, 16, 2>;
 template <bool AK, bool BK, int VA, int VB>
-using CfgS = GemmCfg<64, 64, 32, 32, 4, AK, BK, VA, VB>;
+using CfgS = GemmCfg<64, 64, 32, 32, 4, AK, BK, VA, VB, 16, 2>;
 // Square 128x128 CTA, 16 warps of 32x32, 3 stages (~120 KB smem, 1 CTA/SM):
 // the symmetric (lower-tile) split-K SYRK of Theta^T V Theta.
 template <bool AK, bool BK, int VA, int VB>
@@ -30,13 +32,24 @@ template <int V>
 using CfgH32 = GemmCfg<128, 32, 32, 16, 3, false, false, V, V>;
 // Tall-skinny outputs (N not a multiple of 64): 128x32 CTA, 4 warps of 32x32.
 template <bool AK, bool BK, int VA, int VB>
-using CfgN = GemmCfg<128, 32, 32, 32, 4, AK, BK, VA, VB>;
+using CfgN = GemmCfg<128, 32, 32, 32, 4, AK, BK, VA, VB, 16, 2>;
 // Single-column-tile widths 96 / 128 for the tall-skinny GEMMs of the
 // selection (N = new candidates, K = pivots so far): 12 / 16 warps of 32x32.
 template <bool AK, bool BK, int VA, int VB>
 using Cfg96 = GemmCfg<128, 96, 32, 32, 3, AK, BK, VA, VB>;
 
-enum class Tile { S, L, X, N, W96, W128 };
+// Tall-skinny family (M >> N, N <= 128, A MN-contiguous): one column tile of
+// width 16 Q (Q = ceil(N / 16)) so at most 15 padded columns, 8 warps of
+// 32 x 8Q. A is streamed from HBM exactly once.
+template <int Q, bool BK>
+using CfgT = GemmCfg<128, 16 * Q, 32, 8 * Q, 3, false, BK, 2, 2>;
+// (Hadamard: two live accumulator sets, so 64-row tiles of 8 warps of
+// 16 x 8Q beyond Q = 5.)
+template <int Q>
+using CfgHT = typename std::conditional<(Q <= 5), GemmCfg<128, 16 * Q, 32, 8 * Q, 3, false, false, 2, 2>,
+                                        GemmCfg<64, 16 * Q, 16, 8 * Q, 3, false, false, 2, 2>>::type;
+
+enum class Tile { S, L, X, N, W96, W128, T };
 
 // Column padding of an N-wide output under 64- vs 32-wide tiles.
 bool prefer_narrow(int N) {
@@ -86,6 +99,25 @@ cudaError_t launch_layout(cudaStream_t st, const DgemmParams& p, Tile tile, bool
   }
   if (va && vb) return launch_cfg<CfgS<AK, BK, 2, 2>>(st, p, splits);
   return launch_cfg<CfgS<AK, BK, 1, 1>>(st, p, splits);
+}
+
+template <bool BK>
+cudaError_t launch_tall(cudaStream_t st, const DgemmParams& p, int q) {
+  switch (q) {
+    case 1:
+    case 2: return launch_cfg<CfgT<2, BK>>(st, p, 1);
+    case 3: return launch_cfg<CfgT<3, BK>>(st, p, 1);
+    case 4: return launch_cfg<CfgT<4, BK>>(st, p, 1);
+    case 5: return launch_cfg<CfgT<5, BK>>(st, p, 1);
+    case 6: return launch_cfg<CfgT<6, BK>>(st, p, 1);
+    case 7: return launch_cfg<CfgT<7, BK>>(st, p, 1);
+    default: return launch_cfg<CfgT<8, BK>>(st, p, 1);
+  }
+}
+
+bool tall_family_enabled() {
+  static const bool on = !(getenv("LRGW_TALL") && atoi(getenv("LRGW_TALL")) == 0);
+  return on;
 }
 
 // Split count that fills whole waves of `slots` resident CTAs: the smallest
@@ -215,7 +247,8 @@ cudaError_t gather_cols(cudaStream_t st, const double* src, long long lds, int r
 cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long long lda, Lay la,
                   const double* B, long long ldb, Lay lb, double* C, long long ldc, double alpha,
                   double beta, const double* scale, bool lower, int sm_count, double* work,
-                  size_t work_elems, bool tri_b, const int* colmap, const int* n_dev) {
+                  size_t work_elems, bool tri_b, const int* colmap, const int* n_dev, const double* cin,
+                  long long ldcin, const int* cin_map) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   DgemmParams p{};
   p.M = M;
@@ -234,6 +267,10 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
   p.tri_b = tri_b ? 1 : 0;
   p.colmap = colmap;
   p.n_dev = n_dev;
+  p.Cin = cin;
+  p.ldcin = ldcin;
+  p.cin_map = cin_map;
+  if (cin && (lower || work || !cin_map)) return cudaErrorInvalidValue;
   if ((tri_b || colmap || n_dev) && (lower || work)) return cudaErrorInvalidValue;
   const bool ak = la == Lay::K, bk = lb == Lay::K;
   // 16-byte cp.async needs aligned bases, even leading dims and even extents
@@ -253,9 +290,21 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
     const long long t = (M + 63) / 64;
     tiles = t * (t + 1) / 2;
     occ = 2;
+  } else if (!ak && va && vb && !scale && !n_dev && N > 32 && N <= 128 && ((N + 15) / 16) % 2 == 1 &&
+             (long long)((M + 127) / 128) >= 2LL * sm_count && tall_family_enabled()) {
+    // tall-skinny with N in (32, 48], (64, 80], (96, 112]: one column tile of
+    // width 16 ceil(N / 16) (the 32 / 64 / 96 / 128 tiles cover the rest)
+    tile = Tile::T;
+    tiles = (M + 127) / 128;
+    occ = 1;
+  } else if (n_dev && N > 64 && N <= 128 && (long long)((M + 127) / 128) >= 2LL * sm_count) {
+    // device-side N bound (the selection's L block): one 128-wide column tile
+    // (A streamed once); warps past the live columns skip their MMAs
+    tile = Tile::W128;
+    tiles = (M + 127) / 128;
+    occ = 1;
   } else if (n_dev && (long long)((M + 127) / 128) >= 2LL * sm_count) {
-    // device-side N bound (the selection's L block): 32-wide column tiles so
-    // the CTAs past the live columns exit at once
+    // device-side N bound: 32-wide column tiles (CTAs past the live columns exit)
     tile = Tile::N;
     tiles = (long long)((M + 127) / 128) * ((N + 31) / 32);
     occ = 2;
@@ -292,7 +341,7 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
     p.part_stride = (long long)M * N;
   }
   // v2 (paired fragments) wins for full-width tiles; narrow outputs stay on v1
-  if (!ak && !bk && !lower && !scale && splits <= 1 && N >= 128 && tile == Tile::L) {
+  if (!ak && !bk && !lower && !scale && !cin && splits <= 1 && N >= 128 && tile == Tile::L) {
     Dgemm2Params q{};
     q.M = M;
     q.N = N;
@@ -311,6 +360,10 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
     return (va && vb) ? dispatch2<2>(st, q, false) : dispatch2<1>(st, q, false);
   }
   cudaError_t e;
+  if (tile == Tile::T) {
+    const int q = (N + 15) / 16;
+    return bk ? launch_tall<true>(st, p, q) : launch_tall<false>(st, p, q);
+  }
   if (!ak && !bk) e = launch_layout<false, false>(st, p, tile, va, vb, splits);
   else if (!ak && bk) e = launch_layout<false, true>(st, p, tile, va, vb, splits);
   else if (ak && !bk) e = launch_layout<true, false>(st, p, tile, va, vb, splits);
@@ -339,6 +392,16 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
     kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(p); count_launches(1);
     return cudaGetLastError();
   };
+  if (N < 128 && vec && N > 32 && tall_family_enabled() && (long long)((M + 127) / 128) >= 2LL * 148) {
+    switch ((N + 15) / 16) {
+      case 3: return go(CfgHT<3>{});
+      case 4: return go(CfgHT<4>{});
+      case 5: return go(CfgHT<5>{});
+      case 6: return go(CfgHT<6>{});
+      case 7: return go(CfgHT<7>{});
+      default: return go(CfgHT<8>{});
+    }
+  }
   if (N < 128) {
     if (prefer_narrow(N)) return vec ? go(CfgH32<2>{}) : go(CfgH32<1>{});
     return vec ? go(CfgH<2>{}) : go(CfgH<1>{});

@@ -14,6 +14,8 @@
 // issue DMMA.8x8x4 from padded, bank-conflict-free shared tiles.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace lrgw_dev {
@@ -35,6 +37,9 @@ struct DgemmParams {
   int tri_b;             // B(n, k) == 0 for k < n (lower-triangular operand): K starts at n0
   const int* colmap;     // output column n is written to column colmap[n] of C
   const int* n_dev;      // if set: N = min(N, *n_dev), read on the device (no host sync)
+  const double* Cin;     // if set: the beta term reads Cin[m + cin_map[n] ldcin] instead of C
+  long long ldcin;
+  const int* cin_map;
 };
 
 // Tile loader for one operand. ROWS = BM or BN.
@@ -77,9 +82,11 @@ struct TileLoader {
   }
 };
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, bool AK_, bool BK_MAJ_, int VA_, int VB_, int BK_ = 16>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, bool AK_, bool BK_MAJ_, int VA_, int VB_, int BK_ = 16,
+          int MINB_ = 1>
 struct GemmCfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int MINB = MINB_;  // resident CTAs per SM the register budget is sized for
   static constexpr bool A_KMAJOR = AK_, B_KMAJOR = BK_MAJ_;
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
@@ -91,7 +98,7 @@ struct GemmCfg {
 };
 
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS) dgemm_kernel(DgemmParams p) {
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) dgemm_kernel(DgemmParams p) {
   extern __shared__ __align__(16) double smem[];
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
   constexpr int FM = Cfg::FM, FN = Cfg::FN;
@@ -120,6 +127,7 @@ __global__ void __launch_bounds__(Cfg::THREADS) dgemm_kernel(DgemmParams p) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp % Cfg::WARPS_M) * Cfg::WM, wn = (warp / Cfg::WARPS_M) * Cfg::WN;
   const int g = lane >> 2, t = lane & 3;
+  const bool live = n0 + wn < p.N;  // warps wholly past the (device-bounded) N skip their MMAs
 
   double acc[FM][FN][2];
 #pragma unroll
@@ -148,40 +156,45 @@ __global__ void __launch_bounds__(Cfg::THREADS) dgemm_kernel(DgemmParams p) {
     cp_async_commit();
   }
 
-  for (int kt = 0; kt < nkt; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      const int nx = kt + STAGES - 1;
-      if (nx < nkt) {
-        const int s = nx % STAGES;
-        LA::load(stageA(s), p.A, p.lda, m0, p.M, kb + nx * BK, ke, tid);
-        LB::load(stageB(s), p.B, p.ldb, n0, p.N, kb + nx * BK, ke, tid);
-        load_scale(s, kb + nx * BK);
+  auto mainloop = [&](auto with_mma) {
+    for (int kt = 0; kt < nkt; ++kt) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      {
+        const int nx = kt + STAGES - 1;
+        if (nx < nkt) {
+          const int s = nx % STAGES;
+          LA::load(stageA(s), p.A, p.lda, m0, p.M, kb + nx * BK, ke, tid);
+          LB::load(stageB(s), p.B, p.ldb, n0, p.N, kb + nx * BK, ke, tid);
+          load_scale(s, kb + nx * BK);
+        }
+        cp_async_commit();
       }
-      cp_async_commit();
-    }
-    const double* sa = stageA(kt % STAGES);
-    const double* sb = stageB(kt % STAGES);
-    const double* ss = stageS(kt % STAGES);
+      if (!decltype(with_mma)::value) continue;
+      const double* sa = stageA(kt % STAGES);
+      const double* sb = stageB(kt % STAGES);
+      const double* ss = stageS(kt % STAGES);
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[FM], bf[FN];
+      for (int kk = 0; kk < BK; kk += 4) {
+        double af[FM], bf[FN];
 #pragma unroll
-      for (int i = 0; i < FM; ++i) af[i] = LA::frag(sa, wm + i * 8 + g, kk + t);
+        for (int i = 0; i < FM; ++i) af[i] = LA::frag(sa, wm + i * 8 + g, kk + t);
 #pragma unroll
-      for (int j = 0; j < FN; ++j) bf[j] = LB::frag(sb, wn + j * 8 + g, kk + t);
-      if (p.scale) {
-        const double sc = ss[kk + t];
+        for (int j = 0; j < FN; ++j) bf[j] = LB::frag(sb, wn + j * 8 + g, kk + t);
+        if (p.scale) {
+          const double sc = ss[kk + t];
 #pragma unroll
-        for (int j = 0; j < FN; ++j) bf[j] *= sc;
+          for (int j = 0; j < FN; ++j) bf[j] *= sc;
+        }
+        dmma_block<FM, FN>(acc, af, bf);
       }
-#pragma unroll
-      for (int i = 0; i < FM; ++i)
-#pragma unroll
-        for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-  }
+  };
+  // warps wholly past a device-bounded N only keep the copy / barrier cadence
+  if (live)
+    mainloop(std::true_type{});
+  else
+    mainloop(std::false_type{});
   cp_async_wait<0>();
 
   // Epilogue: c0 = C[m = g][n = 2t], c1 = C[g][2t+1] per 8x8 fragment.
@@ -213,7 +226,10 @@ __global__ void __launch_bounds__(Cfg::THREADS) dgemm_kernel(DgemmParams p) {
             const int nc = p.colmap ? __ldg(p.colmap + n + h) : n + h;
             double* c = p.C + m + (long long)nc * p.ldc;
             const double v = p.alpha * acc[i][j][h];
-            *c = (p.beta == 0.0) ? v : v + p.beta * (*c);
+            if (p.beta == 0.0)
+              *c = v;
+            else
+              *c = v + p.beta * (p.Cin ? p.Cin[m + (long long)__ldg(p.cin_map + n + h) * p.ldcin] : *c);
           }
         }
       }
@@ -284,10 +300,7 @@ __global__ void __launch_bounds__(Cfg::THREADS) hadamard_kernel(HadamardParams p
       for (int i = 0; i < FM; ++i) af[i] = LA::frag(sa, wm + i * 8 + g, kk + t);
 #pragma unroll
       for (int j = 0; j < FN; ++j) bf[j] = LB::frag(sb, wn + j * 8 + g, kk + t);
-#pragma unroll
-      for (int i = 0; i < FM; ++i)
-#pragma unroll
-        for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      dmma_block<FM, FN>(acc, af, bf);
     }
     if (kt == kt1 - 1) {
 #pragma unroll

@@ -136,10 +136,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) dgemm2_kernel(Dgemm2Params p)
         bf[2 * j] = v.x;
         bf[2 * j + 1] = v.y;
       }
-#pragma unroll
-      for (int i = 0; i < FM; ++i)
-#pragma unroll
-        for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      dmma_block<FM, FN>(acc, af, bf);
     }
     if (Cfg::HAD && kt == kt1 - 1) {
 #pragma unroll

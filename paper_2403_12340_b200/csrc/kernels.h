@@ -22,7 +22,8 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
                   const double* B, long long ldb, Lay lb, double* C, long long ldc, double alpha,
                   double beta, const double* scale, bool lower, int sm_count, double* work,
                   size_t work_elems, bool tri_b = false, const int* colmap = nullptr,
-                  const int* n_dev = nullptr);
+                  const int* n_dev = nullptr, const double* cin = nullptr, long long ldcin = 0,
+                  const int* cin_map = nullptr);
 
 // C = alpha * (A1 B1^T) o (A2 B2^T) + beta * C; A1: M x K1, B1: N x K1, A2: M x K2,
 // B2: N x K2, all MN-contiguous (isdf.hpp:132 fit GEMM pair + Hadamard).

@@ -41,19 +41,20 @@ def main():
         print(f"{name:28s} {ta}{tb} m={m:6d} n={n:5d} k={k:6d}: {ms:8.3f} ms {tf:6.2f} TF/s ({tf / 37.17 * 100:5.1f}%) err={err:.1e}",
               flush=True)
 
-    run("theta-like", "N", "N", 110592, 1024, 1024)
-    run("theta-like v2", "N", "T", 110592, 1024, 1024)
-    run("pvp-like (full)", "T", "N", 1024, 1024, 115200)
-    run("lpass-96", "N", "T", 110592, 96, 512)
-    run("lpass-64", "N", "T", 110592, 64, 512)
-    run("lpass-128", "N", "T", 110592, 128, 1000)
-    run("probe Theta^T x", "T", "N", 1024, 8, 110592)
-    run("probe Theta w", "N", "N", 110592, 8, 1024)
-    run("square 1024", "N", "N", 1024, 1024, 1024)
-    run("square 8192", "N", "N", 8192, 8192, 8192, reps=2)
-    run("square 8192 v2", "N", "T", 8192, 8192, 8192, reps=2)
-    run("lpass-80 v2", "N", "T", 110592, 80, 700)
-    run("lpass-32 v2", "N", "T", 110592, 30, 300)
+    shapes = sys.argv[1] if len(sys.argv) > 1 else "path"
+    if shapes in ("path", "all"):
+        run("theta-like", "N", "N", 110592, 1024, 1024)
+        run("theta-like v2", "N", "T", 110592, 1024, 1024)
+        run("pvp-like (full)", "T", "N", 1024, 1024, 115200)
+        run("probe Theta^T x", "T", "N", 1024, 8, 110592)
+        run("probe Theta w", "N", "N", 110592, 8, 1024)
+        run("square 8192 v2", "N", "T", 8192, 8192, 8192, reps=2)
+    if shapes in ("select", "all"):
+        for n in (32, 48, 64, 66, 80, 96, 112, 128):
+            run(f"lpass n={n}", "N", "T", 110592, n, 470)
+        run("lpass n=80 k=1000", "N", "T", 110592, 80, 1000)
+        run("reuse n=49 k=79", "N", "T", 110592, 49, 79)
+        run("lupd n=84 k=128 (B K-major)", "N", "N", 110592, 84, 128)
 
 
 if __name__ == "__main__":
