@@ -56,8 +56,9 @@ def algorithmic_work(cfg, n_mu):
     nh = (cfg.dims[0] // 2 + 1) * cfg.dims[1] * cfg.dims[2]
     return {
         "select": ("tensor", 2.0 * n_r * (n_mu * n + n_mu * (n_mu - 1) / 2.0)),
-        "fit_lhs": ("tensor", 2.0 * n_r * n_mu * n),
-        "fit_gemm": ("tensor", 2.0 * n_r * n_mu * n_mu),
+        # fused fit (lrgw_build): Theta = L L_P^-1 with L_P^-1 lower triangular
+        # -> n_r n_mu^2 / 2 multiply-adds; the unfused lhs pass is skipped
+        "fit_gemm": ("tensor", 1.0 * n_r * n_mu * n_mu),
         "contour": ("tensor", 2.0 * n_mu * (n_mu + 1) * n * (cfg.n_lambda + 1)),
         "fft": ("hbm", 8.0 * n_r * n_mu + 16.0 * nh * n_mu),
         "pvp": ("tensor", 1.0 * n_r * n_mu * (n_mu + 1)),

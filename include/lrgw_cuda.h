@@ -194,6 +194,11 @@ int lrgw_dev_dgemm(lrgw_ctx ctx, char trans_a, char trans_b, int m, int n, int k
                    const double* a, long long lda, const double* b, long long ldb, double beta,
                    double* c, long long ldc);
 
+/* In-place inverse of the lower triangle of a device matrix (n x n, column
+ * major, ld lda); the strict upper triangle is left untouched. Singular ->
+ * LRGW_ERR_SINGULAR with the pivot index. Exposed for tests. */
+int lrgw_dev_trtri_lower(lrgw_ctx ctx, double* a, int n, long long lda);
+
 /* Top s1 rows by (d desc, position asc) among rows with pos[r] >= k — the
  * candidate set of one selection block (device arrays; host outputs, rows of
  * missing entries are -1). Exposed for tests. */

@@ -117,6 +117,7 @@ _SIGS = {
                                          ctypes.c_void_p]),
     "lrgw_dev_coulomb_apply": (ctypes.c_int, [ctx_t, c_int_p, c_double_p, ctypes.c_int, ctypes.c_void_p,
                                               c_ll, ctypes.c_int, ctypes.c_void_p, c_ll]),
+    "lrgw_dev_trtri_lower": (ctypes.c_int, [ctx_t, ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong]),
     "lrgw_dev_select_topk": (ctypes.c_int, [ctx_t, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                             ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "lrgw_dev_dgemm": (ctypes.c_int, [ctx_t, ctypes.c_char, ctypes.c_char, ctypes.c_int, ctypes.c_int,

@@ -481,20 +481,14 @@ void gram_inverse(lrgw_ctx c, const double* gram, int n, double* ginv) {
 
 // In-place inverse of a lower-triangular factor (cuSOLVER trtri, leaf).
 void trtri_lower(lrgw_ctx c, double* a, int n) {
-  size_t wd = 0, wh = 0;
-  cks(cusolverDnXtrtri_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, a, n, &wd,
-                                  &wh),
-      "trtri_bufferSize");
-  DBuf wdev(c, std::max<size_t>(wd, 8));
-  std::vector<char> whost(std::max<size_t>(wh, 8));
-  DBuf info = ialloc(c, 1);
-  ck(cudaMemsetAsync(info.p, 0, sizeof(int), c->stream), "memset");
-  cks(cusolverDnXtrtri(c->solver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, a, n, wdev.p, wd,
-                       whost.data(), wh, info.i()),
-      "trtri");
+  DBuf work = dalloc(c, trtri_work_elems(n));
+  DBuf bad = ialloc(c, 1);
+  const int big = 0x7fffffff;
+  ck(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D");
+  ck(lrgw_dev::trtri_lower(c->stream, a, n, n, work.d(), bad.i(), c->sm_count), "trtri");
   int h = 0;
-  download(c, &h, info.p, sizeof(int));
-  if (h != 0) fail(LRGW_ERR_SINGULAR, "trtri: singular factor", h - 1);
+  download(c, &h, bad.p, sizeof(int));
+  if (h != big) fail(LRGW_ERR_SINGULAR, "trtri: singular factor", h - 1);
 }
 
 // K = (T^-1/2 - P^T V P)^-1 (smw.hpp:42-73). T must be negative definite
@@ -747,20 +741,17 @@ bool fused_fit(lrgw_ctx c, const SelectKeep& keep, int n_r, const std::vector<in
   const double tiny = 1e-14 * (gmax > 0.0 ? gmax : 1.0);
   for (double v : diag)
     if (!(v * v >= tiny)) return false;
-  // X = L_P^-1 in place
-  size_t wd = 0, wh = 0;
-  cks(cusolverDnXtrtri_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n_mu, CUDA_R_64F,
-                                  lp.d(), n_mu, &wd, &wh),
-      "trtri_bufferSize");
-  DBuf wdev(c, std::max<size_t>(wd, 8));
-  std::vector<char> whost(std::max<size_t>(wh, 8));
-  DBuf info = ialloc(c, 1);
-  cks(cusolverDnXtrtri(c->solver, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n_mu, CUDA_R_64F, lp.d(), n_mu,
-                       wdev.p, wd, whost.data(), wh, info.i()),
-      "trtri");
-  int hinfo = 0;
-  download(c, &hinfo, info.p, sizeof(int));
-  if (hinfo != 0) return false;
+  // X = L_P^-1 in place (trtri.cu: recursive 2 x 2 blocking on the DMMA engine)
+  {
+    DBuf work = dalloc(c, trtri_work_elems(n_mu));
+    DBuf bad = ialloc(c, 1);
+    const int big = 0x7fffffff;
+    ck(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D");
+    ck(lrgw_dev::trtri_lower(c->stream, lp.d(), n_mu, n_mu, work.d(), bad.i(), c->sm_count), "trtri");
+    int h = 0;
+    download(c, &h, bad.p, sizeof(int));
+    if (h != big) return false;
+  }
   mark(c, 3);  // FIT_SOLVE = gather L_P + trtri; FIT_GEMM = L L_P^-1 below
   // output column of pivot-ordered column q: its rank among the sorted points
   std::vector<int> colmap(n_mu);
@@ -1498,6 +1489,20 @@ int lrgw_dev_dgemm(lrgw_ctx c, char ta, char tb, int m, int n, int k, double alp
     gemm(c, m, n, k, a, lda, at ? Lay::K : Lay::MN, b, ldb, bt ? Lay::MN : Lay::K, cm, ldc, alpha, beta, nullptr,
          false, &w);
     ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int lrgw_dev_trtri_lower(lrgw_ctx c, double* a, int n, long long lda) {
+  return guarded(c, [&] {
+    if (n < 0 || lda < std::max(1, n)) fail(LRGW_ERR_INVALID_INPUT, "trtri: bad sizes");
+    DBuf work = dalloc(c, trtri_work_elems(n));
+    DBuf bad = ialloc(c, 1);
+    const int big = 0x7fffffff;
+    ck(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D");
+    ck(lrgw_dev::trtri_lower(c->stream, a, n, lda, work.d(), bad.i(), c->sm_count), "trtri");
+    int h = 0;
+    download(c, &h, bad.p, sizeof(int));
+    if (h != big) fail(LRGW_ERR_SINGULAR, "trtri: singular factor", h - 1);
   });
 }
 

@@ -42,7 +42,7 @@ using Cfg96 = GemmCfg<128, 96, 32, 32, 3, AK, BK, VA, VB>;
 // width 16 Q (Q = ceil(N / 16)) so at most 15 padded columns, 8 warps of
 // 32 x 8Q. A is streamed from HBM exactly once.
 template <int Q, bool BK>
-using CfgT = GemmCfg<128, 16 * Q, 32, 8 * Q, 3, false, BK, 2, 2>;
+using CfgT = GemmCfg<128, 16 * Q, 32, 8 * Q, 3, false, BK, 2, 2, (Q >= 5 ? 32 : 16)>;
 // (Hadamard: two live accumulator sets, so 64-row tiles of 8 warps of
 // 16 x 8Q beyond Q = 5.)
 template <int Q>

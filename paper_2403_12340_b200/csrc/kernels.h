@@ -71,6 +71,12 @@ cudaError_t coulomb_scale_half(cudaStream_t st, int n1, int n2, int n3, double c
 cudaError_t scale_copy(cudaStream_t st, const double* src, double* dst, size_t n, double alpha);
 cudaError_t fill(cudaStream_t st, double* dst, size_t n, double v);
 cudaError_t zero_strict_upper(cudaStream_t st, double* a, int n, long long lda);
+
+// In-place inverse of the lower triangle of a (n x n, ld lda) — trtri.cu.
+// work: trtri_work_elems(n) doubles; *bad (device, preset to INT_MAX) gets
+// (first zero pivot + 1) if the factor is singular.
+size_t trtri_work_elems(int n);
+cudaError_t trtri_lower(cudaStream_t st, double* a, int n, long long lda, double* work, int* bad, int sm_count);
 cudaError_t add_diag(cudaStream_t st, double* a, int n, long long lda, double v);
 cudaError_t axpby(cudaStream_t st, int rows, int cols, double alpha, const double* x, long long ldx,
                   double beta, double* y, long long ldy);

@@ -580,6 +580,16 @@ def dgemm_dev(trans_a: str, trans_b: str, alpha: float, a, b, beta: float, c, ct
     return c
 
 
+def trtri_lower_dev(a, ctx=None):
+    """In-place inverse of the lower triangle of a square column-major float64
+    CUDA matrix (the strict upper triangle is left untouched)."""
+    cx = _ctx(ctx)
+    pa, lda = _dev_ptr_cm(a)
+    _sync_torch(a)
+    _check(cx._lib.lrgw_dev_trtri_lower(cx.handle, ctypes.c_void_p(pa), a.shape[0], lda), cx.handle, "trtri")
+    return a
+
+
 def select_topk_dev(d, pos, k: int, s1: int, ctx=None):
     """Top s1 rows by (d desc, position asc) among rows with pos >= k (one
     selection block's candidate set). d: float64, pos: int32 CUDA vectors.
