@@ -8,6 +8,7 @@
 // and cuSOLVER are used only as leaf calls (3-D FFT, N_mu x N_mu factors).
 #include <cufft.h>
 #include <cusolverDn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -207,8 +208,15 @@ void download(lrgw_ctx c, void* h, const void* d, size_t bytes) {
 void use_device(lrgw_ctx c) { ck(cudaSetDevice(c->device), "cudaSetDevice"); }
 
 // Stage boundary i of the build (no-op outside lrgw_build).
+// Stage boundary of lrgw_build: CUDA event for the stage timings plus an NVTX
+// range per stage (profilers attribute kernels to stages; a no-op otherwise).
 void mark(lrgw_ctx c, int i) {
-  if (c->timing) ck(cudaEventRecord(c->ev[i], c->stream), "cudaEventRecord");
+  static const char* const names[LRGW_STAGE_TOTAL] = {"select", "fit_lhs", "fit_solve", "fit_gemm",
+                                                        "contour", "fft", "pvp", "smw"};
+  if (!c->timing) return;
+  ck(cudaEventRecord(c->ev[i], c->stream), "cudaEventRecord");
+  if (i > 0) nvtxRangePop();
+  if (i < LRGW_STAGE_TOTAL) nvtxRangePushA(names[i]);
 }
 
 // The ABI wrapper: run the body, map failures onto status codes.
