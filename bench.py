@@ -60,6 +60,9 @@ def algorithmic_work(cfg, n_mu):
         # -> n_r n_mu^2 / 2 multiply-adds; the unfused lhs pass is skipped
         "fit_gemm": ("tensor", 1.0 * n_r * n_mu * n_mu),
         "contour": ("tensor", 2.0 * n_mu * (n_mu + 1) * n * (cfg.n_lambda + 1)),
+        # the K3 kernel alone (CUDA events around its launch; the stage adds the
+        # node tables, their upload and the fixed-order segment reduction)
+        "quad_kernel": ("tensor", 2.0 * n_mu * (n_mu + 1) * n * (cfg.n_lambda + 1)),
         "fft": ("hbm", 8.0 * n_r * n_mu + 16.0 * nh * n_mu),
         "pvp": ("tensor", 1.0 * n_r * n_mu * (n_mu + 1)),
     }
@@ -259,7 +262,7 @@ def run_ours(args, cfg, world, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="si64")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -45,15 +45,16 @@ enum lrgw_point_selector { LRGW_QRCP_DIRECT = 0, LRGW_QRCP_SKETCHED = 1 };
  * stream, consecutive intervals). */
 enum lrgw_stage {
   LRGW_STAGE_SELECT = 0,    /* K1 ISDF point selection                         */
-  LRGW_STAGE_FIT_LHS = 1,   /* K2a (Phi Phi_mu^T) o (Phi Phi_mu^T) + gathers   */
-  LRGW_STAGE_FIT_SOLVE = 2, /* cuSOLVER leaf: G_mumu LU + inverse              */
-  LRGW_STAGE_FIT_GEMM = 3,  /* K2b Theta = lhs G^-1                            */
-  LRGW_STAGE_CONTOUR = 4,   /* K3 Cauchy quadrature of the core T              */
+  LRGW_STAGE_FIT_LHS = 1,   /* K2a lhs (explicit fit only; empty when fused)   */
+  LRGW_STAGE_FIT_SOLVE = 2, /* L_P gather + recursive DMMA triangular inverse  */
+  LRGW_STAGE_FIT_GEMM = 3,  /* K2b Theta = L L_P^-1                            */
+  LRGW_STAGE_CONTOUR = 4,   /* K3 Cauchy quadrature of the core T (+ tables)   */
   LRGW_STAGE_FFT = 5,       /* cuFFT leaf: batched D2Z of Theta                */
   LRGW_STAGE_PVP = 6,       /* K5 Theta^T V Theta G-space SYRK                 */
-  LRGW_STAGE_SMW = 7,       /* K6 cuSOLVER leaf: SMW core K                    */
+  LRGW_STAGE_SMW = 7,       /* K6 SMW core K (cuSOLVER potrf leaves + DMMA)    */
   LRGW_STAGE_TOTAL = 8,
-  LRGW_NUM_STAGES = 9
+  LRGW_STAGE_QUAD_KERNEL = 9, /* the K3 kernel alone (last quadrature launch)  */
+  LRGW_NUM_STAGES = 10
 };
 
 typedef struct lrgw_ctx_s* lrgw_ctx;

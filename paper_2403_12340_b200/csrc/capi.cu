@@ -71,6 +71,8 @@ struct lrgw_ctx_s {
   int pivot = -1;
   double stage_ms[LRGW_NUM_STAGES] = {};
   cudaEvent_t ev[LRGW_NUM_STAGES + 1] = {};
+  cudaEvent_t ev_quad[2] = {};  // around the K3 kernel (timing builds only)
+  bool quad_timed = false;
   bool timing = false;  // record stage events (lrgw_build only)
   long long launches0 = 0;
   int select_batch = 128;
@@ -799,11 +801,12 @@ void quad_run(lrgw_ctx c, const double* pv, long long ldv, const double* pc, lon
   }
   DBuf ddv = upload(c, dv.data(), dv.size()), ddc = upload(c, dc.data(), dc.size());
   DBuf dgw = upload(c, gw.data(), gw.size());
-  const int groups = quad_partial_groups(n_mu, n_nodes, c->sm_count);
-  DBuf partial = dalloc(c, (size_t)groups * n_mu * n_mu);
-  ck(quad_nodes(c->stream, n_mu, n_v, n_c, pv, ldv, pc, ldpc, n_nodes, ddv.d(), ddc.d(), dgw.d(), groups,
-                partial.d(), running, beta, pref, out, ldo),
+  DBuf partial = dalloc(c, quad_partial_elems(n_mu, n_nodes, c->sm_count));
+  ck(quad_nodes(c->stream, n_mu, n_v, n_c, pv, ldv, pc, ldpc, n_nodes, ddv.d(), ddc.d(), dgw.d(), c->sm_count,
+                partial.d(), running, beta, pref, out, ldo, c->timing ? c->ev_quad[0] : nullptr,
+                c->timing ? c->ev_quad[1] : nullptr),
      "quad_nodes");
+  if (c->timing) c->quad_timed = true;
 }
 
 void node_tables_or_fail(const lrgw_host::Spec& s, const double* e, int n_v, int n_c, const NodeSet& ns,
@@ -930,6 +933,8 @@ int lrgw_ctx_destroy(lrgw_ctx c) {
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   for (auto& x : c->ev)
+    if (x) cudaEventDestroy(x);
+  for (auto& x : c->ev_quad)
     if (x) cudaEventDestroy(x);
   delete c;
   return LRGW_OK;
@@ -1321,6 +1326,8 @@ int lrgw_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, lo
                 "elliptic_params");
     for (auto& x : c->ev)
       if (!x) ck(cudaEventCreate(&x), "event");
+    for (auto& x : c->ev_quad)
+      if (!x) ck(cudaEventCreate(&x), "event");
     struct TimingGuard {
       lrgw_ctx c;
       ~TimingGuard() { c->timing = false; }
@@ -1391,6 +1398,10 @@ int lrgw_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, lo
     }
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[8]);
     c->stage_ms[LRGW_STAGE_TOTAL] = ms;
+    c->stage_ms[LRGW_STAGE_QUAD_KERNEL] = 0.0;
+    if (c->quad_timed && cudaEventElapsedTime(&ms, c->ev_quad[0], c->ev_quad[1]) == cudaSuccess)
+      c->stage_ms[LRGW_STAGE_QUAD_KERNEL] = ms;
+    c->quad_timed = false;
     auto* e = new lrgw_eps_s;
     e->ctx = c;
     e->n_r = n_r;

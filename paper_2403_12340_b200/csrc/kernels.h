@@ -51,11 +51,13 @@ cudaError_t skinny_nn(cudaStream_t st, const double* theta, long long ldt, int n
                       long long ldw, int m, double* z, long long ldz, int sm_count);
 
 // K3 quadrature (quadrature.cu).
-int quad_partial_groups(int n_mu, int n_nodes, int sm_count);
+// Workspace (doubles) of quad_nodes: per-segment 64 x 64 partials + the plan tables.
+size_t quad_partial_elems(int n_mu, int n_nodes, int sm_count);
 cudaError_t quad_nodes(cudaStream_t st, int n_mu, int n_v, int n_c, const double* pv, long long ldv,
                        const double* pc, long long ldc, int n_nodes, const double* dv,
-                       const double* dc, const double* gw, int groups, double* partial,
-                       double* running, double beta, double pref, double* t, long long ldt);
+                       const double* dc, const double* gw, int sm_count, double* partial,
+                       double* running, double beta, double pref, double* t, long long ldt,
+                       cudaEvent_t k_begin = nullptr, cudaEvent_t k_end = nullptr);
 
 // Coulomb (coulomb.cu): G-space half-spectrum weights c(G) = w_G v(G) / N_r
 // (w_G = 2 off the self-conjugate i1 planes, 1 on them) laid out to match a
