@@ -17,6 +17,7 @@
 // one 64 x 64 partial per tile segment it touches; a fixed-order reduction
 // sums the segments of each tile. Phi_mu panels are L2-resident (2 MB at Si64).
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -26,15 +27,20 @@ namespace lrgw_dev {
 
 namespace {
 
-constexpr int QBM = 64, QBK = 32, QSTAGES = 4;
+constexpr int QBM = 64;
 constexpr int QWM = 32, QWN = 16;                      // warp tile
 constexpr int QWARPS_M = QBM / QWM, QWARPS_N = QBM / QWN;  // 2 x 4
 constexpr int QTHREADS = 32 * QWARPS_M * QWARPS_N;     // 256
 constexpr int QFM = QWM / 8, QFN = QWN / 8;            // 4 x 2 fragments
 constexpr int QPITCH = QBM + 4;                        // conflict-free pitch (doubles)
-constexpr int QTILE = QBK * QPITCH;
-constexpr int QSTAGE_ELEMS = 2 * QTILE + 2 * QBK;  // + the k-tile's complex diagonal
-constexpr int QSMEM = QSTAGES * QSTAGE_ELEMS * 8;
+// k-tile depth: 64 (3-stage ring) when both bands reach it, else 32 / 16 (4 stages)
+template <int BK>
+struct QK {
+  static constexpr int QBK = BK, QSTAGES = BK >= 64 ? 3 : 4;
+  static constexpr int QTILE = QBK * QPITCH;
+  static constexpr int QSTAGE_ELEMS = 2 * QTILE + 2 * QBK;  // + the k-tile's complex diagonal
+  static constexpr int QSMEM = QSTAGES * QSTAGE_ELEMS * 8;
+};
 
 struct QuadParams {
   int n_mu, n_v, n_c;
@@ -56,7 +62,7 @@ __host__ __device__ __forceinline__ long long quad_run_begin(long long units, in
   return units * c / ctas;
 }
 
-template <int VEC>
+template <int VEC, int QBK>
 __device__ __forceinline__ void load_panel(double* s, const double* g, long long ld, int row0,
                                            int rows, int k0, int kend, int tid) {
   constexpr int CHUNKS = QBM * QBK / VEC;
@@ -75,9 +81,11 @@ __device__ __forceinline__ void load_panel(double* s, const double* g, long long
   }
 }
 
-template <int VEC>
+template <int VEC, int BK>
 __global__ void __launch_bounds__(QTHREADS, 1) quad_kernel(QuadParams p) {
   extern __shared__ __align__(16) double smem[];
+  constexpr int QBK = QK<BK>::QBK, QSTAGES = QK<BK>::QSTAGES, QTILE = QK<BK>::QTILE;
+  constexpr int QSTAGE_ELEMS = QK<BK>::QSTAGE_ELEMS;
   const long long u0 = quad_run_begin(p.units, gridDim.x, blockIdx.x);
   const long long u1 = quad_run_begin(p.units, gridDim.x, blockIdx.x + 1);
   if (u1 <= u0) return;
@@ -107,8 +115,8 @@ __global__ void __launch_bounds__(QTHREADS, 1) quad_kernel(QuadParams p) {
     const long long ld = cph ? p.ldc : p.ldv;
     const int k0 = (cph ? kt : kt - ktc) * QBK;
     const int kend = cph ? p.n_c : p.n_v;
-    load_panel<VEC>(s, src, ld, tm * QBM, p.n_mu, k0, kend, tid);
-    load_panel<VEC>(s + QTILE, src, ld, tn * QBM, p.n_mu, k0, kend, tid);
+    load_panel<VEC, QBK>(s, src, ld, tm * QBM, p.n_mu, k0, kend, tid);
+    load_panel<VEC, QBK>(s + QTILE, src, ld, tn * QBM, p.n_mu, k0, kend, tid);
     // the node's diagonal 1/(z_k - e) for this k-tile (zero-filled past the band count)
     if (tid < QBK) {
       const double2* dtab = cph ? p.dc + (long long)node * p.n_c : p.dv + (long long)node * p.n_v;
@@ -313,12 +321,24 @@ cudaError_t quad_nodes(cudaStream_t st, int n_mu, int n_v, int n_c, const double
                    (reinterpret_cast<uintptr_t>(pv) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(pc) % 16 == 0);
   if (k_begin) cudaEventRecord(k_begin, st);
-  if (vec) {
-    cudaFuncSetAttribute(quad_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, QSMEM);
-    quad_kernel<2><<<q.ctas, QTHREADS, QSMEM, st>>>(p); count_launches(1);
+  auto go = [&](auto vec_c, auto bk_c) {
+    constexpr int V = decltype(vec_c)::value, B = decltype(bk_c)::value;
+    cudaFuncSetAttribute(quad_kernel<V, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, QK<B>::QSMEM);
+    quad_kernel<V, B><<<q.ctas, QTHREADS, QK<B>::QSMEM, st>>>(p);
+    count_launches(1);
+  };
+  using V1 = std::integral_constant<int, 1>;
+  using V2 = std::integral_constant<int, 2>;
+  const int nb = std::min(n_v, n_c);
+  if (nb >= 64) {
+    using B = std::integral_constant<int, 64>;
+    vec ? go(V2{}, B{}) : go(V1{}, B{});
+  } else if (nb >= 32) {
+    using B = std::integral_constant<int, 32>;
+    vec ? go(V2{}, B{}) : go(V1{}, B{});
   } else {
-    cudaFuncSetAttribute(quad_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, QSMEM);
-    quad_kernel<1><<<q.ctas, QTHREADS, QSMEM, st>>>(p); count_launches(1);
+    using B = std::integral_constant<int, 16>;
+    vec ? go(V2{}, B{}) : go(V1{}, B{});
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
