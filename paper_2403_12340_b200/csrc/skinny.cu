@@ -12,52 +12,56 @@ namespace lrgw_dev {
 
 namespace {
 
-constexpr int TN_MU = 8;         // Theta columns per CTA (accumulators: TN_MU x m per thread)
-constexpr int TN_THREADS = 256;  // 8 warps
+constexpr int TN_MU_W = 4;                // Theta columns per warp
+constexpr int TN_THREADS = 256;           // 8 warps
+constexpr int TN_MU = TN_MU_W * TN_THREADS / 32;  // Theta columns per CTA
 
-// partial[chunk][mu][c] = sum over the chunk's rows of Theta[r, mu] x[r, c]
+// partial[chunk][mu][c] = sum over the chunk's rows of Theta[r, mu] x[r, c].
+// Lane = grid row (coalesced 256-byte row segments of each Theta column and
+// of x), warp = 4 Theta columns, accumulators in registers over the whole
+// row chunk and one warp reduction at the end; x is re-read by the CTA's 8
+// warps from L1. Theta is streamed from HBM exactly once.
 template <int M>
 __global__ void __launch_bounds__(TN_THREADS) tn_kernel(const double* theta, long long ldt, int n_r, int n_mu,
                                                         const double* x, long long ldx, int rows_per_chunk,
                                                         double* partial) {
-  const int mu0 = blockIdx.x * TN_MU;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int mu0 = blockIdx.x * TN_MU + warp * TN_MU_W;
   const int r0 = blockIdx.y * rows_per_chunk;
   const int r1 = min(n_r, r0 + rows_per_chunk);
-  double acc[TN_MU][M];
+  const double* th[TN_MU_W];
+  bool ok[TN_MU_W];
 #pragma unroll
-  for (int i = 0; i < TN_MU; ++i)
+  for (int i = 0; i < TN_MU_W; ++i) {
+    ok[i] = mu0 + i < n_mu;
+    th[i] = theta + (long long)(ok[i] ? mu0 + i : 0) * ldt;
+  }
+  double acc[TN_MU_W][M];
+#pragma unroll
+  for (int i = 0; i < TN_MU_W; ++i)
 #pragma unroll
     for (int c = 0; c < M; ++c) acc[i][c] = 0.0;
-  for (int r = r0 + threadIdx.x; r < r1; r += TN_THREADS) {
-    double xv[M];
+#pragma unroll 4
+  for (int r = r0 + lane; r < r1; r += 32) {
+    double xv[M], tv[TN_MU_W];
 #pragma unroll
     for (int c = 0; c < M; ++c) xv[c] = __ldg(x + r + (long long)c * ldx);
 #pragma unroll
-    for (int i = 0; i < TN_MU; ++i) {
-      const double th = (mu0 + i < n_mu) ? __ldg(theta + r + (long long)(mu0 + i) * ldt) : 0.0;
+    for (int i = 0; i < TN_MU_W; ++i) tv[i] = ok[i] ? __ldcs(th[i] + r) : 0.0;  // streamed once
 #pragma unroll
-      for (int c = 0; c < M; ++c) acc[i][c] = fma(th, xv[c], acc[i][c]);
-    }
+    for (int i = 0; i < TN_MU_W; ++i)
+#pragma unroll
+      for (int c = 0; c < M; ++c) acc[i][c] = fma(tv[i], xv[c], acc[i][c]);
   }
-  // block reduction: warp shuffles, then across the 8 warps through smem
-  __shared__ double red[TN_THREADS / 32][TN_MU * M];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (int i = 0; i < TN_MU; ++i)
+  for (int i = 0; i < TN_MU_W; ++i)
 #pragma unroll
     for (int c = 0; c < M; ++c) {
       double v = acc[i][c];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (lane == 0) red[wid][i * M + c] = v;
+      if (lane == 0 && ok[i]) partial[((long long)blockIdx.y * n_mu + mu0 + i) * M + c] = v;
     }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < TN_MU * M; idx += TN_THREADS) {
-    double v = 0.0;
-    for (int w = 0; w < TN_THREADS / 32; ++w) v += red[w][idx];
-    const int i = idx / M, c = idx % M;
-    if (mu0 + i < n_mu) partial[((long long)blockIdx.y * n_mu + mu0 + i) * M + c] = v;
-  }
 }
 
 template <int M>
@@ -108,8 +112,8 @@ template <int M>
 cudaError_t tn_launch(cudaStream_t st, const double* theta, long long ldt, int n_r, int n_mu, const double* x,
                       long long ldx, double* u, long long ldu, double* work, size_t work_elems, int sm_count) {
   const int mus = (n_mu + TN_MU - 1) / TN_MU;
-  // enough row chunks for ~4 waves, bounded by the workspace
-  int chunks = std::max(1, (4 * sm_count * 2 + mus - 1) / mus);
+  // ~8 resident CTAs per SM, bounded by the workspace
+  int chunks = std::max(1, (8 * sm_count + mus - 1) / mus);
   while (chunks > 1 && (size_t)chunks * n_mu * M > work_elems) --chunks;
   const int rows = (n_r + chunks - 1) / chunks;
   chunks = (n_r + rows - 1) / rows;
