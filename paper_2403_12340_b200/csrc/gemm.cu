@@ -341,7 +341,11 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
     p.part_stride = (long long)M * N;
   }
   // v2 (paired fragments) wins for full-width tiles; narrow outputs stay on v1
-  if (!ak && !bk && !lower && !scale && !cin && splits <= 1 && N >= 128 && tile == Tile::L) {
+  // (and for tall-skinny outputs whose width is a multiple of 32: 32 / 64 / 96)
+  const bool narrow_v2 = !ak && !bk && !lower && !scale && !cin && splits <= 1 && N > 16 && N <= 96 &&
+                         ((N + 15) / 16) % 2 == 0 && (long long)((M + 127) / 128) >= 2LL * sm_count &&
+                         (tile == Tile::W96 || tile == Tile::L || tile == Tile::N);
+  if (narrow_v2 || (!ak && !bk && !lower && !scale && !cin && splits <= 1 && N >= 128 && tile == Tile::L)) {
     Dgemm2Params q{};
     q.M = M;
     q.N = N;
