@@ -191,14 +191,17 @@ __global__ void gather_cols_kernel(const double* src, long long lds, int rows, c
 }
 
 // ---- v2 (paired-fragment) configurations ---------------------------------
-template <int V>
-using G2L = Gemm2Cfg<128, 128, 64, 32, 4, V, false>;
-template <int V>
-using G2W96 = Gemm2Cfg<128, 96, 32, 32, 4, V, false>;  // 12 warps (a multiple of 4 SMSPs)
+// BK = 32 (3-stage ring) for the 128-row-wide 12- and 8-warp configurations,
+// BK = 16 for the narrow ones (measured, tools/bench_gemm.py).
 template <int V>
 using G2W64 = Gemm2Cfg<128, 64, 64, 32, 4, V, false>;
 template <int V>
 using G2W32 = Gemm2Cfg<128, 32, 32, 32, 4, V, false>;
+template <int V>
+using G2L32 = Gemm2Cfg<128, 128, 64, 32, 3, V, false, 32>;  // 8 warps
+template <int V>
+using G2W96_32 = Gemm2Cfg<128, 96, 32, 32, 3, V, false, 32>;  // 12 warps (a multiple of 4 SMSPs)
+
 template <int V>
 using H2W64 = Gemm2Cfg<128, 64, 32, 32, 4, V, true>;
 template <int V>
@@ -230,8 +233,8 @@ cudaError_t dispatch2(cudaStream_t st, const Dgemm2Params& p, bool had) {
   switch (w) {
     case 32: return launch2<G2W32<V>>(st, p);
     case 64: return launch2<G2W64<V>>(st, p);
-    case 96: return launch2<G2W96<V>>(st, p);
-    default: return launch2<G2L<V>>(st, p);
+    case 96: return launch2<G2W96_32<V>>(st, p);
+    default: return launch2<G2L32<V>>(st, p);
   }
 }
 

@@ -38,9 +38,9 @@ struct Dgemm2Params {
   const int* n_dev;
 };
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int VEC_, bool HAD_>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int VEC_, bool HAD_, int BK_ = 16>
 struct Gemm2Cfg {
-  static constexpr int BM = BM_, BN = BN_, BK = 16, WM = WM_, WN = WN_, STAGES = STAGES_, VEC = VEC_;
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_, VEC = VEC_;
   static constexpr bool HAD = HAD_;
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
