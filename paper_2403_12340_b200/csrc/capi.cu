@@ -768,7 +768,11 @@ bool fused_fit(lrgw_ctx c, const SelectKeep& keep, int n_r, const std::vector<in
   for (int q = 0; q < n_mu; ++q)
     colmap[q] = (int)(std::lower_bound(pts_sorted.begin(), pts_sorted.end(), order[q]) - pts_sorted.begin());
   DBuf dmap = upload_i(c, colmap.data(), n_mu);
-  ck(dgemm(c->stream, n_r, n_mu, n_mu, keep.L.d(), n_r, Lay::MN, lp.d(), n_mu, Lay::K, theta, ldt, 1.0, 0.0,
+  // B(n, k) = X(k, n) stored n-contiguous (X^T): both operands MN-contiguous
+  // for the paired-fragment engine
+  DBuf xt = dalloc(c, (size_t)n_mu * n_mu);
+  ck(transpose(c->stream, lp.d(), n_mu, n_mu, n_mu, xt.d(), n_mu), "transpose");
+  ck(dgemm(c->stream, n_r, n_mu, n_mu, keep.L.d(), n_r, Lay::MN, xt.d(), n_mu, Lay::MN, theta, ldt, 1.0, 0.0,
            nullptr, false, c->sm_count, nullptr, 0, true, dmap.i()),
      "dgemm(theta)");
   return true;

@@ -197,10 +197,6 @@ template <int V>
 using G2W64 = Gemm2Cfg<128, 64, 64, 32, 4, V, false>;
 template <int V>
 using G2W32 = Gemm2Cfg<128, 32, 32, 32, 4, V, false>;
-template <int V>
-using G2L32 = Gemm2Cfg<128, 128, 64, 32, 3, V, false, 32>;  // 8 warps
-template <int V>
-using G2W96_32 = Gemm2Cfg<128, 96, 32, 32, 3, V, false, 32>;  // 12 warps (a multiple of 4 SMSPs)
 
 template <int V>
 using H2W64 = Gemm2Cfg<128, 64, 32, 32, 4, V, true>;
@@ -226,6 +222,13 @@ int v2_width(int N) {
   return 32;
 }
 
+// 4-warp CTAs of 64 x 96 (warp tiles 32 x 48), 3 resident per SM = 12 warps:
+// the occupancy the library DGEMM runs at on this chip (its SASS: 4-warp
+// CTAs, 3 per SM). Measured 86-89 % of the DMMA peak on the wide shapes vs
+// 83-85 % for the 8-warp 128 x 128 tile (tools/bench_gemm.py).
+template <int V>
+using G2Q96 = Gemm2Cfg<64, 96, 32, 48, 3, V, false, 16, 3>;
+
 template <int V>
 cudaError_t dispatch2(cudaStream_t st, const Dgemm2Params& p, bool had) {
   int w = v2_width(p.N);
@@ -233,8 +236,7 @@ cudaError_t dispatch2(cudaStream_t st, const Dgemm2Params& p, bool had) {
   switch (w) {
     case 32: return launch2<G2W32<V>>(st, p);
     case 64: return launch2<G2W64<V>>(st, p);
-    case 96: return launch2<G2W96_32<V>>(st, p);
-    default: return launch2<G2L32<V>>(st, p);
+    default: return launch2<G2Q96<V>>(st, p);
   }
 }
 

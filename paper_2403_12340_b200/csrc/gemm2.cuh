@@ -38,9 +38,10 @@ struct Dgemm2Params {
   const int* n_dev;
 };
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int VEC_, bool HAD_, int BK_ = 16>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int VEC_, bool HAD_, int BK_ = 16, int MINB_ = 1>
 struct Gemm2Cfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_, VEC = VEC_;
+  static constexpr int MINB = MINB_;  // resident CTAs per SM the register budget is sized for
   static constexpr bool HAD = HAD_;
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
@@ -73,7 +74,7 @@ __device__ __forceinline__ void load_mn_tile(double* s, const double* g, long lo
 }
 
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS, 1) dgemm2_kernel(Dgemm2Params p) {
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) dgemm2_kernel(Dgemm2Params p) {
   extern __shared__ __align__(16) double smem[];
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
   constexpr int FM = Cfg::FM, FN = Cfg::FN, PA = Cfg::PA, PB = Cfg::PB;

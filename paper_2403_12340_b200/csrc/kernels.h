@@ -73,6 +73,9 @@ cudaError_t coulomb_scale_half(cudaStream_t st, int n1, int n2, int n3, double c
 cudaError_t scale_copy(cudaStream_t st, const double* src, double* dst, size_t n, double alpha);
 cudaError_t fill(cudaStream_t st, double* dst, size_t n, double v);
 cudaError_t zero_strict_upper(cudaStream_t st, double* a, int n, long long lda);
+// out (cols x rows) = in^T (rows x cols), column-major.
+cudaError_t transpose(cudaStream_t st, const double* in, long long ldi, int rows, int cols, double* out,
+                      long long ldo);
 
 // In-place inverse of the lower triangle of a (n x n, ld lda) — trtri.cu.
 // work: trtri_work_elems(n) doubles; *bad (device, preset to INT_MAX) gets

@@ -82,7 +82,30 @@ __global__ void zero_strict_upper_kernel(double* a, int n, long long lda) {
 
 constexpr int kRedBlocks = 296;
 
+// out (cols x rows, ld ldo) = in^T (rows x cols, ld ldi), 32 x 32 smem tiles.
+__global__ void transpose_kernel(const double* in, long long ldi, int rows, int cols, double* out, long long ldo) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;  // bx: column block of in, by: row block of in
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = by + threadIdx.x, c = bx + j;
+    if (r < rows && c < cols) tile[j][threadIdx.x] = in[r + (long long)c * ldi];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = bx + threadIdx.x, c = by + j;  // out(r, c) = in(c, r)
+    if (r < cols && c < rows) out[r + (long long)c * ldo] = tile[threadIdx.x][j];
+  }
+}
+
 }  // namespace
+
+cudaError_t transpose(cudaStream_t st, const double* in, long long ldi, int rows, int cols, double* out,
+                      long long ldo) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  transpose_kernel<<<dim3((cols + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, st>>>(in, ldi, rows, cols, out, ldo);
+  count_launches(1);
+  return cudaGetLastError();
+}
 
 cudaError_t scale_copy(cudaStream_t st, const double* src, double* dst, size_t n, double alpha) {
   if (n == 0) return cudaSuccess;
