@@ -7,6 +7,7 @@
 
 #include "gemm.cuh"
 #include "gemm2.cuh"
+#include "gemm3.cuh"
 #include "kernels.h"
 
 namespace lrgw_dev {
@@ -118,6 +119,42 @@ cudaError_t launch_tall(cudaStream_t st, const DgemmParams& p, int q) {
 bool tall_family_enabled() {
   static const bool on = !(getenv("LRGW_TALL") && atoi(getenv("LRGW_TALL")) == 0);
   return on;
+}
+
+// ---- v3 (paired fragments for either layout) configurations ---------------
+// Symmetric (lower-tile) outputs: 64 x 64 tiles, 4 warps of 32 x 32, 3 per SM.
+template <bool AK, bool BK, int V>
+using G3S = Gemm3Cfg<64, 64, 32, 32, 3, AK, BK, V, 16, 3>;
+
+template <class Cfg>
+cudaError_t launch3(cudaStream_t st, const DgemmParams& p, int splits) {
+  dim3 grid;
+  if (p.lower) {
+    const int t = (p.M + Cfg::BM - 1) / Cfg::BM;
+    grid = dim3(t * (t + 1) / 2, 1, splits);
+  } else {
+    grid = dim3((p.N + Cfg::BN - 1) / Cfg::BN, (p.M + Cfg::BM - 1) / Cfg::BM, splits);
+  }
+  if (grid.x == 0 || grid.y == 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(dgemm3_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Cfg::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  dgemm3_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(p); count_launches(1);
+  return cudaGetLastError();
+}
+
+template <template <bool, bool, int> class C>
+cudaError_t launch3_layout(cudaStream_t st, const DgemmParams& p, bool ak, bool bk, bool vec, int splits) {
+  if (vec) {
+    if (!ak && !bk) return launch3<C<false, false, 2>>(st, p, splits);
+    if (!ak && bk) return launch3<C<false, true, 2>>(st, p, splits);
+    if (ak && !bk) return launch3<C<true, false, 2>>(st, p, splits);
+    return launch3<C<true, true, 2>>(st, p, splits);
+  }
+  if (!ak && !bk) return launch3<C<false, false, 1>>(st, p, splits);
+  if (!ak && bk) return launch3<C<false, true, 1>>(st, p, splits);
+  if (ak && !bk) return launch3<C<true, false, 1>>(st, p, splits);
+  return launch3<C<true, true, 1>>(st, p, splits);
 }
 
 // Split count that fills whole waves of `slots` resident CTAs: the smallest
@@ -290,11 +327,11 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
   int occ;
   if (lower) {
     // symmetric outputs: 64x64 lower tiles + split-K (measured faster than
-    // 128x128 tiles for the long-K SYRK of Theta^T V Theta)
+    // 128x128 tiles for the long-K SYRK of Theta^T V Theta: 4.52 vs 4.66 ms)
     tile = Tile::S;
     const long long t = (M + 63) / 64;
     tiles = t * (t + 1) / 2;
-    occ = 2;
+    occ = 3;  // v3 engine, 3 CTAs per SM
   } else if (!ak && va && vb && !scale && !n_dev && N > 32 && N <= 128 && ((N + 15) / 16) % 2 == 1 &&
              (long long)((M + 127) / 128) >= 2LL * sm_count && tall_family_enabled()) {
     // tall-skinny with N in (32, 48], (64, 80], (96, 112]: one column tile of
@@ -344,6 +381,14 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
     p.k_chunk = kc;
     p.partial = work;
     p.part_stride = (long long)M * N;
+  }
+  if (lower) {
+    // symmetric outputs on the v3 engine (either operand layout, scale, split-K)
+    cudaError_t e = launch3_layout<G3S>(st, p, ak, bk, va && vb, splits);
+    if (e != cudaSuccess || splits <= 1) return e;
+    splitk_reduce_kernel<<<1184, 256, 0, st>>>(work, splits, (long long)M * N, M, N, C, ldc, beta, 1, 64);
+    count_launches(1);
+    return cudaGetLastError();
   }
   // v2 (paired fragments) wins for full-width tiles; narrow outputs stay on v1
   // (and for tall-skinny outputs whose width is a multiple of 32: 32 / 64 / 96)
