@@ -266,6 +266,27 @@ int v2_width(int N) {
 template <int V>
 using G2Q96 = Gemm2Cfg<64, 96, 32, 48, 3, V, false, 16, 3>;
 
+// Tall-skinny widths 48 / 80 / 112: 4-warp 64-row CTAs (warp tiles 16 x 16q).
+template <int V>
+using G2Q48 = Gemm2Cfg<64, 48, 16, 48, 3, V, false, 16, 3>;
+template <int V>
+using G2Q80 = Gemm2Cfg<64, 80, 16, 80, 3, V, false, 16, 3>;
+template <int V>
+using G2Q112 = Gemm2Cfg<64, 112, 16, 112, 3, V, false, 16, 2>;
+template <int V>
+using G2Q128 = Gemm2Cfg<64, 128, 32, 64, 3, V, false, 16, 2>;
+
+// Tall-skinny outputs of width 16q, q odd (the even widths use dispatch2).
+template <int V>
+cudaError_t dispatch2_odd(cudaStream_t st, const Dgemm2Params& p) {
+  const int q = (p.N + 15) / 16;
+  if (q >= 8) return launch2<G2Q128<V>>(st, p);
+  if (q <= 3) return launch2<G2Q48<V>>(st, p);
+  if (q <= 5) return launch2<G2Q80<V>>(st, p);
+  if (q <= 6) return launch2<G2Q96<V>>(st, p);
+  return launch2<G2Q112<V>>(st, p);
+}
+
 template <int V>
 cudaError_t dispatch2(cudaStream_t st, const Dgemm2Params& p, bool had) {
   int w = v2_width(p.N);
@@ -392,9 +413,10 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
   }
   // v2 (paired fragments) wins for full-width tiles; narrow outputs stay on v1
   // (and for tall-skinny outputs whose width is a multiple of 32: 32 / 64 / 96)
-  const bool narrow_v2 = !ak && !bk && !lower && !scale && !cin && splits <= 1 && N > 16 && N <= 96 &&
-                         ((N + 15) / 16) % 2 == 0 && (long long)((M + 127) / 128) >= 2LL * sm_count &&
-                         (tile == Tile::W96 || tile == Tile::L || tile == Tile::N);
+  const bool narrow_v2 = !ak && !bk && !lower && !scale && !cin && splits <= 1 && N > 16 &&
+                         N <= 128 && ((N + 15) / 16) % 2 == 0 &&
+                         (long long)((M + 127) / 128) >= 2LL * sm_count &&
+                         (tile == Tile::W96 || tile == Tile::W128 || tile == Tile::L || tile == Tile::N);
   if (narrow_v2 || (!ak && !bk && !lower && !scale && !cin && splits <= 1 && N >= 128 && tile == Tile::L)) {
     Dgemm2Params q{};
     q.M = M;
@@ -411,11 +433,30 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
     q.tri_b = tri_b ? 1 : 0;
     q.colmap = colmap;
     q.n_dev = n_dev;
+    if (N > 96 && N <= 128 && narrow_v2 && va && vb) return dispatch2_odd<2>(st, q);
     return (va && vb) ? dispatch2<2>(st, q, false) : dispatch2<1>(st, q, false);
   }
   cudaError_t e;
   if (tile == Tile::T) {
     const int q = (N + 15) / 16;
+    if (!bk && va && vb && !cin) {  // (the gathered beta term stays on v1)
+      Dgemm2Params t{};
+      t.M = M;
+      t.N = N;
+      t.K = K;
+      t.A = A;
+      t.lda = lda;
+      t.B = B;
+      t.ldb = ldb;
+      t.C = C;
+      t.ldc = ldc;
+      t.alpha = alpha;
+      t.beta = beta;
+      t.tri_b = tri_b ? 1 : 0;
+      t.colmap = colmap;
+      t.n_dev = n_dev;
+      return dispatch2_odd<2>(st, t);
+    }
     return bk ? launch_tall<true>(st, p, q) : launch_tall<false>(st, p, q);
   }
   if (!ak && !bk) e = launch_layout<false, false>(st, p, tile, va, vb, splits);
