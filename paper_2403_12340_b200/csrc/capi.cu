@@ -588,7 +588,7 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
   DBuf top2(c, (size_t)(s + 1) * sizeof(HostEnt));
   DBuf tmp(c, select_topk_tmp_bytes(n_r, s + 1));
   DBuf cand = ialloc(c, s), oldc = ialloc(c, s);
-  DBuf lcand = dalloc(c, (size_t)s * s), mprime = dalloc(c, (size_t)s * s);
+  DBuf lcand = dalloc(c, (size_t)s * s), mprime = dalloc(c, (size_t)s * s), mpt = dalloc(c, (size_t)s * (s + 1));
   DBuf order = ialloc(c, std::max(steps, 1)), margin = dalloc(c, std::max(steps, 1));
   std::vector<char> hpkt(pkt_bytes);
   const HostEnt* htop = reinterpret_cast<const HostEnt*>(hpkt.data() + 16);
@@ -655,9 +655,12 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
     ck(select_cand_greedy(c->stream, n_r, se, steps, k, top2.p, Wn, pos.i(), perm.i(), lcand.d(), mprime.d(),
                           order.i(), min_margin ? margin.d() : nullptr, bout),
        "cand_greedy");
-    // L[:, k:k+nb] = W M' (M' = E L_sel^-T, s_e x nb), nb read on the device
+    // L[:, k:k+nb] = W M' (M' = E L_sel^-T, s_e x nb), nb read on the device;
+    // M'^T stored n-contiguous so both operands stream MN-contiguous
     const int nmax = std::min(se, steps - k);
-    ck(dgemm(c->stream, n_r, nmax, se, Wn, n_r, Lay::MN, mprime.d(), se, Lay::K, L.d() + (size_t)k * n_r, n_r, 1.0,
+    const int ldt = nmax + (nmax & 1);
+    ck(transpose(c->stream, mprime.d(), se, se, nmax, mpt.d(), ldt), "transpose");
+    ck(dgemm(c->stream, n_r, nmax, se, Wn, n_r, Lay::MN, mpt.d(), ldt, Lay::MN, L.d() + (size_t)k * n_r, n_r, 1.0,
              0.0, nullptr, false, c->sm_count, nullptr, 0, false, nullptr, bout),
        "dgemm(L block)");
     ck(select_downdate(c->stream, L.d(), n_r, k, 0, pos.i(), d.d(), bout), "downdate");

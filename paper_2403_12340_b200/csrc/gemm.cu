@@ -275,6 +275,10 @@ template <int V>
 using G2Q112 = Gemm2Cfg<64, 112, 16, 112, 3, V, false, 16, 2>;
 template <int V>
 using G2Q128 = Gemm2Cfg<64, 128, 32, 64, 3, V, false, 16, 2>;
+// Device-bounded N: 16 warps of 16 x 32, four per column slice so skipping
+// the dead slices unloads every SM sub-partition equally.
+template <int V>
+using G2N128 = Gemm2Cfg<64, 128, 16, 32, 3, V, false, 16, 2, true>;
 
 // Tall-skinny outputs of width 16q, q odd (the even widths use dispatch2).
 template <int V>
@@ -414,7 +418,7 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
   // v2 (paired fragments) wins for full-width tiles; narrow outputs stay on v1
   // (and for tall-skinny outputs whose width is a multiple of 32: 32 / 64 / 96)
   const bool narrow_v2 = !ak && !bk && !lower && !scale && !cin && splits <= 1 && N > 16 &&
-                         N <= 128 && ((N + 15) / 16) % 2 == 0 &&
+                         N <= 128 && (n_dev || ((N + 15) / 16) % 2 == 0) &&
                          (long long)((M + 127) / 128) >= 2LL * sm_count &&
                          (tile == Tile::W96 || tile == Tile::W128 || tile == Tile::L || tile == Tile::N);
   if (narrow_v2 || (!ak && !bk && !lower && !scale && !cin && splits <= 1 && N >= 128 && tile == Tile::L)) {
@@ -433,6 +437,9 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
     q.tri_b = tri_b ? 1 : 0;
     q.colmap = colmap;
     q.n_dev = n_dev;
+    // a device-bounded N (the selection's L block) takes 96-wide column tiles:
+    // the CTAs past the live columns exit at once
+    if (n_dev && narrow_v2 && va && vb) return launch2<G2N128<2>>(st, q);
     if (N > 96 && N <= 128 && narrow_v2 && va && vb) return dispatch2_odd<2>(st, q);
     return (va && vb) ? dispatch2<2>(st, q, false) : dispatch2<1>(st, q, false);
   }

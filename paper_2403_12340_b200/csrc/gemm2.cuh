@@ -38,10 +38,12 @@ struct Dgemm2Params {
   const int* n_dev;
 };
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int VEC_, bool HAD_, int BK_ = 16, int MINB_ = 1>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int VEC_, bool HAD_, int BK_ = 16, int MINB_ = 1,
+          bool SKIP_ = false>
 struct Gemm2Cfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_, VEC = VEC_;
   static constexpr int MINB = MINB_;  // resident CTAs per SM the register budget is sized for
+  static constexpr bool SKIP = SKIP_;  // warps wholly past a device-bounded N skip their MMAs
   static constexpr bool HAD = HAD_;
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
@@ -90,6 +92,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) dgemm2_kernel(Dgemm2P
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp % Cfg::WARPS_M) * Cfg::WM, wn = (warp / Cfg::WARPS_M) * Cfg::WN;
   const int g = lane >> 2, t = lane & 3;
+  const bool live = !Cfg::SKIP || n0 + wn < N;
 
   double acc[FM][FN][2];
   double first[Cfg::HAD ? FM : 1][Cfg::HAD ? FN : 1][2];
@@ -120,6 +123,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) dgemm2_kernel(Dgemm2P
     __syncthreads();
     if (kt + STAGES - 1 < nkt) issue(kt + STAGES - 1);
     cp_async_commit();
+    if (Cfg::SKIP && !live) continue;
     const double* sa = smem + (kt % STAGES) * Cfg::STAGE_ELEMS;
     const double* sb = sa + BK * PA;
 #pragma unroll
