@@ -574,105 +574,64 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
   const int kmax = (int)std::min<long long>(m, n_r);
   const int steps = std::min(n_mu, kmax);
   const int s = std::max(1, std::min({c->select_batch, select_max_candidates(), n_r}));
+  const int lds = s + (s & 1);  // even leading dims: 16-byte operand loads
 
   DBuf d = dalloc(c, n_r), pos = ialloc(c, n_r), perm = ialloc(c, n_r);
   DBuf L = dalloc(c, (size_t)n_r * std::max(steps, 1));
-  DBuf Wbuf[2] = {dalloc(c, (size_t)n_r * s), dalloc(c, (size_t)n_r * s)};
-  DBuf amu = dalloc(c, (size_t)(s + 1) * n1), bmu = dalloc(c, (size_t)(s + 1) * n2);
-  DBuf lcg = dalloc(c, (size_t)(s + 1) * std::max(steps, 1));
-  // one device->host packet per block: {nb, k_next, pad, pad} then s+1 candidates
-  const size_t pkt_bytes = 16 + (size_t)(s + 1) * sizeof(HostEnt);
-  DBuf pkt(c, pkt_bytes);
-  int* bout = static_cast<int*>(pkt.p);
-  void* top = static_cast<char*>(pkt.p) + 16;
-  DBuf top2(c, (size_t)(s + 1) * sizeof(HostEnt));
+  DBuf wsel = dalloc(c, (size_t)n_r * s);                       // W columns of the accepted pivots
+  DBuf amu = dalloc(c, (size_t)lds * n1), bmu = dalloc(c, (size_t)lds * n2);
+  DBuf lrow = dalloc(c, (size_t)lds * std::max(steps, 1));       // L rows of candidates / pivots
+  DBuf wcc = dalloc(c, (size_t)s * s), xcol = dalloc(c, (size_t)s * s);
+  DBuf bout_d = ialloc(c, 4);
+  int* bout = bout_d.i();
+  DBuf top(c, (size_t)(s + 1) * sizeof(HostEnt));
   DBuf tmp(c, select_topk_tmp_bytes(n_r, s + 1));
-  DBuf cand = ialloc(c, s), oldc = ialloc(c, s);
-  DBuf lcand = dalloc(c, (size_t)s * s), mprime = dalloc(c, (size_t)s * s), mpt = dalloc(c, (size_t)s * (s + 1));
+  DBuf cand = ialloc(c, s);
   DBuf order = ialloc(c, std::max(steps, 1)), margin = dalloc(c, std::max(steps, 1));
-  std::vector<char> hpkt(pkt_bytes);
-  const HostEnt* htop = reinterpret_cast<const HostEnt*>(hpkt.data() + 16);
+  Work w = make_work(c, (size_t)8 * s * s);
 
   ck(select_init(c->stream, a, lda, n1, b, ldb, n2, n_r, d.d(), pos.i(), perm.i()), "select_init");
   ck(select_topk_reset(c->stream, tmp.p), "select_topk_reset");
-  ck(select_topk(c->stream, d.d(), pos.i(), n_r, 0, s + 1, tmp.p, top), "select_topk");
-  download(c, hpkt.data(), pkt.p, pkt_bytes);
-  // Candidate columns carried between blocks: a still-unaccepted candidate's
-  // W column only needs the previous block's b new L columns subtracted.
-  std::vector<int> col_of(n_r, -1);  // grid row -> column of the previous W
-  std::vector<int> prev_rows;
-  std::vector<HostEnt> htop2(s + 1);
-  std::vector<int> hcand(s), hold(s);
-  int k = 0, k_prev = 0, b_prev = 0, cur = 0;
+  int k = 0;
   while (k < steps) {
     const int se = std::min(s, n_r - k);
-    // reorder: reused candidates first (their previous columns), new ones after
-    int n_re = 0;
-    for (int i = 0; i < se; ++i)
-      if (htop[i].row >= 0 && col_of[htop[i].row] >= 0) {
-        hold[n_re] = col_of[htop[i].row];
-        htop2[n_re++] = htop[i];
-      }
-    int n_new = 0;
-    for (int i = 0; i < se; ++i)
-      if (!(htop[i].row >= 0 && col_of[htop[i].row] >= 0)) htop2[n_re + n_new++] = htop[i];
-    htop2[se] = htop[se];
-    for (int i = 0; i < se; ++i) hcand[i] = htop2[i].row < 0 ? 0 : htop2[i].row;
-    for (int r : prev_rows) col_of[r] = -1;
-    prev_rows.assign(hcand.begin(), hcand.begin() + se);
-    for (int i = 0; i < se; ++i)
-      if (htop2[i].row >= 0) col_of[htop2[i].row] = i;
-    if (select_trace())
-      fprintf(stderr, "select block k=%d se=%d n_re=%d n_new=%d b_prev=%d\n", k, se, n_re, n_new, b_prev);
-    ck(cudaMemcpyAsync(top2.p, htop2.data(), sizeof(HostEnt) * (se + 1), cudaMemcpyHostToDevice, c->stream), "H2D");
-    ck(cudaMemcpyAsync(cand.p, hcand.data(), sizeof(int) * se, cudaMemcpyHostToDevice, c->stream), "H2D");
-    double* Wn = Wbuf[cur].d();
-    double* Wp = Wbuf[1 - cur].d();
-    if (n_re > 0) {
-      ck(cudaMemcpyAsync(oldc.p, hold.data(), sizeof(int) * n_re, cudaMemcpyHostToDevice, c->stream), "H2D");
-      const int ldr = n_re + (n_re & 1);  // even ld: 16-byte operand loads
-      ck(gather_rows(c->stream, L.d() + (size_t)k_prev * n_r, n_r, b_prev, cand.i(), n_re, lcg.d(), ldr), "gather");
-      // W(:, reused) = Wprev(:, old columns) - L_prev_block L_prev_block[reused, :]^T (column gather in the epilogue)
-      ck(dgemm(c->stream, n_r, n_re, b_prev, L.d() + (size_t)k_prev * n_r, n_r, Lay::MN, lcg.d(), ldr, Lay::MN, Wn,
-               n_r, -1.0, 1.0, nullptr, false, c->sm_count, nullptr, 0, false, nullptr, nullptr, Wp, n_r, oldc.i()),
-         "dgemm(reuse)");
+    // Candidate set C (top s by residual, position) and its Schur block
+    //   W[C, C] = (A_C A_C^T) o (B_C B_C^T) - L[C, :k] L[C, :k]^T
+    // (s x s: only the candidates' rows ever enter the greedy).
+    ck(select_topk(c->stream, d.d(), pos.i(), n_r, k, se + 1, tmp.p, top.p), "select_topk");
+    ck(select_cand_rows(c->stream, top.p, se, cand.i()), "cand_rows");
+    ck(gather_rows(c->stream, a, lda, n1, cand.i(), se, amu.d(), lds), "gather");
+    ck(gather_rows(c->stream, b, ldb, n2, cand.i(), se, bmu.d(), lds), "gather");
+    ck(hadamard_gemm(c->stream, se, se, amu.d(), lds, amu.d(), lds, n1, bmu.d(), lds, bmu.d(), lds, n2, wcc.d(), se,
+                     1.0, 0.0),
+       "hadamard_gemm(W_CC)");
+    if (k > 0) {
+      ck(gather_rows(c->stream, L.d(), n_r, k, cand.i(), se, lrow.d(), lds), "gather");
+      gemm(c, se, se, k, lrow.d(), lds, Lay::MN, lrow.d(), lds, Lay::MN, wcc.d(), se, -1.0, 1.0, nullptr, false, &w);
     }
-    if (n_new > 0) {
-      // W(:, new) = G(:, new) - L[:, :k] L[new, :k]^T
-      double* Wnew = Wn + (size_t)n_re * n_r;
-      const int* cn = cand.i() + n_re;
-      const int ldn = n_new + (n_new & 1);
-      ck(gather_rows(c->stream, a, lda, n1, cn, n_new, amu.d(), ldn), "gather");
-      ck(gather_rows(c->stream, b, ldb, n2, cn, n_new, bmu.d(), ldn), "gather");
-      ck(hadamard_gemm(c->stream, n_r, n_new, a, lda, amu.d(), ldn, n1, b, ldb, bmu.d(), ldn, n2, Wnew, n_r, 1.0,
-                       0.0),
-         "hadamard_gemm");
-      if (k > 0) {
-        ck(gather_rows(c->stream, L.d(), n_r, k, cn, n_new, lcg.d(), ldn), "gather");
-        gemm(c, n_r, n_new, k, L.d(), n_r, Lay::MN, lcg.d(), ldn, Lay::MN, Wnew, n_r, -1.0, 1.0);
-      }
-    }
-    ck(select_cand_greedy(c->stream, n_r, se, steps, k, top2.p, Wn, pos.i(), perm.i(), lcand.d(), mprime.d(),
-                          order.i(), min_margin ? margin.d() : nullptr, bout),
+    ck(select_cand_greedy(c->stream, n_r, se, steps, k, top.p, wcc.d(), pos.i(), perm.i(), xcol.d(), order.i(),
+                          min_margin ? margin.d() : nullptr, bout),
        "cand_greedy");
-    // L[:, k:k+nb] = W M' (M' = E L_sel^-T, s_e x nb), nb read on the device;
-    // M'^T stored n-contiguous so both operands stream MN-contiguous
-    const int nmax = std::min(se, steps - k);
-    const int ldt = nmax + (nmax & 1);
-    ck(transpose(c->stream, mprime.d(), se, se, nmax, mpt.d(), ldt), "transpose");
-    ck(dgemm(c->stream, n_r, nmax, se, Wn, n_r, Lay::MN, mpt.d(), ldt, Lay::MN, L.d() + (size_t)k * n_r, n_r, 1.0,
-             0.0, nullptr, false, c->sm_count, nullptr, 0, false, nullptr, bout),
-       "dgemm(L block)");
-    ck(select_downdate(c->stream, L.d(), n_r, k, 0, pos.i(), d.d(), bout), "downdate");
-    // next block's candidates (k_next read on the device), one sync per block
-    ck(select_topk(c->stream, d.d(), pos.i(), n_r, 0, s + 1, tmp.p, top, bout + 1), "select_topk");
-    download(c, hpkt.data(), pkt.p, pkt_bytes);
-    const int nb = reinterpret_cast<const int*>(hpkt.data())[0];
+    int nb = 0;
+    download(c, &nb, bout, sizeof(int));  // the one host sync per block
     if (nb <= 0) fail(LRGW_ERR_INTERNAL, "select: no progress (non-finite residuals?)");
-    k_prev = k;
-    b_prev = nb;
+    if (select_trace()) fprintf(stderr, "select block k=%d se=%d b=%d\n", k, se, nb);
+    // Full-length W columns of the nb accepted pivots only (grid rows
+    // order[k .. k+nb)), then L[:, k:k+nb] = W_sel X^T with X = L_sel^-1.
+    const int* srow = order.i() + k;
+    const int ldb_ = nb + (nb & 1);
+    ck(gather_rows(c->stream, a, lda, n1, srow, nb, amu.d(), ldb_), "gather");
+    ck(gather_rows(c->stream, b, ldb, n2, srow, nb, bmu.d(), ldb_), "gather");
+    ck(hadamard_gemm(c->stream, n_r, nb, a, lda, amu.d(), ldb_, n1, b, ldb, bmu.d(), ldb_, n2, wsel.d(), n_r, 1.0,
+                     0.0),
+       "hadamard_gemm");
+    if (k > 0) {
+      ck(gather_rows(c->stream, L.d(), n_r, k, srow, nb, lrow.d(), ldb_), "gather");
+      gemm(c, n_r, nb, k, L.d(), n_r, Lay::MN, lrow.d(), ldb_, Lay::MN, wsel.d(), n_r, -1.0, 1.0);
+    }
+    gemm(c, n_r, nb, nb, wsel.d(), n_r, Lay::MN, xcol.d(), se, Lay::MN, L.d() + (size_t)k * n_r, n_r, 1.0, 0.0);
+    ck(select_downdate(c->stream, L.d(), n_r, k, nb, pos.i(), d.d()), "downdate");
     k += nb;
-    cur = 1 - cur;
   }
   std::vector<int32_t> pts(n_mu);
   download(c, pts.data(), perm.p, sizeof(int) * n_mu);

@@ -305,24 +305,14 @@ constexpr int CG_MAX = 128;              // candidates
 struct CandParams {
   int n_r, s, steps, kb;
   const Ent* top;       // s + 1 entries: candidates then the tau entry
-  const double* wcc;    // s x s: W[C, C], row-major (wcc[j + i s] = W(row_i, j))
+  const double* wcc;    // s x s, ld s: W[C, C] (symmetric)
   int* pos;             // grid row -> position
   int* perm;            // position -> grid row
-  double* mprime;       // s x s: E L_sel^-T (rows of unselected candidates zero)
+  double* xcol;         // s x s, ld s: X = L_sel^-1 column-major (b x b lower, zero above)
   int* piv_order;       // [steps]
   double* margin;       // [steps] or nullptr
   int* b_out;           // number of accepted steps
 };
-
-// wcc[j + i s] = W[row_i, j]: the candidates' Schur block, gathered once by
-// many CTAs so the greedy CTA reads it coalesced.
-__global__ void gather_cc_kernel(const double* W, int n_r, int s, const Ent* top, double* wcc) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= s * s) return;
-  const int i = idx / s, j = idx % s;
-  const int g = top[i].row;
-  wcc[idx] = g >= 0 ? W[g + (long long)j * n_r] : 0.0;
-}
 
 __device__ __forceinline__ double pick8(const double (&x)[CG_ROWS], int r) {
   double v = x[0];
@@ -384,7 +374,7 @@ __device__ __forceinline__ void cand_argmax(const double (&dj)[4], const int (&p
 //   the diagonal blocks are inverted by one warp each (lane = column,
 //   unrolled forward substitution with reciprocal pivots), then block row I
 //   takes X_Ik = -X_II sum_{m=k}^{I-1} L_Im X_mk (k < I) — all threads.
-__device__ void cand_tri_inverse(double* lcs, double* lsel, const int* sel, int b, int s, double* mprime) {
+__device__ void cand_tri_inverse(double* lcs, double* lsel, const int* sel, int b, int s, double* xcol) {
   __shared__ double rdiag[CG_MAX];
   double* X = lcs;
   auto L = [&](int i, int m) -> double {  // L_sel (identity beyond b)
@@ -441,7 +431,7 @@ __device__ void cand_tri_inverse(double* lcs, double* lsel, const int* sel, int 
   // M'[sel[j]][i] = X[i][j] (i >= j); the rows of unselected candidates stay 0
   for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
     const int i = idx / b, j = idx % b;
-    if (j <= i) mprime[sel[j] + (size_t)i * s] = X[i * CG_MAX + j];
+    if (j <= i) xcol[i + (size_t)j * s] = X[i * CG_MAX + j];
   }
 }
 
@@ -472,7 +462,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
   __shared__ int pss[CG_MAX];  // controller: perm[kb + j] (position slots of the block)
   __shared__ unsigned usedsh[4];  // candidates taken / absent before this step (bit l of word c: l + 32 c)
 
-  for (int idx = threadIdx.x; idx < s * s; idx += blockDim.x) p.mprime[idx] = 0.0;
+  for (int idx = threadIdx.x; idx < s * s; idx += blockDim.x) p.xcol[idx] = 0.0;
 
   const double tau = p.top[s].row >= 0 ? p.top[s].v : -DBL_MAX;
   const int tmax = min(s, p.steps - p.kb);
@@ -604,7 +594,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
     __syncthreads();
   }
   const int b = t;
-  cand_tri_inverse(lcs, lsel, sel, b, s, p.mprime);
+  cand_tri_inverse(lcs, lsel, sel, b, s, p.xcol);
   if (threadIdx.x == 0) {
     p.b_out[0] = b;
     p.b_out[1] = p.kb + b;  // next block start, consumed on the device
@@ -668,12 +658,10 @@ size_t select_cand_smem_bytes(int) {
 
 int select_max_candidates() { return CG_MAX; }
 
-cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* W,
-                               int* pos, int* perm, double* scratch, double* mprime, int* piv_order, double* margin,
-                               int* b_out) {
+cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* wcc,
+                               int* pos, int* perm, double* xcol, int* piv_order, double* margin, int* b_out) {
   const Ent* tp = static_cast<const Ent*>(top);
-  gather_cc_kernel<<<(s * s + 255) / 256, 256, 0, st>>>(W, n_r, s, tp, scratch); count_launches(1);
-  CandParams p{n_r, s, steps, kb, tp, scratch, pos, perm, mprime, piv_order, margin, b_out};
+  CandParams p{n_r, s, steps, kb, tp, wcc, pos, perm, xcol, piv_order, margin, b_out};
   const size_t smem = select_cand_smem_bytes(s);
   cudaError_t e = cudaFuncSetAttribute(cand_greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -20,12 +20,13 @@ cudaError_t select_topk(cudaStream_t st, const double* d, const int* pos, int n_
 cudaError_t select_cand_rows(cudaStream_t st, const void* top, int n, int* rows);
 int select_max_candidates();
 size_t select_cand_smem_bytes(int s);
-// Certified greedy on the s candidates (one CTA): accepted steps -> *b_out,
-// pivots, margins (if margin != nullptr), positions; mprime (s x b) = E L_sel^-T.
-// scratch: s x s doubles (the gathered candidate block).
-cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* W,
-                               int* pos, int* perm, double* scratch, double* mprime, int* piv_order, double* margin,
-                               int* b_out);
+// Certified greedy on the s candidates (one CTA) from their Schur block
+// wcc = W[C, C] (s x s, ld s, symmetric): accepted steps -> *b_out (and the
+// next block start -> b_out[1]), pivots (perm / pos / piv_order), margins (if
+// margin != nullptr); xcol (ld s) = X = L_sel^-1 column-major (b x b lower,
+// L_sel the accepted steps' l values at the accepted rows, in pivot order).
+cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* wcc,
+                               int* pos, int* perm, double* xcol, int* piv_order, double* margin, int* b_out);
 // d -= rowsum(L[:, kb:kb+b]^2) over unselected rows.
 cudaError_t select_downdate(cudaStream_t st, const double* L, int n_r, int kb, int b, const int* pos, double* d,
                             const int* b_dev = nullptr);
