@@ -160,7 +160,9 @@ cudaError_t launch3_layout(cudaStream_t st, const DgemmParams& p, bool ak, bool 
 // Split count that fills whole waves of `slots` resident CTAs: the smallest
 // s (each split >= 16 k-tiles) whose last wave is >= 90% full, else the best.
 int choose_splits(long long tiles, int ktiles, long long slots) {
-  const int smax = std::max(1, std::min(ktiles / 16, 64));
+  // chunks of >= 16 k-tiles; >= 4 when the tile grid is a handful of CTAs
+  const int min_chunk = tiles * 8 < slots ? 4 : 16;
+  const int smax = std::max(1, std::min(ktiles / min_chunk, 64));
   int best = 1;
   double best_eff = 0.0;
   for (int s = 1; s <= smax; ++s) {
@@ -396,7 +398,8 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
   // split-K when the output tile grid cannot fill the chip and K is long
   int splits = 1;
   const int ktiles = (K + 15) / 16;
-  if (tiles < 2LL * sm_count * occ && ktiles >= 32 && work) {
+  if (tiles < 2LL * sm_count * occ && (ktiles >= 32 || (tiles * 8 < (long long)sm_count * occ && ktiles >= 8)) &&
+      work) {
     splits = choose_splits(tiles, ktiles, (long long)sm_count * occ);
     while (splits > 1 && (size_t)splits * M * N > work_elems) --splits;
   }
@@ -503,6 +506,10 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
       case 7: return go(CfgHT<7>{});
       default: return go(CfgHT<8>{});
     }
+  }
+  if (M <= 256 && N <= 256) {
+    // a candidate block's Schur block (s x s): 32 x 32 tiles for parallelism
+    return vec ? go(GemmCfg<32, 32, 16, 16, 3, false, false, 2, 2>{}) : go(GemmCfg<32, 32, 16, 16, 3, false, false, 1, 1>{});
   }
   if (N < 128) {
     if (prefer_narrow(N)) return vec ? go(CfgH32<2>{}) : go(CfgH32<1>{});
