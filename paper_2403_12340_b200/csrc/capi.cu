@@ -1201,7 +1201,11 @@ static void eps_apply_impl(lrgw_ctx c, lrgw_eps e, const double* x, long long ld
   } else {
     gemm(c, n_mu, m, n_r, e->theta, n_r, Lay::K, x, ldx, Lay::K, u.d(), n_mu, 1.0, 0.0, nullptr, false, &wk);
   }
-  gemm(c, n_mu, m, n_mu, e->k, n_mu, Lay::MN, u.d(), n_mu, Lay::K, w.d(), n_mu, 1.0, 0.0);
+  if (skinny_supported(m))  // w = K u = K^T u (K symmetric): the row-chunked stream
+    ck(skinny_tn(c->stream, e->k, n_mu, n_mu, n_mu, u.d(), n_mu, m, w.d(), n_mu, wk.buf.d(), wk.elems, c->sm_count),
+       "skinny_tn(K)");
+  else
+    gemm(c, n_mu, m, n_mu, e->k, n_mu, Lay::MN, u.d(), n_mu, Lay::K, w.d(), n_mu, 1.0, 0.0);
   if (skinny_supported(m) && (size_t)n_mu * m * 8 <= 200 * 1024) {
     ck(skinny_nn(c->stream, e->theta, n_r, n_r, n_mu, w.d(), n_mu, m, z.d(), n_r, c->sm_count), "skinny_nn");
   } else {

@@ -6,6 +6,8 @@
 // (N_r x N_mu FP64, 906 MB at Si64); a DMMA tile would waste >90% of its
 // columns, so these are coalesced FMA streams: one pass over Theta each,
 // the small operand (x chunk / w) staged in shared memory.
+#include <cstdint>
+
 #include "kernels.h"
 
 namespace lrgw_dev {
@@ -41,17 +43,42 @@ __global__ void __launch_bounds__(TN_THREADS) tn_kernel(const double* theta, lon
   for (int i = 0; i < TN_MU_W; ++i)
 #pragma unroll
     for (int c = 0; c < M; ++c) acc[i][c] = 0.0;
-#pragma unroll 4
-  for (int r = r0 + lane; r < r1; r += 32) {
-    double xv[M], tv[TN_MU_W];
+  // pairs of rows per lane (16-byte loads) when the layout allows, then the tail
+  const bool vec = ((ldt | ldx | r0) & 1) == 0 && ((reinterpret_cast<uintptr_t>(theta) |
+                                                    reinterpret_cast<uintptr_t>(x)) & 15) == 0;
+  int r = r0 + 2 * lane;
+  if (vec) {
+    for (; r + 1 < r1; r += 64) {
+      double2 xv[M], tv[TN_MU_W];
 #pragma unroll
-    for (int c = 0; c < M; ++c) xv[c] = __ldg(x + r + (long long)c * ldx);
+      for (int c = 0; c < M; ++c) xv[c] = __ldg(reinterpret_cast<const double2*>(x + r + (long long)c * ldx));
 #pragma unroll
-    for (int i = 0; i < TN_MU_W; ++i) tv[i] = ok[i] ? __ldcs(th[i] + r) : 0.0;  // streamed once
+      for (int i = 0; i < TN_MU_W; ++i)
+        tv[i] = ok[i] ? __ldcs(reinterpret_cast<const double2*>(th[i] + r)) : make_double2(0.0, 0.0);
 #pragma unroll
-    for (int i = 0; i < TN_MU_W; ++i)
+      for (int i = 0; i < TN_MU_W; ++i)
 #pragma unroll
-      for (int c = 0; c < M; ++c) acc[i][c] = fma(tv[i], xv[c], acc[i][c]);
+        for (int c = 0; c < M; ++c) acc[i][c] = fma(tv[i].y, xv[c].y, fma(tv[i].x, xv[c].x, acc[i][c]));
+    }
+  } else {
+    r = r0 + lane;
+  }
+  for (; r < r1; r += vec ? 64 : 32) {  // scalar rows (the odd tail, or an unaligned layout)
+    const int rr = r;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int q = rr + h;
+      if (q >= r1 || (!vec && h == 1)) break;
+      double xv[M], tv[TN_MU_W];
+#pragma unroll
+      for (int c = 0; c < M; ++c) xv[c] = __ldg(x + q + (long long)c * ldx);
+#pragma unroll
+      for (int i = 0; i < TN_MU_W; ++i) tv[i] = ok[i] ? __ldcs(th[i] + q) : 0.0;
+#pragma unroll
+      for (int i = 0; i < TN_MU_W; ++i)
+#pragma unroll
+        for (int c = 0; c < M; ++c) acc[i][c] = fma(tv[i], xv[c], acc[i][c]);
+    }
   }
 #pragma unroll
   for (int i = 0; i < TN_MU_W; ++i)
