@@ -6,10 +6,12 @@ per-rank arrays (row panels of Phi, L, W, Theta) stay with a *stage backend*
 deterministic exchange logic:
 
   stage 1  grid-row panels aligned to z-planes; per candidate block one
-           all-gather of the local top-(s+1) lists, owner-contributed rows of
-           Phi / L / W[C, :] (sum of zero-padded contributions: exact), the
-           certified candidate greedy replicated on every rank, local panel
-           updates. Pivots are the greedy pivots (reference linalg.hpp:26-111).
+           all-gather of the local top-(s+1) lists and owner-contributed rows
+           of Phi / L at the candidates (sum of zero-padded contributions:
+           exact), the candidates' Schur block W[C, C] and the certified
+           greedy replicated on every rank, then the accepted pivots' W
+           columns and the L block on the local panel only. Pivots are the
+           greedy pivots (reference linalg.hpp:26-111).
   stage 2  Theta panel = L panel L_P^-1 (L_P rows owner-contributed).
   stage 3  quadrature nodes split across ranks, all-reduce of the partial T.
   stage 4-5a  z-slab 3-D FFT: local 2-D transforms, one all-to-all to
@@ -68,22 +70,24 @@ class Comm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # NCCL moves device buffers (over NVLink); gloo host buffers
+        self.device = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
 
     def _t(self, a):
         import torch
 
-        return torch.from_numpy(np.ascontiguousarray(a))
+        return torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
 
     def allreduce_sum(self, a):
         t = self._t(a)
         self.dist.all_reduce(t, group=self.group)
-        return t.numpy()
+        return t.cpu().numpy()
 
     def allgather(self, a):
         t = self._t(a)
         out = [t.clone() for _ in range(self.world)]
         self.dist.all_gather(out, t, group=self.group)
-        return [o.numpy() for o in out]
+        return [o.cpu().numpy() for o in out]
 
     def alltoall(self, blocks):
         """blocks[q] goes to rank q; returns the blocks received from each rank.
@@ -92,7 +96,8 @@ class Comm:
 
         send = [self._t(b) for b in blocks]
         shapes = self.allgather(np.array([b.size for b in blocks], dtype=np.int64))
-        recv = [torch.empty(int(shapes[q][self.rank]), dtype=send[0].dtype) for q in range(self.world)]
+        recv = [torch.empty(int(shapes[q][self.rank]), dtype=send[0].dtype, device=self.device)
+                for q in range(self.world)]
         try:
             self.dist.all_to_all([r for r in recv], [s.reshape(-1) for s in send], group=self.group)
         except (RuntimeError, ValueError):
@@ -105,7 +110,7 @@ class Comm:
                 reqs.append(self.dist.irecv(recv[q], q, group=self.group))
             for r in reqs:
                 r.wait()
-        return [r.numpy() for r in recv]
+        return [r.cpu().numpy() for r in recv]
 
 
 # ---------------------------------------------------------------------------
@@ -132,7 +137,8 @@ def cand_greedy(top, w_cc, kb, steps, pos, perm):
     """Exact greedy steps on the candidate Schur complement (select.cu
     cand_greedy_kernel semantics). top: s+1 entries (d, pos, row); w_cc: s x s.
     Mutates pos/perm (replicated position bookkeeping). Returns
-    (b, pivot rows, M' = E L_sel^-T (s x b), margins)."""
+    (b, pivot rows, X = L_sel^-1 (b x b, pivot order), margins); the block's
+    L columns are W[:, pivots] X^T."""
     s = len(top) - 1
     tau = top[s][0] if top[s][2] >= 0 else -math.inf
     d = np.array([e[0] for e in top[:s]], dtype=np.float64)
@@ -176,17 +182,14 @@ def cand_greedy(top, w_cc, kb, steps, pos, perm):
         pivots.append(prow)
         margins.append((best - max(second, tau)) / best if best > 0 else 0.0)
     b = len(sel)
-    mprime = np.zeros((s, b))
+    x = np.zeros((b, b))
     if b:
         lsel = np.array([[lcols[t2][sel[t1]] if t2 <= t1 else 0.0 for t2 in range(b)] for t1 in range(b)])
-        x = np.zeros((b, b))
         for j in range(b):
             for i in range(j, b):
                 acc = (1.0 if i == j else 0.0) - float(np.dot(lsel[i, j:i], x[j:i, j]))
                 x[i, j] = acc / lsel[i, i] if lsel[i, i] != 0.0 else 0.0
-        for j in range(b):
-            mprime[sel[j], :] = x[:, j]
-    return b, pivots, mprime, margins
+    return b, pivots, x, margins
 
 
 # ---------------------------------------------------------------------------
@@ -246,12 +249,17 @@ class DistributedBuild:
             amu = self._owned_rows(lambda i: be.row(phi_v_p, i), cand, n1)
             bmu = self._owned_rows(lambda i: be.row(phi_c_p, i), cand, n2)
             lc = self._owned_rows(lambda i: be.row(st.L, i)[:k], cand, k) if k else np.zeros((se, 0))
-            w_p = be.w_panel(phi_v_p, phi_c_p, amu, bmu, st.L, lc, k)
-            w_cc = self._owned_rows(lambda i: be.row(w_p, i), cand, se)
-            b, piv, mprime, margins = cand_greedy(top, w_cc, k, steps, pos, perm)
+            # the candidates' Schur block, replicated (s x s)
+            w_cc = (amu @ amu.T) * (bmu @ bmu.T) - lc @ lc.T
+            b, piv, x, margins = cand_greedy(top, w_cc, k, steps, pos, perm)
             if b <= 0:
                 raise RuntimeError("distributed select: no progress")
-            be.l_update(w_p, mprime, st.L, k, b)
+            # W columns of the accepted pivots on the local panel, then L block
+            amu_s = self._owned_rows(lambda i: be.row(phi_v_p, i), piv, n1)
+            bmu_s = self._owned_rows(lambda i: be.row(phi_c_p, i), piv, n2)
+            ls = self._owned_rows(lambda i: be.row(st.L, i)[:k], piv, k) if k else np.zeros((b, 0))
+            w_p = be.w_panel(phi_v_p, phi_c_p, amu_s, bmu_s, st.L, ls, k)
+            be.l_update(w_p, x, st.L, k, b)
             be.downdate(st.L, k, b, pos[st.r0:st.r1], st.d)
             st.pivots += piv
             st.margins += margins

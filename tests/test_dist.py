@@ -42,8 +42,8 @@ class NumpyBackend:
             w -= L[:, :k] @ lc.T
         return w
 
-    def l_update(self, w, mprime, L, k, b):
-        L[:, k:k + b] = w @ mprime
+    def l_update(self, w, x, L, k, b):
+        L[:, k:k + b] = w @ x.T
 
     def downdate(self, L, k, b, pos_p, d):
         m = pos_p >= k + b
