@@ -222,11 +222,20 @@ class DistributedBuild:
         self.st = RankState(r0, r1)
 
     # ---- owner contributions: rows of a panel array at global row indices --
-    def _owned_rows(self, panel_rows_fn, rows, width):
+    def _owned_rows(self, panel_rows_fn, rows, width, panel=None, cols=None):
+        """Rows of a panel array at global row indices: every rank contributes
+        the rows it owns (zeros elsewhere), summed across ranks (exact)."""
         out = np.zeros((len(rows), width))
-        for i, r in enumerate(rows):
-            if self.st.r0 <= r < self.st.r1:
-                out[i] = panel_rows_fn(r - self.st.r0)
+        mine = [(i, r - self.st.r0) for i, r in enumerate(rows) if self.st.r0 <= r < self.st.r1]
+        if mine and panel is not None and hasattr(self.be, "rows"):
+            vals = self.be.rows(panel, [j for _, j in mine])
+            if cols is not None:
+                vals = vals[:, :cols]
+            for (i, _), v in zip(mine, vals):
+                out[i] = v
+        else:
+            for i, j in mine:
+                out[i] = panel_rows_fn(j)
         return self.comm.allreduce_sum(out)
 
     def select(self, phi_v_p, phi_c_p):
@@ -246,18 +255,18 @@ class DistributedBuild:
             gathered = np.concatenate(self.comm.allgather(np.asarray(local, dtype=np.float64).reshape(-1, 3)))
             top = merge_top([(e[0], int(e[1]), int(e[2])) for e in gathered], se + 1)
             cand = [max(e[2], 0) for e in top[:se]]
-            amu = self._owned_rows(lambda i: be.row(phi_v_p, i), cand, n1)
-            bmu = self._owned_rows(lambda i: be.row(phi_c_p, i), cand, n2)
-            lc = self._owned_rows(lambda i: be.row(st.L, i)[:k], cand, k) if k else np.zeros((se, 0))
+            amu = self._owned_rows(lambda i: be.row(phi_v_p, i), cand, n1, phi_v_p)
+            bmu = self._owned_rows(lambda i: be.row(phi_c_p, i), cand, n2, phi_c_p)
+            lc = self._owned_rows(lambda i: be.row(st.L, i)[:k], cand, k, st.L, k) if k else np.zeros((se, 0))
             # the candidates' Schur block, replicated (s x s)
             w_cc = (amu @ amu.T) * (bmu @ bmu.T) - lc @ lc.T
             b, piv, x, margins = cand_greedy(top, w_cc, k, steps, pos, perm)
             if b <= 0:
                 raise RuntimeError("distributed select: no progress")
             # W columns of the accepted pivots on the local panel, then L block
-            amu_s = self._owned_rows(lambda i: be.row(phi_v_p, i), piv, n1)
-            bmu_s = self._owned_rows(lambda i: be.row(phi_c_p, i), piv, n2)
-            ls = self._owned_rows(lambda i: be.row(st.L, i)[:k], piv, k) if k else np.zeros((b, 0))
+            amu_s = self._owned_rows(lambda i: be.row(phi_v_p, i), piv, n1, phi_v_p)
+            bmu_s = self._owned_rows(lambda i: be.row(phi_c_p, i), piv, n2, phi_c_p)
+            ls = self._owned_rows(lambda i: be.row(st.L, i)[:k], piv, k, st.L, k) if k else np.zeros((b, 0))
             w_p = be.w_panel(phi_v_p, phi_c_p, amu_s, bmu_s, st.L, ls, k)
             be.l_update(w_p, x, st.L, k, b)
             be.downdate(st.L, k, b, pos[st.r0:st.r1], st.d)
@@ -273,7 +282,7 @@ class DistributedBuild:
         if self.steps != self.n_mu:
             raise NotImplementedError("distributed fit needs N_mu <= N_v N_c")
         order = st.pivots
-        lp = self._owned_rows(lambda i: be.row(st.L, i)[:self.n_mu], order, self.n_mu)
+        lp = self._owned_rows(lambda i: be.row(st.L, i)[:self.n_mu], order, self.n_mu, st.L, self.n_mu)
         lp = np.tril(lp)
         x = be.tri_inverse(lp)
         colmap = np.searchsorted(pts, np.asarray(order))

@@ -518,9 +518,12 @@ def _dev_ptr_cm(t):
 
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64):
         raise InvalidInput("expected a float64 CUDA tensor")
-    if t.dim() != 2 or t.stride(0) != 1:
+    if t.dim() != 2 or (t.stride(0) != 1 and t.shape[0] > 1):
         raise InvalidInput("expected a column-major (stride(0) == 1) 2-D tensor")
-    return t.data_ptr(), max(t.stride(1), t.shape[0])
+    ld = t.stride(1) if t.shape[1] > 1 else t.shape[0]
+    if ld < t.shape[0]:
+        raise InvalidInput("column stride below the row count")
+    return t.data_ptr(), max(ld, 1)
 
 
 def build(phi_v, phi_c, energies, dims, cell, k_mu: float = 8.0, n_lambda: int = 16, delta_rel: float = 1e-7,
@@ -619,3 +622,32 @@ def coulomb_apply_dev(dims, cell, x, y, zero_kernel: bool = False, ctx=None):
                                           ctypes.c_void_p(px), ldx, x.shape[1], ctypes.c_void_p(py), ldy),
            cx.handle, "coulomb_apply")
     return y
+
+
+def contour_partial_dev(pv, pc, energies, n_lambda: int, node0: int, count: int, acc, ctx=None):
+    """acc (N_mu x N_mu, CUDA, column-major) = sum over nodes [node0, node0 +
+    count) of an n_lambda-interval trapezoid of w_k term_k, unscaled (the
+    multi-rank node split; contour.hpp:185-222)."""
+    cx = _ctx(ctx)
+    ppv, ldv = _dev_ptr_cm(pv)
+    ppc, ldc = _dev_ptr_cm(pc)
+    pa, _ = _dev_ptr_cm(acc)
+    e = _f(energies).ravel()
+    _sync_torch(pv)
+    _check(cx._lib.lrgw_dev_contour_partial(cx.handle, ctypes.c_void_p(ppv), ldv, ctypes.c_void_p(ppc), ldc,
+                                            pv.shape[0], pv.shape[1], pc.shape[1], _dp(e), e.size, int(n_lambda),
+                                            int(node0), int(count), ctypes.c_void_p(pa)),
+           cx.handle, "contour_partial")
+    return acc
+
+
+def smw_core_dev(t, pvp, k, ctx=None):
+    """K = (T^-1/2 - Theta^T V Theta)^-1 on CUDA N_mu x N_mu matrices (smw.hpp:42-73)."""
+    cx = _ctx(ctx)
+    pt, _ = _dev_ptr_cm(t)
+    pp, _ = _dev_ptr_cm(pvp)
+    pk, _ = _dev_ptr_cm(k)
+    _sync_torch(t)
+    _check(cx._lib.lrgw_dev_smw_core(cx.handle, ctypes.c_void_p(pt), ctypes.c_void_p(pp), t.shape[0],
+                                     ctypes.c_void_p(pk)), cx.handle, "smw_core")
+    return k
