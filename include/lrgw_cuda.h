@@ -206,6 +206,29 @@ int lrgw_dev_trtri_lower(lrgw_ctx ctx, double* a, int n, long long lda);
 int lrgw_dev_select_topk(lrgw_ctx ctx, const double* d, const int32_t* pos, int n_r, int k, int s1,
                          int32_t* rows_host, double* vals_host, int32_t* pos_host);
 
+/* Certified greedy of one selection block (the controller-warp kernel of
+ * lrgw_select_interpolation_points) on the s candidates' Schur block wcc
+ * (device, s x s, ld s): top = the s+1 entries of lrgw_dev_select_topk (host
+ * values / positions / rows); pos / perm (device, n_r each) are the position
+ * bookkeeping, updated in place. Outputs: x (device, s x s, ld s) = L_sel^-1
+ * (b x b lower, pivot order), the b accepted pivot rows (host), their
+ * margins (host, optional) and b (host). Reference: linalg.hpp:26-111 steps
+ * k .. k+b-1. Used by the multi-rank build (paper_2403_12340_b200/dist.py). */
+/* Theta row panel from the selection factor: theta(:, colmap[q]) =
+ * sum_{p >= q} L(:, p) X(p, q) with L the panel's pivoted-Cholesky factor
+ * (rows x n_mu, pivot order), X = L_P^-1 (device, lower, ld ldx) and colmap
+ * (host) the sorted-point rank of pivot q — the fused fit of lrgw_build
+ * (isdf.hpp:132-170 Theta = Z C^T (C C^T)^-1 in factored form) for one
+ * rank's panel. */
+int lrgw_dev_theta_from_factor(lrgw_ctx ctx, const double* l, long long ldl, int rows, int n_mu,
+                               const double* x, long long ldx, const int32_t* colmap_host,
+                               double* theta, long long ldt);
+
+int lrgw_dev_cand_greedy(lrgw_ctx ctx, int n_r, int s, int steps, int k, const double* top_vals,
+                         const int32_t* top_pos, const int32_t* top_rows, const double* wcc, int32_t* pos,
+                         int32_t* perm, double* x, int32_t* piv_rows_host, double* margins_host,
+                         int32_t* b_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1513,4 +1513,52 @@ int lrgw_dev_select_topk(lrgw_ctx c, const double* d, const int32_t* pos, int n_
   });
 }
 
+int lrgw_dev_cand_greedy(lrgw_ctx c, int n_r, int s, int steps, int k, const double* top_vals,
+                         const int32_t* top_pos, const int32_t* top_rows, const double* wcc, int32_t* pos,
+                         int32_t* perm, double* x, int32_t* piv_rows, double* margins, int32_t* b) {
+  return guarded(c, [&] {
+    if (n_r < 1 || s < 1 || s > select_max_candidates() || k < 0 || steps > n_r || k >= steps)
+      fail(LRGW_ERR_INVALID_INPUT, "cand_greedy: bad sizes");
+    std::vector<HostEnt> h(s + 1);
+    for (int i = 0; i <= s; ++i) h[i] = HostEnt{top_vals[i], top_pos[i], top_rows[i]};
+    DBuf top(c, sizeof(HostEnt) * (s + 1));
+    ck(cudaMemcpyAsync(top.p, h.data(), sizeof(HostEnt) * (s + 1), cudaMemcpyHostToDevice, c->stream), "H2D");
+    DBuf order = ialloc(c, steps);
+    DBuf marg = dalloc(c, steps);
+    DBuf bout = ialloc(c, 2);
+    ck(select_cand_greedy(c->stream, n_r, s, steps, k, top.p, wcc, pos, perm, x, (int*)order.p,
+                          margins ? (double*)marg.p : nullptr, (int*)bout.p),
+       "cand_greedy");
+    int nb[2] = {0, 0};
+    download(c, nb, bout.p, sizeof(nb));
+    *b = nb[0];
+    if (nb[0] > 0) {
+      download(c, piv_rows, (int*)order.p + k, sizeof(int) * nb[0]);
+      if (margins) download(c, margins, (double*)marg.p + k, sizeof(double) * nb[0]);
+    }
+  });
+}
+
+int lrgw_dev_theta_from_factor(lrgw_ctx c, const double* l, long long ldl, int rows, int n_mu, const double* x,
+                               long long ldx, const int32_t* colmap, double* theta, long long ldt) {
+  return guarded(c, [&] {
+    if (rows < 0 || n_mu < 1 || ldl < std::max(rows, 1) || ldx < n_mu || ldt < std::max(rows, 1))
+      fail(LRGW_ERR_INVALID_INPUT, "theta_from_factor: bad sizes");
+    std::vector<int> map(colmap, colmap + n_mu);
+    std::vector<char> seen(n_mu, 0);
+    for (int q : map) {
+      if (q < 0 || q >= n_mu || seen[q]) fail(LRGW_ERR_INVALID_INPUT, "theta_from_factor: colmap is not a permutation");
+      seen[q] = 1;
+    }
+    if (rows == 0) return;
+    DBuf dmap = upload_i(c, map.data(), n_mu);
+    DBuf xt = dalloc(c, (size_t)n_mu * n_mu);
+    ck(transpose(c->stream, x, ldx, n_mu, n_mu, xt.d(), n_mu), "transpose");
+    ck(dgemm(c->stream, rows, n_mu, n_mu, l, ldl, Lay::MN, xt.d(), n_mu, Lay::MN, theta, ldt, 1.0, 0.0, nullptr,
+             false, c->sm_count, nullptr, 0, true, dmap.i()),
+       "dgemm(theta)");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
 }  // extern "C"

@@ -61,7 +61,13 @@ def y_chunks(n2, world):
 # ---------------------------------------------------------------------------
 
 class Comm:
-    """Thin wrapper: rank/world and the handful of exchanges the build needs."""
+    """Thin wrapper: rank/world and the handful of exchanges the build needs.
+
+    Payloads are numpy arrays (small replicated data: candidate lists, rows
+    at the pivots) or torch tensors (the per-rank device arrays: partial
+    cores, the slab spectra). Tensors stay on the device under NCCL (NVLink)
+    and are staged through the host under gloo; every call returns the
+    payload's own type (and device)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -70,47 +76,84 @@ class Comm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        # NCCL moves device buffers (over NVLink); gloo host buffers
         self.device = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+
+    @staticmethod
+    def _is_tensor(a):
+        import torch
+
+        return isinstance(a, torch.Tensor)
 
     def _t(self, a):
         import torch
 
+        if self._is_tensor(a):
+            return a.contiguous().to(self.device)
         return torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
+
+    def _back(self, t, like):
+        if self._is_tensor(like):
+            return t.to(like.device)
+        return t.cpu().numpy()
 
     def allreduce_sum(self, a):
         t = self._t(a)
+        if t is a:
+            t = t.clone()
         self.dist.all_reduce(t, group=self.group)
-        return t.cpu().numpy()
+        return self._back(t, a)
 
-    def allgather(self, a):
+    def allgather(self, a, ragged=False):
+        """Every rank's `a`; ragged: the leading dimension may differ by rank
+        (padded to the largest for the collective, trimmed after)."""
         t = self._t(a)
-        out = [t.clone() for _ in range(self.world)]
-        self.dist.all_gather(out, t, group=self.group)
-        return [o.cpu().numpy() for o in out]
+        if not ragged:
+            out = [torch_empty_like(t) for _ in range(self.world)]
+            self.dist.all_gather(out, t, group=self.group)
+            return [self._back(o, a) for o in out]
+        rows = [int(r[0]) for r in self.allgather(np.array([t.shape[0]], dtype=np.int64))]
+        pad = torch_zeros((max(rows),) + tuple(t.shape[1:]), t)
+        pad[:t.shape[0]] = t
+        out = [torch_empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(out, pad, group=self.group)
+        return [self._back(o[:r], a) for o, r in zip(out, rows)]
 
     def alltoall(self, blocks):
-        """blocks[q] goes to rank q; returns the blocks received from each rank.
-        Uses all_to_all when the backend has it, else pairwise send/recv."""
+        """blocks[q] (flat) goes to rank q; returns the blocks received from
+        each rank. Uses all_to_all when the backend has it, else pairwise
+        send/recv."""
         import torch
 
-        send = [self._t(b) for b in blocks]
-        shapes = self.allgather(np.array([b.size for b in blocks], dtype=np.int64))
+        send = [self._t(b).reshape(-1) for b in blocks]
+        sizes = np.array([int(s.numel()) for s in send], dtype=np.int64)
+        shapes = self.allgather(sizes)
         recv = [torch.empty(int(shapes[q][self.rank]), dtype=send[0].dtype, device=self.device)
                 for q in range(self.world)]
         try:
-            self.dist.all_to_all([r for r in recv], [s.reshape(-1) for s in send], group=self.group)
+            self.dist.all_to_all(recv, send, group=self.group)
         except (RuntimeError, ValueError):
             reqs = []
             for q in range(self.world):
                 if q == self.rank:
-                    recv[q].copy_(send[q].reshape(-1))
+                    recv[q].copy_(send[q])
                     continue
-                reqs.append(self.dist.isend(send[q].reshape(-1).contiguous(), q, group=self.group))
+                reqs.append(self.dist.isend(send[q], q, group=self.group))
                 reqs.append(self.dist.irecv(recv[q], q, group=self.group))
             for r in reqs:
                 r.wait()
-        return [r.cpu().numpy() for r in recv]
+        return [self._back(r, blocks[0]) for r in recv]
+
+
+def torch_empty_like(t):
+    import torch
+
+    return torch.empty_like(t)
+
+
+def torch_zeros(shape, like):
+    import torch
+
+    return torch.zeros(shape, dtype=like.dtype, device=like.device)
 
 
 # ---------------------------------------------------------------------------
@@ -244,8 +287,8 @@ class DistributedBuild:
         n_r, n1, n2 = self.n_r, self.n_v, self.n_c
         steps = min(self.n_mu, n1 * n2, n_r)
         s = max(1, min(self.batch, n_r))
-        pos = np.arange(n_r, dtype=np.int64)
-        perm = np.arange(n_r, dtype=np.int64)
+        # position bookkeeping, replicated (identical updates on every rank)
+        pos, perm = be.iota(n_r), be.iota(n_r)
         st.d = be.init_diag(phi_v_p, phi_c_p)
         st.L = be.zeros(st.r1 - st.r0, max(steps, 1))
         k = 0
@@ -260,7 +303,8 @@ class DistributedBuild:
             lc = self._owned_rows(lambda i: be.row(st.L, i)[:k], cand, k, st.L, k) if k else np.zeros((se, 0))
             # the candidates' Schur block, replicated (s x s)
             w_cc = (amu @ amu.T) * (bmu @ bmu.T) - lc @ lc.T
-            b, piv, x, margins = cand_greedy(top, w_cc, k, steps, pos, perm)
+            greedy = getattr(be, "cand_greedy", None) or cand_greedy
+            b, piv, x, margins = greedy(top, w_cc, k, steps, pos, perm)
             if b <= 0:
                 raise RuntimeError("distributed select: no progress")
             # W columns of the accepted pivots on the local panel, then L block
@@ -274,21 +318,21 @@ class DistributedBuild:
             st.margins += margins
             k += b
         self.pos, self.perm, self.steps = pos, perm, steps
-        return np.sort(perm[:self.n_mu]).astype(np.int32)
+        return np.sort(be.to_host(perm)[:self.n_mu]).astype(np.int32)
 
     def fit(self, pts):
-        """Stage 2: Theta panel = L panel L_P^-1, columns in sorted-point order."""
+        """Stage 2: Theta panel = L panel L_P^-1, columns in sorted-point order.
+        L_P (the pivot rows of the factor) is owner-contributed and summed in
+        the backend's memory."""
         be, st = self.be, self.st
         if self.steps != self.n_mu:
             raise NotImplementedError("distributed fit needs N_mu <= N_v N_c")
-        order = st.pivots
-        lp = self._owned_rows(lambda i: be.row(st.L, i)[:self.n_mu], order, self.n_mu, st.L, self.n_mu)
-        lp = np.tril(lp)
+        order = np.asarray(st.pivots, dtype=np.int64)
+        mine = np.nonzero((order >= st.r0) & (order < st.r1))[0]
+        lp = self.comm.allreduce_sum(be.scatter_rows(st.L, order[mine] - st.r0, mine, self.n_mu, self.n_mu))
         x = be.tri_inverse(lp)
-        colmap = np.searchsorted(pts, np.asarray(order))
-        xs = np.zeros_like(x)
-        xs[:, colmap] = x
-        st.theta = be.theta_panel(st.L, xs)
+        colmap = np.searchsorted(pts, order)
+        st.theta = be.theta_panel(st.L, x, colmap)
         return st.theta
 
     def contour(self, pv, pc, energies):
@@ -300,20 +344,17 @@ class DistributedBuild:
         return self.be.contour_finish(acc, energies, self.n_v, self.n_c)
 
     def pvp(self):
-        """Stages 4-5a: slab FFT + G-slab SYRK + all-reduce."""
+        """Stages 4-5a: slab FFT + G-slab SYRK + all-reduce. The spectra stay
+        in the backend's memory: the all-to-all moves them rank to rank."""
         n1, n2, n3 = self.dims
         be, st = self.be, self.st
         z0, z1 = st.r0 // (n1 * n2), st.r1 // (n1 * n2)
         xh = be.rfft2_planes(st.theta, z1 - z0, n2, n1)          # (zl, n2, n1h, n_mu) complex
         chunks = y_chunks(n2, self.comm.world)
-        blocks = [be.to_host(xh[:, a:b]) for (a, b) in chunks]
-        recv = self.comm.alltoall([np.ascontiguousarray(bl).view(np.float64) for bl in blocks])
+        recv = self.comm.alltoall(be.y_blocks(xh, chunks))
         ya, yb = chunks[self.comm.rank]
-        planes = [z1_ - z0_ for (z0_, z1_) in [(r0 // (n1 * n2), r1 // (n1 * n2))
-                                               for (r0, r1) in z_panels(self.dims, self.comm.world)]]
-        n1h = n1 // 2 + 1
-        parts = [recv[q].view(np.complex128).reshape(planes[q], yb - ya, n1h, self.n_mu) for q in range(self.comm.world)]
-        pencil = np.concatenate(parts, axis=0)                      # (n3, ny, n1h, n_mu)
+        planes = [(r1 - r0) // (n1 * n2) for (r0, r1) in z_panels(self.dims, self.comm.world)]
+        pencil = be.z_join(recv, planes, (yb - ya, n1 // 2 + 1, self.n_mu))  # (n3, ny, n1h, n_mu)
         ghat = be.fft_z(pencil)
         part = be.pvp_slab(ghat, (ya, yb), self.dims, self.cell)
         return self.comm.allreduce_sum(part)
@@ -326,6 +367,6 @@ class DistributedBuild:
         be, st = self.be, self.st
         u = self.comm.allreduce_sum(be.theta_t_x(st.theta, x_p))
         z_p = be.theta_w(st.theta, k @ u)
-        z = np.concatenate(self.comm.allgather(be.to_host(z_p)))
+        z = be.vcat(self.comm.allgather(z_p, ragged=True))
         vz = be.apply_coulomb(self.dims, self.cell, z)
-        return be.to_host(x_p) + vz[st.r0:st.r1]
+        return be.to_host(x_p) + be.to_host(vz)[st.r0:st.r1]

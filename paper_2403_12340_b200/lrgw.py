@@ -611,6 +611,59 @@ def select_topk_dev(d, pos, k: int, s1: int, ctx=None):
     return rows, vals, poss
 
 
+def theta_from_factor_dev(l, x, colmap, theta, ctx=None):
+    """theta(:, colmap[q]) = (L X)(:, q) for X = L_P^-1 lower triangular
+    (column-major float64 CUDA tensors; colmap a permutation, host)."""
+    import numpy as np
+
+    cx = _ctx(ctx)
+    rows, n_mu = theta.shape
+    if x.shape != (n_mu, n_mu) or l.shape[0] != rows or l.shape[1] < n_mu:
+        raise InvalidInput("theta_from_factor: shape mismatch")
+    pl, ldl = _dev_ptr_cm(l)
+    px, ldx = _dev_ptr_cm(x)
+    pt, ldt = _dev_ptr_cm(theta)
+    cm = np.ascontiguousarray(colmap, dtype=np.int32)
+    _sync_torch(l)
+    _check(cx._lib.lrgw_dev_theta_from_factor(cx.handle, ctypes.c_void_p(pl), ldl, rows, n_mu, ctypes.c_void_p(px),
+                                              ldx, cm.ctypes.data_as(L.c_int32_p), ctypes.c_void_p(pt), ldt),
+           cx.handle, "theta_from_factor")
+    return theta
+
+
+def cand_greedy_dev(n_r: int, steps: int, k: int, top_vals, top_pos, top_rows, wcc, pos, perm, x, ctx=None):
+    """One selection block's certified greedy on the device (the kernel of
+    the single-GPU selection): top_* = the s+1 candidate entries (host), wcc
+    = their Schur block (s x s column-major CUDA), pos / perm = int32 CUDA
+    position bookkeeping (updated in place), x (s x s CUDA) <- L_sel^-1.
+    Returns (b, pivot rows, margins) with host arrays of length b."""
+    import numpy as np
+
+    cx = _ctx(ctx)
+    s = int(wcc.shape[0])
+    tv = np.ascontiguousarray(top_vals, dtype=np.float64)
+    tp = np.ascontiguousarray(top_pos, dtype=np.int32)
+    tr = np.ascontiguousarray(top_rows, dtype=np.int32)
+    if tv.size != s + 1 or tp.size != s + 1 or tr.size != s + 1:
+        raise InvalidInput("cand_greedy: top needs s + 1 entries")
+    pw, ldw = _dev_ptr_cm(wcc)
+    px, ldx = _dev_ptr_cm(x)
+    if ldw != s or ldx != s or x.shape[0] != s:
+        raise InvalidInput("cand_greedy: wcc and x must be s x s with ld s")
+    piv = np.empty(s, np.int32)
+    mg = np.empty(s, np.float64)
+    b = np.zeros(1, np.int32)
+    _sync_torch(wcc)
+    _check(cx._lib.lrgw_dev_cand_greedy(cx.handle, int(n_r), s, int(steps), int(k), _dp(tv),
+                                        tp.ctypes.data_as(L.c_int32_p), tr.ctypes.data_as(L.c_int32_p),
+                                        ctypes.c_void_p(pw), ctypes.c_void_p(pos.data_ptr()),
+                                        ctypes.c_void_p(perm.data_ptr()), ctypes.c_void_p(px),
+                                        piv.ctypes.data_as(L.c_int32_p), _dp(mg), b.ctypes.data_as(L.c_int32_p)),
+           cx.handle, "cand_greedy")
+    nb = int(b[0])
+    return nb, piv[:nb].copy(), mg[:nb].copy()
+
+
 def coulomb_apply_dev(dims, cell, x, y, zero_kernel: bool = False, ctx=None):
     """y = V x for column-major float64 CUDA tensors (N_r x m)."""
     cx = _ctx(ctx)

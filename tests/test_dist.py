@@ -22,6 +22,9 @@ class NumpyBackend:
     def zeros(self, r, c):
         return np.zeros((r, c))
 
+    def iota(self, n):
+        return np.arange(n, dtype=np.int64)
+
     def init_diag(self, a, b):
         return (a * a).sum(1) * (b * b).sum(1)
 
@@ -49,12 +52,19 @@ class NumpyBackend:
         m = pos_p >= k + b
         d[m] -= (L[m, k:k + b] ** 2).sum(1)
 
+    def scatter_rows(self, m, local, at, n, cols):
+        out = np.zeros((n, cols))
+        out[at] = m[local, :cols]
+        return out
+
     def tri_inverse(self, lp):
         import scipy.linalg as sla
 
-        return sla.solve_triangular(lp, np.eye(lp.shape[0]), lower=True)
+        return sla.solve_triangular(np.tril(lp), np.eye(lp.shape[0]), lower=True)
 
-    def theta_panel(self, L, xs):
+    def theta_panel(self, L, x, colmap):
+        xs = np.zeros_like(x)
+        xs[:, colmap] = x
         return L[:, :self.n_mu] @ xs
 
     def contour_partial(self, pv, pc, e, n_lambda, k0, cnt):
@@ -69,6 +79,15 @@ class NumpyBackend:
     def rfft2_planes(self, theta_p, zl, n2, n1):
         x = theta_p.reshape(zl, n2, n1, -1)
         return np.fft.rfftn(x, axes=(1, 2))
+
+    def y_blocks(self, xh, chunks):
+        return [np.ascontiguousarray(xh[:, a:b]).view(np.float64).reshape(-1) for (a, b) in chunks]
+
+    def z_join(self, recv, planes, tail):
+        return np.concatenate([r.view(np.complex128).reshape(p, *tail) for r, p in zip(recv, planes)], axis=0)
+
+    def vcat(self, parts):
+        return np.concatenate(parts)
 
     def fft_z(self, pencil):
         return np.fft.fft(pencil, axis=0)
@@ -106,9 +125,9 @@ DIMS, CELL = (8, 8, 6), (6.0, 6.0, 4.5)
 NV = NC = 8
 
 
-def _problem():
+def _problem(dims=DIMS):
     rng = np.random.default_rng(11)
-    n_r = int(np.prod(DIMS))
+    n_r = int(np.prod(dims))
     psi = np.linalg.qr(rng.standard_normal((n_r, NV + NC)))[0]
     e = np.concatenate([np.sort(rng.uniform(-0.5, -0.1, NV)), np.sort(rng.uniform(0.05, 0.8, NC))])
     e[NV - 1], e[NV] = -0.1, 0.05
@@ -124,17 +143,17 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, dims=DIMS):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        psi, e, x = _problem()
+        psi, e, x = _problem(dims)
         comm = D.Comm()
         n_mu = R.num_aux(8.0, NV, NC)
-        b = D.DistributedBuild(comm, NumpyBackend(n_mu), DIMS, CELL, NV, NC, k_mu=8.0, n_lambda=16, batch=16)
+        b = D.DistributedBuild(comm, NumpyBackend(n_mu), dims, CELL, NV, NC, k_mu=8.0, n_lambda=16, batch=16)
         r0, r1 = b.st.r0, b.st.r1
         pts = b.select(psi[r0:r1, :NV].copy(), psi[r0:r1, NV:].copy())
         theta_p = b.fit(pts)
@@ -148,21 +167,22 @@ def _worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_distributed_build_matches_oracle(world, tmp_path):
+@pytest.mark.parametrize("world,dims", [(2, DIMS), (3, DIMS), (2, (8, 6, 7))])
+def test_distributed_build_matches_oracle(world, dims, tmp_path):
+    """(8, 6, 7): ragged z-panels (4 + 3 planes) and y-chunks."""
     import torch.multiprocessing as mp
 
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
-    psi, e, x = _problem()
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), dims), nprocs=world, join=True)
+    psi, e, x = _problem(dims)
     a, b = psi[:, :NV], psi[:, NV:]
     n_mu = R.num_aux(8.0, NV, NC)
     pts_or = R.select_points(a, b, n_mu)
     theta_or = R.fit_auxiliary_basis(a, b, pts_or)
     spec = R.elliptic_params(e, NV, NC, 1e-7)
     t_or = R.coupled_coefficients_fixed(a[pts_or], b[pts_or], e, spec, 16)
-    pvp_or = R.pvp(theta_or, DIMS, CELL)
-    k_or = R.assemble_K(t_or, theta_or, DIMS, CELL)
-    y_or = R.epsilon_inverse_apply(theta_or, k_or, DIMS, CELL, x)
+    pvp_or = R.pvp(theta_or, dims, CELL)
+    k_or = R.assemble_K(t_or, theta_or, dims, CELL)
+    y_or = R.epsilon_inverse_apply(theta_or, k_or, dims, CELL, x)
     res = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
     rel = lambda u, v: np.linalg.norm(u - v) / np.linalg.norm(v)  # noqa: E731
     for r in res:
