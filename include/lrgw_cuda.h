@@ -224,6 +224,28 @@ int lrgw_dev_theta_from_factor(lrgw_ctx ctx, const double* l, long long ldl, int
                                const double* x, long long ldx, const int32_t* colmap_host,
                                double* theta, long long ldt);
 
+/* One selection block's panel update on a rank's rows [r0, r0 + rows):
+ *   W = (A A_sel^T) o (B B_sel^T) - L[:, :k] L_sel^T     (rows x nb)
+ *   L[:, k:k+nb] = W X^T,  d -= rowsum(L[:, k:k+nb]^2) where pos >= k + nb
+ * with piv = [A_sel | B_sel | L_sel] (device, nb x (n1 + n2 + k), column
+ * major, ld ldpiv) the accepted pivots' rows, X = L_sel^-1 (device, ld ldx)
+ * from lrgw_dev_cand_greedy, L (device, ld rows) and d, pos (device, the
+ * panel's residual diagonal and positions). The tail of one block of
+ * lrgw_select_interpolation_points (linalg.hpp:60-100 for steps k..k+nb-1). */
+int lrgw_dev_select_panel_update(lrgw_ctx ctx, const double* a, long long lda, int n1, const double* b,
+                                 long long ldb, int n2, int rows, double* l, long long ldl, int k, int nb,
+                                 const double* piv, long long ldpiv, const double* x, long long ldx,
+                                 const int32_t* pos, double* d);
+
+/* out = X^T diag(w) X (m x m, symmetric) for X (device, kdim x m, column
+ * major, ld ldx) and w (device, kdim) — the weighted G-space SYRK of
+ * Theta^T V Theta (smw.hpp:61-62) on one rank's G-slab, with X the slab's
+ * spectrum viewed as interleaved reals and w the Hermitian-weighted v(G)/N_r
+ * repeated for the real and imaginary parts. Lower-triangle DMMA tiles +
+ * mirror. */
+int lrgw_dev_gram_weighted(lrgw_ctx ctx, const double* x, long long ldx, int kdim, int m, const double* w,
+                           double* out, long long ldo);
+
 int lrgw_dev_cand_greedy(lrgw_ctx ctx, int n_r, int s, int steps, int k, const double* top_vals,
                          const int32_t* top_pos, const int32_t* top_rows, const double* wcc, int32_t* pos,
                          int32_t* perm, double* x, int32_t* piv_rows_host, double* margins_host,

@@ -125,6 +125,12 @@ _SIGS = {
                                             ctypes.c_void_p, ctypes.c_void_p, c_int32_p, c_double_p, c_int32_p]),
     "lrgw_dev_theta_from_factor": (ctypes.c_int, [ctx_t, ctypes.c_void_p, c_ll, ctypes.c_int, ctypes.c_int,
                                                   ctypes.c_void_p, c_ll, c_int32_p, ctypes.c_void_p, c_ll]),
+    "lrgw_dev_select_panel_update": (ctypes.c_int, [ctx_t, ctypes.c_void_p, c_ll, ctypes.c_int, ctypes.c_void_p,
+                                                    c_ll, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, c_ll,
+                                                    ctypes.c_int, ctypes.c_int, ctypes.c_void_p, c_ll,
+                                                    ctypes.c_void_p, c_ll, ctypes.c_void_p, ctypes.c_void_p]),
+    "lrgw_dev_gram_weighted": (ctypes.c_int, [ctx_t, ctypes.c_void_p, c_ll, ctypes.c_int, ctypes.c_int,
+                                              ctypes.c_void_p, ctypes.c_void_p, c_ll]),
     "lrgw_dev_dgemm": (ctypes.c_int, [ctx_t, ctypes.c_char, ctypes.c_char, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, ctypes.c_double, ctypes.c_void_p, c_ll, ctypes.c_void_p,
                                       c_ll, ctypes.c_double, ctypes.c_void_p, c_ll]),

@@ -1561,4 +1561,41 @@ int lrgw_dev_theta_from_factor(lrgw_ctx c, const double* l, long long ldl, int r
   });
 }
 
+int lrgw_dev_select_panel_update(lrgw_ctx c, const double* a, long long lda, int n1, const double* b, long long ldb,
+                                 int n2, int rows, double* l, long long ldl, int k, int nb, const double* piv,
+                                 long long ldpiv, const double* x, long long ldx, const int32_t* pos, double* d) {
+  return guarded(c, [&] {
+    if (rows < 1 || n1 < 1 || n2 < 1 || nb < 1 || k < 0 || ldl != rows || lda < rows || ldb < rows || ldx < nb ||
+        ldpiv < nb)
+      fail(LRGW_ERR_INVALID_INPUT, "select_panel_update: bad sizes");
+    const int width = n1 + n2 + k;
+    const int ldp = nb + (nb & 1);  // even leading dim: 16-byte operand loads
+    DBuf pr = dalloc(c, (size_t)ldp * width);
+    ck(cudaMemcpy2DAsync(pr.d(), ldp * sizeof(double), piv, ldpiv * sizeof(double), nb * sizeof(double), width,
+                         cudaMemcpyDeviceToDevice, c->stream),
+       "D2D");
+    const double* amu = pr.d();
+    const double* bmu = amu + (size_t)ldp * n1;
+    const double* lsel = bmu + (size_t)ldp * n2;
+    DBuf wsel = dalloc(c, (size_t)rows * nb);
+    ck(hadamard_gemm(c->stream, rows, nb, a, lda, amu, ldp, n1, b, ldb, bmu, ldp, n2, wsel.d(), rows, 1.0, 0.0),
+       "hadamard_gemm");
+    if (k > 0) gemm(c, rows, nb, k, l, ldl, Lay::MN, lsel, ldp, Lay::MN, wsel.d(), rows, -1.0, 1.0);
+    gemm(c, rows, nb, nb, wsel.d(), rows, Lay::MN, x, ldx, Lay::MN, l + (size_t)k * ldl, ldl, 1.0, 0.0);
+    ck(select_downdate(c->stream, l, rows, k, nb, pos, d), "downdate");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int lrgw_dev_gram_weighted(lrgw_ctx c, const double* x, long long ldx, int kdim, int m, const double* w,
+                           double* out, long long ldo) {
+  return guarded(c, [&] {
+    if (kdim < 1 || m < 1 || ldx < kdim || ldo < m) fail(LRGW_ERR_INVALID_INPUT, "gram_weighted: bad sizes");
+    Work wk = make_work(c, (size_t)16 * m * m);
+    gemm(c, m, m, kdim, x, ldx, Lay::K, x, ldx, Lay::K, out, ldo, 1.0, 0.0, w, true, &wk);
+    ck(mirror_lower(c->stream, out, m, ldo, false), "mirror");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
 }  // extern "C"

@@ -97,6 +97,8 @@ class Comm:
         return t.cpu().numpy()
 
     def allreduce_sum(self, a):
+        if self.world == 1:
+            return a
         t = self._t(a)
         if t is a:
             t = t.clone()
@@ -106,6 +108,8 @@ class Comm:
     def allgather(self, a, ragged=False):
         """Every rank's `a`; ragged: the leading dimension may differ by rank
         (padded to the largest for the collective, trimmed after)."""
+        if self.world == 1:
+            return [a]
         t = self._t(a)
         if not ragged:
             out = [torch_empty_like(t) for _ in range(self.world)]
@@ -265,21 +269,13 @@ class DistributedBuild:
         self.st = RankState(r0, r1)
 
     # ---- owner contributions: rows of a panel array at global row indices --
-    def _owned_rows(self, panel_rows_fn, rows, width, panel=None, cols=None):
-        """Rows of a panel array at global row indices: every rank contributes
-        the rows it owns (zeros elsewhere), summed across ranks (exact)."""
-        out = np.zeros((len(rows), width))
-        mine = [(i, r - self.st.r0) for i, r in enumerate(rows) if self.st.r0 <= r < self.st.r1]
-        if mine and panel is not None and hasattr(self.be, "rows"):
-            vals = self.be.rows(panel, [j for _, j in mine])
-            if cols is not None:
-                vals = vals[:, :cols]
-            for (i, _), v in zip(mine, vals):
-                out[i] = v
-        else:
-            for i, j in mine:
-                out[i] = panel_rows_fn(j)
-        return self.comm.allreduce_sum(out)
+    def _owned_cat(self, rows, parts):
+        """[P_1 | P_2 | ...] at global rows for panel arrays P_i (first w_i
+        columns each), owner-contributed and summed in one all-reduce (in the
+        backend's memory)."""
+        rows = np.asarray(rows, dtype=np.int64)
+        at = np.nonzero((rows >= self.st.r0) & (rows < self.st.r1))[0]
+        return self.comm.allreduce_sum(self.be.rows_cat(parts, rows[at] - self.st.r0, at, len(rows)))
 
     def select(self, phi_v_p, phi_c_p):
         """Stage 1 over the local panels (rows [r0, r1) of Phi_v / Phi_c)."""
@@ -298,22 +294,19 @@ class DistributedBuild:
             gathered = np.concatenate(self.comm.allgather(np.asarray(local, dtype=np.float64).reshape(-1, 3)))
             top = merge_top([(e[0], int(e[1]), int(e[2])) for e in gathered], se + 1)
             cand = [max(e[2], 0) for e in top[:se]]
-            amu = self._owned_rows(lambda i: be.row(phi_v_p, i), cand, n1, phi_v_p)
-            bmu = self._owned_rows(lambda i: be.row(phi_c_p, i), cand, n2, phi_c_p)
-            lc = self._owned_rows(lambda i: be.row(st.L, i)[:k], cand, k, st.L, k) if k else np.zeros((se, 0))
+            # rows of Phi_v | Phi_c | L[:, :k] at the candidates: one exchange
+            rows_c = self._owned_cat(cand, ((phi_v_p, n1), (phi_c_p, n2), (st.L, k)))
             # the candidates' Schur block, replicated (s x s)
-            w_cc = (amu @ amu.T) * (bmu @ bmu.T) - lc @ lc.T
+            w_cc = be.schur_block(rows_c, n1, n2)
             greedy = getattr(be, "cand_greedy", None) or cand_greedy
             b, piv, x, margins = greedy(top, w_cc, k, steps, pos, perm)
             if b <= 0:
                 raise RuntimeError("distributed select: no progress")
             # W columns of the accepted pivots on the local panel, then L block
-            amu_s = self._owned_rows(lambda i: be.row(phi_v_p, i), piv, n1, phi_v_p)
-            bmu_s = self._owned_rows(lambda i: be.row(phi_c_p, i), piv, n2, phi_c_p)
-            ls = self._owned_rows(lambda i: be.row(st.L, i)[:k], piv, k, st.L, k) if k else np.zeros((b, 0))
-            w_p = be.w_panel(phi_v_p, phi_c_p, amu_s, bmu_s, st.L, ls, k)
-            be.l_update(w_p, x, st.L, k, b)
-            be.downdate(st.L, k, b, pos[st.r0:st.r1], st.d)
+            # the accepted pivots are candidates: their rows are already here
+            at = {top[i][2]: i for i in range(se) if top[i][2] >= 0}
+            sel = [at[r] for r in piv]
+            be.panel_update(phi_v_p, phi_c_p, be.take_rows(rows_c, sel), x, st.L, k, b, pos[st.r0:st.r1], st.d)
             st.pivots += piv
             st.margins += margins
             k += b

@@ -82,23 +82,36 @@ class CudaBackend:
             pos, perm, x, ctx=self.ctx)
         return b, [int(r) for r in piv], x[:b, :b], [float(m) for m in margins]
 
-    def w_panel(self, a, b, amu, bmu, L, lc, k):
-        nb = amu.shape[0]
-        p1, p2 = _cm(a.shape[0], nb), _cm(a.shape[0], nb)
-        lrgw.dgemm_dev("N", "T", 1.0, a, _dev(amu), 0.0, p1, ctx=self.ctx)
-        lrgw.dgemm_dev("N", "T", 1.0, b, _dev(bmu), 0.0, p2, ctx=self.ctx)
-        w = (p1 * p2).t().contiguous().t()
-        if k:
-            lrgw.dgemm_dev("N", "T", -1.0, L[:, :k], _dev(lc), 1.0, w, ctx=self.ctx)
+    def rows_cat(self, parts, local, at, n):
+        """n x sum(w) zeros with [P_1 | P_2 | ...][local] placed at rows `at`."""
+        width = sum(w for _, w in parts)
+        out = torch.zeros(n, width, dtype=torch.float64, device="cuda")
+        if len(local):
+            li = torch.as_tensor(np.asarray(local, dtype=np.int64), device="cuda")
+            ai = torch.as_tensor(np.asarray(at, dtype=np.int64), device="cuda")
+            out[ai] = torch.cat([m.index_select(0, li)[:, :w] for m, w in parts if w], 1)
+        return out
+
+    def schur_block(self, rc, n1, n2):
+        """W[C, C] = (A_C A_C^T) o (B_C B_C^T) - L_C L_C^T on the DMMA engine."""
+        rc = _dev(rc)
+        s = rc.shape[0]
+        p1, p2 = _cm(s, s), _cm(s, s)
+        lrgw.dgemm_dev("N", "T", 1.0, rc[:, :n1], rc[:, :n1], 0.0, p1, ctx=self.ctx)
+        lrgw.dgemm_dev("N", "T", 1.0, rc[:, n1:n1 + n2], rc[:, n1:n1 + n2], 0.0, p2, ctx=self.ctx)
+        w = _dev(p1 * p2)
+        if rc.shape[1] > n1 + n2:
+            lc = rc[:, n1 + n2:]
+            lrgw.dgemm_dev("N", "T", -1.0, lc, lc, 1.0, w, ctx=self.ctx)
         return w
 
-    def l_update(self, w, x, L, k, b):
-        lrgw.dgemm_dev("N", "T", 1.0, w, _dev(x), 0.0, L[:, k:k + b], ctx=self.ctx)
+    def take_rows(self, m, idx):
+        return _dev(m.index_select(0, torch.as_tensor(np.asarray(idx, dtype=np.int64), device=m.device)))
 
-    def downdate(self, L, k, b, pos_p, d):
-        live = pos_p >= k + b
-        blk = L[:, k:k + b]
-        d -= torch.where(live, (blk * blk).sum(1), torch.zeros_like(d))
+    def panel_update(self, a, b, prow, x, L, k, nb, pos_p, d):
+        """W columns of the accepted pivots on the panel, the L block and the
+        residual downdate in one call (one host sync)."""
+        lrgw.select_panel_update_dev(a, b, L, k, prow, x, pos_p.contiguous(), d, ctx=self.ctx)
 
     # ---- stage 2 --------------------------------------------------------------
     def scatter_rows(self, m, local, at, n, cols):
@@ -136,26 +149,27 @@ class CudaBackend:
         return _dev(0.5 * (t + t.t()))
 
     # ---- stages 4-5 -------------------------------------------------------------
+    # Spectra are kept with N_mu outermost, (n_mu, z, y, x) — each Theta
+    # column's slab contiguous, the K-major layout of the single-GPU SYRK.
     def rfft2_planes(self, theta_p, zl, n2, n1):
-        x = theta_p.t().reshape(-1, zl, n2, n1)                   # (n_mu, zl, n2, n1)
-        f = torch.fft.rfftn(x, dim=(2, 3))                        # (n_mu, zl, n2, n1h)
-        return f.permute(1, 2, 3, 0).contiguous()                 # (zl, n2, n1h, n_mu)
+        x = theta_p.t().reshape(-1, zl, n2, n1)                   # (n_mu, zl, n2, n1), a view
+        return torch.fft.rfftn(x, dim=(2, 3))                     # (n_mu, zl, n2, n1h)
 
     def y_blocks(self, xh, chunks):
         """The slab spectrum cut into y-chunks, one flat real block per rank."""
-        return [torch.view_as_real(xh[:, a:b].contiguous()).reshape(-1) for (a, b) in chunks]
+        return [torch.view_as_real(xh[:, :, a:b].contiguous()).reshape(-1) for (a, b) in chunks]
 
     def z_join(self, recv, planes, tail):
-        """Blocks received from every rank -> this rank's y-pencil (n3, ny, n1h, n_mu)."""
-        return torch.cat([torch.view_as_complex(r.reshape(-1, 2)).reshape(p, *tail)
-                          for r, p in zip(recv, planes)], 0)
+        """Blocks received from every rank -> this rank's y-pencil (n_mu, n3, ny, n1h)."""
+        ny, n1h, n_mu = tail
+        return torch.cat([torch.view_as_complex(r.reshape(-1, 2)).reshape(n_mu, p, ny, n1h)
+                          for r, p in zip(recv, planes)], 1)
 
     def vcat(self, parts):
         return torch.cat([_dev(p) for p in parts], 0).t().contiguous().t()
 
     def fft_z(self, pencil):
-        g = torch.as_tensor(pencil, device="cuda")
-        return torch.fft.fft(g, dim=0)
+        return torch.fft.fft(pencil, dim=1)                       # (n_mu, n3, ny, n1h)
 
     def pvp_slab(self, ghat, yr, dims, cell):
         n1, n2, n3 = dims
@@ -165,13 +179,12 @@ class CudaBackend:
         herm[0] = 1.0
         if n1 % 2 == 0:
             herm[-1] = 1.0
-        w = (v * herm[None, None, :] / (n1 * n2 * n3)).reshape(-1)  # >= 0 (4 pi / |G|^2)
-        sw = torch.as_tensor(np.sqrt(w), device="cuda")
-        g = ghat.reshape(-1, ghat.shape[-1]) * sw[:, None]          # (K, n_mu) complex
-        x = torch.cat([g.real, g.imag], 0)                          # (2K, n_mu) real
-        xc = x.t().contiguous().t()
-        out = _cm(x.shape[1], x.shape[1])
-        lrgw.dgemm_dev("T", "N", 1.0, xc, xc, 0.0, out, ctx=self.ctx)
+        w = (v * herm[None, None, :] / (n1 * n2 * n3)).reshape(-1)
+        w2 = torch.as_tensor(np.repeat(w, 2), device="cuda")     # re / im interleaved
+        n_mu = ghat.shape[0]
+        x = torch.view_as_real(ghat.contiguous()).reshape(n_mu, -1).t()   # (2K, n_mu) column-major
+        out = _cm(n_mu, n_mu)
+        lrgw.gram_weighted_dev(x, w2, out, ctx=self.ctx)
         return out
 
     def smw_core(self, t, pvp):

@@ -631,6 +631,43 @@ def theta_from_factor_dev(l, x, colmap, theta, ctx=None):
     return theta
 
 
+def select_panel_update_dev(a, b, L, k: int, piv_rows, x, pos, d, ctx=None):
+    """One selection block's update of a row panel (column-major float64
+    CUDA tensors a, b, L; pos int32, d float64; piv_rows nb x (n1 + n2 + k) =
+    [A_sel | B_sel | L_sel]; x = L_sel^-1, nb x nb)."""
+    cx = _ctx(ctx)
+    pa, lda = _dev_ptr_cm(a)
+    pb, ldb = _dev_ptr_cm(b)
+    pl, ldl = _dev_ptr_cm(L)
+    px, ldx = _dev_ptr_cm(x)
+    pp, ldp = _dev_ptr_cm(piv_rows)
+    nb = piv_rows.shape[0]
+    n1, n2 = a.shape[1], b.shape[1]
+    if piv_rows.shape[1] != n1 + n2 + k or x.shape[0] < nb or L.shape[1] < k + nb:
+        raise InvalidInput("select_panel_update: shape mismatch")
+    _sync_torch(d)
+    _check(cx._lib.lrgw_dev_select_panel_update(cx.handle, ctypes.c_void_p(pa), lda, n1, ctypes.c_void_p(pb), ldb,
+                                                n2, a.shape[0], ctypes.c_void_p(pl), ldl, int(k), nb,
+                                                ctypes.c_void_p(pp), ldp, ctypes.c_void_p(px), ldx,
+                                                ctypes.c_void_p(pos.data_ptr()), ctypes.c_void_p(d.data_ptr())),
+           cx.handle, "select_panel_update")
+
+
+def gram_weighted_dev(x, w, out, ctx=None):
+    """out = X^T diag(w) X for a column-major float64 CUDA X (kdim x m), w
+    (kdim,) and out (m x m)."""
+    cx = _ctx(ctx)
+    px, ldx = _dev_ptr_cm(x)
+    po, ldo = _dev_ptr_cm(out)
+    kdim, m = x.shape
+    if w.numel() != kdim or not w.is_contiguous() or out.shape != (m, m):
+        raise InvalidInput("gram_weighted: shape mismatch")
+    _sync_torch(x)
+    _check(cx._lib.lrgw_dev_gram_weighted(cx.handle, ctypes.c_void_p(px), ldx, kdim, m, ctypes.c_void_p(w.data_ptr()),
+                                          ctypes.c_void_p(po), ldo), cx.handle, "gram_weighted")
+    return out
+
+
 def cand_greedy_dev(n_r: int, steps: int, k: int, top_vals, top_pos, top_rows, wcc, pos, perm, x, ctx=None):
     """One selection block's certified greedy on the device (the kernel of
     the single-GPU selection): top_* = the s+1 candidate entries (host), wcc

@@ -39,18 +39,32 @@ class NumpyBackend:
     def row(self, m, i):
         return m[i]
 
-    def w_panel(self, a, b, amu, bmu, L, lc, k):
-        w = (a @ amu.T) * (b @ bmu.T)
+    def rows(self, m, idx):
+        return m[np.asarray(idx, dtype=np.int64)]
+
+    def rows_cat(self, parts, local, at, n):
+        out = np.zeros((n, sum(w for _, w in parts)))
+        c0 = 0
+        for m, w in parts:
+            out[at, c0:c0 + w] = m[local, :w]
+            c0 += w
+        return out
+
+    def schur_block(self, rc, n1, n2):
+        a, b, lc = rc[:, :n1], rc[:, n1:n1 + n2], rc[:, n1 + n2:]
+        return (a @ a.T) * (b @ b.T) - lc @ lc.T
+
+    def take_rows(self, m, idx):
+        return m[np.asarray(idx, dtype=np.int64)]
+
+    def panel_update(self, a, b, prow, x, L, k, nb, pos_p, d):
+        n1, n2 = a.shape[1], b.shape[1]
+        w = (a @ prow[:, :n1].T) * (b @ prow[:, n1:n1 + n2].T)
         if k:
-            w -= L[:, :k] @ lc.T
-        return w
-
-    def l_update(self, w, x, L, k, b):
-        L[:, k:k + b] = w @ x.T
-
-    def downdate(self, L, k, b, pos_p, d):
-        m = pos_p >= k + b
-        d[m] -= (L[m, k:k + b] ** 2).sum(1)
+            w -= L[:, :k] @ prow[:, n1 + n2:].T
+        L[:, k:k + nb] = w @ x.T
+        m = pos_p >= k + nb
+        d[m] -= (L[m, k:k + nb] ** 2).sum(1)
 
     def scatter_rows(self, m, local, at, n, cols):
         out = np.zeros((n, cols))

@@ -44,7 +44,7 @@ def main():
     rows = []
     for rep in range(args.reps):
         b = D.DistributedBuild(comm, CudaBackend(n_mu), cfg.dims, cfg.cell3, cfg.n_v, cfg.n_c, k_mu=cfg.k_mu,
-                               n_lambda=cfg.n_lambda, batch=80)
+                               n_lambda=cfg.n_lambda, batch=128)
         r0, r1 = b.st.r0, b.st.r1
         t = {}
         sync()
