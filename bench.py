@@ -18,8 +18,10 @@ eps^-1 applied to the seeded 8-column probe block, on the Si64-sized config
              cores on a bounded, extrapolated sample (oracle/cpu_baseline.py)
 
 Inputs are larger than L2 (Phi 226 MB, Theta 906 MB) — no explicit flush.
-N > 1 (torchrun): "replicas only" this round — every rank builds its own
-replica (no data-path collective); the per-rank time is max-reduced.
+N > 1 (torchrun): the sharded build (dist.py, --mode sharded, default):
+grid-row panels, quadrature nodes split across ranks, NCCL all-reduces and
+one all-to-all — strong scaling of one build of the config; --mode replicas
+runs one full build per rank instead (weak).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config si64] [--impl ours|reference]
 """
@@ -262,6 +264,92 @@ def run_ours(args, cfg, world, rank, local):
             "stages": stages, "kernels": kernels, "roofline": roofline, "psi": psi, "e": e, "ctx": ctx}
 
 
+def run_sharded(args, cfg, world, rank, local):
+    """The multi-rank build (paper_2403_12340_b200/dist.py + the device
+    backend): grid-row panels for selection / fit / the slab FFT, quadrature
+    nodes split across ranks, NCCL all-reduces of the N_mu^2 partials and one
+    all-to-all of the slab spectra. Strong scaling: one build of the config
+    across all ranks; CUDA events on each rank, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_12340_b200 import dist as D
+    from paper_2403_12340_b200 import lrgw, synth
+    from paper_2403_12340_b200.dist_cuda import CudaBackend
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world == 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29541")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    comm = D.Comm()
+    psi = synth.orbitals_device(cfg, seed=1, device=dev)
+    e = synth.energies(cfg)
+    x_host = synth.probe_host(cfg.n_r)
+    n_mu = lrgw.num_aux(cfg.k_mu, cfg.n_v, cfg.n_c)
+    ctx = lrgw.Context(local)
+    r0, r1 = D.z_panels(cfg.dims, world)[rank]
+    # this rank's panel of Phi (column-major) and of the probe, host-pinned for e2e
+    psi_p = psi[r0:r1].t().contiguous().t()
+    del psi
+    psi_h = torch.empty(psi_p.shape[1], psi_p.shape[0], dtype=torch.float64).pin_memory()
+    psi_h.copy_(psi_p.t())
+    x_p = np.ascontiguousarray(x_host[r0:r1])
+
+    def step(phi_p):
+        b = D.DistributedBuild(comm, CudaBackend(n_mu, ctx), cfg.dims, cfg.cell3, cfg.n_v, cfg.n_c, k_mu=cfg.k_mu,
+                               n_lambda=cfg.n_lambda, batch=128)
+        a, bb = phi_p[:, :cfg.n_v], phi_p[:, cfg.n_v:]
+        pts = b.select(a, bb)
+        b.fit(pts)
+        pv, pc = b.point_rows(pts, a, bb)
+        t = b.contour(pv, pc, e)
+        k = b.smw(t, b.pvp())
+        return b.apply(k, x_p)
+
+    for _ in range(args.warmup):
+        step(psi_p)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = Clocks(local)
+    launches0 = ctx.kernel_launches()
+    t_steps = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record()
+        y = step(psi_p)
+        e1.record()
+        e1.synchronize()
+        t_steps.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    launches = ctx.kernel_launches() - launches0
+    assert np.isfinite(y).all()
+    ms = max_over_ranks(sum(t_steps) / len(t_steps), world, dev)
+    # e2e: the panel H2D from pinned host inside the timed region (the probe
+    # panel enters and eps^-1 x leaves through the host in apply)
+    psi_d = torch.empty_like(psi_h, device=dev)
+    e2e_ms = []
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record()
+        psi_d.copy_(psi_h, non_blocking=True)
+        y = step(psi_d.t())
+        e1.record()
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e = max_over_ranks(sum(e2e_ms) / len(e2e_ms), world, dev)
+    h2d = psi_h.numel() * 8 + x_p.size * 8
+    d2h = y.size * 8
+    return {"ms": ms, "e2e_ms": e2e, "h2d": h2d, "d2h": d2h, "launches": launches, "clocks": clk}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -270,18 +358,25 @@ def main():
     ap.add_argument("--config", default="si64")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default=None, choices=["single", "sharded", "replicas"],
+                    help="single (N = 1 default): the one-GPU build; sharded (N > 1 default): one build "
+                         "split across the ranks (strong scaling); replicas: one full build per rank")
     args = ap.parse_args()
 
     from paper_2403_12340_b200 import synth
 
     cfg = synth.CONFIGS[args.config]
     world, rank, local = dist_setup(args)
+    mode = args.mode or ("single" if world == 1 else "sharded")
+    if mode == "single" and world > 1:
+        mode = "replicas"
     workload = {"workload": f"{cfg.name}: grid {cfg.dims[0]}^3 = {cfg.n_r} points, cell {cfg.cell} bohr, "
                             f"N_v = N_c = {cfg.n_v}, N_mu = {int(round(cfg.k_mu * (cfg.n_v * cfg.n_c) ** 0.5))}, "
                             f"N_lambda = {cfg.n_lambda}, eps^-1 X on an {cfg.n_r}x8 probe",
                 "stages": "1-5 (select, fit, quadrature, Coulomb/ThetaVTheta, SMW) + probe apply",
                 "l2": "inputs larger than L2 (Phi 226 MB, Theta 906 MB at si64); no flush",
-                "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"}
+                "parallelism": {"single": "1 GPU", "replicas": f"replicas x{world}",
+                                "sharded": f"sharded x{world} (grid-row panels, node split, NCCL)"}[mode]}
     metric = "low-rank eps^-1 build time (s), stages 1-5 + probe apply"
 
     if args.impl == "reference":
@@ -298,7 +393,7 @@ def main():
         v = statistics.median(vals)
         line = {"impl": "reference", "metric": metric, "value": v, "unit": "s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": 1, "ms_per_step": v * 1e3, "higher_is_better": False,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
                 "config": workload,
                 "cpu_baseline": {"value": v, "unit": "s", "cores": r["cores"], "kind": "reference",
                                  "sample": r["sample"], "stages_s": r["stages"],
@@ -307,6 +402,22 @@ def main():
         print(json.dumps(line))
         return
 
+    if mode == "sharded":
+        res = run_sharded(args, cfg, world, rank, local)
+        if rank == 0:
+            line = {"metric": metric, "value": res["ms"] / 1e3, "unit": "s", "n_gpus": world,
+                    "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"],
+                    "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                    "data": "synthetic (seeded)", "config": workload,
+                    "e2e": {"value": res["e2e_ms"] / 1e3, "unit": "s", "h2d_bytes_per_step": res["h2d"],
+                            "d2h_bytes_per_step": res["d2h"]},
+                    "gpu_launches": res["launches"], "clocks": res["clocks"], "roofline": None,
+                    "cpu_baseline": None}
+            print(json.dumps(line))
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+        return
     res = run_ours(args, cfg, world, rank, local)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -320,8 +431,8 @@ def main():
     if rank == 0:
         line = {"metric": metric, "value": res["ms"] / 1e3, "unit": "s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": False,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-                "config": workload,
+                "scaling": "weak" if mode == "replicas" else "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded)", "config": workload,
                 "e2e": {"value": res["e2e_ms"] / 1e3, "unit": "s", "h2d_bytes_per_step": res["h2d"],
                         "d2h_bytes_per_step": res["d2h"]},
                 "gpu_launches": res["launches"], "clocks": res["clocks"],

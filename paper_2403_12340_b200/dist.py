@@ -313,6 +313,13 @@ class DistributedBuild:
         self.pos, self.perm, self.steps = pos, perm, steps
         return np.sort(be.to_host(perm)[:self.n_mu]).astype(np.int32)
 
+    def point_rows(self, pts, phi_v_p, phi_c_p):
+        """Phi_v, Phi_c at the (sorted) interpolation points, replicated on
+        every rank (owner-contributed, one all-reduce)."""
+        n1, n2 = self.n_v, self.n_c
+        rc = self._owned_cat(pts, ((phi_v_p, n1), (phi_c_p, n2)))
+        return self.be.take_cols(rc, 0, n1), self.be.take_cols(rc, n1, n1 + n2)
+
     def fit(self, pts):
         """Stage 2: Theta panel = L panel L_P^-1, columns in sorted-point order.
         L_P (the pivot rows of the factor) is owner-contributed and summed in

@@ -105,6 +105,9 @@ class CudaBackend:
             lrgw.dgemm_dev("N", "T", -1.0, lc, lc, 1.0, w, ctx=self.ctx)
         return w
 
+    def take_cols(self, m, c0, c1):
+        return _dev(m[:, c0:c1])
+
     def take_rows(self, m, idx):
         return _dev(m.index_select(0, torch.as_tensor(np.asarray(idx, dtype=np.int64), device=m.device)))
 

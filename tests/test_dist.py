@@ -54,6 +54,9 @@ class NumpyBackend:
         a, b, lc = rc[:, :n1], rc[:, n1:n1 + n2], rc[:, n1 + n2:]
         return (a @ a.T) * (b @ b.T) - lc @ lc.T
 
+    def take_cols(self, m, c0, c1):
+        return np.ascontiguousarray(m[:, c0:c1])
+
     def take_rows(self, m, idx):
         return m[np.asarray(idx, dtype=np.int64)]
 
@@ -171,7 +174,9 @@ def _worker(rank, world, port, out_dir, dims=DIMS):
         r0, r1 = b.st.r0, b.st.r1
         pts = b.select(psi[r0:r1, :NV].copy(), psi[r0:r1, NV:].copy())
         theta_p = b.fit(pts)
-        t = b.contour(psi[pts, :NV], psi[pts, NV:], e)
+        pv, pc = b.point_rows(pts, psi[r0:r1, :NV], psi[r0:r1, NV:])
+        assert np.array_equal(pv, psi[pts, :NV]) and np.array_equal(pc, psi[pts, NV:])
+        t = b.contour(pv, pc, e)
         pvp = b.pvp()
         k = b.smw(t, pvp)
         y_p = b.apply(k, x[r0:r1])
