@@ -164,6 +164,23 @@ int lrgw_eps_device_ptrs(lrgw_eps e, double** theta, double** k, double** t);
 int lrgw_eps_apply_dev(lrgw_ctx ctx, lrgw_eps e, const double* x, long long ldx, int m, double* y,
                        long long ldy);
 
+/* Projected screened interactions (reference gw.hpp:73-88
+ * project_screened_interactions) from a factored inverse e and the vn / nn
+ * interpolation vectors P_vn (N_r x n_vn) and P_nn (N_r x n_nn), column
+ * major:
+ *   B_x = P_x^T V P_vc,  W_x = B_x K B_x^T (x = vn, nn),  V_vn = P_vn^T V P_vn
+ * (each symmetric). Host arrays; outputs n_vn^2, n_nn^2, n_vn^2. The vn / nn
+ * decompositions themselves are lrgw_select_interpolation_points +
+ * lrgw_fit_auxiliary_basis on the pair factors (Phi_v, Psi) / (Psi, Psi)
+ * (isdf.hpp:166-183). */
+int lrgw_project_screened_interactions(lrgw_ctx ctx, lrgw_eps e, const double* p_vn, int n_vn,
+                                       const double* p_nn, int n_nn, double* w_vn, double* w_nn,
+                                       double* v_vn);
+/* The same on device arrays (P_x with leading dims ld_x; outputs n x n, ld n). */
+int lrgw_dev_project_screened(lrgw_ctx ctx, lrgw_eps e, const double* p_vn, long long ld_vn, int n_vn,
+                              const double* p_nn, long long ld_nn, int n_nn, double* w_vn, double* w_nn,
+                              double* v_vn);
+
 /* Stage-level device entry points (multi-rank orchestration composes these). */
 int lrgw_dev_select(lrgw_ctx ctx, const double* a, long long lda, int n1, const double* b,
                     long long ldb, int n2, int n_r, int n_mu, int32_t* pts_host,

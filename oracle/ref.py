@@ -293,3 +293,18 @@ def lu_solve(a, b):
     x = np.zeros_like(b, order="F")
     _check(lib().ref_lu_solve(_d(a), a.shape[0], _d(b), b.shape[1], _d(x)), "lu_solve")
     return x
+
+
+def project_screened(t, p, dims, cell, p_vn, p_nn, zero=False):
+    """gw.hpp:73-88 through the reference: (w_vn, w_nn, v_vn)."""
+    t, p, p_vn, p_nn = _f(t), _f(p), _f(p_vn), _f(p_nn)
+    d = np.array(dims, dtype=np.int32)
+    c = np.array(cell, dtype=np.float64)
+    n_vn, n_nn = p_vn.shape[1], p_nn.shape[1]
+    w_vn = np.zeros((n_vn, n_vn), order="F")
+    w_nn = np.zeros((n_nn, n_nn), order="F")
+    v_vn = np.zeros((n_vn, n_vn), order="F")
+    _check(lib().ref_project_screened(_d(t), _d(p), p.shape[0], p.shape[1], _i(d), _d(c), 1 if zero else 0,
+                                      _d(p_vn), n_vn, _d(p_nn), n_nn, _d(w_vn), _d(w_nn), _d(v_vn)),
+           "project_screened_interactions")
+    return w_vn, w_nn, v_vn

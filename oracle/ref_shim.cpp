@@ -17,6 +17,7 @@
 
 #include "lrgw/contour.hpp"
 #include "lrgw/elliptic.hpp"
+#include "lrgw/gw.hpp"
 #include "lrgw/isdf.hpp"
 #include "lrgw/linalg.hpp"
 #include "lrgw/model.hpp"
@@ -362,6 +363,26 @@ int ref_build_and_apply(const double* t, const double* p, int n_r, int n_mu,
     if (x && y) to_ptr(epsilon_inverse_apply(e, from_ptr(x, n_r, m)), y);
     if (k_out) to_ptr(e.k, k_out);
     if (vp_out) to_ptr(e.vp, vp_out);
+  });
+}
+
+// gw.hpp:73-88 — projected screened interactions from the factored inverse
+// built on (T, P_vc) (smw.hpp:84-95) and the vn / nn interpolation vectors.
+int ref_project_screened(const double* t, const double* p, int n_r, int n_mu, const int* dims,
+                         const double* cell, int zero_kernel, const double* p_vn, int n_vn,
+                         const double* p_nn, int n_nn, double* w_vn, double* w_nn, double* v_vn) {
+  return guarded([&] {
+    Grid g = make_grid(dims, cell);
+    if (g.n_r() != n_r) throw invalid_input("shim: grid / N_r mismatch");
+    CoulombOperator v = zero_kernel ? zero_coulomb(g) : build_coulomb(g, CoulombMode::reciprocal_diagonal);
+    EpsilonInverseLowRank e = build_epsilon_inverse(from_ptr(t, n_mu, n_mu), from_ptr(p, n_r, n_mu), v);
+    IsdfDecomposition vn, nn;
+    vn.p = from_ptr(p_vn, n_r, n_vn);
+    nn.p = from_ptr(p_nn, n_r, n_nn);
+    ScreenedProjections out = project_screened_interactions(e, vn, nn);
+    to_ptr(out.w_vn, w_vn);
+    to_ptr(out.w_nn, w_nn);
+    to_ptr(out.v_vn, v_vn);
   });
 }
 

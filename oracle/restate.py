@@ -578,3 +578,15 @@ def epsilon_inverse_apply(p, k, dims, cell, x) -> np.ndarray:
     """smw.hpp:84-103 — X + (V P) (K (P^T X))."""
     vp = apply_coulomb(dims, cell, p)
     return x + vp @ (k @ (p.T @ x))
+
+
+def project_screened(p_vc, k, dims, cell, p_vn, p_nn, kernel=None):
+    """gw.hpp:73-88 — B_x = P_x^T (V P_vc), W_x = B_x K B_x^T (x = vn, nn),
+    V_vn = P_vn^T V P_vn, each symmetrised. Returns (w_vn, w_nn, v_vn)."""
+    vp = apply_coulomb(dims, cell, p_vc, kernel)
+    b_vn = p_vn.T @ vp
+    b_nn = p_nn.T @ vp
+    w_vn = symmetrize((b_vn @ k) @ b_vn.T)
+    w_nn = symmetrize((b_nn @ k) @ b_nn.T)
+    v_vn = symmetrize(p_vn.T @ apply_coulomb(dims, cell, p_vn, kernel))
+    return w_vn, w_nn, v_vn

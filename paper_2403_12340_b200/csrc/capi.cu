@@ -377,6 +377,47 @@ void pvp_impl(lrgw_ctx c, const int* dims, const double* cell, int zero, const d
   ck(mirror_lower(c->stream, pvp, n_mu, n_mu, false), "mirror");
 }
 
+// Projected screened interactions (gw.hpp:73-88) from the factored inverse:
+//   B_x = P_x^T V P_vc,  W_x = B_x K B_x^T  (x = vn, nn),  V_vn = P_vn^T V P_vn.
+// Every N_r contraction runs in G space over the half spectrum, like pvp_impl:
+// one D2Z per operand (P_vc's spectrum shared by both B), then DMMA GEMMs
+// with w_G v(G)/N_r fused as the k-scale — B_x is a cross GEMM, V_vn a
+// lower-tile SYRK. The N_mu-sized products are lower-tile GEMMs, mirrored
+// (exactly symmetric, the reference's symmetrize).
+void project_impl(lrgw_ctx c, const lrgw_eps_s* e, const double* p_vn, long long ld_vn, int n_vn,
+                  const double* p_nn, long long ld_nn, int n_nn, double* w_vn, double* w_nn, double* v_vn) {
+  const int n_mu = e->n_mu;
+  const long long nh = half_len(e->dims);
+  DBuf xvc = dalloc(c, (size_t)2 * nh * n_mu);
+  fft_forward(c, e->dims, e->theta, e->n_r, n_mu, xvc.d());
+  DBuf wts = dalloc(c, (size_t)2 * nh);
+  ck(coulomb_half_weights(c->stream, e->dims[0], e->dims[1], e->dims[2], e->cell[0], e->cell[1], e->cell[2],
+                          e->zero, wts.d()),
+     "coulomb_half_weights");
+  const int nmax = std::max({n_vn, n_nn, n_mu});
+  Work w = make_work(c, (size_t)16 * nmax * nmax);
+  DBuf b = dalloc(c, (size_t)nmax * n_mu), bk = dalloc(c, (size_t)nmax * n_mu);
+  auto one = [&](const double* px, long long ldx, int nx, double* wx, double* vx) {
+    if (nx <= 0) return;
+    DBuf xh = dalloc(c, (size_t)2 * nh * nx);
+    fft_forward(c, e->dims, px, ldx, nx, xh.d());
+    // B = P_x^T V P_vc (nx x n_mu): k = interleaved half-spectrum reals
+    gemm(c, nx, n_mu, (int)(2 * nh), xh.d(), 2 * nh, Lay::K, xvc.d(), 2 * nh, Lay::K, b.d(), nx, 1.0, 0.0,
+         wts.d(), false, &w);
+    // B K (K symmetric), then W = (B K) B^T on lower tiles
+    gemm(c, nx, n_mu, n_mu, b.d(), nx, Lay::MN, e->k, n_mu, Lay::MN, bk.d(), nx, 1.0, 0.0);
+    gemm(c, nx, nx, n_mu, bk.d(), nx, Lay::MN, b.d(), nx, Lay::MN, wx, nx, 1.0, 0.0, nullptr, true, &w);
+    ck(mirror_lower(c->stream, wx, nx, nx, false), "mirror");
+    if (vx) {
+      gemm(c, nx, nx, (int)(2 * nh), xh.d(), 2 * nh, Lay::K, xh.d(), 2 * nh, Lay::K, vx, nx, 1.0, 0.0, wts.d(),
+           true, &w);
+      ck(mirror_lower(c->stream, vx, nx, nx, false), "mirror");
+    }
+  };
+  one(p_vn, ld_vn, n_vn, w_vn, v_vn);
+  one(p_nn, ld_nn, n_nn, w_nn, nullptr);
+}
+
 // ---------------------------------------------------------------------------
 // Dense N_mu x N_mu leaf factorisations (cuSOLVER).
 // ---------------------------------------------------------------------------
@@ -1594,6 +1635,34 @@ int lrgw_dev_gram_weighted(lrgw_ctx c, const double* x, long long ldx, int kdim,
     Work wk = make_work(c, (size_t)16 * m * m);
     gemm(c, m, m, kdim, x, ldx, Lay::K, x, ldx, Lay::K, out, ldo, 1.0, 0.0, w, true, &wk);
     ck(mirror_lower(c->stream, out, m, ldo, false), "mirror");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int lrgw_project_screened_interactions(lrgw_ctx c, lrgw_eps e, const double* p_vn, int n_vn, const double* p_nn,
+                                       int n_nn, double* w_vn, double* w_nn, double* v_vn) {
+  return guarded(c, [&] {
+    if (!e) fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: null handle");
+    if (n_vn < 0 || n_nn < 0 || (n_vn > 0 && !p_vn) || (n_nn > 0 && !p_nn))
+      fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: bad sizes");
+    const size_t n_r = e->n_r;
+    DBuf dvn = upload(c, p_vn, n_r * n_vn), dnn = upload(c, p_nn, n_r * n_nn);
+    DBuf wvn = dalloc(c, (size_t)n_vn * n_vn), wnn = dalloc(c, (size_t)n_nn * n_nn), vvn = dalloc(c, (size_t)n_vn * n_vn);
+    project_impl(c, e, dvn.d(), e->n_r, n_vn, dnn.d(), e->n_r, n_nn, wvn.d(), wnn.d(), vvn.d());
+    download(c, w_vn, wvn.p, sizeof(double) * n_vn * n_vn);
+    download(c, w_nn, wnn.p, sizeof(double) * n_nn * n_nn);
+    download(c, v_vn, vvn.p, sizeof(double) * n_vn * n_vn);
+  });
+}
+
+int lrgw_dev_project_screened(lrgw_ctx c, lrgw_eps e, const double* p_vn, long long ld_vn, int n_vn,
+                              const double* p_nn, long long ld_nn, int n_nn, double* w_vn, double* w_nn,
+                              double* v_vn) {
+  return guarded(c, [&] {
+    if (!e) fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: null handle");
+    if (n_vn < 0 || n_nn < 0 || (n_vn > 0 && ld_vn < e->n_r) || (n_nn > 0 && ld_nn < e->n_r))
+      fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: bad sizes");
+    project_impl(c, e, p_vn, ld_vn, n_vn, p_nn, ld_nn, n_nn, w_vn, w_nn, v_vn);
     ck(cudaStreamSynchronize(c->stream), "sync");
   });
 }

@@ -223,12 +223,24 @@ class IsdfDecomposition:
     p: np.ndarray
 
 
-def build_isdf(psi, n_v, n_c, k_mu, ctx=None) -> IsdfDecomposition:
-    """isdf.hpp:176-183 for the vc pair set."""
-    a, b = psi[:, :n_v], psi[:, n_v:n_v + n_c]
-    n_mu = min(max(num_aux(k_mu, n_v, n_c), 1), psi.shape[0])
+def pair_factors(psi, n_v, n_c, label: str = "vc"):
+    """isdf.hpp:166-173 — (occupied, unoccupied), (occupied, all) or (all, all)."""
+    occ, allb = psi[:, :n_v], psi[:, :n_v + n_c]
+    if label == "vc":
+        return occ, psi[:, n_v:n_v + n_c]
+    if label == "vn":
+        return occ, allb
+    if label == "nn":
+        return allb, allb
+    raise InvalidInput(f"pair_factors: unknown pair set {label!r}")
+
+
+def build_isdf(psi, n_v, n_c, k_mu, ctx=None, label: str = "vc") -> IsdfDecomposition:
+    """isdf.hpp:176-183 — select + fit for the vc / vn / nn pair set."""
+    a, b = pair_factors(psi, n_v, n_c, label)
+    n_mu = min(max(num_aux(k_mu, a.shape[1], b.shape[1]), 1), psi.shape[0])
     pts = select_interpolation_points(a, b, n_mu, ctx=ctx)
-    return IsdfDecomposition("vc", k_mu, n_mu, pts, fit_auxiliary_basis(a, b, pts, ctx=ctx))
+    return IsdfDecomposition(label, k_mu, n_mu, pts, fit_auxiliary_basis(a, b, pts, ctx=ctx))
 
 
 # ---------------------------------------------------------------------------
@@ -481,6 +493,32 @@ def build_epsilon_inverse(t, p, dims, cell, threads: int = 1, zero_kernel: bool 
                                              d.ctypes.data_as(L.c_int_p), _dp(cl), int(zero_kernel),
                                              ctypes.byref(h)), c.handle, "build_epsilon_inverse")
     return EpsilonInverseLowRank(c, h)
+
+
+@dataclass
+class ScreenedProjections:
+    """gw.hpp:65-69."""
+    w_vn: np.ndarray  # (P_vn^T V P_vc) K (P_vn^T V P_vc)^T
+    w_nn: np.ndarray
+    v_vn: np.ndarray  # P_vn^T V P_vn
+
+
+def project_screened_interactions(e: EpsilonInverseLowRank, dec_vn, dec_nn, threads: int = 1) -> ScreenedProjections:
+    """gw.hpp:73-88 on the GPU (G-space contractions against e's device
+    factors). dec_vn / dec_nn: IsdfDecomposition or N_r x n matrices."""
+    p_vn = _f(getattr(dec_vn, "p", dec_vn))
+    p_nn = _f(getattr(dec_nn, "p", dec_nn))
+    if p_vn.shape[0] != e.n_r or p_nn.shape[0] != e.n_r:
+        raise InvalidInput("project_screened_interactions: grid mismatch")
+    n_vn, n_nn = p_vn.shape[1], p_nn.shape[1]
+    w_vn = np.zeros((n_vn, n_vn), order="F")
+    w_nn = np.zeros((n_nn, n_nn), order="F")
+    v_vn = np.zeros((n_vn, n_vn), order="F")
+    c = e.ctx
+    _check(c._lib.lrgw_project_screened_interactions(c.handle, e.handle, _dp(p_vn), n_vn, _dp(p_nn), n_nn,
+                                                     _dp(w_vn), _dp(w_nn), _dp(v_vn)),
+           c.handle, "project_screened_interactions")
+    return ScreenedProjections(w_vn, w_nn, v_vn)
 
 
 def epsilon_inverse_from_parts(p, k, dims, cell, ctx=None) -> EpsilonInverseLowRank:

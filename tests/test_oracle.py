@@ -147,6 +147,39 @@ def test_restatement_matches_reference_smw(ref):
     assert rel(R.epsilon_inverse_apply(th, k_o, dims, cell, x), y_r) < 1e-13
 
 
+def gw_system(ref, seed=2, dims=(8, 8, 4), n=8, k=6.0):
+    """test_gw.cpp:18-30 System: synthetic orbitals and the vc / vn / nn ISDF
+    (pair factors isdf.hpp:166-173) through the reference."""
+    psi, e = ref.build_synthetic(seed, dims, (6.0, 6.0, 6.0), n, n, 1.0, 4.0)
+    a, b = psi[:, :n], psi[:, n:]
+    decs = {}
+    for label, (f1, f2) in {"vc": (a, b), "vn": (a, psi), "nn": (psi, psi)}.items():
+        nmu = min(max(R.num_aux(k, f1.shape[1], f2.shape[1]), 1), f1.shape[0])
+        pts = ref.select_points(f1, f2, nmu)
+        decs[label] = (pts, ref.fit(f1, f2, pts))
+    t = ref.coupled_direct(a[decs["vc"][0]], b[decs["vc"][0]], e)
+    return psi, e, decs, t
+
+
+def test_restatement_matches_reference_projections(ref):
+    dims, cell = (8, 8, 4), (6.0, 6.0, 6.0)
+    psi, e, decs, t = gw_system(ref)
+    th_vc, th_vn, th_nn = decs["vc"][1], decs["vn"][1], decs["nn"][1]
+    got_r = ref.project_screened(t, th_vc, dims, cell, th_vn, th_nn)
+    k = R.assemble_K(t, th_vc, dims, cell)
+    got_o = R.project_screened(th_vc, k, dims, cell, th_vn, th_nn)
+    for x, y in zip(got_o, got_r):
+        assert rel(x, y) <= 1e-11
+    # test_gw.cpp:91-110: W_vn is P_vn^T (eps^-1 - I) V P_vn of the same ISDF eps
+    n_r = psi.shape[0]
+    em = R.epsilon_inverse_apply(th_vc, k, dims, cell, np.eye(n_r)) - np.eye(n_r)
+    w_dense = R.symmetrize(th_vn.T @ (em @ R.apply_coulomb(dims, cell, th_vn)))
+    assert rel(got_o[0], w_dense) <= 1e-9
+    # zero interaction (test_gw.cpp:66-89)
+    z = ref.project_screened(t, th_vc, dims, cell, th_vn, th_nn, zero=True)
+    assert np.linalg.norm(z[0]) <= 1e-12 and np.linalg.norm(z[2]) <= 1e-12
+
+
 def test_restatement_error_behaviour(ref):
     # degenerate Gram (test_isdf.cpp:228-231) and rank-deficient T (test_smw.cpp:74-85)
     with pytest.raises(R.NumericError):
