@@ -386,13 +386,13 @@ def main():
 
         cores = os.cpu_count() or 1
         vals = []
-        for i in range(args.steps + 1):  # one untimed warm-up sample
+        for i in range(args.warmup + args.steps):  # W untimed warm-up samples, then K timed
             r = cpu_baseline.run(cfg, cores=cores, sel_steps=16, fit_rows=(1536, 2560), cols=64, seed=5 + i)
-            if i > 0:
+            if i >= args.warmup:
                 vals.append(r["total_s"])
         v = statistics.median(vals)
         line = {"impl": "reference", "metric": metric, "value": v, "unit": "s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": 1, "ms_per_step": v * 1e3, "higher_is_better": False,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
                 "config": workload,
                 "cpu_baseline": {"value": v, "unit": "s", "cores": r["cores"], "kind": "reference",

@@ -1,5 +1,3 @@
-for env in 0 512; do
-  LRGW_SYRK_L=$env python tools/bench_syrk.py 1024 115200
-  LRGW_SYRK_L=$env python tools/bench_syrk.py 3456 383616 3
-  LRGW_SYRK_L=$env python tools/bench_syrk.py 960 256000
-done
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_gw.py tests/test_dropin.py tests/test_gpu_projections.py -x -q > gpurun_out/gw_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gw_tests.log
+tail -30 gpurun_out/gw_tests.log

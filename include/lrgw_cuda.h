@@ -181,6 +181,28 @@ int lrgw_dev_project_screened(lrgw_ctx ctx, lrgw_eps e, const double* p_vn, long
                               const double* p_nn, long long ld_nn, int n_nn, double* w_vn, double* w_nn,
                               double* v_vn);
 
+/* Static-COHSEX self-energy diagonals of the low-rank pipeline (reference
+ * gw.hpp:93-137 detail::sigma_hadamard + gw.hpp:143-153
+ * self_energies_lowrank): with Psi = orbitals (n_r x (n_v + n_c), column
+ * major), Psi_vn / Psi_nn its rows at the vn / nn points,
+ *   sigma_sex_x = -diag(Psi_vn^T (W_vn o Psi_o Psi_o^T) Psi_vn)
+ *   sigma_x     = -diag(Psi_vn^T (V_vn o Psi_o Psi_o^T) Psi_vn)
+ *   sigma_coh   = 1/2 diag(Psi_nn^T (W_nn o Psi_nn Psi_nn^T) Psi_nn)
+ * (Psi_o = the occupied columns of Psi_vn) and sigma_total their sum
+ * (SelfEnergies::finalize, gw.hpp:31-41: LRGW_ERR_NUMERIC on a non-finite
+ * band). Host arrays; outputs of length n_v + n_c (any may be null). */
+int lrgw_self_energies_lowrank(lrgw_ctx ctx, const double* psi, int n_r, int n_v, int n_c,
+                               const int32_t* pts_vn, int n_vn, const int32_t* pts_nn, int n_nn,
+                               const double* w_vn, const double* w_nn, const double* v_vn,
+                               double* sigma_sex_x, double* sigma_x, double* sigma_coh,
+                               double* sigma_total);
+/* The same on device arrays (psi with leading dim ldp; W / V blocks n x n,
+ * ld n; point arrays on the host; device outputs, no finiteness check). */
+int lrgw_dev_self_energies(lrgw_ctx ctx, const double* psi, long long ldp, int n_r, int n_v, int n_c,
+                           const int32_t* pts_vn, int n_vn, const int32_t* pts_nn, int n_nn,
+                           const double* w_vn, const double* w_nn, const double* v_vn,
+                           double* sigma_sex_x, double* sigma_x, double* sigma_coh);
+
 /* Stage-level device entry points (multi-rank orchestration composes these). */
 int lrgw_dev_select(lrgw_ctx ctx, const double* a, long long lda, int n1, const double* b,
                     long long ldb, int n2, int n_r, int n_mu, int32_t* pts_host,

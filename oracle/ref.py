@@ -308,3 +308,44 @@ def project_screened(t, p, dims, cell, p_vn, p_nn, zero=False):
                                       _d(p_vn), n_vn, _d(p_nn), n_nn, _d(w_vn), _d(w_nn), _d(v_vn)),
            "project_screened_interactions")
     return w_vn, w_nn, v_vn
+
+
+def sigma_lowrank(psi, n_v, pts_vn, pts_nn, w_vn, w_nn, v_vn):
+    """gw.hpp:143-153 on given projections: (sex_x, x, coh, total)."""
+    psi = _f(psi)
+    n_r, nb = psi.shape
+    pv = _i(np.ascontiguousarray(pts_vn, dtype=np.int32))
+    pn = _i(np.ascontiguousarray(pts_nn, dtype=np.int32))
+    out = np.zeros(4 * nb)
+    _check(lib().ref_sigma_lowrank(_d(psi), n_r, n_v, nb - n_v, pv, len(pts_vn), pn, len(pts_nn), _d(_f(w_vn)),
+                                   _d(_f(w_nn)), _d(_f(v_vn)), _d(out)), "self_energies_lowrank")
+    return tuple(out.reshape(4, nb))
+
+
+def self_energies(psi, n_v, dims, cell, energies, pts_vc, pts_vn, pts_nn, which="lowrank"):
+    """The gw.hpp pipelines on fixed point sets (test_gw.cpp:13-41):
+    which = lowrank | conventional | bruteforce -> (sex_x, x, coh, total)."""
+    psi = _f(psi)
+    n_r, nb = psi.shape
+    d = np.array(dims, dtype=np.int32)
+    c = np.array(cell, dtype=np.float64)
+    e = np.ascontiguousarray(energies, dtype=np.float64)
+    code = {"lowrank": 0, "conventional": 1, "bruteforce": 2}[which]
+    out = np.zeros(4 * nb)
+    args = []
+    for pts in (pts_vc, pts_vn, pts_nn):
+        p = np.ascontiguousarray(pts, dtype=np.int32)
+        args += [_i(p), len(p)]
+    _check(lib().ref_self_energies(_d(psi), n_r, n_v, nb - n_v, _i(d), _d(c), _d(e), *args, code, _d(out)),
+           "self_energies_" + which)
+    return tuple(out.reshape(4, nb))
+
+
+def quasiparticle(energies, vxc, sigma_total):
+    """gw.hpp:48-58."""
+    e = np.ascontiguousarray(energies, dtype=np.float64)
+    v = np.ascontiguousarray(vxc, dtype=np.float64)
+    s = np.ascontiguousarray(sigma_total, dtype=np.float64)
+    out = np.zeros(e.size)
+    _check(lib().ref_quasiparticle(_d(e), _d(v), _d(s), e.size, s.size, _d(out)), "quasiparticle_energies")
+    return out

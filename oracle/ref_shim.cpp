@@ -386,6 +386,102 @@ int ref_project_screened(const double* t, const double* p, int n_r, int n_mu, co
   });
 }
 
+ElectronicStructure make_es(const double* psi, int n_r, int n_v, int n_c, const int* dims, const double* cell,
+                            const double* energies) {
+  ElectronicStructure es;
+  es.grid = make_grid(dims, cell);
+  if (es.grid.n_r() != n_r) throw invalid_input("shim: grid / N_r mismatch");
+  es.psi = from_ptr(psi, n_r, n_v + n_c);
+  es.n_v = n_v;
+  es.n_c = n_c;
+  es.energies.assign(energies, energies + n_v + n_c);
+  es.vxc.assign(n_v + n_c, 0.0);
+  return es;
+}
+
+IsdfDecomposition dec_at(const ElectronicStructure& es, PairSetLabel label, const int* pts, int n) {
+  Matrix a = label == PairSetLabel::nn ? es.psi : es.occupied();
+  Matrix b = label == PairSetLabel::vc ? es.unoccupied() : es.psi;
+  return fit_auxiliary_basis(a, b, std::vector<int>(pts, pts + n), label);
+}
+
+void put_sigma(const SelfEnergies& s, int nb, double* out4) {
+  for (int n = 0; n < nb; ++n) {
+    out4[n] = s.sigma_sex_x[n];
+    out4[nb + n] = s.sigma_x[n];
+    out4[2 * nb + n] = s.sigma_coh[n];
+    out4[3 * nb + n] = s.sigma_total[n];
+  }
+}
+
+// gw.hpp:143-153 — self_energies_lowrank on caller-supplied projections
+// (the leaf the GPU's lrgw_self_energies_lowrank replaces).
+int ref_sigma_lowrank(const double* psi, int n_r, int n_v, int n_c, const int* pts_vn, int n_vn,
+                      const int* pts_nn, int n_nn, const double* w_vn, const double* w_nn,
+                      const double* v_vn, double* out4) {
+  return guarded([&] {
+    ElectronicStructure es;
+    es.psi = from_ptr(psi, n_r, n_v + n_c);
+    es.n_v = n_v;
+    es.n_c = n_c;
+    IsdfDecomposition vn, nn;
+    vn.point_indices.assign(pts_vn, pts_vn + n_vn);
+    nn.point_indices.assign(pts_nn, pts_nn + n_nn);
+    SelfEnergies s = self_energies_lowrank(es, from_ptr(w_vn, n_vn, n_vn), from_ptr(w_nn, n_nn, n_nn),
+                                           from_ptr(v_vn, n_vn, n_vn), vn, nn);
+    put_sigma(s, n_v + n_c, out4);
+  });
+}
+
+// The three self-energy pipelines of gw.hpp on fixed point sets, composed as
+// test_gw.cpp:13-41 does: which = 0 low-rank (T direct, build_epsilon_inverse,
+// project_screened_interactions, self_energies_lowrank), 1 conventional ISDF
+// (dense eps, gw.hpp:158-181), 2 brute force (gw.hpp:189-222).
+int ref_self_energies(const double* psi, int n_r, int n_v, int n_c, const int* dims, const double* cell,
+                      const double* energies, const int* pts_vc, int n_vc, const int* pts_vn, int n_vn,
+                      const int* pts_nn, int n_nn, int which, double* out4) {
+  return guarded([&] {
+    ElectronicStructure es = make_es(psi, n_r, n_v, n_c, dims, cell, energies);
+    CoulombOperator v = build_coulomb(es.grid, CoulombMode::reciprocal_diagonal);
+    SelfEnergies s;
+    if (which == 2) {
+      s = self_energies_bruteforce(es, v);
+    } else {
+      IsdfDecomposition vc = dec_at(es, PairSetLabel::vc, pts_vc, n_vc);
+      IsdfDecomposition vn = dec_at(es, PairSetLabel::vn, pts_vn, n_vn);
+      IsdfDecomposition nn = dec_at(es, PairSetLabel::nn, pts_nn, n_nn);
+      if (which == 1) {
+        s = self_energies_isdf_conventional(es, v, vc, vn, nn);
+      } else {
+        Matrix t = coupled_coefficients_direct(rows_at(es.occupied(), vc.point_indices),
+                                               rows_at(es.unoccupied(), vc.point_indices), es.energies)
+                       .t;
+        EpsilonInverseLowRank e = build_epsilon_inverse(t, vc.p, v);
+        ScreenedProjections proj = project_screened_interactions(e, vn, nn);
+        s = self_energies_lowrank(es, proj.w_vn, proj.w_nn, proj.v_vn, vn, nn);
+      }
+    }
+    put_sigma(s, n_v + n_c, out4);
+  });
+}
+
+// gw.hpp:48-58
+int ref_quasiparticle(const double* energies, const double* vxc, const double* sigma_total, int n,
+                      int n_sigma, double* out) {
+  return guarded([&] {
+    ElectronicStructure es;
+    es.energies.assign(energies, energies + n);
+    es.vxc.assign(vxc, vxc + n);
+    SelfEnergies s;
+    s.sigma_sex_x.assign(sigma_total, sigma_total + n_sigma);
+    s.sigma_x.assign(n_sigma, 0.0);
+    s.sigma_coh.assign(n_sigma, 0.0);
+    s.finalize(PipelineTag::lowrank);
+    QuasiparticleEnergies q = quasiparticle_energies(es, s);
+    for (int i = 0; i < n; ++i) out[i] = q.eps_gw[i];
+  });
+}
+
 // smw.hpp:97-103 with caller-supplied K (e.g. K = 0 identity check).
 int ref_eps_apply_given(const double* p, const double* k, int n_r, int n_mu,
                         const int* dims, const double* cell, const double* x,

@@ -590,3 +590,34 @@ def project_screened(p_vc, k, dims, cell, p_vn, p_nn, kernel=None):
     w_nn = symmetrize((b_nn @ k) @ b_nn.T)
     v_vn = symmetrize(p_vn.T @ apply_coulomb(dims, cell, p_vn, kernel))
     return w_vn, w_nn, v_vn
+
+
+def hadamard_diag(h: np.ndarray, mask: np.ndarray, psi_pts: np.ndarray) -> np.ndarray:
+    """gw.hpp:93-107 — diag(Psi^T (H o M) Psi) for all bands."""
+    hp = (h * mask) @ psi_pts
+    return np.einsum("in,in->n", psi_pts, hp)
+
+
+def sigma_lowrank(psi, n_v: int, pts_vn, pts_nn, w_vn, w_nn, v_vn):
+    """gw.hpp:112-137 (detail::sigma_hadamard) + finalize (gw.hpp:31-41):
+    returns (sigma_sex_x, sigma_x, sigma_coh, sigma_total)."""
+    psi_vn = psi[np.asarray(pts_vn)]
+    psi_nn = psi[np.asarray(pts_nn)]
+    occ = psi_vn[:, :n_v]
+    mask_occ = occ @ occ.T
+    mask_all = psi_nn @ psi_nn.T
+    sex_x = -hadamard_diag(w_vn, mask_occ, psi_vn)
+    sx = -hadamard_diag(v_vn, mask_occ, psi_vn)
+    coh = 0.5 * hadamard_diag(w_nn, mask_all, psi_nn)
+    total = sex_x + sx + coh
+    if not np.all(np.isfinite(total)):
+        raise NumericError("self-energies: non-finite value")
+    return sex_x, sx, coh, total
+
+
+def quasiparticle_energies(energies, vxc, sigma_total) -> np.ndarray:
+    """gw.hpp:48-58."""
+    e = np.asarray(energies, dtype=np.float64)
+    if len(sigma_total) != e.size or len(vxc) != e.size:
+        raise InvalidInput("quasiparticle_energies: length mismatch")
+    return e + np.asarray(sigma_total) - np.asarray(vxc)

@@ -136,6 +136,14 @@ _SIGS = {
     "lrgw_dev_project_screened": (ctypes.c_int, [ctx_t, eps_t, ctypes.c_void_p, c_ll, ctypes.c_int, ctypes.c_void_p,
                                                  c_ll, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                                  ctypes.c_void_p]),
+    "lrgw_self_energies_lowrank": (ctypes.c_int, [ctx_t, c_double_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                  c_int32_p, ctypes.c_int, c_int32_p, ctypes.c_int, c_double_p,
+                                                  c_double_p, c_double_p, c_double_p, c_double_p, c_double_p,
+                                                  c_double_p]),
+    "lrgw_dev_self_energies": (ctypes.c_int, [ctx_t, ctypes.c_void_p, c_ll, ctypes.c_int, ctypes.c_int,
+                                              ctypes.c_int, c_int32_p, ctypes.c_int, c_int32_p, ctypes.c_int,
+                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "lrgw_dev_dgemm": (ctypes.c_int, [ctx_t, ctypes.c_char, ctypes.c_char, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, ctypes.c_double, ctypes.c_void_p, c_ll, ctypes.c_void_p,
                                       c_ll, ctypes.c_double, ctypes.c_void_p, c_ll]),

@@ -418,6 +418,59 @@ void project_impl(lrgw_ctx c, const lrgw_eps_s* e, const double* p_vn, long long
   one(p_nn, ld_nn, n_nn, w_nn, nullptr);
 }
 
+// Static-COHSEX self-energy diagonals (gw.hpp:93-137, sigma_hadamard) on
+// the device: Psi rows at the vn / nn points (gather), the occupied and
+// all-band masks as lower-tile DMMA SYRKs, H o M in place, (H o M) Psi as a
+// DMMA GEMM and the per-band column dot with the sign / 1/2 folded in:
+//   sex_x = -diag(Psi_vn^T (W_vn o M_occ) Psi_vn), x = -diag(... V_vn ...),
+//   coh = 1/2 diag(Psi_nn^T (W_nn o M_all) Psi_nn).
+void sigma_impl(lrgw_ctx c, const double* psi, long long ldp, int n_v, int nb, const int32_t* pts_vn,
+                int n_vn, const int32_t* pts_nn, int n_nn, const double* w_vn, const double* v_vn,
+                const double* w_nn, double* sex_x, double* sx, double* coh) {
+  const int nmax = std::max(n_vn, n_nn);
+  Work w = make_work(c, (size_t)16 * std::max(nmax, 1) * std::max(nmax, 1));
+  DBuf mask = dalloc(c, (size_t)nmax * nmax), hm = dalloc(c, (size_t)nmax * nmax);
+  auto one_set = [&](const int32_t* pts, int n, int n_occ, const double* h1, double* out1, double a1,
+                     const double* h2, double* out2, double a2) {
+    DBuf dp = upload_i(c, pts, n);
+    DBuf ps = dalloc(c, (size_t)n * nb), hp = dalloc(c, (size_t)n * nb);
+    ck(gather_rows(c->stream, psi, ldp, nb, dp.i(), n, ps.d(), n), "gather");
+    // M = Psi_o Psi_o^T (n x n, lower tiles + mirror)
+    if (n_occ > 0) {
+      gemm(c, n, n, n_occ, ps.d(), n, Lay::MN, ps.d(), n, Lay::MN, mask.d(), n, 1.0, 0.0, nullptr, true, &w);
+      ck(mirror_lower(c->stream, mask.d(), n, n, false), "mirror");
+    } else {
+      ck(fill(c->stream, mask.d(), (size_t)n * n, 0.0), "fill");
+    }
+    auto diag = [&](const double* h, double* out, double alpha) {
+      ck(cudaMemcpyAsync(hm.d(), mask.d(), sizeof(double) * n * n, cudaMemcpyDeviceToDevice, c->stream), "D2D");
+      ck(hadamard_inplace(c->stream, n, h, n, hm.d(), n), "hadamard");
+      // hp = (H o M) Psi: B(band, nu) = Psi(nu, band) is K-contiguous
+      gemm(c, n, nb, n, hm.d(), n, Lay::MN, ps.d(), n, Lay::K, hp.d(), n, 1.0, 0.0);
+      ck(col_dot(c->stream, n, nb, ps.d(), n, hp.d(), n, alpha, out), "col_dot");
+    };
+    diag(h1, out1, a1);
+    if (h2) diag(h2, out2, a2);
+  };
+  if (n_vn > 0) {
+    one_set(pts_vn, n_vn, n_v, w_vn, sex_x, -1.0, v_vn, sx, -1.0);
+  } else {
+    ck(fill(c->stream, sex_x, nb, 0.0), "fill");
+    ck(fill(c->stream, sx, nb, 0.0), "fill");
+  }
+  if (n_nn > 0) {
+    one_set(pts_nn, n_nn, nb, w_nn, coh, 0.5, nullptr, nullptr, 0.0);
+  } else {
+    ck(fill(c->stream, coh, nb, 0.0), "fill");
+  }
+}
+
+void check_points(const int32_t* pts, int n, int n_r, const char* what) {
+  if (n > 0 && !pts) fail(LRGW_ERR_INVALID_INPUT, std::string(what) + ": null point array");
+  for (int i = 0; i < n; ++i)
+    if (pts[i] < 0 || pts[i] >= n_r) fail(LRGW_ERR_INVALID_INPUT, std::string(what) + ": point index out of range");
+}
+
 // ---------------------------------------------------------------------------
 // Dense N_mu x N_mu leaf factorisations (cuSOLVER).
 // ---------------------------------------------------------------------------
@@ -1663,6 +1716,54 @@ int lrgw_dev_project_screened(lrgw_ctx c, lrgw_eps e, const double* p_vn, long l
     if (n_vn < 0 || n_nn < 0 || (n_vn > 0 && ld_vn < e->n_r) || (n_nn > 0 && ld_nn < e->n_r))
       fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: bad sizes");
     project_impl(c, e, p_vn, ld_vn, n_vn, p_nn, ld_nn, n_nn, w_vn, w_nn, v_vn);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int lrgw_self_energies_lowrank(lrgw_ctx c, const double* psi, int n_r, int n_v, int n_c, const int32_t* pts_vn,
+                               int n_vn, const int32_t* pts_nn, int n_nn, const double* w_vn, const double* w_nn,
+                               const double* v_vn, double* sigma_sex_x, double* sigma_x, double* sigma_coh,
+                               double* sigma_total) {
+  return guarded(c, [&] {
+    const int nb = n_v + n_c;
+    if (n_r < 1 || n_v < 0 || n_c < 0 || nb < 1 || n_vn < 0 || n_nn < 0 || !psi)
+      fail(LRGW_ERR_INVALID_INPUT, "self_energies_lowrank: bad sizes");
+    if ((n_vn > 0 && (!w_vn || !v_vn)) || (n_nn > 0 && !w_nn))
+      fail(LRGW_ERR_INVALID_INPUT, "self_energies_lowrank: null interaction block");
+    check_points(pts_vn, n_vn, n_r, "self_energies_lowrank: vn");
+    check_points(pts_nn, n_nn, n_r, "self_energies_lowrank: nn");
+    DBuf dpsi = upload(c, psi, (size_t)n_r * nb);
+    DBuf dwvn = upload(c, w_vn, (size_t)n_vn * n_vn), dvvn = upload(c, v_vn, (size_t)n_vn * n_vn);
+    DBuf dwnn = upload(c, w_nn, (size_t)n_nn * n_nn);
+    DBuf out = dalloc(c, (size_t)3 * nb);
+    sigma_impl(c, dpsi.d(), n_r, n_v, nb, pts_vn, n_vn, pts_nn, n_nn, dwvn.d(), dvvn.d(), dwnn.d(), out.d(),
+               out.d() + nb, out.d() + 2 * nb);
+    std::vector<double> h((size_t)3 * nb);
+    download(c, h.data(), out.p, sizeof(double) * 3 * nb);
+    for (int n = 0; n < nb; ++n) {
+      const double tot = h[n] + h[nb + n] + h[2 * nb + n];  // SelfEnergies::finalize order (gw.hpp:36)
+      if (sigma_sex_x) sigma_sex_x[n] = h[n];
+      if (sigma_x) sigma_x[n] = h[nb + n];
+      if (sigma_coh) sigma_coh[n] = h[2 * nb + n];
+      if (sigma_total) sigma_total[n] = tot;
+      if (!std::isfinite(tot))
+        fail(LRGW_ERR_NUMERIC, "self-energies: non-finite value at band " + std::to_string(n));
+    }
+  });
+}
+
+int lrgw_dev_self_energies(lrgw_ctx c, const double* psi, long long ldp, int n_r, int n_v, int n_c,
+                           const int32_t* pts_vn, int n_vn, const int32_t* pts_nn, int n_nn, const double* w_vn,
+                           const double* w_nn, const double* v_vn, double* sigma_sex_x, double* sigma_x,
+                           double* sigma_coh) {
+  return guarded(c, [&] {
+    const int nb = n_v + n_c;
+    if (n_r < 1 || n_v < 0 || n_c < 0 || nb < 1 || n_vn < 0 || n_nn < 0 || ldp < n_r)
+      fail(LRGW_ERR_INVALID_INPUT, "self_energies_lowrank: bad sizes");
+    check_points(pts_vn, n_vn, n_r, "self_energies_lowrank: vn");
+    check_points(pts_nn, n_nn, n_r, "self_energies_lowrank: nn");
+    sigma_impl(c, psi, ldp, n_v, nb, pts_vn, n_vn, pts_nn, n_nn, w_vn, v_vn, w_nn, sigma_sex_x, sigma_x,
+               sigma_coh);
     ck(cudaStreamSynchronize(c->stream), "sync");
   });
 }

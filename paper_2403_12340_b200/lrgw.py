@@ -521,6 +521,54 @@ def project_screened_interactions(e: EpsilonInverseLowRank, dec_vn, dec_nn, thre
     return ScreenedProjections(w_vn, w_nn, v_vn)
 
 
+@dataclass
+class SelfEnergies:
+    """gw.hpp:28-42 — per-band static-COHSEX components (hartree)."""
+    sigma_sex_x: np.ndarray
+    sigma_x: np.ndarray
+    sigma_coh: np.ndarray
+    sigma_total: np.ndarray
+    pipeline_tag: str = "lowrank"
+
+
+def self_energies_lowrank(psi, n_v: int, w_vn, w_nn, v_vn, dec_vn, dec_nn, ctx=None) -> SelfEnergies:
+    """gw.hpp:143-153 (detail::sigma_hadamard, gw.hpp:93-137) on the GPU.
+    psi: N_r x (n_v + n_c) orbitals; w_vn / w_nn / v_vn from
+    project_screened_interactions; dec_vn / dec_nn: IsdfDecomposition or
+    point-index arrays. Raises NumericError on a non-finite band
+    (SelfEnergies::finalize)."""
+    c = _ctx(ctx)
+    ps = _f(psi)
+    n_r, nb = ps.shape
+    if not 0 <= n_v <= nb:
+        raise InvalidInput("self_energies_lowrank: n_v out of range")
+    pv = np.ascontiguousarray(getattr(dec_vn, "point_indices", dec_vn), dtype=np.int32)
+    pn = np.ascontiguousarray(getattr(dec_nn, "point_indices", dec_nn), dtype=np.int32)
+    wv, wn, vv = _f(w_vn), _f(w_nn), _f(v_vn)
+    if wv.shape != (pv.size, pv.size) or vv.shape != wv.shape or wn.shape != (pn.size, pn.size):
+        raise InvalidInput("self_energies_lowrank: interaction block / point count mismatch")
+    out = [np.zeros(nb) for _ in range(4)]
+    _check(c._lib.lrgw_self_energies_lowrank(c.handle, _dp(ps), n_r, n_v, nb - n_v, _ip(pv), pv.size, _ip(pn),
+                                             pn.size, _dp(wv), _dp(wn), _dp(vv), *[_dp(o) for o in out]),
+           c.handle, "self_energies_lowrank")
+    return SelfEnergies(*out)
+
+
+@dataclass
+class QuasiparticleEnergies:
+    """gw.hpp:44-46."""
+    eps_gw: np.ndarray
+
+
+def quasiparticle_energies(energies, vxc, sig: SelfEnergies) -> QuasiparticleEnergies:
+    """gw.hpp:48-58: eps_gw = eps + sigma_total - vxc (host, O(N_b))."""
+    e = np.asarray(energies, dtype=np.float64)
+    v = np.asarray(vxc, dtype=np.float64)
+    if sig.sigma_total.shape != e.shape or v.shape != e.shape:
+        raise InvalidInput("quasiparticle_energies: length mismatch")
+    return QuasiparticleEnergies(e + sig.sigma_total - v)
+
+
 def epsilon_inverse_from_parts(p, k, dims, cell, ctx=None) -> EpsilonInverseLowRank:
     c = _ctx(ctx)
     d, cl = _grid(dims, cell)

@@ -141,6 +141,37 @@ int main() {
     Matrix t8 = coupled_coefficients_direct(rows_at(qa, p8), rows_at(qb, p8), {-1.0, -0.5, 0.5, 1.0}).t;
     CHECK(throws<numeric_error>([&] { assemble_K(t8, d8.p, build_coulomb(g4, CoulombMode::reciprocal_diagonal)); }));
   }
+  // GW consumers (test_gw.cpp:66-90, 174-233): vn / nn ISDF, projections, Sigma
+  {
+    ElectronicStructure es;
+    es.grid = grid;
+    es.psi = psi;
+    es.n_v = 16;
+    es.n_c = 16;
+    es.energies = e;
+    es.vxc.assign(32, 0.0);
+    IsdfDecomposition vn = build_isdf(es, PairSetLabel::vn, 4.0);
+    IsdfDecomposition nn = build_isdf(es, PairSetLabel::nn, 4.0);
+    CHECK(vn.n_mu == num_aux(4.0, 16, 32) && nn.n_mu == num_aux(4.0, 32, 32));
+    ScreenedProjections proj = project_screened_interactions(eps, vn, nn);
+    CHECK(symmetry_defect(proj.w_vn) == 0.0 && symmetry_defect(proj.v_vn) == 0.0);
+    SelfEnergies sig = self_energies_lowrank(es, proj.w_vn, proj.w_nn, proj.v_vn, vn, nn);
+    CHECK(sig.pipeline_tag == PipelineTag::lowrank);
+    for (int n = 0; n < 32; ++n) {
+      CHECK(sig.sigma_x[n] <= 1e-12);
+      CHECK(sig.sigma_total[n] == sig.sigma_sex_x[n] + sig.sigma_x[n] + sig.sigma_coh[n]);
+    }
+    EpsilonInverseLowRank e0 = build_epsilon_inverse(t_dir.t, dec.p, zero_coulomb(grid));
+    ScreenedProjections p0 = project_screened_interactions(e0, vn, nn);
+    CHECK(frobenius_norm(p0.w_vn) <= 1e-12 && frobenius_norm(p0.v_vn) <= 1e-12);
+    SelfEnergies s0 = self_energies_lowrank(es, p0.w_vn, p0.w_nn, p0.v_vn, vn, nn);
+    for (int n = 0; n < 32; ++n) CHECK(std::abs(s0.sigma_total[n]) <= 1e-14);
+    es.vxc.assign(32, 0.05);
+    QuasiparticleEnergies qp = quasiparticle_energies(es, sig);
+    for (int n = 0; n < 32; ++n) CHECK(qp.eps_gw[n] == es.energies[n] + sig.sigma_total[n] - 0.05);
+    es.vxc.assign(31, 0.0);
+    CHECK(throws<invalid_input>([&] { quasiparticle_energies(es, sig); }));
+  }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ok", failures);
   return failures ? 1 : 0;
 }

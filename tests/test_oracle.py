@@ -192,7 +192,8 @@ def test_restatement_error_behaviour(ref):
 
 # ---- golden fixtures (generated by tests/golden/make_golden.py from _ref) --
 
-@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "*.npz"))))
+@pytest.mark.parametrize("path", sorted(p for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                                          if not os.path.basename(p).startswith("gw_")))
 def test_oracle_against_golden(path):
     g = np.load(path)
     n_v, n_c = int(g["n_v"]), int(g["n_c"])
@@ -208,3 +209,55 @@ def test_oracle_against_golden(path):
         assert rel(R.coupled_coefficients_fixed(pv, pc, g["energies"], spec, int(g["n_lambda"])), g["t_fixed"]) <= 1e-12
     assert rel(R.assemble_K(g["t_direct"], g["theta"], dims, cell), g["k"]) <= 1e-10
     assert rel(R.epsilon_inverse_apply(g["theta"], g["k"], dims, cell, g["x"]), g["y"]) <= 1e-12
+
+
+# ---- GW self-energies (gw.hpp:48-153; fixtures from make_golden_gw.py) -----
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "gw_*.npz"))))
+def test_sigma_restatement_against_golden(path):
+    g = np.load(path)
+    n_v = int(g["n_v"])
+    dims, cell = tuple(g["dims"]), tuple(g["cell"])
+    psi = g["psi"]
+    for lab, (a, b) in {"vn": (psi[:, :n_v], psi), "nn": (psi, psi)}.items():
+        assert np.array_equal(R.select_points(a, b, len(g[f"pts_{lab}"])), g[f"pts_{lab}"]), lab
+        assert rel(R.fit_auxiliary_basis(a, b, g[f"pts_{lab}"]), g[f"theta_{lab}"]) <= 1e-10, lab
+    w = R.project_screened(g["theta_vc"], g["k"], dims, cell, g["theta_vn"], g["theta_nn"])
+    for got, name in zip(w, ("w_vn", "w_nn", "v_vn")):
+        assert rel(got, g[name]) <= 1e-10, name
+    sig = R.sigma_lowrank(psi, n_v, g["pts_vn"], g["pts_nn"], g["w_vn"], g["w_nn"], g["v_vn"])
+    for got, want, name in zip(sig, g["sig_lowrank"], ("sex_x", "x", "coh", "total")):
+        assert np.max(np.abs(got - want)) <= 1e-12 * max(np.max(np.abs(want)), 1e-30), name
+    # test_gw.cpp:116-127: low-rank == conventional ISDF per band (1e-9 of the scale)
+    scale = np.max(np.abs(g["sig_conventional"][3]))
+    assert np.max(np.abs(g["sig_lowrank"] - g["sig_conventional"])) <= 1e-9 * scale
+    # test_gw.cpp:174-184: sigma_x <= 0, exact additivity
+    assert np.all(sig[1] <= 1e-12)
+    assert np.array_equal(sig[3], sig[0] + sig[1] + sig[2])
+
+
+def test_sigma_restatement_against_reference_leaf(ref):
+    g = np.load(os.path.join(GOLDEN, "gw_s7.npz"))
+    n_v = int(g["n_v"])
+    rng = np.random.default_rng(4)
+    nv, nn = len(g["pts_vn"]), len(g["pts_nn"])
+    wv = R.symmetrize(rng.standard_normal((nv, nv)))
+    wn = R.symmetrize(rng.standard_normal((nn, nn)))
+    vv = R.symmetrize(rng.standard_normal((nv, nv)))
+    got = R.sigma_lowrank(g["psi"], n_v, g["pts_vn"], g["pts_nn"], wv, wn, vv)
+    want = ref.sigma_lowrank(g["psi"], n_v, g["pts_vn"], g["pts_nn"], wv, wn, vv)
+    for a, b in zip(got, want):
+        assert np.max(np.abs(a - b)) <= 1e-12 * np.max(np.abs(b))
+
+
+def test_quasiparticle_kats(ref):
+    # test_gw.cpp:186-233
+    e = np.array([-0.4, -0.2, 0.1, 0.3])
+    assert np.array_equal(R.quasiparticle_energies(e, np.zeros(4), np.zeros(4)), e)
+    got = R.quasiparticle_energies(e, np.full(4, 0.05), np.full(4, 0.25))
+    assert np.allclose(got, e + 0.25 - 0.05, rtol=1e-14)
+    assert np.array_equal(got, ref.quasiparticle(e, np.full(4, 0.05), np.full(4, 0.25)))
+    with pytest.raises(R.InvalidInput):
+        R.quasiparticle_energies(e, np.zeros(4), np.zeros(3))
+    with pytest.raises(R.InvalidInput):
+        ref.quasiparticle(e, np.zeros(4), np.zeros(3))
