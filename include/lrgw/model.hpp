@@ -1,8 +1,10 @@
 // model.hpp — drop-in electronic-structure container and Coulomb operator
-// (reference model.hpp:27-50, 151-223). apply_coulomb runs on the GPU (cuFFT
+// (reference model.hpp:27-50, 151-223) and the WFN1 file format
+// (model.hpp:236-339). apply_coulomb runs on the GPU (cuFFT
 // leaf + the fused v(G)/N_r scale kernel).
 #pragma once
 
+#include <string>
 #include <vector>
 
 #include "lrgw/grid.hpp"
@@ -67,6 +69,34 @@ inline Matrix apply_coulomb(const CoulombOperator& v, const Matrix& x, int threa
                                    y.data()),
                 c, "apply_coulomb");
   return y;
+}
+
+// WFN1 files (model.hpp:236-339): the same bytes and io_error messages as the
+// reference; I/O in liblrgw_cuda (csrc/wfn1.cpp).
+inline void save_system(const std::string& path, const ElectronicStructure& es) {
+  if (es.psi.rows() != es.grid.n_r() || es.psi.cols() != es.n_bands() ||
+      static_cast<int>(es.energies.size()) != es.n_bands() || static_cast<int>(es.vxc.size()) != es.n_bands())
+    throw invalid_input("save_system: array shapes do not match the header");
+  if (lrgw_wfn1_save(path.c_str(), es.grid.dims.data(), es.grid.cell.data(), es.n_v, es.n_c, es.psi.data(),
+                     es.energies.data(), es.vxc.data()) != LRGW_OK)
+    throw io_error(lrgw_last_error());
+}
+
+inline ElectronicStructure load_system(const std::string& path) {
+  std::array<int, 3> dims{};
+  std::array<double, 3> cell{};
+  int n_v = 0, n_c = 0;
+  if (lrgw_wfn1_info(path.c_str(), dims.data(), cell.data(), &n_v, &n_c) != LRGW_OK) throw io_error(lrgw_last_error());
+  ElectronicStructure es;
+  es.grid = Grid(dims, cell);
+  es.n_v = n_v;
+  es.n_c = n_c;
+  es.psi = Matrix(es.grid.n_r(), n_v + n_c);
+  es.energies.resize(n_v + n_c);
+  es.vxc.resize(n_v + n_c);
+  if (lrgw_wfn1_load(path.c_str(), es.psi.data(), es.energies.data(), es.vxc.data()) != LRGW_OK)
+    throw io_error(lrgw_last_error());
+  return es;
 }
 
 }  // namespace lrgw

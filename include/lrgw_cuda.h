@@ -203,6 +203,22 @@ int lrgw_dev_self_energies(lrgw_ctx ctx, const double* psi, long long ldp, int n
                            const double* w_vn, const double* w_nn, const double* v_vn,
                            double* sigma_sex_x, double* sigma_x, double* sigma_coh);
 
+/* WFN1 orbital files (reference model.hpp:236-339, save_system /
+ * load_system): "WFN1", uint32 LE header length, JSON header
+ * {cell, dims, nc, nr, nv}, f64 LE psi (column major), energies, vxc.
+ * Failures return LRGW_ERR_IO with the reference's io_error message in
+ * lrgw_last_error() (thread-local; the context-free calls' error text). */
+const char* lrgw_last_error(void);
+int lrgw_wfn1_info(const char* path, int* dims3, double* cell3, int* n_v, int* n_c);
+/* Host load: psi (n_r x (n_v + n_c)), energies, vxc (n_v + n_c); any may be null. */
+int lrgw_wfn1_load(const char* path, double* psi, double* energies, double* vxc);
+/* Device load: psi streamed straight into HBM (leading dim ld >= n_r) in
+ * column blocks through pinned double buffers; energies / vxc to the host. */
+int lrgw_wfn1_load_device(lrgw_ctx ctx, const char* path, double* psi, long long ld, double* energies,
+                          double* vxc);
+int lrgw_wfn1_save(const char* path, const int* dims3, const double* cell3, int n_v, int n_c,
+                   const double* psi, const double* energies, const double* vxc);
+
 /* Stage-level device entry points (multi-rank orchestration composes these). */
 int lrgw_dev_select(lrgw_ctx ctx, const double* a, long long lda, int n1, const double* b,
                     long long ldb, int n2, int n_r, int n_mu, int32_t* pts_host,

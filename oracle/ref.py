@@ -349,3 +349,32 @@ def quasiparticle(energies, vxc, sigma_total):
     out = np.zeros(e.size)
     _check(lib().ref_quasiparticle(_d(e), _d(v), _d(s), e.size, s.size, _d(out)), "quasiparticle_energies")
     return out
+
+
+def save_system(path, dims, cell, n_v, n_c, psi, energies, vxc):
+    """model.hpp:262-285 (the reference writer)."""
+    d = np.array(dims, dtype=np.int32)
+    c = np.array(cell, dtype=np.float64)
+    _check(lib().ref_save_system(str(path).encode(), _i(d), _d(c), n_v, n_c, _d(_f(psi)),
+                                 _d(np.ascontiguousarray(energies, dtype=np.float64)),
+                                 _d(np.ascontiguousarray(vxc, dtype=np.float64))), "save_system")
+
+
+def load_system(path):
+    """model.hpp:287-339 (the reference reader). Returns
+    (dims, cell, n_v, n_c, psi, energies, vxc); raises OracleError subclasses
+    carrying the reference's io_error text."""
+    L = lib()
+    L.ref_last_message.restype = ctypes.c_char_p
+    d = np.zeros(3, dtype=np.int32)
+    c = np.zeros(3)
+    nv, nc = ctypes.c_int(0), ctypes.c_int(0)
+    rc = L.ref_load_system(str(path).encode(), _i(d), _d(c), ctypes.byref(nv), ctypes.byref(nc), None, None, None)
+    if rc != 0:
+        _check(rc, L.ref_last_message().decode())
+    n_r, nb = int(np.prod(d)), nv.value + nc.value
+    psi = np.zeros((n_r, nb), order="F")
+    e, v = np.zeros(nb), np.zeros(nb)
+    _check(L.ref_load_system(str(path).encode(), _i(d), _d(c), ctypes.byref(nv), ctypes.byref(nc), _d(psi), _d(e),
+                             _d(v)), "load_system")
+    return tuple(int(x) for x in d), tuple(float(x) for x in c), nv.value, nc.value, psi, e, v

@@ -482,6 +482,47 @@ int ref_quasiparticle(const double* energies, const double* vxc, const double* s
   });
 }
 
+// model.hpp:236-339 — WFN1 writer / reader. The reader reports the
+// io_error text through ref_last_message().
+thread_local std::string g_msg;
+
+int ref_save_system(const char* path, const int* dims, const double* cell, int n_v, int n_c,
+                    const double* psi, const double* energies, const double* vxc) {
+  return guarded([&] {
+    ElectronicStructure es;
+    es.grid = make_grid(dims, cell);
+    es.n_v = n_v;
+    es.n_c = n_c;
+    es.psi = from_ptr(psi, es.grid.n_r(), n_v + n_c);
+    es.energies.assign(energies, energies + n_v + n_c);
+    es.vxc.assign(vxc, vxc + n_v + n_c);
+    save_system(path, es);
+  });
+}
+
+int ref_load_system(const char* path, int* dims, double* cell, int* n_v, int* n_c, double* psi,
+                    double* energies, double* vxc) {
+  g_msg.clear();
+  try {
+    ElectronicStructure es = load_system(path);
+    for (int k = 0; k < 3; ++k) {
+      dims[k] = es.grid.dims[k];
+      cell[k] = es.grid.cell[k];
+    }
+    *n_v = es.n_v;
+    *n_c = es.n_c;
+    if (psi) to_ptr(es.psi, psi);
+    if (energies) std::memcpy(energies, es.energies.data(), sizeof(double) * es.energies.size());
+    if (vxc) std::memcpy(vxc, es.vxc.data(), sizeof(double) * es.vxc.size());
+    return kOk;
+  } catch (const std::exception& e) {
+    g_msg = e.what();
+    return guarded([&] { throw; });
+  }
+}
+
+const char* ref_last_message() { return g_msg.c_str(); }
+
 // smw.hpp:97-103 with caller-supplied K (e.g. K = 0 identity check).
 int ref_eps_apply_given(const double* p, const double* k, int n_r, int n_mu,
                         const int* dims, const double* cell, const double* x,

@@ -144,6 +144,13 @@ _SIGS = {
                                               ctypes.c_int, c_int32_p, ctypes.c_int, c_int32_p, ctypes.c_int,
                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "lrgw_last_error": (ctypes.c_char_p, []),
+    "lrgw_wfn1_info": (ctypes.c_int, [ctypes.c_char_p, c_int_p, c_double_p, c_int_p, c_int_p]),
+    "lrgw_wfn1_load": (ctypes.c_int, [ctypes.c_char_p, c_double_p, c_double_p, c_double_p]),
+    "lrgw_wfn1_load_device": (ctypes.c_int, [ctx_t, ctypes.c_char_p, ctypes.c_void_p, c_ll, c_double_p,
+                                             c_double_p]),
+    "lrgw_wfn1_save": (ctypes.c_int, [ctypes.c_char_p, c_int_p, c_double_p, ctypes.c_int, ctypes.c_int,
+                                      c_double_p, c_double_p, c_double_p]),
     "lrgw_dev_dgemm": (ctypes.c_int, [ctx_t, ctypes.c_char, ctypes.c_char, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, ctypes.c_double, ctypes.c_void_p, c_ll, ctypes.c_void_p,
                                       c_ll, ctypes.c_double, ctypes.c_void_p, c_ll]),

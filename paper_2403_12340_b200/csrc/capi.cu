@@ -25,6 +25,7 @@
 #include "kernels.h"
 #include "lrgw_cuda.h"
 #include "select.h"
+#include "wfn1.h"
 
 namespace lrgw_dev {
 static std::atomic<long long> g_launches{0};
@@ -1765,6 +1766,131 @@ int lrgw_dev_self_energies(lrgw_ctx c, const double* psi, long long ldp, int n_r
     sigma_impl(c, psi, ldp, n_v, nb, pts_vn, n_vn, pts_nn, n_nn, w_vn, v_vn, w_nn, sigma_sex_x, sigma_x,
                sigma_coh);
     ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+}  // extern "C"
+
+// ---- WFN1 orbital files (model.hpp:236-339) -------------------------------
+namespace {
+thread_local std::string g_thread_err;
+
+template <class F>
+int io_guarded(F&& f) {
+  try {
+    g_thread_err.clear();
+    f();
+    return LRGW_OK;
+  } catch (const lrgw_host::Wfn1Error& e) {
+    g_thread_err = e.what();
+    return LRGW_ERR_IO;
+  } catch (const Fail& e) {
+    g_thread_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_thread_err = "host allocation failure";
+    return LRGW_ERR_INTERNAL;
+  } catch (...) {
+    g_thread_err = "internal error";
+    return LRGW_ERR_INTERNAL;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* lrgw_last_error(void) { return g_thread_err.c_str(); }
+
+int lrgw_wfn1_info(const char* path, int* dims, double* cell, int* n_v, int* n_c) {
+  return io_guarded([&] {
+    if (!path) fail(LRGW_ERR_INVALID_INPUT, "load_system: null path");
+    const lrgw_host::Wfn1Header h = lrgw_host::wfn1_read_header(path);
+    for (int k = 0; k < 3; ++k) {
+      if (dims) dims[k] = h.dims[k];
+      if (cell) cell[k] = h.cell[k];
+    }
+    if (n_v) *n_v = h.n_v;
+    if (n_c) *n_c = h.n_c;
+  });
+}
+
+int lrgw_wfn1_load(const char* path, double* psi, double* energies, double* vxc) {
+  return io_guarded([&] {
+    if (!path) fail(LRGW_ERR_INVALID_INPUT, "load_system: null path");
+    const lrgw_host::Wfn1Header h = lrgw_host::wfn1_read_header(path);
+    const size_t nb = static_cast<size_t>(h.n_v) + h.n_c, n_psi = static_cast<size_t>(h.n_r) * nb;
+    const long long off_e = h.payload_offset + static_cast<long long>(n_psi * sizeof(double));
+    if (psi) lrgw_host::wfn1_read_payload(path, h.payload_offset, psi, n_psi, "psi");
+    std::vector<double> tmp(nb);
+    lrgw_host::wfn1_read_payload(path, off_e, energies ? energies : tmp.data(), nb, "energies");
+    lrgw_host::wfn1_read_payload(path, off_e + static_cast<long long>(nb * sizeof(double)), vxc ? vxc : tmp.data(),
+                                 nb, "vxc");
+  });
+}
+
+int lrgw_wfn1_load_device(lrgw_ctx c, const char* path, double* psi, long long ld, double* energies, double* vxc) {
+  if (!c) return LRGW_ERR_INVALID_INPUT;
+  int st = io_guarded([&] {
+    use_device(c);
+    if (!path || !psi) fail(LRGW_ERR_INVALID_INPUT, "load_system: null argument");
+    const lrgw_host::Wfn1Header h = lrgw_host::wfn1_read_header(path);
+    const int nb = h.n_v + h.n_c;
+    const size_t n_r = static_cast<size_t>(h.n_r);
+    if (ld < h.n_r) fail(LRGW_ERR_INVALID_INPUT, "load_system: device leading dimension < N_r");
+    // psi streamed in whole-column blocks through two pinned staging buffers:
+    // block i is read from the file while block i - 1 is copied to HBM.
+    const size_t target = size_t(64) << 20;
+    const int cols_blk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(nb, target / (n_r * sizeof(double)))));
+    const size_t blk_elems = n_r * cols_blk;
+    double* pin[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    auto cleanup = [&] {
+      for (int i = 0; i < 2; ++i) {
+        if (done[i]) {
+          cudaEventSynchronize(done[i]);
+          cudaEventDestroy(done[i]);
+        }
+        if (pin[i]) cudaFreeHost(pin[i]);
+      }
+    };
+    try {
+      for (int i = 0; i < 2; ++i) {
+        ck(cudaMallocHost(&pin[i], blk_elems * sizeof(double)), "cudaMallocHost");
+        ck(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming), "cudaEventCreate");
+      }
+      int slot = 0;
+      for (int j0 = 0; j0 < nb; j0 += cols_blk, slot ^= 1) {
+        const int cols = std::min(cols_blk, nb - j0);
+        ck(cudaEventSynchronize(done[slot]), "cudaEventSynchronize");
+        lrgw_host::wfn1_read_payload(path, h.payload_offset + static_cast<long long>(n_r * j0 * sizeof(double)),
+                                     pin[slot], n_r * cols, "psi");
+        ck(cudaMemcpy2DAsync(psi + static_cast<size_t>(j0) * ld, ld * sizeof(double), pin[slot],
+                             n_r * sizeof(double), n_r * sizeof(double), cols, cudaMemcpyHostToDevice, c->stream),
+           "H2D psi");
+        ck(cudaEventRecord(done[slot], c->stream), "cudaEventRecord");
+      }
+      const long long off_e = h.payload_offset + static_cast<long long>(n_r * nb * sizeof(double));
+      std::vector<double> tmp(nb);
+      lrgw_host::wfn1_read_payload(path, off_e, energies ? energies : tmp.data(), nb, "energies");
+      lrgw_host::wfn1_read_payload(path, off_e + static_cast<long long>(nb * sizeof(double)),
+                                   vxc ? vxc : tmp.data(), nb, "vxc");
+      ck(cudaStreamSynchronize(c->stream), "sync");
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+  if (st != LRGW_OK) c->err = g_thread_err;
+  return st;
+}
+
+int lrgw_wfn1_save(const char* path, const int* dims, const double* cell, int n_v, int n_c, const double* psi,
+                   const double* energies, const double* vxc) {
+  return io_guarded([&] {
+    if (!path || !dims || !cell || (n_v + n_c > 0 && (!psi || !energies || !vxc)))
+      fail(LRGW_ERR_INVALID_INPUT, "save_system: null argument");
+    lrgw_host::wfn1_write(path, dims, cell, n_v, n_c, psi, energies, vxc);
   });
 }
 

@@ -569,6 +569,86 @@ def quasiparticle_energies(energies, vxc, sig: SelfEnergies) -> QuasiparticleEne
     return QuasiparticleEnergies(e + sig.sigma_total - v)
 
 
+# ---- WFN1 orbital files (model.hpp:236-339) --------------------------------
+
+@dataclass
+class ElectronicStructure:
+    """model.hpp:27-50 (host arrays; psi N_r x (n_v + n_c), column major)."""
+    dims: tuple
+    cell: tuple
+    psi: np.ndarray
+    energies: np.ndarray
+    vxc: np.ndarray
+    n_v: int
+    n_c: int
+
+    @property
+    def n_r(self) -> int:
+        return int(np.prod(self.dims))
+
+    @property
+    def n_bands(self) -> int:
+        return self.n_v + self.n_c
+
+
+def _io_check(rc, what):
+    if rc != 0:
+        msg = (L.load().lrgw_last_error() or b"").decode() or what
+        _raise(rc, None, msg)
+
+
+def save_system(path: str, es: ElectronicStructure) -> None:
+    """model.hpp:262-285 — byte-identical to the reference writer."""
+    lib = L.load()
+    d = np.ascontiguousarray(es.dims, dtype=np.int32)
+    cl = np.ascontiguousarray(es.cell, dtype=np.float64)
+    psi = _f(es.psi)
+    e = np.ascontiguousarray(es.energies, dtype=np.float64)
+    v = np.ascontiguousarray(es.vxc, dtype=np.float64)
+    nb = es.n_v + es.n_c
+    if psi.shape != (int(np.prod(d)), nb) or e.size != nb or v.size != nb:
+        raise InvalidInput("save_system: array shapes do not match the header")
+    _io_check(lib.lrgw_wfn1_save(str(path).encode(), d.ctypes.data_as(L.c_int_p), _dp(cl), es.n_v, es.n_c,
+                                 _dp(psi), _dp(e), _dp(v)), "save_system")
+
+
+def _wfn1_info(path):
+    lib = L.load()
+    d = np.zeros(3, dtype=np.int32)
+    cl = np.zeros(3)
+    nv, nc = ctypes.c_int(0), ctypes.c_int(0)
+    _io_check(lib.lrgw_wfn1_info(str(path).encode(), d.ctypes.data_as(L.c_int_p), _dp(cl), ctypes.byref(nv),
+                                 ctypes.byref(nc)), "load_system")
+    return tuple(int(x) for x in d), tuple(float(x) for x in cl), nv.value, nc.value
+
+
+def load_system(path: str) -> ElectronicStructure:
+    """model.hpp:287-339 — same validation and io_error messages."""
+    lib = L.load()
+    dims, cell, nv, nc = _wfn1_info(path)
+    n_r = int(np.prod(dims))
+    psi = np.zeros((n_r, nv + nc), order="F")
+    e, v = np.zeros(nv + nc), np.zeros(nv + nc)
+    _io_check(lib.lrgw_wfn1_load(str(path).encode(), _dp(psi), _dp(e), _dp(v)), "load_system")
+    return ElectronicStructure(dims, cell, psi, e, v, nv, nc)
+
+
+def load_system_device(path: str, ctx=None):
+    """WFN1 straight into HBM: psi streamed in column blocks through pinned
+    buffers (a column-major torch.cuda tensor), energies / vxc on the host.
+    Returns (dims, cell, psi_dev, energies, vxc, n_v, n_c)."""
+    import torch
+
+    c = _ctx(ctx)
+    dims, cell, nv, nc = _wfn1_info(path)
+    n_r = int(np.prod(dims))
+    psi = torch.empty((nv + nc, n_r), dtype=torch.float64, device=f"cuda:{c.device}").t()
+    e, v = np.zeros(nv + nc), np.zeros(nv + nc)
+    _check(c._lib.lrgw_wfn1_load_device(c.handle, str(path).encode(), psi.data_ptr(), n_r, _dp(e), _dp(v)),
+           c.handle, "")
+    return dims, cell, psi, e, v, nv, nc
+
+
 def epsilon_inverse_from_parts(p, k, dims, cell, ctx=None) -> EpsilonInverseLowRank:
     c = _ctx(ctx)
     d, cl = _grid(dims, cell)

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
+#include <string>
 
 #include "lrgw/lrgw.hpp"
 
@@ -171,6 +172,35 @@ int main() {
     for (int n = 0; n < 32; ++n) CHECK(qp.eps_gw[n] == es.energies[n] + sig.sigma_total[n] - 0.05);
     es.vxc.assign(31, 0.0);
     CHECK(throws<invalid_input>([&] { quasiparticle_energies(es, sig); }));
+  }
+  // WFN1 round trip and error messages (test_model.cpp:125-193)
+  {
+    ElectronicStructure es;
+    es.grid = grid;
+    es.psi = psi;
+    es.n_v = 16;
+    es.n_c = 16;
+    es.energies = e;
+    es.vxc.assign(32, 0.01);
+    const std::string path = "/tmp/lrgw_dropin_test.wfn1";
+    save_system(path, es);
+    ElectronicStructure back = load_system(path);
+    CHECK(back.grid == es.grid && back.n_v == 16 && back.n_c == 16);
+    CHECK(back.psi == es.psi && back.energies == es.energies && back.vxc == es.vxc);
+    {
+      std::FILE* f = std::fopen(path.c_str(), "r+b");
+      std::fputc('X', f);
+      std::fclose(f);
+    }
+    bool msg_ok = false;
+    try {
+      load_system(path);
+    } catch (const io_error& ex) {
+      msg_ok = std::string(ex.what()) == "load_system: bad magic";
+    }
+    CHECK(msg_ok);
+    CHECK(throws<io_error>([] { load_system("lrgw_test_does_not_exist.wfn1"); }));
+    std::remove(path.c_str());
   }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ok", failures);
   return failures ? 1 : 0;
