@@ -139,6 +139,18 @@ def max_over_ranks(x, world, device):
     return float(t.item())
 
 
+def cpu_config(cfg):
+    """The config the CPU reference is timed on and the factor to this one:
+    Si512 is timed on Si216 and extrapolated by the N^3 model (BASELINE.json
+    configs[4]); every other config is sampled directly."""
+    from paper_2403_12340_b200 import synth
+
+    if cfg.name == "si512":
+        small = synth.CONFIGS["si216"]
+        return small, (cfg.n_v / small.n_v) ** 3
+    return cfg, 1.0
+
+
 def run_ours(args, cfg, world, rank, local):
     import torch
 
@@ -149,6 +161,8 @@ def run_ours(args, cfg, world, rank, local):
     ctx = lrgw.Context(local)
     stream = torch.cuda.ExternalStream(lrgw.L.load().lrgw_ctx_stream(ctx.handle), device=dev)
     psi = synth.orbitals_device(cfg, seed=1, device=dev)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()  # the QR work area (Si512: ~14 GB) back to the device before the builds
     e = synth.energies(cfg)
     phi_v, phi_c = psi[:, :cfg.n_v], psi[:, cfg.n_v:]
     x_host = synth.probe_host(cfg.n_r)
@@ -195,7 +209,7 @@ def run_ours(args, cfg, world, rank, local):
     psi_h.copy_(psi.t())
     x_h = torch.from_numpy(np.ascontiguousarray(x_host.T)).pin_memory()
     y_h = torch.empty(8, cfg.n_r, dtype=torch.float64).pin_memory()
-    psi_d = torch.empty(psi.shape[1], psi.shape[0], dtype=torch.float64, device=dev)
+    psi_d = psi.t()  # the H2D lands in the orbitals' own storage (no second N_r x N_b copy in HBM)
     x_d = torch.empty(8, cfg.n_r, dtype=torch.float64, device=dev)
     y_d = torch.empty(8, cfg.n_r, dtype=torch.float64, device=dev)
 
@@ -246,7 +260,7 @@ def run_ours(args, cfg, world, rank, local):
                           "frac": round(ach / hbm, 4)}
     for k in ("fit_solve", "smw"):
         kernels[k] = {"ms": round(stages.get(k, 0.0), 4), "bound": "latency (N_mu^3 leaves)"}
-    kernels["select"]["note"] = "stage of ~18 launches per candidate block (13 blocks), not one kernel"
+    kernels["select"]["note"] = "stage of ~18 launches per candidate block (one block per <= 128 pivots), not one kernel"
     # roofline: the dominant single kernel (stages whose events bracket one
     # launch: the Theta^T V Theta SYRK, the fit GEMM, the K3 quadrature kernel)
     dom = max(("pvp", "fit_gemm", "quad_kernel"), key=lambda k: kernels.get(k, {}).get("ms", -1.0))
@@ -374,7 +388,8 @@ def main():
                             f"N_v = N_c = {cfg.n_v}, N_mu = {int(round(cfg.k_mu * (cfg.n_v * cfg.n_c) ** 0.5))}, "
                             f"N_lambda = {cfg.n_lambda}, eps^-1 X on an {cfg.n_r}x8 probe",
                 "stages": "1-5 (select, fit, quadrature, Coulomb/ThetaVTheta, SMW) + probe apply",
-                "l2": "inputs larger than L2 (Phi 226 MB, Theta 906 MB at si64); no flush",
+                "l2": f"inputs larger than L2 (Phi {cfg.n_r * (cfg.n_v + cfg.n_c) * 8 / 1e6:.0f} MB, Theta "
+                      f"{cfg.n_r * int(round(cfg.k_mu * (cfg.n_v * cfg.n_c) ** 0.5)) * 8 / 1e6:.0f} MB); no flush",
                 "parallelism": {"single": "1 GPU", "replicas": f"replicas x{world}",
                                 "sharded": f"sharded x{world} (grid-row panels, node split, NCCL)"}[mode]}
     metric = "low-rank eps^-1 build time (s), stages 1-5 + probe apply"
@@ -386,10 +401,14 @@ def main():
 
         cores = os.cpu_count() or 1
         vals = []
+        ccfg, scale = cpu_config(cfg)
         for i in range(args.warmup + args.steps):  # W untimed warm-up samples, then K timed
-            r = cpu_baseline.run(cfg, cores=cores, sel_steps=16, fit_rows=(1536, 2560), cols=64, seed=5 + i)
+            r = cpu_baseline.run(ccfg, cores=cores, sel_steps=16, fit_rows=(1536, 2560), cols=64, seed=5 + i)
             if i >= args.warmup:
-                vals.append(r["total_s"])
+                vals.append(r["total_s"] * scale)
+        if scale != 1.0:
+            r["sample"] += f"; x{scale:.2f} = (N_v {cfg.n_v} / {ccfg.n_v})^3 (N^3 model, BASELINE.json configs[4])"
+            r["stages"] = {k: v * scale for k, v in r["stages"].items()}
         v = statistics.median(vals)
         line = {"impl": "reference", "metric": metric, "value": v, "unit": "s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
@@ -423,11 +442,18 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import cpu_baseline
 
-        psi_h = np.asfortranarray(res["psi"].cpu().numpy())
-        r = cpu_baseline.run(cfg, psi=psi_h, energies=res["e"], cores=os.cpu_count())
-        cpu = {"value": r["total_s"], "unit": "s", "cores": r["cores"], "kind": "reference",
-               "sample": r["sample"], "stages_s": {k: round(v, 3) for k, v in r["stages"].items()},
-               "no_select_s": r["total_no_select_s"]}
+        ccfg, scale = cpu_config(cfg)
+        if ccfg is cfg:
+            psi_h = np.asfortranarray(res["psi"].cpu().numpy())
+            r = cpu_baseline.run(cfg, psi=psi_h, energies=res["e"], cores=os.cpu_count())
+        else:
+            r = cpu_baseline.run(ccfg, cores=os.cpu_count())
+        cpu = {"value": r["total_s"] * scale, "unit": "s", "cores": r["cores"], "kind": "reference",
+               "sample": r["sample"] + (f"; then x{scale:.2f} = (N_v {cfg.n_v} / {ccfg.n_v})^3, the N^3 model of "
+                                        f"BASELINE.json configs[4] (extrapolated, not run at {cfg.name})"
+                                        if scale != 1.0 else ""),
+               "stages_s": {k: round(v * scale, 3) for k, v in r["stages"].items()},
+               "no_select_s": r["total_no_select_s"] * scale}
     if rank == 0:
         line = {"metric": metric, "value": res["ms"] / 1e3, "unit": "s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": False,

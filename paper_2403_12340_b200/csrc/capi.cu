@@ -314,17 +314,30 @@ cufftHandle get_plan(lrgw_ctx c, const int* dims, int batch, long long rdist, lo
 long long half_len(const int* dims) { return (long long)(dims[0] / 2 + 1) * dims[1] * dims[2]; }
 
 // xhat (complex, half spectrum, column stride half_len) = D2Z(x)
+// Columns per cuFFT execution: bounds the plan's work area (a single plan
+// over all 8192 Theta columns of Si512 would ask cuFFT for a Theta-sized
+// work buffer next to the 58 GB Theta and its 59 GB spectrum).
+constexpr int kFftBatch = 1024;
+
 void fft_forward(lrgw_ctx c, const int* dims, const double* x, long long ldx, int m, double* xhat) {
-  if (m <= 0) return;
-  cufftHandle plan = get_plan(c, dims, m, ldx, half_len(dims), true);
-  ckf(cufftExecD2Z(plan, const_cast<double*>(x), reinterpret_cast<cufftDoubleComplex*>(xhat)),
-      "cufftExecD2Z");
+  const long long nh = half_len(dims);
+  for (int j0 = 0; j0 < m; j0 += kFftBatch) {
+    const int b = std::min(kFftBatch, m - j0);
+    cufftHandle plan = get_plan(c, dims, b, ldx, nh, true);
+    ckf(cufftExecD2Z(plan, const_cast<double*>(x) + (size_t)j0 * ldx,
+                     reinterpret_cast<cufftDoubleComplex*>(xhat + (size_t)j0 * 2 * nh)),
+        "cufftExecD2Z");
+  }
 }
 
 void fft_inverse(lrgw_ctx c, const int* dims, double* xhat, int m, double* y, long long ldy) {
-  if (m <= 0) return;
-  cufftHandle plan = get_plan(c, dims, m, ldy, half_len(dims), false);
-  ckf(cufftExecZ2D(plan, reinterpret_cast<cufftDoubleComplex*>(xhat), y), "cufftExecZ2D");
+  const long long nh = half_len(dims);
+  for (int j0 = 0; j0 < m; j0 += kFftBatch) {
+    const int b = std::min(kFftBatch, m - j0);
+    cufftHandle plan = get_plan(c, dims, b, ldy, nh, false);
+    ckf(cufftExecZ2D(plan, reinterpret_cast<cufftDoubleComplex*>(xhat + (size_t)j0 * 2 * nh), y + (size_t)j0 * ldy),
+        "cufftExecZ2D");
+  }
 }
 
 // y = V x = Re(F^-1 diag(v) F x) (model.hpp:208-223)

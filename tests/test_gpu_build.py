@@ -114,3 +114,51 @@ def test_si64_build_properties_and_pivots(L, ctx):
     x = _cm(torch.randn(cfg.n_r, 8, dtype=torch.float64, device="cuda",
                         generator=torch.Generator(device="cuda").manual_seed(7)))
     assert _eps_residual(L, ctx, ep, cfg, x) <= 1e-9
+
+
+def test_si512_build_on_one_gpu(L, ctx):
+    """The Si512 scaling workload (N_r 884 736, N_v = N_c = 1024, N_mu 8192,
+    Theta 58 GB) built on ONE B200: the oracle's first 64 greedy pivots
+    bit-exact (the greedy is prefix-consistent, so these are the build's
+    first 64 steps; oracle/select.c on the host), K and T symmetric negative
+    definite, and the matrix-free SMW residual ||eps eps^-1 x - x|| <= 1e-9."""
+    import ctypes
+
+    import torch
+
+    from oracle import restate as R
+    from paper_2403_12340_b200 import synth
+
+    cfg = synth.CONFIGS["si512"]
+    psi = synth.orbitals_device(cfg)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    e = synth.energies(cfg)
+    n = cfg.n_v
+    # first 64 pivots: device selection vs the oracle restatement
+    pts64 = np.zeros(64, dtype=np.int32)
+    lib = L.L.load()
+    margin = ctypes.c_double(0.0)
+    rc = lib.lrgw_dev_select(ctx.handle, ctypes.c_void_p(psi.data_ptr()), cfg.n_r, n,
+                             ctypes.c_void_p(psi[:, n:].data_ptr()), cfg.n_r, cfg.n_c, cfg.n_r, 64,
+                             pts64.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ctypes.byref(margin))
+    assert rc == 0
+    hpsi = psi.cpu().numpy()
+    assert np.array_equal(pts64, R.select_points(hpsi[:, :n], hpsi[:, n:], 64))
+    del hpsi
+    ep = L.build(psi[:, :n], psi[:, n:], e, cfg.dims, cfg.cell3, k_mu=cfg.k_mu, n_lambda=cfg.n_lambda, ctx=ctx)
+    assert ep.n_mu == 8192
+    pts = ep.point_indices
+    assert np.all(np.diff(pts) > 0) and set(pts64.tolist()) <= set(pts.tolist())
+    th_p, k_p, t_p = ep.device_ptrs()
+    k = L_tensor(k_p, (ep.n_mu, ep.n_mu))
+    t = L_tensor(t_p, (ep.n_mu, ep.n_mu))
+    assert float(torch.linalg.norm(k - k.T)) == 0.0
+    assert float(torch.linalg.eigvalsh(k).max()) < 0
+    assert float(torch.linalg.eigvalsh(t).max()) < 0
+    x = _cm(torch.randn(cfg.n_r, 8, dtype=torch.float64, device="cuda",
+                        generator=torch.Generator(device="cuda").manual_seed(7)))
+    assert _eps_residual(L, ctx, ep, cfg, x) <= 1e-9
+    ep.close()
+    del psi
+    torch.cuda.empty_cache()
