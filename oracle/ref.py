@@ -378,3 +378,14 @@ def load_system(path):
     _check(L.ref_load_system(str(path).encode(), _i(d), _d(c), ctypes.byref(nv), ctypes.byref(nc), _d(psi), _d(e),
                              _d(v)), "load_system")
     return tuple(int(x) for x in d), tuple(float(x) for x in c), nv.value, nc.value, psi, e, v
+
+
+def run_pipeline_json(config: dict) -> dict:
+    """driver.hpp:253-329: the reference's run command on a config dict."""
+    import json
+
+    cap = 1 << 24
+    buf = ctypes.create_string_buffer(cap)
+    n = ctypes.c_int(0)
+    _check(lib().ref_run_pipeline_json(json.dumps(config).encode(), buf, cap, ctypes.byref(n)), "run_pipeline")
+    return json.loads(buf.raw[:n.value].decode())

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "lrgw/contour.hpp"
+#include "lrgw/driver.hpp"
 #include "lrgw/elliptic.hpp"
 #include "lrgw/gw.hpp"
 #include "lrgw/isdf.hpp"
@@ -522,6 +523,17 @@ int ref_load_system(const char* path, int* dims, double* cell, int* n_v, int* n_
 }
 
 const char* ref_last_message() { return g_msg.c_str(); }
+
+// driver.hpp:253-329 — run_pipeline on a JSON config, result as
+// run_result_to_json(...).dump() (truncated to cap bytes; returns the length).
+int ref_run_pipeline_json(const char* config_json, char* out, int cap, int* out_len) {
+  return guarded([&] {
+    RunConfig c = parse_config(json::parse(config_json));
+    std::string d = run_result_to_json(run_pipeline(c), c).dump();
+    *out_len = static_cast<int>(d.size());
+    std::memcpy(out, d.data(), std::min<std::size_t>(d.size(), static_cast<std::size_t>(cap)));
+  });
+}
 
 // smw.hpp:97-103 with caller-supplied K (e.g. K = 0 identity check).
 int ref_eps_apply_given(const double* p, const double* k, int n_r, int n_mu,
