@@ -16,6 +16,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
 #include <unordered_map>
 #include <string>
 #include <tuple>
@@ -87,6 +88,10 @@ struct lrgw_ctx_s {
   std::multimap<size_t, void*> mem_free;
   std::unordered_map<void*, size_t> mem_live;
   size_t mem_cached = 0;
+  // Factored-inverse handles created on this context: destroying the context
+  // frees their device buffers and orphans them (lrgw_eps_destroy then only
+  // deletes the handle), so handles may outlive their context safely.
+  std::set<struct lrgw_eps_s*> live_eps;
 };
 
 struct lrgw_eps_s {
@@ -209,6 +214,14 @@ void download(lrgw_ctx c, void* h, const void* d, size_t bytes) {
 }
 
 void use_device(lrgw_ctx c) { ck(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+lrgw_eps_s* new_eps(lrgw_ctx c) {
+  auto* e = new lrgw_eps_s;
+  e->ctx = c;
+  std::lock_guard<std::mutex> lk(c->mem_mu);
+  c->live_eps.insert(e);
+  return e;
+}
 
 // Stage boundary i of the build (no-op outside lrgw_build).
 // Stage boundary of lrgw_build: CUDA event for the stage timings plus an NVTX
@@ -1001,6 +1014,18 @@ int lrgw_ctx_destroy(lrgw_ctx c) {
   cudaStreamSynchronize(c->stream);
   {
     std::lock_guard<std::mutex> lk(c->mem_mu);
+    for (lrgw_eps_s* e : c->live_eps) {  // orphan the handles, free their buffers
+      for (double* p : {e->theta, e->k, e->t}) {
+        auto it = c->mem_live.find(p);
+        if (it != c->mem_live.end()) {
+          cudaFree(p);
+          c->mem_live.erase(it);
+        }
+      }
+      e->theta = e->k = e->t = nullptr;
+      e->ctx = nullptr;
+    }
+    c->live_eps.clear();
     release_cached(c);
   }
   for (auto& kv : c->plans) cufftDestroy(kv.second);
@@ -1258,7 +1283,7 @@ int lrgw_eps_from_parts(lrgw_ctx c, const double* p, const double* k, int n_r, i
   return guarded(c, [&] {
     check_grid(dims, cell);
     if ((long long)dims[0] * dims[1] * dims[2] != n_r) fail(LRGW_ERR_INVALID_INPUT, "eps: grid / N_r mismatch");
-    auto* e = new lrgw_eps_s;
+    auto* e = new_eps(c);
     e->ctx = c;
     e->n_r = n_r;
     e->n_mu = n_mu;
@@ -1284,7 +1309,7 @@ int lrgw_build_epsilon_inverse(lrgw_ctx c, const double* t, const double* p, int
     pvp_impl(c, dims, cell, zero, dp.d(), n_r, n_mu, pvp.d());
     smw_core(c, dt.d(), pvp.d(), n_mu, dk.d());
     ck(cudaStreamSynchronize(c->stream), "sync");
-    auto* e = new lrgw_eps_s;
+    auto* e = new_eps(c);
     e->ctx = c;
     e->n_r = n_r;
     e->n_mu = n_mu;
@@ -1325,7 +1350,7 @@ static void eps_apply_impl(lrgw_ctx c, lrgw_eps e, const double* x, long long ld
 
 int lrgw_epsilon_inverse_apply(lrgw_ctx c, lrgw_eps e, const double* x, int m, double* y) {
   return guarded(c, [&] {
-    if (!e) fail(LRGW_ERR_INVALID_INPUT, "epsilon_inverse_apply: null handle");
+    if (!e || !e->ctx) fail(LRGW_ERR_INVALID_INPUT, "epsilon_inverse_apply: null handle");
     const size_t n = (size_t)e->n_r * m;
     DBuf dx = upload(c, x, n), dy = dalloc(c, n);
     eps_apply_impl(c, e, dx.d(), e->n_r, m, dy.d(), e->n_r);
@@ -1335,7 +1360,7 @@ int lrgw_epsilon_inverse_apply(lrgw_ctx c, lrgw_eps e, const double* x, int m, d
 
 int lrgw_eps_apply_dev(lrgw_ctx c, lrgw_eps e, const double* x, long long ldx, int m, double* y, long long ldy) {
   return guarded(c, [&] {
-    if (!e) fail(LRGW_ERR_INVALID_INPUT, "epsilon_inverse_apply: null handle");
+    if (!e || !e->ctx) fail(LRGW_ERR_INVALID_INPUT, "epsilon_inverse_apply: null handle");
     if (ldx < e->n_r || ldy < e->n_r) fail(LRGW_ERR_INVALID_INPUT, "epsilon_inverse_apply: row mismatch");
     eps_apply_impl(c, e, x, ldx, m, y, ldy);
     ck(cudaStreamSynchronize(c->stream), "sync");
@@ -1344,7 +1369,7 @@ int lrgw_eps_apply_dev(lrgw_ctx c, lrgw_eps e, const double* x, long long ldx, i
 
 int lrgw_eps_get(lrgw_ctx c, lrgw_eps e, double* k, double* p, double* vp, double* t, int32_t* pts) {
   return guarded(c, [&] {
-    if (!e) fail(LRGW_ERR_INVALID_INPUT, "eps: null handle");
+    if (!e || !e->ctx) fail(LRGW_ERR_INVALID_INPUT, "eps: null handle");
     const size_t nn = (size_t)e->n_mu * e->n_mu, np = (size_t)e->n_r * e->n_mu;
     if (k) download(c, k, e->k, nn * sizeof(double));
     if (p) download(c, p, e->theta, np * sizeof(double));
@@ -1367,11 +1392,15 @@ int lrgw_eps_shape(lrgw_eps e, int* n_r, int* n_mu) {
 
 int lrgw_eps_destroy(lrgw_eps e) {
   if (!e) return LRGW_OK;
-  cudaSetDevice(e->ctx->device);
-  cudaStreamSynchronize(e->ctx->stream);
-  ctx_free(e->ctx, e->theta);
-  ctx_free(e->ctx, e->k);
-  ctx_free(e->ctx, e->t);
+  if (lrgw_ctx c = e->ctx) {  // null once the context is gone (buffers already freed)
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    ctx_free(c, e->theta);
+    ctx_free(c, e->k);
+    ctx_free(c, e->t);
+    std::lock_guard<std::mutex> lk(c->mem_mu);
+    c->live_eps.erase(e);
+  }
   delete e;
   return LRGW_OK;
 }
@@ -1480,7 +1509,7 @@ int lrgw_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, lo
     if (c->quad_timed && cudaEventElapsedTime(&ms, c->ev_quad[0], c->ev_quad[1]) == cudaSuccess)
       c->stage_ms[LRGW_STAGE_QUAD_KERNEL] = ms;
     c->quad_timed = false;
-    auto* e = new lrgw_eps_s;
+    auto* e = new_eps(c);
     e->ctx = c;
     e->n_r = n_r;
     e->n_mu = n_mu;
@@ -1709,7 +1738,7 @@ int lrgw_dev_gram_weighted(lrgw_ctx c, const double* x, long long ldx, int kdim,
 int lrgw_project_screened_interactions(lrgw_ctx c, lrgw_eps e, const double* p_vn, int n_vn, const double* p_nn,
                                        int n_nn, double* w_vn, double* w_nn, double* v_vn) {
   return guarded(c, [&] {
-    if (!e) fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: null handle");
+    if (!e || !e->ctx) fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: null handle");
     if (n_vn < 0 || n_nn < 0 || (n_vn > 0 && !p_vn) || (n_nn > 0 && !p_nn))
       fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: bad sizes");
     const size_t n_r = e->n_r;
@@ -1726,7 +1755,7 @@ int lrgw_dev_project_screened(lrgw_ctx c, lrgw_eps e, const double* p_vn, long l
                               const double* p_nn, long long ld_nn, int n_nn, double* w_vn, double* w_nn,
                               double* v_vn) {
   return guarded(c, [&] {
-    if (!e) fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: null handle");
+    if (!e || !e->ctx) fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: null handle");
     if (n_vn < 0 || n_nn < 0 || (n_vn > 0 && ld_vn < e->n_r) || (n_nn > 0 && ld_nn < e->n_r))
       fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: bad sizes");
     project_impl(c, e, p_vn, ld_vn, n_vn, p_nn, ld_nn, n_nn, w_vn, w_nn, v_vn);

@@ -162,3 +162,19 @@ def test_si512_build_on_one_gpu(L, ctx):
     ep.close()
     del psi
     torch.cuda.empty_cache()
+
+
+def test_handles_survive_their_context(L):
+    """A factored-inverse handle destroyed after its context (garbage
+    collection order) is orphaned, not a use-after-free."""
+    rng = np.random.default_rng(0)
+    p = np.linalg.qr(rng.standard_normal((64, 6)))[0]
+    c2 = L.Context(0)
+    eps = L.build_epsilon_inverse(-np.eye(6) * 1e-3, p, (4, 4, 4), (6.0, 6.0, 6.0), ctx=c2)
+    c2.close()
+    eps.close()
+    c3 = L.Context(0)
+    eps = L.build_epsilon_inverse(-np.eye(6) * 1e-3, p, (4, 4, 4), (6.0, 6.0, 6.0), ctx=c3)
+    c3.close()
+    with pytest.raises(L.InvalidInput):
+        L.epsilon_inverse_apply(eps, np.zeros((64, 1)))

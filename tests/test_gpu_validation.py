@@ -13,8 +13,7 @@ def test_validation_suite_passes(ref, ctx, tmp_path):
     from paper_2403_12340_b200 import driver
     from validation import run_validation
 
-    cfg = driver.parse_config({"system": {"dims": [8, 8, 4], "nv": 8, "nc": 8, "seed": 7},
-                               "isdf": {"k_vc": 6.0, "k_vn": 6.0, "k_nn": 6.0}})
+    cfg = driver.parse_config({})  # the reference's default system: 8^3 grid, 16 + 16 bands, k = 8
     res = run_validation(cfg, ctx)
     failed = [c for c in res["checks"] if not c["pass"]]
     assert res["pass"], failed
@@ -29,9 +28,7 @@ def test_validation_catches_the_sign_mutation(ref, ctx):
     from paper_2403_12340_b200 import driver
     from validation import run_validation
 
-    cfg = driver.parse_config({"system": {"dims": [8, 8, 4], "nv": 8, "nc": 8, "seed": 7},
-                               "isdf": {"k_vc": 6.0, "k_vn": 6.0, "k_nn": 6.0},
-                               "_test_hooks": {"flip_sex_x_sign": True}})
+    cfg = driver.parse_config({"_test_hooks": {"flip_sex_x_sign": True}})
     res = run_validation(cfg, ctx)
     by = {c["name"]: c for c in res["checks"]}
     assert not res["pass"] and not by["gw.pipeline_equivalence"]["pass"]
