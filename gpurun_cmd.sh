@@ -1,13 +1,4 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 300 python tools/dist_time.py --config si64 > gpurun_out/dist_time_si64.log 2>&1
-timeout 300 python -c "
-import cProfile, pstats, sys, os
-sys.argv=['dist_time.py','--config','si64','--reps','2']
-sys.path.insert(0,'tools')
-import dist_time
-cProfile.run('dist_time.main()', 'gpurun_out/dist.prof')
-p=pstats.Stats('gpurun_out/dist.prof'); p.sort_stats('tottime').print_stats(35)
-" > gpurun_out/dist_profile.log 2>&1
-tail -4 gpurun_out/gpu_tests.log; tail -2 gpurun_out/smoke.log; tail -20 gpurun_out/dist_time_si64.log
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_build.py tests/test_gpu_topk.py tests/test_gpu_dist.py -x -q -k "not si512" > gpurun_out/sel_tests.log 2>&1; echo "rc=$?" >> gpurun_out/sel_tests.log
+timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1
+tail -3 gpurun_out/sel_tests.log; grep -o '"value": [0-9.]*\|"stages_ms": {[^}]*}' gpurun_out/bench.log | head -3

@@ -376,18 +376,14 @@ __device__ __forceinline__ void cand_argmax(const double (&dj)[4], const int (&p
 //   takes X_Ik = -X_II sum_{m=k}^{I-1} L_Im X_mk (k < I) — all threads.
 __device__ void cand_tri_inverse(double* lcs, double* lsel, const int* sel, int b, int s, double* xcol) {
   __shared__ double rdiag[CG_MAX];
-  double* X = lcs;
-  auto L = [&](int i, int m) -> double {  // L_sel (identity beyond b)
-    if (i >= b || m >= b) return i == m ? 1.0 : 0.0;
-    return m <= i ? lsel[i * (i + 1) / 2 + m] : 0.0;
-  };
+  double* X = lcs;  // L_sel (packed lower in lsel) is the identity beyond b
   for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
     const int i = idx / b, m = idx % b;
     if (m <= i) lsel[i * (i + 1) / 2 + m] = lcs[m * CG_MAX + sel[i]];
   }
   __syncthreads();
   for (int i = threadIdx.x; i < CG_MAX; i += blockDim.x) {
-    const double d = L(i, i);
+    const double d = i < b ? lsel[i * (i + 1) / 2 + i] : 1.0;
     rdiag[i] = d != 0.0 ? 1.0 / d : 0.0;
   }
   for (int idx = threadIdx.x; idx < CG_MAX * CG_MAX; idx += blockDim.x) X[idx] = 0.0;
@@ -401,9 +397,13 @@ __device__ void cand_tri_inverse(double* lcs, double* lsel, const int* sel, int 
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       double acc = (i == lane) ? 1.0 : 0.0;
+      const int row = o + i;
+      if (row < b) {  // rows >= b are identity rows (warp-uniform branch)
+        const double* lr = lsel + row * (row + 1) / 2 + o;  // L_sel[row][o + m], m < i <= row - o
 #pragma unroll
-      for (int m = 0; m < i; ++m) acc = fma(-L(o + i, o + m), x[m], acc);
-      x[i] = (i >= lane) ? acc * rdiag[o + i] : 0.0;
+        for (int m = 0; m < i; ++m) acc = fma(-lr[m], x[m], acc);
+      }
+      x[i] = (i >= lane) ? acc * rdiag[row] : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < 32; ++i) X[(o + i) * CG_MAX + o + lane] = x[i];
@@ -414,8 +414,13 @@ __device__ void cand_tri_inverse(double* lcs, double* lsel, const int* sel, int 
     // P_k = sum_{m=32k}^{32I-1} L[32I + i][m] X[m][32k + j], k < I
     for (int idx = threadIdx.x; idx < I * 1024; idx += blockDim.x) {
       const int k = idx / 1024, i = (idx / 32) % 32, j = idx % 32;
+      const int row = 32 * I + i, col = 32 * k + j;
       double acc = 0.0;
-      for (int m = 32 * k + j; m < 32 * I; ++m) acc = fma(L(32 * I + i, m), X[m * CG_MAX + 32 * k + j], acc);
+      if (row < b) {  // beyond b, L_sel rows are identity rows: zero left of the diagonal
+        // X is lower triangular: X[m][col] = 0 for m < col; m < 32 I <= row < b
+        const double* lr = lsel + row * (row + 1) / 2;
+        for (int m = col; m < 32 * I; ++m) acc = fma(lr[m], X[m * CG_MAX + col], acc);
+      }
       P[idx] = acc;
     }
     __syncthreads();
@@ -465,7 +470,8 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
   for (int idx = threadIdx.x; idx < s * s; idx += blockDim.x) p.xcol[idx] = 0.0;
 
   const double tau = p.top[s].row >= 0 ? p.top[s].v : -DBL_MAX;
-  const int tmax = min(s, p.steps - p.kb);
+  __shared__ int tmax_s;  // read from smem on the controller's path (keeps it out of the register budget)
+  if (threadIdx.x == 0) tmax_s = min(s, p.steps - p.kb);
   const bool want_sv = p.margin != nullptr;
 
   // controller state (warp 0), entries j = lane + 32 c
@@ -491,7 +497,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
     int i0;
     cand_argmax(dj, pj, usedl, lane, want_sv, v0, ppos, i0, sv);
     // the first step of a block is the exact argmax (C is sorted by the pivot rule)
-    if (lane == 0) piv[0] = CandPivot{v0, v0 > 0.0 ? 1.0 / v0 : 0.0, i0, (0 < tmax && i0 >= 0) ? 1 : 0};
+    if (lane == 0) piv[0] = CandPivot{v0, v0 > 0.0 ? 1.0 / v0 : 0.0, i0, (0 < min(s, p.steps - p.kb) && i0 >= 0) ? 1 : 0};
   }
 
   const int base = CG_ROWS * wid;
@@ -544,7 +550,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
       cand_argmax(dj, pj, usedl, lane, want_sv, v1, ppos, i1, sv);
       if (lane == 0)
         piv[(t + 1) & 1] = CandPivot{v1, v1 > 0.0 ? 1.0 / v1 : 0.0, i1,
-                                     (t + 1 < tmax && i1 >= 0 && v1 > tau) ? 1 : 0};
+                                     (t + 1 < tmax_s && i1 >= 0 && v1 > tau) ? 1 : 0};
       if (lane == 0) {
         const int gp = rjs[i0];  // pivot grid row
         p.perm[k] = gp;
