@@ -242,6 +242,16 @@ using H2W64 = Gemm2Cfg<128, 64, 32, 32, 4, V, true>;
 template <int V>
 using H2W32 = Gemm2Cfg<128, 32, 32, 32, 4, V, true>;
 
+// Tall Hadamard (selection: W columns of the accepted pivots, N = 48..128):
+// 64 x 16Q CTAs of 4 warps (16 x 16Q each), 2 per SM.
+template <int Q>
+using H2T = Gemm2Cfg<64, 16 * Q, 16, 16 * Q, 3, 2, true, 16, (Q <= 4 ? 3 : 2), false, true>;
+
+bool had_tall_v2_enabled() {
+  static const bool on = !(getenv("LRGW_HAD_TALL") && atoi(getenv("LRGW_HAD_TALL")) == 0);
+  return on;
+}
+
 template <class Cfg>
 cudaError_t launch2(cudaStream_t st, const Dgemm2Params& p) {
   dim3 grid((p.N + Cfg::BN - 1) / Cfg::BN, (p.M + Cfg::BM - 1) / Cfg::BM);
@@ -497,6 +507,23 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
     kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(p); count_launches(1);
     return cudaGetLastError();
   };
+  if (N < 128 && vec && N > 32 && tall_family_enabled() && had_tall_v2_enabled() &&
+      (long long)((M + 63) / 64) >= 2LL * 148) {
+    // paired-fragment engine, one column tile of width 16 Q, 4 warps of 16 x 16 Q; the first
+    // product parks in shared memory (one register accumulator set)
+    Dgemm2Params q{};
+    q.M = M, q.N = N, q.K = k1, q.K2 = k2;
+    q.A = a1, q.lda = lda1, q.B = b1, q.ldb = ldb1, q.A2 = a2, q.lda2 = lda2, q.B2 = b2, q.ldb2 = ldb2;
+    q.C = C, q.ldc = ldc, q.alpha = alpha, q.beta = beta;
+    switch ((N + 15) / 16) {
+      case 3: return launch2<H2T<3>>(st, q);
+      case 4: return launch2<H2T<4>>(st, q);
+      case 5: return launch2<H2T<5>>(st, q);
+      case 6: return launch2<H2T<6>>(st, q);
+      case 7: return launch2<H2T<7>>(st, q);
+      default: return launch2<H2T<8>>(st, q);
+    }
+  }
   if (N < 128 && vec && N > 32 && tall_family_enabled() && (long long)((M + 127) / 128) >= 2LL * 148) {
     switch ((N + 15) / 16) {
       case 3: return go(CfgHT<3>{});

@@ -39,18 +39,23 @@ struct Dgemm2Params {
 };
 
 template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int VEC_, bool HAD_, int BK_ = 16, int MINB_ = 1,
-          bool SKIP_ = false>
+          bool SKIP_ = false, bool PARK_ = false>
 struct Gemm2Cfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_, VEC = VEC_;
   static constexpr int MINB = MINB_;  // resident CTAs per SM the register budget is sized for
   static constexpr bool SKIP = SKIP_;  // warps wholly past a device-bounded N skip their MMAs
   static constexpr bool HAD = HAD_;
+  // PARK: the first Hadamard product waits in shared memory (thread-private
+  // slots) instead of a second register accumulator set — wide warp tiles
+  // without spills.
+  static constexpr bool PARK = HAD_ && PARK_;
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
   static constexpr int FM = WM / 8, FN = WN / 8;
   static constexpr int PA = BM + 4, PB = BN + 4;  // doubles; == 4 (mod 16): conflict-free LDS.128
   static constexpr int STAGE_ELEMS = BK * (PA + PB);
-  static constexpr int SMEM_BYTES = STAGES * STAGE_ELEMS * 8;
+  static constexpr int PARK_ELEMS = PARK ? FM * FN * 2 * THREADS : 0;
+  static constexpr int SMEM_BYTES = (STAGES * STAGE_ELEMS + PARK_ELEMS) * 8;
   static_assert(WM % 16 == 0 && WN % 16 == 0, "paired fragments need 16-row groups");
 };
 
@@ -95,7 +100,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) dgemm2_kernel(Dgemm2P
   const bool live = !Cfg::SKIP || n0 + wn < N;
 
   double acc[FM][FN][2];
-  double first[Cfg::HAD ? FM : 1][Cfg::HAD ? FN : 1][2];
+  constexpr bool REG1 = Cfg::HAD && !Cfg::PARK;  // first product in registers
+  double first[REG1 ? FM : 1][REG1 ? FN : 1][2];
+  double* park = smem + STAGES * Cfg::STAGE_ELEMS + tid;  // slot q of this thread: park[q * THREADS]
 #pragma unroll
   for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -148,8 +155,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) dgemm2_kernel(Dgemm2P
       for (int i = 0; i < FM; ++i)
 #pragma unroll
         for (int j = 0; j < FN; ++j) {
-          first[Cfg::HAD ? i : 0][Cfg::HAD ? j : 0][0] = acc[i][j][0];
-          first[Cfg::HAD ? i : 0][Cfg::HAD ? j : 0][1] = acc[i][j][1];
+          if (Cfg::PARK) {
+            park[((i * FN + j) * 2 + 0) * Cfg::THREADS] = acc[i][j][0];
+            park[((i * FN + j) * 2 + 1) * Cfg::THREADS] = acc[i][j][1];
+          } else {
+            first[REG1 ? i : 0][REG1 ? j : 0][0] = acc[i][j][0];
+            first[REG1 ? i : 0][REG1 ? j : 0][1] = acc[i][j][1];
+          }
           acc[i][j][0] = acc[i][j][1] = 0.0;
         }
     }
@@ -168,9 +180,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) dgemm2_kernel(Dgemm2P
         const int n = n0 + wn + 16 * (jn / 2) + 4 * t + 2 * h + (jn % 2);
         if (n >= N) continue;
         double v0 = acc[2 * j][jn][h], v1 = acc[2 * j + 1][jn][h];
-        if (Cfg::HAD) {
-          v0 *= first[Cfg::HAD ? 2 * j : 0][Cfg::HAD ? jn : 0][h];
-          v1 *= first[Cfg::HAD ? 2 * j + 1 : 0][Cfg::HAD ? jn : 0][h];
+        if (Cfg::PARK) {
+          v0 *= park[(((2 * j) * FN + jn) * 2 + h) * Cfg::THREADS];
+          v1 *= park[(((2 * j + 1) * FN + jn) * 2 + h) * Cfg::THREADS];
+        } else if (Cfg::HAD) {
+          v0 *= first[REG1 ? 2 * j : 0][REG1 ? jn : 0][h];
+          v1 *= first[REG1 ? 2 * j + 1 : 0][REG1 ? jn : 0][h];
         }
         v0 *= p.alpha;
         v1 *= p.alpha;
