@@ -773,6 +773,66 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
   return pts;
 }
 
+// The reference's seeded stream (rng.hpp:13-48: PCG32 oneseq, Box-Muller with
+// the cached second variate) for the sketch of qrcp_sketched.
+struct Pcg32 {
+  uint64_t s = 0;
+  bool have = false;
+  double spare = 0.0;
+  explicit Pcg32(uint64_t seed) {
+    next();
+    s += 0x853c49e6748fea9bULL ^ seed;
+    next();
+  }
+  uint32_t next() {
+    const uint64_t old = s;
+    s = old * 6364136223846793005ULL + 1442695040888963407ULL;
+    const uint32_t x = static_cast<uint32_t>(((old >> 18u) ^ old) >> 27u);
+    const uint32_t rot = static_cast<uint32_t>(old >> 59u);
+    return (x >> rot) | (x << ((32u - rot) & 31u));
+  }
+  double uniform() { return (static_cast<double>(next()) + 1.0) / 4294967296.0; }
+  double gaussian() {
+    if (have) {
+      have = false;
+      return spare;
+    }
+    const double u1 = uniform(), u2 = uniform();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double a = 6.283185307179586476925286766559 * u2;
+    spare = r * std::sin(a);
+    have = true;
+    return r * std::cos(a);
+  }
+};
+
+// PointSelector::qrcp_sketched (isdf.hpp:95-112): the pair rows compressed by
+// the reference's fixed Gaussian sketch G (2 N_mu x N1 N2, Rng(0x15df)) when
+// 2 N_mu < N1 N2, then greedy QRCP on the sketch's columns. The sketch is
+// formed on the device as F = M G^T (M the N_r x N1 N2 pair matrix, one DMMA
+// GEMM; the reference's guard on materialising M applies), and the QRCP
+// pivots of Z_s = F^T are the greedy pivoted-Cholesky pivots of F F^T —
+// select_impl with a = F and b = 1 ((F F^T) o (1 1^T) = F F^T).
+std::vector<int32_t> select_sketched(lrgw_ctx c, const double* a, long long lda, int n1, const double* b,
+                                     long long ldb, int n2, int n_r, int n_mu) {
+  const long long m = (long long)n1 * n2;
+  if ((long long)n_r * m > (1LL << 26))
+    fail(LRGW_ERR_GUARD_EXCEEDED, "pair_matrix_transposed: materialization guard exceeded");
+  if (2LL * n_mu >= m) return select_impl(c, a, lda, n1, b, ldb, n2, n_r, n_mu, nullptr);
+  const int ns = 2 * n_mu;
+  std::vector<double> g((size_t)ns * m);
+  Pcg32 rng(0x15dfu);
+  for (double& x : g) x = rng.gaussian();  // Matrix::gaussian: column-major fill (matrix.hpp:29-33)
+  DBuf dg = upload(c, g.data(), g.size());
+  DBuf pm = dalloc(c, (size_t)n_r * m);
+  ck(pair_matrix(c->stream, a, lda, n1, b, ldb, n2, n_r, pm.d(), n_r), "pair_matrix");
+  DBuf f = dalloc(c, (size_t)n_r * ns), ones = dalloc(c, (size_t)n_r);
+  Work w = make_work(c, (size_t)4 * n_r * ns);
+  gemm(c, n_r, ns, (int)m, pm.d(), n_r, Lay::MN, dg.d(), ns, Lay::MN, f.d(), n_r, 1.0, 0.0, nullptr, false, &w);
+  ck(fill(c->stream, ones.d(), (size_t)n_r, 1.0), "fill");
+  return select_impl(c, f.d(), n_r, ns, ones.d(), n_r, 1, n_r, n_mu, nullptr);
+}
+
 // ---------------------------------------------------------------------------
 // Stage 2: Theta = lhs G^-1 with lhs = (A A_mu^T) o (B B_mu^T) (isdf.hpp:118-163).
 // ---------------------------------------------------------------------------
@@ -1128,12 +1188,14 @@ int lrgw_coulomb_kernel(const int* dims, const double* cell, double* kernel) {
 int lrgw_select_interpolation_points(lrgw_ctx c, const double* psi_a, const double* psi_b, int n_r, int n1,
                                      int n2, int n_mu, int method, int32_t* pts) {
   return guarded(c, [&] {
-    if (method == LRGW_QRCP_SKETCHED)
-      fail(LRGW_ERR_UNSUPPORTED, "select_interpolation_points: qrcp_sketched is not implemented on B200");
+    if (method != LRGW_QRCP_DIRECT && method != LRGW_QRCP_SKETCHED)
+      fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: unknown point selector");
     if (n_mu > n_r) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: N_mu > N_r");
     if (n_mu < 1) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: N_mu < 1");
     DBuf a = upload(c, psi_a, (size_t)n_r * n1), b = upload(c, psi_b, (size_t)n_r * n2);
-    std::vector<int32_t> p = select_impl(c, a.d(), n_r, n1, b.d(), n_r, n2, n_r, n_mu, nullptr);
+    std::vector<int32_t> p = method == LRGW_QRCP_SKETCHED
+                                 ? select_sketched(c, a.d(), n_r, n1, b.d(), n_r, n2, n_r, n_mu)
+                                 : select_impl(c, a.d(), n_r, n1, b.d(), n_r, n2, n_r, n_mu, nullptr);
     std::copy(p.begin(), p.end(), pts);
   });
 }

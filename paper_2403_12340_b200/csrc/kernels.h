@@ -72,6 +72,9 @@ cudaError_t coulomb_scale_half(cudaStream_t st, int n1, int n2, int n3, double c
 // scalar helpers (misc.cu)
 cudaError_t scale_copy(cudaStream_t st, const double* src, double* dst, size_t n, double alpha);
 cudaError_t fill(cudaStream_t st, double* dst, size_t n, double v);
+// M (n_r x n1 n2): column i + n1 j = a(:, i) .* b(:, j) (the reference's pair matrix)
+cudaError_t pair_matrix(cudaStream_t st, const double* a, long long lda, int n1, const double* b, long long ldb,
+                        int n2, int n_r, double* m, long long ldm);
 cudaError_t zero_strict_upper(cudaStream_t st, double* a, int n, long long lda);
 // out (cols x rows) = in^T (rows x cols), column-major.
 cudaError_t transpose(cudaStream_t st, const double* in, long long ldi, int rows, int cols, double* out,

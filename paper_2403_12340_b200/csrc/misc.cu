@@ -97,6 +97,19 @@ __global__ void transpose_kernel(const double* in, long long ldi, int rows, int 
   }
 }
 
+// pair matrix M (N_r x n1 n2, column i + n1 j = a(:, i) .* b(:, j)); isdf.hpp:51-66
+__global__ void pair_matrix_kernel(const double* a, long long lda, int n1, const double* b, long long ldb, int n2,
+                                   int n_r, double* m, long long ldm) {
+  const long long total = (long long)n_r * n1 * n2;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(idx % n_r);
+    const long long col = idx / n_r;
+    const int i = static_cast<int>(col % n1), j = static_cast<int>(col / n1);
+    m[r + col * ldm] = a[r + i * lda] * b[r + j * ldb];
+  }
+}
+
 }  // namespace
 
 cudaError_t transpose(cudaStream_t st, const double* in, long long ldi, int rows, int cols, double* out,
@@ -104,6 +117,13 @@ cudaError_t transpose(cudaStream_t st, const double* in, long long ldi, int rows
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   transpose_kernel<<<dim3((cols + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, st>>>(in, ldi, rows, cols, out, ldo);
   count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t pair_matrix(cudaStream_t st, const double* a, long long lda, int n1, const double* b, long long ldb,
+                        int n2, int n_r, double* m, long long ldm) {
+  if ((long long)n_r * n1 * n2 == 0) return cudaSuccess;
+  pair_matrix_kernel<<<1184, 256, 0, st>>>(a, lda, n1, b, ldb, n2, n_r, m, ldm); count_launches(1);
   return cudaGetLastError();
 }
 

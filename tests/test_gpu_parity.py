@@ -154,8 +154,21 @@ def test_selection_errors(L, ctx, ref):
         L.select_interpolation_points(a, b, a.shape[0] + 1, ctx=ctx)
     with pytest.raises(L.InvalidInput):
         L.select_interpolation_points(a, b, 0, ctx=ctx)
-    with pytest.raises(L.InvalidInput):
-        L.select_interpolation_points(a, b, 16, method="qrcp_sketched", ctx=ctx)
+    with pytest.raises(L.GuardExceeded):  # the sketch materialises the pair matrix (isdf.hpp:49, 77-78)
+        psi, _ = ref.build_synthetic(2, (24, 24, 24), (10.0, 10.0, 10.0), 72, 72, 1.0, 4.0)
+        L.select_interpolation_points(psi[:, :72], psi[:, 72:], 64, method="qrcp_sketched", ctx=ctx)
+
+
+@pytest.mark.parametrize("seed,dims,n,k", [(1, (8, 8, 8), 24, 4.0), (3, (8, 8, 8), 32, 3.0), (5, (8, 8, 4), 16, 2.0),
+                                           (2, (8, 8, 8), 16, 8.0)])
+def test_sketched_selection_matches_reference(L, ctx, ref, seed, dims, n, k):
+    """PointSelector::qrcp_sketched (isdf.hpp:95-112): the reference's fixed
+    Gaussian sketch of the pair rows, then QRCP — pivots bit-exact. The last
+    case has 2 N_mu >= N1 N2, where the reference falls back to plain QRCP."""
+    a, b, _ = _desk(ref, seed=seed, dims=dims, n=n)
+    n_mu = ref.num_aux(k, n, n)
+    got = L.select_interpolation_points(a, b, n_mu, method="qrcp_sketched", ctx=ctx)
+    assert np.array_equal(got, ref.select_points(a, b, n_mu, sketched=True))
 
 
 def test_fit_fallback_and_degenerate(L, ctx, ref):
