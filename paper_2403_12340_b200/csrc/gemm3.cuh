@@ -135,7 +135,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) dgemm3_kernel(DgemmPa
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp % Cfg::WARPS_M) * Cfg::WM, wn = (warp / Cfg::WARPS_M) * Cfg::WN;
   const int g = lane >> 2, t = lane & 3;
-  const bool live = n0 + wn < p.N;  // warps wholly past a device-bounded N skip their MMAs
+  // warps wholly past a device-bounded N skip their MMAs, and so do the warps
+  // of a diagonal lower tile that sit strictly above the diagonal (every
+  // lower-tile caller mirrors the lower triangle over the upper one)
+  const bool live = n0 + wn < p.N && !(p.lower && tm == tn && wn >= wm + Cfg::WM);
 
   double acc[FM][FN][2];
 #pragma unroll

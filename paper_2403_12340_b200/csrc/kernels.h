@@ -15,7 +15,8 @@ void count_launches(int n);
 enum class Lay { MN, K };  // operand stored MN-contiguous (col-major) or K-contiguous
 
 // C = alpha * A diag(scale) B^T + beta * C with A: M x K, B: N x K (see gemm.cuh).
-// lower: only lower-triangle tiles (M == N). `work` enables split-K.
+// lower: only lower-triangle tiles (M == N); the strict upper triangle of the
+// result is unspecified (callers mirror the lower one). `work` enables split-K.
 // tri_b: B(n, k) == 0 for k < n (skip those k); colmap: output column n goes
 // to column colmap[n] of C (device array).
 cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long long lda, Lay la,
