@@ -366,7 +366,7 @@ class DistributedBuild:
         """eps^-1 x on the local panel rows: x_p + (V Theta (K Theta^T x))_p."""
         be, st = self.be, self.st
         u = self.comm.allreduce_sum(be.theta_t_x(st.theta, x_p))
-        z_p = be.theta_w(st.theta, k @ u)
+        z_p = be.theta_w(st.theta, be.matmul(k, u))
         z = be.vcat(self.comm.allgather(z_p, ragged=True))
         vz = be.apply_coulomb(self.dims, self.cell, z)
         return be.to_host(x_p) + be.to_host(vz)[st.r0:st.r1]

@@ -202,6 +202,13 @@ class CudaBackend:
         lrgw.dgemm_dev("T", "N", 1.0, theta, xd, 0.0, out, ctx=self.ctx)
         return out
 
+    def matmul(self, a, b):
+        """a b on the DMMA engine (the replicated K u of the probe apply)."""
+        ad, bd = _dev(a), _dev(b)
+        out = _cm(ad.shape[0], bd.shape[1])
+        lrgw.dgemm_dev("N", "N", 1.0, ad, bd, 0.0, out, ctx=self.ctx)
+        return out
+
     def theta_w(self, theta, w):
         wd = _dev(w)
         out = _cm(theta.shape[0], wd.shape[1])

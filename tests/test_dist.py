@@ -128,6 +128,9 @@ class NumpyBackend:
     def theta_t_x(self, theta, x):
         return theta.T @ x
 
+    def matmul(self, a, b):
+        return np.asarray(a) @ np.asarray(b)
+
     def theta_w(self, theta, w):
         return theta @ w
 
