@@ -6,6 +6,8 @@ inversion of arXiv 2403.12340 behind the reference `lrgw` interface.
     lrgw.py    Python mirror of the reference hot-path API over the C-ABI
     synth.py   seeded synthetic Si-like / C60-like workloads (BASELINE configs)
     dist.py    multi-rank orchestration (node / row-panel sharding)
+    dist_cuda.py  the per-rank device backend of dist.py
+    driver.py  the reference driver's run / scale commands over the GPU path
 """
 from . import lrgw  # noqa: F401  (raises ImportError when the extension is missing)
 

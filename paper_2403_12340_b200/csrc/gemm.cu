@@ -244,8 +244,20 @@ using H2W32 = Gemm2Cfg<128, 32, 32, 32, 4, V, true>;
 
 // Tall Hadamard (selection: W columns of the accepted pivots, N = 48..128):
 // 64 x 16Q CTAs of 4 warps (16 x 16Q each), 2 per SM.
+// Shared memory decides the residency: the parked product (FM FN 2 doubles
+// per thread) plus the operand ring must leave room for 8 warps per SM.
+//   Q <= 4: 64-row CTAs, 3-stage ring (<= 84 KB: 2 CTAs per SM);
+//   Q 5-7:  64-row CTAs, 2-stage ring (<= 105 KB: 2 CTAs per SM) or, with
+//           LRGW_HAD_WIDE=1, 128-row CTAs of 8 warps with a 3-stage ring (1 per SM).
 template <int Q>
-using H2T = Gemm2Cfg<64, 16 * Q, 16, 16 * Q, 3, 2, true, 16, (Q <= 4 ? 3 : 2), false, true>;
+using H2T = Gemm2Cfg<64, 16 * Q, 16, 16 * Q, (Q <= 4 ? 3 : 2), 2, true, 16, 2, false, true>;
+template <int Q>
+using H2TW = Gemm2Cfg<128, 16 * Q, 16, 16 * Q, 3, 2, true, 16, 1, false, true>;
+
+bool had_wide() {
+  static const bool on = getenv("LRGW_HAD_WIDE") && atoi(getenv("LRGW_HAD_WIDE")) == 1;
+  return on;
+}
 
 bool had_tall_v2_enabled() {
   static const bool on = !(getenv("LRGW_HAD_TALL") && atoi(getenv("LRGW_HAD_TALL")) == 0);
@@ -507,7 +519,7 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
     kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(p); count_launches(1);
     return cudaGetLastError();
   };
-  if (N < 128 && vec && N > 32 && tall_family_enabled() && had_tall_v2_enabled() &&
+  if (N <= 112 && vec && N > 32 && tall_family_enabled() && had_tall_v2_enabled() &&
       (long long)((M + 63) / 64) >= 2LL * 148) {
     // paired-fragment engine, one column tile of width 16 Q, 4 warps of 16 x 16 Q; the first
     // product parks in shared memory (one register accumulator set)
@@ -518,13 +530,14 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
     switch ((N + 15) / 16) {
       case 3: return launch2<H2T<3>>(st, q);
       case 4: return launch2<H2T<4>>(st, q);
-      case 5: return launch2<H2T<5>>(st, q);
-      case 6: return launch2<H2T<6>>(st, q);
-      case 7: return launch2<H2T<7>>(st, q);
-      default: return launch2<H2T<8>>(st, q);
+      case 5: return had_wide() ? launch2<H2TW<5>>(st, q) : launch2<H2T<5>>(st, q);
+      case 6: return had_wide() ? launch2<H2TW<6>>(st, q) : launch2<H2T<6>>(st, q);
+      default: return had_wide() ? launch2<H2TW<7>>(st, q) : launch2<H2T<7>>(st, q);
     }
   }
-  if (N < 128 && vec && N > 32 && tall_family_enabled() && (long long)((M + 127) / 128) >= 2LL * 148) {
+  // widths 113-127: the general paired-fragment Hadamard below (two 64-wide column tiles)
+  const bool v2_wide = vec && N > 112 && had_tall_v2_enabled();
+  if (!v2_wide && N < 128 && vec && N > 32 && tall_family_enabled() && (long long)((M + 127) / 128) >= 2LL * 148) {
     switch ((N + 15) / 16) {
       case 3: return go(CfgHT<3>{});
       case 4: return go(CfgHT<4>{});
@@ -538,7 +551,7 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
     // a candidate block's Schur block (s x s): 32 x 32 tiles for parallelism
     return vec ? go(GemmCfg<32, 32, 16, 16, 3, false, false, 2, 2>{}) : go(GemmCfg<32, 32, 16, 16, 3, false, false, 1, 1>{});
   }
-  if (N < 128) {
+  if (N < 128 && !v2_wide) {
     if (prefer_narrow(N)) return vec ? go(CfgH32<2>{}) : go(CfgH32<1>{});
     return vec ? go(CfgH<2>{}) : go(CfgH<1>{});
   }
