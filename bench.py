@@ -196,6 +196,7 @@ def run_ours(args, cfg, world, rank, local):
         t_steps.append(e0.elapsed_time(e1))
         for k, v in ctx.stage_ms().items():
             stage_acc.setdefault(k, []).append(v)
+        points = ep.point_indices  # the CPU baseline's fit sample uses the build's own ISDF points
         ep.close()
     torch.cuda.synchronize()
     barrier(world)
@@ -275,7 +276,8 @@ def run_ours(args, cfg, world, rank, local):
                 "peak_source": "profiles/FP64_PEAK.json (measured DMMA)" if dk["bound"] == "tensor"
                 else "MEASURED_PEAKS.json hbm_gbs"}
     return {"ms": ms, "e2e_ms": e2e, "h2d": h2d, "d2h": d2h, "launches": launches, "clocks": clk,
-            "stages": stages, "kernels": kernels, "roofline": roofline, "psi": psi, "e": e, "ctx": ctx}
+            "stages": stages, "kernels": kernels, "roofline": roofline, "psi": psi, "e": e, "ctx": ctx,
+            "points": points}
 
 
 def run_sharded(args, cfg, world, rank, local):
@@ -445,7 +447,7 @@ def main():
         ccfg, scale = cpu_config(cfg)
         if ccfg is cfg:
             psi_h = np.asfortranarray(res["psi"].cpu().numpy())
-            r = cpu_baseline.run(cfg, psi=psi_h, energies=res["e"], cores=os.cpu_count())
+            r = cpu_baseline.run(cfg, psi=psi_h, energies=res["e"], cores=os.cpu_count(), points=res["points"])
         else:
             r = cpu_baseline.run(ccfg, cores=os.cpu_count())
         cpu = {"value": r["total_s"] * scale, "unit": "s", "cores": r["cores"], "kind": "reference",

@@ -11,7 +11,8 @@ each stage is sampled:
              (OpenMP, all cores) runs the first S pivot steps; per-step cost
              is linear in (N_v + N_c + k), summed over k < N_mu.
   2 fit      reference fit_auxiliary_basis (isdf.hpp:118-163, serial) on two
-             row samples (all N_mu point rows + filler rows); t = a + b N_rows
+             row samples (all N_mu point rows — the GPU build's points when
+             given — + filler rows); t = a + b N_rows
              fitted and evaluated at N_r (LU of the N_mu Gram is the constant).
   3 contour  reference detail::sum_node_terms (contour.hpp:185-222) over ALL
              N_lambda + 1 nodes with threads = cores (no extrapolation).
@@ -39,7 +40,8 @@ def _t(fn):
     return time.perf_counter() - t0, out
 
 
-def run(cfg, psi=None, energies=None, cores=None, sel_steps=64, fit_rows=(2048, 4096), cols=128, seed=5):
+def run(cfg, psi=None, energies=None, cores=None, sel_steps=64, fit_rows=(2048, 4096), cols=128, seed=5,
+        points=None):
     """Returns dict(total_s, total_no_select_s, stages, sample, cores)."""
     cores = cores or os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
@@ -62,7 +64,10 @@ def run(cfg, psi=None, energies=None, cores=None, sel_steps=64, fit_rows=(2048, 
     stages["select"] = t_sel * w_all / w_s
 
     # 2: reference fit on two row samples containing all point rows
-    pts = np.sort(rng.choice(n_r, n_mu, replace=False)).astype(np.int32)
+    # the build's own ISDF points when given (random grid points can make the
+    # Gram of localised orbitals singular — C60 — where the reference throws)
+    pts = (np.sort(np.asarray(points)).astype(np.int32) if points is not None
+           else np.sort(rng.choice(n_r, n_mu, replace=False)).astype(np.int32))
     others = np.setdiff1d(np.arange(n_r), pts)
     times = []
     for rows in fit_rows:

@@ -253,6 +253,13 @@ template <int Q>
 using H2T = Gemm2Cfg<64, 16 * Q, 16, 16 * Q, (Q <= 4 ? 3 : 2), 2, true, 16, 2, false, true>;
 template <int Q>
 using H2TW = Gemm2Cfg<128, 16 * Q, 16, 16 * Q, 3, 2, true, 16, 1, false, true>;
+// widths 113-128: BK = 8 keeps the 2-stage ring + parked product at 91 KB (2 CTAs per SM)
+using H2T8 = Gemm2Cfg<64, 128, 16, 128, 2, 2, true, 8, 2, false, true>;
+
+bool had128_park() {
+  static const bool on = !(getenv("LRGW_HAD128") && atoi(getenv("LRGW_HAD128")) == 0);
+  return on;
+}
 
 bool had_wide() {
   static const bool on = getenv("LRGW_HAD_WIDE") && atoi(getenv("LRGW_HAD_WIDE")) == 1;
@@ -519,7 +526,7 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
     kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(p); count_launches(1);
     return cudaGetLastError();
   };
-  if (N <= 112 && vec && N > 32 && tall_family_enabled() && had_tall_v2_enabled() &&
+  if (N <= 128 && vec && N > 32 && tall_family_enabled() && had_tall_v2_enabled() && (N <= 112 || had128_park()) &&
       (long long)((M + 63) / 64) >= 2LL * 148) {
     // paired-fragment engine, one column tile of width 16 Q, 4 warps of 16 x 16 Q; the first
     // product parks in shared memory (one register accumulator set)
@@ -532,11 +539,12 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
       case 4: return launch2<H2T<4>>(st, q);
       case 5: return had_wide() ? launch2<H2TW<5>>(st, q) : launch2<H2T<5>>(st, q);
       case 6: return had_wide() ? launch2<H2TW<6>>(st, q) : launch2<H2T<6>>(st, q);
-      default: return had_wide() ? launch2<H2TW<7>>(st, q) : launch2<H2T<7>>(st, q);
+      case 7: return had_wide() ? launch2<H2TW<7>>(st, q) : launch2<H2T<7>>(st, q);
+      default: return launch2<H2T8>(st, q);
     }
   }
   // widths 113-127: the general paired-fragment Hadamard below (two 64-wide column tiles)
-  const bool v2_wide = vec && N > 112 && had_tall_v2_enabled();
+  const bool v2_wide = vec && N > 112 && had_tall_v2_enabled() && !had128_park();
   if (!v2_wide && N < 128 && vec && N > 32 && tall_family_enabled() && (long long)((M + 127) / 128) >= 2LL * 148) {
     switch ((N + 15) / 16) {
       case 3: return go(CfgHT<3>{});
