@@ -268,7 +268,7 @@ def run_ours(args, cfg, world, rank, local):
     dk = kernels[dom]
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and cfg.name == "si64":  # the committed ncu traffic capture is of the Si64 build
         traffic = json.load(open(tp)).get(dom)
     roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"],
                 "peak": FP64_PEAK_TFLOPS if dk["bound"] == "tensor" else hbm,
