@@ -1,6 +1,4 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
-tail -n 3 gpurun_out/gpu_tests.log; tail -n 1 gpurun_out/smoke.log; grep -o '"value": [0-9.]*' gpurun_out/bench.log | head -3; tail -n 1 gpurun_out/bench_ref.log
+timeout 900 python -m pytest tests/test_gpu_build.py tests/test_gpu_dist.py tests/test_gpu_parity.py -x -q -k "not si512" > gpurun_out/sk_tests.log 2>&1; echo "rc=$?" >> gpurun_out/sk_tests.log
+timeout 300 python tools/dist_time.py --config si64 > gpurun_out/dist_time_si64.log 2>&1
+tail -n 2 gpurun_out/sk_tests.log; tail -n 1 gpurun_out/dist_time_si64.log | cut -c1-200

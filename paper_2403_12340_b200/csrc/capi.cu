@@ -1673,9 +1673,19 @@ int lrgw_dev_dgemm(lrgw_ctx c, char ta, char tb, int m, int n, int k, double alp
                    const double* b, long long ldb, double beta, double* cm, long long ldc) {
   return guarded(c, [&] {
     const bool at = ta == 'T' || ta == 't', bt = tb == 'T' || tb == 't';
-    Work w = make_work(c, (size_t)8 * m * n);
-    gemm(c, m, n, k, a, lda, at ? Lay::K : Lay::MN, b, ldb, bt ? Lay::MN : Lay::K, cm, ldc, alpha, beta, nullptr,
-         false, &w);
+    // probe-shaped products (<= 16 columns against a tall panel): the K7
+    // streams of the probe apply instead of the tiled engine
+    const bool plain = alpha == 1.0 && beta == 0.0 && !bt && skinny_supported(n) && k > 0 && m > 0;
+    if (plain && at && (long long)k >= 8LL * m) {  // u = A^T x, A: k x m (Theta panel), x: k x n
+      Work w = make_work(c, (size_t)1200 * m * n);
+      ck(skinny_tn(c->stream, a, lda, k, m, b, ldb, n, cm, ldc, w.buf.d(), w.elems, c->sm_count), "skinny_tn");
+    } else if (plain && !at && (long long)m >= 8LL * k && (size_t)k * n * 8 <= 200 * 1024) {  // z = A w
+      ck(skinny_nn(c->stream, a, lda, m, k, b, ldb, n, cm, ldc, c->sm_count), "skinny_nn");
+    } else {
+      Work w = make_work(c, (size_t)8 * m * n);
+      gemm(c, m, n, k, a, lda, at ? Lay::K : Lay::MN, b, ldb, bt ? Lay::MN : Lay::K, cm, ldc, alpha, beta, nullptr,
+           false, &w);
+    }
     ck(cudaStreamSynchronize(c->stream), "sync");
   });
 }
