@@ -673,6 +673,11 @@ struct HostEnt {
 
 // keep (optional): the pivoted-Cholesky factor L (n_r x steps, pivot order)
 // and the pivot sequence, reused by the fused fit of lrgw_build.
+bool fused_downdate_enabled() {
+  static const bool on = !(getenv("LRGW_FUSED_DOWNDATE") && atoi(getenv("LRGW_FUSED_DOWNDATE")) == 0);
+  return on;
+}
+
 bool select_trace() {
   static const bool on = getenv("LRGW_SELECT_TRACE") != nullptr;
   return on;
@@ -750,8 +755,18 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
       ck(gather_rows(c->stream, L.d(), n_r, k, srow, nb, lrow.d(), ldb_), "gather");
       gemm(c, n_r, nb, k, L.d(), n_r, Lay::MN, lrow.d(), ldb_, Lay::MN, wsel.d(), n_r, -1.0, 1.0);
     }
-    gemm(c, n_r, nb, nb, wsel.d(), n_r, Lay::MN, xcol.d(), se, Lay::MN, L.d() + (size_t)k * n_r, n_r, 1.0, 0.0);
-    ck(select_downdate(c->stream, L.d(), n_r, k, nb, pos.i(), d.d()), "downdate");
+    // L[:, k:k+nb] = W_sel X^T with d -= rowsum(L_blk^2) fused in the epilogue (rows not yet taken)
+    cudaError_t fe = fused_downdate_enabled()
+                         ? dgemm_tall_downdate(c->stream, n_r, nb, nb, wsel.d(), n_r, xcol.d(), se,
+                                               L.d() + (size_t)k * n_r, n_r, d.d(), pos.i(), k + nb)
+                         : cudaErrorNotSupported;
+    if (fe == cudaErrorNotSupported) {
+      cudaGetLastError();
+      gemm(c, n_r, nb, nb, wsel.d(), n_r, Lay::MN, xcol.d(), se, Lay::MN, L.d() + (size_t)k * n_r, n_r, 1.0, 0.0);
+      ck(select_downdate(c->stream, L.d(), n_r, k, nb, pos.i(), d.d()), "downdate");
+    } else {
+      ck(fe, "dgemm_tall_downdate");
+    }
     k += nb;
   }
   std::vector<int32_t> pts(n_mu);
@@ -1790,8 +1805,17 @@ int lrgw_dev_select_panel_update(lrgw_ctx c, const double* a, long long lda, int
     ck(hadamard_gemm(c->stream, rows, nb, a, lda, amu, ldp, n1, b, ldb, bmu, ldp, n2, wsel.d(), rows, 1.0, 0.0),
        "hadamard_gemm");
     if (k > 0) gemm(c, rows, nb, k, l, ldl, Lay::MN, lsel, ldp, Lay::MN, wsel.d(), rows, -1.0, 1.0);
-    gemm(c, rows, nb, nb, wsel.d(), rows, Lay::MN, x, ldx, Lay::MN, l + (size_t)k * ldl, ldl, 1.0, 0.0);
-    ck(select_downdate(c->stream, l, rows, k, nb, pos, d), "downdate");
+    cudaError_t fe = fused_downdate_enabled() && ldl == rows
+                         ? dgemm_tall_downdate(c->stream, rows, nb, nb, wsel.d(), rows, x, ldx, l + (size_t)k * ldl,
+                                               ldl, d, pos, k + nb)
+                         : cudaErrorNotSupported;
+    if (fe == cudaErrorNotSupported) {
+      cudaGetLastError();
+      gemm(c, rows, nb, nb, wsel.d(), rows, Lay::MN, x, ldx, Lay::MN, l + (size_t)k * ldl, ldl, 1.0, 0.0);
+      ck(select_downdate(c->stream, l, rows, k, nb, pos, d), "downdate");
+    } else {
+      ck(fe, "dgemm_tall_downdate");
+    }
     ck(cudaStreamSynchronize(c->stream), "sync");
   });
 }

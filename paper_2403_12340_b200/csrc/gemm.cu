@@ -508,6 +508,34 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
   return cudaGetLastError();
 }
 
+// The selection's L block with the residual downdate fused in the epilogue:
+// C = A B^T (M x N, N <= 128 in one column tile whose warps span all N
+// columns) and d[m] -= sum_n C(m, n)^2 for rows with pos[m] >= kend.
+// Returns cudaErrorNotSupported when the shape / alignment does not fit (the
+// caller then runs the GEMM and the downdate kernel separately).
+template <int Q, int V>
+using G2D = Gemm2Cfg<64, 16 * Q, 16, 16 * Q, 3, V, false, 16, (Q <= 5 ? 3 : 2)>;
+
+cudaError_t dgemm_tall_downdate(cudaStream_t st, int M, int N, int K, const double* A, long long lda,
+                                const double* B, long long ldb, double* C, long long ldc, double* d,
+                                const int* pos, int kend) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  const bool vec = aligned16(A) && aligned16(B) && aligned16(C) && lda % 2 == 0 && ldb % 2 == 0 && ldc % 2 == 0;
+  if (N > 128 || N < 17 || !vec) return cudaErrorNotSupported;
+  Dgemm2Params q{};
+  q.M = M, q.N = N, q.K = K, q.A = A, q.lda = lda, q.B = B, q.ldb = ldb, q.C = C, q.ldc = ldc;
+  q.alpha = 1.0, q.beta = 0.0, q.dd = d, q.dpos = pos, q.dkend = kend;
+  switch ((N + 15) / 16) {
+    case 2: return launch2<G2D<2, 2>>(st, q);
+    case 3: return launch2<G2D<3, 2>>(st, q);
+    case 4: return launch2<G2D<4, 2>>(st, q);
+    case 5: return launch2<G2D<5, 2>>(st, q);
+    case 6: return launch2<G2D<6, 2>>(st, q);
+    case 7: return launch2<G2D<7, 2>>(st, q);
+    default: return launch2<G2D<8, 2>>(st, q);
+  }
+}
+
 cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long long lda1,
                           const double* b1, long long ldb1, int k1, const double* a2,
                           long long lda2, const double* b2, long long ldb2, int k2, double* C,

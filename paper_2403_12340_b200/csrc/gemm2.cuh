@@ -36,6 +36,11 @@ struct Dgemm2Params {
   int tri_b;
   const int* colmap;
   const int* n_dev;
+  // fused residual downdate of the selection (one warp column per CTA only):
+  // dd[m] -= sum_n C(m, n)^2 for rows with dpos[m] >= dkend
+  double* dd;
+  const int* dpos;
+  int dkend;
 };
 
 template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int VEC_, bool HAD_, int BK_ = 16, int MINB_ = 1,
@@ -173,6 +178,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) dgemm2_kernel(Dgemm2P
 #pragma unroll
   for (int j = 0; j < FM / 2; ++j) {
     const int m = m0 + wm + 16 * j + 2 * g;
+    double sq0 = 0.0, sq1 = 0.0;  // fused downdate: this thread's share of the rows' squared sums
 #pragma unroll
     for (int jn = 0; jn < FN; ++jn)
 #pragma unroll
@@ -189,6 +195,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) dgemm2_kernel(Dgemm2P
         }
         v0 *= p.alpha;
         v1 *= p.alpha;
+        sq0 = fma(v0, v0, sq0);
+        sq1 = fma(v1, v1, sq1);
         const int nc = p.colmap ? __ldg(p.colmap + n) : n;
         double* c = p.C + m + (long long)nc * p.ldc;
         if (m + 1 < p.M && ((reinterpret_cast<uintptr_t>(c) & 15) == 0)) {
@@ -204,6 +212,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) dgemm2_kernel(Dgemm2P
           if (m + 1 < p.M) c[1] = (p.beta == 0.0) ? v1 : v1 + p.beta * c[1];
         }
       }
+    if (p.dd) {  // the 4 lanes of a row pair (t = 0..3) hold disjoint columns; WARPS_N == 1
+      sq0 += __shfl_xor_sync(0xffffffffu, sq0, 1);
+      sq1 += __shfl_xor_sync(0xffffffffu, sq1, 1);
+      sq0 += __shfl_xor_sync(0xffffffffu, sq0, 2);
+      sq1 += __shfl_xor_sync(0xffffffffu, sq1, 2);
+      if (t == 0) {
+        if (m < p.M && p.dpos[m] >= p.dkend) p.dd[m] -= sq0;
+        if (m + 1 < p.M && p.dpos[m + 1] >= p.dkend) p.dd[m + 1] -= sq1;
+      }
+    }
   }
 }
 

@@ -33,6 +33,13 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
                           long long lda2, const double* b2, long long ldb2, int k2, double* C,
                           long long ldc, double alpha, double beta);
 
+// C = A B^T (A: M x K, B: N x K, both MN-contiguous; N <= 128) with the
+// selection's residual downdate fused: d[m] -= sum_n C(m, n)^2 where
+// pos[m] >= kend. cudaErrorNotSupported: shape / alignment not covered.
+cudaError_t dgemm_tall_downdate(cudaStream_t st, int M, int N, int K, const double* A, long long lda,
+                                const double* B, long long ldb, double* C, long long ldc, double* d,
+                                const int* pos, int kend);
+
 // a(j,i) = a(i,j) for i > j (average = 0) or both = (a(i,j) + a(j,i))/2.
 cudaError_t mirror_lower(cudaStream_t st, double* a, int n, long long lda, bool average);
 
