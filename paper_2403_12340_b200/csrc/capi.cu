@@ -726,15 +726,13 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
     // (s x s: only the candidates' rows ever enter the greedy).
     ck(select_topk(c->stream, d.d(), pos.i(), n_r, k, se + 1, tmp.p, top.p), "select_topk");
     ck(select_cand_rows(c->stream, top.p, se, cand.i()), "cand_rows");
-    ck(gather_rows(c->stream, a, lda, n1, cand.i(), se, amu.d(), lds), "gather");
-    ck(gather_rows(c->stream, b, ldb, n2, cand.i(), se, bmu.d(), lds), "gather");
+    ck(gather_rows3(c->stream, a, lda, n1, b, ldb, n2, L.d(), n_r, k, cand.i(), se, amu.d(), bmu.d(), lrow.d(), lds),
+       "gather");
     ck(hadamard_gemm(c->stream, se, se, amu.d(), lds, amu.d(), lds, n1, bmu.d(), lds, bmu.d(), lds, n2, wcc.d(), se,
                      1.0, 0.0),
        "hadamard_gemm(W_CC)");
-    if (k > 0) {
-      ck(gather_rows(c->stream, L.d(), n_r, k, cand.i(), se, lrow.d(), lds), "gather");
+    if (k > 0)
       gemm(c, se, se, k, lrow.d(), lds, Lay::MN, lrow.d(), lds, Lay::MN, wcc.d(), se, -1.0, 1.0, nullptr, false, &w);
-    }
     ck(select_cand_greedy(c->stream, n_r, se, steps, k, top.p, wcc.d(), pos.i(), perm.i(), xcol.d(), order.i(),
                           min_margin ? margin.d() : nullptr, bout),
        "cand_greedy");
@@ -746,15 +744,12 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
     // order[k .. k+nb)), then L[:, k:k+nb] = W_sel X^T with X = L_sel^-1.
     const int* srow = order.i() + k;
     const int ldb_ = nb + (nb & 1);
-    ck(gather_rows(c->stream, a, lda, n1, srow, nb, amu.d(), ldb_), "gather");
-    ck(gather_rows(c->stream, b, ldb, n2, srow, nb, bmu.d(), ldb_), "gather");
+    ck(gather_rows3(c->stream, a, lda, n1, b, ldb, n2, L.d(), n_r, k, srow, nb, amu.d(), bmu.d(), lrow.d(), ldb_),
+       "gather");
     ck(hadamard_gemm(c->stream, n_r, nb, a, lda, amu.d(), ldb_, n1, b, ldb, bmu.d(), ldb_, n2, wsel.d(), n_r, 1.0,
                      0.0),
        "hadamard_gemm");
-    if (k > 0) {
-      ck(gather_rows(c->stream, L.d(), n_r, k, srow, nb, lrow.d(), ldb_), "gather");
-      gemm(c, n_r, nb, k, L.d(), n_r, Lay::MN, lrow.d(), ldb_, Lay::MN, wsel.d(), n_r, -1.0, 1.0);
-    }
+    if (k > 0) gemm(c, n_r, nb, k, L.d(), n_r, Lay::MN, lrow.d(), ldb_, Lay::MN, wsel.d(), n_r, -1.0, 1.0);
     // L[:, k:k+nb] = W_sel X^T with d -= rowsum(L_blk^2) fused in the epilogue (rows not yet taken)
     cudaError_t fe = fused_downdate_enabled()
                          ? dgemm_tall_downdate(c->stream, n_r, nb, nb, wsel.d(), n_r, xcol.d(), se,

@@ -219,6 +219,28 @@ __global__ void gather_rows_kernel(const double* src, long long lds, int cols, c
   }
 }
 
+// The selection's row gathers in one launch: rows `rows` of three column-major
+// sources (a: n1 cols, b: n2 cols, l: nl cols) into three destinations of leading dim ldd.
+__global__ void gather_rows3_kernel(const double* a, long long lda, int n1, const double* b, long long ldb, int n2,
+                                    const double* l, long long ldl, int nl, const int* rows, int n_rows, double* da,
+                                    double* db, double* dl, long long ldd) {
+  const long long total = (long long)n_rows * (n1 + n2 + nl);
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(idx % n_rows);
+    int c = static_cast<int>(idx / n_rows);
+    const int g = rows[r];
+    if (c < n1) {
+      da[r + c * ldd] = a[g + c * lda];
+    } else if ((c -= n1) < n2) {
+      db[r + c * ldd] = b[g + c * ldb];
+    } else {
+      c -= n2;
+      dl[r + c * ldd] = l[g + c * ldl];
+    }
+  }
+}
+
 __global__ void gather_cols_kernel(const double* src, long long lds, int rows, const int* cols, int n,
                                    double* dst, long long ldd) {
   const long long total = (long long)rows * n;
@@ -334,6 +356,15 @@ cudaError_t dispatch2(cudaStream_t st, const Dgemm2Params& p, bool had) {
 }
 
 }  // namespace
+
+cudaError_t gather_rows3(cudaStream_t st, const double* a, long long lda, int n1, const double* b, long long ldb,
+                        int n2, const double* l, long long ldl, int nl, const int* rows, int n_rows, double* da,
+                        double* db, double* dl, long long ldd) {
+  if (n_rows <= 0 || n1 + n2 + nl <= 0) return cudaSuccess;
+  gather_rows3_kernel<<<592, 256, 0, st>>>(a, lda, n1, b, ldb, n2, l, ldl, nl, rows, n_rows, da, db, dl, ldd);
+  count_launches(1);
+  return cudaGetLastError();
+}
 
 cudaError_t gather_cols(cudaStream_t st, const double* src, long long lds, int rows, const int* cols, int n,
                         double* dst, long long ldd) {

@@ -47,6 +47,11 @@ cudaError_t mirror_lower(cudaStream_t st, double* a, int n, long long lda, bool 
 cudaError_t gather_rows(cudaStream_t st, const double* src, long long lds, int cols, const int* rows,
                         int n_rows, double* dst, long long ldd);
 
+// rows `rows` of a (n1 cols), b (n2 cols) and l (nl cols) into da, db, dl (ld ldd), one launch.
+cudaError_t gather_rows3(cudaStream_t st, const double* a, long long lda, int n1, const double* b, long long ldb,
+                         int n2, const double* l, long long ldl, int nl, const int* rows, int n_rows, double* da,
+                         double* db, double* dl, long long ldd);
+
 // dst(:, c) = src(:, cols[c]), cols on device.
 cudaError_t gather_cols(cudaStream_t st, const double* src, long long lds, int rows, const int* cols, int n,
                         double* dst, long long ldd);
