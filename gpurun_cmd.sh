@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_build.py tests/test_gpu_topk.py tests/test_gpu_projections.py -x -q > gpurun_out/g3_tests.log 2>&1; echo "rc=$?" >> gpurun_out/g3_tests.log
-timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_g3.log 2>&1
-tail -n 2 gpurun_out/g3_tests.log; grep -o '"value": [0-9.]*\|"select": [0-9.]*' gpurun_out/bench_g3.log | head -3
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+tail -n 3 gpurun_out/gpu_tests.log; tail -n 1 gpurun_out/smoke.log; grep -o '"value": [0-9.]*' gpurun_out/bench.log | head -3
