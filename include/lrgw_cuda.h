@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define LRGW_ABI_VERSION 1
+#define LRGW_ABI_VERSION 2
 
 enum lrgw_status {
   LRGW_OK = 0,
@@ -151,6 +151,7 @@ typedef struct {
   double delta_rel;  /* adaptive stopping rule (contour.hpp:313-320) */
   int max_nodes;     /* adaptive node cap (contour.hpp:31) */
   int zero_kernel;   /* 1: V = 0 (zero_coulomb) */
+  int n_e;           /* length of `energies` (>= n_v + n_c; contour.hpp:35-44) */
 } lrgw_build_params;
 
 /* The factored eps^-1 build, stages 1-5, from device-resident orbitals
@@ -158,6 +159,22 @@ typedef struct {
  * (ascending, n_v + n_c). Stage device times: lrgw_ctx_stage_ms. */
 int lrgw_build(lrgw_ctx ctx, const lrgw_build_params* prm, const double* phi_v, long long ldv,
                const double* phi_c, long long ldc, const double* energies, lrgw_eps* out);
+/* Build diagnostics and device pointers of a factored inverse. Pointers are
+ * owned by the handle (pvp and the selection / fit fields only for handles
+ * made by lrgw_build; otherwise NULL / -1). */
+typedef struct {
+  int n_r, n_mu;
+  double* theta;        /* n_r x n_mu, sorted-point column order       */
+  double* k;            /* n_mu x n_mu SMW core                        */
+  double* t;            /* n_mu x n_mu quadrature core T               */
+  double* pvp;          /* n_mu x n_mu Theta^T V Theta                 */
+  double min_margin;    /* smallest relative top-2 residual margin (d1 - d2) / d1 over the greedy steps */
+  int min_margin_step;  /* the step it occurred at                     */
+  int fit_path;         /* 0: fused Theta = L L_P^-1; 1: explicit Gram LU (isdf.hpp:143) */
+  double lp_diag_ratio; /* (max|L_P,ii| / min|L_P,ii|)^2, a lower bound on cond(G(P,P)) */
+  int select_blocks;    /* candidate blocks of the selection            */
+} lrgw_eps_info;
+int lrgw_eps_info_get(lrgw_eps e, lrgw_eps_info* out);
 /* Device pointers owned by the handle (n_r x n_mu Theta, n_mu^2 K and T). */
 int lrgw_eps_device_ptrs(lrgw_eps e, double** theta, double** k, double** t);
 /* eps^-1 applied to a device block: y = x + V Theta (K (Theta^T x)). */

@@ -389,3 +389,60 @@ def run_pipeline_json(config: dict) -> dict:
     n = ctypes.c_int(0)
     _check(lib().ref_run_pipeline_json(json.dumps(config).encode(), buf, cap, ctypes.byref(n)), "run_pipeline")
     return json.loads(buf.raw[:n.value].decode())
+
+
+# ---- stage-wise checkers for the large BASELINE configs (ref_shim.cpp) -----
+def fit_rows(a_rows, b_rows, a_mu, b_mu, threads=1):
+    """Rows of the reference fit (isdf.hpp:118-163): psi_a / psi_b at the rows
+    under test and at the sorted points. Bit-identical to those rows of
+    fit(a, b, pts). Returns (theta_rows, used_pinv)."""
+    a_rows, b_rows, a_mu, b_mu = _f(a_rows), _f(b_rows), _f(a_mu), _f(b_mu)
+    out = np.zeros((a_rows.shape[0], a_mu.shape[0]), order="F")
+    pinv = ctypes.c_int(0)
+    _check(lib().ref_fit_rows(_d(a_rows), _d(b_rows), a_rows.shape[0], _d(a_mu), _d(b_mu), a_mu.shape[0],
+                              a_rows.shape[1], b_rows.shape[1], threads, _d(out), ctypes.byref(pinv)),
+           "fit_auxiliary_basis (rows)")
+    return out, bool(pinv.value)
+
+
+def pvp_cols(p, dims, cell, cols, threads=1, want_vp=False):
+    """Columns `cols` of P^T (V P) (smw.hpp:61, before symmetrisation) and
+    optionally V P(:, cols) — the reference's apply_coulomb + matmul_tn."""
+    p = _f(p)
+    d = np.array(dims, dtype=np.int32)
+    c = np.array(cell, dtype=np.float64)
+    cols = np.ascontiguousarray(cols, dtype=np.int32)
+    out = np.zeros((p.shape[1], cols.size), order="F")
+    vp = np.zeros((p.shape[0], cols.size), order="F") if want_vp else None
+    _check(lib().ref_pvp_cols(_d(p), p.shape[0], p.shape[1], _i(d), _d(c), _i(cols), cols.size, threads, _d(out),
+                              _d(vp) if want_vp else None), "pvp columns")
+    return (out, vp) if want_vp else out
+
+
+def smw_from_pvp(t, pvp, check_eig=True, threads=1):
+    """assemble_K (smw.hpp:42-73) with P^T V P supplied."""
+    t, pvp = _f(t), _f(pvp)
+    k = np.zeros_like(t, order="F")
+    _check(lib().ref_smw_from_pvp(_d(t), _d(pvp), t.shape[0], 1 if check_eig else 0, threads, _d(k)),
+           "assemble_K")
+    return k
+
+
+def eps_apply_vp(p, k, vp, x):
+    """epsilon_inverse_apply (smw.hpp:97-103) with V P supplied."""
+    p, k, vp, x = _f(p), _f(k), _f(vp), _f(x)
+    y = np.zeros_like(x, order="F")
+    _check(lib().ref_eps_apply_vp(_d(p), _d(k), _d(vp), p.shape[0], p.shape[1], _d(x), x.shape[1], _d(y)),
+           "epsilon_inverse_apply")
+    return y
+
+
+def eps_apply_factored(p, k, dims, cell, x, threads=1):
+    """X + V (P (K (P^T X))): smw.hpp:101-102 with V applied last."""
+    p, k, x = _f(p), _f(k), _f(x)
+    d = np.array(dims, dtype=np.int32)
+    c = np.array(cell, dtype=np.float64)
+    y = np.zeros_like(x, order="F")
+    _check(lib().ref_eps_apply_factored(_d(p), _d(k), p.shape[0], p.shape[1], _i(d), _d(c), _d(x), x.shape[1],
+                                        threads, _d(y)), "epsilon_inverse_apply (factored)")
+    return y

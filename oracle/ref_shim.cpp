@@ -10,6 +10,7 @@
 // Every entry point returns an lrgw status code (same numbering as
 // include/lrgw_cuda.h) mapped 1:1 from the reference exception taxonomy
 // (errors.hpp:10-36, contour.hpp:92-96).
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -590,6 +591,178 @@ int ref_sym_eig_values(const double* a, int n, double* values) {
   return guarded([&] {
     SymEigResult r = sym_eig(from_ptr(a, n, n));
     for (int i = 0; i < n; ++i) values[i] = r.values[i];
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Stage-wise checkers at the large BASELINE configs. Each composes the
+// reference's own primitives in the reference's own order, restricted to the
+// rows / columns under test; every restricted quantity is separable, so the
+// outputs are bit-identical to the corresponding rows / columns of the full
+// reference call (matmul_nt / hadamard / lu_solve_factored / matmul_tn act
+// row- or column-wise). parallel_for (parallel.hpp:11-29) spreads the
+// independent columns over host threads.
+// ---------------------------------------------------------------------------
+
+// fit_auxiliary_basis (isdf.hpp:118-163) for selected rows: a_rows / b_rows
+// (nrows x n1 / n2) are psi_a / psi_b at the rows under test, a_mu / b_mu
+// (n_mu x n1 / n2) at the sorted points. theta_rows (nrows x n_mu) = those
+// rows of the reference P (LU path, or the pseudo-inverse fallback on a
+// singular Gram exactly as isdf.hpp:144-161).
+int ref_fit_rows(const double* a_rows, const double* b_rows, int nrows, const double* a_mu,
+                 const double* b_mu, int n_mu, int n1, int n2, int threads, double* theta_rows,
+                 int* used_pinv) {
+  return guarded([&] {
+    Matrix am = from_ptr(a_mu, n_mu, n1), bm = from_ptr(b_mu, n_mu, n2);
+    Matrix gram = hadamard(matmul_nt(am, am), matmul_nt(bm, bm));  // = rows_at(lhs, points)
+    symmetrize(gram);
+    Matrix ar = from_ptr(a_rows, nrows, n1), br = from_ptr(b_rows, nrows, n2);
+    if (used_pinv) *used_pinv = 0;
+    LuFactors f;
+    bool singular = false;
+    try {
+      f = lu_factor(gram);
+    } catch (const singular_matrix&) {
+      singular = true;
+    }
+    Matrix pinv;
+    if (singular) {  // isdf.hpp:144-161
+      if (used_pinv) *used_pinv = 1;
+      SymEigResult ev = sym_eig(gram);
+      double lam_max = 0.0;
+      for (double v : ev.values) lam_max = std::max(lam_max, std::abs(v));
+      if (lam_max <= 0.0) throw numeric_error("fit_auxiliary_basis: degenerate Gram matrix");
+      std::vector<double> inv(ev.values.size(), 0.0);
+      int kept = 0;
+      for (std::size_t i = 0; i < ev.values.size(); ++i)
+        if (std::abs(ev.values[i]) > 1e-12 * lam_max) {
+          inv[i] = 1.0 / ev.values[i];
+          ++kept;
+        }
+      if (kept == 0) throw numeric_error("fit_auxiliary_basis: degenerate Gram matrix");
+      pinv = matmul_nt(scale_cols(ev.q, inv), ev.q);
+    }
+    // row blocks: lhs = (A A_mu^T) o (B B_mu^T) and its solve, per block
+    Matrix out(nrows, n_mu);
+    const int nb = std::max(1, std::min(threads, nrows));
+    parallel_for(nb, nb, [&](int t) {
+      const int lo = static_cast<int>(static_cast<long long>(nrows) * t / nb);
+      const int hi = static_cast<int>(static_cast<long long>(nrows) * (t + 1) / nb);
+      if (hi <= lo) return;
+      std::vector<int> idx(hi - lo);
+      for (int i = lo; i < hi; ++i) idx[i - lo] = i;
+      Matrix lhs = hadamard(matmul_nt(rows_at(ar, idx), am), matmul_nt(rows_at(br, idx), bm));
+      Matrix pb = singular ? matmul(lhs, pinv) : transpose(lu_solve_factored(f, transpose(lhs)));
+      for (int j = 0; j < n_mu; ++j)
+        for (int i = lo; i < hi; ++i) out(i, j) = pb(i - lo, j);
+    });
+    to_ptr(out, theta_rows);
+  });
+}
+
+// Columns `cols` of pvp = P^T (V P) before symmetrisation (smw.hpp:61):
+// apply_coulomb on the selected columns (model.hpp:208-223, threaded), then
+// matmul_tn (matrix.hpp:88-102) per column block. vp_cols (optional,
+// n_r x ncols) returns V P(:, cols).
+int ref_pvp_cols(const double* p, int n_r, int n_mu, const int* dims, const double* cell,
+                 const int* cols, int ncols, int threads, double* out, double* vp_cols) {
+  return guarded([&] {
+    Grid g = make_grid(dims, cell);
+    if (g.n_r() != n_r) throw invalid_input("shim: grid / N_r mismatch");
+    CoulombOperator v = build_coulomb(g, CoulombMode::reciprocal_diagonal);
+    Matrix pm = from_ptr(p, n_r, n_mu);
+    Matrix sel(n_r, ncols);
+    for (int j = 0; j < ncols; ++j) {
+      if (cols[j] < 0 || cols[j] >= n_mu) throw invalid_input("shim: column out of range");
+      std::copy(pm.col(cols[j]), pm.col(cols[j]) + n_r, sel.col(j));
+    }
+    Matrix vp = apply_coulomb(v, sel, threads);
+    Matrix c(n_mu, ncols);
+    const int nb = std::max(1, std::min(threads, ncols));
+    parallel_for(nb, nb, [&](int t) {
+      const int lo = static_cast<int>(static_cast<long long>(ncols) * t / nb);
+      const int hi = static_cast<int>(static_cast<long long>(ncols) * (t + 1) / nb);
+      if (hi <= lo) return;
+      Matrix cb = matmul_tn(pm, cols_block(vp, lo, hi - lo));
+      for (int j = 0; j < hi - lo; ++j) std::copy(cb.col(j), cb.col(j) + n_mu, c.col(lo + j));
+    });
+    to_ptr(c, out);
+    if (vp_cols) to_ptr(vp, vp_cols);
+  });
+}
+
+// assemble_K (smw.hpp:42-73) with pvp = P^T V P supplied (unsymmetrised):
+// the sym_eig definiteness check, lu_solve(T, I/2), the three symmetrisations
+// and lu_invert, in the reference's order.
+int ref_smw_from_pvp(const double* t, const double* pvp, int n_mu, int check_eig, int threads, double* k) {
+  return guarded([&] {
+    // lu_solve(A, B) = lu_solve_factored(lu_factor(A), B), column by column:
+    // the right-hand sides are spread over threads (bit-identical result)
+    auto solve = [&](const Matrix& a, const Matrix& b) {
+      LuFactors f = lu_factor(a);
+      Matrix x(b.rows(), b.cols());
+      const int nb = std::max(1, std::min(threads, b.cols()));
+      parallel_for(nb, nb, [&](int q) {
+        const int lo = static_cast<int>(static_cast<long long>(b.cols()) * q / nb);
+        const int hi = static_cast<int>(static_cast<long long>(b.cols()) * (q + 1) / nb);
+        if (hi <= lo) return;
+        Matrix xb = lu_solve_factored(f, cols_block(b, lo, hi - lo));
+        for (int j = 0; j < hi - lo; ++j) std::copy(xb.col(j), xb.col(j) + b.rows(), x.col(lo + j));
+      });
+      return x;
+    };
+    Matrix tm = from_ptr(t, n_mu, n_mu);
+    if (check_eig) {
+      SymEigResult ev = sym_eig(tm);
+      if (!(ev.values.back() < 0.0))
+        throw numeric_error("assemble_K: T is not negative definite (gapless or rank-deficient input)");
+    }
+    Matrix half_t_inv;
+    try {
+      half_t_inv = solve(tm, 0.5 * Matrix::identity(n_mu));
+    } catch (const singular_matrix& e) {
+      throw singular_matrix("assemble_K: T singular", e.pivot_index);
+    }
+    symmetrize(half_t_inv);
+    Matrix pv = from_ptr(pvp, n_mu, n_mu);
+    symmetrize(pv);
+    Matrix km;
+    try {
+      km = solve(half_t_inv - pv, Matrix::identity(n_mu));  // lu_invert (linalg.hpp:181-183)
+    } catch (const singular_matrix& e) {
+      throw singular_matrix("assemble_K: middle matrix singular", e.pivot_index);
+    }
+    symmetrize(km);
+    to_ptr(km, k);
+  });
+}
+
+// epsilon_inverse_apply (smw.hpp:97-103) given P, K and VP = V P:
+// Y = X + VP (K (P^T X)).
+int ref_eps_apply_vp(const double* p, const double* k, const double* vp, int n_r, int n_mu,
+                     const double* x, int m, double* y) {
+  return guarded([&] {
+    EpsilonInverseLowRank e;
+    e.p_vc = from_ptr(p, n_r, n_mu);
+    e.k = from_ptr(k, n_mu, n_mu);
+    e.vp = from_ptr(vp, n_r, n_mu);
+    to_ptr(epsilon_inverse_apply(e, from_ptr(x, n_r, m)), y);
+  });
+}
+
+// The same operator with V applied last: Y = X + V (P (K (P^T X))) — equal to
+// smw.hpp:101-102 up to rounding (V is linear), for sizes where V P (all N_mu
+// columns through the dense DFT) is out of reach on the host.
+int ref_eps_apply_factored(const double* p, const double* k, int n_r, int n_mu, const int* dims,
+                           const double* cell, const double* x, int m, int threads, double* y) {
+  return guarded([&] {
+    Grid g = make_grid(dims, cell);
+    if (g.n_r() != n_r) throw invalid_input("shim: grid / N_r mismatch");
+    CoulombOperator v = build_coulomb(g, CoulombMode::reciprocal_diagonal);
+    Matrix pm = from_ptr(p, n_r, n_mu);
+    Matrix xm = from_ptr(x, n_r, m);
+    Matrix z = matmul(pm, matmul(from_ptr(k, n_mu, n_mu), matmul_tn(pm, xm)));
+    to_ptr(xm + apply_coulomb(v, z, threads), y);
   });
 }
 

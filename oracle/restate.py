@@ -191,6 +191,24 @@ def fit_auxiliary_basis(a: np.ndarray, b: np.ndarray, pts) -> np.ndarray:
         return lhs @ pinv
 
 
+def fit_rows(a_rows, b_rows, a_mu, b_mu) -> np.ndarray:
+    """Rows of fit_auxiliary_basis (isdf.hpp:118-163) from the orbitals at
+    those rows and at the sorted points (the fit is row-separable); LAPACK
+    LU, for sizes where the reference's serial LU is out of reach."""
+    gram = symmetrize((a_mu @ a_mu.T) * (b_mu @ b_mu.T))
+    lhs = (a_rows @ a_mu.T) * (b_rows @ b_mu.T)
+    try:
+        return lu_solve(gram, lhs.T).T
+    except SingularMatrix:
+        w, q = sym_eig(gram)
+        lam_max = float(np.max(np.abs(w))) if w.size else 0.0
+        keep = np.abs(w) > 1e-12 * lam_max
+        if lam_max <= 0.0 or not np.any(keep):
+            raise NumericError("fit_auxiliary_basis: degenerate Gram matrix")
+        inv = np.where(keep, 1.0 / np.where(keep, w, 1.0), 0.0)
+        return lhs @ ((q * inv) @ q.T)
+
+
 def isdf_error(a, b, pts, theta) -> float:
     """isdf.hpp:195-202 — ||M - P C||_F / ||M||_F (small sizes only)."""
     m = np.einsum("ri,rj->rji", a, b).reshape(a.shape[0], -1)

@@ -46,11 +46,17 @@ int oracle_select_points(const double* a, const double* b, int n_r, int n1,
   double* d0 = (double*)malloc(sizeof(double) * n_r);
   int* perm = (int*)malloc(sizeof(int) * n_r);
   int* pos = (int*)malloc(sizeof(int) * n_r);
-  double* L = (double*)malloc(sizeof(double) * (size_t)n_r * (steps > 0 ? steps : 1));
+  /* row-major copies: each grid row's orbital values and L row are contiguous
+   * (the same sums in the same order as a column-major sweep, just cache-
+   * friendly on the host) */
+  const int ldl = steps > 0 ? steps : 1;
+  double* L = (double*)malloc(sizeof(double) * (size_t)n_r * ldl);
+  double* ar = (double*)malloc(sizeof(double) * (size_t)n_r * n1);
+  double* br = (double*)malloc(sizeof(double) * (size_t)n_r * n2);
   double* ap = (double*)malloc(sizeof(double) * n1);
   double* bp = (double*)malloc(sizeof(double) * n2);
-  if (!d || !d0 || !perm || !pos || !L || !ap || !bp) {
-    free(d); free(d0); free(perm); free(pos); free(L); free(ap); free(bp);
+  if (!d || !d0 || !perm || !pos || !L || !ap || !bp || !ar || !br) {
+    free(d); free(d0); free(perm); free(pos); free(L); free(ap); free(bp); free(ar); free(br);
     return 9;
   }
   int events = 0;
@@ -58,8 +64,12 @@ int oracle_select_points(const double* a, const double* b, int n_r, int n1,
 #pragma omp parallel for schedule(static)
   for (int g = 0; g < n_r; ++g) {
     double sa = 0.0, sb = 0.0;
-    for (int i = 0; i < n1; ++i) sa += a[(size_t)i * n_r + g] * a[(size_t)i * n_r + g];
-    for (int j = 0; j < n2; ++j) sb += b[(size_t)j * n_r + g] * b[(size_t)j * n_r + g];
+    double* arg = ar + (size_t)g * n1;
+    double* brg = br + (size_t)g * n2;
+    for (int i = 0; i < n1; ++i) arg[i] = a[(size_t)i * n_r + g];
+    for (int j = 0; j < n2; ++j) brg[j] = b[(size_t)j * n_r + g];
+    for (int i = 0; i < n1; ++i) sa += arg[i] * arg[i];
+    for (int j = 0; j < n2; ++j) sb += brg[j] * brg[j];
     d[g] = d0[g] = sa * sb;
     perm[g] = g;
     pos[g] = g;
@@ -90,27 +100,30 @@ int oracle_select_points(const double* a, const double* b, int n_r, int n1,
     const int gp = perm[s];
     if (pivots_in_order) pivots_in_order[s] = gp;
     const double dp = d[gp];
-    double* Ls = L + (size_t)s * n_r;
     if (!(dp > 0.0)) {
       /* exhausted: Householder with alpha == 0 leaves the trailing columns
        * untouched (linalg.hpp:60-61) */
-      memset(Ls, 0, sizeof(double) * n_r);
+      for (int g = 0; g < n_r; ++g) L[(size_t)g * ldl + s] = 0.0;
       continue;
     }
     const double inv = 1.0 / sqrt(dp);
-    for (int i = 0; i < n1; ++i) ap[i] = a[(size_t)i * n_r + gp];
-    for (int j = 0; j < n2; ++j) bp[j] = b[(size_t)j * n_r + gp];
+    for (int i = 0; i < n1; ++i) ap[i] = ar[(size_t)gp * n1 + i];
+    for (int j = 0; j < n2; ++j) bp[j] = br[(size_t)gp * n2 + j];
+    const double* Lp = L + (size_t)gp * ldl;
     int ev = 0;
 #pragma omp parallel for schedule(static) reduction(+ : ev)
     for (int g = 0; g < n_r; ++g) {
-      if (pos[g] < s) { Ls[g] = 0.0; continue; }
+      double* Lg = L + (size_t)g * ldl;
+      if (pos[g] < s) { Lg[s] = 0.0; continue; }
+      const double* arg = ar + (size_t)g * n1;
+      const double* brg = br + (size_t)g * n2;
       double sa = 0.0, sb = 0.0;
-      for (int i = 0; i < n1; ++i) sa += a[(size_t)i * n_r + g] * ap[i];
-      for (int j = 0; j < n2; ++j) sb += b[(size_t)j * n_r + g] * bp[j];
+      for (int i = 0; i < n1; ++i) sa += arg[i] * ap[i];
+      for (int j = 0; j < n2; ++j) sb += brg[j] * bp[j];
       double c = sa * sb;
-      for (int t = 0; t < s; ++t) c -= L[(size_t)t * n_r + g] * L[(size_t)t * n_r + gp];
+      for (int t = 0; t < s; ++t) c -= Lg[t] * Lp[t];
       double l = (g == gp) ? sqrt(dp) : c * inv;
-      Ls[g] = l;
+      Lg[s] = l;
       if (g != gp) {
         d[g] -= l * l;
         if (d[g] < 1e-12 * d0[g] || d[g] < 0.0) ++ev;
@@ -122,6 +135,6 @@ int oracle_select_points(const double* a, const double* b, int n_r, int n1,
   for (int i = 0; i < n_mu; ++i) pts[i] = perm[i];
   qsort(pts, (size_t)n_mu, sizeof(int), cmp_int);
   if (recompute_events) *recompute_events = events;
-  free(d); free(d0); free(perm); free(pos); free(L); free(ap); free(bp);
+  free(d); free(d0); free(perm); free(pos); free(L); free(ap); free(bp); free(ar); free(br);
   return 0;
 }

@@ -31,7 +31,17 @@ class BuildParams(ctypes.Structure):
         ("dims", ctypes.c_int * 3), ("cell", ctypes.c_double * 3),
         ("k_mu", ctypes.c_double), ("n_lambda", ctypes.c_int),
         ("delta_rel", ctypes.c_double), ("max_nodes", ctypes.c_int),
-        ("zero_kernel", ctypes.c_int),
+        ("zero_kernel", ctypes.c_int), ("n_e", ctypes.c_int),
+    ]
+
+
+class EpsInfo(ctypes.Structure):
+    """lrgw_eps_info (include/lrgw_cuda.h)."""
+    _fields_ = [
+        ("n_r", ctypes.c_int), ("n_mu", ctypes.c_int),
+        ("theta", ctypes.c_void_p), ("k", ctypes.c_void_p), ("t", ctypes.c_void_p), ("pvp", ctypes.c_void_p),
+        ("min_margin", ctypes.c_double), ("min_margin_step", ctypes.c_int), ("fit_path", ctypes.c_int),
+        ("lp_diag_ratio", ctypes.c_double), ("select_blocks", ctypes.c_int),
     ]
 
 
@@ -93,6 +103,7 @@ _SIGS = {
     "lrgw_eps_destroy": (ctypes.c_int, [eps_t]),
     "lrgw_build": (ctypes.c_int, [ctx_t, ctypes.POINTER(BuildParams), ctypes.c_void_p, c_ll, ctypes.c_void_p,
                                   c_ll, c_double_p, ctypes.POINTER(eps_t)]),
+    "lrgw_eps_info_get": (ctypes.c_int, [eps_t, ctypes.POINTER(EpsInfo)]),
     "lrgw_eps_device_ptrs": (ctypes.c_int, [eps_t, ctypes.POINTER(ctypes.c_void_p),
                                             ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]),
     "lrgw_eps_apply_dev": (ctypes.c_int, [ctx_t, eps_t, ctypes.c_void_p, c_ll, ctypes.c_int, ctypes.c_void_p,

@@ -103,7 +103,14 @@ struct lrgw_eps_s {
   double* theta = nullptr;
   double* k = nullptr;
   double* t = nullptr;
+  double* pvp = nullptr;  // Theta^T V Theta (lrgw_build only)
   std::vector<int32_t> pts;
+  // build diagnostics (lrgw_build only; lrgw_eps_info)
+  double min_margin = -1.0;
+  int min_margin_step = -1;
+  int fit_path = -1;
+  double lp_diag_ratio = 0.0;
+  int select_blocks = 0;
 };
 
 namespace {
@@ -687,6 +694,8 @@ struct SelectKeep {
   DBuf L;
   std::vector<int> order;
   int steps = 0;
+  int blocks = 0;           // candidate blocks (one host sync each)
+  int min_margin_step = -1; // step of the smallest top-2 margin (when margins are requested)
 };
 
 std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int n1, const double* b,
@@ -763,6 +772,7 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
       ck(fe, "dgemm_tall_downdate");
     }
     k += nb;
+    if (keep) ++keep->blocks;
   }
   std::vector<int32_t> pts(n_mu);
   download(c, pts.data(), perm.p, sizeof(int) * n_mu);
@@ -777,8 +787,14 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
     std::vector<double> mg(std::max(steps, 1));
     download(c, mg.data(), margin.p, sizeof(double) * std::max(steps, 1));
     double mn = 1.0;
-    for (int i = 0; i < steps; ++i) mn = std::min(mn, mg[i]);
+    int at = -1;
+    for (int i = 0; i < steps; ++i)
+      if (mg[i] < mn) {
+        mn = mg[i];
+        at = i;
+      }
     *min_margin = mn;
+    if (keep) keep->min_margin_step = at;
   }
   return pts;
 }
@@ -886,7 +902,7 @@ void fit_impl(lrgw_ctx c, const double* a, long long lda, int n1, const double* 
 // Returns false (caller falls back to the explicit path) when L_P has a pivot
 // below the LU singularity threshold of linalg.hpp:128, 137.
 bool fused_fit(lrgw_ctx c, const SelectKeep& keep, int n_r, const std::vector<int32_t>& pts_sorted, int n_mu,
-               double* theta, long long ldt) {
+               double* theta, long long ldt, double* diag_ratio) {
   if (keep.steps != n_mu) return false;
   std::vector<int> order(keep.order.begin(), keep.order.end());
   DBuf dorder = upload_i(c, order.data(), n_mu);
@@ -899,8 +915,14 @@ bool fused_fit(lrgw_ctx c, const SelectKeep& keep, int n_r, const std::vector<in
                        n_mu, cudaMemcpyDeviceToHost, c->stream),
      "D2H diag");
   ck(cudaStreamSynchronize(c->stream), "sync");
-  double gmax = 0.0;
-  for (double v : diag) gmax = std::max(gmax, v * v);  // G(p_i, p_i) >= L_ii^2; the LU scale
+  double gmax = 0.0, dmin = HUGE_VAL, dmax = 0.0;
+  for (double v : diag) {
+    gmax = std::max(gmax, v * v);  // G(p_i, p_i) >= L_ii^2; the LU scale
+    dmin = std::min(dmin, std::abs(v));
+    dmax = std::max(dmax, std::abs(v));
+  }
+  // (max |L_ii| / min |L_ii|)^2 is a lower bound on cond(G(P, P)) = cond(L_P)^2
+  if (diag_ratio) *diag_ratio = dmin > 0.0 ? (dmax / dmin) * (dmax / dmin) : HUGE_VAL;
   const double tiny = 1e-14 * (gmax > 0.0 ? gmax : 1.0);
   for (double v : diag)
     if (!(v * v >= tiny)) return false;
@@ -1085,14 +1107,14 @@ int lrgw_ctx_destroy(lrgw_ctx c) {
   {
     std::lock_guard<std::mutex> lk(c->mem_mu);
     for (lrgw_eps_s* e : c->live_eps) {  // orphan the handles, free their buffers
-      for (double* p : {e->theta, e->k, e->t}) {
+      for (double* p : {e->theta, e->k, e->t, e->pvp}) {
         auto it = c->mem_live.find(p);
         if (it != c->mem_live.end()) {
           cudaFree(p);
           c->mem_live.erase(it);
         }
       }
-      e->theta = e->k = e->t = nullptr;
+      e->theta = e->k = e->t = e->pvp = nullptr;
       e->ctx = nullptr;
     }
     c->live_eps.clear();
@@ -1470,10 +1492,27 @@ int lrgw_eps_destroy(lrgw_eps e) {
     ctx_free(c, e->theta);
     ctx_free(c, e->k);
     ctx_free(c, e->t);
+    ctx_free(c, e->pvp);
     std::lock_guard<std::mutex> lk(c->mem_mu);
     c->live_eps.erase(e);
   }
   delete e;
+  return LRGW_OK;
+}
+
+int lrgw_eps_info_get(lrgw_eps e, lrgw_eps_info* out) {
+  if (!e || !out) return LRGW_ERR_INVALID_INPUT;
+  out->n_r = e->n_r;
+  out->n_mu = e->n_mu;
+  out->theta = e->theta;
+  out->k = e->k;
+  out->t = e->t;
+  out->pvp = e->pvp;
+  out->min_margin = e->min_margin;
+  out->min_margin_step = e->min_margin_step;
+  out->fit_path = e->fit_path;
+  out->lp_diag_ratio = e->lp_diag_ratio;
+  out->select_blocks = e->select_blocks;
   return LRGW_OK;
 }
 
@@ -1495,10 +1534,20 @@ int lrgw_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, lo
     const int n_r = P.n_r, n_v = P.n_v, n_c = P.n_c;
     if ((long long)P.dims[0] * P.dims[1] * P.dims[2] != n_r) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: grid / N_r mismatch");
     if (n_v < 1 || n_c < 1) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: need n_v >= 1 and n_c >= 1");
+    if (P.n_e < n_v + n_c) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: energies must hold n_v + n_c values");
+    if (!phi_v || !phi_c || !energies) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: null orbital / energy pointer");
+    if (ldv < n_r || ldc < n_r) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: leading dimension below N_r");
+    for (const double* ph : {phi_v, phi_c}) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, ph) != cudaSuccess || at.type != cudaMemoryTypeDevice || at.device != c->device) {
+        cudaGetLastError();
+        fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: orbitals must be device memory on the context's GPU");
+      }
+    }
     int n_mu = 0;
     if (lrgw_num_aux(P.k_mu, n_v, n_c, &n_mu) != LRGW_OK) fail(LRGW_ERR_INVALID_INPUT, "num_aux: k_mu must be > 0");
     n_mu = std::clamp(n_mu, 1, n_r);
-    const int n_e = n_v + n_c;
+    const int n_e = P.n_e;
     lrgw_host::Spec spec;
     host_status(lrgw_host::elliptic_params(energies, n_e, n_v, n_c, P.delta_rel > 0 ? P.delta_rel : 1e-7,
                                            P.max_nodes > 0 ? P.max_nodes : 1025, &spec),
@@ -1515,12 +1564,14 @@ int lrgw_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, lo
     mark(c, 0);
     // stage 1
     SelectKeep keep;
-    std::vector<int32_t> pts = select_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, n_mu, nullptr, &keep);
+    double min_margin = -1.0;  // smallest relative top-2 residual margin over all steps (linalg.hpp:45-47)
+    std::vector<int32_t> pts = select_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, n_mu, &min_margin, &keep);
     mark(c, 1);
     // stage 2: fused fit from the selection's factor (explicit path otherwise)
     DBuf theta = dalloc(c, (size_t)n_r * n_mu);
     mark(c, 2);  // FIT_LHS is empty on the fused path (lhs lives in L)
-    const bool fused = fused_fit(c, keep, n_r, pts, n_mu, theta.d(), n_r);
+    double lp_ratio = 0.0;
+    const bool fused = fused_fit(c, keep, n_r, pts, n_mu, theta.d(), n_r, &lp_ratio);
     keep.L.release();
     if (!fused) {  // explicit path re-marks its own lhs / solve boundaries
       fit_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, pts.data(), n_mu, theta.d(), n_r);
@@ -1591,7 +1642,13 @@ int lrgw_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, lo
     e->theta = static_cast<double*>(theta.take());
     e->k = static_cast<double*>(k.take());
     e->t = static_cast<double*>(t.take());
+    e->pvp = static_cast<double*>(pvp.take());
     e->pts = pts;
+    e->min_margin = min_margin;
+    e->min_margin_step = keep.min_margin_step;
+    e->fit_path = fused ? 0 : 1;
+    e->lp_diag_ratio = lp_ratio;
+    e->select_blocks = keep.blocks;
     *out = e;
   });
 }

@@ -465,6 +465,16 @@ class EpsilonInverseLowRank:
                self.ctx.handle, "eps_get")
         return pts
 
+    def info(self) -> dict:
+        """Build diagnostics (lrgw_eps_info): the smallest relative top-2
+        pivot margin of the greedy selection and its step, the fit path
+        (0 fused L L_P^-1, 1 explicit Gram LU), the lower bound
+        (max|L_ii| / min|L_ii|)^2 on cond(G(P, P)), the candidate-block count,
+        and the device pointers (theta, k, t, pvp)."""
+        inf = L.EpsInfo()
+        _check(self.ctx._lib.lrgw_eps_info_get(self.handle, ctypes.byref(inf)), self.ctx.handle, "eps_info")
+        return {f: getattr(inf, f) for f, _ in L.EpsInfo._fields_}
+
     def device_ptrs(self):
         th, k, t = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
         self.ctx._lib.lrgw_eps_device_ptrs(self.handle, ctypes.byref(th), ctypes.byref(k), ctypes.byref(t))
@@ -698,11 +708,21 @@ def build(phi_v, phi_c, energies, dims, cell, k_mu: float = 8.0, n_lambda: int =
     tensors, N_r x N_v and N_r x N_c) and host energies: point selection,
     Theta fit, Cauchy quadrature core, G-space Theta^T V Theta, SMW core K."""
     c = _ctx(ctx)
+    for name, t in (("phi_v", phi_v), ("phi_c", phi_c)):
+        if not getattr(t, "is_cuda", False) or t.dim() != 2:
+            raise InvalidInput(f"build: {name} must be a 2-D CUDA tensor")
+        if t.device.index != c.device:
+            raise InvalidInput(f"build: {name} is on cuda:{t.device.index}, the context on cuda:{c.device}")
+    if phi_c.shape[0] != phi_v.shape[0]:
+        raise InvalidInput("build: phi_v and phi_c must have the same number of grid rows")
     pv, ldv = _dev_ptr_cm(phi_v)
     pc, ldc = _dev_ptr_cm(phi_c)
     e = np.ascontiguousarray(energies, dtype=np.float64)
+    if e.ndim != 1 or e.size != phi_v.shape[1] + phi_c.shape[1]:
+        raise InvalidInput("build: energies must hold exactly N_v + N_c values")
     prm = L.BuildParams()
     prm.n_r, prm.n_v, prm.n_c = phi_v.shape[0], phi_v.shape[1], phi_c.shape[1]
+    prm.n_e = e.size
     prm.dims[:] = [int(x) for x in dims]
     prm.cell[:] = [float(x) for x in cell]
     prm.k_mu = float(k_mu)

@@ -17,7 +17,7 @@ def test_exports_every_declared_symbol():
     assert len(declared) >= 40
     missing = [s for s in declared if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.lrgw_abi_version() == 1
+    assert lib.lrgw_abi_version() == 2
 
 
 def test_num_aux_matches_oracle():

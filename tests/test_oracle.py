@@ -261,3 +261,45 @@ def test_quasiparticle_kats(ref):
         R.quasiparticle_energies(e, np.zeros(4), np.zeros(3))
     with pytest.raises(R.InvalidInput):
         ref.quasiparticle(e, np.zeros(4), np.zeros(3))
+
+
+# ---- the stage-wise checkers used at the large configs ----------------------
+
+@pytest.mark.parametrize("name", ["si8shaped_s1", "acc_s3", "wide_s3"])
+def test_stagewise_checkers_equal_full_reference_calls(ref, name):
+    """ref.fit_rows / pvp_cols / smw_from_pvp / eps_apply_vp (the large-config
+    checkers of tests/test_gpu_configs.py) are bit-identical to the rows /
+    columns of the reference's own fit_auxiliary_basis, assemble_K and
+    build_epsilon_inverse + epsilon_inverse_apply (isdf.hpp:118-163,
+    smw.hpp:42-103) — they only restrict and parallelise separable work."""
+    g = np.load(os.path.join(GOLDEN, name + ".npz"))
+    psi, nv = g["psi"], int(g["n_v"])
+    a, b, pts = psi[:, :nv], psi[:, nv:], g["pts"]
+    dims, cell = tuple(int(x) for x in g["dims"]), tuple(float(x) for x in g["cell"])
+    th = ref.fit(a, b, pts)
+    rows = np.sort(np.random.default_rng(0).choice(psi.shape[0], psi.shape[0] // 3, replace=False))
+    th_rows, pinv = ref.fit_rows(a[rows], b[rows], a[pts], b[pts], threads=3)
+    assert np.array_equal(th_rows, th[rows])
+    t = g["t_fixed"]
+    x = g["x"]
+    y, k, vp = ref.build_and_apply(t, th, dims, cell, x, threads=2, want_vp=True)
+    pvp, vpc = ref.pvp_cols(th, dims, cell, np.arange(th.shape[1]), threads=3, want_vp=True)
+    assert np.array_equal(vpc, vp)
+    k2 = ref.smw_from_pvp(t, pvp, threads=4)
+    assert np.array_equal(k2, k)
+    assert np.array_equal(ref.eps_apply_vp(th, k2, vpc, x), y)
+    assert rel(ref.eps_apply_factored(th, k2, dims, cell, x, threads=2), y) <= 1e-13
+    cols = np.array([3, 0, th.shape[1] - 1], dtype=np.int32)
+    assert np.array_equal(ref.pvp_cols(th, dims, cell, cols, threads=2), pvp[:, cols])
+
+
+def test_select_oracle_layout_independent():
+    """oracle/select.c on row-major copies gives the same pivots, order and
+    margins on a transposed-storage input (the sums run in one fixed order)."""
+    rng = np.random.default_rng(5)
+    q = np.linalg.qr(rng.standard_normal((3000, 24)))[0]
+    a, b = q[:, :12], q[:, 12:]
+    p1, d1 = R.select_points(np.asfortranarray(a), np.asfortranarray(b), 64, return_diag=True)
+    p2, d2 = R.select_points(np.ascontiguousarray(a), np.ascontiguousarray(b), 64, return_diag=True)
+    assert np.array_equal(p1, p2) and np.array_equal(d1["margins"], d2["margins"])
+    assert np.array_equal(d1["order"], d2["order"])
