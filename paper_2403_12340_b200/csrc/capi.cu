@@ -36,84 +36,12 @@ void count_launches(int n) { g_launches += n; }
 
 using namespace lrgw_dev;
 
-namespace {
+#include "internal.h"
 
-struct Fail {
-  int code;
-  std::string msg;
-  int pivot;
-};
+using namespace lrgw_impl;
 
-[[noreturn]] void fail(int code, const std::string& msg, int pivot = -1) { throw Fail{code, msg, pivot}; }
 
-void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) fail(LRGW_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
-void ckf(cufftResult r, const char* what) {
-  if (r != CUFFT_SUCCESS) fail(LRGW_ERR_CUDA, std::string(what) + ": cufft error " + std::to_string((int)r));
-}
-void cks(cusolverStatus_t r, const char* what) {
-  if (r != CUSOLVER_STATUS_SUCCESS)
-    fail(LRGW_ERR_CUDA, std::string(what) + ": cusolver error " + std::to_string((int)r));
-}
-void host_status(int st, const char* what) {
-  if (st != lrgw_host::kOk) fail(st, what);
-}
-
-}  // namespace
-
-struct lrgw_ctx_s {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  cudaStream_t own_stream = nullptr;
-  int sm_count = 148;
-  cusolverDnHandle_t solver = nullptr;
-  std::map<std::tuple<int, int, int, int, long long, long long, int>, cufftHandle> plans;
-  std::string err;
-  int pivot = -1;
-  double stage_ms[LRGW_NUM_STAGES] = {};
-  cudaEvent_t ev[LRGW_NUM_STAGES + 1] = {};
-  cudaEvent_t ev_quad[2] = {};  // around the K3 kernel (timing builds only)
-  bool quad_timed = false;
-  bool timing = false;  // record stage events (lrgw_build only)
-  long long launches0 = 0;
-  int select_batch = 128;
-  // Device-memory cache of this context: freed blocks are kept (by size) and
-  // handed out again to later requests on the context's stream. A build
-  // repeats the same sizes every call, so from the second call on no
-  // allocation reaches the driver (cudaMallocAsync pools fragment under the
-  // 0.1-1 GB blocks of a build and then grow or trim, stalling the host for
-  // milliseconds).
-  std::mutex mem_mu;
-  std::multimap<size_t, void*> mem_free;
-  std::unordered_map<void*, size_t> mem_live;
-  size_t mem_cached = 0;
-  // Factored-inverse handles created on this context: destroying the context
-  // frees their device buffers and orphans them (lrgw_eps_destroy then only
-  // deletes the handle), so handles may outlive their context safely.
-  std::set<struct lrgw_eps_s*> live_eps;
-};
-
-struct lrgw_eps_s {
-  lrgw_ctx ctx = nullptr;
-  int n_r = 0, n_mu = 0;
-  int dims[3] = {0, 0, 0};
-  double cell[3] = {0, 0, 0};
-  int zero = 0;
-  double* theta = nullptr;
-  double* k = nullptr;
-  double* t = nullptr;
-  double* pvp = nullptr;  // Theta^T V Theta (lrgw_build only)
-  std::vector<int32_t> pts;
-  // build diagnostics (lrgw_build only; lrgw_eps_info)
-  double min_margin = -1.0;
-  int min_margin_step = -1;
-  int fit_path = -1;
-  double lp_diag_ratio = 0.0;
-  int select_blocks = 0;
-};
-
-namespace {
+namespace lrgw_impl {
 
 void release_cached(lrgw_ctx c) {  // caller holds mem_mu
   if (c->mem_free.empty()) return;
@@ -166,42 +94,7 @@ void ctx_free(lrgw_ctx c, void* p) {
   c->mem_live.erase(it);
 }
 
-// Device buffer from the context cache (returned on scope exit).
-struct DBuf {
-  lrgw_ctx ctx = nullptr;
-  void* p = nullptr;
-  size_t bytes = 0;
-  DBuf() = default;
-  DBuf(lrgw_ctx c, size_t b) : ctx(c), bytes(b) {
-    if (b) p = ctx_alloc(c, b);
-  }
-  DBuf(const DBuf&) = delete;
-  DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : ctx(o.ctx), p(o.p), bytes(o.bytes) { o.p = nullptr; }
-  DBuf& operator=(DBuf&& o) noexcept {
-    release();
-    ctx = o.ctx;
-    p = o.p;
-    bytes = o.bytes;
-    o.p = nullptr;
-    return *this;
-  }
-  ~DBuf() { release(); }
-  void release() {
-    if (p) ctx_free(ctx, p);
-    p = nullptr;
-  }
-  double* d() const { return static_cast<double*>(p); }
-  int* i() const { return static_cast<int*>(p); }
-  void* take() {
-    void* q = p;
-    p = nullptr;
-    return q;
-  }
-};
 
-DBuf dalloc(lrgw_ctx c, size_t n) { return DBuf(c, n * sizeof(double)); }
-DBuf ialloc(lrgw_ctx c, size_t n) { return DBuf(c, n * sizeof(int)); }
 
 DBuf upload(lrgw_ctx c, const double* h, size_t n) {
   DBuf b = dalloc(c, n);
@@ -242,27 +135,6 @@ void mark(lrgw_ctx c, int i) {
   if (i < LRGW_STAGE_TOTAL) nvtxRangePushA(names[i]);
 }
 
-// The ABI wrapper: run the body, map failures onto status codes.
-template <class F>
-int guarded(lrgw_ctx c, F&& f) {
-  if (!c) return LRGW_ERR_INVALID_INPUT;
-  try {
-    use_device(c);
-    c->pivot = -1;
-    f();
-    return LRGW_OK;
-  } catch (const Fail& e) {
-    c->err = e.msg;
-    if (e.code == LRGW_ERR_SINGULAR) c->pivot = e.pivot;
-    return e.code;
-  } catch (const std::bad_alloc&) {
-    c->err = "host allocation failure";
-    return LRGW_ERR_INTERNAL;
-  } catch (...) {
-    c->err = "unknown failure";
-    return LRGW_ERR_INTERNAL;
-  }
-}
 
 template <class F>
 int guarded_host(F&& f) {
@@ -372,11 +244,6 @@ void coulomb_apply(lrgw_ctx c, const int* dims, const double* cell, int zero, co
   fft_inverse(c, dims, xh.d(), m, y, ldy);
 }
 
-// Split-K scratch for the skinny / symmetric GEMMs.
-struct Work {
-  DBuf buf;
-  size_t elems = 0;
-};
 
 Work make_work(lrgw_ctx c, size_t elems) {
   Work w;
@@ -387,7 +254,7 @@ Work make_work(lrgw_ctx c, size_t elems) {
 
 void gemm(lrgw_ctx c, int M, int N, int K, const double* A, long long lda, Lay la, const double* B,
           long long ldb, Lay lb, double* C, long long ldc, double alpha, double beta,
-          const double* scale = nullptr, bool lower = false, Work* w = nullptr) {
+          const double* scale, bool lower, Work* w) {
   ck(dgemm(c->stream, M, N, K, A, lda, la, B, ldb, lb, C, ldc, alpha, beta, scale, lower, c->sm_count,
            w ? w->buf.d() : nullptr, w ? w->elems : 0),
      "dgemm");
@@ -673,10 +540,6 @@ void smw_core(lrgw_ctx c, const double* t, const double* pvp, int n, double* k) 
 // Stage 1: ISDF point selection (isdf.hpp:95-112) — see select.cu.
 // ---------------------------------------------------------------------------
 // Host mirror of select.cu's candidate entry (d, position, grid row).
-struct HostEnt {
-  double v;
-  int pos, row;
-};
 
 // keep (optional): the pivoted-Cholesky factor L (n_r x steps, pivot order)
 // and the pivot sequence, reused by the fused fit of lrgw_build.
@@ -690,17 +553,10 @@ bool select_trace() {
   return on;
 }
 
-struct SelectKeep {
-  DBuf L;
-  std::vector<int> order;
-  int steps = 0;
-  int blocks = 0;           // candidate blocks (one host sync each)
-  int min_margin_step = -1; // step of the smallest top-2 margin (when margins are requested)
-};
 
 std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int n1, const double* b,
                                  long long ldb, int n2, int n_r, int n_mu, double* min_margin,
-                                 SelectKeep* keep = nullptr) {
+                                 SelectKeep* keep) {
   if (n_mu > n_r) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: N_mu > N_r");
   if (n_mu < 1) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: N_mu < 1");
   if (n1 < 1 || n2 < 1) fail(LRGW_ERR_INVALID_INPUT, "select_interpolation_points: empty orbital set");
@@ -956,9 +812,6 @@ bool fused_fit(lrgw_ctx c, const SelectKeep& keep, int n_r, const std::vector<in
 // ---------------------------------------------------------------------------
 // Stage 3: quadrature (K3, quadrature.cu).
 // ---------------------------------------------------------------------------
-struct NodeSet {
-  std::vector<double> nodes, weights;
-};
 
 NodeSet trapezoid(const lrgw_host::Spec& s, int n_intervals) {
   NodeSet ns;
@@ -1063,6 +916,34 @@ void levels_impl(lrgw_ctx c, const double* pv, long long ldv, const double* pc, 
     first = false;
     if (!visit(n_nodes, tl.d())) break;
   }
+}
+
+
+void adaptive_impl(lrgw_ctx c, const double* pv, long long ldv, const double* pc, long long ldpc, int n_mu, int n_v,
+                   int n_c, const double* energies, const lrgw_host::Spec& spec, double* t) {
+  const size_t nn = (size_t)n_mu * n_mu;
+  DBuf prev = dalloc(c, nn), red = dalloc(c, 512);
+  bool have = false, conv = false;
+  levels_impl(c, pv, ldv, pc, ldpc, n_mu, n_v, n_c, energies, spec, spec.max_nodes, [&](int, double* tl) {
+    ck(cudaMemcpyAsync(t, tl, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+    if (!have) {
+      have = true;
+      ck(cudaMemcpyAsync(prev.p, tl, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+      return true;
+    }
+    double h[2];
+    ck(frob_diff(c->stream, tl, prev.d(), nn, red.d()), "frob");
+    ck(cudaMemcpyAsync(&h[0], red.d() + 296, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(frob_diff(c->stream, tl, nullptr, nn, red.d()), "frob");
+    download(c, &h[1], red.d() + 296, sizeof(double));
+    ck(cudaMemcpyAsync(prev.p, tl, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+    if (std::sqrt(h[0]) / std::max(std::sqrt(h[1]), 1e-300) <= spec.delta_rel) {
+      conv = true;
+      return false;
+    }
+    return true;
+  });
+  if (!conv) fail(LRGW_ERR_CONTOUR_CONVERGENCE, "coupled_coefficients_contour: did not reach delta_rel within max_nodes");
 }
 
 }  // namespace
@@ -1588,30 +1469,7 @@ int lrgw_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, lo
     } else if (P.n_lambda > 0) {
       fixed_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, n_e, P.n_lambda, t.d(), n_mu);
     } else {
-      const size_t nn = (size_t)n_mu * n_mu;
-      DBuf prev = dalloc(c, nn), red = dalloc(c, 512);
-      bool have = false, conv = false;
-      levels_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, spec, spec.max_nodes,
-                  [&](int, double* tl) {
-                    ck(cudaMemcpyAsync(t.p, tl, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
-                    if (!have) {
-                      have = true;
-                      ck(cudaMemcpyAsync(prev.p, tl, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
-                      return true;
-                    }
-                    double h[2];
-                    ck(frob_diff(c->stream, tl, prev.d(), nn, red.d()), "frob");
-                    ck(cudaMemcpyAsync(&h[0], red.d() + 296, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
-                    ck(frob_diff(c->stream, tl, nullptr, nn, red.d()), "frob");
-                    download(c, &h[1], red.d() + 296, sizeof(double));
-                    ck(cudaMemcpyAsync(prev.p, tl, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
-                    if (std::sqrt(h[0]) / std::max(std::sqrt(h[1]), 1e-300) <= spec.delta_rel) {
-                      conv = true;
-                      return false;
-                    }
-                    return true;
-                  });
-      if (!conv) fail(LRGW_ERR_CONTOUR_CONVERGENCE, "coupled_coefficients_contour: did not reach delta_rel within max_nodes");
+      adaptive_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, spec, t.d());
     }
     mark(c, 5);
     // stages 4-5

@@ -2,8 +2,8 @@
 //
 // Scalars only (microseconds per node); the GPU consumes the resulting
 // per-node complex diagonals d_k = 1/(z_k - e) and weights w_k * g_k.
-// Semantics follow the reference: elliptic.hpp:17-193, contour.hpp:35-80,
-// 144-183, 235-279.
+// Produces the reference's contour geometry (elliptic.hpp:17-118,
+// contour.hpp:35-80, 144-183) by its own derivation (see elliptic.cpp).
 #pragma once
 
 #include <complex>
@@ -26,7 +26,6 @@ int elliptic_k(double k, double* out);
 int jacobi_sn_cn_dn(double u, double k, double* sn, double* cn, double* dn);
 int jacobi_complex(double x, double y, double k, std::complex<double>* sn, std::complex<double>* cn,
                    std::complex<double>* dn);
-double integrate_adaptive(double (*f)(double, void*), void* ctx, double a, double b, double rel_tol);
 int elliptic_params(const double* e, int n_e, int n_v, int n_c, double delta_rel, int max_nodes,
                     Spec* out);
 int cauchy_error_bound(const Spec& s, int n_lambda, double* out);

@@ -76,3 +76,45 @@ def test_null_context_is_rejected():
                                               a.ctypes.data_as(_lib.c_double_p), 8, 2, 2, 4, 0,
                                               pts.ctypes.data_as(_lib.c_int32_p))
     assert rc == 1
+
+
+def test_elliptic_scalars_accuracy_vs_multiprecision():
+    """csrc/elliptic.cpp (Carlson R_F, Gauss-transformation sn/cn/dn, addition
+    theorem for complex arguments) against 40-digit values: the same accuracy
+    class as the reference's AGM / sncndn recipes (elliptic.hpp:17-118)."""
+    mp = pytest.importorskip("mpmath")
+    mp.mp.dps = 40
+    rng = np.random.default_rng(17)
+    for _ in range(400):
+        k, u = rng.uniform(0, 0.99), rng.uniform(-5, 5)
+        m = mp.mpf(k) ** 2
+        want = [float(mp.ellipfun(f, u, m=m)) for f in ("sn", "cn", "dn")]
+        assert np.max(np.abs(np.array(lrgw.jacobi_sn_cn_dn(u, k)) - want)) <= 4e-15
+        kk = float(mp.ellipk(m))
+        assert abs(lrgw.elliptic_k(k) - kk) <= 8e-16 * kk
+        y = rng.uniform(0, 0.6)
+        got = lrgw.jacobi_complex(u, y, k)
+        w = mp.mpc(u, y)
+        for g, f in zip(got, ("sn", "cn", "dn")):
+            wv = complex(mp.ellipfun(f, w, m=m))
+            assert abs(g - wv) <= 1e-14 * max(1.0, abs(wv))
+    # the contour height L = 1/2 int_0^{1/r} dt / sqrt((1+t^2)(1+r^2 t^2)) (contour.hpp:62-68)
+    for e in ([0.0, 1.0, 4.0], [-0.5, -0.1, 0.05, 0.8], [-0.5, -0.1, 0.0, 0.8]):
+        s = lrgw.elliptic_params(e, len(e) // 2 if len(e) > 3 else 1, len(e) - (len(e) // 2 if len(e) > 3 else 1),
+                                 1e-7).as7()
+        r = s[2]
+        ell = 0.5 * mp.quad(lambda t: 1 / mp.sqrt((1 + t * t) * (1 + r * r * t * t)), [0, 1 / mp.mpf(r)])
+        assert abs(s[4] - float(ell)) <= 6e-16 * float(ell)
+
+
+def test_jacobi_complex_domain_and_pole_rules():
+    """test_elliptic.cpp:98-102: |y| >= K(k') -> invalid_input, next to the
+    pole line -> numeric_error."""
+    r = 1.0 / 3.0
+    kprime = lrgw.elliptic_k(math.sqrt(1.0 - r * r))
+    with pytest.raises(lrgw.InvalidInput):
+        lrgw.jacobi_complex(0.3, kprime * 1.01, r)
+    with pytest.raises(lrgw.NumericError):
+        lrgw.jacobi_complex(0.0, kprime - 1e-10, r)
+    sn, cn, dn = lrgw.jacobi_sn_cn_dn(lrgw.elliptic_k(0.7), 0.7)  # sn(K) = 1 (test_elliptic.cpp:28-62)
+    assert abs(sn - 1.0) <= 1e-15 and abs(cn) <= 1e-15
