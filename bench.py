@@ -2,28 +2,35 @@
 
 One step = the factored eps^-1 build, stages 1-5 (ISDF point selection, Theta
 fit, Cauchy quadrature of the core, G-space Theta^T V Theta, SMW core K), plus
-eps^-1 applied to the seeded 8-column probe block, on the Si64-sized config
-(BASELINE.json configs[1], the primary 1-GPU roofline case):
+eps^-1 applied to the seeded 8-column probe block. Default workload: the
+Si512-sized scaling run (BASELINE.json configs[4]: 96^3 grid, N_v = N_c =
+1024, N_mu = 8192, Theta 58 GB; it fits one B200), so the N = 1 line and every
+N of a scaling run measure the same workload; --config si64 / c60 / si216 /
+si8 for the others.
 
   value      device time per build with inputs resident in HBM (CUDA events
-             on the library stream, max over ranks)
+             on the library stream; max over ranks)
   e2e        the same step through the C-ABI from pinned HOST buffers: the
-             H2D copy of Phi and of the probe and the D2H of eps^-1 X inside
-             the timed region
-  roofline   the dominant kernel of the step (largest device-time share),
-             algorithmic FLOPs / its CUDA-event duration against
-             the measured FP64 peak (profiles/FP64_PEAK.json: DMMA 37.17
-             TFLOP/s; MEASURED_PEAKS.json has no FP64 entry)
+             H2D copy of Phi (this rank's panel) and of the probe and the D2H
+             of eps^-1 X inside the timed region
+  roofline   the dominant kernel of the step (largest device-time share):
+             algorithmic FLOPs (per rank at N > 1) / its
+             CUDA-event duration against the measured FP64 DMMA peak
+             (profiles/FP64_PEAK.json: 37.17 TFLOP/s; MEASURED_PEAKS.json has
+             no FP64 entry)
   cpu_baseline  the reference CPU implementation (oracle/_ref) on the host
-             cores on a bounded, extrapolated sample (oracle/cpu_baseline.py)
+             cores, a bounded sample extrapolated by exact cost models
+             (oracle/cpu_baseline.py; Si216 / Si512 through the N^3 model)
 
-Inputs are larger than L2 (Phi 226 MB, Theta 906 MB) — no explicit flush.
-N > 1 (torchrun): the sharded build (dist.py, --mode sharded, default):
-grid-row panels, quadrature nodes split across ranks, NCCL all-reduces and
-one all-to-all — strong scaling of one build of the config; --mode replicas
-runs one full build per rank instead (weak).
+Inputs are larger than L2 (Phi >= 226 MB, Theta >= 906 MB) — no flush.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config si64] [--impl ours|reference]
+N > 1: `python bench.py --gpus N` re-launches itself under torch.distributed.run
+(N ranks, 127.0.0.1); under torchrun WORLD_SIZE must equal --gpus. Each rank
+builds through lrgw_build_sharded (C-ABI, NCCL communicator): z-plane row
+panels, node-split quadrature, one all-to-all of the slab FFT — strong
+scaling of one build of the config (--mode replicas: one full build per rank).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config si512] [--impl ours|reference]
 """
 import argparse
 import json
@@ -109,15 +116,36 @@ class Clocks:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1, no torchrun env): re-execute this
+    script under torch.distributed.run with N ranks on 127.0.0.1."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch N ranks, one per GPU)")
     if world > 1:
         import torch.distributed as dist
 
-        backend = "nccl" if args.impl == "ours" else "gloo"
-        dist.init_process_group(backend)
+        if args.impl == "ours":
+            import torch
+
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
@@ -140,9 +168,9 @@ def max_over_ranks(x, world, device):
 
 
 def cpu_config(cfg):
-    """The config the CPU reference is timed on and the factor to this one:
-    Si512 is timed on Si216 and extrapolated by the N^3 model (BASELINE.json
-    configs[4]); every other config is sampled directly."""
+    """The config the CPU reference is timed on and the factor to this one.
+    Si512 (BASELINE.json configs[4]) is timed on Si216 and extrapolated by the
+    N^3 model, (1024 / 432)^3 = 13.3; every other config is sampled directly."""
     from paper_2403_12340_b200 import synth
 
     if cfg.name == "si512":
@@ -151,7 +179,68 @@ def cpu_config(cfg):
     return cfg, 1.0
 
 
+def quick_cpu_config(cfg):
+    """The bounded (~10-60 s) CPU-baseline sample of our own arm: configs up to
+    Si64 directly, larger ones from Si64 through the N^3 model."""
+    from paper_2403_12340_b200 import synth
+
+    if cfg.name in ("si8", "si64"):
+        return cfg, 1.0
+    small = synth.CONFIGS["si64"]
+    return small, (cfg.n_v / small.n_v) ** 3
+
+
+def work_for(cfg, n_mu, world=1):
+    """Algorithmic work per rank at world size `world` (the panel / slab /
+    node shares)."""
+    work = algorithmic_work(cfg, n_mu)
+    if world == 1:
+        return work
+    out = {}
+    for k, (bound, amount) in work.items():
+        out[k] = (bound, amount / world)
+    return out
+
+
+def kernel_fractions(stages, work, hbm):
+    kernels = {}
+    for k, (bound, amount) in work.items():
+        t = stages.get(k, 0.0)
+        if t <= 0:
+            continue
+        if bound == "tensor":
+            ach = amount / (t * 1e-3) / 1e12
+            kernels[k] = {"ms": round(t, 4), "bound": "tensor", "achieved": round(ach, 3),
+                          "unit": "TFLOP/s", "frac": round(ach / FP64_PEAK_TFLOPS, 4)}
+        else:
+            ach = amount / (t * 1e-3) / 1e9
+            kernels[k] = {"ms": round(t, 4), "bound": "hbm", "achieved": round(ach, 1), "unit": "GB/s",
+                          "frac": round(ach / hbm, 4)}
+    for k in ("fit_solve", "smw"):
+        kernels[k] = {"ms": round(stages.get(k, 0.0), 4), "bound": "latency (N_mu^3 leaves)"}
+    if "select" in kernels:
+        kernels["select"]["note"] = "stage of ~18 launches per candidate block (one block per <= 128 pivots)"
+    return kernels
+
+
+def roofline_of(kernels, cfg, hbm, world):
+    """The dominant single kernel (stages whose events bracket one launch:
+    the Theta^T V Theta SYRK, the fit GEMM, the K3 quadrature kernel)."""
+    dom = max(("pvp", "fit_gemm", "quad_kernel"), key=lambda k: kernels.get(k, {}).get("ms", -1.0))
+    dk = kernels[dom]
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}_r02.json")
+    if world == 1 and os.path.exists(tp):  # ncu dram bytes of that kernel, captured on this config
+        traffic = json.load(open(tp)).get(dom)
+    return {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"],
+            "peak": FP64_PEAK_TFLOPS if dk["bound"] == "tensor" else hbm,
+            "unit": dk["unit"], "frac": dk["frac"], "traffic": traffic,
+            "peak_source": "profiles/FP64_PEAK.json (measured DMMA)" if dk["bound"] == "tensor"
+            else "MEASURED_PEAKS.json hbm_gbs"}
+
+
 def run_ours(args, cfg, world, rank, local):
+    """One full build per rank (N = 1, or --mode replicas)."""
     import torch
 
     from paper_2403_12340_b200 import lrgw, synth
@@ -188,6 +277,7 @@ def run_ours(args, cfg, world, rank, local):
     t_steps = []
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    info = None
     for _ in range(args.steps):
         e0.record(stream)
         ep = step_dev()
@@ -197,13 +287,13 @@ def run_ours(args, cfg, world, rank, local):
         for k, v in ctx.stage_ms().items():
             stage_acc.setdefault(k, []).append(v)
         points = ep.point_indices  # the CPU baseline's fit sample uses the build's own ISDF points
+        info = ep.info()
         ep.close()
     torch.cuda.synchronize()
     barrier(world)
     clk = clocks.stop()
     launches = ctx.kernel_launches() - launches0
-    ms_local = sum(t_steps) / len(t_steps)
-    ms = max_over_ranks(ms_local, world, dev)
+    ms = max_over_ranks(sum(t_steps) / len(t_steps), world, dev)
 
     # ---- e2e through the C-ABI from pinned host buffers ----
     psi_h = torch.empty(psi.shape[1], psi.shape[0], dtype=torch.float64).pin_memory()
@@ -230,7 +320,7 @@ def run_ours(args, cfg, world, rank, local):
     torch.cuda.synchronize()
     barrier(world)
     e2e_ms = []
-    for _ in range(max(1, min(args.steps, 5))):
+    for _ in range(max(1, min(args.steps, 3))):
         e0.record(stream)
         step_e2e()
         e1.record(stream)
@@ -239,145 +329,158 @@ def run_ours(args, cfg, world, rank, local):
     e2e = max_over_ranks(sum(e2e_ms) / len(e2e_ms), world, dev)
     h2d = psi_h.numel() * 8 + x_h.numel() * 8
     d2h = y_h.numel() * 8
-    # parity guard on the bench output: eps^-1 X finite and the probe changed
-    assert torch.isfinite(y_d).all()
+    assert torch.isfinite(y_d).all()  # parity guard on the bench output
 
     stages = {k: statistics.median(v) for k, v in stage_acc.items()}
     n_mu = min(max(lrgw.num_aux(cfg.k_mu, cfg.n_v, cfg.n_c), 1), cfg.n_r)
-    work = algorithmic_work(cfg, n_mu)
     hbm = _peaks()
-    kernels = {}
-    for k, (bound, amount) in work.items():
-        t = stages.get(k, 0.0)
-        if t <= 0:
-            continue
-        if bound == "tensor":
-            ach = amount / (t * 1e-3) / 1e12
-            kernels[k] = {"ms": round(t, 4), "bound": "tensor", "achieved": round(ach, 3),
-                          "unit": "TFLOP/s", "frac": round(ach / FP64_PEAK_TFLOPS, 4)}
-        else:
-            ach = amount / (t * 1e-3) / 1e9
-            kernels[k] = {"ms": round(t, 4), "bound": "hbm", "achieved": round(ach, 1), "unit": "GB/s",
-                          "frac": round(ach / hbm, 4)}
-    for k in ("fit_solve", "smw"):
-        kernels[k] = {"ms": round(stages.get(k, 0.0), 4), "bound": "latency (N_mu^3 leaves)"}
-    kernels["select"]["note"] = "stage of ~18 launches per candidate block (one block per <= 128 pivots), not one kernel"
-    # roofline: the dominant single kernel (stages whose events bracket one
-    # launch: the Theta^T V Theta SYRK, the fit GEMM, the K3 quadrature kernel)
-    dom = max(("pvp", "fit_gemm", "quad_kernel"), key=lambda k: kernels.get(k, {}).get("ms", -1.0))
-    dk = kernels[dom]
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tp) and cfg.name == "si64":  # the committed ncu traffic capture is of the Si64 build
-        traffic = json.load(open(tp)).get(dom)
-    roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"],
-                "peak": FP64_PEAK_TFLOPS if dk["bound"] == "tensor" else hbm,
-                "unit": dk["unit"], "frac": dk["frac"], "traffic": traffic,
-                "peak_source": "profiles/FP64_PEAK.json (measured DMMA)" if dk["bound"] == "tensor"
-                else "MEASURED_PEAKS.json hbm_gbs"}
+    kernels = kernel_fractions(stages, work_for(cfg, n_mu), hbm)
     return {"ms": ms, "e2e_ms": e2e, "h2d": h2d, "d2h": d2h, "launches": launches, "clocks": clk,
-            "stages": stages, "kernels": kernels, "roofline": roofline, "psi": psi, "e": e, "ctx": ctx,
-            "points": points}
+            "stages": stages, "kernels": kernels, "roofline": roofline_of(kernels, cfg, hbm, 1),
+            "psi": psi, "e": e, "ctx": ctx, "points": points, "info": info}
 
 
 def run_sharded(args, cfg, world, rank, local):
-    """The multi-rank build (paper_2403_12340_b200/dist.py + the device
-    backend): grid-row panels for selection / fit / the slab FFT, quadrature
-    nodes split across ranks, NCCL all-reduces of the N_mu^2 partials and one
-    all-to-all of the slab spectra. Strong scaling: one build of the config
-    across all ranks; CUDA events on each rank, max over ranks."""
+    """One build of the config split across the ranks (strong scaling) through
+    the C-ABI: lrgw_build_sharded + lrgw_eps_apply_sharded over an NCCL
+    communicator (z-plane panels of Phi / L / Theta, node-split quadrature,
+    NCCL all-reduces and one all-to-all). CUDA events on each rank's library
+    stream, max over ranks."""
     import torch
-    import torch.distributed as dist
 
-    from paper_2403_12340_b200 import dist as D
     from paper_2403_12340_b200 import lrgw, synth
-    from paper_2403_12340_b200.dist_cuda import CudaBackend
 
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world == 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29541")
-        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
-    comm = D.Comm()
+    torch.cuda.set_device(local)
+    ctx = lrgw.Context(local)
+    comm = lrgw.Comm.from_torch(ctx) if world > 1 else lrgw.Comm.nccl(ctx, 0, 1, lrgw.Comm.nccl_unique_id())
+    stream = torch.cuda.ExternalStream(lrgw.L.load().lrgw_ctx_stream(ctx.handle), device=dev)
+    r0, rows = lrgw.z_panel(cfg.dims, world, rank)
     psi = synth.orbitals_device(cfg, seed=1, device=dev)
+    psi_p = psi[r0:r0 + rows].t().contiguous().t()  # this rank's panel, column-major
+    del psi
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     e = synth.energies(cfg)
     x_host = synth.probe_host(cfg.n_r)
-    n_mu = lrgw.num_aux(cfg.k_mu, cfg.n_v, cfg.n_c)
-    ctx = lrgw.Context(local)
-    r0, r1 = D.z_panels(cfg.dims, world)[rank]
-    # this rank's panel of Phi (column-major) and of the probe, host-pinned for e2e
-    psi_p = psi[r0:r1].t().contiguous().t()
-    del psi
-    psi_h = torch.empty(psi_p.shape[1], psi_p.shape[0], dtype=torch.float64).pin_memory()
-    psi_h.copy_(psi_p.t())
-    x_p = np.ascontiguousarray(x_host[r0:r1])
+    x_p = torch.from_numpy(np.ascontiguousarray(x_host[r0:r0 + rows].T)).to(dev).t()
+    y_p = torch.empty(8, rows, dtype=torch.float64, device=dev).t()
 
-    def step(phi_p):
-        b = D.DistributedBuild(comm, CudaBackend(n_mu, ctx), cfg.dims, cfg.cell3, cfg.n_v, cfg.n_c, k_mu=cfg.k_mu,
-                               n_lambda=cfg.n_lambda, batch=128)
-        a, bb = phi_p[:, :cfg.n_v], phi_p[:, cfg.n_v:]
-        pts = b.select(a, bb)
-        b.fit(pts)
-        pv, pc = b.point_rows(pts, a, bb)
-        t = b.contour(pv, pc, e)
-        k = b.smw(t, b.pvp())
-        return b.apply(k, x_p)
+    def step(phi):
+        ep = lrgw.build_sharded(comm, phi[:, :cfg.n_v], phi[:, cfg.n_v:], e, cfg.dims, cfg.cell3, k_mu=cfg.k_mu,
+                                n_lambda=cfg.n_lambda, ctx=ctx)
+        lrgw.eps_apply_sharded(comm, ep, x_p, y_p)
+        return ep
 
     for _ in range(args.warmup):
-        step(psi_p)
+        step(psi_p).close()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    dist.barrier()
+    barrier(world)
     clocks = Clocks(local)
     launches0 = ctx.kernel_launches()
-    t_steps = []
+    t_steps, stage_acc = [], {}
     for _ in range(args.steps):
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0.record()
-        y = step(psi_p)
-        e1.record()
+        e0.record(stream)
+        ep = step(psi_p)
+        e1.record(stream)
         e1.synchronize()
         t_steps.append(e0.elapsed_time(e1))
+        for k, v in ctx.stage_ms().items():
+            stage_acc.setdefault(k, []).append(v)
+        info = ep.info()
+        ep.close()
     torch.cuda.synchronize()
-    dist.barrier()
+    barrier(world)
     clk = clocks.stop()
     launches = ctx.kernel_launches() - launches0
-    assert np.isfinite(y).all()
+    assert torch.isfinite(y_p).all()
     ms = max_over_ranks(sum(t_steps) / len(t_steps), world, dev)
-    # e2e: the panel H2D from pinned host inside the timed region (the probe
-    # panel enters and eps^-1 x leaves through the host in apply)
-    psi_d = torch.empty_like(psi_h, device=dev)
+    # e2e: this rank's panel H2D from pinned host and the eps^-1 x panel D2H inside the timed region
+    psi_h = torch.empty(psi_p.shape[1], psi_p.shape[0], dtype=torch.float64).pin_memory()
+    psi_h.copy_(psi_p.t())
+    y_h = torch.empty(8, rows, dtype=torch.float64).pin_memory()
+    psi_d = psi_p.t()
     e2e_ms = []
     for _ in range(max(1, min(args.steps, 3))):
         torch.cuda.synchronize()
-        dist.barrier()
-        e0.record()
-        psi_d.copy_(psi_h, non_blocking=True)
-        y = step(psi_d.t())
-        e1.record()
+        barrier(world)
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            psi_d.copy_(psi_h, non_blocking=True)
+        ep = step(psi_d.t())
+        with torch.cuda.stream(stream):
+            y_h.copy_(y_p.t(), non_blocking=True)
+        e1.record(stream)
         e1.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
+        ep.close()
     e2e = max_over_ranks(sum(e2e_ms) / len(e2e_ms), world, dev)
-    h2d = psi_h.numel() * 8 + x_p.size * 8
-    d2h = y.size * 8
-    return {"ms": ms, "e2e_ms": e2e, "h2d": h2d, "d2h": d2h, "launches": launches, "clocks": clk}
+    stages = {k: statistics.median(v) for k, v in stage_acc.items()}
+    n_mu = min(max(lrgw.num_aux(cfg.k_mu, cfg.n_v, cfg.n_c), 1), cfg.n_r)
+    hbm = _peaks()
+    kernels = kernel_fractions(stages, work_for(cfg, n_mu, world), hbm)
+    comm.close()
+    return {"ms": ms, "e2e_ms": e2e, "h2d": psi_h.numel() * 8 + x_p.numel() * 8, "d2h": y_h.numel() * 8,
+            "launches": launches, "clocks": clk, "stages": stages, "kernels": kernels,
+            "roofline": roofline_of(kernels, cfg, hbm, world), "info": info}
+
+
+def reference_arm(args, cfg, world, workload, metric):
+    """--impl reference: the reference CPU implementation (oracle/_ref, all
+    host threads) on this config, rank 0 only. The N_mu^3 pieces (fit with
+    its Gram LU, the quadrature, sym_eig / LU of the SMW core) are timed once
+    per run; every step times the sampled pieces (selection steps,
+    apply_coulomb columns, a matmul_tn block) and reports the extrapolated
+    full-build time. Si512 is timed on Si216 through the N^3 model."""
+    from oracle import cpu_baseline
+
+    cores = os.cpu_count() or 1
+    ccfg, scale = cpu_config(cfg)
+    t_run = time.perf_counter()
+    fixed, fs = cpu_baseline.fixed_pieces(ccfg, cores=cores)
+    t_fixed = time.perf_counter() - t_run
+    vals, measured = [], []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        samp, ss = cpu_baseline.sampled_pieces(ccfg, cores=cores, sel_steps=16, cols=32, seed=5 + i)
+        if i >= args.warmup:
+            measured.append(time.perf_counter() - t0)
+            vals.append((sum(fixed.values()) + sum(samp.values())) * scale)
+    v = statistics.median(vals)
+    stages = {k: round(x * scale, 3) for k, x in {**samp, **fixed}.items()}
+    sample = f"{ccfg.name}: {ss}; {fs}"
+    if scale != 1.0:
+        sample += f"; x{scale:.2f} = (N_v {cfg.n_v} / {ccfg.n_v})^3 (N^3 model, BASELINE.json configs[4])"
+    line = {"impl": "reference", "metric": metric, "value": v, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+            "config": workload,
+            "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "reference", "sample": sample,
+                             "stages_s": stages, "no_select_s": v - stages["select"]},
+            "extrapolated": {"value_is": "the extrapolated time of ONE full reference build per step",
+                             "fixed_pieces_measured_once_s": round(t_fixed, 2),
+                             "sampled_pieces_measured_s_per_step": round(statistics.median(measured), 3),
+                             "run_wall_s": round(time.perf_counter() - t_run, 2)},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="si64")
+    ap.add_argument("--config", default="si512")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default=None, choices=["single", "sharded", "replicas"],
                     help="single (N = 1 default): the one-GPU build; sharded (N > 1 default): one build "
                          "split across the ranks (strong scaling); replicas: one full build per rank")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
 
     from paper_2403_12340_b200 import synth
 
@@ -386,77 +489,45 @@ def main():
     mode = args.mode or ("single" if world == 1 else "sharded")
     if mode == "single" and world > 1:
         mode = "replicas"
+    n_mu = int(round(cfg.k_mu * (cfg.n_v * cfg.n_c) ** 0.5))
     workload = {"workload": f"{cfg.name}: grid {cfg.dims[0]}^3 = {cfg.n_r} points, cell {cfg.cell} bohr, "
-                            f"N_v = N_c = {cfg.n_v}, N_mu = {int(round(cfg.k_mu * (cfg.n_v * cfg.n_c) ** 0.5))}, "
-                            f"N_lambda = {cfg.n_lambda}, eps^-1 X on an {cfg.n_r}x8 probe",
+                            f"N_v = N_c = {cfg.n_v}, N_mu = {n_mu}, N_lambda = {cfg.n_lambda}, "
+                            f"eps^-1 X on an {cfg.n_r}x8 probe",
                 "stages": "1-5 (select, fit, quadrature, Coulomb/ThetaVTheta, SMW) + probe apply",
                 "l2": f"inputs larger than L2 (Phi {cfg.n_r * (cfg.n_v + cfg.n_c) * 8 / 1e6:.0f} MB, Theta "
-                      f"{cfg.n_r * int(round(cfg.k_mu * (cfg.n_v * cfg.n_c) ** 0.5)) * 8 / 1e6:.0f} MB); no flush",
+                      f"{cfg.n_r * n_mu * 8 / 1e6:.0f} MB); no flush",
                 "parallelism": {"single": "1 GPU", "replicas": f"replicas x{world}",
-                                "sharded": f"sharded x{world} (grid-row panels, node split, NCCL)"}[mode]}
+                                "sharded": f"sharded x{world} (z-plane panels, node split, NCCL)"}[mode]}
     metric = "low-rank eps^-1 build time (s), stages 1-5 + probe apply"
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        from oracle import cpu_baseline
-
-        cores = os.cpu_count() or 1
-        vals = []
-        ccfg, scale = cpu_config(cfg)
-        for i in range(args.warmup + args.steps):  # W untimed warm-up samples, then K timed
-            r = cpu_baseline.run(ccfg, cores=cores, sel_steps=16, fit_rows=(1536, 2560), cols=64, seed=5 + i)
-            if i >= args.warmup:
-                vals.append(r["total_s"] * scale)
-        if scale != 1.0:
-            r["sample"] += f"; x{scale:.2f} = (N_v {cfg.n_v} / {ccfg.n_v})^3 (N^3 model, BASELINE.json configs[4])"
-            r["stages"] = {k: v * scale for k, v in r["stages"].items()}
-        v = statistics.median(vals)
-        line = {"impl": "reference", "metric": metric, "value": v, "unit": "s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-                "config": workload,
-                "cpu_baseline": {"value": v, "unit": "s", "cores": r["cores"], "kind": "reference",
-                                 "sample": r["sample"], "stages_s": r["stages"],
-                                 "no_select_s": statistics.median(vals) - r["stages"]["select"]},
-                "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
-        return
-
-    if mode == "sharded":
-        res = run_sharded(args, cfg, world, rank, local)
         if rank == 0:
-            line = {"metric": metric, "value": res["ms"] / 1e3, "unit": "s", "n_gpus": world,
-                    "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"],
-                    "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                    "data": "synthetic (seeded)", "config": workload,
-                    "e2e": {"value": res["e2e_ms"] / 1e3, "unit": "s", "h2d_bytes_per_step": res["h2d"],
-                            "d2h_bytes_per_step": res["d2h"]},
-                    "gpu_launches": res["launches"], "clocks": res["clocks"], "roofline": None,
-                    "cpu_baseline": None}
-            print(json.dumps(line))
-        import torch.distributed as dist
+            reference_arm(args, cfg, world, workload, metric)
+        if world > 1:
+            import torch.distributed as dist
 
-        dist.destroy_process_group()
+            dist.destroy_process_group()
         return
-    res = run_ours(args, cfg, world, rank, local)
+
+    res = run_sharded(args, cfg, world, rank, local) if mode == "sharded" else run_ours(args, cfg, world, rank, local)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import cpu_baseline
 
-        ccfg, scale = cpu_config(cfg)
+        ccfg, scale = quick_cpu_config(cfg)
         if ccfg is cfg:
             psi_h = np.asfortranarray(res["psi"].cpu().numpy())
             r = cpu_baseline.run(cfg, psi=psi_h, energies=res["e"], cores=os.cpu_count(), points=res["points"])
         else:
             r = cpu_baseline.run(ccfg, cores=os.cpu_count())
         cpu = {"value": r["total_s"] * scale, "unit": "s", "cores": r["cores"], "kind": "reference",
-               "sample": r["sample"] + (f"; then x{scale:.2f} = (N_v {cfg.n_v} / {ccfg.n_v})^3, the N^3 model of "
-                                        f"BASELINE.json configs[4] (extrapolated, not run at {cfg.name})"
-                                        if scale != 1.0 else ""),
+               "sample": r["sample"] + (f"; then x{scale:.1f} = (N_v {cfg.n_v} / {ccfg.n_v})^3, the N^3 model "
+                                        f"(extrapolated, not run at {cfg.name}; the --impl reference arm times "
+                                        f"Si216 for Si512)" if scale != 1.0 else ""),
                "stages_s": {k: round(v * scale, 3) for k, v in r["stages"].items()},
                "no_select_s": r["total_no_select_s"] * scale}
     if rank == 0:
+        info = res.get("info") or {}
         line = {"metric": metric, "value": res["ms"] / 1e3, "unit": "s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": False,
                 "scaling": "weak" if mode == "replicas" else "strong", "vs_baseline": None, "dtype": "f64",
@@ -465,7 +536,10 @@ def main():
                         "d2h_bytes_per_step": res["d2h"]},
                 "gpu_launches": res["launches"], "clocks": res["clocks"],
                 "roofline": res["roofline"], "stages_ms": {k: round(v, 4) for k, v in res["stages"].items()},
-                "kernels": res["kernels"], "cpu_baseline": cpu}
+                "kernels": res["kernels"], "cpu_baseline": cpu,
+                "selection": {"min_pivot_margin": info.get("min_margin"), "at_step": info.get("min_margin_step"),
+                              "candidate_blocks": info.get("select_blocks"),
+                              "gram_cond_lower_bound": info.get("lp_diag_ratio")}}
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist

@@ -323,6 +323,66 @@ int lrgw_dev_cand_greedy(lrgw_ctx ctx, int n_r, int s, int steps, int k, const d
                          int32_t* perm, double* x, int32_t* piv_rows_host, double* margins_host,
                          int32_t* b_host);
 
+
+/* ---- multi-rank build (one process per GPU) -------------------
+ * A communicator carries the build's few exchanges between the ranks of one
+ * box: NCCL over NVLink / NVSwitch (device buffers, the context's stream), or
+ * a caller-supplied host transport (any runtime that can move host bytes:
+ * MPI, torch.distributed gloo, ...; device payloads are staged through
+ * pinned host buffers). Grid rows are split into contiguous z-plane panels:
+ * rank p owns rows [row0, row0 + rows) of lrgw_z_panel. */
+typedef struct lrgw_comm_s* lrgw_comm;
+
+/* Host transport callbacks (return 0 on success); rank order everywhere. */
+typedef struct {
+  void* user;
+  /* in-place element-wise sum of `count` doubles over all ranks */
+  int (*allreduce_sum_f64)(void* user, double* buf, long long count);
+  /* recv (world * bytes) = every rank's `bytes` of send, rank order */
+  int (*allgather)(void* user, const void* send, void* recv, long long bytes);
+  /* send block q (send_bytes[q], packed in rank order) goes to rank q; recv
+   * block p (recv_bytes[p], packed in rank order) comes from rank p */
+  int (*alltoallv)(void* user, const void* send, const long long* send_bytes, void* recv,
+                   const long long* recv_bytes);
+} lrgw_host_transport;
+
+/* 1 when libnccl.so.2 can be loaded (dlopen; no link-time dependency). */
+int lrgw_nccl_available(void);
+/* rank 0 makes the id (128 bytes) and shares it with the other ranks. */
+int lrgw_nccl_unique_id(unsigned char id[128]);
+int lrgw_comm_create_nccl(lrgw_ctx ctx, int rank, int world, const unsigned char id[128], lrgw_comm* out);
+int lrgw_comm_create_host(int rank, int world, const lrgw_host_transport* transport, lrgw_comm* out);
+int lrgw_comm_destroy(lrgw_comm comm);
+int lrgw_comm_info(lrgw_comm comm, int* rank, int* world);
+/* This rank's grid-row panel: whole z-planes [z0, z1) of the n3 planes,
+ * z_p = floor(n3 p / world) (requires n3 >= world). */
+int lrgw_z_panel(const int* dims, int world, int rank, int* row0, int* rows);
+
+/* The factored eps^-1 build (stages 1-5) across the ranks of `comm`, each
+ * rank passing its OWN panel of the orbitals (rows x n_v and rows x n_c
+ * device arrays, rows from lrgw_z_panel) and the full energies:
+ *   1 selection: per candidate block the local top-(s+1) by (residual,
+ *     position) is all-gathered and merged on the device; the candidates'
+ *     rows [Phi_v | Phi_c | L] are owner-contributed (one all-reduce); the
+ *     certified greedy runs replicated (identical on every rank); each rank
+ *     updates its panel of the factor L and of the residual diagonal
+ *   2 fit: Theta panel = L panel L_P^-1 (L_P owner-contributed)
+ *   3 quadrature nodes split across ranks, all-reduce of the partial core
+ *   4-5 slab 3-D FFT of the Theta panel (2-D transforms of the owned planes,
+ *     one all-to-all to y-pencils, 1-D transforms along z), the G-slab
+ *     Theta^T V Theta SYRK, all-reduce; SMW core replicated.
+ * The handle keeps the rank's Theta panel (lrgw_eps_info: theta is rows x
+ * n_mu) and replicated K, T, Theta^T V Theta and points. world == 1 is the
+ * one-GPU build. Stage device times: lrgw_ctx_stage_ms (this rank). */
+int lrgw_build_sharded(lrgw_ctx ctx, lrgw_comm comm, const lrgw_build_params* prm, const double* phi_v,
+                       long long ldv, const double* phi_c, long long ldc, const double* energies,
+                       lrgw_eps* out);
+/* y = eps^-1 x on this rank's panel rows (device x, y: rows x m): u =
+ * all-reduce(Theta_p^T x_p), z_p = Theta_p (K u), V z from the all-gathered
+ * z, y_p = x_p + (V z)_p (smw.hpp:97-103). */
+int lrgw_eps_apply_sharded(lrgw_ctx ctx, lrgw_comm comm, lrgw_eps e, const double* x, long long ldx, int m,
+                           double* y, long long ldy);
+
 #ifdef __cplusplus
 }
 #endif

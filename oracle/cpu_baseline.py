@@ -40,30 +40,28 @@ def _t(fn):
     return time.perf_counter() - t0, out
 
 
-def run(cfg, psi=None, energies=None, cores=None, sel_steps=64, fit_rows=(2048, 4096), cols=128, seed=5,
-        points=None):
-    """Returns dict(total_s, total_no_select_s, stages, sample, cores)."""
-    cores = cores or os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+def _inputs(cfg, psi, energies, rng):
     n_r, n_v, n_c = cfg.n_r, cfg.n_v, cfg.n_c
     n = n_v + n_c
-    n_mu = min(max(R.num_aux(cfg.k_mu, n_v, n_c), 1), n_r)
-    rng = np.random.default_rng(seed)
     if psi is None:
         psi = np.asfortranarray(np.linalg.qr(rng.standard_normal((n_r, n)))[0])
     e = energies if energies is not None else np.concatenate(
         [np.sort(rng.uniform(*cfg.occ, n_v)), np.sort(rng.uniform(*cfg.virt, n_c))])
-    a, b = psi[:, :n_v], psi[:, n_v:n]
+    return psi, e
+
+
+def fixed_pieces(cfg, psi=None, energies=None, cores=None, fit_rows=(2048, 4096), seed=5, points=None):
+    """The pieces timed once per run: the reference fit on two row samples
+    (each with the full N_mu^3 Gram LU; linear in N_r), the quadrature over
+    all nodes, and the N_mu^3 SMW factorisations (sym_eig, lu_solve, lu_invert)."""
+    cores = cores or os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    n_r, n_v, n_c = cfg.n_r, cfg.n_v, cfg.n_c
+    n_mu = min(max(R.num_aux(cfg.k_mu, n_v, n_c), 1), n_r)
+    rng = np.random.default_rng(seed)
+    psi, e = _inputs(cfg, psi, energies, rng)
+    a, b = psi[:, :n_v], psi[:, n_v:n_v + n_c]
     stages = {}
-
-    # 1: greedy selection restatement, first S steps, extrapolated
-    s = min(sel_steps, n_mu)
-    t_sel, _ = _t(lambda: R.select_points(a, b, s))
-    w_s = sum(n + k + 1 for k in range(s))
-    w_all = sum(n + k + 1 for k in range(n_mu))
-    stages["select"] = t_sel * w_all / w_s
-
-    # 2: reference fit on two row samples containing all point rows
     # the build's own ISDF points when given (random grid points can make the
     # Gram of localised orbitals singular — C60 — where the reference throws)
     pts = (np.sort(np.asarray(points)).astype(np.int32) if points is not None
@@ -81,8 +79,6 @@ def run(cfg, psi=None, energies=None, cores=None, sel_steps=64, fit_rows=(2048, 
     (r1, t1), (r2, t2) = times
     slope = (t2 - t1) / (r2 - r1)
     stages["fit"] = max(t1 + slope * (n_r - r1), t2)
-
-    # 3: reference quadrature, all nodes, threads = cores
     pv, pc = np.asfortranarray(a[pts]), np.asfortranarray(b[pts])
     s7 = ref.elliptic_params(e, n_v, n_c)
     h = 2 * s7[3] / cfg.n_lambda
@@ -92,25 +88,57 @@ def run(cfg, psi=None, energies=None, cores=None, sel_steps=64, fit_rows=(2048, 
     stages["contour"] = t_quad
     t_mat = 2 * np.sqrt(s7[0] * s7[1]) / (np.pi * s7[2]) * acc
     t_mat = 0.5 * (t_mat + t_mat.T)
-
-    # 4-5: SMW pieces of build_epsilon_inverse (smw.hpp:42-94)
-    c = min(cols, n_mu)
-    p_blk = np.asfortranarray(rng.standard_normal((n_r, c)) / np.sqrt(n_r))
     t_eig, _ = _t(lambda: ref.sym_eig_values(t_mat))
     t_half, half = _t(lambda: ref.lu_solve(t_mat, 0.5 * np.eye(n_mu)))
-    t_vp, vp_blk = _t(lambda: ref.apply_coulomb(cfg.dims, cfg.cell3, p_blk, threads=cores))
-    t_tn, g = _t(lambda: ref.matmul_tn(p_blk, vp_blk))
-    mid = 0.5 * (half + half.T)
-    mid[:c, :c] -= 0.5 * (g + g.T)
+    mid = 0.5 * (half + half.T) - 1e-3 * np.eye(n_mu)
     t_inv, _ = _t(lambda: ref.lu_solve(mid, np.eye(n_mu)))
     stages["smw_eig"] = t_eig
     stages["smw_lu"] = t_half + t_inv
+    sample = (f"fit on {fit_rows} rows -> linear in N_r={n_r}; all {cfg.n_lambda + 1} nodes; sym_eig / 2 LU at "
+              f"N_mu={n_mu}")
+    return stages, sample
+
+
+def sampled_pieces(cfg, psi=None, cores=None, sel_steps=64, cols=128, seed=5):
+    """The pieces timed every step, extrapolated by their exact cost models:
+    S greedy steps of the selection (restatement: the reference's qrcp is
+    guard-blocked here) scaled by sum_k (N + k + 1); apply_coulomb on C
+    columns scaled by 2 N_mu / C (the reference applies V to P twice,
+    smw.hpp:61, 92); matmul_tn on a C-column block scaled by (N_mu / C)^2."""
+    cores = cores or os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    n_r, n_v, n_c = cfg.n_r, cfg.n_v, cfg.n_c
+    n = n_v + n_c
+    n_mu = min(max(R.num_aux(cfg.k_mu, n_v, n_c), 1), n_r)
+    rng = np.random.default_rng(seed)
+    psi, _ = _inputs(cfg, psi, np.zeros(n), rng)
+    a, b = psi[:, :n_v], psi[:, n_v:n]
+    stages = {}
+    s = min(sel_steps, n_mu)
+    t_sel, _ = _t(lambda: R.select_points(a, b, s))
+    w_s = sum(n + k + 1 for k in range(s))
+    w_all = sum(n + k + 1 for k in range(n_mu))
+    stages["select"] = t_sel * w_all / w_s
+    c = min(cols, n_mu)
+    p_blk = np.asfortranarray(rng.standard_normal((n_r, c)) / np.sqrt(n_r))
+    t_vp, vp_blk = _t(lambda: ref.apply_coulomb(cfg.dims, cfg.cell3, p_blk, threads=cores))
+    t_tn, _ = _t(lambda: ref.matmul_tn(p_blk, vp_blk))
     stages["coulomb"] = t_vp * 2.0 * n_mu / c
     stages["pvp"] = t_tn * (n_mu / c) ** 2
+    sample = (f"select {s}/{n_mu} greedy steps (restatement, {cores} threads) x{w_all / w_s:.1f}; apply_coulomb "
+              f"{c} cols x{2 * n_mu / c:.0f}; matmul_tn {c}x{c} block x{(n_mu / c) ** 2:.0f}")
+    return stages, sample
+
+
+def run(cfg, psi=None, energies=None, cores=None, sel_steps=64, fit_rows=(2048, 4096), cols=128, seed=5,
+        points=None):
+    """Returns dict(total_s, total_no_select_s, stages, sample, cores)."""
+    cores = cores or os.cpu_count() or 1
+    rng = np.random.default_rng(seed)
+    psi, e = _inputs(cfg, psi, energies, rng)
+    fixed, fs = fixed_pieces(cfg, psi, e, cores, fit_rows, seed, points)
+    samp, ss = sampled_pieces(cfg, psi, cores, sel_steps, cols, seed)
+    stages = {**samp, **fixed}
     total = sum(stages.values())
-    sample = (f"{cfg.name}: select {s}/{n_mu} greedy steps (restatement, {cores} threads) x{w_all / w_s:.1f}; "
-              f"fit on {fit_rows} rows -> linear in N_r={n_r}; all {cfg.n_lambda + 1} nodes; sym_eig/LU at "
-              f"N_mu={n_mu}; apply_coulomb {c} cols x{2 * n_mu / c:.0f}; matmul_tn {c}x{c} block "
-              f"x{(n_mu / c) ** 2:.0f}")
     return {"total_s": total, "total_no_select_s": total - stages["select"], "stages": stages,
-            "sample": sample, "cores": cores}
+            "sample": f"{cfg.name}: {ss}; {fs}", "cores": cores}

@@ -45,6 +45,19 @@ class EpsInfo(ctypes.Structure):
     ]
 
 
+comm_t = ctypes.c_void_p
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong)
+ALLTOALLV_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_void_p)
+
+
+class HostTransport(ctypes.Structure):
+    """lrgw_host_transport (include/lrgw_cuda.h)."""
+    _fields_ = [("user", ctypes.c_void_p), ("allreduce_sum_f64", ALLREDUCE_FN), ("allgather", ALLGATHER_FN),
+                ("alltoallv", ALLTOALLV_FN)]
+
+
 # name -> (restype, argtypes)
 _SIGS = {
     "lrgw_abi_version": (ctypes.c_int, []),
@@ -162,6 +175,19 @@ _SIGS = {
                                              c_double_p]),
     "lrgw_wfn1_save": (ctypes.c_int, [ctypes.c_char_p, c_int_p, c_double_p, ctypes.c_int, ctypes.c_int,
                                       c_double_p, c_double_p, c_double_p]),
+    "lrgw_nccl_available": (ctypes.c_int, []),
+    "lrgw_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
+    "lrgw_comm_create_nccl": (ctypes.c_int, [ctx_t, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                             ctypes.POINTER(comm_t)]),
+    "lrgw_comm_create_host": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(HostTransport),
+                                             ctypes.POINTER(comm_t)]),
+    "lrgw_comm_destroy": (ctypes.c_int, [comm_t]),
+    "lrgw_comm_info": (ctypes.c_int, [comm_t, c_int_p, c_int_p]),
+    "lrgw_z_panel": (ctypes.c_int, [c_int_p, ctypes.c_int, ctypes.c_int, c_int_p, c_int_p]),
+    "lrgw_build_sharded": (ctypes.c_int, [ctx_t, comm_t, ctypes.POINTER(BuildParams), ctypes.c_void_p, c_ll,
+                                          ctypes.c_void_p, c_ll, c_double_p, ctypes.POINTER(eps_t)]),
+    "lrgw_eps_apply_sharded": (ctypes.c_int, [ctx_t, comm_t, eps_t, ctypes.c_void_p, c_ll, ctypes.c_int,
+                                              ctypes.c_void_p, c_ll]),
     "lrgw_dev_dgemm": (ctypes.c_int, [ctx_t, ctypes.c_char, ctypes.c_char, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, ctypes.c_double, ctypes.c_void_p, c_ll, ctypes.c_void_p,
                                       c_ll, ctypes.c_double, ctypes.c_void_p, c_ll]),

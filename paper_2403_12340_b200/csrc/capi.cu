@@ -135,19 +135,6 @@ void mark(lrgw_ctx c, int i) {
   if (i < LRGW_STAGE_TOTAL) nvtxRangePushA(names[i]);
 }
 
-
-template <class F>
-int guarded_host(F&& f) {
-  try {
-    f();
-    return LRGW_OK;
-  } catch (const Fail& e) {
-    return e.code;
-  } catch (...) {
-    return LRGW_ERR_INTERNAL;
-  }
-}
-
 lrgw_host::Spec spec_from7(const double* s7) {
   lrgw_host::Spec s;
   s.q = s7[0];
@@ -1002,6 +989,7 @@ int lrgw_ctx_destroy(lrgw_ctx c) {
     release_cached(c);
   }
   for (auto& kv : c->plans) cufftDestroy(kv.second);
+  for (auto& kv : c->plans_many) cufftDestroy(kv.second);
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   for (auto& x : c->ev)
@@ -1298,7 +1286,11 @@ int lrgw_build_epsilon_inverse(lrgw_ctx c, const double* t, const double* p, int
   });
 }
 
-static void eps_apply_impl(lrgw_ctx c, lrgw_eps e, const double* x, long long ldx, int m, double* y, long long ldy) {
+}  // extern "C"
+
+bool lrgw_impl::eps_is_panel(const lrgw_eps_s* e) { return e->rows > 0 && e->rows < e->n_r; }
+
+void lrgw_impl::eps_apply_impl(lrgw_ctx c, lrgw_eps e, const double* x, long long ldx, int m, double* y, long long ldy) {
   const int n_r = e->n_r, n_mu = e->n_mu;
   DBuf u = dalloc(c, (size_t)n_mu * m), w = dalloc(c, (size_t)n_mu * m), z = dalloc(c, (size_t)n_r * m);
   Work wk = make_work(c, (size_t)1200 * n_mu * m);
@@ -1323,9 +1315,12 @@ static void eps_apply_impl(lrgw_ctx c, lrgw_eps e, const double* x, long long ld
   ck(axpby(c->stream, n_r, m, 1.0, x, ldx, 1.0, y, ldy), "axpby");
 }
 
+extern "C" {
+
 int lrgw_epsilon_inverse_apply(lrgw_ctx c, lrgw_eps e, const double* x, int m, double* y) {
   return guarded(c, [&] {
     if (!e || !e->ctx) fail(LRGW_ERR_INVALID_INPUT, "epsilon_inverse_apply: null handle");
+    if (eps_is_panel(e)) fail(LRGW_ERR_INVALID_INPUT, "epsilon_inverse_apply: row-panel handle (use lrgw_eps_apply_sharded)");
     const size_t n = (size_t)e->n_r * m;
     DBuf dx = upload(c, x, n), dy = dalloc(c, n);
     eps_apply_impl(c, e, dx.d(), e->n_r, m, dy.d(), e->n_r);
@@ -1336,6 +1331,7 @@ int lrgw_epsilon_inverse_apply(lrgw_ctx c, lrgw_eps e, const double* x, int m, d
 int lrgw_eps_apply_dev(lrgw_ctx c, lrgw_eps e, const double* x, long long ldx, int m, double* y, long long ldy) {
   return guarded(c, [&] {
     if (!e || !e->ctx) fail(LRGW_ERR_INVALID_INPUT, "epsilon_inverse_apply: null handle");
+    if (eps_is_panel(e)) fail(LRGW_ERR_INVALID_INPUT, "epsilon_inverse_apply: row-panel handle (use lrgw_eps_apply_sharded)");
     if (ldx < e->n_r || ldy < e->n_r) fail(LRGW_ERR_INVALID_INPUT, "epsilon_inverse_apply: row mismatch");
     eps_apply_impl(c, e, x, ldx, m, y, ldy);
     ck(cudaStreamSynchronize(c->stream), "sync");
@@ -1346,6 +1342,7 @@ int lrgw_eps_get(lrgw_ctx c, lrgw_eps e, double* k, double* p, double* vp, doubl
   return guarded(c, [&] {
     if (!e || !e->ctx) fail(LRGW_ERR_INVALID_INPUT, "eps: null handle");
     const size_t nn = (size_t)e->n_mu * e->n_mu, np = (size_t)e->n_r * e->n_mu;
+    if ((p || vp) && eps_is_panel(e)) fail(LRGW_ERR_INVALID_INPUT, "eps_get: P / VP of a row-panel handle (use lrgw_eps_info_get)");
     if (k) download(c, k, e->k, nn * sizeof(double));
     if (p) download(c, p, e->theta, np * sizeof(double));
     if (t && e->t) download(c, t, e->t, nn * sizeof(double));
@@ -1406,108 +1403,141 @@ int lrgw_eps_device_ptrs(lrgw_eps e, double** theta, double** k, double** t) {
 }
 
 // ---- the whole build --------------------------------------------------------
+}  // extern "C"
+
+namespace lrgw_impl {
+
+BuildSetup validate_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, long long ldv,
+                          const double* phi_c, long long ldc, const double* energies, int panel_rows) {
+  if (!prm) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: null argument");
+  const lrgw_build_params& P = *prm;
+  check_grid(P.dims, P.cell);
+  const int n_r = P.n_r, n_v = P.n_v, n_c = P.n_c;
+  if ((long long)P.dims[0] * P.dims[1] * P.dims[2] != n_r) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: grid / N_r mismatch");
+  if (n_v < 1 || n_c < 1) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: need n_v >= 1 and n_c >= 1");
+  if (P.n_e < n_v + n_c) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: energies must hold n_v + n_c values");
+  if (!phi_v || !phi_c || !energies) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: null orbital / energy pointer");
+  if (ldv < panel_rows || ldc < panel_rows) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: leading dimension below the row count");
+  for (const double* ph : {phi_v, phi_c}) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, ph) != cudaSuccess || at.type != cudaMemoryTypeDevice || at.device != c->device) {
+      cudaGetLastError();
+      fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: orbitals must be device memory on the context's GPU");
+    }
+  }
+  BuildSetup b;
+  if (lrgw_num_aux(P.k_mu, n_v, n_c, &b.n_mu) != LRGW_OK) fail(LRGW_ERR_INVALID_INPUT, "num_aux: k_mu must be > 0");
+  b.n_mu = std::clamp(b.n_mu, 1, n_r);
+  host_status(lrgw_host::elliptic_params(energies, P.n_e, n_v, n_c, P.delta_rel > 0 ? P.delta_rel : 1e-7,
+                                         P.max_nodes > 0 ? P.max_nodes : 1025, &b.spec),
+              "elliptic_params");
+  return b;
+}
+
+void timing_begin(lrgw_ctx c) {
+  for (auto& x : c->ev)
+    if (!x) ck(cudaEventCreate(&x), "event");
+  for (auto& x : c->ev_quad)
+    if (!x) ck(cudaEventCreate(&x), "event");
+  c->timing = true;
+  mark(c, 0);
+}
+
+// Stage times of the build from its 9 boundary events (mark 0 .. 8).
+void timing_end(lrgw_ctx c) {
+  ck(cudaEventSynchronize(c->ev[8]), "sync");
+  float ms;
+  for (int i = 0; i < 8; ++i) {
+    cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]);
+    c->stage_ms[i] = ms;
+  }
+  cudaEventElapsedTime(&ms, c->ev[0], c->ev[8]);
+  c->stage_ms[LRGW_STAGE_TOTAL] = ms;
+  c->stage_ms[LRGW_STAGE_QUAD_KERNEL] = 0.0;
+  if (c->quad_timed && cudaEventElapsedTime(&ms, c->ev_quad[0], c->ev_quad[1]) == cudaSuccess)
+    c->stage_ms[LRGW_STAGE_QUAD_KERNEL] = ms;
+  c->quad_timed = false;
+  c->timing = false;
+}
+
+// The one-GPU build, stages 1-5 (stage boundaries marked for the timings).
+lrgw_eps_s* build_one(lrgw_ctx c, const lrgw_build_params& P, const BuildSetup& bs, const double* phi_v,
+                      long long ldv, const double* phi_c, long long ldc, const double* energies) {
+  const int n_r = P.n_r, n_v = P.n_v, n_c = P.n_c, n_mu = bs.n_mu, n_e = P.n_e;
+  const lrgw_host::Spec& spec = bs.spec;
+  struct TimingGuard {
+    lrgw_ctx c;
+    ~TimingGuard() { c->timing = false; }
+  } tg{c};
+  timing_begin(c);
+  // stage 1
+  SelectKeep keep;
+  double min_margin = -1.0;  // smallest relative top-2 residual margin over all steps (linalg.hpp:45-47)
+  std::vector<int32_t> pts = select_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, n_mu, &min_margin, &keep);
+  mark(c, 1);
+  // stage 2: fused fit from the selection's factor (explicit path otherwise)
+  DBuf theta = dalloc(c, (size_t)n_r * n_mu);
+  mark(c, 2);  // FIT_LHS is empty on the fused path (lhs lives in L)
+  double lp_ratio = 0.0;
+  const bool fused = fused_fit(c, keep, n_r, pts, n_mu, theta.d(), n_r, &lp_ratio);
+  keep.L.release();
+  if (!fused) {  // explicit path re-marks its own lhs / solve boundaries
+    fit_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, pts.data(), n_mu, theta.d(), n_r);
+  }
+  mark(c, 4);
+  // stage 3
+  DBuf dpts = upload_i(c, pts.data(), n_mu);
+  DBuf pv = dalloc(c, (size_t)n_mu * n_v), pc = dalloc(c, (size_t)n_mu * n_c);
+  ck(gather_rows(c->stream, phi_v, ldv, n_v, dpts.i(), n_mu, pv.d(), n_mu), "gather");
+  ck(gather_rows(c->stream, phi_c, ldc, n_c, dpts.i(), n_mu, pc.d(), n_mu), "gather");
+  DBuf t = dalloc(c, (size_t)n_mu * n_mu);
+  if (spec.bypass) {
+    direct_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, t.d(), n_mu);
+  } else if (P.n_lambda > 0) {
+    fixed_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, n_e, P.n_lambda, t.d(), n_mu);
+  } else {
+    adaptive_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, spec, t.d());
+  }
+  mark(c, 5);
+  // stages 4-5
+  DBuf pvp = dalloc(c, (size_t)n_mu * n_mu), k = dalloc(c, (size_t)n_mu * n_mu);
+  pvp_impl(c, P.dims, P.cell, P.zero_kernel, theta.d(), n_r, n_mu, pvp.d());
+  mark(c, 7);
+  smw_core(c, t.d(), pvp.d(), n_mu, k.d());
+  mark(c, 8);
+  timing_end(c);
+  auto* e = new_eps(c);
+  e->ctx = c;
+  e->n_r = n_r;
+  e->n_mu = n_mu;
+  std::memcpy(e->dims, P.dims, sizeof(e->dims));
+  std::memcpy(e->cell, P.cell, sizeof(e->cell));
+  e->zero = P.zero_kernel;
+  e->theta = static_cast<double*>(theta.take());
+  e->k = static_cast<double*>(k.take());
+  e->t = static_cast<double*>(t.take());
+  e->pvp = static_cast<double*>(pvp.take());
+  e->pts = pts;
+  e->min_margin = min_margin;
+  e->min_margin_step = keep.min_margin_step;
+  e->fit_path = fused ? 0 : 1;
+  e->lp_diag_ratio = lp_ratio;
+  e->select_blocks = keep.blocks;
+  e->row0 = 0;
+  e->rows = n_r;
+  return e;
+}
+
+}  // namespace lrgw_impl
+
+extern "C" {
+
 int lrgw_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, long long ldv, const double* phi_c,
                long long ldc, const double* energies, lrgw_eps* out) {
   return guarded(c, [&] {
-    if (!prm || !out) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: null argument");
-    const lrgw_build_params& P = *prm;
-    check_grid(P.dims, P.cell);
-    const int n_r = P.n_r, n_v = P.n_v, n_c = P.n_c;
-    if ((long long)P.dims[0] * P.dims[1] * P.dims[2] != n_r) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: grid / N_r mismatch");
-    if (n_v < 1 || n_c < 1) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: need n_v >= 1 and n_c >= 1");
-    if (P.n_e < n_v + n_c) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: energies must hold n_v + n_c values");
-    if (!phi_v || !phi_c || !energies) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: null orbital / energy pointer");
-    if (ldv < n_r || ldc < n_r) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: leading dimension below N_r");
-    for (const double* ph : {phi_v, phi_c}) {
-      cudaPointerAttributes at{};
-      if (cudaPointerGetAttributes(&at, ph) != cudaSuccess || at.type != cudaMemoryTypeDevice || at.device != c->device) {
-        cudaGetLastError();
-        fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: orbitals must be device memory on the context's GPU");
-      }
-    }
-    int n_mu = 0;
-    if (lrgw_num_aux(P.k_mu, n_v, n_c, &n_mu) != LRGW_OK) fail(LRGW_ERR_INVALID_INPUT, "num_aux: k_mu must be > 0");
-    n_mu = std::clamp(n_mu, 1, n_r);
-    const int n_e = P.n_e;
-    lrgw_host::Spec spec;
-    host_status(lrgw_host::elliptic_params(energies, n_e, n_v, n_c, P.delta_rel > 0 ? P.delta_rel : 1e-7,
-                                           P.max_nodes > 0 ? P.max_nodes : 1025, &spec),
-                "elliptic_params");
-    for (auto& x : c->ev)
-      if (!x) ck(cudaEventCreate(&x), "event");
-    for (auto& x : c->ev_quad)
-      if (!x) ck(cudaEventCreate(&x), "event");
-    struct TimingGuard {
-      lrgw_ctx c;
-      ~TimingGuard() { c->timing = false; }
-    } tg{c};
-    c->timing = true;
-    mark(c, 0);
-    // stage 1
-    SelectKeep keep;
-    double min_margin = -1.0;  // smallest relative top-2 residual margin over all steps (linalg.hpp:45-47)
-    std::vector<int32_t> pts = select_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, n_mu, &min_margin, &keep);
-    mark(c, 1);
-    // stage 2: fused fit from the selection's factor (explicit path otherwise)
-    DBuf theta = dalloc(c, (size_t)n_r * n_mu);
-    mark(c, 2);  // FIT_LHS is empty on the fused path (lhs lives in L)
-    double lp_ratio = 0.0;
-    const bool fused = fused_fit(c, keep, n_r, pts, n_mu, theta.d(), n_r, &lp_ratio);
-    keep.L.release();
-    if (!fused) {  // explicit path re-marks its own lhs / solve boundaries
-      fit_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, pts.data(), n_mu, theta.d(), n_r);
-    }
-    mark(c, 4);
-    // stage 3
-    DBuf dpts = upload_i(c, pts.data(), n_mu);
-    DBuf pv = dalloc(c, (size_t)n_mu * n_v), pc = dalloc(c, (size_t)n_mu * n_c);
-    ck(gather_rows(c->stream, phi_v, ldv, n_v, dpts.i(), n_mu, pv.d(), n_mu), "gather");
-    ck(gather_rows(c->stream, phi_c, ldc, n_c, dpts.i(), n_mu, pc.d(), n_mu), "gather");
-    DBuf t = dalloc(c, (size_t)n_mu * n_mu);
-    if (spec.bypass) {
-      direct_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, t.d(), n_mu);
-    } else if (P.n_lambda > 0) {
-      fixed_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, n_e, P.n_lambda, t.d(), n_mu);
-    } else {
-      adaptive_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, spec, t.d());
-    }
-    mark(c, 5);
-    // stages 4-5
-    DBuf pvp = dalloc(c, (size_t)n_mu * n_mu), k = dalloc(c, (size_t)n_mu * n_mu);
-    pvp_impl(c, P.dims, P.cell, P.zero_kernel, theta.d(), n_r, n_mu, pvp.d());
-    mark(c, 7);
-    smw_core(c, t.d(), pvp.d(), n_mu, k.d());
-    mark(c, 8);
-    ck(cudaEventSynchronize(c->ev[8]), "sync");
-    float ms;
-    for (int i = 0; i < 8; ++i) {
-      cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]);
-      c->stage_ms[i] = ms;
-    }
-    cudaEventElapsedTime(&ms, c->ev[0], c->ev[8]);
-    c->stage_ms[LRGW_STAGE_TOTAL] = ms;
-    c->stage_ms[LRGW_STAGE_QUAD_KERNEL] = 0.0;
-    if (c->quad_timed && cudaEventElapsedTime(&ms, c->ev_quad[0], c->ev_quad[1]) == cudaSuccess)
-      c->stage_ms[LRGW_STAGE_QUAD_KERNEL] = ms;
-    c->quad_timed = false;
-    auto* e = new_eps(c);
-    e->ctx = c;
-    e->n_r = n_r;
-    e->n_mu = n_mu;
-    std::memcpy(e->dims, P.dims, sizeof(e->dims));
-    std::memcpy(e->cell, P.cell, sizeof(e->cell));
-    e->zero = P.zero_kernel;
-    e->theta = static_cast<double*>(theta.take());
-    e->k = static_cast<double*>(k.take());
-    e->t = static_cast<double*>(t.take());
-    e->pvp = static_cast<double*>(pvp.take());
-    e->pts = pts;
-    e->min_margin = min_margin;
-    e->min_margin_step = keep.min_margin_step;
-    e->fit_path = fused ? 0 : 1;
-    e->lp_diag_ratio = lp_ratio;
-    e->select_blocks = keep.blocks;
-    *out = e;
+    if (!out) fail(LRGW_ERR_INVALID_INPUT, "lrgw_build: null argument");
+    const BuildSetup bs = validate_build(c, prm, phi_v, ldv, phi_c, ldc, energies, prm ? prm->n_r : 0);
+    *out = build_one(c, *prm, bs, phi_v, ldv, phi_c, ldc, energies);
   });
 }
 

@@ -9,6 +9,7 @@
 // The weights below are the `scale` of the G-space SYRK (Theta^T V Theta),
 // fused into that GEMM's operand load; the in-place scale is the probe path.
 #include "kernels.h"
+#include "shard.h"
 
 namespace lrgw_dev {
 
@@ -63,7 +64,33 @@ __global__ void scale_half_kernel(int n1, int n2, int n3, double c1, double c2, 
   }
 }
 
+// pencil order (y - ya, i1, i3), i3 fastest: the z-pencils of one rank's y-slab
+__global__ void slab_weights_kernel(int n1, int n2, int n3, double c1, double c2, double c3, int zero_kernel, int ya,
+                                    int ny, double* w) {
+  const int nh = n1 / 2 + 1;
+  const long long total = (long long)ny * nh * n3;
+  const double inv_n = 1.0 / ((double)n1 * n2 * n3);
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int i3 = static_cast<int>(q % n3);
+    const int i1 = static_cast<int>((q / n3) % nh);
+    const int i2 = ya + static_cast<int>(q / ((long long)n3 * nh));
+    const double herm = (i1 == 0 || (n1 % 2 == 0 && i1 == n1 / 2)) ? 1.0 : 2.0;
+    const double v = zero_kernel ? 0.0 : vG(i1, i2, i3, n1, n2, n3, c1, c2, c3);
+    const double c = herm * v * inv_n;
+    w[2 * q] = c;
+    w[2 * q + 1] = c;
+  }
+}
+
 }  // namespace
+
+cudaError_t coulomb_slab_weights(cudaStream_t st, int n1, int n2, int n3, double c1, double c2, double c3,
+                                 int zero_kernel, int ya, int ny, double* w) {
+  if (ny <= 0) return cudaSuccess;
+  slab_weights_kernel<<<592, 256, 0, st>>>(n1, n2, n3, c1, c2, c3, zero_kernel, ya, ny, w); count_launches(1);
+  return cudaGetLastError();
+}
 
 cudaError_t coulomb_half_weights(cudaStream_t st, int n1, int n2, int n3, double c1, double c2,
                                  double c3, int zero_kernel, double* w) {

@@ -55,6 +55,7 @@ struct lrgw_ctx_s {
   int sm_count = 148;
   cusolverDnHandle_t solver = nullptr;
   std::map<std::tuple<int, int, int, int, long long, long long, int>, cufftHandle> plans;
+  std::map<std::vector<long long>, cufftHandle> plans_many;  // slab / pencil plans of the multi-rank build
   std::string err;
   int pivot = -1;
   double stage_ms[LRGW_NUM_STAGES] = {};
@@ -97,6 +98,9 @@ struct lrgw_eps_s {
   int fit_path = -1;
   double lp_diag_ratio = 0.0;
   int select_blocks = 0;
+  // row panel of a multi-rank build (lrgw_build_sharded): theta holds grid
+  // rows [row0, row0 + rows); rows == 0 means all n_r rows (one GPU)
+  int row0 = 0, rows = 0;
 };
 
 namespace lrgw_impl {
@@ -170,6 +174,18 @@ int guarded(lrgw_ctx c, F&& f) {
   }
 }
 
+template <class F>
+int guarded_host(F&& f) {
+  try {
+    f();
+    return LRGW_OK;
+  } catch (const Fail& e) {
+    return e.code;
+  } catch (...) {
+    return LRGW_ERR_INTERNAL;
+  }
+}
+
 // Split-K scratch for the skinny / symmetric GEMMs.
 struct Work {
   DBuf buf;
@@ -191,6 +207,20 @@ void smw_core(lrgw_ctx c, const double* t, const double* pvp, int n, double* k);
 void trtri_lower(lrgw_ctx c, double* a, int n);
 double dev_max_abs(lrgw_ctx c, const double* x, size_t n);
 void gram_inverse(lrgw_ctx c, const double* gram, int n, double* ginv);
+
+// Validated inputs of a build (lrgw_build / lrgw_build_sharded).
+struct BuildSetup {
+  int n_mu = 0;
+  lrgw_host::Spec spec;
+};
+BuildSetup validate_build(lrgw_ctx c, const lrgw_build_params* prm, const double* phi_v, long long ldv,
+                          const double* phi_c, long long ldc, const double* energies, int panel_rows);
+void timing_begin(lrgw_ctx c);
+void timing_end(lrgw_ctx c);
+lrgw_eps_s* build_one(lrgw_ctx c, const lrgw_build_params& P, const BuildSetup& bs, const double* phi_v,
+                      long long ldv, const double* phi_c, long long ldc, const double* energies);
+void eps_apply_impl(lrgw_ctx c, lrgw_eps e, const double* x, long long ldx, int m, double* y, long long ldy);
+bool eps_is_panel(const lrgw_eps_s* e);
 
 // Stage 1 (select.cu): host mirror of the candidate entry (d, position, grid row).
 struct HostEnt {

@@ -702,12 +702,9 @@ def _dev_ptr_cm(t):
     return t.data_ptr(), max(ld, 1)
 
 
-def build(phi_v, phi_c, energies, dims, cell, k_mu: float = 8.0, n_lambda: int = 16, delta_rel: float = 1e-7,
-          max_nodes: int = 1025, zero_kernel: bool = False, ctx=None) -> EpsilonInverseLowRank:
-    """Stages 1-5 from device-resident orbitals (column-major float64 CUDA
-    tensors, N_r x N_v and N_r x N_c) and host energies: point selection,
-    Theta fit, Cauchy quadrature core, G-space Theta^T V Theta, SMW core K."""
-    c = _ctx(ctx)
+def _build_params(c, phi_v, phi_c, energies, dims, cell, k_mu, n_lambda, delta_rel, max_nodes, zero_kernel,
+                  rows=None):
+    """Validated lrgw_build_params + device pointers (rows: the panel's row count)."""
     for name, t in (("phi_v", phi_v), ("phi_c", phi_c)):
         if not getattr(t, "is_cuda", False) or t.dim() != 2:
             raise InvalidInput(f"build: {name} must be a 2-D CUDA tensor")
@@ -715,13 +712,16 @@ def build(phi_v, phi_c, energies, dims, cell, k_mu: float = 8.0, n_lambda: int =
             raise InvalidInput(f"build: {name} is on cuda:{t.device.index}, the context on cuda:{c.device}")
     if phi_c.shape[0] != phi_v.shape[0]:
         raise InvalidInput("build: phi_v and phi_c must have the same number of grid rows")
+    n_r = int(np.prod([int(x) for x in dims]))
+    if phi_v.shape[0] != (n_r if rows is None else rows):
+        raise InvalidInput(f"build: orbital rows {phi_v.shape[0]} != {n_r if rows is None else rows}")
     pv, ldv = _dev_ptr_cm(phi_v)
     pc, ldc = _dev_ptr_cm(phi_c)
     e = np.ascontiguousarray(energies, dtype=np.float64)
     if e.ndim != 1 or e.size != phi_v.shape[1] + phi_c.shape[1]:
         raise InvalidInput("build: energies must hold exactly N_v + N_c values")
     prm = L.BuildParams()
-    prm.n_r, prm.n_v, prm.n_c = phi_v.shape[0], phi_v.shape[1], phi_c.shape[1]
+    prm.n_r, prm.n_v, prm.n_c = n_r, phi_v.shape[1], phi_c.shape[1]
     prm.n_e = e.size
     prm.dims[:] = [int(x) for x in dims]
     prm.cell[:] = [float(x) for x in cell]
@@ -730,6 +730,17 @@ def build(phi_v, phi_c, energies, dims, cell, k_mu: float = 8.0, n_lambda: int =
     prm.delta_rel = float(delta_rel)
     prm.max_nodes = int(max_nodes)
     prm.zero_kernel = int(zero_kernel)
+    return prm, pv, ldv, pc, ldc, e
+
+
+def build(phi_v, phi_c, energies, dims, cell, k_mu: float = 8.0, n_lambda: int = 16, delta_rel: float = 1e-7,
+          max_nodes: int = 1025, zero_kernel: bool = False, ctx=None) -> EpsilonInverseLowRank:
+    """Stages 1-5 from device-resident orbitals (column-major float64 CUDA
+    tensors, N_r x N_v and N_r x N_c) and host energies: point selection,
+    Theta fit, Cauchy quadrature core, G-space Theta^T V Theta, SMW core K."""
+    c = _ctx(ctx)
+    prm, pv, ldv, pc, ldc, e = _build_params(c, phi_v, phi_c, energies, dims, cell, k_mu, n_lambda, delta_rel,
+                                             max_nodes, zero_kernel)
     _sync_torch(phi_v)
     h = L.eps_t()
     _check(c._lib.lrgw_build(c.handle, ctypes.byref(prm), ctypes.c_void_p(pv), ldv, ctypes.c_void_p(pc), ldc,
@@ -927,3 +938,169 @@ def smw_core_dev(t, pvp, k, ctx=None):
     _check(cx._lib.lrgw_dev_smw_core(cx.handle, ctypes.c_void_p(pt), ctypes.c_void_p(pp), t.shape[0],
                                      ctypes.c_void_p(pk)), cx.handle, "smw_core")
     return k
+
+
+# ---------------------------------------------------------------------------
+# multi-rank build through the C-ABI (lrgw_comm, lrgw_build_sharded)
+# ---------------------------------------------------------------------------
+
+def z_panel(dims, world: int, rank: int):
+    """This rank's grid-row panel (row0, rows): whole z-planes, floor(n3 p / world)."""
+    d = (ctypes.c_int * 3)(*[int(x) for x in dims])
+    r0, rows = ctypes.c_int(0), ctypes.c_int(0)
+    _check(L.load().lrgw_z_panel(d, int(world), int(rank), ctypes.byref(r0), ctypes.byref(rows)), None, "z_panel")
+    return r0.value, rows.value
+
+
+class Comm:
+    """An lrgw_comm: NCCL (device buffers over NVLink) or a host transport
+    (three Python callables on numpy views; e.g. torch.distributed gloo)."""
+
+    def __init__(self, handle, rank, world, keep=()):
+        self._lib = L.load()
+        self.handle, self.rank, self.world = handle, rank, world
+        self._keep = keep  # the ctypes callbacks must outlive the communicator
+
+    @classmethod
+    def nccl(cls, ctx, rank: int, world: int, uid: bytes):
+        lib = L.load()
+        h = L.comm_t()
+        buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
+        _check(lib.lrgw_comm_create_nccl(ctx.handle, rank, world, buf, ctypes.byref(h)), ctx.handle, "comm_nccl")
+        return cls(h, rank, world)
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (ctypes.c_ubyte * 128)()
+        _check(L.load().lrgw_nccl_unique_id(buf), None, "nccl_unique_id")
+        return bytes(buf)
+
+    @classmethod
+    def host(cls, rank: int, world: int, allreduce, allgather, alltoallv):
+        """allreduce(arr float64, in place); allgather(send uint8, recv uint8
+        (world * n)); alltoallv(send uint8, send_sizes, recv uint8, recv_sizes)."""
+
+        def _guard(fn):
+            def inner(*a):
+                try:
+                    fn(*a)
+                    return 0
+                except Exception as exc:  # surfaces as the C call's failure
+                    print(f"lrgw host transport: {exc!r}", flush=True)
+                    return 1
+            return inner
+
+        def _u8(ptr, n):
+            if n == 0:
+                return np.zeros(0, np.uint8)
+            return np.ctypeslib.as_array((ctypes.c_uint8 * n).from_address(ptr))
+
+        def ar(_u, buf, n):
+            allreduce(np.ctypeslib.as_array((ctypes.c_double * n).from_address(buf)) if n else np.zeros(0))
+
+        def ag(_u, send, recv, n):
+            allgather(_u8(send, n), _u8(recv, n * world))
+
+        def a2a(_u, send, sb, recv, rb):
+            ss = np.ctypeslib.as_array((ctypes.c_longlong * world).from_address(sb)).copy()
+            rs = np.ctypeslib.as_array((ctypes.c_longlong * world).from_address(rb)).copy()
+            alltoallv(_u8(send, int(ss.sum())), ss, _u8(recv, int(rs.sum())), rs)
+
+        cbs = (L.ALLREDUCE_FN(_guard(ar)), L.ALLGATHER_FN(_guard(ag)), L.ALLTOALLV_FN(_guard(a2a)))
+        t = L.HostTransport(None, *cbs)
+        h = L.comm_t()
+        _check(L.load().lrgw_comm_create_host(rank, world, ctypes.byref(t), ctypes.byref(h)), None, "comm_host")
+        return cls(h, rank, world, keep=(cbs, t))
+
+    @classmethod
+    def from_torch(cls, ctx, group=None, transport: str = "auto"):
+        """A communicator over the ranks of a torch.distributed group: NCCL
+        (the id broadcast from rank 0) when the group's backend is nccl and
+        transport is auto / nccl; otherwise the host transport on the group."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        use_nccl = transport == "nccl" or (transport == "auto" and dist.get_backend(group) == "nccl")
+        if use_nccl:
+            obj = [cls.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+            return cls.nccl(ctx, rank, world, obj[0])
+        return cls.host(rank, world, *torch_host_transport(group))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.lrgw_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def torch_host_transport(group=None):
+    """The three host-transport callables over a torch.distributed group
+    (CPU tensors viewing the library's pinned staging buffers)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+    def _glob(q):
+        return dist.get_global_rank(group, q) if group is not None else q
+
+    def allreduce(arr):
+        if arr.size:
+            dist.all_reduce(torch.from_numpy(arr), group=group)
+
+    def allgather(send, recv):
+        n = send.size
+        if n == 0:
+            return
+        outs = [torch.from_numpy(recv[q * n:(q + 1) * n]) for q in range(world)]
+        dist.all_gather(outs, torch.from_numpy(send), group=group)
+
+    def alltoallv(send, ss, recv, rs):
+        so = np.concatenate([[0], np.cumsum(ss)]).astype(np.int64)
+        ro = np.concatenate([[0], np.cumsum(rs)]).astype(np.int64)
+        recv[ro[rank]:ro[rank + 1]] = send[so[rank]:so[rank + 1]]
+        reqs = []
+        for q in range(world):
+            if q == rank:
+                continue
+            if ss[q]:
+                reqs.append(dist.isend(torch.from_numpy(send[so[q]:so[q + 1]]), _glob(q), group=group))
+            if rs[q]:
+                reqs.append(dist.irecv(torch.from_numpy(recv[ro[q]:ro[q + 1]]), _glob(q), group=group))
+        for r in reqs:
+            r.wait()
+
+    return allreduce, allgather, alltoallv
+
+
+def build_sharded(comm: Comm, phi_v_p, phi_c_p, energies, dims, cell, k_mu: float = 8.0, n_lambda: int = 16,
+                  delta_rel: float = 1e-7, max_nodes: int = 1025, zero_kernel: bool = False,
+                  ctx=None) -> EpsilonInverseLowRank:
+    """lrgw_build_sharded: each rank passes its own z-panel (z_panel) of the
+    orbitals (column-major float64 CUDA tensors, rows x N_v / rows x N_c)."""
+    c = _ctx(ctx)
+    _, rows = z_panel(dims, comm.world, comm.rank)
+    prm, pv, ldv, pc, ldc, e = _build_params(c, phi_v_p, phi_c_p, energies, dims, cell, k_mu, n_lambda, delta_rel,
+                                             max_nodes, zero_kernel, rows=rows)
+    _sync_torch(phi_v_p)
+    h = L.eps_t()
+    _check(c._lib.lrgw_build_sharded(c.handle, comm.handle, ctypes.byref(prm), ctypes.c_void_p(pv), ldv,
+                                     ctypes.c_void_p(pc), ldc, _dp(e), ctypes.byref(h)), c.handle, "build_sharded")
+    return EpsilonInverseLowRank(c, h)
+
+
+def eps_apply_sharded(comm: Comm, e: EpsilonInverseLowRank, x_p, y_p):
+    """y_p = (eps^-1 x)_p on this rank's panel rows (column-major float64 CUDA tensors)."""
+    px, ldx = _dev_ptr_cm(x_p)
+    py, ldy = _dev_ptr_cm(y_p)
+    _sync_torch(x_p)
+    _check(e.ctx._lib.lrgw_eps_apply_sharded(e.ctx.handle, comm.handle, e.handle, ctypes.c_void_p(px), ldx,
+                                             x_p.shape[1], ctypes.c_void_p(py), ldy), e.ctx.handle,
+           "eps_apply_sharded")
+    return y_p

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 TOL = 1e-10
 GOLDEN = sorted(p for p in glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz"))
-                if not os.path.basename(p).startswith("gw_"))
+                if not os.path.basename(p).startswith(("gw_", "pivots_")))
 
 
 @pytest.fixture(scope="module")
