@@ -402,6 +402,13 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
   if (cin && (lower || work || !cin_map)) return cudaErrorInvalidValue;
   if ((tri_b || colmap || n_dev) && (lower || work)) return cudaErrorInvalidValue;
   const bool ak = la == Lay::K, bk = lb == Lay::K;
+  // TMA-fed engine for MN-contiguous operands when the tile grid fills the chip
+  if (!ak && !bk && !lower && !scale && !cin && tma_gemm_enabled() &&
+      (long long)((M + 127) / 128) * ((N + 127) / 128) >= sm_count) {
+    const cudaError_t e = dgemm_tma(st, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, tri_b, colmap, n_dev);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();
+  }
   // 16-byte cp.async needs aligned bases, even leading dims and even extents
   // along the contiguous axis.
   // (an odd M / N is fine with a padded even ld: the straddling pair only
@@ -572,6 +579,11 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
                           long long lda2, const double* b2, long long ldb2, int k2, double* C,
                           long long ldc, double alpha, double beta) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  if (tma_gemm_enabled() && (long long)((M + 63) / 64) >= 2 * 148) {
+    const cudaError_t e = hadamard_tma(st, M, N, a1, lda1, b1, ldb1, k1, a2, lda2, b2, ldb2, k2, C, ldc, alpha, beta);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();
+  }
   HadamardParams p{M, N, k1, k2, a1, b1, a2, b2, lda1, ldb1, lda2, ldb2, C, ldc, alpha, beta};
   const bool vec = aligned16(a1) && aligned16(b1) && aligned16(a2) && aligned16(b2) &&
              lda1 % 2 == 0 && ldb1 % 2 == 0 && lda2 % 2 == 0 && ldb2 % 2 == 0 &&

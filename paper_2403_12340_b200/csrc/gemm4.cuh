@@ -1,0 +1,253 @@
+// gemm4.cuh — TMA-fed FP64 DMMA GEMM for MN-contiguous operands.
+//
+//   C = alpha * A B^T [o (A2 B2^T)] + beta * C,   A: M x K, B: N x K column-major
+//
+// The Blackwell-native staging of the path's tall GEMMs (the fused fit
+// Theta = L L_P^-1, the selection's L-pass and W columns): one producer warp
+// issues cp.async.bulk.tensor (TMA) loads of 16-row x BK-deep boxes of A and B
+// into a STAGES-deep shared-memory ring and arms an mbarrier per stage with
+// the stage's byte count; the consumer warps wait on that barrier, run the
+// DMMA.8x8x4 mainloop and release the slot through a second mbarrier. No
+// per-thread address arithmetic or LDGSTS in the mainloop, no CTA barrier
+// per k-tile; out-of-range rows / k are zero-filled by the TMA unit.
+//
+// Shared layout: each box is BK rows of 128 bytes (16 doubles) written with
+// CU_TENSOR_MAP_SWIZZLE_128B — 16-byte chunk c of row k lands at chunk
+// c ^ (k & 7). The paired fragments of gemm2.cuh (rows 2g, 2g + 1 of a
+// 16-row group in one LDS.128; k order permuted to 8p + 2t, 8p + 2t + 1) read
+// chunk g of rows k: across a quarter-warp (g in {2q, 2q+1}, t = 0..3,
+// k & 7 = 2t or 2t + 1) the swizzled chunks g ^ (k & 7) are 8 distinct
+// chunks — conflict-free without padding.
+#pragma once
+
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace lrgw_dev {
+
+struct Dgemm4Params {
+  int M, N, K, K2;  // K2 > 0: Hadamard second phase (maps A2 / B2)
+  double* C;
+  long long ldc;
+  double alpha, beta;
+  int tri_b;           // B(n, k) == 0 for k < n: K starts at the tile's n0
+  const int* colmap;   // output column n -> colmap[n]
+  const int* n_dev;    // device-side bound on N
+  int vec_store;       // C 16-byte aligned with even ldc: paired double2 stores
+};
+
+template <int BM_, int BN_, int WM_, int WN_, int BK_, int STAGES_, bool HAD_, int MINB_>
+struct Gemm4Cfg {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, BK = BK_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr bool HAD = HAD_;
+  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  static constexpr int CWARPS = WARPS_M * WARPS_N;  // consumers; + 1 producer warp
+  static constexpr int THREADS = 32 * (CWARPS + 1);
+  static constexpr int FM = WM / 8, FN = WN / 8;
+  static constexpr int BOX = BK * 16;  // doubles per 16-row box
+  static constexpr int A_BOXES = BM / 16, B_BOXES = BN / 16;
+  static constexpr int STAGE_ELEMS = (A_BOXES + B_BOXES) * BOX;
+  static constexpr unsigned STAGE_BYTES = STAGE_ELEMS * 8;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_ELEMS * 8 + 1024 /* 1024-B alignment */ + 2 * STAGES * 8;
+  static_assert(BM % 16 == 0 && BN % 16 == 0 && WM % 16 == 0 && WN % 16 == 0, "16-row boxes / pairs");
+  static_assert(BK % 8 == 0, "k pairs, 1024-B aligned boxes");
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 2-D TMA load of box (c0 = row, c1 = k) into shared memory, completing on bar.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// Paired fragments of k steps 8p + 2t and 8p + 2t + 1 for FR 8-row MMA tiles
+// whose 16-row groups start at local row w (tile 2j: rows w + 16j + 2g,
+// tile 2j + 1: the next row), from a swizzled [box][BK][16] stage.
+template <int FR, int BK>
+__device__ __forceinline__ void load_frag_swz(const double* s, int w, int p, int g, int t, double (&f0)[FR],
+                                              double (&f1)[FR]) {
+  const int k0 = 8 * p + 2 * t, k1 = k0 + 1;
+#pragma unroll
+  for (int j = 0; j < FR / 2; ++j) {
+    const double* box = s + ((w >> 4) + j) * (BK * 16);
+    const double2 v0 = *reinterpret_cast<const double2*>(box + k0 * 16 + 2 * (g ^ (k0 & 7)));
+    const double2 v1 = *reinterpret_cast<const double2*>(box + k1 * 16 + 2 * (g ^ (k1 & 7)));
+    f0[2 * j] = v0.x;
+    f0[2 * j + 1] = v0.y;
+    f1[2 * j] = v1.x;
+    f1[2 * j + 1] = v1.y;
+  }
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
+    dgemm4_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                  const __grid_constant__ CUtensorMap map_a2, const __grid_constant__ CUtensorMap map_b2,
+                  Dgemm4Params p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
+  constexpr int FM = Cfg::FM, FN = Cfg::FN;
+  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * Cfg::STAGE_ELEMS);
+  uint64_t* empty = full + STAGES;
+
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;  // N tiles fastest (A panel reuse in L2)
+  int N = p.N;
+  if (p.n_dev) N = min(N, *p.n_dev);
+  if (n0 >= N) return;
+  const int kb = p.tri_b ? (n0 / BK) * BK : 0;
+  const int kt1 = p.K > kb ? (p.K - kb + BK - 1) / BK : 0;
+  const int kt2 = Cfg::HAD ? (p.K2 + BK - 1) / BK : 0;
+  const int nkt = kt1 + kt2;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, Cfg::CWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == Cfg::CWARPS) {
+    // ===== producer: one elected lane issues every TMA of the ring =====
+    if (lane == 0) {
+      tma_prefetch_desc(&map_a);
+      tma_prefetch_desc(&map_b);
+      if (Cfg::HAD) {
+        tma_prefetch_desc(&map_a2);
+        tma_prefetch_desc(&map_b2);
+      }
+      for (int kt = 0; kt < nkt; ++kt) {
+        const int s = kt % STAGES;
+        if (kt >= STAGES) mbar_wait(empty + s, ((kt / STAGES) - 1) & 1);
+        double* sa = ring + s * Cfg::STAGE_ELEMS;
+        double* sb = sa + Cfg::A_BOXES * Cfg::BOX;
+        mbar_arrive_expect_tx(full + s, Cfg::STAGE_BYTES);
+        const bool ph2 = Cfg::HAD && kt >= kt1;
+        const CUtensorMap* ma = ph2 ? &map_a2 : &map_a;
+        const CUtensorMap* mb = ph2 ? &map_b2 : &map_b;
+        const int k0 = ph2 ? (kt - kt1) * BK : kb + kt * BK;
+#pragma unroll
+        for (int b = 0; b < Cfg::A_BOXES; ++b) tma_load_2d(sa + b * Cfg::BOX, ma, full + s, m0 + 16 * b, k0);
+#pragma unroll
+        for (int b = 0; b < Cfg::B_BOXES; ++b) tma_load_2d(sb + b * Cfg::BOX, mb, full + s, n0 + 16 * b, k0);
+      }
+    }
+    return;
+  }
+
+  // ===== consumers =====
+  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM, wn = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int g = lane >> 2, t = lane & 3;
+  const bool live = n0 + wn < N;
+  double acc[FM][FN][2];
+  double first[Cfg::HAD ? FM : 1][Cfg::HAD ? FN : 1][2];
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int kt = 0; kt < nkt; ++kt) {
+    const int s = kt % STAGES;
+    if (Cfg::HAD && kt == kt1) {  // the first product waits in registers
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) {
+          first[i][j][0] = acc[i][j][0];
+          first[i][j][1] = acc[i][j][1];
+          acc[i][j][0] = acc[i][j][1] = 0.0;
+        }
+    }
+    mbar_wait(full + s, (kt / STAGES) & 1);
+    if (live) {
+      const double* sa = ring + s * Cfg::STAGE_ELEMS;
+      const double* sb = sa + Cfg::A_BOXES * Cfg::BOX;
+#pragma unroll
+      for (int pp = 0; pp < BK / 8; ++pp) {
+        double a0[FM], a1[FM], b0[FN], b1[FN];
+        load_frag_swz<FM, BK>(sa, wm, pp, g, t, a0, a1);
+        load_frag_swz<FN, BK>(sb, wn, pp, g, t, b0, b1);
+        dmma_block<FM, FN>(acc, a0, b0);
+        dmma_block<FM, FN>(acc, a1, b1);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
+  }
+  if (!live) return;
+  if (Cfg::HAD) {
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) {
+        acc[i][j][0] *= first[i][j][0];
+        acc[i][j][1] *= first[i][j][1];
+      }
+  }
+  // epilogue: accumulator (i, j, h) = C(m0 + wm + 16 (i/2) + 2g + (i&1), n0 + wn + 16 (j/2) + 4t + 2h + (j&1))
+#pragma unroll
+  for (int j = 0; j < FN; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int n = n0 + wn + 16 * (j / 2) + 4 * t + 2 * h + (j & 1);
+      if (n >= N) continue;
+      const long long nc = p.colmap ? __ldg(p.colmap + n) : n;
+      double* col = p.C + nc * p.ldc;
+#pragma unroll
+      for (int ii = 0; ii < FM / 2; ++ii) {
+        const int m = m0 + wm + 16 * ii + 2 * g;
+        double v0 = p.alpha * acc[2 * ii][j][h], v1 = p.alpha * acc[2 * ii + 1][j][h];
+        if (p.vec_store && m + 1 < p.M) {
+          double2* c2 = reinterpret_cast<double2*>(col + m);
+          if (p.beta != 0.0) {
+            const double2 o = *c2;
+            v0 += p.beta * o.x;
+            v1 += p.beta * o.y;
+          }
+          *c2 = make_double2(v0, v1);
+        } else {
+          if (m < p.M) col[m] = p.beta != 0.0 ? v0 + p.beta * col[m] : v0;
+          if (m + 1 < p.M) col[m + 1] = p.beta != 0.0 ? v1 + p.beta * col[m + 1] : v1;
+        }
+      }
+    }
+}
+
+}  // namespace lrgw_dev

@@ -1,0 +1,110 @@
+// gemm_tma.cu — host side of the TMA-fed DMMA GEMM (gemm4.cuh): tensor-map
+// encoding (cuTensorMapEncodeTiled through the runtime's driver entry point,
+// no link-time libcuda dependency), tile selection and launch.
+#include <cuda.h>
+
+#include <cstdlib>
+
+#include "gemm4.cuh"
+#include "kernels.h"
+
+namespace lrgw_dev {
+
+namespace {
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encoder() {
+  static const EncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<EncodeTiled>(nullptr);
+    }
+    return reinterpret_cast<EncodeTiled>(p);
+  }();
+  return fn;
+}
+
+// Column-major rows x cols matrix (rows contiguous, ld >= rows) as a 2-D
+// tensor of boxes {16 rows, bk columns}, 128-byte swizzle.
+bool encode_mn(CUtensorMap* map, const double* ptr, long long rows, long long cols, long long ld, int bk) {
+  EncodeTiled enc = encoder();
+  if (!enc || rows < 1 || cols < 1) return false;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || (ld * 8) % 16 != 0) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+  const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(bk)};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <class Cfg>
+cudaError_t launch4(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2,
+                    const CUtensorMap& b2, const Dgemm4Params& p) {
+  auto kern = dgemm4_kernel<Cfg>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  dim3 grid((p.N + Cfg::BN - 1) / Cfg::BN, (p.M + Cfg::BM - 1) / Cfg::BM);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(a, b, a2, b2, p);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+constexpr int kBK = 16;
+// 64 x 32 warp tiles, 2 warp rows; BN = 32 x warp columns
+template <int BN>
+using T4 = Gemm4Cfg<128, BN, 64, 32, kBK, 4, false, 1>;
+// Hadamard pair: two accumulator sets -> 32 x 32 warp tiles
+template <int BN>
+using H4 = Gemm4Cfg<64, BN, 32, 32, kBK, 4, true, 1>;
+
+}  // namespace
+
+bool tma_gemm_enabled() {
+  static const bool on = getenv("LRGW_TMA") && atoi(getenv("LRGW_TMA")) == 1;
+  return on && encoder() != nullptr;
+}
+
+cudaError_t dgemm_tma(cudaStream_t st, int M, int N, int K, const double* A, long long lda, const double* B,
+                      long long ldb, double* C, long long ldc, double alpha, double beta, bool tri_b,
+                      const int* colmap, const int* n_dev) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  if (K <= 0) return cudaErrorNotSupported;
+  CUtensorMap ma, mb;
+  if (!encode_mn(&ma, A, M, K, lda, kBK) || !encode_mn(&mb, B, N, K, ldb, kBK)) return cudaErrorNotSupported;
+  Dgemm4Params p{};
+  p.M = M, p.N = N, p.K = K, p.C = C, p.ldc = ldc, p.alpha = alpha, p.beta = beta;
+  p.tri_b = tri_b ? 1 : 0, p.colmap = colmap, p.n_dev = n_dev;
+  p.vec_store = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 2 == 0;
+  const int w = (N + 31) / 32;
+  if (n_dev || w >= 4) return launch4<T4<128>>(st, ma, mb, ma, mb, p);
+  if (w == 3) return launch4<T4<96>>(st, ma, mb, ma, mb, p);
+  return launch4<T4<64>>(st, ma, mb, ma, mb, p);
+}
+
+cudaError_t hadamard_tma(cudaStream_t st, int M, int N, const double* a1, long long lda1, const double* b1,
+                         long long ldb1, int k1, const double* a2, long long lda2, const double* b2, long long ldb2,
+                         int k2, double* C, long long ldc, double alpha, double beta) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  if (k1 <= 0 || k2 <= 0) return cudaErrorNotSupported;
+  CUtensorMap ma, mb, ma2, mb2;
+  if (!encode_mn(&ma, a1, M, k1, lda1, kBK) || !encode_mn(&mb, b1, N, k1, ldb1, kBK) ||
+      !encode_mn(&ma2, a2, M, k2, lda2, kBK) || !encode_mn(&mb2, b2, N, k2, ldb2, kBK))
+    return cudaErrorNotSupported;
+  Dgemm4Params p{};
+  p.M = M, p.N = N, p.K = k1, p.K2 = k2, p.C = C, p.ldc = ldc, p.alpha = alpha, p.beta = beta;
+  p.vec_store = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 2 == 0;
+  const int w = (N + 31) / 32;
+  if (w >= 4) return launch4<H4<128>>(st, ma, mb, ma2, mb2, p);
+  if (w == 3) return launch4<H4<96>>(st, ma, mb, ma2, mb2, p);
+  return launch4<H4<64>>(st, ma, mb, ma2, mb2, p);
+}
+
+}  // namespace lrgw_dev

@@ -26,6 +26,17 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
                   const int* n_dev = nullptr, const double* cin = nullptr, long long ldcin = 0,
                   const int* cin_map = nullptr);
 
+// TMA-fed engine (gemm4.cuh / gemm_tma.cu) for MN-contiguous operands:
+// cudaErrorNotSupported when a shape / alignment is not covered (callers fall
+// back to the cp.async engines). Enabled with LRGW_TMA=1.
+bool tma_gemm_enabled();
+cudaError_t dgemm_tma(cudaStream_t st, int M, int N, int K, const double* A, long long lda, const double* B,
+                      long long ldb, double* C, long long ldc, double alpha, double beta, bool tri_b,
+                      const int* colmap, const int* n_dev);
+cudaError_t hadamard_tma(cudaStream_t st, int M, int N, const double* a1, long long lda1, const double* b1,
+                         long long ldb1, int k1, const double* a2, long long lda2, const double* b2, long long ldb2,
+                         int k2, double* C, long long ldc, double alpha, double beta);
+
 // C = alpha * (A1 B1^T) o (A2 B2^T) + beta * C; A1: M x K1, B1: N x K1, A2: M x K2,
 // B2: N x K2, all MN-contiguous (isdf.hpp:132 fit GEMM pair + Hadamard).
 cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long long lda1,
