@@ -11,7 +11,8 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "liblrgw_cuda.so")
+# LRGW_LIB: an alternative build of the same library (A/B experiments of tools/)
+LIB_PATH = os.environ.get("LRGW_LIB") or os.path.join(_HERE, "lib", "liblrgw_cuda.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "lrgw_cuda.h")
 
 _lib = None

@@ -116,6 +116,18 @@ cudaError_t launch_tall(cudaStream_t st, const DgemmParams& p, int q) {
   }
 }
 
+// The TMA Hadamard pair (32 x 32 warp tiles) measured slower than the parked
+// cp.async family at the selection's widths: opt-in only (LRGW_TMA_HAD=1).
+bool tma_k_enabled() {
+  static const bool on = !(getenv("LRGW_TMA_K") && atoi(getenv("LRGW_TMA_K")) == 0);
+  return on;
+}
+
+bool hadamard_tma_enabled() {
+  static const bool on = getenv("LRGW_TMA_HAD") && atoi(getenv("LRGW_TMA_HAD")) == 1;
+  return on;
+}
+
 bool tall_family_enabled() {
   static const bool on = !(getenv("LRGW_TALL") && atoi(getenv("LRGW_TALL")) == 0);
   return on;
@@ -402,6 +414,34 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
   if (cin && (lower || work || !cin_map)) return cudaErrorInvalidValue;
   if ((tri_b || colmap || n_dev) && (lower || work)) return cudaErrorInvalidValue;
   const bool ak = la == Lay::K, bk = lb == Lay::K;
+  // TMA-fed engine for K-contiguous operands (the G-space SYRK): 128 x 128
+  // tiles (lower ones when symmetric), split-K when the tile grid is small
+  if (ak && bk && !cin && !tri_b && !colmap && !n_dev && tma_gemm_enabled() && tma_k_enabled() &&
+      (lower || (long long)((M + 127) / 128) * ((N + 127) / 128) >= sm_count)) {
+    const int bt = dgemm_tma_k_tile();
+    const long long tm = (M + bt - 1) / bt, tn = (N + bt - 1) / bt;
+    const long long tiles = lower ? tm * (tm + 1) / 2 : tm * tn;
+    const int ktiles = (K + 15) / 16;
+    int splits = 1, kc = 0;
+    if (tiles < 2LL * sm_count && ktiles >= 32 && work) {
+      splits = choose_splits(tiles, ktiles, (long long)sm_count);
+      while (splits > 1 && (size_t)splits * M * N > work_elems) --splits;
+      if (splits > 1) {
+        kc = ((ktiles + splits - 1) / splits) * 16;
+        splits = (K + kc - 1) / kc;
+      }
+    }
+    const cudaError_t e = dgemm_tma_k(st, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, scale, lower, splits, kc,
+                                      splits > 1 ? work : nullptr);
+    if (e != cudaErrorNotSupported) {
+      if (e != cudaSuccess || splits <= 1) return e;
+      splitk_reduce_kernel<<<1184, 256, 0, st>>>(work, splits, (long long)M * N, M, N, C, ldc, beta, lower ? 1 : 0,
+                                                 bt);
+      count_launches(1);
+      return cudaGetLastError();
+    }
+    cudaGetLastError();
+  }
   // TMA-fed engine for MN-contiguous operands when the tile grid fills the chip
   if (!ak && !bk && !lower && !scale && !cin && tma_gemm_enabled() &&
       (long long)((M + 127) / 128) * ((N + 127) / 128) >= sm_count) {
@@ -579,7 +619,7 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
                           long long lda2, const double* b2, long long ldb2, int k2, double* C,
                           long long ldc, double alpha, double beta) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  if (tma_gemm_enabled() && (long long)((M + 63) / 64) >= 2 * 148) {
+  if (tma_gemm_enabled() && hadamard_tma_enabled() && (long long)((M + 63) / 64) >= 2 * 148) {
     const cudaError_t e = hadamard_tma(st, M, N, a1, lda1, b1, ldb1, k1, a2, lda2, b2, ldb2, k2, C, ldc, alpha, beta);
     if (e != cudaErrorNotSupported) return e;
     cudaGetLastError();

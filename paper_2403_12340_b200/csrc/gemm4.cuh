@@ -42,8 +42,8 @@ struct Gemm4Cfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, BK = BK_, STAGES = STAGES_, MINB = MINB_;
   static constexpr bool HAD = HAD_;
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
-  static constexpr int CWARPS = WARPS_M * WARPS_N;  // consumers; + 1 producer warp
-  static constexpr int THREADS = 32 * (CWARPS + 1);
+  static constexpr int CWARPS = WARPS_M * WARPS_N;  // every warp computes; thread 0 also issues the TMAs
+  static constexpr int THREADS = 32 * CWARPS;
   static constexpr int FM = WM / 8, FN = WN / 8;
   static constexpr int BOX = BK * 16;  // doubles per 16-row box
   static constexpr int A_BOXES = BM / 16, B_BOXES = BN / 16;
@@ -144,32 +144,30 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   }
   __syncthreads();
 
-  if (warp == Cfg::CWARPS) {
-    // ===== producer: one elected lane issues every TMA of the ring =====
-    if (lane == 0) {
-      tma_prefetch_desc(&map_a);
-      tma_prefetch_desc(&map_b);
-      if (Cfg::HAD) {
-        tma_prefetch_desc(&map_a2);
-        tma_prefetch_desc(&map_b2);
-      }
-      for (int kt = 0; kt < nkt; ++kt) {
-        const int s = kt % STAGES;
-        if (kt >= STAGES) mbar_wait(empty + s, ((kt / STAGES) - 1) & 1);
-        double* sa = ring + s * Cfg::STAGE_ELEMS;
-        double* sb = sa + Cfg::A_BOXES * Cfg::BOX;
-        mbar_arrive_expect_tx(full + s, Cfg::STAGE_BYTES);
-        const bool ph2 = Cfg::HAD && kt >= kt1;
-        const CUtensorMap* ma = ph2 ? &map_a2 : &map_a;
-        const CUtensorMap* mb = ph2 ? &map_b2 : &map_b;
-        const int k0 = ph2 ? (kt - kt1) * BK : kb + kt * BK;
+  // thread 0 keeps the ring full: stage s of k-tile kt + STAGES is refilled
+  // once every warp has released k-tile kt (the empty barrier)
+  auto issue = [&](int kt) {
+    const int s = kt % STAGES;
+    double* sa = ring + s * Cfg::STAGE_ELEMS;
+    double* sb = sa + Cfg::A_BOXES * Cfg::BOX;
+    mbar_arrive_expect_tx(full + s, Cfg::STAGE_BYTES);
+    const bool ph2 = Cfg::HAD && kt >= kt1;
+    const CUtensorMap* ma = ph2 ? &map_a2 : &map_a;
+    const CUtensorMap* mb = ph2 ? &map_b2 : &map_b;
+    const int k0 = ph2 ? (kt - kt1) * BK : kb + kt * BK;
 #pragma unroll
-        for (int b = 0; b < Cfg::A_BOXES; ++b) tma_load_2d(sa + b * Cfg::BOX, ma, full + s, m0 + 16 * b, k0);
+    for (int b = 0; b < Cfg::A_BOXES; ++b) tma_load_2d(sa + b * Cfg::BOX, ma, full + s, m0 + 16 * b, k0);
 #pragma unroll
-        for (int b = 0; b < Cfg::B_BOXES; ++b) tma_load_2d(sb + b * Cfg::BOX, mb, full + s, n0 + 16 * b, k0);
-      }
+    for (int b = 0; b < Cfg::B_BOXES; ++b) tma_load_2d(sb + b * Cfg::BOX, mb, full + s, n0 + 16 * b, k0);
+  };
+  if (tid == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    if (Cfg::HAD) {
+      tma_prefetch_desc(&map_a2);
+      tma_prefetch_desc(&map_b2);
     }
-    return;
+    for (int kt = 0; kt < STAGES && kt < nkt; ++kt) issue(kt);
   }
 
   // ===== consumers =====
@@ -210,6 +208,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);
+    if (tid == 0 && kt + STAGES < nkt) {
+      mbar_wait(empty + s, (kt / STAGES) & 1);
+      issue(kt + STAGES);
+    }
   }
   if (!live) return;
   if (Cfg::HAD) {
@@ -248,6 +250,172 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
         }
       }
     }
+}
+
+// ---------------------------------------------------------------------------
+// K-contiguous operands (the G-space SYRK Theta^T V Theta over the half
+// spectrum: X is 2K x n_mu with each column's k contiguous):
+//   C = alpha * sum_k A(m, k) s(k) B(n, k) (+ beta C),   A(m, k) at m * lda + k
+// Boxes are {16 k, BM rows}: each row's 16 k values are one 128-byte line,
+// 128B-swizzled (chunk c of row r at c ^ (r & 7)). A thread's k pair
+// (8p + 2t, 8p + 2t + 1) is chunk 4p + t; to keep a quarter-warp's 8 LDS.128
+// on 8 distinct chunks, the MMA fragment row g maps to the physical row
+// rp(g) = (g >> 1) + 4 (g & 1) of its 8-row group (the two rows a
+// quarter-warp touches then differ in bit 2 of the swizzle key). The same
+// permutation is undone in the epilogue (C's row g -> rp(g); its columns
+// 2t, 2t + 1 -> t, t + 4). Lower-triangle tiles, the diagonal scale s(k)
+// (read through L1, one double2 per k pair) and split-K partials as in the
+// v3 engine (gemm3.cuh).
+// ---------------------------------------------------------------------------
+struct Dgemm4kParams {
+  int M, N, K;
+  double* C;
+  long long ldc;
+  double alpha, beta;
+  const double* scale;  // length K or nullptr
+  int lower;            // only tiles with tile_n <= tile_m (BM == BN)
+  int k_chunk;          // split-K chunk (multiple of 16) when gridDim.z > 1
+  double* partial;      // split-K: alpha * acc to partial + z * part_stride (ld M)
+  long long part_stride;
+};
+
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_>
+struct Gemm4kCfg {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, BK = 16, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  static constexpr int CWARPS = WARPS_M * WARPS_N;  // every warp computes; thread 0 also issues the TMAs
+  static constexpr int THREADS = 32 * CWARPS;
+  static constexpr int FM = WM / 8, FN = WN / 8;
+  static constexpr int STAGE_ELEMS = (BM + BN) * 16;
+  static constexpr unsigned STAGE_BYTES = STAGE_ELEMS * 8;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_ELEMS * 8 + 1024 + 2 * STAGES * 8;
+  static_assert(BM % 8 == 0 && BN % 8 == 0 && BM <= 256 && BN <= 256, "one box of <= 256 rows per operand");
+};
+
+__device__ __forceinline__ int perm_row(int g) { return (g >> 1) + 4 * (g & 1); }
+
+// k-pair fragments (steps 2p, 2p+1) of FR 8-row tiles from a swizzled [rows][16] stage
+template <int FR>
+__device__ __forceinline__ void load_frag_kswz(const double* s, int w, int p, int g, int t, double (&f0)[FR],
+                                               double (&f1)[FR]) {
+  const int rp = perm_row(g);
+  const int chunk = (4 * p + t) ^ rp;  // (w + 8 i) is a multiple of 8: row & 7 == rp
+#pragma unroll
+  for (int i = 0; i < FR; ++i) {
+    const double2 v = *reinterpret_cast<const double2*>(s + (w + 8 * i + rp) * 16 + 2 * chunk);
+    f0[i] = v.x;
+    f1[i] = v.y;
+  }
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
+    dgemm4k_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   Dgemm4kParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, STAGES = Cfg::STAGES, FM = Cfg::FM, FN = Cfg::FN;
+  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * Cfg::STAGE_ELEMS);
+  uint64_t* empty = full + STAGES;
+  int tm, tn;
+  if (p.lower) {
+    lower_tile(blockIdx.x, tm, tn);
+  } else {
+    tn = blockIdx.x;
+    tm = blockIdx.y;
+  }
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int kb = p.k_chunk > 0 ? blockIdx.z * p.k_chunk : 0;
+  const int ke = p.k_chunk > 0 ? min(p.K, kb + p.k_chunk) : p.K;
+  const int nkt = ke > kb ? (ke - kb + 15) / 16 : 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, Cfg::CWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int kt) {
+    const int s = kt % STAGES;
+    double* sa = ring + s * Cfg::STAGE_ELEMS;
+    mbar_arrive_expect_tx(full + s, Cfg::STAGE_BYTES);
+    tma_load_2d(sa, &map_a, full + s, kb + kt * 16, m0);
+    tma_load_2d(sa + BM * 16, &map_b, full + s, kb + kt * 16, n0);
+  };
+  if (tid == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int kt = 0; kt < STAGES && kt < nkt; ++kt) issue(kt);
+  }
+  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM, wn = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int g = lane >> 2, t = lane & 3;
+  // warps of a diagonal lower tile strictly above the diagonal skip their MMAs
+  const bool live = !(p.lower && tm == tn && wn >= wm + Cfg::WM);
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int kt = 0; kt < nkt; ++kt) {
+    const int s = kt % STAGES;
+    const int kg = kb + kt * 16;
+    double2 sc[2] = {make_double2(1.0, 1.0), make_double2(1.0, 1.0)};
+    if (p.scale) {
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        const int k = kg + 8 * pp + 2 * t;
+        sc[pp] = k + 1 < ke ? __ldg(reinterpret_cast<const double2*>(p.scale + k))
+                            : make_double2(k < ke ? __ldg(p.scale + k) : 0.0, 0.0);
+      }
+    }
+    mbar_wait(full + s, (kt / STAGES) & 1);
+    if (live) {
+      const double* sa = ring + s * Cfg::STAGE_ELEMS;
+      const double* sb = sa + BM * 16;
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        double a0[FM], a1[FM], b0[FN], b1[FN];
+        load_frag_kswz<FM>(sa, wm, pp, g, t, a0, a1);
+        load_frag_kswz<FN>(sb, wn, pp, g, t, b0, b1);
+        if (p.scale) {
+#pragma unroll
+          for (int j = 0; j < FN; ++j) {
+            b0[j] *= sc[pp].x;
+            b1[j] *= sc[pp].y;
+          }
+        }
+        dmma_block<FM, FN>(acc, a0, b0);
+        dmma_block<FM, FN>(acc, a1, b1);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
+    if (tid == 0 && kt + STAGES < nkt) {
+      mbar_wait(empty + s, (kt / STAGES) & 1);
+      issue(kt + STAGES);
+    }
+  }
+  if (!live) return;
+  const int rp = perm_row(g);
+  double* out = p.partial ? p.partial + (long long)blockIdx.z * p.part_stride : p.C;
+  const long long ldo = p.partial ? p.M : p.ldc;
+#pragma unroll
+  for (int i = 0; i < FM; ++i) {
+    const int m = m0 + wm + 8 * i + rp;
+    if (m >= p.M) continue;
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = n0 + wn + 8 * j + t + 4 * h;
+        if (n >= p.N) continue;
+        double* c = out + m + (long long)n * ldo;
+        const double v = p.alpha * acc[i][j][h];
+        *c = (p.partial || p.beta == 0.0) ? v : v + p.beta * *c;
+      }
+  }
 }
 
 }  // namespace lrgw_dev

@@ -45,6 +45,23 @@ bool encode_mn(CUtensorMap* map, const double* ptr, long long rows, long long co
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// K-contiguous rows x k matrix (A(r, k) at r * ld + k) as a 2-D tensor of
+// boxes {16 k, box_rows rows}, 128-byte swizzle.
+bool encode_k(CUtensorMap* map, const double* ptr, long long rows, long long k, long long ld, int box_rows) {
+  EncodeTiled enc = encoder();
+  if (!enc || rows < 1 || k < 1) return false;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || (ld * 8) % 16 != 0) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+  const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+using K4 = Gemm4kCfg<128, 128, 64, 32, 5, 1>;
+
 template <class Cfg>
 cudaError_t launch4(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2,
                     const CUtensorMap& b2, const Dgemm4Params& p) {
@@ -67,8 +84,38 @@ using H4 = Gemm4Cfg<64, BN, 32, 32, kBK, 4, true, 1>;
 
 }  // namespace
 
+int dgemm_tma_k_tile() { return K4::BM; }
+
+cudaError_t dgemm_tma_k(cudaStream_t st, int M, int N, int K, const double* A, long long lda, const double* B,
+                        long long ldb, double* C, long long ldc, double alpha, double beta, const double* scale,
+                        bool lower, int splits, int k_chunk, double* partial) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  if (K <= 0 || (lower && M != N) || (splits > 1 && (!partial || k_chunk % 16 != 0))) return cudaErrorNotSupported;
+  CUtensorMap ma, mb;
+  if (!encode_k(&ma, A, M, K, lda, K4::BM) || !encode_k(&mb, B, N, K, ldb, K4::BN)) return cudaErrorNotSupported;
+  Dgemm4kParams p{};
+  p.M = M, p.N = N, p.K = K, p.C = C, p.ldc = ldc, p.alpha = alpha, p.beta = beta, p.scale = scale;
+  p.lower = lower ? 1 : 0;
+  if (splits > 1) {
+    p.k_chunk = k_chunk;
+    p.partial = partial;
+    p.part_stride = (long long)M * N;
+  }
+  auto kern = dgemm4k_kernel<K4>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K4::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int tm = (M + K4::BM - 1) / K4::BM, tn = (N + K4::BN - 1) / K4::BN;
+  dim3 grid(lower ? tm * (tm + 1) / 2 : tn, lower ? 1 : tm, splits > 1 ? splits : 1);
+  kern<<<grid, K4::THREADS, K4::SMEM_BYTES, st>>>(ma, mb, p);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+// On by default (LRGW_TMA=0 turns it off). Measured (tools/bench_gemm.py,
+// profiles/r02/gemm_engines.txt): 110592 x 1024 x 1024 86.0 -> 93.9 % and
+// 8192^3 89.0 -> 95.7 % of the DMMA peak against the cp.async engines.
 bool tma_gemm_enabled() {
-  static const bool on = getenv("LRGW_TMA") && atoi(getenv("LRGW_TMA")) == 1;
+  static const bool on = !(getenv("LRGW_TMA") && atoi(getenv("LRGW_TMA")) == 0);
   return on && encoder() != nullptr;
 }
 
@@ -83,10 +130,10 @@ cudaError_t dgemm_tma(cudaStream_t st, int M, int N, int K, const double* A, lon
   p.M = M, p.N = N, p.K = K, p.C = C, p.ldc = ldc, p.alpha = alpha, p.beta = beta;
   p.tri_b = tri_b ? 1 : 0, p.colmap = colmap, p.n_dev = n_dev;
   p.vec_store = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 2 == 0;
-  const int w = (N + 31) / 32;
-  if (n_dev || w >= 4) return launch4<T4<128>>(st, ma, mb, ma, mb, p);
-  if (w == 3) return launch4<T4<96>>(st, ma, mb, ma, mb, p);
-  return launch4<T4<64>>(st, ma, mb, ma, mb, p);
+  // full 128-wide column tiles only: the tall-skinny widths of the selection
+  // stay on the cp.async family (2-3 CTAs per SM; 33-62 % here at widths 32-96)
+  if (n_dev || N < 128) return cudaErrorNotSupported;
+  return launch4<T4<128>>(st, ma, mb, ma, mb, p);
 }
 
 cudaError_t hadamard_tma(cudaStream_t st, int M, int N, const double* a1, long long lda1, const double* b1,

@@ -33,6 +33,12 @@ bool tma_gemm_enabled();
 cudaError_t dgemm_tma(cudaStream_t st, int M, int N, int K, const double* A, long long lda, const double* B,
                       long long ldb, double* C, long long ldc, double alpha, double beta, bool tri_b,
                       const int* colmap, const int* n_dev);
+// K-contiguous operands (A(m, k) at m lda + k): lower tiles, k-scale, split-K
+// partials (k_chunk a multiple of 16; the caller reduces with dgemm_tma_k_tile()).
+int dgemm_tma_k_tile();
+cudaError_t dgemm_tma_k(cudaStream_t st, int M, int N, int K, const double* A, long long lda, const double* B,
+                        long long ldb, double* C, long long ldc, double alpha, double beta, const double* scale,
+                        bool lower, int splits, int k_chunk, double* partial);
 cudaError_t hadamard_tma(cudaStream_t st, int M, int N, const double* a1, long long lda1, const double* b1,
                          long long ldb1, int k1, const double* a2, long long lda2, const double* b2, long long ldb2,
                          int k2, double* C, long long ldc, double alpha, double beta);
