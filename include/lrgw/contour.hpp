@@ -3,6 +3,7 @@
 // scalar code; every node term runs in the fused K3 DMMA kernel on the GPU.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <string>
 #include <utility>
@@ -103,50 +104,105 @@ inline CoupledCoefficients coupled_coefficients_fixed(const Matrix& psi_v_pts, c
   return out;
 }
 
-inline CoupledCoefficients coupled_coefficients_contour(const Matrix& psi_v_pts, const Matrix& psi_c_pts,
-                                                        const std::vector<double>& energies, const ContourSpec& spec,
-                                                        int threads = 1) {
+namespace detail {
+
+// acc = sum_k w_k term_k on the device (the fused K3 kernel; contour.hpp:185-222).
+inline Matrix sum_node_terms(const Matrix& psi_v_pts, const Matrix& psi_c_pts, const std::vector<double>& energies,
+                             const ContourSpec& spec, const std::vector<double>& nodes,
+                             const std::vector<double>& weights, int threads = 1) {
   (void)threads;
-  detail::check_coupled(psi_v_pts, psi_c_pts, energies);
-  if (spec.bypass) throw invalid_input("contour quadrature: spec is bypass-flagged; use the direct sum");
-  CoupledCoefficients out;
-  out.t = Matrix(psi_v_pts.rows(), psi_v_pts.rows());
+  check_coupled(psi_v_pts, psi_c_pts, energies);
+  if (nodes.size() != weights.size()) throw invalid_input("sum_node_terms: nodes / weights length mismatch");
+  Matrix acc(psi_v_pts.rows(), psi_v_pts.rows());
+  if (nodes.empty()) return acc;
+  double s7[7];
+  to7(spec, s7);
   lrgw_ctx c = context();
-  const int st = lrgw_coupled_coefficients_contour(
-      c, psi_v_pts.data(), psi_c_pts.data(), psi_v_pts.rows(), psi_v_pts.cols(), psi_c_pts.cols(), energies.data(),
-      static_cast<int>(energies.size()), spec.delta_rel, spec.max_nodes, out.t.data(), &out.nodes_used,
-      &out.est_rel_error);
-  if (st == LRGW_ERR_CONTOUR_CONVERGENCE)
-    throw contour_convergence_error("coupled_coefficients_contour: did not reach delta_rel within max_nodes",
-                                    std::move(out));
-  detail::check(st, c, "coupled_coefficients_contour");
-  return out;
+  detail::check(lrgw_sum_node_terms(c, psi_v_pts.data(), psi_c_pts.data(), psi_v_pts.rows(), psi_v_pts.cols(),
+                                    psi_c_pts.cols(), energies.data(), static_cast<int>(energies.size()), s7,
+                                    nodes.data(), weights.data(), static_cast<int>(nodes.size()), acc.data()),
+                c, "sum_node_terms");
+  return acc;
 }
 
+// Im(g J(z(t + iL))) at one parameter node (contour.hpp:140-183).
+inline Matrix contour_node_term(const Matrix& psi_v_pts, const Matrix& psi_c_pts, const std::vector<double>& energies,
+                                const ContourSpec& spec, double t_node) {
+  return sum_node_terms(psi_v_pts, psi_c_pts, energies, spec, {t_node}, {1.0});
+}
+
+}  // namespace detail
+
+// Nested trapezoid levels of 2^m + 1 nodes, m = 4, 5, ... on [-R, R] of the
+// given spec; each level evaluates only its new midpoints on the device
+// (running = running / 2 + new, T = pref running, symmetrised); the visitor
+// gets (node count, T) and returns false to stop (contour.hpp:224-279).
+template <typename Visitor>
+void visit_contour_levels(const Matrix& psi_v_pts, const Matrix& psi_c_pts, const std::vector<double>& energies,
+                          const ContourSpec& spec, int max_level_nodes, int threads, Visitor&& visit) {
+  detail::check_coupled(psi_v_pts, psi_c_pts, energies);
+  if (spec.bypass) throw invalid_input("contour quadrature: spec is bypass-flagged; use the direct sum");
+  if ((1 << 4) + 1 > max_level_nodes) throw invalid_input("contour quadrature: node cap below one level");
+  const double pref = 2.0 * std::sqrt(spec.q * spec.big_q) / (3.14159265358979323846 * spec.r);
+  Matrix running;
+  for (int m = 4;; ++m) {
+    const int n_nodes = (1 << m) + 1;
+    if (n_nodes > max_level_nodes) break;
+    const double h = 2.0 * spec.big_r / (n_nodes - 1);
+    std::vector<double> nodes, weights;
+    const bool first = running.empty();
+    for (int k = first ? 0 : 1; k < n_nodes; k += first ? 1 : 2) {
+      nodes.push_back(-spec.big_r + k * h);
+      weights.push_back((first && (k == 0 || k == n_nodes - 1)) ? 0.5 * h : h);
+    }
+    Matrix add = detail::sum_node_terms(psi_v_pts, psi_c_pts, energies, spec, nodes, weights, threads);
+    running = first ? std::move(add) : 0.5 * running + add;
+    Matrix t = pref * running;
+    symmetrize(t);
+    if (!visit(n_nodes, std::move(t))) break;
+  }
+}
+
+// Every level's estimate up to the node cap, on the given spec (contour.hpp:281-294).
 inline std::vector<std::pair<int, Matrix>> contour_refinement_levels(const Matrix& psi_v_pts, const Matrix& psi_c_pts,
                                                                      const std::vector<double>& energies,
                                                                      const ContourSpec& spec, int max_level_nodes,
                                                                      int threads = 1) {
-  (void)threads;
-  (void)spec;
-  detail::check_coupled(psi_v_pts, psi_c_pts, energies);
-  const int n_mu = psi_v_pts.rows(), max_levels = 16;
-  std::vector<double> buf(static_cast<std::size_t>(max_levels) * n_mu * n_mu);
-  std::vector<int> counts(max_levels);
-  int n_levels = 0;
-  lrgw_ctx c = context();
-  detail::check(lrgw_contour_refinement_levels(c, psi_v_pts.data(), psi_c_pts.data(), n_mu, psi_v_pts.cols(),
-                                               psi_c_pts.cols(), energies.data(), static_cast<int>(energies.size()),
-                                               max_level_nodes, max_levels, buf.data(), counts.data(), &n_levels),
-                c, "contour_refinement_levels");
-  std::vector<std::pair<int, Matrix>> out;
-  for (int i = 0; i < n_levels; ++i) {
-    Matrix t(n_mu, n_mu);
-    std::copy(buf.begin() + static_cast<std::ptrdiff_t>(i) * n_mu * n_mu,
-              buf.begin() + static_cast<std::ptrdiff_t>(i + 1) * n_mu * n_mu, t.data());
-    out.emplace_back(counts[i], std::move(t));
-  }
-  return out;
+  std::vector<std::pair<int, Matrix>> levels;
+  visit_contour_levels(psi_v_pts, psi_c_pts, energies, spec, max_level_nodes, threads, [&](int n, Matrix t) {
+    levels.emplace_back(n, std::move(t));
+    return true;
+  });
+  return levels;
+}
+
+// Adaptive refinement to spec.delta_rel within spec.max_nodes; on failure
+// contour_convergence_error carries the best estimate (contour.hpp:296-329).
+inline CoupledCoefficients coupled_coefficients_contour(const Matrix& psi_v_pts, const Matrix& psi_c_pts,
+                                                        const std::vector<double>& energies, const ContourSpec& spec,
+                                                        int threads = 1) {
+  CoupledCoefficients best;
+  bool converged = false;
+  Matrix prev;
+  visit_contour_levels(psi_v_pts, psi_c_pts, energies, spec, spec.max_nodes, threads, [&](int n_nodes, Matrix t) {
+    if (prev.empty()) {
+      best = CoupledCoefficients{t, n_nodes, 1.0};
+      prev = std::move(t);
+      return true;
+    }
+    const double rel = frobenius_norm(t - prev) / std::max(frobenius_norm(t), 1e-300);
+    best = CoupledCoefficients{t, n_nodes, rel};
+    prev = std::move(t);
+    if (rel <= spec.delta_rel) {
+      converged = true;
+      return false;
+    }
+    return true;
+  });
+  if (!converged)
+    throw contour_convergence_error("coupled_coefficients_contour: did not reach delta_rel within max_nodes",
+                                    std::move(best));
+  return best;
 }
 
 }  // namespace lrgw

@@ -324,6 +324,31 @@ int lrgw_dev_cand_greedy(lrgw_ctx ctx, int n_r, int s, int steps, int k, const d
                          int32_t* b_host);
 
 
+/* ---- dense utility layer of the reference API (host buffers) --------------
+ * The drop-in headers' matrix.hpp / linalg.hpp / dft.hpp / isdf.hpp helpers
+ * over the device: DMMA products, cuSOLVER factorisations with the
+ * reference's singularity rule, QRCP pivots from the path's greedy selection. */
+/* C = op(A) op(B), op = 'N' | 'T' (matrix.hpp:71-120 matmul / matmul_tn / matmul_nt). */
+int lrgw_matmul(lrgw_ctx ctx, char trans_a, char trans_b, int m, int n, int k, const double* a, long long lda,
+                const double* b, long long ldb, double* c, long long ldc);
+/* linalg.hpp:117-150: partial-pivot LU; piv[i] = row swapped with row i at step i;
+ * LRGW_ERR_SINGULAR (pivot index) when |u_ii| < 1e-14 max|A|. */
+int lrgw_lu_factor(lrgw_ctx ctx, const double* a, int n, double* lu, int32_t* piv, double* max_abs);
+/* linalg.hpp:152-175: X = A^-1 B from the factors (B n x nrhs). */
+int lrgw_lu_solve_factored(lrgw_ctx ctx, const double* lu, const int32_t* piv, int n, const double* b, int nrhs,
+                           double* x);
+/* linalg.hpp:190-345: ascending eigenvalues; eigenvectors in the columns of q (may be NULL). */
+int lrgw_sym_eig(lrgw_ctx ctx, const double* a, int n, double* values, double* q);
+/* linalg.hpp:17-111: A P = Q R; perm (n) = columns in selection order, q (m x k), r (k x n), k = min(m, n). */
+int lrgw_qrcp(lrgw_ctx ctx, const double* a, int m, int n, int32_t* perm, double* q, double* r);
+/* dft.hpp:37-68: unitary 3-D DFT of an interleaved complex grid vector (x, y: 2 n_r doubles). */
+int lrgw_dft(lrgw_ctx ctx, const int* dims, const double* x, int inverse, double* y);
+/* apply_coulomb with the operator's own kernel array (CoulombOperator::kernel, N_r values). */
+int lrgw_apply_coulomb_kernel(lrgw_ctx ctx, const int* dims, const double* kernel, const double* x, int m, double* y);
+/* isdf.hpp:49-88: the pair matrix (N_r x N1 N2) or its transpose, 2^26-entry guard. */
+int lrgw_pair_matrix(lrgw_ctx ctx, const double* a, const double* b, int n_r, int n1, int n2, int transposed,
+                     double* out);
+
 /* ---- multi-rank build (one process per GPU) -------------------
  * A communicator carries the build's few exchanges between the ranks of one
  * box: NCCL over NVLink / NVSwitch (device buffers, the context's stream), or

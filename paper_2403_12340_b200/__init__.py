@@ -5,8 +5,8 @@ inversion of arXiv 2403.12340 behind the reference `lrgw` interface.
     lib/       liblrgw_cuda.so (built in-tree)
     lrgw.py    Python mirror of the reference hot-path API over the C-ABI
     synth.py   seeded synthetic Si-like / C60-like workloads (BASELINE configs)
-    dist.py    multi-rank orchestration (node / row-panel sharding)
-    dist_cuda.py  the per-rank device backend of dist.py
+    dist.py    the multi-rank exchange scheme in Python (numpy stage backend for
+               the CPU tests); the product path is lrgw_build_sharded (csrc/sharded.cu)
     driver.py  the reference driver's run / scale commands over the GPU path
 """
 from . import lrgw  # noqa: F401  (raises ImportError when the extension is missing)

@@ -196,12 +196,16 @@ long long half_len(const int* dims) { return (long long)(dims[0] / 2 + 1) * dims
 // Columns per cuFFT execution: bounds the plan's work area (a single plan
 // over all 8192 Theta columns of Si512 would ask cuFFT for a Theta-sized
 // work buffer next to the 58 GB Theta and its 59 GB spectrum).
-constexpr int kFftBatch = 1024;
+int fft_batch() {
+  static const int v = getenv("LRGW_FFT_BATCH") ? std::max(1, atoi(getenv("LRGW_FFT_BATCH"))) : 1024;
+  return v;
+}
 
 void fft_forward(lrgw_ctx c, const int* dims, const double* x, long long ldx, int m, double* xhat) {
   const long long nh = half_len(dims);
-  for (int j0 = 0; j0 < m; j0 += kFftBatch) {
-    const int b = std::min(kFftBatch, m - j0);
+  const int fb = fft_batch();
+  for (int j0 = 0; j0 < m; j0 += fb) {
+    const int b = std::min(fb, m - j0);
     cufftHandle plan = get_plan(c, dims, b, ldx, nh, true);
     ckf(cufftExecD2Z(plan, const_cast<double*>(x) + (size_t)j0 * ldx,
                      reinterpret_cast<cufftDoubleComplex*>(xhat + (size_t)j0 * 2 * nh)),
@@ -211,8 +215,9 @@ void fft_forward(lrgw_ctx c, const int* dims, const double* x, long long ldx, in
 
 void fft_inverse(lrgw_ctx c, const int* dims, double* xhat, int m, double* y, long long ldy) {
   const long long nh = half_len(dims);
-  for (int j0 = 0; j0 < m; j0 += kFftBatch) {
-    const int b = std::min(kFftBatch, m - j0);
+  const int fb = fft_batch();
+  for (int j0 = 0; j0 < m; j0 += fb) {
+    const int b = std::min(fb, m - j0);
     cufftHandle plan = get_plan(c, dims, b, ldy, nh, false);
     ckf(cufftExecZ2D(plan, reinterpret_cast<cufftDoubleComplex*>(xhat + (size_t)j0 * 2 * nh), y + (size_t)j0 * ldy),
         "cufftExecZ2D");

@@ -83,7 +83,39 @@ __global__ void slab_weights_kernel(int n1, int n2, int n3, double c1, double c2
   }
 }
 
+// a caller's kernel v (full grid, linear index i1 + n1 (i2 + n2 i3)): the real
+// part of F^-1 diag(v) F x equals F^-1 diag((v(G) + v(-G)) / 2) F x for real x,
+// which is what the half spectrum carries
+__global__ void scale_half_custom_kernel(int n1, int n2, int n3, const double* v, double2* x, int cols) {
+  const int nh = n1 / 2 + 1;
+  const long long per = (long long)nh * n2 * n3;
+  const long long total = per * cols;
+  const double inv_n = 1.0 / ((double)n1 * n2 * n3);
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long q = idx % per;
+    const int i1 = static_cast<int>(q % nh);
+    const int i2 = static_cast<int>((q / nh) % n2);
+    const int i3 = static_cast<int>(q / ((long long)nh * n2));
+    const int j1 = (n1 - i1) % n1, j2 = (n2 - i2) % n2, j3 = (n3 - i3) % n3;
+    const double vp = v[i1 + (long long)n1 * (i2 + (long long)n2 * i3)];
+    const double vm = v[j1 + (long long)n1 * (j2 + (long long)n2 * j3)];
+    const double s = 0.5 * (vp + vm) * inv_n;
+    double2 t = x[idx];
+    t.x *= s;
+    t.y *= s;
+    x[idx] = t;
+  }
+}
+
 }  // namespace
+
+cudaError_t coulomb_scale_half_custom(cudaStream_t st, int n1, int n2, int n3, const double* v, double* xhat,
+                                      int cols) {
+  scale_half_custom_kernel<<<1184, 256, 0, st>>>(n1, n2, n3, v, reinterpret_cast<double2*>(xhat), cols);
+  count_launches(1);
+  return cudaGetLastError();
+}
 
 cudaError_t coulomb_slab_weights(cudaStream_t st, int n1, int n2, int n3, double c1, double c2, double c3,
                                  int zero_kernel, int ya, int ny, double* w) {

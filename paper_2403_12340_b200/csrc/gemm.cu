@@ -418,7 +418,7 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
   // tiles (lower ones when symmetric), split-K when the tile grid is small
   if (ak && bk && !cin && !tri_b && !colmap && !n_dev && tma_gemm_enabled() && tma_k_enabled() &&
       (lower || (long long)((M + 127) / 128) * ((N + 127) / 128) >= sm_count)) {
-    const int bt = dgemm_tma_k_tile();
+    const int bt = dgemm_tma_k_tile(M);
     const long long tm = (M + bt - 1) / bt, tn = (N + bt - 1) / bt;
     const long long tiles = lower ? tm * (tm + 1) / 2 : tm * tn;
     const int ktiles = (K + 15) / 16;

@@ -37,13 +37,16 @@ struct Dgemm4Params {
   int vec_store;       // C 16-byte aligned with even ldc: paired double2 stores
 };
 
-template <int BM_, int BN_, int WM_, int WN_, int BK_, int STAGES_, bool HAD_, int MINB_>
+// PROD: one extra warp does nothing but issue the TMAs (its lane 0 waits on
+// the empty barriers); otherwise thread 0 of the compute warps refills the
+// ring after each k-tile.
+template <int BM_, int BN_, int WM_, int WN_, int BK_, int STAGES_, bool HAD_, int MINB_, bool PROD_ = true>
 struct Gemm4Cfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, BK = BK_, STAGES = STAGES_, MINB = MINB_;
-  static constexpr bool HAD = HAD_;
+  static constexpr bool HAD = HAD_, PROD = PROD_;
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
-  static constexpr int CWARPS = WARPS_M * WARPS_N;  // every warp computes; thread 0 also issues the TMAs
-  static constexpr int THREADS = 32 * CWARPS;
+  static constexpr int CWARPS = WARPS_M * WARPS_N;  // compute warps
+  static constexpr int THREADS = 32 * (CWARPS + (PROD ? 1 : 0));
   static constexpr int FM = WM / 8, FN = WN / 8;
   static constexpr int BOX = BK * 16;  // doubles per 16-row box
   static constexpr int A_BOXES = BM / 16, B_BOXES = BN / 16;
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
 #pragma unroll
     for (int b = 0; b < Cfg::B_BOXES; ++b) tma_load_2d(sb + b * Cfg::BOX, mb, full + s, n0 + 16 * b, k0);
   };
-  if (tid == 0) {
+  if (tid == (Cfg::PROD ? 32 * Cfg::CWARPS : 0)) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
     if (Cfg::HAD) {
@@ -168,7 +171,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
       tma_prefetch_desc(&map_b2);
     }
     for (int kt = 0; kt < STAGES && kt < nkt; ++kt) issue(kt);
+    if (Cfg::PROD)
+      for (int kt = STAGES; kt < nkt; ++kt) {
+        mbar_wait(empty + kt % STAGES, ((kt / STAGES) - 1) & 1);
+        issue(kt);
+      }
   }
+  if (Cfg::PROD && warp == Cfg::CWARPS) return;
 
   // ===== consumers =====
   const int wm = (warp % Cfg::WARPS_M) * Cfg::WM, wn = (warp / Cfg::WARPS_M) * Cfg::WN;
@@ -208,7 +217,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);
-    if (tid == 0 && kt + STAGES < nkt) {
+    if (!Cfg::PROD && tid == 0 && kt + STAGES < nkt) {
       mbar_wait(empty + s, (kt / STAGES) & 1);
       issue(kt + STAGES);
     }
@@ -279,12 +288,13 @@ struct Dgemm4kParams {
   long long part_stride;
 };
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_, bool PROD_ = false>
 struct Gemm4kCfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, BK = 16, STAGES = STAGES_, MINB = MINB_;
+  static constexpr bool PROD = PROD_;
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
-  static constexpr int CWARPS = WARPS_M * WARPS_N;  // every warp computes; thread 0 also issues the TMAs
-  static constexpr int THREADS = 32 * CWARPS;
+  static constexpr int CWARPS = WARPS_M * WARPS_N;  // compute warps (+ 1 TMA warp when PROD)
+  static constexpr int THREADS = 32 * (CWARPS + (PROD ? 1 : 0));
   static constexpr int FM = WM / 8, FN = WN / 8;
   static constexpr int STAGE_ELEMS = (BM + BN) * 16;
   static constexpr unsigned STAGE_BYTES = STAGE_ELEMS * 8;
@@ -344,11 +354,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     tma_load_2d(sa, &map_a, full + s, kb + kt * 16, m0);
     tma_load_2d(sa + BM * 16, &map_b, full + s, kb + kt * 16, n0);
   };
-  if (tid == 0) {
+  if (tid == (Cfg::PROD ? 32 * Cfg::CWARPS : 0)) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
     for (int kt = 0; kt < STAGES && kt < nkt; ++kt) issue(kt);
+    if (Cfg::PROD)
+      for (int kt = STAGES; kt < nkt; ++kt) {
+        mbar_wait(empty + kt % STAGES, ((kt / STAGES) - 1) & 1);
+        issue(kt);
+      }
   }
+  if (Cfg::PROD && warp == Cfg::CWARPS) return;
   const int wm = (warp % Cfg::WARPS_M) * Cfg::WM, wn = (warp / Cfg::WARPS_M) * Cfg::WN;
   const int g = lane >> 2, t = lane & 3;
   // warps of a diagonal lower tile strictly above the diagonal skip their MMAs
@@ -392,7 +408,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);
-    if (tid == 0 && kt + STAGES < nkt) {
+    if (!Cfg::PROD && tid == 0 && kt + STAGES < nkt) {
       mbar_wait(empty + s, (kt / STAGES) & 1);
       issue(kt + STAGES);
     }

@@ -60,7 +60,18 @@ bool encode_k(CUtensorMap* map, const double* ptr, long long rows, long long k, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-using K4 = Gemm4kCfg<128, 128, 64, 32, 5, 1>;
+// K-contiguous SYRK configurations (LRGW_TMA_KCFG picks one; measured in profiles/r02/)
+using K4 = Gemm4kCfg<128, 128, 64, 32, 5, 1>;         // 8 compute warps, thread 0 refills
+using K4P = Gemm4kCfg<96, 96, 48, 48, 6, 1, true>;     // 4 compute warps + TMA warp
+using K4S = Gemm4kCfg<64, 64, 32, 32, 6, 2, true>;     // 4 compute warps + TMA warp, 2 CTAs per SM
+// Measured (tools/bench_syrk.py, profiles/r02/syrk_engines.txt): the 64 x 64
+// two-CTA configuration wins from N_mu = 3456 up (0.897 of the DMMA peak at
+// 8192), the 128 x 128 one at N_mu = 1024 (0.803). LRGW_TMA_KCFG forces one.
+int kcfg(int m) {
+  static const int v = getenv("LRGW_TMA_KCFG") ? atoi(getenv("LRGW_TMA_KCFG")) : -1;
+  if (v >= 0) return v;
+  return m >= 2048 ? 2 : 0;
+}
 
 template <class Cfg>
 cudaError_t launch4(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& a2,
@@ -77,22 +88,27 @@ cudaError_t launch4(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b,
 constexpr int kBK = 16;
 // 64 x 32 warp tiles, 2 warp rows; BN = 32 x warp columns
 template <int BN>
-using T4 = Gemm4Cfg<128, BN, 64, 32, kBK, 4, false, 1>;
+using T4 = Gemm4Cfg<128, BN, 64, 32, kBK, 4, false, 1>;         // + TMA warp
+using T4S = Gemm4Cfg<128, 128, 64, 32, kBK, 4, false, 1, false>;  // thread 0 refills
+int mncfg() {
+  static const int v = getenv("LRGW_TMA_MNCFG") ? atoi(getenv("LRGW_TMA_MNCFG")) : 0;
+  return v;
+}
 // Hadamard pair: two accumulator sets -> 32 x 32 warp tiles
 template <int BN>
 using H4 = Gemm4Cfg<64, BN, 32, 32, kBK, 4, true, 1>;
 
 }  // namespace
 
-int dgemm_tma_k_tile() { return K4::BM; }
+int dgemm_tma_k_tile(int m) { return kcfg(m) == 1 ? K4P::BM : kcfg(m) == 2 ? K4S::BM : K4::BM; }
 
-cudaError_t dgemm_tma_k(cudaStream_t st, int M, int N, int K, const double* A, long long lda, const double* B,
-                        long long ldb, double* C, long long ldc, double alpha, double beta, const double* scale,
-                        bool lower, int splits, int k_chunk, double* partial) {
-  if (M <= 0 || N <= 0) return cudaSuccess;
+template <class Cfg>
+cudaError_t launch4k(cudaStream_t st, int M, int N, int K, const double* A, long long lda, const double* B,
+                     long long ldb, double* C, long long ldc, double alpha, double beta, const double* scale,
+                     bool lower, int splits, int k_chunk, double* partial) {
   if (K <= 0 || (lower && M != N) || (splits > 1 && (!partial || k_chunk % 16 != 0))) return cudaErrorNotSupported;
   CUtensorMap ma, mb;
-  if (!encode_k(&ma, A, M, K, lda, K4::BM) || !encode_k(&mb, B, N, K, ldb, K4::BN)) return cudaErrorNotSupported;
+  if (!encode_k(&ma, A, M, K, lda, Cfg::BM) || !encode_k(&mb, B, N, K, ldb, Cfg::BN)) return cudaErrorNotSupported;
   Dgemm4kParams p{};
   p.M = M, p.N = N, p.K = K, p.C = C, p.ldc = ldc, p.alpha = alpha, p.beta = beta, p.scale = scale;
   p.lower = lower ? 1 : 0;
@@ -101,14 +117,25 @@ cudaError_t dgemm_tma_k(cudaStream_t st, int M, int N, int K, const double* A, l
     p.partial = partial;
     p.part_stride = (long long)M * N;
   }
-  auto kern = dgemm4k_kernel<K4>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K4::SMEM_BYTES);
+  auto kern = dgemm4k_kernel<Cfg>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  const int tm = (M + K4::BM - 1) / K4::BM, tn = (N + K4::BN - 1) / K4::BN;
+  const int tm = (M + Cfg::BM - 1) / Cfg::BM, tn = (N + Cfg::BN - 1) / Cfg::BN;
   dim3 grid(lower ? tm * (tm + 1) / 2 : tn, lower ? 1 : tm, splits > 1 ? splits : 1);
-  kern<<<grid, K4::THREADS, K4::SMEM_BYTES, st>>>(ma, mb, p);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(ma, mb, p);
   count_launches(1);
   return cudaGetLastError();
+}
+
+cudaError_t dgemm_tma_k(cudaStream_t st, int M, int N, int K, const double* A, long long lda, const double* B,
+                        long long ldb, double* C, long long ldc, double alpha, double beta, const double* scale,
+                        bool lower, int splits, int k_chunk, double* partial) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  switch (kcfg(M)) {
+    case 1: return launch4k<K4P>(st, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, scale, lower, splits, k_chunk, partial);
+    case 2: return launch4k<K4S>(st, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, scale, lower, splits, k_chunk, partial);
+    default: return launch4k<K4>(st, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, scale, lower, splits, k_chunk, partial);
+  }
 }
 
 // On by default (LRGW_TMA=0 turns it off). Measured (tools/bench_gemm.py,
@@ -133,6 +160,7 @@ cudaError_t dgemm_tma(cudaStream_t st, int M, int N, int K, const double* A, lon
   // full 128-wide column tiles only: the tall-skinny widths of the selection
   // stay on the cp.async family (2-3 CTAs per SM; 33-62 % here at widths 32-96)
   if (n_dev || N < 128) return cudaErrorNotSupported;
+  if (mncfg() == 1) return launch4<T4S>(st, ma, mb, ma, mb, p);
   return launch4<T4<128>>(st, ma, mb, ma, mb, p);
 }
 

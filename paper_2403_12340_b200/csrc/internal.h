@@ -199,6 +199,7 @@ void gemm(lrgw_ctx c, int M, int N, int K, const double* A, long long lda, Lay l
 void check_grid(const int* dims, const double* cell);
 long long half_len(const int* dims);
 void fft_forward(lrgw_ctx c, const int* dims, const double* x, long long ldx, int m, double* xhat);
+void fft_inverse(lrgw_ctx c, const int* dims, double* xhat, int m, double* y, long long ldy);
 void coulomb_apply(lrgw_ctx c, const int* dims, const double* cell, int zero, const double* x, long long ldx, int m,
                    double* y, long long ldy);
 void pvp_impl(lrgw_ctx c, const int* dims, const double* cell, int zero, const double* theta, long long ldt,

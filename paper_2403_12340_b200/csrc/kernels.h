@@ -34,8 +34,8 @@ cudaError_t dgemm_tma(cudaStream_t st, int M, int N, int K, const double* A, lon
                       long long ldb, double* C, long long ldc, double alpha, double beta, bool tri_b,
                       const int* colmap, const int* n_dev);
 // K-contiguous operands (A(m, k) at m lda + k): lower tiles, k-scale, split-K
-// partials (k_chunk a multiple of 16; the caller reduces with dgemm_tma_k_tile()).
-int dgemm_tma_k_tile();
+// partials (k_chunk a multiple of 16; the caller reduces with dgemm_tma_k_tile(M)).
+int dgemm_tma_k_tile(int m);
 cudaError_t dgemm_tma_k(cudaStream_t st, int M, int N, int K, const double* A, long long lda, const double* B,
                         long long ldb, double* C, long long ldc, double alpha, double beta, const double* scale,
                         bool lower, int splits, int k_chunk, double* partial);
@@ -94,6 +94,9 @@ cudaError_t quad_nodes(cudaStream_t st, int n_mu, int n_v, int n_c, const double
 // D2Z output column of 2*n3*n2*(n1/2+1) interleaved reals.
 cudaError_t coulomb_half_weights(cudaStream_t st, int n1, int n2, int n3, double c1, double c2,
                                  double c3, int zero_kernel, double* w);
+// The same scale with a caller-supplied full-grid kernel v (its G / -G average).
+cudaError_t coulomb_scale_half_custom(cudaStream_t st, int n1, int n2, int n3, const double* v, double* xhat,
+                                      int cols);
 // y(r) = x_hat(G) * v(G) / N_r over the half spectrum (in place, complex).
 cudaError_t coulomb_scale_half(cudaStream_t st, int n1, int n2, int n3, double c1, double c2,
                                double c3, int zero_kernel, double* xhat, int cols);

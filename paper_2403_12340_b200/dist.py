@@ -20,7 +20,9 @@ deterministic exchange logic:
   stage 5b SMW core replicated; probe: all-reduce of Theta_p^T x.
 
 `Backend` is the per-rank compute interface; tests inject a numpy backend
-(tests/test_dist.py) and run world sizes 2-3 over gloo on CPU.
+(tests/test_dist.py) and run world sizes 2-3 over gloo on CPU. The product
+path is the same scheme in C++/CUDA behind the C-ABI (lrgw_build_sharded,
+csrc/sharded.cu), which tests/test_gpu_dist.py checks at worlds 1-3.
 """
 from __future__ import annotations
 
@@ -262,7 +264,9 @@ class DistributedBuild:
         self.dims, self.cell = tuple(dims), tuple(cell)
         self.n_r = dims[0] * dims[1] * dims[2]
         self.n_v, self.n_c = n_v, n_c
-        self.n_mu = min(max(int(math.floor(k_mu * math.sqrt(n_v * n_c) + 0.5)), 1), self.n_r)
+        from . import lrgw  # num_aux through the C-ABI (llround, isdf.hpp:42-46)
+
+        self.n_mu = min(max(lrgw.num_aux(k_mu, n_v, n_c), 1), self.n_r)
         self.n_lambda = n_lambda
         self.batch = batch
         r0, r1 = z_panels(dims, comm.world)[comm.rank]

@@ -28,3 +28,19 @@ def test_dropin_reference_kats(tmp_path):
     _compile(exe)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+SUITES = ["smw", "contour", "isdf", "elliptic", "linalg", "model"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_suite_unchanged_on_dropin(tmp_path, suite):
+    """The reference's OWN proj/tests/test_<suite>.cpp, compiled unchanged
+    against include/lrgw/*.hpp (tests/cpp/Makefile, doctest stand-in), runs
+    green on the B200 path."""
+    exe = os.path.join(ROOT, "tests", "cpp", "_ref", f"ref_test_{suite}")
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900, cwd=str(tmp_path))
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
