@@ -54,7 +54,9 @@ enum lrgw_stage {
   LRGW_STAGE_SMW = 7,       /* K6 SMW core K (cuSOLVER potrf leaves + DMMA)    */
   LRGW_STAGE_TOTAL = 8,
   LRGW_STAGE_QUAD_KERNEL = 9, /* the K3 kernel alone (last quadrature launch)  */
-  LRGW_NUM_STAGES = 10
+  LRGW_STAGE_CUSOLVER = 10,   /* the cuSOLVER potrf leaves inside SMW (summed)  */
+  LRGW_STAGE_CUFFT = 11,      /* the cuFFT D2Z leaf of FFT (= FFT; listed apart) */
+  LRGW_NUM_STAGES = 12
 };
 
 typedef struct lrgw_ctx_s* lrgw_ctx;

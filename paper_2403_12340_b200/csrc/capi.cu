@@ -381,9 +381,13 @@ int potrf_lower(lrgw_ctx c, double* a, int n) {
   cks(cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, n, a, n, &lwork), "potrf_bufferSize");
   DBuf work = dalloc(c, (size_t)std::max(lwork, 1));
   DBuf info = ialloc(c, 1);
+  if (c->timing) ck(cudaEventRecord(c->ev_lib[0], c->stream), "cudaEventRecord");
   cks(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, n, a, n, work.d(), lwork, info.i()), "potrf");
+  if (c->timing) ck(cudaEventRecord(c->ev_lib[1], c->stream), "cudaEventRecord");
   int h = 0;
   download(c, &h, info.p, sizeof(int));
+  float ms = 0.0f;
+  if (c->timing && cudaEventElapsedTime(&ms, c->ev_lib[0], c->ev_lib[1]) == cudaSuccess) c->lib_ms += ms;
   return h;
 }
 
@@ -1001,6 +1005,8 @@ int lrgw_ctx_destroy(lrgw_ctx c) {
     if (x) cudaEventDestroy(x);
   for (auto& x : c->ev_quad)
     if (x) cudaEventDestroy(x);
+  for (auto& x : c->ev_lib)
+    if (x) cudaEventDestroy(x);
   delete c;
   return LRGW_OK;
 }
@@ -1444,6 +1450,9 @@ void timing_begin(lrgw_ctx c) {
     if (!x) ck(cudaEventCreate(&x), "event");
   for (auto& x : c->ev_quad)
     if (!x) ck(cudaEventCreate(&x), "event");
+  for (auto& x : c->ev_lib)
+    if (!x) ck(cudaEventCreate(&x), "event");
+  c->lib_ms = 0.0;
   c->timing = true;
   mark(c, 0);
 }
@@ -1462,6 +1471,8 @@ void timing_end(lrgw_ctx c) {
   if (c->quad_timed && cudaEventElapsedTime(&ms, c->ev_quad[0], c->ev_quad[1]) == cudaSuccess)
     c->stage_ms[LRGW_STAGE_QUAD_KERNEL] = ms;
   c->quad_timed = false;
+  c->stage_ms[LRGW_STAGE_CUSOLVER] = c->lib_ms;
+  c->stage_ms[LRGW_STAGE_CUFFT] = c->stage_ms[LRGW_STAGE_FFT];
   c->timing = false;
 }
 

@@ -93,7 +93,8 @@ def _check(rc, ctx_handle=None, what=""):
 # ---------------------------------------------------------------------------
 
 
-STAGES = ["select", "fit_lhs", "fit_solve", "fit_gemm", "contour", "fft", "pvp", "smw", "total", "quad_kernel"]
+STAGES = ["select", "fit_lhs", "fit_solve", "fit_gemm", "contour", "fft", "pvp", "smw", "total", "quad_kernel",
+          "cusolver", "cufft"]
 
 
 class Context:
