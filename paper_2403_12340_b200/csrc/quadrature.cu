@@ -330,8 +330,21 @@ cudaError_t quad_nodes(cudaStream_t st, int n_mu, int n_v, int n_c, const double
   using V1 = std::integral_constant<int, 1>;
   using V2 = std::integral_constant<int, 2>;
   const int nb = std::min(n_v, n_c);
-  if (nb >= 64) {
+  // k-tile depth: the deepest of 64 / 48 / 40 that pads the two bands least
+  // (C60's 120 = 3 x 40: no dead k; Si216's 432 = 9 x 48)
+  auto waste = [&](int bk) { return (n_v + bk - 1) / bk * bk - n_v + (n_c + bk - 1) / bk * bk - n_c; };
+  int bk = 64;
+  if (nb >= 40)
+    for (int cand : {48, 40})
+      if (waste(cand) < waste(bk)) bk = cand;
+  if (nb >= 64 && bk == 64) {
     using B = std::integral_constant<int, 64>;
+    vec ? go(V2{}, B{}) : go(V1{}, B{});
+  } else if (nb >= 48 && bk == 48) {
+    using B = std::integral_constant<int, 48>;
+    vec ? go(V2{}, B{}) : go(V1{}, B{});
+  } else if (nb >= 40 && bk == 40) {
+    using B = std::integral_constant<int, 40>;
     vec ? go(V2{}, B{}) : go(V1{}, B{});
   } else if (nb >= 32) {
     using B = std::integral_constant<int, 32>;

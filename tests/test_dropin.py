@@ -30,7 +30,7 @@ def test_dropin_reference_kats(tmp_path):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
-SUITES = ["smw", "contour", "isdf", "elliptic", "linalg", "model"]
+SUITES = ["smw", "contour", "isdf", "elliptic", "linalg", "model", "gw"]
 
 
 @pytest.mark.gpu
