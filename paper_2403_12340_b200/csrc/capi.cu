@@ -564,7 +564,9 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
   const int lds = s + (s & 1);  // even leading dims: 16-byte operand loads
 
   DBuf d = dalloc(c, n_r), pos = ialloc(c, n_r), perm = ialloc(c, n_r);
-  DBuf L = dalloc(c, (size_t)n_r * std::max(steps, 1));
+  // (lrgw_build sizes L like the half spectrum that later takes its block from
+  // the cache: one Theta-sized block cycles L -> spectrum -> L across builds)
+  DBuf L = dalloc(c, std::max((size_t)n_r * std::max(steps, 1), keep ? keep->min_l_elems : 0));
   DBuf wsel = dalloc(c, (size_t)n_r * s);                       // W columns of the accepted pivots
   DBuf amu = dalloc(c, (size_t)lds * n1), bmu = dalloc(c, (size_t)lds * n2);
   DBuf lrow = dalloc(c, (size_t)lds * std::max(steps, 1));       // L rows of candidates / pivots
@@ -1488,6 +1490,7 @@ lrgw_eps_s* build_one(lrgw_ctx c, const lrgw_build_params& P, const BuildSetup& 
   timing_begin(c);
   // stage 1
   SelectKeep keep;
+  keep.min_l_elems = (size_t)2 * half_len(P.dims) * n_mu;
   double min_margin = -1.0;  // smallest relative top-2 residual margin over all steps (linalg.hpp:45-47)
   std::vector<int32_t> pts = select_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, n_mu, &min_margin, &keep);
   mark(c, 1);

@@ -237,6 +237,7 @@ struct SelectKeep {
   int steps = 0;
   int blocks = 0;           // candidate blocks (one host sync each)
   int min_margin_step = -1; // step of the smallest top-2 margin (when margins are requested)
+  size_t min_l_elems = 0;   // allocate L at least this large (cache block reuse; see select_impl)
 };
 std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int n1, const double* b, long long ldb,
                                  int n2, int n_r, int n_mu, double* min_margin, SelectKeep* keep = nullptr);
