@@ -304,3 +304,47 @@ def test_si8_pipeline_matches_reference(L, ctx, ref):
     ep = L.build_epsilon_inverse(t, th, cfg.dims, cfg.cell3, ctx=ctx)
     assert rel(ep.k, k_ref) <= TOL
     assert rel(L.epsilon_inverse_apply(ep, x), y_ref) <= TOL
+
+
+_DOWNDATE_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2403_12340_b200 import lrgw
+rng = np.random.default_rng(23)
+n_r = int(sys.argv[2])
+q = np.linalg.qr(rng.standard_normal((n_r, 28)))[0]
+a, b = np.asfortranarray(q[:, :14]), np.asfortranarray(q[:, 14:])
+ctx = lrgw.Context(0)
+ctx.set_select_batch(24)
+pts = lrgw.select_interpolation_points(a, b, 96, ctx=ctx)
+np.save(sys.argv[3], pts)
+"""
+
+
+@pytest.mark.parametrize("n_r", [315, 1000])
+def test_selection_pivots_with_and_without_fused_downdate(tmp_path, n_r):
+    """The residual downdate fused into the L-block GEMM epilogue and the
+    separate downdate kernel (LRGW_FUSED_DOWNDATE=0) round d differently; on
+    odd and even row counts both must give the oracle's pivots (several
+    candidate blocks, batch 24)."""
+    import os
+    import subprocess
+    import sys
+
+    from oracle import restate as R
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "sel.py"
+    script.write_text(_DOWNDATE_SCRIPT)
+    out = {}
+    for fused in ("1", "0"):
+        env = dict(os.environ, LRGW_FUSED_DOWNDATE=fused)
+        path = tmp_path / f"pts_{fused}.npy"
+        r = subprocess.run([sys.executable, str(script), root, str(n_r), str(path)], env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[fused] = np.load(path)
+    rng = np.random.default_rng(23)
+    q = np.linalg.qr(rng.standard_normal((n_r, 28)))[0]
+    want = R.select_points(q[:, :14], q[:, 14:], 96)
+    assert np.array_equal(out["1"], want) and np.array_equal(out["0"], want)
