@@ -597,7 +597,8 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
     if (k > 0)
       gemm(c, se, se, k, lrow.d(), lds, Lay::MN, lrow.d(), lds, Lay::MN, wcc.d(), se, -1.0, 1.0, nullptr, false, &w);
     ck(select_cand_greedy(c->stream, n_r, se, steps, k, top.p, wcc.d(), pos.i(), perm.i(), xcol.d(), order.i(),
-                          min_margin ? margin.d() : nullptr, bout),
+                          min_margin ? margin.d() : nullptr, bout, select_accept_cap(se, n_r),
+                          select_accept_round()),
        "cand_greedy");
     int nb = 0;
     download(c, &nb, bout, sizeof(int));  // the one host sync per block
@@ -1710,7 +1711,7 @@ int lrgw_dev_cand_greedy(lrgw_ctx c, int n_r, int s, int steps, int k, const dou
     DBuf marg = dalloc(c, steps);
     DBuf bout = ialloc(c, 2);
     ck(select_cand_greedy(c->stream, n_r, s, steps, k, top.p, wcc, pos, perm, x, (int*)order.p,
-                          margins ? (double*)marg.p : nullptr, (int*)bout.p),
+                          margins ? (double*)marg.p : nullptr, (int*)bout.p, s, 0),
        "cand_greedy");
     int nb[2] = {0, 0};
     download(c, nb, bout.p, sizeof(nb));

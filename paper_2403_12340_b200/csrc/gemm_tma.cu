@@ -159,7 +159,9 @@ cudaError_t dgemm_tma(cudaStream_t st, int M, int N, int K, const double* A, lon
   p.vec_store = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 2 == 0;
   // full 128-wide column tiles only: the tall-skinny widths of the selection
   // stay on the cp.async family (2-3 CTAs per SM; 33-62 % here at widths 32-96)
-  if (n_dev || N < 128) return cudaErrorNotSupported;
+  static const int tall_min = getenv("LRGW_TMA_TALL") ? atoi(getenv("LRGW_TMA_TALL")) : 0;
+  if (N < 128 && !(tall_min > 0 && N >= tall_min)) return cudaErrorNotSupported;
+  if (n_dev && !(tall_min > 0)) return cudaErrorNotSupported;
   if (mncfg() == 1) return launch4<T4S>(st, ma, mb, ma, mb, p);
   return launch4<T4<128>>(st, ma, mb, ma, mb, p);
 }

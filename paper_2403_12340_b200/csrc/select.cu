@@ -304,6 +304,7 @@ constexpr int CG_MAX = 128;              // candidates
 
 struct CandParams {
   int n_r, s, steps, kb;
+  int bmax, bround;  // accept at most bmax steps; a shorter run of >= bround steps keeps bround
   const Ent* top;       // s + 1 entries: candidates then the tau entry
   const double* wcc;    // s x s, ld s: W[C, C] (symmetric)
   int* pos;             // grid row -> position
@@ -466,12 +467,16 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
   __shared__ int rjs[CG_MAX];  // controller: candidate grid rows
   __shared__ int pss[CG_MAX];  // controller: perm[kb + j] (position slots of the block)
   __shared__ unsigned usedsh[4];  // candidates taken / absent before this step (bit l of word c: l + 32 c)
+  // per-step position swaps and margins, applied to global memory after the
+  // loop for the accepted prefix only
+  __shared__ int rec_gp[CG_MAX], rec_occ[CG_MAX], rec_pp[CG_MAX];
+  __shared__ double rec_mg[CG_MAX];
 
   for (int idx = threadIdx.x; idx < s * s; idx += blockDim.x) p.xcol[idx] = 0.0;
 
   const double tau = p.top[s].row >= 0 ? p.top[s].v : -DBL_MAX;
   __shared__ int tmax_s;  // read from smem on the controller's path (keeps it out of the register budget)
-  if (threadIdx.x == 0) tmax_s = min(s, p.steps - p.kb);
+  if (threadIdx.x == 0) tmax_s = min(min(s, p.bmax), p.steps - p.kb);
   const bool want_sv = p.margin != nullptr;
 
   // controller state (warp 0), entries j = lane + 32 c
@@ -553,17 +558,15 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
                                      (t + 1 < tmax_s && i1 >= 0 && v1 > tau) ? 1 : 0};
       if (lane == 0) {
         const int gp = rjs[i0];  // pivot grid row
-        p.perm[k] = gp;
-        p.perm[piv_pos] = occ;
-        p.pos[gp] = k;
-        p.pos[occ] = piv_pos;
+        rec_gp[t] = gp;
+        rec_occ[t] = occ;
+        rec_pp[t] = piv_pos;
         sel[t] = i0;
         // position slots: perm[ppos] = occ, then perm[k] = gp
         if (piv_pos - p.kb < CG_MAX) pss[piv_pos - p.kb] = occ;
         pss[t] = gp;
-        p.piv_order[k] = gp;
         usedsh[i0 >> 5] |= 1u << (i0 & 31);  // only bit i0 changes: workers exclude it already
-        if (want_sv) p.margin[k] = pv.v0 > 0.0 ? (pv.v0 - fmax(svp, tau)) / pv.v0 : 0.0;
+        rec_mg[t] = pv.v0 > 0.0 ? (pv.v0 - fmax(svp, tau)) / pv.v0 : 0.0;
       }
     }
     // ---- eliminate: w -= r_i r_j / d_i0 (row / column i0 are never read
@@ -599,7 +602,22 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
     }
     __syncthreads();
   }
-  const int b = t;
+  // the accepted prefix: every step of the run is certified, so any prefix is
+  // exactly the reference's next pivots; a run the certificate stopped short
+  // of bmax keeps a tile-friendly bround steps (the rest are re-found next
+  // block)
+  const int b = (t < tmax_s && p.bround > 0 && t >= p.bround) ? p.bround : t;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < b; ++q) {  // the swaps in step order
+      const int k = p.kb + q, gp = rec_gp[q], occ = rec_occ[q], pp = rec_pp[q];
+      p.perm[k] = gp;
+      p.perm[pp] = occ;
+      p.pos[gp] = k;
+      p.pos[occ] = pp;
+      p.piv_order[k] = gp;
+      if (want_sv) p.margin[k] = rec_mg[q];
+    }
+  }
   cand_tri_inverse(lcs, lsel, sel, b, s, p.xcol);
   if (threadIdx.x == 0) {
     p.b_out[0] = b;
@@ -664,10 +682,29 @@ size_t select_cand_smem_bytes(int) {
 
 int select_max_candidates() { return CG_MAX; }
 
+// Measured on the Si512 selection (profiles/r02/select_widths_si512.txt): the
+// tall-skinny engines run 0.85-0.90 of the DMMA peak at an exact 96-wide
+// column tile and 0.74-0.80 at the 100-127 widths a 128-candidate block
+// certifies (112 / 128 tiles with dead columns), so a block accepts the first
+// 96 certified pivots — 80 below 2e5 grid rows, where the 96-wide tiles'
+// last wave is mostly empty (profiles/r02/select_accept.txt: Si64 10.9 ->
+// 10.45 ms, Si216 255 -> 234 ms, Si512 3192 -> 2868 ms). LRGW_SELECT_ACCEPT
+// overrides (0 = all certified steps).
+int select_accept_cap(int s, int n_r) {
+  static const int env = getenv("LRGW_SELECT_ACCEPT") ? atoi(getenv("LRGW_SELECT_ACCEPT")) : -1;
+  const int cap = env >= 0 ? env : (n_r < 200000 ? 80 : 96);
+  return cap > 0 ? std::min(cap, s) : s;
+}
+int select_accept_round() {
+  static const int r = getenv("LRGW_SELECT_ROUND") ? atoi(getenv("LRGW_SELECT_ROUND")) : 80;
+  return std::max(0, r);
+}
+
 cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* wcc,
-                               int* pos, int* perm, double* xcol, int* piv_order, double* margin, int* b_out) {
+                               int* pos, int* perm, double* xcol, int* piv_order, double* margin, int* b_out,
+                               int bmax, int bround) {
   const Ent* tp = static_cast<const Ent*>(top);
-  CandParams p{n_r, s, steps, kb, tp, wcc, pos, perm, xcol, piv_order, margin, b_out};
+  CandParams p{n_r, s, steps, kb, std::max(1, bmax), bround, tp, wcc, pos, perm, xcol, piv_order, margin, b_out};
   const size_t smem = select_cand_smem_bytes(s);
   cudaError_t e = cudaFuncSetAttribute(cand_greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

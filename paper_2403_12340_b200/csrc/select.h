@@ -26,7 +26,14 @@ size_t select_cand_smem_bytes(int s);
 // margin != nullptr); xcol (ld s) = X = L_sel^-1 column-major (b x b lower,
 // L_sel the accepted steps' l values at the accepted rows, in pivot order).
 cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* wcc,
-                               int* pos, int* perm, double* xcol, int* piv_order, double* margin, int* b_out);
+                               int* pos, int* perm, double* xcol, int* piv_order, double* margin, int* b_out,
+                               int bmax, int bround);
+// Pivots the block pipeline accepts per candidate block (a prefix of the
+// certified greedy run): at most select_accept_cap, and a run that stops
+// between select_accept_round and the cap keeps select_accept_round — the
+// widths the tall-skinny GEMM tiles run best at.
+int select_accept_cap(int s, int n_r);
+int select_accept_round();
 // d -= rowsum(L[:, kb:kb+b]^2) over unselected rows.
 cudaError_t select_downdate(cudaStream_t st, const double* L, int n_r, int kb, int b, const int* pos, double* d,
                             const int* b_dev = nullptr);

@@ -263,7 +263,8 @@ PanelSelect select_panel(lrgw_ctx c, lrgw_comm m, const Panels& pn, const double
        "hadamard_gemm(W_CC)");
     if (k > 0) gemm(c, se, se, k, lrow, lds, Lay::MN, lrow, lds, Lay::MN, wcc.d(), se, -1.0, 1.0, nullptr, false, &w);
     ck(select_cand_greedy(c->stream, n_r, se, steps, k, top.p, wcc.d(), pos.i(), perm.i(), xcol.d(), order.i(),
-                          margin.d(), bout.i()),
+                          margin.d(), bout.i(), select_accept_cap(se, n_r),
+                          select_accept_round()),
        "cand_greedy");
     int nb = 0;
     download(c, &nb, bout.p, sizeof(int));  // the one host sync per block
