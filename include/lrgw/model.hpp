@@ -63,8 +63,10 @@ inline ElectronicStructure build_synthetic_system(std::uint64_t seed, const Grid
   std::vector<cplx> coef(n_r);
   for (int b = 0; b < nb; ++b) {
     for (int idx = 0; idx < n_r; ++idx) {
-      const double re = rng.gaussian(), im = rng.gaussian();  // the reference's draw order
-      coef[idx] = env[idx] * cplx(re, im);
+      // the same expression as model.hpp:84: C++ leaves the order of the two
+      // draws to the compiler (GCC evaluates the imaginary argument first),
+      // so the drop-in inherits whatever order the reference's build gets
+      coef[idx] = env[idx] * cplx(rng.gaussian(), rng.gaussian());
     }
     const std::vector<cplx> field = dft(grid, coef, DftDirection::inverse);
     for (int idx = 0; idx < n_r; ++idx) fields(idx, b) = field[idx].real();

@@ -499,15 +499,32 @@ void trtri_lower(lrgw_ctx c, double* a, int n) {
 //   K = -R M^-1 R^T = -Z Z^T,   Z = R Q^-T,  M = Q Q^T
 // i.e. two Cholesky factorisations and one triangular inverse (cuSOLVER
 // leaves) plus four N_mu^3 DMMA GEMMs; K is symmetric by construction.
+// Every check (the two potrf infos, the two tiny-pivot scans, the trtri flag)
+// lands in one device status block read once at the end — one host sync
+// instead of seven — and is evaluated in the order the steps run, so the
+// first failing step names the error as before.
 void smw_core(lrgw_ctx c, const double* t, const double* pvp, int n, double* k) {
   const size_t nn = (size_t)n * n;
-  const double mx = dev_max_abs(c, t, nn);
+  enum { INFO_T, TINY_T, INFO_M, TINY_M, TRTRI_BAD, NSTAT };
+  DBuf stat = ialloc(c, NSTAT);
+  int* sd = stat.i();
+  ck(cudaMemsetAsync(sd, 0x7f, NSTAT * sizeof(int), c->stream), "memset");
+  DBuf mxb = dalloc(c, 2 * 512);
+  int lwork = 0;
+  cks(cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, n, const_cast<double*>(t), n, &lwork),
+      "potrf_bufferSize");
+  DBuf pwork = dalloc(c, (size_t)std::max(lwork, 1));
+  float lib_ms = 0.0f;
+  auto potrf = [&](double* a, int* info, int ev0) {
+    if (c->timing) ck(cudaEventRecord(c->ev_lib[ev0], c->stream), "cudaEventRecord");
+    cks(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, n, a, n, pwork.d(), lwork, info), "potrf");
+    if (c->timing) ck(cudaEventRecord(c->ev_lib[ev0 + 1], c->stream), "cudaEventRecord");
+  };
+  ck(max_abs(c->stream, t, nn, mxb.d()), "max_abs");
   DBuf r = dalloc(c, nn);
   ck(scale_copy(c->stream, t, r.d(), nn, -1.0), "scale_copy");
-  if (potrf_lower(c, r.d(), n) != 0)
-    fail(LRGW_ERR_NUMERIC, "assemble_K: T is not negative definite (gapless or rank-deficient input)");
-  const int tp = tiny_pivot(c, r.d(), n, mx);
-  if (tp >= 0) fail(LRGW_ERR_SINGULAR, "assemble_K: T singular", tp);
+  potrf(r.d(), sd + INFO_T, 0);
+  ck(tiny_pivot_dev(c->stream, r.d(), n, n, mxb.d() + 296, sd + TINY_T), "tiny_pivot");
   ck(zero_strict_upper(c->stream, r.d(), n, n), "zero_upper");
   Work w = make_work(c, 8 * nn);
   // Y = P R   (R lower: R(k, j) = 0 for k < j)
@@ -520,16 +537,33 @@ void smw_core(lrgw_ctx c, const double* t, const double* pvp, int n, double* k) 
   gemm(c, n, n, n, r.d(), n, Lay::K, y.d(), n, Lay::K, m.d(), n, 1.0, 0.0, nullptr, true, &w);
   ck(mirror_lower(c->stream, m.d(), n, n, false), "mirror");
   ck(add_diag(c->stream, m.d(), n, n, 0.5), "add_diag");
-  const double mx2 = dev_max_abs(c, m.d(), nn);
-  if (potrf_lower(c, m.d(), n) != 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", 0);
-  const int tp2 = tiny_pivot(c, m.d(), n, mx2);
-  if (tp2 >= 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", tp2);
+  ck(max_abs(c->stream, m.d(), nn, mxb.d() + 512), "max_abs");
+  potrf(m.d(), sd + INFO_M, 2);
+  ck(tiny_pivot_dev(c->stream, m.d(), n, n, mxb.d() + 512 + 296, sd + TINY_M), "tiny_pivot");
   ck(zero_strict_upper(c->stream, m.d(), n, n), "zero_upper");
-  trtri_lower(c, m.d(), n);  // Q^-1
+  // Q^-1 (recursive DMMA trtri; a zero pivot -> TRTRI_BAD = its index + 1)
+  {
+    DBuf twork = dalloc(c, trtri_work_elems(n));
+    ck(lrgw_dev::trtri_lower(c->stream, m.d(), n, n, twork.d(), sd + TRTRI_BAD, c->sm_count), "trtri");
+  }
   // Z = R Q^-T ; K = -Z Z^T (lower tiles, mirrored)
   gemm(c, n, n, n, r.d(), n, Lay::MN, m.d(), n, Lay::MN, y.d(), n, 1.0, 0.0);
   gemm(c, n, n, n, y.d(), n, Lay::MN, y.d(), n, Lay::MN, k, n, -1.0, 0.0, nullptr, true, &w);
   ck(mirror_lower(c->stream, k, n, n, false), "mirror");
+  int h[NSTAT];
+  download(c, h, sd, sizeof(h));
+  if (c->timing) {
+    float ms = 0.0f;
+    for (int e = 0; e < 4; e += 2)
+      if (cudaEventElapsedTime(&ms, c->ev_lib[e], c->ev_lib[e + 1]) == cudaSuccess) lib_ms += ms;
+    c->lib_ms += lib_ms;
+  }
+  const int unset = 0x7f7f7f7f;
+  if (h[INFO_T] != 0) fail(LRGW_ERR_NUMERIC, "assemble_K: T is not negative definite (gapless or rank-deficient input)");
+  if (h[TINY_T] >= 0) fail(LRGW_ERR_SINGULAR, "assemble_K: T singular", h[TINY_T]);
+  if (h[INFO_M] != 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", 0);
+  if (h[TINY_M] >= 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", h[TINY_M]);
+  if (h[TRTRI_BAD] != unset) fail(LRGW_ERR_SINGULAR, "trtri: singular factor", h[TRTRI_BAD] - 1);
 }
 
 // ---------------------------------------------------------------------------

@@ -61,7 +61,7 @@ struct lrgw_ctx_s {
   double stage_ms[LRGW_NUM_STAGES] = {};
   cudaEvent_t ev[LRGW_NUM_STAGES + 1] = {};
   cudaEvent_t ev_quad[2] = {};  // around the K3 kernel (timing builds only)
-  cudaEvent_t ev_lib[2] = {};   // around each cuSOLVER leaf of a timed build
+  cudaEvent_t ev_lib[4] = {};   // around the cuSOLVER leaves of a timed build
   double lib_ms = 0.0;          // their sum
   bool quad_timed = false;
   bool timing = false;  // record stage events (lrgw_build only)

@@ -122,6 +122,9 @@ cudaError_t add_diag(cudaStream_t st, double* a, int n, long long lda, double v)
 cudaError_t axpby(cudaStream_t st, int rows, int cols, double alpha, const double* x, long long ldx,
                   double beta, double* y, long long ldy);
 cudaError_t max_abs(cudaStream_t st, const double* x, size_t n, double* d_out);
+// first i with chol(i, i)^2 < 1e-14 max(*max_abs_a, 1 if 0) (or NaN), else -1 -> *out
+cudaError_t tiny_pivot_dev(cudaStream_t st, const double* chol, int n, long long ld, const double* max_abs_a,
+                           int* out);
 // sigma.cu: m = h o m (n x n); out[j] = alpha * a(:, j) . b(:, j).
 cudaError_t hadamard_inplace(cudaStream_t st, int n, const double* h, long long ldh, double* m, long long ldm);
 cudaError_t col_dot(cudaStream_t st, int rows, int cols, const double* a, long long lda, const double* b,

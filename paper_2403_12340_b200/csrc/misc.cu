@@ -1,4 +1,5 @@
 // misc.cu — small elementwise / reduction kernels used around the hot path.
+#include <climits>
 #include "kernels.h"
 
 namespace lrgw_dev {
@@ -162,6 +163,33 @@ cudaError_t zero_strict_upper(cudaStream_t st, double* a, int n, long long lda) 
 cudaError_t max_abs(cudaStream_t st, const double* x, size_t n, double* d_out) {
   max_abs_kernel<<<kRedBlocks, 256, 0, st>>>(x, n, d_out); count_launches(1);
   finish_kernel<<<1, 32, 0, st>>>(d_out, kRedBlocks, d_out + kRedBlocks, 1); count_launches(1);
+  return cudaGetLastError();
+}
+
+// First index i with chol(i, i)^2 < 1e-14 max|A| (the LU singularity rule of
+// linalg.hpp:128, 137 on a Cholesky factor), or -1, into *out. One CTA.
+__global__ void tiny_pivot_kernel(const double* chol, int n, long long ld, const double* max_abs_a, int* out) {
+  __shared__ int best;
+  if (threadIdx.x == 0) best = INT_MAX;
+  __syncthreads();
+  const double mx = *max_abs_a;
+  const double tiny = 1e-14 * (mx > 0.0 ? mx : 1.0);
+  int mine = INT_MAX;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double d = chol[(long long)i * (ld + 1)];
+    if (d * d < tiny) {
+      mine = i;
+      break;
+    }
+  }
+  if (mine != INT_MAX) atomicMin(&best, mine);
+  __syncthreads();
+  if (threadIdx.x == 0) *out = best == INT_MAX ? -1 : best;
+}
+
+cudaError_t tiny_pivot_dev(cudaStream_t st, const double* chol, int n, long long ld, const double* max_abs_a,
+                           int* out) {
+  tiny_pivot_kernel<<<1, 256, 0, st>>>(chol, n, ld, max_abs_a, out); count_launches(1);
   return cudaGetLastError();
 }
 

@@ -48,7 +48,7 @@ def main():
             print(json.dumps({"variant": var, "error": (r.stderr or r.stdout)[-800:]}), flush=True)
             continue
         for row in json.loads(line[0][7:]):
-            keep = {k: row[k] for k in ("select", "fit_gemm", "pvp", "contour", "fft", "total", "pts") if k in row}
+            keep = {k: row[k] for k in ("select", "fit_gemm", "pvp", "contour", "fft", "smw", "cusolver", "total", "pts") if k in row}
             print(json.dumps({"variant": var, **keep}), flush=True)
 
 
