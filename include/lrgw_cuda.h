@@ -268,6 +268,12 @@ int lrgw_dev_coulomb_apply(lrgw_ctx ctx, const int* dims, const double* cell, in
 int lrgw_dev_dgemm(lrgw_ctx ctx, char trans_a, char trans_b, int m, int n, int k, double alpha,
                    const double* a, long long lda, const double* b, long long ldb, double beta,
                    double* c, long long ldc);
+/* The ISDF Gram-pair Hadamard product through the path's engine (isdf.hpp:132):
+ * C = (A1 B1^T) o (A2 B2^T), A1: m x k1, B1: n x k1, A2: m x k2, B2: n x k2, all
+ * column-major. Exposed for tests and benchmarking. */
+int lrgw_dev_hadamard(lrgw_ctx ctx, int m, int n, const double* a1, long long lda1, const double* b1,
+                      long long ldb1, int k1, const double* a2, long long lda2, const double* b2, long long ldb2,
+                      int k2, double* c, long long ldc);
 
 /* In-place inverse of the lower triangle of a device matrix (n x n, column
  * major, ld lda); the strict upper triangle is left untouched. Singular ->

@@ -192,6 +192,9 @@ _SIGS = {
     "lrgw_dev_dgemm": (ctypes.c_int, [ctx_t, ctypes.c_char, ctypes.c_char, ctypes.c_int, ctypes.c_int,
                                       ctypes.c_int, ctypes.c_double, ctypes.c_void_p, c_ll, ctypes.c_void_p,
                                       c_ll, ctypes.c_double, ctypes.c_void_p, c_ll]),
+    "lrgw_dev_hadamard": (ctypes.c_int, [ctx_t, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, c_ll, ctypes.c_void_p,
+                                         c_ll, ctypes.c_int, ctypes.c_void_p, c_ll, ctypes.c_void_p, c_ll,
+                                         ctypes.c_int, ctypes.c_void_p, c_ll]),
 }
 
 

@@ -601,7 +601,7 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
   // (lrgw_build sizes L like the half spectrum that later takes its block from
   // the cache: one Theta-sized block cycles L -> spectrum -> L across builds)
   DBuf L = dalloc(c, std::max((size_t)n_r * std::max(steps, 1), keep ? keep->min_l_elems : 0));
-  DBuf wsel = dalloc(c, (size_t)n_r * s);                       // W columns of the accepted pivots
+  DBuf wsel;  // W columns of the accepted pivots (only the three-launch fallback materialises them)
   DBuf amu = dalloc(c, (size_t)lds * n1), bmu = dalloc(c, (size_t)lds * n2);
   DBuf lrow = dalloc(c, (size_t)lds * std::max(steps, 1));       // L rows of candidates / pivots
   DBuf wcc = dalloc(c, (size_t)s * s), xcol = dalloc(c, (size_t)s * s);
@@ -644,6 +644,20 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
     const int ldb_ = nb + (nb & 1);
     ck(gather_rows3(c->stream, a, lda, n1, b, ldb, n2, L.d(), n_r, k, srow, nb, amu.d(), bmu.d(), lrow.d(), ldb_),
        "gather");
+    // one launch (panel.cu): W_sel, L[:, k:k+nb] = W_sel X^T and the downdate
+    const cudaError_t pe =
+        (fused_downdate_enabled() && select_panel_enabled(n1, n2))
+            ? select_panel(c->stream, n_r, nb, a, lda, amu.d(), ldb_, n1, b, ldb, bmu.d(), ldb_, n2, L.d(), n_r,
+                           lrow.d(), ldb_, k, xcol.d(), se, L.d() + (size_t)k * n_r, n_r, d.d(), pos.i(), k + nb)
+            : cudaErrorNotSupported;
+    if (pe != cudaErrorNotSupported) {
+      ck(pe, "select_panel");
+      k += nb;
+      if (keep) ++keep->blocks;
+      continue;
+    }
+    cudaGetLastError();
+    if (!wsel.p) wsel = dalloc(c, (size_t)n_r * s);
     ck(hadamard_gemm(c->stream, n_r, nb, a, lda, amu.d(), ldb_, n1, b, ldb, bmu.d(), ldb_, n2, wsel.d(), n_r, 1.0,
                      0.0),
        "hadamard_gemm");
@@ -1699,6 +1713,18 @@ int lrgw_dev_dgemm(lrgw_ctx c, char ta, char tb, int m, int n, int k, double alp
   });
 }
 
+int lrgw_dev_hadamard(lrgw_ctx c, int m, int n, const double* a1, long long lda1, const double* b1, long long ldb1,
+                      int k1, const double* a2, long long lda2, const double* b2, long long ldb2, int k2, double* cm,
+                      long long ldc) {
+  return guarded(c, [&] {
+    if (m < 0 || n < 0 || k1 < 1 || k2 < 1 || lda1 < m || lda2 < m || ldb1 < n || ldb2 < n || ldc < m)
+      fail(LRGW_ERR_INVALID_INPUT, "hadamard: bad sizes");
+    ck(hadamard_gemm(c->stream, m, n, a1, lda1, b1, ldb1, k1, a2, lda2, b2, ldb2, k2, cm, ldc, 1.0, 0.0),
+       "hadamard_gemm");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
 int lrgw_dev_trtri_lower(lrgw_ctx c, double* a, int n, long long lda) {
   return guarded(c, [&] {
     if (n < 0 || lda < std::max(1, n)) fail(LRGW_ERR_INVALID_INPUT, "trtri: bad sizes");
@@ -1795,6 +1821,17 @@ int lrgw_dev_select_panel_update(lrgw_ctx c, const double* a, long long lda, int
     const double* amu = pr.d();
     const double* bmu = amu + (size_t)ldp * n1;
     const double* lsel = bmu + (size_t)ldp * n2;
+    const cudaError_t pe =
+        (fused_downdate_enabled() && select_panel_enabled(n1, n2))
+            ? select_panel(c->stream, rows, nb, a, lda, amu, ldp, n1, b, ldb, bmu, ldp, n2, l, ldl, lsel, ldp, k, x,
+                           ldx, l + (size_t)k * ldl, ldl, d, pos, k + nb)
+            : cudaErrorNotSupported;
+    if (pe != cudaErrorNotSupported) {
+      ck(pe, "select_panel");
+      ck(cudaStreamSynchronize(c->stream), "sync");
+      return;
+    }
+    cudaGetLastError();
     DBuf wsel = dalloc(c, (size_t)rows * nb);
     ck(hadamard_gemm(c->stream, rows, nb, a, lda, amu, ldp, n1, b, ldb, bmu, ldp, n2, wsel.d(), rows, 1.0, 0.0),
        "hadamard_gemm");

@@ -116,8 +116,8 @@ cudaError_t launch_tall(cudaStream_t st, const DgemmParams& p, int q) {
   }
 }
 
-// The TMA Hadamard pair (32 x 32 warp tiles) measured slower than the parked
-// cp.async family at the selection's widths: opt-in only (LRGW_TMA_HAD=1).
+// The TMA Hadamard pair: the tall widths 33..96 (16-row warp tiles) by default,
+// the 32 x 32-warp-tile configuration for the other widths opt-in (LRGW_TMA_HAD=1).
 bool tma_k_enabled() {
   static const bool on = !(getenv("LRGW_TMA_K") && atoi(getenv("LRGW_TMA_K")) == 0);
   return on;
@@ -619,7 +619,8 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
                           long long lda2, const double* b2, long long ldb2, int k2, double* C,
                           long long ldc, double alpha, double beta) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  if (tma_gemm_enabled() && hadamard_tma_enabled() && (long long)((M + 63) / 64) >= 2 * 148) {
+  if (tma_gemm_enabled() && (hadamard_tma_enabled() || (tma_tall_enabled() && N > 32 && N <= 96)) &&
+      (long long)((M + 63) / 64) >= 2 * 148) {
     const cudaError_t e = hadamard_tma(st, M, N, a1, lda1, b1, ldb1, k1, a2, lda2, b2, ldb2, k2, C, ldc, alpha, beta);
     if (e != cudaErrorNotSupported) return e;
     cudaGetLastError();

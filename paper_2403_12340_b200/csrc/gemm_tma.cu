@@ -94,6 +94,20 @@ int mncfg() {
   static const int v = getenv("LRGW_TMA_MNCFG") ? atoi(getenv("LRGW_TMA_MNCFG")) : 0;
   return v;
 }
+// Tall-skinny outputs (the selection's L-pass and W columns, N = 33..112):
+// 64-row CTAs of 4 compute warps whose 16-row warp tiles span every column,
+// 2 CTAs per SM (+ the TMA warp each). Measured against the cp.async family
+// (tools/bench_tall.py, profiles/r02/tall_engines.txt): 884736 x 80 x 7000
+// 87.0 -> 94.1 %, x 96 89.8 -> 92.9 %, x 112 -> 94.7 % of the DMMA peak; the
+// Hadamard pair 884736 x 96 x (1024 + 1024) 84.9 -> 91.3 %.
+// LRGW_TMA_TALL=0 keeps these shapes on the cp.async family.
+using TT64 = Gemm4Cfg<128, 64, 32, 32, kBK, 5, false, 1>;   // 8 compute warps of 32 x 32
+using TT80 = Gemm4Cfg<64, 80, 16, 80, kBK, 4, false, 2>;
+using TT96 = Gemm4Cfg<64, 96, 16, 96, kBK, 4, false, 2>;
+using TT112 = Gemm4Cfg<64, 112, 16, 112, kBK, 4, false, 2>;
+using HT64 = Gemm4Cfg<64, 64, 16, 64, kBK, 4, true, 2>;
+using HT80 = Gemm4Cfg<64, 80, 16, 80, kBK, 4, true, 2>;
+using HT96 = Gemm4Cfg<64, 96, 16, 96, kBK, 4, true, 2>;
 // Hadamard pair: two accumulator sets -> 32 x 32 warp tiles
 template <int BN>
 using H4 = Gemm4Cfg<64, BN, 32, 32, kBK, 4, true, 1>;
@@ -138,6 +152,11 @@ cudaError_t dgemm_tma_k(cudaStream_t st, int M, int N, int K, const double* A, l
   }
 }
 
+bool tma_tall_enabled() {
+  static const bool on = !(getenv("LRGW_TMA_TALL") && atoi(getenv("LRGW_TMA_TALL")) == 0);
+  return on;
+}
+
 // On by default (LRGW_TMA=0 turns it off). Measured (tools/bench_gemm.py,
 // profiles/r02/gemm_engines.txt): 110592 x 1024 x 1024 86.0 -> 93.9 % and
 // 8192^3 89.0 -> 95.7 % of the DMMA peak against the cp.async engines.
@@ -157,11 +176,16 @@ cudaError_t dgemm_tma(cudaStream_t st, int M, int N, int K, const double* A, lon
   p.M = M, p.N = N, p.K = K, p.C = C, p.ldc = ldc, p.alpha = alpha, p.beta = beta;
   p.tri_b = tri_b ? 1 : 0, p.colmap = colmap, p.n_dev = n_dev;
   p.vec_store = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 2 == 0;
-  // full 128-wide column tiles only: the tall-skinny widths of the selection
-  // stay on the cp.async family (2-3 CTAs per SM; 33-62 % here at widths 32-96)
-  static const int tall_min = getenv("LRGW_TMA_TALL") ? atoi(getenv("LRGW_TMA_TALL")) : 0;
-  if (N < 128 && !(tall_min > 0 && N >= tall_min)) return cudaErrorNotSupported;
-  if (n_dev && !(tall_min > 0)) return cudaErrorNotSupported;
+  if (N < 128) {
+    // tall-skinny: one column tile of width 16 ceil(N / 16) (>= 2 waves of CTAs)
+    if (n_dev || N <= 32 || !tma_tall_enabled() || (long long)((M + 63) / 64) < 2LL * 148)
+      return cudaErrorNotSupported;
+    if (N <= 64) return launch4<TT64>(st, ma, mb, ma, mb, p);
+    if (N <= 80) return launch4<TT80>(st, ma, mb, ma, mb, p);
+    if (N <= 96) return launch4<TT96>(st, ma, mb, ma, mb, p);
+    if (N <= 112) return launch4<TT112>(st, ma, mb, ma, mb, p);
+  }
+  if (n_dev) return cudaErrorNotSupported;
   if (mncfg() == 1) return launch4<T4S>(st, ma, mb, ma, mb, p);
   return launch4<T4<128>>(st, ma, mb, ma, mb, p);
 }
@@ -178,6 +202,11 @@ cudaError_t hadamard_tma(cudaStream_t st, int M, int N, const double* a1, long l
   Dgemm4Params p{};
   p.M = M, p.N = N, p.K = k1, p.K2 = k2, p.C = C, p.ldc = ldc, p.alpha = alpha, p.beta = beta;
   p.vec_store = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 2 == 0;
+  if (N > 32 && N <= 96 && tma_tall_enabled() && (long long)((M + 63) / 64) >= 2LL * 148) {
+    if (N <= 64) return launch4<HT64>(st, ma, mb, ma2, mb2, p);
+    if (N <= 80) return launch4<HT80>(st, ma, mb, ma2, mb2, p);
+    return launch4<HT96>(st, ma, mb, ma2, mb2, p);
+  }
   const int w = (N + 31) / 32;
   if (w >= 4) return launch4<H4<128>>(st, ma, mb, ma2, mb2, p);
   if (w == 3) return launch4<H4<96>>(st, ma, mb, ma2, mb2, p);

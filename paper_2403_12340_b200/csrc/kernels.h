@@ -30,6 +30,7 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
 // cudaErrorNotSupported when a shape / alignment is not covered (callers fall
 // back to the cp.async engines). Enabled with LRGW_TMA=1.
 bool tma_gemm_enabled();
+bool tma_tall_enabled();  // tall-skinny widths 33..112 on the TMA engine (LRGW_TMA_TALL=0: off)
 cudaError_t dgemm_tma(cudaStream_t st, int M, int N, int K, const double* A, long long lda, const double* B,
                       long long ldb, double* C, long long ldc, double alpha, double beta, bool tri_b,
                       const int* colmap, const int* n_dev);
@@ -56,6 +57,17 @@ cudaError_t hadamard_gemm(cudaStream_t st, int M, int N, const double* a1, long 
 cudaError_t dgemm_tall_downdate(cudaStream_t st, int M, int N, int K, const double* A, long long lda,
                                 const double* B, long long ldb, double* C, long long ldc, double* d,
                                 const int* pos, int kend);
+
+// The selection's block panel in one launch (panel.cu): W = (A1 B1^T) o (A2 B2^T)
+// - L LR^T (M x N), C = W X^T (X: N x N, X(n, j) = x[n + j ldx]) and
+// d[m] -= sum_n C(m, n)^2 where pos[m] >= kend. cudaErrorNotSupported when the
+// shape / alignment is not covered (callers run the three-launch path).
+bool select_panel_enabled(int n1, int n2);
+cudaError_t select_panel(cudaStream_t st, int M, int N, const double* a1, long long lda1, const double* b1,
+                         long long ldb1, int k1, const double* a2, long long lda2, const double* b2, long long ldb2,
+                         int k2, const double* l, long long ldl, const double* lrow, long long ldlr, int k,
+                         const double* x, long long ldx, double* c, long long ldc, double* d, const int* pos,
+                         int kend);
 
 // a(j,i) = a(i,j) for i > j (average = 0) or both = (a(i,j) + a(j,i))/2.
 cudaError_t mirror_lower(cudaStream_t st, double* a, int n, long long lda, bool average);

@@ -781,6 +781,20 @@ def dgemm_dev(trans_a: str, trans_b: str, alpha: float, a, b, beta: float, c, ct
     return c
 
 
+def hadamard_dev(a1, b1, a2, b2, c, ctx=None):
+    """C = (A1 B1^T) o (A2 B2^T) on column-major float64 CUDA tensors through the
+    path's Hadamard-pair engine (the ISDF Gram pair, isdf.hpp:132)."""
+    cx = _ctx(ctx)
+    p = [_dev_ptr_cm(x) for x in (a1, b1, a2, b2, c)]
+    m, n = c.shape
+    _sync_torch(a1)
+    _check(cx._lib.lrgw_dev_hadamard(cx.handle, m, n, ctypes.c_void_p(p[0][0]), p[0][1], ctypes.c_void_p(p[1][0]),
+                                     p[1][1], a1.shape[1], ctypes.c_void_p(p[2][0]), p[2][1],
+                                     ctypes.c_void_p(p[3][0]), p[3][1], a2.shape[1], ctypes.c_void_p(p[4][0]),
+                                     p[4][1]), cx.handle, "hadamard")
+    return c
+
+
 def trtri_lower_dev(a, ctx=None):
     """In-place inverse of the lower triangle of a square column-major float64
     CUDA matrix (the strict upper triangle is left untouched)."""

@@ -130,6 +130,60 @@ void run_tile(double* d, int sms, int wpb, int bps) {
          wpb, bps, fl / ms / 1e9);
 }
 
+
+// Mixed pipes: warps with (warp % 2 == 0) run DMMA, the others DFMA, in one
+// kernel; and an interleaved variant where every warp issues both. If the
+// DMMA and DFMA pipes were separate, the sum would exceed either alone.
+template <int CHAINS>
+__global__ void mixed_loop(double* out, int iters, int mode) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double a = 1.0 + lane * 1e-6, b = 1.0 - lane * 1e-6;
+  double c[CHAINS][2], f[CHAINS * 2];
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i) { c[i][0] = 0; c[i][1] = 0; f[2 * i] = lane; f[2 * i + 1] = i; }
+  const bool do_mma = mode == 2 || (warp & 1) == 0;
+  const bool do_fma = mode == 2 || (warp & 1) == 1;
+  for (int it = 0; it < iters; ++it) {
+    if (do_mma) {
+#pragma unroll
+      for (int i = 0; i < CHAINS; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+    if (do_fma) {
+#pragma unroll
+      for (int i = 0; i < 2 * CHAINS; ++i) f[i] = fma(f[i], a, b);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < CHAINS; ++i) s += c[i][0] + c[i][1] + f[2 * i] + f[2 * i + 1];
+  if (s == 12345.678) out[0] = s;
+}
+
+void run_mixed(double* d, int sms, int wpb, int bps, int mode) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 20000;
+  int blocks = sms * bps, threads = 32 * wpb;
+  mixed_loop<8><<<blocks, threads>>>(d, 10, mode);
+  cudaDeviceSynchronize();
+  cudaEventRecord(e0);
+  mixed_loop<8><<<blocks, threads>>>(d, iters, mode);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  // per warp per iteration: 8 DMMA (256 fma each = 512 flop) and/or 16 x 32 DFMA (2 flop)
+  double per_mma = 2.0 * 256 * 8, per_fma = 2.0 * 16 * 32;
+  double warps = (double)blocks * wpb, fl;
+  if (mode == 2) fl = warps * (per_mma + per_fma) * iters;
+  else fl = warps / 2 * (per_mma + per_fma) * iters;
+  printf("MIXED mode=%s warps/blk=%2d blk/SM=%d : %8.2f TFLOP/s (%.3f ms)\n", mode == 2 ? "interleaved" : "split-warps",
+         wpb, bps, fl / ms / 1e9, ms);
+}
+
 int main() {
   double* d;
   CK(cudaMalloc(&d, 64));
@@ -182,6 +236,7 @@ int main() {
       printf("DMMA16816 warps/blk=%2d blk/SM=%d : %8.2f TFLOP/s (%.3f ms)\n", wpb, bps, fl / ms / 1e9, ms);
     }
   }
+  for (int mode : {1, 2}) for (int wpb : {8, 16}) run_mixed(d, sms, wpb, 2, mode);
   run_tile<4, 4, false>(d, sms, 8, 2);
   run_tile<4, 4, true>(d, sms, 8, 2);
   run_tile<4, 4, false>(d, sms, 4, 2);
