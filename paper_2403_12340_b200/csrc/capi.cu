@@ -503,67 +503,119 @@ void trtri_lower(lrgw_ctx c, double* a, int n) {
 // lands in one device status block read once at the end — one host sync
 // instead of seven — and is evaluated in the order the steps run, so the
 // first failing step names the error as before.
-void smw_core(lrgw_ctx c, const double* t, const double* pvp, int n, double* k) {
+//
+// Split in two so the build can overlap the first factorisation (it needs T
+// only) with the Coulomb stage on a side stream: smw_factor_t enqueues
+// R = chol(-T) and its checks on `st`; smw_finish the rest on the context
+// stream (the caller orders the two).
+enum { SMW_INFO_T, SMW_TINY_T, SMW_INFO_M, SMW_TINY_M, SMW_TRTRI_BAD, SMW_NSTAT };
+
+struct SmwState {
+  DBuf stat, mxb, r, pwork;  // held until the side stream is joined
+  bool leaf_timed = false;
+  cudaStream_t pending = nullptr;  // side stream not yet joined (error paths drain it)
+  ~SmwState() {
+    if (pending) cudaStreamSynchronize(pending);
+  }
+};
+
+void smw_factor_t(lrgw_ctx c, cudaStream_t st, const double* t, int n, SmwState& s) {
   const size_t nn = (size_t)n * n;
-  enum { INFO_T, TINY_T, INFO_M, TINY_M, TRTRI_BAD, NSTAT };
-  DBuf stat = ialloc(c, NSTAT);
-  int* sd = stat.i();
-  ck(cudaMemsetAsync(sd, 0x7f, NSTAT * sizeof(int), c->stream), "memset");
-  DBuf mxb = dalloc(c, 2 * 512);
+  s.stat = ialloc(c, SMW_NSTAT);
+  s.mxb = dalloc(c, 2 * 512);
+  s.r = dalloc(c, nn);
+  int* sd = s.stat.i();
+  ck(cudaMemsetAsync(sd, 0x7f, SMW_NSTAT * sizeof(int), st), "memset");
   int lwork = 0;
-  cks(cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, n, const_cast<double*>(t), n, &lwork),
-      "potrf_bufferSize");
+  cks(cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, n, s.r.d(), n, &lwork), "potrf_bufferSize");
+  s.pwork = dalloc(c, (size_t)std::max(lwork, 1));
+  ck(max_abs(st, t, nn, s.mxb.d()), "max_abs");
+  ck(scale_copy(st, t, s.r.d(), nn, -1.0), "scale_copy");
+  if (st != c->stream) cks(cusolverDnSetStream(c->solver, st), "cusolverDnSetStream");
+  if (c->timing) ck(cudaEventRecord(c->ev_lib[0], st), "cudaEventRecord");
+  const cusolverStatus_t ps = cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, n, s.r.d(), n, s.pwork.d(), lwork,
+                                               sd + SMW_INFO_T);
+  if (c->timing) ck(cudaEventRecord(c->ev_lib[1], st), "cudaEventRecord");
+  if (st != c->stream) cks(cusolverDnSetStream(c->solver, c->stream), "cusolverDnSetStream");
+  cks(ps, "potrf");
+  s.leaf_timed = c->timing;
+  ck(tiny_pivot_dev(st, s.r.d(), n, n, s.mxb.d() + 296, sd + SMW_TINY_T), "tiny_pivot");
+  ck(zero_strict_upper(st, s.r.d(), n, n), "zero_upper");
+  if (st != c->stream) s.pending = st;
+}
+
+// The context stream waits for the side stream's factorisation.
+void smw_join(lrgw_ctx c, SmwState& s) {
+  if (!s.pending) return;
+  ck(cudaEventRecord(c->ev_join, s.pending), "cudaEventRecord");
+  ck(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "cudaStreamWaitEvent");
+  s.pending = nullptr;
+}
+
+void smw_finish(lrgw_ctx c, SmwState& s, const double* pvp, int n, double* k) {
+  const size_t nn = (size_t)n * n;
+  int* sd = s.stat.i();
+  double* r = s.r.d();
+  int lwork = 0;
+  cks(cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, n, r, n, &lwork), "potrf_bufferSize");
   DBuf pwork = dalloc(c, (size_t)std::max(lwork, 1));
-  float lib_ms = 0.0f;
-  auto potrf = [&](double* a, int* info, int ev0) {
-    if (c->timing) ck(cudaEventRecord(c->ev_lib[ev0], c->stream), "cudaEventRecord");
-    cks(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, n, a, n, pwork.d(), lwork, info), "potrf");
-    if (c->timing) ck(cudaEventRecord(c->ev_lib[ev0 + 1], c->stream), "cudaEventRecord");
-  };
-  ck(max_abs(c->stream, t, nn, mxb.d()), "max_abs");
-  DBuf r = dalloc(c, nn);
-  ck(scale_copy(c->stream, t, r.d(), nn, -1.0), "scale_copy");
-  potrf(r.d(), sd + INFO_T, 0);
-  ck(tiny_pivot_dev(c->stream, r.d(), n, n, mxb.d() + 296, sd + TINY_T), "tiny_pivot");
-  ck(zero_strict_upper(c->stream, r.d(), n, n), "zero_upper");
   Work w = make_work(c, 8 * nn);
   // Y = P R   (R lower: R(k, j) = 0 for k < j)
   DBuf y = dalloc(c, nn);
-  ck(dgemm(c->stream, n, n, n, pvp, n, Lay::MN, r.d(), n, Lay::K, y.d(), n, 1.0, 0.0, nullptr, false, c->sm_count,
+  ck(dgemm(c->stream, n, n, n, pvp, n, Lay::MN, r, n, Lay::K, y.d(), n, 1.0, 0.0, nullptr, false, c->sm_count,
            nullptr, 0, true, nullptr),
      "dgemm(PR)");
   // M = R^T Y + I/2 (lower tiles, mirrored)
   DBuf m = dalloc(c, nn);
-  gemm(c, n, n, n, r.d(), n, Lay::K, y.d(), n, Lay::K, m.d(), n, 1.0, 0.0, nullptr, true, &w);
+  gemm(c, n, n, n, r, n, Lay::K, y.d(), n, Lay::K, m.d(), n, 1.0, 0.0, nullptr, true, &w);
   ck(mirror_lower(c->stream, m.d(), n, n, false), "mirror");
   ck(add_diag(c->stream, m.d(), n, n, 0.5), "add_diag");
-  ck(max_abs(c->stream, m.d(), nn, mxb.d() + 512), "max_abs");
-  potrf(m.d(), sd + INFO_M, 2);
-  ck(tiny_pivot_dev(c->stream, m.d(), n, n, mxb.d() + 512 + 296, sd + TINY_M), "tiny_pivot");
+  ck(max_abs(c->stream, m.d(), nn, s.mxb.d() + 512), "max_abs");
+  if (c->timing) ck(cudaEventRecord(c->ev_lib[2], c->stream), "cudaEventRecord");
+  cks(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, n, m.d(), n, pwork.d(), lwork, sd + SMW_INFO_M), "potrf");
+  if (c->timing) ck(cudaEventRecord(c->ev_lib[3], c->stream), "cudaEventRecord");
+  ck(tiny_pivot_dev(c->stream, m.d(), n, n, s.mxb.d() + 512 + 296, sd + SMW_TINY_M), "tiny_pivot");
   ck(zero_strict_upper(c->stream, m.d(), n, n), "zero_upper");
   // Q^-1 (recursive DMMA trtri; a zero pivot -> TRTRI_BAD = its index + 1)
   {
     DBuf twork = dalloc(c, trtri_work_elems(n));
-    ck(lrgw_dev::trtri_lower(c->stream, m.d(), n, n, twork.d(), sd + TRTRI_BAD, c->sm_count), "trtri");
+    ck(lrgw_dev::trtri_lower(c->stream, m.d(), n, n, twork.d(), sd + SMW_TRTRI_BAD, c->sm_count), "trtri");
   }
   // Z = R Q^-T ; K = -Z Z^T (lower tiles, mirrored)
-  gemm(c, n, n, n, r.d(), n, Lay::MN, m.d(), n, Lay::MN, y.d(), n, 1.0, 0.0);
+  gemm(c, n, n, n, r, n, Lay::MN, m.d(), n, Lay::MN, y.d(), n, 1.0, 0.0);
   gemm(c, n, n, n, y.d(), n, Lay::MN, y.d(), n, Lay::MN, k, n, -1.0, 0.0, nullptr, true, &w);
   ck(mirror_lower(c->stream, k, n, n, false), "mirror");
-  int h[NSTAT];
+  int h[SMW_NSTAT];
   download(c, h, sd, sizeof(h));
   if (c->timing) {
     float ms = 0.0f;
-    for (int e = 0; e < 4; e += 2)
-      if (cudaEventElapsedTime(&ms, c->ev_lib[e], c->ev_lib[e + 1]) == cudaSuccess) lib_ms += ms;
-    c->lib_ms += lib_ms;
+    double lib = 0.0;
+    if (s.leaf_timed && cudaEventElapsedTime(&ms, c->ev_lib[0], c->ev_lib[1]) == cudaSuccess) lib += ms;
+    if (cudaEventElapsedTime(&ms, c->ev_lib[2], c->ev_lib[3]) == cudaSuccess) lib += ms;
+    c->lib_ms += lib;
   }
   const int unset = 0x7f7f7f7f;
-  if (h[INFO_T] != 0) fail(LRGW_ERR_NUMERIC, "assemble_K: T is not negative definite (gapless or rank-deficient input)");
-  if (h[TINY_T] >= 0) fail(LRGW_ERR_SINGULAR, "assemble_K: T singular", h[TINY_T]);
-  if (h[INFO_M] != 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", 0);
-  if (h[TINY_M] >= 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", h[TINY_M]);
-  if (h[TRTRI_BAD] != unset) fail(LRGW_ERR_SINGULAR, "trtri: singular factor", h[TRTRI_BAD] - 1);
+  if (h[SMW_INFO_T] != 0)
+    fail(LRGW_ERR_NUMERIC, "assemble_K: T is not negative definite (gapless or rank-deficient input)");
+  if (h[SMW_TINY_T] >= 0) fail(LRGW_ERR_SINGULAR, "assemble_K: T singular", h[SMW_TINY_T]);
+  if (h[SMW_INFO_M] != 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", 0);
+  if (h[SMW_TINY_M] >= 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", h[SMW_TINY_M]);
+  if (h[SMW_TRTRI_BAD] != unset) fail(LRGW_ERR_SINGULAR, "trtri: singular factor", h[SMW_TRTRI_BAD] - 1);
+}
+
+cudaStream_t side_stream(lrgw_ctx c) {
+  if (!c->side) {
+    ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "event");
+  }
+  return c->side;
+}
+
+void smw_core(lrgw_ctx c, const double* t, const double* pvp, int n, double* k) {
+  SmwState s;
+  smw_factor_t(c, c->stream, t, n, s);
+  smw_finish(c, s, pvp, n, k);
 }
 
 // ---------------------------------------------------------------------------
@@ -1051,6 +1103,12 @@ int lrgw_ctx_destroy(lrgw_ctx c) {
   for (auto& kv : c->plans) cufftDestroy(kv.second);
   for (auto& kv : c->plans_many) cufftDestroy(kv.second);
   if (c->solver) cusolverDnDestroy(c->solver);
+  if (c->side) {
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+    cudaEventDestroy(c->ev_side);
+    cudaEventDestroy(c->ev_join);
+  }
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   for (auto& x : c->ev)
     if (x) cudaEventDestroy(x);
@@ -1567,11 +1625,18 @@ lrgw_eps_s* build_one(lrgw_ctx c, const lrgw_build_params& P, const BuildSetup& 
     adaptive_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, spec, t.d());
   }
   mark(c, 5);
-  // stages 4-5
+  // stages 4-5: R = chol(-T) (a latency-bound leaf that needs T only) runs on
+  // the side stream under the Coulomb stage; smw_factor_t joins it back
   DBuf pvp = dalloc(c, (size_t)n_mu * n_mu), k = dalloc(c, (size_t)n_mu * n_mu);
+  SmwState smw;
+  cudaStream_t side = side_stream(c);
+  ck(cudaEventRecord(c->ev_side, c->stream), "cudaEventRecord");
+  ck(cudaStreamWaitEvent(side, c->ev_side, 0), "cudaStreamWaitEvent");
+  smw_factor_t(c, side, t.d(), n_mu, smw);
   pvp_impl(c, P.dims, P.cell, P.zero_kernel, theta.d(), n_r, n_mu, pvp.d());
   mark(c, 7);
-  smw_core(c, t.d(), pvp.d(), n_mu, k.d());
+  smw_join(c, smw);
+  smw_finish(c, smw, pvp.d(), n_mu, k.d());
   mark(c, 8);
   timing_end(c);
   auto* e = new_eps(c);

@@ -52,6 +52,8 @@ struct lrgw_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
+  cudaStream_t side = nullptr;  // the build's side stream (chol(-T) under the Coulomb stage)
+  cudaEvent_t ev_side = nullptr, ev_join = nullptr;
   int sm_count = 148;
   cusolverDnHandle_t solver = nullptr;
   std::map<std::tuple<int, int, int, int, long long, long long, int>, cufftHandle> plans;
