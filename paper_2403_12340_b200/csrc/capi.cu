@@ -636,6 +636,36 @@ bool select_trace() {
 }
 
 
+// Opt-in (LRGW_SELECT_DEVLOOP=1): measured no faster than the host loop —
+// Si64 select 10.28 vs 10.12 ms, C60 42.5 vs 41.7 ms (profiles/r02/
+// sweep_devloop.txt): the per-block read-back of nb costs less than the
+// device loop's speculative last block and split-K W[C, C] update.
+bool select_device_loop_enabled() {
+  static const bool on = getenv("LRGW_SELECT_DEVLOOP") && atoi(getenv("LRGW_SELECT_DEVLOOP")) == 1;
+  return on;
+}
+
+// The device loop's pinned read-back slots and event ring live in the context
+// (cudaHostAlloc / cudaFreeHost synchronise the device: never per call).
+int* select_pinned(lrgw_ctx c, size_t n) {
+  if (c->sel_pinned_n < n) {
+    if (c->sel_pinned) cudaFreeHost(c->sel_pinned);
+    c->sel_pinned = nullptr;
+    c->sel_pinned_n = 0;
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&c->sel_pinned), n * sizeof(int), cudaHostAllocDefault),
+       "cudaHostAlloc");
+    c->sel_pinned_n = n;
+  }
+  return c->sel_pinned;
+}
+
+cudaEvent_t select_event(lrgw_ctx c, int j) {
+  constexpr int R = sizeof(c->sel_ev) / sizeof(c->sel_ev[0]);
+  cudaEvent_t& e = c->sel_ev[j % R];
+  if (!e) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+  return e;
+}
+
 std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int n1, const double* b,
                                  long long ldb, int n2, int n_r, int n_mu, double* min_margin,
                                  SelectKeep* keep) {
@@ -668,6 +698,66 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
   ck(select_init(c->stream, a, lda, n1, b, ldb, n2, n_r, d.d(), pos.i(), perm.i()), "select_init");
   ck(select_topk_reset(c->stream, tmp.p), "select_topk_reset");
   int k = 0;
+  // Device-driven block loop (the fused-panel path, where the per-block host
+  // round trip is a visible share of the stage): every kernel of block j reads
+  // the pivots-so-far k from kb2[j & 1] and the accepted count from bout[0];
+  // the greedy writes k + nb to kb2[(j + 1) & 1]. The host never waits on the
+  // block it just enqueued: it reads k back (pinned, two blocks behind) only
+  // to decide when to stop; blocks enqueued past the end find k >= steps and
+  // do nothing.
+  const int cap = select_accept_cap(s, n_r);
+  const bool dev_loop = select_device_loop_enabled() && fused_downdate_enabled() && select_panel_enabled(n1, n2) &&
+                        (long long)n_r >= (long long)steps + s + 1 && n_r % 2 == 0 && lda % 2 == 0 &&
+                        ldb % 2 == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0 &&
+                        (reinterpret_cast<uintptr_t>(b) & 15) == 0 && cap > 16 && s % 2 == 0;
+  if (dev_loop) {
+    DBuf kb2 = ialloc(c, 2), wpart = dalloc(c, select_wcc_work_elems());
+    ck(cudaMemsetAsync(kb2.p, 0, 2 * sizeof(int), c->stream), "memset");
+    int* hk = select_pinned(c, (size_t)steps + 8);
+    int j = 0, known = 0;
+    while (known < steps) {
+      int* kin = kb2.i() + (j & 1);
+      int* kout = kb2.i() + ((j + 1) & 1);
+      ck(select_topk(c->stream, d.d(), pos.i(), n_r, 0, s + 1, tmp.p, top.p, kin), "select_topk");
+      ck(select_cand_rows(c->stream, top.p, s, cand.i()), "cand_rows");
+      ck(gather_rows3(c->stream, a, lda, n1, b, ldb, n2, L.d(), n_r, 0, cand.i(), s, amu.d(), bmu.d(), lrow.d(), lds,
+                      kin),
+         "gather");
+      ck(hadamard_gemm(c->stream, s, s, amu.d(), lds, amu.d(), lds, n1, bmu.d(), lds, bmu.d(), lds, n2, wcc.d(), s,
+                       1.0, 0.0),
+         "hadamard_gemm(W_CC)");
+      ck(select_wcc_lsub(c->stream, lrow.d(), lds, s, kin, wcc.d(), wpart.d()), "wcc_lsub");
+      ck(select_cand_greedy(c->stream, n_r, s, steps, 0, top.p, wcc.d(), pos.i(), perm.i(), xcol.d(), order.i(),
+                            min_margin ? margin.d() : nullptr, bout, cap, select_accept_round(), kin, kout),
+         "cand_greedy");
+      ck(gather_rows3(c->stream, a, lda, n1, b, ldb, n2, L.d(), n_r, 0, order.i(), 0, amu.d(), bmu.d(), lrow.d(), lds,
+                      kin, bout, kin),
+         "gather");
+      ck(select_panel(c->stream, n_r, cap, a, lda, amu.d(), lds, n1, b, ldb, bmu.d(), lds, n2, L.d(), n_r, lrow.d(),
+                      lds, 0, xcol.d(), s, L.d(), n_r, d.d(), pos.i(), 0, kin, bout),
+         "select_panel");
+      ck(cudaMemcpyAsync(hk + j, kout, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+      ck(cudaEventRecord(select_event(c, j), c->stream), "cudaEventRecord");
+      ++j;
+      if (j >= 2) {
+        ck(cudaEventSynchronize(select_event(c, j - 2)), "cudaEventSynchronize");
+        const int prev = j >= 3 ? hk[j - 3] : 0;
+        known = hk[j - 2];
+        if (known <= prev && known < steps) fail(LRGW_ERR_INTERNAL, "select: no progress (non-finite residuals?)");
+      }
+      if (j > steps + 4) fail(LRGW_ERR_INTERNAL, "select: block loop did not terminate");
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    int prev = 0;
+    for (int q = 0; q < j; ++q) {
+      if (hk[q] > prev) {
+        if (select_trace()) fprintf(stderr, "select block k=%d se=%d b=%d (device loop)\n", prev, s, hk[q] - prev);
+        if (keep) ++keep->blocks;
+        prev = hk[q];
+      }
+    }
+    k = steps;
+  }
   while (k < steps) {
     const int se = std::min(s, n_r - k);
     // Candidate set C (top s by residual, position) and its Schur block
@@ -1103,6 +1193,9 @@ int lrgw_ctx_destroy(lrgw_ctx c) {
   for (auto& kv : c->plans) cufftDestroy(kv.second);
   for (auto& kv : c->plans_many) cufftDestroy(kv.second);
   if (c->solver) cusolverDnDestroy(c->solver);
+  if (c->sel_pinned) cudaFreeHost(c->sel_pinned);
+  for (auto e : c->sel_ev)
+    if (e) cudaEventDestroy(e);
   if (c->side) {
     cudaStreamSynchronize(c->side);
     cudaStreamDestroy(c->side);

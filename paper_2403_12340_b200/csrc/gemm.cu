@@ -235,7 +235,11 @@ __global__ void gather_rows_kernel(const double* src, long long lds, int cols, c
 // sources (a: n1 cols, b: n2 cols, l: nl cols) into three destinations of leading dim ldd.
 __global__ void gather_rows3_kernel(const double* a, long long lda, int n1, const double* b, long long ldb, int n2,
                                     const double* l, long long ldl, int nl, const int* rows, int n_rows, double* da,
-                                    double* db, double* dl, long long ldd) {
+                                    double* db, double* dl, long long ldd, const int* nl_dev, const int* nrows_dev,
+                                    const int* row_off_dev) {
+  if (nl_dev) nl = *nl_dev;
+  if (nrows_dev) n_rows = *nrows_dev;
+  if (row_off_dev) rows += *row_off_dev;
   const long long total = (long long)n_rows * (n1 + n2 + nl);
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -371,9 +375,11 @@ cudaError_t dispatch2(cudaStream_t st, const Dgemm2Params& p, bool had) {
 
 cudaError_t gather_rows3(cudaStream_t st, const double* a, long long lda, int n1, const double* b, long long ldb,
                         int n2, const double* l, long long ldl, int nl, const int* rows, int n_rows, double* da,
-                        double* db, double* dl, long long ldd) {
-  if (n_rows <= 0 || n1 + n2 + nl <= 0) return cudaSuccess;
-  gather_rows3_kernel<<<592, 256, 0, st>>>(a, lda, n1, b, ldb, n2, l, ldl, nl, rows, n_rows, da, db, dl, ldd);
+                        double* db, double* dl, long long ldd, const int* nl_dev, const int* nrows_dev,
+                        const int* row_off_dev) {
+  if ((n_rows <= 0 && !nrows_dev) || (n1 + n2 + nl <= 0 && !nl_dev)) return cudaSuccess;
+  gather_rows3_kernel<<<592, 256, 0, st>>>(a, lda, n1, b, ldb, n2, l, ldl, nl, rows, n_rows, da, db, dl, ldd, nl_dev,
+                                           nrows_dev, row_off_dev);
   count_launches(1);
   return cudaGetLastError();
 }

@@ -54,6 +54,9 @@ struct lrgw_ctx_s {
   cudaStream_t own_stream = nullptr;
   cudaStream_t side = nullptr;  // the build's side stream (chol(-T) under the Coulomb stage)
   cudaEvent_t ev_side = nullptr, ev_join = nullptr;
+  int* sel_pinned = nullptr;  // the selection's device-loop read-back slots (pinned)
+  size_t sel_pinned_n = 0;
+  cudaEvent_t sel_ev[4] = {};
   int sm_count = 148;
   cusolverDnHandle_t solver = nullptr;
   std::map<std::tuple<int, int, int, int, long long, long long, int>, cufftHandle> plans;

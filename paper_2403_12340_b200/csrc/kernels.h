@@ -63,11 +63,14 @@ cudaError_t dgemm_tall_downdate(cudaStream_t st, int M, int N, int K, const doub
 // d[m] -= sum_n C(m, n)^2 where pos[m] >= kend. cudaErrorNotSupported when the
 // shape / alignment is not covered (callers run the three-launch path).
 bool select_panel_enabled(int n1, int n2);
+// Device-driven form (k_dev != nullptr): k = *k_dev, N = *n_dev (<= the N
+// given, which sizes the tile), c is the factor's column 0 (the block writes
+// columns k .. k + N) and kend = k + N.
 cudaError_t select_panel(cudaStream_t st, int M, int N, const double* a1, long long lda1, const double* b1,
                          long long ldb1, int k1, const double* a2, long long lda2, const double* b2, long long ldb2,
                          int k2, const double* l, long long ldl, const double* lrow, long long ldlr, int k,
                          const double* x, long long ldx, double* c, long long ldc, double* d, const int* pos,
-                         int kend);
+                         int kend, const int* k_dev = nullptr, const int* n_dev = nullptr);
 
 // a(j,i) = a(i,j) for i > j (average = 0) or both = (a(i,j) + a(j,i))/2.
 cudaError_t mirror_lower(cudaStream_t st, double* a, int n, long long lda, bool average);
@@ -77,9 +80,11 @@ cudaError_t gather_rows(cudaStream_t st, const double* src, long long lds, int c
                         int n_rows, double* dst, long long ldd);
 
 // rows `rows` of a (n1 cols), b (n2 cols) and l (nl cols) into da, db, dl (ld ldd), one launch.
+// Device-side counts (optional): nl = *nl_dev, n_rows = *nrows_dev, rows += *row_off_dev.
 cudaError_t gather_rows3(cudaStream_t st, const double* a, long long lda, int n1, const double* b, long long ldb,
                          int n2, const double* l, long long ldl, int nl, const int* rows, int n_rows, double* da,
-                         double* db, double* dl, long long ldd);
+                         double* db, double* dl, long long ldd, const int* nl_dev = nullptr,
+                         const int* nrows_dev = nullptr, const int* row_off_dev = nullptr);
 
 // dst(:, c) = src(:, cols[c]), cols on device.
 cudaError_t gather_cols(cudaStream_t st, const double* src, long long lds, int rows, const int* cols, int n,

@@ -21,6 +21,7 @@
 //            fragment reads pick up the matching k.
 // CTAs are 64 x 16Q (4 warps of 16 rows x all columns), so every row's sum
 // of squares is complete inside one warp and the downdate needs no atomics.
+#include <algorithm>
 #include <cstdlib>
 
 #include "gemm2.cuh"
@@ -52,6 +53,8 @@ struct PanelParams {
   double* d;
   const int* pos;
   int kend;
+  const int* kdev;  // device-driven loop: k, N from the device (see select_panel)
+  const int* ndev;
 };
 
 template <int Q, int STAGES_, int MINB_>
@@ -86,13 +89,12 @@ __device__ __forceinline__ void load_x_tile(double* s, const double* g, long lon
 }
 
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) panel_kernel(PanelParams p) {
-  extern __shared__ __align__(16) double smem[];
+__device__ __forceinline__ void panel_body(const PanelParams& p, double* smem, const int N, const int K3,
+                                           const int kend, double* cout) {
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
   constexpr int FM = Cfg::FM, FN = Cfg::FN, PA = Cfg::PA, PB = Cfg::PB, T = Cfg::THREADS;
   const int m0 = blockIdx.x * BM;
-  const int N = p.N;
-  const int kt1 = (p.K1 + BK - 1) / BK, kt2 = (p.K2 + BK - 1) / BK, kt3 = (p.K3 + BK - 1) / BK;
+  const int kt1 = (p.K1 + BK - 1) / BK, kt2 = (p.K2 + BK - 1) / BK, kt3 = (K3 + BK - 1) / BK;
   const int e1 = kt1, e2 = e1 + kt2, e3 = e2 + kt3, nkt = e3 + (N + BK - 1) / BK;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -116,8 +118,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) panel_kernel(PanelPar
       load_mn_tile<BM, BK, PA, 2, T>(sa, p.A2, p.lda2, m0, p.M, (kt - e1) * BK, p.K2, tid);
       load_mn_tile<BN, BK, PB, 2, T>(sb, p.B2, p.ldb2, 0, N, (kt - e1) * BK, p.K2, tid);
     } else if (kt < e3) {
-      load_mn_tile<BM, BK, PA, 2, T>(sa, p.A3, p.lda3, m0, p.M, (kt - e2) * BK, p.K3, tid);
-      load_mn_tile<BN, BK, PB, 2, T>(sb, p.B3, p.ldb3, 0, N, (kt - e2) * BK, p.K3, tid);
+      load_mn_tile<BM, BK, PA, 2, T>(sa, p.A3, p.lda3, m0, p.M, (kt - e2) * BK, K3, tid);
+      load_mn_tile<BN, BK, PB, 2, T>(sb, p.B3, p.ldb3, 0, N, (kt - e2) * BK, K3, tid);
     } else {
       load_x_tile<BN, PB, T>(sb, p.X, p.ldx, N, (kt - e3) * BK, N, tid);
     }
@@ -216,7 +218,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) panel_kernel(PanelPar
         const double v0 = acc[2 * j][jn][h], v1 = acc[2 * j + 1][jn][h];
         sq0 = fma(v0, v0, sq0);
         sq1 = fma(v1, v1, sq1);
-        double* c = p.C + m + (long long)n * p.ldc;
+        double* c = cout + m + (long long)n * p.ldc;
         if (m + 1 < p.M) {
           *reinterpret_cast<double2*>(c) = make_double2(v0, v1);
         } else if (m < p.M) {
@@ -228,20 +230,76 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) panel_kernel(PanelPar
     sq0 += __shfl_xor_sync(0xffffffffu, sq0, 2);
     sq1 += __shfl_xor_sync(0xffffffffu, sq1, 2);
     if (t == 0) {
-      if (m < p.M && p.pos[m] >= p.kend) p.d[m] -= sq0;
-      if (m + 1 < p.M && p.pos[m + 1] >= p.kend) p.d[m + 1] -= sq1;
+      if (m < p.M && p.pos[m] >= kend) p.d[m] -= sq0;
+      if (m + 1 < p.M && p.pos[m + 1] >= kend) p.d[m + 1] -= sq1;
     }
   }
 }
 
-template <class Cfg>
-cudaError_t launch_panel(cudaStream_t st, const PanelParams& p) {
-  const int grid = (p.M + Cfg::BM - 1) / Cfg::BM;
+// The tile configuration of width 16 Q.
+template <int Q>
+struct PanelQ;
+template <> struct PanelQ<2> { using C = PanelCfg<2, 3, 2>; };
+template <> struct PanelQ<3> { using C = PanelCfg<3, 3, 2>; };
+template <> struct PanelQ<4> { using C = PanelCfg<4, 3, 2>; };
+template <> struct PanelQ<5> { using C = PanelCfg<5, 2, 2>; };
+template <> struct PanelQ<6> { using C = PanelCfg<6, 2, 2>; };
+template <> struct PanelQ<7> { using C = PanelCfg<7, 2, 2>; };
+template <> struct PanelQ<8> { using C = PanelCfg<8, 3, 1>; };
+
+// Width 16 ceil(N / 16) for a block whose N is known on the device only
+// (QMAX from the accept cap), else width 16 QMAX.
+template <int Q, bool DISPATCH>
+__device__ __forceinline__ void panel_pick(const PanelParams& p, double* smem, int N, int K3, int kend,
+                                           double* cout) {
+  if constexpr (DISPATCH && Q > 2) {
+    if (N <= 16 * (Q - 1)) {
+      panel_pick<Q - 1, true>(p, smem, N, K3, kend, cout);
+      return;
+    }
+  }
+  panel_body<typename PanelQ<Q>::C>(p, smem, N, K3, kend, cout);
+}
+
+template <int Q>
+constexpr int panel_smem_max() {
+  if constexpr (Q <= 2)
+    return PanelQ<2>::C::SMEM_BYTES;
+  else
+    return PanelQ<Q>::C::SMEM_BYTES > panel_smem_max<Q - 1>() ? PanelQ<Q>::C::SMEM_BYTES : panel_smem_max<Q - 1>();
+}
+
+// resident CTAs per SM the register budget is sized for (PanelQ<Q>::C::MINB)
+template <int Q>
+constexpr int panel_minb() {
+  return Q >= 8 ? 1 : 2;
+}
+
+template <int Q, bool DISPATCH>
+__global__ void __launch_bounds__(128, panel_minb<Q>()) panel_kernel(PanelParams p) {
+  static_assert(PanelQ<Q>::C::MINB == panel_minb<Q>(), "register budget");
+  extern __shared__ __align__(16) double smem[];
+  int N = p.N, K3 = p.K3, kend = p.kend;
+  double* cout = p.C;
+  if (p.kdev) {
+    K3 = *p.kdev;
+    N = min(N, *p.ndev);
+    kend = K3 + N;
+    cout += (long long)K3 * p.ldc;
+  }
+  if (N <= 0) return;
+  panel_pick<Q, DISPATCH>(p, smem, N, K3, kend, cout);
+}
+
+template <int Q>
+cudaError_t launch_panel(cudaStream_t st, const PanelParams& p, bool dispatch) {
+  const int grid = (p.M + 63) / 64;
   if (grid == 0) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(panel_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       Cfg::SMEM_BYTES);
+  const int smem = dispatch ? panel_smem_max<Q>() : PanelQ<Q>::C::SMEM_BYTES;
+  auto kern = dispatch ? panel_kernel<Q, true> : panel_kernel<Q, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  panel_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(p);
+  kern<<<grid, 128, smem, st>>>(p);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -265,13 +323,14 @@ cudaError_t select_panel(cudaStream_t st, int M, int N, const double* a1, long l
                          long long ldb1, int k1, const double* a2, long long lda2, const double* b2, long long ldb2,
                          int k2, const double* l, long long ldl, const double* lrow, long long ldlr, int k,
                          const double* x, long long ldx, double* c, long long ldc, double* d, const int* pos,
-                         int kend) {
+                         int kend, const int* k_dev, const int* n_dev) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (N < 17 || N > 128 || k1 < 1 || k2 < 1 || k < 0) return cudaErrorNotSupported;
   const bool vec = aligned16p(a1) && aligned16p(b1) && aligned16p(a2) && aligned16p(b2) && aligned16p(x) &&
                    aligned16p(c) && (k == 0 || (aligned16p(l) && aligned16p(lrow))) && lda1 % 2 == 0 &&
                    ldb1 % 2 == 0 && lda2 % 2 == 0 && ldb2 % 2 == 0 && ldx % 2 == 0 && ldc % 2 == 0 &&
-                   (k == 0 || (ldl % 2 == 0 && ldlr % 2 == 0)) && (M % 2 == 0 || (lda1 > M && lda2 > M && ldl > M));
+                   ((k == 0 && !k_dev) || (ldl % 2 == 0 && ldlr % 2 == 0)) &&
+                   (M % 2 == 0 || (lda1 > M && lda2 > M && ldl > M));
   if (!vec) return cudaErrorNotSupported;
   PanelParams p{};
   p.M = M, p.N = N, p.K1 = k1, p.K2 = k2, p.K3 = k;
@@ -279,14 +338,16 @@ cudaError_t select_panel(cudaStream_t st, int M, int N, const double* a1, long l
   p.A2 = a2, p.lda2 = lda2, p.B2 = b2, p.ldb2 = ldb2;
   p.A3 = l, p.lda3 = ldl, p.B3 = lrow, p.ldb3 = ldlr;
   p.X = x, p.ldx = ldx, p.C = c, p.ldc = ldc, p.d = d, p.pos = pos, p.kend = kend;
+  p.kdev = k_dev, p.ndev = n_dev;
+  const bool dispatch = k_dev != nullptr;  // the block's width is known on the device only
   switch ((N + 15) / 16) {
-    case 2: return launch_panel<PanelCfg<2, 3, 2>>(st, p);
-    case 3: return launch_panel<PanelCfg<3, 3, 2>>(st, p);
-    case 4: return launch_panel<PanelCfg<4, 3, 2>>(st, p);
-    case 5: return launch_panel<PanelCfg<5, 2, 2>>(st, p);
-    case 6: return launch_panel<PanelCfg<6, 2, 2>>(st, p);
-    case 7: return launch_panel<PanelCfg<7, 2, 2>>(st, p);
-    default: return launch_panel<PanelCfg<8, 3, 1>>(st, p);
+    case 2: return launch_panel<2>(st, p, dispatch);
+    case 3: return launch_panel<3>(st, p, dispatch);
+    case 4: return launch_panel<4>(st, p, dispatch);
+    case 5: return launch_panel<5>(st, p, dispatch);
+    case 6: return launch_panel<6>(st, p, dispatch);
+    case 7: return launch_panel<7>(st, p, dispatch);
+    default: return launch_panel<8>(st, p, dispatch);
   }
 }
 

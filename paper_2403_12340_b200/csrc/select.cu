@@ -313,6 +313,10 @@ struct CandParams {
   int* piv_order;       // [steps]
   double* margin;       // [steps] or nullptr
   int* b_out;           // number of accepted steps
+  // device-driven block loop (all optional): the block start is read from
+  // *kb_dev, the next block start kb + b written to *k_next
+  const int* kb_dev;
+  int* k_next;
 };
 
 __device__ __forceinline__ double pick8(const double (&x)[CG_ROWS], int r) {
@@ -458,6 +462,7 @@ __device__ void cand_tri_inverse(double* lcs, double* lsel, const int* sel, int 
 __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p) {
   extern __shared__ __align__(16) double sm[];
   const int s = p.s, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int kb = p.kb_dev ? *p.kb_dev : p.kb;
   const bool ctl = wid == 0;
   double* rowbuf = sm;                              // 2 x 128: published pivot rows
   double* lcs = rowbuf + 2 * CG_MAX;                // [t][j]: l of candidate j at step t; later X
@@ -476,7 +481,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
 
   const double tau = p.top[s].row >= 0 ? p.top[s].v : -DBL_MAX;
   __shared__ int tmax_s;  // read from smem on the controller's path (keeps it out of the register budget)
-  if (threadIdx.x == 0) tmax_s = min(min(s, p.bmax), p.steps - p.kb);
+  if (threadIdx.x == 0) tmax_s = min(min(s, p.bmax), p.steps - kb);
   const bool want_sv = p.margin != nullptr;
 
   // controller state (warp 0), entries j = lane + 32 c
@@ -493,7 +498,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
       dj[c] = e.row >= 0 ? e.v : -DBL_MAX;
       pj[c] = e.row >= 0 ? e.pos : INT_MAX;
       rjs[j] = e.row;
-      pss[j] = (j < s && p.kb + j < p.n_r) ? p.perm[p.kb + j] : -1;
+      pss[j] = (j < s && kb + j < p.n_r) ? p.perm[kb + j] : -1;
       usedl |= (e.row < 0 ? 1u : 0u) << c;
       const unsigned m = __ballot_sync(0xffffffffu, e.row < 0);
       if (lane == 0) usedsh[c] = m;
@@ -502,7 +507,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
     int i0;
     cand_argmax(dj, pj, usedl, lane, want_sv, v0, ppos, i0, sv);
     // the first step of a block is the exact argmax (C is sorted by the pivot rule)
-    if (lane == 0) piv[0] = CandPivot{v0, v0 > 0.0 ? 1.0 / v0 : 0.0, i0, (0 < min(s, p.steps - p.kb) && i0 >= 0) ? 1 : 0};
+    if (lane == 0) piv[0] = CandPivot{v0, v0 > 0.0 ? 1.0 / v0 : 0.0, i0, (0 < min(s, p.steps - kb) && i0 >= 0) ? 1 : 0};
   }
 
   const int base = CG_ROWS * wid;
@@ -537,7 +542,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
     __syncthreads();
     if (ctl) {
       // ---- critical path: downdate d, pick and publish the next pivot ----
-      const int k = p.kb + t;
+      const int k = kb + t;
       const int occ = pss[t];  // perm[k] before the swap
       const int piv_pos = ppos;
 #pragma unroll
@@ -563,7 +568,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
         rec_pp[t] = piv_pos;
         sel[t] = i0;
         // position slots: perm[ppos] = occ, then perm[k] = gp
-        if (piv_pos - p.kb < CG_MAX) pss[piv_pos - p.kb] = occ;
+        if (piv_pos - kb < CG_MAX) pss[piv_pos - kb] = occ;
         pss[t] = gp;
         usedsh[i0 >> 5] |= 1u << (i0 & 31);  // only bit i0 changes: workers exclude it already
         rec_mg[t] = pv.v0 > 0.0 ? (pv.v0 - fmax(svp, tau)) / pv.v0 : 0.0;
@@ -609,7 +614,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
   const int b = (t < tmax_s && p.bround > 0 && t >= p.bround) ? p.bround : t;
   if (threadIdx.x == 0) {
     for (int q = 0; q < b; ++q) {  // the swaps in step order
-      const int k = p.kb + q, gp = rec_gp[q], occ = rec_occ[q], pp = rec_pp[q];
+      const int k = kb + q, gp = rec_gp[q], occ = rec_occ[q], pp = rec_pp[q];
       p.perm[k] = gp;
       p.perm[pp] = occ;
       p.pos[gp] = k;
@@ -621,7 +626,8 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
   cand_tri_inverse(lcs, lsel, sel, b, s, p.xcol);
   if (threadIdx.x == 0) {
     p.b_out[0] = b;
-    p.b_out[1] = p.kb + b;  // next block start, consumed on the device
+    p.b_out[1] = kb + b;  // next block start, consumed on the device
+    if (p.k_next) *p.k_next = kb + b;
   }
 }
 
@@ -702,13 +708,64 @@ int select_accept_round() {
 
 cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* wcc,
                                int* pos, int* perm, double* xcol, int* piv_order, double* margin, int* b_out,
-                               int bmax, int bround) {
+                               int bmax, int bround, const int* kb_dev, int* k_next) {
   const Ent* tp = static_cast<const Ent*>(top);
-  CandParams p{n_r, s, steps, kb, std::max(1, bmax), bround, tp, wcc, pos, perm, xcol, piv_order, margin, b_out};
+  CandParams p{n_r,  s,    steps, kb,        std::max(1, bmax), bround, tp,     wcc,
+               pos,  perm, xcol,  piv_order, margin,            b_out,  kb_dev, k_next};
   const size_t smem = select_cand_smem_bytes(s);
   cudaError_t e = cudaFuncSetAttribute(cand_greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cand_greedy_kernel<<<1, CG_THREADS, smem, st>>>(p); count_launches(1);
+  return cudaGetLastError();
+}
+
+// W[C, C] -= Lr Lr^T over the k = *k_dev pivots so far (Lr: s x k, ld ldl):
+// WCC_SPLITS k-chunks into partials, then one fixed-order reduction (the same
+// sum for every run: the greedy's pivots must not depend on scheduling).
+constexpr int WCC_SPLITS = 16;
+__global__ void __launch_bounds__(256) wcc_lsub_partial_kernel(const double* lr, long long ldl, int s, const int* k_dev,
+                                                               double* part) {
+  const int k = *k_dev;
+  const int ch = ((k + WCC_SPLITS - 1) / WCC_SPLITS + 7) / 8 * 8;
+  const int k0 = blockIdx.y * ch, k1 = min(k, k0 + ch);
+  const int ti = blockIdx.x % 4, tj = blockIdx.x / 4;  // 32 x 32 tile of the 128 x 128 block
+  const int i = 32 * ti + 2 * (threadIdx.x % 16), j = 32 * tj + 2 * (threadIdx.x / 16);
+  double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
+  if (i < s && j < s) {
+    for (int kk = k0; kk < k1; ++kk) {
+      const double* col = lr + (long long)kk * ldl;
+      const double x0 = col[i], x1 = i + 1 < s ? col[i + 1] : 0.0;
+      const double y0 = col[j], y1 = j + 1 < s ? col[j + 1] : 0.0;
+      a00 = fma(x0, y0, a00);
+      a01 = fma(x0, y1, a01);
+      a10 = fma(x1, y0, a10);
+      a11 = fma(x1, y1, a11);
+    }
+  }
+  double* out = part + (size_t)blockIdx.y * CG_MAX * CG_MAX;
+  out[i + j * CG_MAX] = a00;
+  out[i + 1 + j * CG_MAX] = a10;
+  out[i + (j + 1) * CG_MAX] = a01;
+  out[i + 1 + (j + 1) * CG_MAX] = a11;
+}
+
+__global__ void wcc_lsub_reduce_kernel(double* wcc, int s, const double* part) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < s * s; idx += gridDim.x * blockDim.x) {
+    const int i = idx % s, j = idx / s;
+    double acc = 0.0;
+    for (int q = 0; q < WCC_SPLITS; ++q) acc += part[(size_t)q * CG_MAX * CG_MAX + i + j * CG_MAX];
+    wcc[i + (size_t)j * s] -= acc;
+  }
+}
+
+size_t select_wcc_work_elems() { return (size_t)WCC_SPLITS * CG_MAX * CG_MAX; }
+
+cudaError_t select_wcc_lsub(cudaStream_t st, const double* lr, long long ldl, int s, const int* k_dev, double* wcc,
+                            double* work) {
+  if (s > CG_MAX) return cudaErrorInvalidValue;
+  wcc_lsub_partial_kernel<<<dim3(16, WCC_SPLITS), 256, 0, st>>>(lr, ldl, s, k_dev, work);
+  wcc_lsub_reduce_kernel<<<64, 256, 0, st>>>(wcc, s, work);
+  count_launches(2);
   return cudaGetLastError();
 }
 

@@ -348,3 +348,47 @@ def test_selection_pivots_with_and_without_fused_downdate(tmp_path, n_r):
     q = np.linalg.qr(rng.standard_normal((n_r, 28)))[0]
     want = R.select_points(q[:, :14], q[:, 14:], 96)
     assert np.array_equal(out["1"], want) and np.array_equal(out["0"], want)
+
+
+_ENGINE_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2403_12340_b200 import lrgw
+n_r = int(sys.argv[2])
+rng = np.random.default_rng(31)
+q = np.linalg.qr(rng.standard_normal((n_r, 48)))[0]
+a, b = np.asfortranarray(q[:, :24]), np.asfortranarray(q[:, 24:])
+pts = lrgw.select_interpolation_points(a, b, 300, ctx=lrgw.Context(0))
+np.save(sys.argv[3], pts)
+"""
+
+
+@pytest.mark.parametrize("variant", ["", "LRGW_SELECT_DEVLOOP=1", "LRGW_PANEL=0", "LRGW_PANEL=0 LRGW_TMA_TALL=0"])
+def test_selection_engines_agree_with_oracle(tmp_path, variant):
+    """Every selection block engine gives the oracle's pivots (linalg.hpp:26-111)
+    on a shape with several candidate blocks that reaches the tall-skinny
+    engines (n_r = 20000): the fused panel with the host block loop (default
+    at this Hadamard depth), the device-driven block loop, the three TMA
+    launches and the three cp.async launches."""
+    import os
+    import subprocess
+    import sys
+
+    from oracle import restate as R
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "sel.py"
+    script.write_text(_ENGINE_SCRIPT)
+    env = dict(os.environ)
+    for kv in variant.split():
+        k, v = kv.split("=")
+        env[k] = v
+    path = tmp_path / "pts.npy"
+    r = subprocess.run([sys.executable, str(script), root, "20000", str(path)], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    rng = np.random.default_rng(31)
+    q = np.linalg.qr(rng.standard_normal((20000, 48)))[0]
+    want = R.select_points(q[:, :24], q[:, 24:], 300)
+    assert np.array_equal(np.load(path), want)
