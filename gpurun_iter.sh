@@ -1,4 +1,2 @@
-mkdir -p gpurun_out
-( SWEEP_REPS=3 timeout 900 python tools/env_sweep.py si64 '' 'LRGW_SELECT_DEVLOOP=0'
-  SWEEP_REPS=2 timeout 900 python tools/env_sweep.py c60 '' 'LRGW_SELECT_DEVLOOP=0' ) > gpurun_out/sweep_devloop.txt 2>&1
-grep -v Warn gpurun_out/sweep_devloop.txt
+timeout 600 ncu --set full --import-source on -k regex:fft_ -c 2 -o gpurun_out/ncu_fft python tools/trace_build.py si64 2 > gpurun_out/ncu_fft.log 2>&1
+tail -2 gpurun_out/ncu_fft.log

@@ -203,6 +203,14 @@ int fft_batch() {
 
 void fft_forward(lrgw_ctx c, const int* dims, const double* x, long long ldx, int m, double* xhat) {
   const long long nh = half_len(dims);
+  if (fft_own_enabled()) {  // the two-pass shared-memory D2Z (fft.cu) where the axes allow it
+    const cudaError_t e = fft_d2z_3d(c->stream, dims, x, ldx, m, xhat, c->sm_count);
+    if (e != cudaErrorNotSupported) {
+      ck(e, "fft_d2z_3d");
+      return;
+    }
+    cudaGetLastError();
+  }
   const int fb = fft_batch();
   for (int j0 = 0; j0 < m; j0 += fb) {
     const int b = std::min(fb, m - j0);

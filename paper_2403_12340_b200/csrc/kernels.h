@@ -106,6 +106,13 @@ cudaError_t quad_nodes(cudaStream_t st, int n_mu, int n_v, int n_c, const double
                        double* running, double beta, double pref, double* t, long long ldt,
                        cudaEvent_t k_begin = nullptr, cudaEvent_t k_end = nullptr);
 
+// The batched 3-D D2Z of m columns (fft.cu; cuFFT's layout and sign):
+// cudaErrorNotSupported for axes that do not factor into 2, 3, 5 or an odd
+// dims[0] / dims[1] (callers use the cuFFT leaf). LRGW_FFT_OWN=0: always cuFFT.
+bool fft_own_enabled();
+cudaError_t fft_d2z_3d(cudaStream_t st, const int* dims, const double* x, long long ldx, int m, double* xhat,
+                       int sm_count);
+
 // Coulomb (coulomb.cu): G-space half-spectrum weights c(G) = w_G v(G) / N_r
 // (w_G = 2 off the self-conjugate i1 planes, 1 on them) laid out to match a
 // D2Z output column of 2*n3*n2*(n1/2+1) interleaved reals.
