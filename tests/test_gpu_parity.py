@@ -392,3 +392,38 @@ def test_selection_engines_agree_with_oracle(tmp_path, variant):
     q = np.linalg.qr(rng.standard_normal((20000, 48)))[0]
     want = R.select_points(q[:, :24], q[:, 24:], 300)
     assert np.array_equal(np.load(path), want)
+
+
+_FFT_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2403_12340_b200 import lrgw
+n = int(sys.argv[2])
+rng = np.random.default_rng(n)
+x = rng.standard_normal((n ** 3, 6))
+y = lrgw.apply_coulomb((n, n, n), (9.0, 9.0, 9.0), x, ctx=lrgw.Context(0))
+np.save(sys.argv[3], y)
+"""
+
+
+@pytest.mark.parametrize("n", [24, 48])
+def test_own_fft_matches_cufft_leaf(tmp_path, n):
+    """The opt-in two-pass D2Z (fft.cu, LRGW_FFT_OWN=1) gives the Coulomb
+    application (model.hpp:208-223) of the cuFFT leaf to round-off."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "fft.py"
+    script.write_text(_FFT_SCRIPT)
+    out = {}
+    for own in ("0", "1"):
+        path = tmp_path / f"y_{own}.npy"
+        r = subprocess.run([sys.executable, str(script), root, str(n), str(path)],
+                           env=dict(os.environ, LRGW_FFT_OWN=own), capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[own] = np.load(path)
+    rel = np.linalg.norm(out["1"] - out["0"]) / np.linalg.norm(out["0"])
+    assert rel <= 1e-13, rel
