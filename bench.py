@@ -219,7 +219,9 @@ def kernel_fractions(stages, work, hbm):
     for k in ("fit_solve", "smw"):
         kernels[k] = {"ms": round(stages.get(k, 0.0), 4), "bound": "latency (N_mu^3 leaves)"}
     # the library leaves the north star allows, timed apart (CUDA events around the calls)
-    kernels["cusolver"] = {"ms": round(stages.get("cusolver", 0.0), 4), "what": "2 potrf leaves inside smw"}
+    kernels["cusolver"] = {"ms": round(stages.get("cusolver", 0.0), 4),
+                           "what": "2 potrf leaves: chol(-T) on the side stream under the Coulomb stage (its wall "
+                                   "time while sharing the SMs, hidden) + chol(M) inside smw"}
     kernels["cufft"] = {"ms": round(stages.get("cufft", 0.0), 4), "what": "the batched D2Z leaf of Theta (= fft)"}
     if "select" in kernels:
         kernels["select"]["note"] = "stage of ~18 launches per candidate block (one block per <= 128 pivots)"

@@ -1,2 +1,4 @@
-timeout 600 ncu --set full --import-source on -k regex:fft_ -c 2 -o gpurun_out/ncu_fft python tools/trace_build.py si64 2 > gpurun_out/ncu_fft.log 2>&1
-tail -2 gpurun_out/ncu_fft.log
+( SWEEP_REPS=3 timeout 900 python tools/env_sweep.py si64 ''
+  SWEEP_REPS=2 timeout 900 python tools/env_sweep.py c60 ''
+  SWEEP_REPS=2 timeout 900 python tools/env_sweep.py si216 '' ) 2>&1 | grep -v Warn
+timeout 1500 python -m pytest tests -m gpu -x -q -rf -k "config or build or projection or gw or dist" > gpurun_out/gpu_tests_sub.log 2>&1; tail -2 gpurun_out/gpu_tests_sub.log

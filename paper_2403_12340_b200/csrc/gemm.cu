@@ -190,6 +190,25 @@ int choose_splits(long long tiles, int ktiles, long long slots) {
   return best;
 }
 
+// Splits (<= 8) that keep the tile grid closest to whole waves of `slots`;
+// a smaller split wins ties within 2 % (each split adds an M N partial to
+// the reduction).
+int choose_splits_waves(long long tiles, int ktiles, long long slots) {
+  const int smax = std::max(1, std::min(ktiles / 16, 8));
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= smax; ++s) {
+    const long long ctas = tiles * s;
+    const long long waves = (ctas + slots - 1) / slots;
+    const double eff = (double)ctas / (double)(waves * slots);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 __global__ void splitk_reduce_kernel(const double* partial, int splits, long long stride, int M,
@@ -429,8 +448,12 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
     const long long tiles = lower ? tm * (tm + 1) / 2 : tm * tn;
     const int ktiles = (K + 15) / 16;
     int splits = 1, kc = 0;
-    if (tiles < 2LL * sm_count && ktiles >= 32 && work) {
-      splits = choose_splits(tiles, ktiles, (long long)sm_count);
+    // split-K against the wave quantisation of the resident tile slots (a
+    // 1485-tile grid on 296 slots runs 5.02 waves: 84 % busy)
+    const long long slots = (long long)sm_count * dgemm_tma_k_per_sm(M);
+    static const int force = getenv("LRGW_TMA_KSPLITS") ? atoi(getenv("LRGW_TMA_KSPLITS")) : 0;
+    if (ktiles >= 32 && work) {
+      splits = force > 0 ? force : choose_splits_waves(tiles, ktiles, slots);
       while (splits > 1 && (size_t)splits * M * N > work_elems) --splits;
       if (splits > 1) {
         kc = ((ktiles + splits - 1) / splits) * 16;

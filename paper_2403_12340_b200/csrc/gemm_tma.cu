@@ -64,13 +64,15 @@ bool encode_k(CUtensorMap* map, const double* ptr, long long rows, long long k, 
 using K4 = Gemm4kCfg<128, 128, 64, 32, 5, 1>;         // 8 compute warps, thread 0 refills
 using K4P = Gemm4kCfg<96, 96, 48, 48, 6, 1, true>;     // 4 compute warps + TMA warp
 using K4S = Gemm4kCfg<64, 64, 32, 32, 6, 2, true>;     // 4 compute warps + TMA warp, 2 CTAs per SM
-// Measured (tools/bench_syrk.py, profiles/r02/syrk_engines.txt): the 64 x 64
-// two-CTA configuration wins from N_mu = 3456 up (0.897 of the DMMA peak at
-// 8192), the 128 x 128 one at N_mu = 1024 (0.803). LRGW_TMA_KCFG forces one.
+// Measured with the wave-aware split-K (tools/bench_syrk.py,
+// profiles/r02/syrk_splits.txt): 128 x 128 tiles where N_mu is a multiple of
+// 128 below 4096 (1024: 0.804, 3456: 0.886 of the DMMA peak), the 64 x 64
+// two-CTA tiles for other widths (960: 0.805 vs 0.709 — a half-empty 128 edge
+// tile row) and from 4096 up (8192: 0.897). LRGW_TMA_KCFG forces one.
 int kcfg(int m) {
   static const int v = getenv("LRGW_TMA_KCFG") ? atoi(getenv("LRGW_TMA_KCFG")) : -1;
   if (v >= 0) return v;
-  return m >= 2048 ? 2 : 0;
+  return (m >= 4096 || m % 128 != 0) ? 2 : 0;
 }
 
 template <class Cfg>
@@ -115,6 +117,7 @@ using H4 = Gemm4Cfg<64, BN, 32, 32, kBK, 4, true, 1>;
 }  // namespace
 
 int dgemm_tma_k_tile(int m) { return kcfg(m) == 1 ? K4P::BM : kcfg(m) == 2 ? K4S::BM : K4::BM; }
+int dgemm_tma_k_per_sm(int m) { return kcfg(m) == 2 ? K4S::MINB : 1; }
 
 template <class Cfg>
 cudaError_t launch4k(cudaStream_t st, int M, int N, int K, const double* A, long long lda, const double* B,

@@ -37,6 +37,7 @@ cudaError_t dgemm_tma(cudaStream_t st, int M, int N, int K, const double* A, lon
 // K-contiguous operands (A(m, k) at m lda + k): lower tiles, k-scale, split-K
 // partials (k_chunk a multiple of 16; the caller reduces with dgemm_tma_k_tile(M)).
 int dgemm_tma_k_tile(int m);
+int dgemm_tma_k_per_sm(int m);  // resident CTAs per SM of that configuration
 cudaError_t dgemm_tma_k(cudaStream_t st, int M, int N, int K, const double* A, long long lda, const double* B,
                         long long ldb, double* C, long long ldc, double alpha, double beta, const double* scale,
                         bool lower, int splits, int k_chunk, double* partial);
