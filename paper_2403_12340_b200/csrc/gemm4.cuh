@@ -203,7 +203,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
         }
     }
     mbar_wait(full + s, (kt / STAGES) & 1);
-    if (live) {
+    // triangular B: a k-tile wholly left of the warp's first column is zero
+    // for the whole warp (the tile-level skip only starts K at n0) — skip its
+    // MMAs (exact: the skipped products are zeros)
+    const bool zero_k = p.tri_b && kt < kt1 && kb + (kt + 1) * BK <= n0 + wn;
+    if (live && !zero_k) {
       const double* sa = ring + s * Cfg::STAGE_ELEMS;
       const double* sb = sa + Cfg::A_BOXES * Cfg::BOX;
 #pragma unroll
