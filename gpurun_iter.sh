@@ -1,5 +1,2 @@
-( SWEEP_REPS=3 timeout 900 python tools/env_sweep.py si64 ''
-  SWEEP_REPS=2 timeout 900 python tools/env_sweep.py c60 ''
-  SWEEP_REPS=2 timeout 900 python tools/env_sweep.py si216 ''
-  SWEEP_REPS=1 timeout 900 python tools/env_sweep.py si512 '' ) 2>&1 | grep -v Warn
-timeout 1500 python -m pytest tests -m gpu -x -q -rf -k "config or build or parity" > gpurun_out/gpu_tests_sub.log 2>&1; tail -2 gpurun_out/gpu_tests_sub.log
+for sp in 0 1 2 3; do echo -n "kcfg=0 splits=$sp "; LRGW_TMA_KCFG=0 LRGW_TMA_KSPLITS=$sp timeout 300 python tools/bench_syrk.py 8192 903168 3 2>&1 | grep syrk; done
+for sp in 0 1 2; do echo -n "kcfg=1 splits=$sp "; LRGW_TMA_KCFG=1 LRGW_TMA_KSPLITS=$sp timeout 300 python tools/bench_syrk.py 8192 903168 3 2>&1 | grep syrk; done

@@ -65,14 +65,15 @@ using K4 = Gemm4kCfg<128, 128, 64, 32, 5, 1>;         // 8 compute warps, thread
 using K4P = Gemm4kCfg<96, 96, 48, 48, 6, 1, true>;     // 4 compute warps + TMA warp
 using K4S = Gemm4kCfg<64, 64, 32, 32, 6, 2, true>;     // 4 compute warps + TMA warp, 2 CTAs per SM
 // Measured with the wave-aware split-K (tools/bench_syrk.py,
-// profiles/r02/syrk_splits.txt): 128 x 128 tiles where N_mu is a multiple of
-// 128 below 4096 (1024: 0.804, 3456: 0.886 of the DMMA peak), the 64 x 64
-// two-CTA tiles for other widths (960: 0.805 vs 0.709 — a half-empty 128 edge
-// tile row) and from 4096 up (8192: 0.897). LRGW_TMA_KCFG forces one.
+// profiles/r02/syrk_splits.txt): 128 x 128 tiles where 128 divides N_mu
+// (1024: 0.804, 3456: 0.886, 8192: 0.912 of the DMMA peak against 0.782 /
+// 0.862 / 0.897 for 64 x 64), the 64 x 64 two-CTA tiles for other widths
+// (960: 0.805 vs 0.709 — a half-empty 128 edge tile row). LRGW_TMA_KCFG
+// forces one.
 int kcfg(int m) {
   static const int v = getenv("LRGW_TMA_KCFG") ? atoi(getenv("LRGW_TMA_KCFG")) : -1;
   if (v >= 0) return v;
-  return (m >= 4096 || m % 128 != 0) ? 2 : 0;
+  return m % 128 != 0 ? 2 : 0;
 }
 
 template <class Cfg>
