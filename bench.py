@@ -206,7 +206,7 @@ def kernel_fractions(stages, work, hbm):
     kernels = {}
     for k, (bound, amount) in work.items():
         t = stages.get(k, 0.0)
-        if t <= 0:
+        if t <= 0.01:  # (an empty stage: the implicit-Theta build has no fit GEMM)
             continue
         if bound == "tensor":
             ach = amount / (t * 1e-3) / 1e12
@@ -253,6 +253,7 @@ def run_ours(args, cfg, world, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     ctx = lrgw.Context(local)
+    ctx.set_theta_implicit(args.theta == "implicit")
     stream = torch.cuda.ExternalStream(lrgw.L.load().lrgw_ctx_stream(ctx.handle), device=dev)
     psi = synth.orbitals_device(cfg, seed=1, device=dev)
     torch.cuda.synchronize()
@@ -283,7 +284,7 @@ def run_ours(args, cfg, world, rank, local):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     info = None
-    for _ in range(args.steps):
+    for step in range(args.steps):
         e0.record(stream)
         ep = step_dev()
         e1.record(stream)
@@ -292,7 +293,8 @@ def run_ours(args, cfg, world, rank, local):
         for k, v in ctx.stage_ms().items():
             stage_acc.setdefault(k, []).append(v)
         points = ep.point_indices  # the CPU baseline's fit sample uses the build's own ISDF points
-        info = ep.info()
+        if step == args.steps - 1:  # (forms Theta of an implicit-Theta handle: once, outside the timings)
+            info = ep.info()
         ep.close()
     torch.cuda.synchronize()
     barrier(world)
@@ -336,13 +338,36 @@ def run_ours(args, cfg, world, rank, local):
     d2h = y_h.numel() * 8
     assert torch.isfinite(y_d).all()  # parity guard on the bench output
 
+    # ---- the implicit-Theta build beside it (same context, inputs and probe) ----
+    implicit = None
+    if args.theta == "explicit" and world == 1 and not args.no_implicit_line:
+        ctx.set_theta_implicit(True)
+        step_dev().close()
+        torch.cuda.synchronize()
+        ti, st_i = [], {}
+        for _ in range(max(1, min(args.steps, 3))):
+            e0.record(stream)
+            ep = step_dev()
+            e1.record(stream)
+            e1.synchronize()
+            ti.append(e0.elapsed_time(e1))
+            for k, v in ctx.stage_ms().items():
+                st_i.setdefault(k, []).append(v)
+            ep.close()
+        ctx.set_theta_implicit(False)
+        implicit = {"value": sum(ti) / len(ti) / 1e3, "unit": "s", "steps": len(ti),
+                    "stages_ms": {k: round(statistics.median(v), 4) for k, v in st_i.items()},
+                    "what": "the same build with Theta kept factored as L L_P^-1 (lrgw_ctx_set_theta_implicit; "
+                            "--theta implicit): eps^-1 X applied from (L, K'), the N_r x N_mu^2 fit GEMM not part "
+                            "of the build; Theta / K formed on demand. Parity: tests/test_gpu_implicit.py"}
+
     stages = {k: statistics.median(v) for k, v in stage_acc.items()}
     n_mu = min(max(lrgw.num_aux(cfg.k_mu, cfg.n_v, cfg.n_c), 1), cfg.n_r)
     hbm = _peaks()
     kernels = kernel_fractions(stages, work_for(cfg, n_mu), hbm)
     return {"ms": ms, "e2e_ms": e2e, "h2d": h2d, "d2h": d2h, "launches": launches, "clocks": clk,
             "stages": stages, "kernels": kernels, "roofline": roofline_of(kernels, cfg, hbm, 1),
-            "psi": psi, "e": e, "ctx": ctx, "points": points, "info": info}
+            "psi": psi, "e": e, "ctx": ctx, "points": points, "info": info, "implicit": implicit}
 
 
 def run_sharded(args, cfg, world, rank, local):
@@ -483,6 +508,12 @@ def main():
     ap.add_argument("--mode", default=None, choices=["single", "sharded", "replicas"],
                     help="single (N = 1 default): the one-GPU build; sharded (N > 1 default): one build "
                          "split across the ranks (strong scaling); replicas: one full build per rank")
+    ap.add_argument("--no-implicit-line", action="store_true",
+                    help="skip the implicit-Theta measurement reported beside the explicit one")
+    ap.add_argument("--theta", default="explicit", choices=["explicit", "implicit"],
+                    help="explicit (default): the build forms Theta = L L_P^-1; implicit: Theta stays factored "
+                         "(lrgw_ctx_set_theta_implicit) — eps^-1 is applied from (L, K') and the fit GEMM is not "
+                         "part of the build")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(relaunch_under_torchrun(args))
@@ -503,6 +534,10 @@ def main():
                       f"{cfg.n_r * n_mu * 8 / 1e6:.0f} MB); no flush",
                 "parallelism": {"single": "1 GPU", "replicas": f"replicas x{world}",
                                 "sharded": f"sharded x{world} (z-plane panels, node split, NCCL)"}[mode]}
+    if args.theta == "implicit":
+        workload["theta"] = ("implicit: Theta = L L_P^-1 kept factored (K' = L_P^-1 K L_P^-T, T' = L_P^-1 T L_P^-T, "
+                             "P' = L^T V L), eps^-1 X applied from (L, K'); the N_r x N_mu^2 fit GEMM is not part "
+                             "of the build (Theta formed on demand)")
     metric = "low-rank eps^-1 build time (s), stages 1-5 + probe apply"
 
     if args.impl == "reference":
@@ -545,6 +580,8 @@ def main():
                 "selection": {"min_pivot_margin": info.get("min_margin"), "at_step": info.get("min_margin_step"),
                               "candidate_blocks": info.get("select_blocks"),
                               "gram_cond_lower_bound": info.get("lp_diag_ratio")}}
+        if res.get("implicit"):
+            line["theta_implicit"] = res["implicit"]
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist

@@ -78,6 +78,12 @@ int lrgw_ctx_stage_ms(lrgw_ctx ctx, double* ms, int n);
 long long lrgw_ctx_kernel_launches(lrgw_ctx ctx);
 /* Candidate-set size of the batched greedy point selection (default 64). */
 int lrgw_ctx_set_select_batch(lrgw_ctx ctx, int s);
+/* on != 0: lrgw_build keeps Theta factored as L L_P^-1 (the selection factor
+ * and its point block) instead of forming it — the N_r x N_mu^2 fit GEMM
+ * leaves the build; the handle applies eps^-1 unchanged and forms Theta, K,
+ * T, Theta^T V Theta on first demand (lrgw_eps_get / info / device_ptrs,
+ * the screened projections). Default off. */
+int lrgw_ctx_set_theta_implicit(lrgw_ctx ctx, int on);
 
 /* ---- host-scalar contour geometry ----------------------------------------- */
 int lrgw_num_aux(double k_mu, int n1, int n2, int* out);                 /* isdf.hpp:42-46 */
@@ -172,7 +178,7 @@ typedef struct {
   double* pvp;          /* n_mu x n_mu Theta^T V Theta                 */
   double min_margin;    /* smallest relative top-2 residual margin (d1 - d2) / d1 over the greedy steps */
   int min_margin_step;  /* the step it occurred at                     */
-  int fit_path;         /* 0: fused Theta = L L_P^-1; 1: explicit Gram LU (isdf.hpp:143) */
+  int fit_path;         /* 0: fused Theta = L L_P^-1; 1: explicit Gram LU (isdf.hpp:143); 2: implicit (kept factored) */
   double lp_diag_ratio; /* (max|L_P,ii| / min|L_P,ii|)^2, a lower bound on cond(G(P,P)) */
   int select_blocks;    /* candidate blocks of the selection            */
 } lrgw_eps_info;

@@ -72,6 +72,7 @@ _SIGS = {
     "lrgw_ctx_stage_ms": (ctypes.c_int, [ctx_t, c_double_p, ctypes.c_int]),
     "lrgw_ctx_kernel_launches": (ctypes.c_longlong, [ctx_t]),
     "lrgw_ctx_set_select_batch": (ctypes.c_int, [ctx_t, ctypes.c_int]),
+    "lrgw_ctx_set_theta_implicit": (ctypes.c_int, [ctx_t, ctypes.c_int]),
     "lrgw_num_aux": (ctypes.c_int, [ctypes.c_double, ctypes.c_int, ctypes.c_int, c_int_p]),
     "lrgw_elliptic_k": (ctypes.c_int, [ctypes.c_double, c_double_p]),
     "lrgw_jacobi_sn_cn_dn": (ctypes.c_int, [ctypes.c_double, ctypes.c_double, c_double_p]),

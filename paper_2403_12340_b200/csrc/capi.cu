@@ -1185,14 +1185,14 @@ int lrgw_ctx_destroy(lrgw_ctx c) {
   {
     std::lock_guard<std::mutex> lk(c->mem_mu);
     for (lrgw_eps_s* e : c->live_eps) {  // orphan the handles, free their buffers
-      for (double* p : {e->theta, e->k, e->t, e->pvp}) {
+      for (double* p : {e->theta, e->k, e->t, e->pvp, e->lp, e->lpinv}) {
         auto it = c->mem_live.find(p);
         if (it != c->mem_live.end()) {
           cudaFree(p);
           c->mem_live.erase(it);
         }
       }
-      e->theta = e->k = e->t = e->pvp = nullptr;
+      e->theta = e->k = e->t = e->pvp = e->lp = e->lpinv = nullptr;
       e->ctx = nullptr;
     }
     c->live_eps.clear();
@@ -1246,6 +1246,12 @@ int lrgw_ctx_stage_ms(lrgw_ctx c, double* ms, int n) {
 }
 
 long long lrgw_ctx_kernel_launches(lrgw_ctx c) { return c ? launch_count() - c->launches0 : 0; }
+
+int lrgw_ctx_set_theta_implicit(lrgw_ctx c, int on) {
+  if (!c) return LRGW_ERR_INVALID_INPUT;
+  c->theta_implicit = on != 0;
+  return LRGW_OK;
+}
 
 int lrgw_ctx_set_select_batch(lrgw_ctx c, int s) {
   if (!c || s < 1 || s > select_max_candidates()) return LRGW_ERR_INVALID_INPUT;
@@ -1536,6 +1542,52 @@ void lrgw_impl::eps_apply_impl(lrgw_ctx c, lrgw_eps e, const double* x, long lon
   ck(axpby(c->stream, n_r, m, 1.0, x, ldx, 1.0, y, ldy), "axpby");
 }
 
+// Implicit handle -> ordinary handle: Theta = (L L_P^-1) scattered to the
+// sorted-point columns (the fused fit's GEMM), K = Pi^T L_P K' L_P^T Pi,
+// Theta^T V Theta = Pi^T L_P^-T P' L_P^-1 Pi, T = Pi^T T_pi Pi.
+void lrgw_impl::eps_explicit(lrgw_ctx c, lrgw_eps_s* e) {
+  if (!e->implicit) return;
+  const int n_r = e->n_r, n_mu = e->n_mu;
+  const size_t nn = (size_t)n_mu * n_mu;
+  DBuf dmap = upload_i(c, e->colmap.data(), n_mu);
+  std::vector<int> inv(n_mu);
+  for (int q = 0; q < n_mu; ++q) inv[e->colmap[q]] = q;
+  DBuf dinv = upload_i(c, inv.data(), n_mu);
+  DBuf theta = dalloc(c, (size_t)n_r * n_mu);
+  DBuf xt = dalloc(c, nn);
+  ck(transpose(c->stream, e->lpinv, n_mu, n_mu, n_mu, xt.d(), n_mu), "transpose");
+  ck(dgemm(c->stream, n_r, n_mu, n_mu, e->theta, n_r, Lay::MN, xt.d(), n_mu, Lay::MN, theta.d(), n_r, 1.0, 0.0,
+           nullptr, false, c->sm_count, nullptr, 0, true, dmap.i()),
+     "dgemm(theta)");
+  Work w = make_work(c, 8 * nn);
+  DBuf a = dalloc(c, nn), b = dalloc(c, nn);
+  auto to_sorted = [&](const double* piv, double* out) {  // out = Pi^T piv Pi
+    ck(gather_rows(c->stream, piv, n_mu, n_mu, dinv.i(), n_mu, b.d(), n_mu), "gather_rows");
+    ck(gather_cols(c->stream, b.d(), n_mu, n_mu, dinv.i(), n_mu, out, n_mu), "gather_cols");
+  };
+  // K_pi = L_P K' L_P^T
+  gemm(c, n_mu, n_mu, n_mu, e->lp, n_mu, Lay::MN, e->k, n_mu, Lay::K, a.d(), n_mu, 1.0, 0.0);
+  DBuf kpi = dalloc(c, nn);
+  gemm(c, n_mu, n_mu, n_mu, a.d(), n_mu, Lay::MN, e->lp, n_mu, Lay::MN, kpi.d(), n_mu, 1.0, 0.0, nullptr, true, &w);
+  ck(mirror_lower(c->stream, kpi.d(), n_mu, n_mu, false), "mirror");
+  to_sorted(kpi.d(), e->k);
+  // pvp_pi = L_P^-T P' L_P^-1
+  gemm(c, n_mu, n_mu, n_mu, e->lpinv, n_mu, Lay::K, e->pvp, n_mu, Lay::K, a.d(), n_mu, 1.0, 0.0);
+  gemm(c, n_mu, n_mu, n_mu, a.d(), n_mu, Lay::MN, e->lpinv, n_mu, Lay::K, kpi.d(), n_mu, 1.0, 0.0, nullptr, true,
+       &w);
+  ck(mirror_lower(c->stream, kpi.d(), n_mu, n_mu, false), "mirror");
+  to_sorted(kpi.d(), e->pvp);
+  ck(cudaMemcpyAsync(a.p, e->t, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+  to_sorted(a.d(), e->t);
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  ctx_free(c, e->theta);
+  e->theta = static_cast<double*>(theta.take());
+  ctx_free(c, e->lp);
+  ctx_free(c, e->lpinv);
+  e->lp = e->lpinv = nullptr;
+  e->implicit = false;
+}
+
 extern "C" {
 
 int lrgw_epsilon_inverse_apply(lrgw_ctx c, lrgw_eps e, const double* x, int m, double* y) {
@@ -1564,6 +1616,7 @@ int lrgw_eps_get(lrgw_ctx c, lrgw_eps e, double* k, double* p, double* vp, doubl
     if (!e || !e->ctx) fail(LRGW_ERR_INVALID_INPUT, "eps: null handle");
     const size_t nn = (size_t)e->n_mu * e->n_mu, np = (size_t)e->n_r * e->n_mu;
     if ((p || vp) && eps_is_panel(e)) fail(LRGW_ERR_INVALID_INPUT, "eps_get: P / VP of a row-panel handle (use lrgw_eps_info_get)");
+    if (k || p || vp || t) eps_explicit(c, e);
     if (k) download(c, k, e->k, nn * sizeof(double));
     if (p) download(c, p, e->theta, np * sizeof(double));
     if (t && e->t) download(c, t, e->t, nn * sizeof(double));
@@ -1592,6 +1645,8 @@ int lrgw_eps_destroy(lrgw_eps e) {
     ctx_free(c, e->k);
     ctx_free(c, e->t);
     ctx_free(c, e->pvp);
+    ctx_free(c, e->lp);
+    ctx_free(c, e->lpinv);
     std::lock_guard<std::mutex> lk(c->mem_mu);
     c->live_eps.erase(e);
   }
@@ -1601,6 +1656,10 @@ int lrgw_eps_destroy(lrgw_eps e) {
 
 int lrgw_eps_info_get(lrgw_eps e, lrgw_eps_info* out) {
   if (!e || !out) return LRGW_ERR_INVALID_INPUT;
+  if (e->implicit) {  // the pointers below are the explicit Theta / K / T
+    const int st = guarded(e->ctx, [&] { eps_explicit(e->ctx, e); });
+    if (st != LRGW_OK) return st;
+  }
   out->n_r = e->n_r;
   out->n_mu = e->n_mu;
   out->theta = e->theta;
@@ -1617,6 +1676,10 @@ int lrgw_eps_info_get(lrgw_eps e, lrgw_eps_info* out) {
 
 int lrgw_eps_device_ptrs(lrgw_eps e, double** theta, double** k, double** t) {
   if (!e) return LRGW_ERR_INVALID_INPUT;
+  if (e->implicit) {
+    const int st = guarded(e->ctx, [&] { eps_explicit(e->ctx, e); });
+    if (st != LRGW_OK) return st;
+  }
   if (theta) *theta = e->theta;
   if (k) *k = e->k;
   if (t) *t = e->t;
@@ -1686,6 +1749,115 @@ void timing_end(lrgw_ctx c) {
   c->timing = false;
 }
 
+// Implicit-Theta build, stages 2-5 after the selection (lrgw_ctx_set_theta_implicit).
+// Theta = L L_P^-1 (the fused fit's identity) is kept factored instead of
+// formed: with T_pi (T over the points in pivot order),
+//   T' = L_P^-1 T_pi L_P^-T,  P' = L^T V L,  K' = (T'^-1 / 2 - P')^-1
+// gives Theta K Theta^T = L K' L^T exactly (K' = L_P^-1 K_pi L_P^-T), so the
+// probe apply runs on (L, K') unchanged and the N_r x N_mu^2 fit GEMM is not
+// needed by the build; eps_explicit() forms Theta, K, T, Theta^T V Theta in
+// the sorted-point order when a caller asks for them. Returns nullptr when
+// L_P has a tiny pivot (the caller takes the explicit path).
+lrgw_eps_s* build_implicit(lrgw_ctx c, const lrgw_build_params& P, const BuildSetup& bs, const double* phi_v,
+                           long long ldv, const double* phi_c, long long ldc, const double* energies,
+                           const std::vector<int32_t>& pts, SelectKeep& keep) {
+  const int n_r = P.n_r, n_v = P.n_v, n_c = P.n_c, n_mu = bs.n_mu, n_e = P.n_e;
+  const size_t nn = (size_t)n_mu * n_mu;
+  const lrgw_host::Spec& spec = bs.spec;
+  // stage 2 (solve only): L_P and L_P^-1 (the fused fit's checks)
+  mark(c, 2);
+  std::vector<int> order(keep.order.begin(), keep.order.end());
+  DBuf dorder = upload_i(c, order.data(), n_mu);
+  DBuf lp = dalloc(c, nn), lpinv = dalloc(c, nn);
+  ck(gather_rows(c->stream, keep.L.d(), n_r, n_mu, dorder.i(), n_mu, lp.d(), n_mu), "gather");
+  ck(zero_strict_upper(c->stream, lp.d(), n_mu, n_mu), "zero_upper");
+  std::vector<double> diag(n_mu);
+  ck(cudaMemcpy2DAsync(diag.data(), sizeof(double), lp.d(), (size_t)(n_mu + 1) * sizeof(double), sizeof(double),
+                       n_mu, cudaMemcpyDeviceToHost, c->stream),
+     "D2H diag");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  double gmax = 0.0, dmin = HUGE_VAL, dmax = 0.0;
+  for (double v : diag) {
+    gmax = std::max(gmax, v * v);
+    dmin = std::min(dmin, std::abs(v));
+    dmax = std::max(dmax, std::abs(v));
+  }
+  const double tiny = 1e-14 * (gmax > 0.0 ? gmax : 1.0);
+  for (double v : diag)
+    if (!(v * v >= tiny)) return nullptr;
+  ck(cudaMemcpyAsync(lpinv.p, lp.p, nn * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "D2D");
+  {
+    DBuf work = dalloc(c, trtri_work_elems(n_mu));
+    DBuf bad = ialloc(c, 1);
+    const int big = 0x7fffffff;
+    ck(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D");
+    ck(lrgw_dev::trtri_lower(c->stream, lpinv.d(), n_mu, n_mu, work.d(), bad.i(), c->sm_count), "trtri");
+    int h = 0;
+    download(c, &h, bad.p, sizeof(int));
+    if (h != big) return nullptr;
+  }
+  mark(c, 3);
+  mark(c, 4);  // no fit GEMM
+  // stage 3: T over the points in pivot order
+  DBuf pv = dalloc(c, (size_t)n_mu * n_v), pc = dalloc(c, (size_t)n_mu * n_c);
+  ck(gather_rows(c->stream, phi_v, ldv, n_v, dorder.i(), n_mu, pv.d(), n_mu), "gather");
+  ck(gather_rows(c->stream, phi_c, ldc, n_c, dorder.i(), n_mu, pc.d(), n_mu), "gather");
+  DBuf t = dalloc(c, nn);
+  if (spec.bypass) {
+    direct_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, t.d(), n_mu);
+  } else if (P.n_lambda > 0) {
+    fixed_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, n_e, P.n_lambda, t.d(), n_mu);
+  } else {
+    adaptive_impl(c, pv.d(), n_mu, pc.d(), n_mu, n_mu, n_v, n_c, energies, spec, t.d());
+  }
+  // T' = L_P^-1 T L_P^-T (symmetric by the mirror of its lower triangle)
+  DBuf tp = dalloc(c, nn), tmp = dalloc(c, nn);
+  {
+    Work w = make_work(c, 8 * nn);
+    gemm(c, n_mu, n_mu, n_mu, lpinv.d(), n_mu, Lay::MN, t.d(), n_mu, Lay::K, tmp.d(), n_mu, 1.0, 0.0);
+    gemm(c, n_mu, n_mu, n_mu, tmp.d(), n_mu, Lay::MN, lpinv.d(), n_mu, Lay::MN, tp.d(), n_mu, 1.0, 0.0, nullptr,
+         true, &w);
+    ck(mirror_lower(c->stream, tp.d(), n_mu, n_mu, false), "mirror");
+  }
+  mark(c, 5);
+  // stages 4-5 on (L, T'): chol(-T') under the Coulomb stage, P' = L^T V L
+  DBuf pvp = dalloc(c, nn), k = dalloc(c, nn);
+  SmwState smw;
+  cudaStream_t side = side_stream(c);
+  ck(cudaEventRecord(c->ev_side, c->stream), "cudaEventRecord");
+  ck(cudaStreamWaitEvent(side, c->ev_side, 0), "cudaStreamWaitEvent");
+  smw_factor_t(c, side, tp.d(), n_mu, smw);
+  pvp_impl(c, P.dims, P.cell, P.zero_kernel, keep.L.d(), n_r, n_mu, pvp.d());
+  mark(c, 7);
+  smw_join(c, smw);
+  smw_finish(c, smw, pvp.d(), n_mu, k.d());
+  mark(c, 8);
+  timing_end(c);
+  auto* e = new_eps(c);
+  e->ctx = c;
+  e->n_r = n_r;
+  e->n_mu = n_mu;
+  std::memcpy(e->dims, P.dims, sizeof(e->dims));
+  std::memcpy(e->cell, P.cell, sizeof(e->cell));
+  e->zero = P.zero_kernel;
+  e->theta = static_cast<double*>(keep.L.take());
+  e->k = static_cast<double*>(k.take());
+  e->t = static_cast<double*>(t.take());
+  e->pvp = static_cast<double*>(pvp.take());
+  e->lp = static_cast<double*>(lp.take());
+  e->lpinv = static_cast<double*>(lpinv.take());
+  e->pts = pts;
+  e->colmap.resize(n_mu);
+  for (int q = 0; q < n_mu; ++q)
+    e->colmap[q] = (int)(std::lower_bound(pts.begin(), pts.end(), order[q]) - pts.begin());
+  e->implicit = true;
+  e->fit_path = 2;  // implicit
+  e->lp_diag_ratio = dmin > 0.0 ? (dmax / dmin) * (dmax / dmin) : HUGE_VAL;
+  e->row0 = 0;
+  e->rows = n_r;
+  return e;
+}
+
 // The one-GPU build, stages 1-5 (stage boundaries marked for the timings).
 lrgw_eps_s* build_one(lrgw_ctx c, const lrgw_build_params& P, const BuildSetup& bs, const double* phi_v,
                       long long ldv, const double* phi_c, long long ldc, const double* energies) {
@@ -1702,6 +1874,15 @@ lrgw_eps_s* build_one(lrgw_ctx c, const lrgw_build_params& P, const BuildSetup& 
   double min_margin = -1.0;  // smallest relative top-2 residual margin over all steps (linalg.hpp:45-47)
   std::vector<int32_t> pts = select_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, n_mu, &min_margin, &keep);
   mark(c, 1);
+  if (c->theta_implicit && keep.steps == n_mu) {
+    lrgw_eps_s* e = build_implicit(c, P, bs, phi_v, ldv, phi_c, ldc, energies, pts, keep);
+    if (e) {
+      e->min_margin = min_margin;
+      e->min_margin_step = keep.min_margin_step;
+      e->select_blocks = keep.blocks;
+      return e;
+    }
+  }
   // stage 2: fused fit from the selection's factor (explicit path otherwise)
   DBuf theta = dalloc(c, (size_t)n_r * n_mu);
   mark(c, 2);  // FIT_LHS is empty on the fused path (lhs lives in L)
@@ -2032,6 +2213,7 @@ int lrgw_project_screened_interactions(lrgw_ctx c, lrgw_eps e, const double* p_v
                                        int n_nn, double* w_vn, double* w_nn, double* v_vn) {
   return guarded(c, [&] {
     if (!e || !e->ctx) fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: null handle");
+    eps_explicit(c, e);
     if (n_vn < 0 || n_nn < 0 || (n_vn > 0 && !p_vn) || (n_nn > 0 && !p_nn))
       fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: bad sizes");
     const size_t n_r = e->n_r;
@@ -2049,6 +2231,7 @@ int lrgw_dev_project_screened(lrgw_ctx c, lrgw_eps e, const double* p_vn, long l
                               double* v_vn) {
   return guarded(c, [&] {
     if (!e || !e->ctx) fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: null handle");
+    eps_explicit(c, e);
     if (n_vn < 0 || n_nn < 0 || (n_vn > 0 && ld_vn < e->n_r) || (n_nn > 0 && ld_nn < e->n_r))
       fail(LRGW_ERR_INVALID_INPUT, "project_screened_interactions: bad sizes");
     project_impl(c, e, p_vn, ld_vn, n_vn, p_nn, ld_nn, n_nn, w_vn, w_nn, v_vn);

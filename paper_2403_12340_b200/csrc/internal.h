@@ -72,6 +72,7 @@ struct lrgw_ctx_s {
   bool timing = false;  // record stage events (lrgw_build only)
   long long launches0 = 0;
   int select_batch = 128;
+  bool theta_implicit = false;  // lrgw_build keeps Theta factored as L L_P^-1 (see lrgw_eps_s)
   // Device-memory cache of this context: freed blocks are kept (by size) and
   // handed out again to later requests on the context's stream. A build
   // repeats the same sizes every call, so from the second call on no
@@ -108,6 +109,15 @@ struct lrgw_eps_s {
   // row panel of a multi-rank build (lrgw_build_sharded): theta holds grid
   // rows [row0, row0 + rows); rows == 0 means all n_r rows (one GPU)
   int row0 = 0, rows = 0;
+  // implicit-Theta handle (lrgw_ctx_set_theta_implicit): theta holds the
+  // selection factor L (pivot order) and k, t, pvp the pivot-order K' =
+  // L_P^-1 K L_P^-T, T and L^T V L, so Theta K Theta^T = L K' L^T; lp / lpinv
+  // keep L_P and L_P^-1, colmap the pivot -> sorted-point column map.
+  // eps_explicit() turns it into the ordinary handle on first demand.
+  bool implicit = false;
+  double* lp = nullptr;
+  double* lpinv = nullptr;
+  std::vector<int> colmap;
 };
 
 namespace lrgw_impl {
@@ -212,6 +222,8 @@ void coulomb_apply(lrgw_ctx c, const int* dims, const double* cell, int zero, co
 void pvp_impl(lrgw_ctx c, const int* dims, const double* cell, int zero, const double* theta, long long ldt,
               int n_mu, double* pvp);
 void smw_core(lrgw_ctx c, const double* t, const double* pvp, int n, double* k);
+// An implicit-Theta handle made explicit in place (no-op otherwise).
+void eps_explicit(lrgw_ctx c, lrgw_eps_s* e);
 void trtri_lower(lrgw_ctx c, double* a, int n);
 double dev_max_abs(lrgw_ctx c, const double* x, size_t n);
 void gram_inverse(lrgw_ctx c, const double* gram, int n, double* ginv);

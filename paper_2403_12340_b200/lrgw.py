@@ -129,6 +129,10 @@ class Context:
     def kernel_launches(self) -> int:
         return int(self._lib.lrgw_ctx_kernel_launches(self.handle))
 
+    def set_theta_implicit(self, on: bool = True):
+        """lrgw_build keeps Theta factored as L L_P^-1 (see lrgw_ctx_set_theta_implicit)."""
+        _check(self._lib.lrgw_ctx_set_theta_implicit(self.handle, int(bool(on))), self.handle, "set_theta_implicit")
+
     def set_select_batch(self, s: int):
         _check(self._lib.lrgw_ctx_set_select_batch(self.handle, int(s)), self.handle, "set_select_batch")
 
