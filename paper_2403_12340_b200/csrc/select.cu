@@ -99,6 +99,11 @@ struct TopkScratch {
   unsigned hist[TK_BINS];
   Ent sure[TK_SCAP];
   Ent bnd[TK_BCAP];
+  // refinement of an over-full boundary bin (large grids): the next 12 key
+  // bits of its rows, the sure count before it, and the refined boundary rows
+  unsigned hist2[TK_BINS];
+  unsigned sure0, bnd2_cnt, refine_ran;
+  Ent bnd2[TK_BCAP];
 };
 
 __device__ __forceinline__ int tk_bin(unsigned long long key, unsigned ref) {
@@ -204,6 +209,83 @@ __global__ void __launch_bounds__(256) topk_compact_kernel(const double* d, cons
   }
 }
 
+// Sub-bin of a key inside its 17-bit bin (the next 12 bits; larger keys first).
+__device__ __forceinline__ int tk_sub(unsigned long long key) {
+  return (TK_BINS - 1) - static_cast<int>((key >> 35) & (TK_BINS - 1));
+}
+
+// Boundary bin over TK_BCAP rows: histogram its rows by sub-bin.
+__global__ void __launch_bounds__(256) topk_hist2_kernel(const double* d, const int* pos, int n_r, int k,
+                                                         const int* k_dev, int s1, TopkScratch* sc) {
+  if (sc->bnd_cnt <= static_cast<unsigned>(TK_BCAP)) return;
+  __shared__ unsigned h[TK_BINS];
+  if (k_dev) k = *k_dev;
+  const int bstar = tk_boundary(sc->hist, s1);
+  for (int i = threadIdx.x; i < TK_BINS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const unsigned ref = static_cast<unsigned>(sc->maxkey >> 47);
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_r; r += gridDim.x * blockDim.x) {
+    if (pos[r] < k) continue;
+    const unsigned long long key = dkey(d[r]);
+    if (tk_bin(key, ref) == bstar) atomicAdd(&h[tk_sub(key)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < TK_BINS; i += blockDim.x)
+    if (h[i]) atomicAdd(&sc->hist2[i], h[i]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->sure0 = sc->sure_cnt;
+    sc->refine_ran = 1u;
+  }
+}
+
+// ... and split it: sub-bins before the refined boundary join the sure rows,
+// the boundary sub-bin becomes the (short) boundary list bnd2.
+__global__ void __launch_bounds__(256) topk_compact2_kernel(const double* d, const int* pos, int n_r, int k,
+                                                            const int* k_dev, int s1, TopkScratch* sc) {
+  if (sc->bnd_cnt <= static_cast<unsigned>(TK_BCAP)) return;
+  if (k_dev) k = *k_dev;
+  const int bstar = tk_boundary(sc->hist, s1);
+  const int b2 = tk_boundary(sc->hist2, s1 - static_cast<int>(sc->sure0));
+  const unsigned ref = static_cast<unsigned>(sc->maxkey >> 47);
+  const int lane = threadIdx.x & 31;
+  const int n_it = (n_r + gridDim.x * blockDim.x - 1) / (gridDim.x * blockDim.x);
+  for (int it = 0; it < n_it; ++it) {
+    const int r = (it * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+    bool sure = false, bnd = false;
+    double v = 0.0;
+    int pr = 0;
+    if (r < n_r) {
+      pr = pos[r];
+      if (pr >= k) {
+        v = d[r];
+        const unsigned long long key = dkey(v);
+        if (tk_bin(key, ref) == bstar) {
+          const int sb = tk_sub(key);
+          sure = sb < b2;
+          bnd = sb == b2;
+        }
+      }
+    }
+    const unsigned ms = __ballot_sync(0xffffffffu, sure), mb = __ballot_sync(0xffffffffu, bnd);
+    unsigned bs = 0, bb = 0;
+    if (lane == 0) {
+      if (ms) bs = atomicAdd(&sc->sure_cnt, __popc(ms));
+      if (mb) bb = atomicAdd(&sc->bnd2_cnt, __popc(mb));
+    }
+    bs = __shfl_sync(0xffffffffu, bs, 0);
+    bb = __shfl_sync(0xffffffffu, bb, 0);
+    const unsigned below = (1u << lane) - 1u;
+    if (sure) {
+      const unsigned idx = bs + __popc(ms & below);
+      if (idx < TK_SCAP) sc->sure[idx] = Ent{v, pr, r};
+    }
+    if (bnd) {
+      const unsigned idx = bb + __popc(mb & below);
+      if (idx < TK_BCAP) sc->bnd2[idx] = Ent{v, pr, r};
+    }
+  }
+}
+
 // One CTA (TK_FINAL threads): rank, sort, write `out` (s1 entries), reset.
 constexpr int TK_FINAL = 1024;
 __global__ void __launch_bounds__(TK_FINAL) topk_final_kernel(const double* d, const int* pos, int n_r, int k,
@@ -214,12 +296,18 @@ __global__ void __launch_bounds__(TK_FINAL) topk_final_kernel(const double* d, c
   __shared__ int nwin_s;
   if (k_dev) k = *k_dev;
   const int tid = threadIdx.x;
-  const int c0 = min(static_cast<int>(sc->sure_cnt), s1);
-  const int nb = static_cast<int>(sc->bnd_cnt);
+  // a refined boundary (topk_compact2) replaces an over-full one; a
+  // refinement that still overflows (massive exact ties) falls back to the
+  // chunked scan below on the pass-1 sure rows only
+  const bool ran = sc->refine_ran != 0u;
+  const bool refined = ran && sc->bnd2_cnt > 0u && sc->bnd2_cnt <= static_cast<unsigned>(TK_BCAP);
+  const int c0 = min(static_cast<int>(ran && !refined ? sc->sure0 : sc->sure_cnt), s1);
+  const int nb = static_cast<int>(refined ? sc->bnd2_cnt : sc->bnd_cnt);
+  const Ent* bl = refined ? sc->bnd2 : sc->bnd;
   const int need = min(s1 - c0, nb);
   for (int i = tid; i < c0; i += blockDim.x) win[i] = sc->sure[i];
   if (nb <= TK_BCAP) {
-    for (int i = tid; i < nb; i += blockDim.x) cand[i] = sc->bnd[i];
+    for (int i = tid; i < nb; i += blockDim.x) cand[i] = bl[i];
     __syncthreads();
     for (int i = tid; i < nb; i += blockDim.x) {
       const Ent e = cand[i];
@@ -289,10 +377,15 @@ __global__ void __launch_bounds__(TK_FINAL) topk_final_kernel(const double* d, c
   for (int i = nw + tid; i < s1; i += blockDim.x) out[i] = ent_none();
   // reset the scratch for the next call
   for (int i = tid; i < TK_BINS; i += blockDim.x) sc->hist[i] = 0;
+  if (ran)
+    for (int i = tid; i < TK_BINS; i += blockDim.x) sc->hist2[i] = 0;
+  __syncthreads();
   if (tid == 0) {
     sc->maxkey = 0;
     sc->sure_cnt = 0;
     sc->bnd_cnt = 0;
+    sc->bnd2_cnt = 0;
+    sc->refine_ran = 0u;
   }
 }
 
@@ -674,6 +767,11 @@ cudaError_t select_topk(cudaStream_t st, const double* d, const int* pos, int n_
   topk_max_kernel<<<grid, 256, 0, st>>>(d, pos, n_r, k, k_dev, sc); count_launches(1);
   topk_hist_kernel<<<grid, 256, 0, st>>>(d, pos, n_r, k, k_dev, sc); count_launches(1);
   topk_compact_kernel<<<grid, 256, 0, st>>>(d, pos, n_r, k, k_dev, s1, sc); count_launches(1);
+  if (n_r > 200000) {  // a boundary bin over TK_BCAP rows is refined on the device (the kernels exit otherwise)
+    topk_hist2_kernel<<<grid, 256, 0, st>>>(d, pos, n_r, k, k_dev, s1, sc);
+    topk_compact2_kernel<<<grid, 256, 0, st>>>(d, pos, n_r, k, k_dev, s1, sc);
+    count_launches(2);
+  }
   const size_t smem = (TK_SCAP + TK_BCAP) * sizeof(Ent);
   cudaError_t e = cudaFuncSetAttribute(topk_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

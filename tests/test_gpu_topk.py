@@ -2,7 +2,8 @@
 position asc among the unselected positions) against a numpy sort — the
 reference's strict '>' scan order (linalg.hpp:45-47) — including exact ties,
 ties across the boundary, NaN residuals, fewer eligible rows than s+1 and a
-boundary bin holding most of the grid (the chunked tie path)."""
+boundary bin holding most of the grid (the sub-bin refinement above 2e5
+rows, the chunked tie path)."""
 import numpy as np
 import pytest
 
@@ -31,7 +32,11 @@ def _run(d, pos, k, s1):
 @pytest.mark.parametrize("n_r,k,s1,mode", [
     (110592, 0, 129, "random"), (110592, 5000, 129, "random"), (4096, 100, 65, "ties"),
     (50000, 0, 129, "allequal"), (300, 250, 129, "few"), (20000, 10, 33, "nan"), (1, 0, 1, "random"),
-    (70000, 0, 129, "boundary"), (12345, 7, 129, "negative")])
+    (70000, 0, 129, "boundary"), (12345, 7, 129, "negative"),
+    # above 2e5 rows an over-full boundary bin is refined by the next 12 key
+    # bits (split: "boundary"; exact ties defeat it and take the chunked scan)
+    (300000, 0, 129, "boundary"), (300000, 1000, 129, "ties"), (300000, 0, 129, "allequal"),
+    (900000, 300, 129, "random")])
 def test_topk_matches_sort(n_r, k, s1, mode):
     rng = np.random.default_rng(n_r + k + s1)
     pos = rng.permutation(n_r).astype(np.int32)
