@@ -692,6 +692,7 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
   // the cache: one Theta-sized block cycles L -> spectrum -> L across builds)
   DBuf L = dalloc(c, std::max((size_t)n_r * std::max(steps, 1), keep ? keep->min_l_elems : 0));
   DBuf wsel;  // W columns of the accepted pivots (only the three-launch fallback materialises them)
+  DBuf xperm;  // X with permuted column groups for the TMA panel (panel4.cu)
   DBuf amu = dalloc(c, (size_t)lds * n1), bmu = dalloc(c, (size_t)lds * n2);
   DBuf lrow = dalloc(c, (size_t)lds * std::max(steps, 1));       // L rows of candidates / pivots
   DBuf wcc = dalloc(c, (size_t)s * s), xcol = dalloc(c, (size_t)s * s);
@@ -780,9 +781,12 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
        "hadamard_gemm(W_CC)");
     if (k > 0)
       gemm(c, se, se, k, lrow.d(), lds, Lay::MN, lrow.d(), lds, Lay::MN, wcc.d(), se, -1.0, 1.0, nullptr, false, &w);
+    const bool use_panel = fused_downdate_enabled() && select_panel_enabled(n1, n2);
+    const bool use_p4 = use_panel && select_panel_tma_enabled();
+    if (use_p4 && !xperm.p) xperm = dalloc(c, (size_t)s * s);
     ck(select_cand_greedy(c->stream, n_r, se, steps, k, top.p, wcc.d(), pos.i(), perm.i(), xcol.d(), order.i(),
                           min_margin ? margin.d() : nullptr, bout, select_accept_cap(se, n_r),
-                          select_accept_round()),
+                          select_accept_round(), nullptr, nullptr, use_p4 ? xperm.d() : nullptr),
        "cand_greedy");
     int nb = 0;
     download(c, &nb, bout, sizeof(int));  // the one host sync per block
@@ -794,12 +798,17 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
     const int ldb_ = nb + (nb & 1);
     ck(gather_rows3(c->stream, a, lda, n1, b, ldb, n2, L.d(), n_r, k, srow, nb, amu.d(), bmu.d(), lrow.d(), ldb_),
        "gather");
-    // one launch (panel.cu): W_sel, L[:, k:k+nb] = W_sel X^T and the downdate
-    const cudaError_t pe =
-        (fused_downdate_enabled() && select_panel_enabled(n1, n2))
-            ? select_panel(c->stream, n_r, nb, a, lda, amu.d(), ldb_, n1, b, ldb, bmu.d(), ldb_, n2, L.d(), n_r,
-                           lrow.d(), ldb_, k, xcol.d(), se, L.d() + (size_t)k * n_r, n_r, d.d(), pos.i(), k + nb)
-            : cudaErrorNotSupported;
+    // one launch (panel4.cu on the TMA engine, else panel.cu): W_sel,
+    // L[:, k:k+nb] = W_sel X^T and the downdate
+    cudaError_t pe = cudaErrorNotSupported;
+    if (use_p4)
+      pe = select_panel_tma(c->stream, n_r, nb, a, lda, amu.d(), ldb_, n1, b, ldb, bmu.d(), ldb_, n2, L.d(), n_r,
+                            lrow.d(), ldb_, k, xperm.d(), se, L.d() + (size_t)k * n_r, n_r, d.d(), pos.i(), k + nb);
+    if (pe == cudaErrorNotSupported && use_panel) {
+      cudaGetLastError();
+      pe = select_panel(c->stream, n_r, nb, a, lda, amu.d(), ldb_, n1, b, ldb, bmu.d(), ldb_, n2, L.d(), n_r,
+                        lrow.d(), ldb_, k, xcol.d(), se, L.d() + (size_t)k * n_r, n_r, d.d(), pos.i(), k + nb);
+    }
     if (pe != cudaErrorNotSupported) {
       ck(pe, "select_panel");
       k += nb;

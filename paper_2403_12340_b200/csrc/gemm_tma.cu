@@ -117,6 +117,10 @@ using H4 = Gemm4Cfg<64, BN, 32, 32, kBK, 4, true, 1>;
 
 }  // namespace
 
+bool tma_encode_mn(void* map, const double* ptr, long long rows, long long cols, long long ld, int bk) {
+  return encode_mn(static_cast<CUtensorMap*>(map), ptr, rows, cols, ld, bk);
+}
+
 int dgemm_tma_k_tile(int m) { return kcfg(m) == 1 ? K4P::BM : kcfg(m) == 2 ? K4S::BM : K4::BM; }
 int dgemm_tma_k_per_sm(int m) { return kcfg(m) == 2 ? K4S::MINB : 1; }
 

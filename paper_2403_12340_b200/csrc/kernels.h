@@ -31,6 +31,8 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
 // back to the cp.async engines). Enabled with LRGW_TMA=1.
 bool tma_gemm_enabled();
 bool tma_tall_enabled();  // tall-skinny widths 33..112 on the TMA engine (LRGW_TMA_TALL=0: off)
+// map: a CUtensorMap (cuda.h) of a column-major rows x cols matrix, boxes {16 rows, bk cols}, 128 B swizzle
+bool tma_encode_mn(void* map, const double* ptr, long long rows, long long cols, long long ld, int bk);
 cudaError_t dgemm_tma(cudaStream_t st, int M, int N, int K, const double* A, long long lda, const double* B,
                       long long ldb, double* C, long long ldc, double alpha, double beta, bool tri_b,
                       const int* colmap, const int* n_dev);
@@ -64,6 +66,14 @@ cudaError_t dgemm_tall_downdate(cudaStream_t st, int M, int N, int K, const doub
 // d[m] -= sum_n C(m, n)^2 where pos[m] >= kend. cudaErrorNotSupported when the
 // shape / alignment is not covered (callers run the three-launch path).
 bool select_panel_enabled(int n1, int n2);
+// The panel on the TMA engine (panel4.cu): X given with its columns permuted
+// inside 16-groups (select_cand_greedy's xperm); N <= 112.
+bool select_panel_tma_enabled();
+cudaError_t select_panel_tma(cudaStream_t st, int M, int N, const double* a1, long long lda1, const double* b1,
+                             long long ldb1, int k1, const double* a2, long long lda2, const double* b2,
+                             long long ldb2, int k2, const double* l, long long ldl, const double* lrow,
+                             long long ldlr, int k, const double* xperm, long long ldx, double* c, long long ldc,
+                             double* d, const int* pos, int kend);
 // Device-driven form (k_dev != nullptr): k = *k_dev, N = *n_dev (<= the N
 // given, which sizes the tile), c is the factor's column 0 (the block writes
 // columns k .. k + N) and kend = k + N.

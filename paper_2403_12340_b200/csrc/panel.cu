@@ -308,15 +308,16 @@ bool aligned16p(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) ==
 
 }  // namespace
 
-// LRGW_PANEL=0 / 1 forces the choice; by default the fused panel runs where its
-// fixed per-CTA cost pays (short Hadamard K: Si64, C60), and the three TMA
-// launches where the long K phases dominate (measured per block,
-// profiles/r02/panel_vs_3launch.txt: Si64 every block faster fused, Si512
-// every block faster on the TMA family).
+// LRGW_PANEL=0 / 1 forces the choice. By default the fused panel runs where
+// it beats the three TMA launches (measured, profiles/r02/): on the TMA
+// engine (panel4.cu) up to a Hadamard depth N_v + N_c of 1024 — Si64 select
+// 10.11 -> 9.40 ms, C60 41.9 -> 35.2 ms, Si216 229.5 -> 223.3 ms — but not
+// at Si512's 2048 (2799 vs 2739 ms); the cp.async panel (panel.cu) only up to
+// 512.
 bool select_panel_enabled(int n1, int n2) {
   static const int v = getenv("LRGW_PANEL") ? atoi(getenv("LRGW_PANEL")) : -1;
   if (v >= 0) return v != 0;
-  return n1 + n2 <= 512;
+  return n1 + n2 <= (select_panel_tma_enabled() ? 1024 : 512);
 }
 
 cudaError_t select_panel(cudaStream_t st, int M, int N, const double* a1, long long lda1, const double* b1,

@@ -403,6 +403,7 @@ struct CandParams {
   int* pos;             // grid row -> position
   int* perm;            // position -> grid row
   double* xcol;         // s x s, ld s: X = L_sel^-1 column-major (b x b lower, zero above)
+  double* xperm;        // optional: X again with its columns permuted inside 16-groups (panel4.cu)
   int* piv_order;       // [steps]
   double* margin;       // [steps] or nullptr
   int* b_out;           // number of accepted steps
@@ -472,7 +473,8 @@ __device__ __forceinline__ void cand_argmax(const double (&dj)[4], const int (&p
 //   the diagonal blocks are inverted by one warp each (lane = column,
 //   unrolled forward substitution with reciprocal pivots), then block row I
 //   takes X_Ik = -X_II sum_{m=k}^{I-1} L_Im X_mk (k < I) — all threads.
-__device__ void cand_tri_inverse(double* lcs, double* lsel, const int* sel, int b, int s, double* xcol) {
+__device__ void cand_tri_inverse(double* lcs, double* lsel, const int* sel, int b, int s, double* xcol,
+                                 double* xperm) {
   __shared__ double rdiag[CG_MAX];
   double* X = lcs;  // L_sel (packed lower in lsel) is the identity beyond b
   for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
@@ -534,7 +536,13 @@ __device__ void cand_tri_inverse(double* lcs, double* lsel, const int* sel, int 
   // M'[sel[j]][i] = X[i][j] (i >= j); the rows of unselected candidates stay 0
   for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
     const int i = idx / b, j = idx % b;
-    if (j <= i) xcol[i + (size_t)j * s] = X[i * CG_MAX + j];
+    if (j <= i) {
+      xcol[i + (size_t)j * s] = X[i * CG_MAX + j];
+      if (xperm) {  // column j at 16 (j / 16) + 8 ((jl >> 1) & 1) + 2 (jl >> 2) + (jl & 1), jl = j % 16
+        const int jl = j & 15, jm = (j & ~15) + 8 * ((jl >> 1) & 1) + 2 * (jl >> 2) + (jl & 1);
+        xperm[i + (size_t)jm * s] = X[i * CG_MAX + j];
+      }
+    }
   }
 }
 
@@ -570,7 +578,10 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
   __shared__ int rec_gp[CG_MAX], rec_occ[CG_MAX], rec_pp[CG_MAX];
   __shared__ double rec_mg[CG_MAX];
 
-  for (int idx = threadIdx.x; idx < s * s; idx += blockDim.x) p.xcol[idx] = 0.0;
+  for (int idx = threadIdx.x; idx < s * s; idx += blockDim.x) {
+    p.xcol[idx] = 0.0;
+    if (p.xperm) p.xperm[idx] = 0.0;
+  }
 
   const double tau = p.top[s].row >= 0 ? p.top[s].v : -DBL_MAX;
   __shared__ int tmax_s;  // read from smem on the controller's path (keeps it out of the register budget)
@@ -716,7 +727,7 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
       if (want_sv) p.margin[k] = rec_mg[q];
     }
   }
-  cand_tri_inverse(lcs, lsel, sel, b, s, p.xcol);
+  cand_tri_inverse(lcs, lsel, sel, b, s, p.xcol, p.xperm);
   if (threadIdx.x == 0) {
     p.b_out[0] = b;
     p.b_out[1] = kb + b;  // next block start, consumed on the device
@@ -806,10 +817,10 @@ int select_accept_round() {
 
 cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* wcc,
                                int* pos, int* perm, double* xcol, int* piv_order, double* margin, int* b_out,
-                               int bmax, int bround, const int* kb_dev, int* k_next) {
+                               int bmax, int bround, const int* kb_dev, int* k_next, double* xperm) {
   const Ent* tp = static_cast<const Ent*>(top);
-  CandParams p{n_r,  s,    steps, kb,        std::max(1, bmax), bround, tp,     wcc,
-               pos,  perm, xcol,  piv_order, margin,            b_out,  kb_dev, k_next};
+  CandParams p{n_r,  s,    steps,     kb,     std::max(1, bmax), bround, tp,     wcc,   pos,
+               perm, xcol, xperm, piv_order, margin,            b_out,  kb_dev, k_next};
   const size_t smem = select_cand_smem_bytes(s);
   cudaError_t e = cudaFuncSetAttribute(cand_greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

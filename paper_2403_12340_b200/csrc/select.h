@@ -27,7 +27,8 @@ size_t select_cand_smem_bytes(int s);
 // L_sel the accepted steps' l values at the accepted rows, in pivot order).
 cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* wcc,
                                int* pos, int* perm, double* xcol, int* piv_order, double* margin, int* b_out,
-                               int bmax, int bround, const int* kb_dev = nullptr, int* k_next = nullptr);
+                               int bmax, int bround, const int* kb_dev = nullptr, int* k_next = nullptr,
+                               double* xperm = nullptr);
 // W[C, C] -= Lr Lr^T over the device-side pivot count *k_dev (Lr: s x k, ld
 // ldl; s <= 128); work: select_wcc_work_elems() doubles.
 size_t select_wcc_work_elems();
