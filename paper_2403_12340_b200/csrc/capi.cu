@@ -785,7 +785,7 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
     const bool use_p4 = use_panel && select_panel_tma_enabled();
     if (use_p4 && !xperm.p) xperm = dalloc(c, (size_t)s * s);
     ck(select_cand_greedy(c->stream, n_r, se, steps, k, top.p, wcc.d(), pos.i(), perm.i(), xcol.d(), order.i(),
-                          min_margin ? margin.d() : nullptr, bout, select_accept_cap(se, n_r),
+                          min_margin ? margin.d() : nullptr, bout, select_accept_cap(se, n_r, use_p4),
                           select_accept_round(), nullptr, nullptr, use_p4 ? xperm.d() : nullptr),
        "cand_greedy");
     int nb = 0;

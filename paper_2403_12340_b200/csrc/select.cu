@@ -805,9 +805,12 @@ int select_max_candidates() { return CG_MAX; }
 // last wave is mostly empty (profiles/r02/select_accept.txt: Si64 10.9 ->
 // 10.45 ms, Si216 255 -> 234 ms, Si512 3192 -> 2868 ms). LRGW_SELECT_ACCEPT
 // overrides (0 = all certified steps).
-int select_accept_cap(int s, int n_r) {
+// With the fused TMA panel (panel4.cu, N <= 112) the large grids take 112
+// (Si216 select 223.2 -> 218.3 ms; Si64 keeps 80: 9.39 vs 9.62-9.70 ms,
+// profiles/r02/sweep_accept_panel4.txt).
+int select_accept_cap(int s, int n_r, bool panel_tma) {
   static const int env = getenv("LRGW_SELECT_ACCEPT") ? atoi(getenv("LRGW_SELECT_ACCEPT")) : -1;
-  const int cap = env >= 0 ? env : (n_r < 200000 ? 80 : 96);
+  const int cap = env >= 0 ? env : (n_r < 200000 ? 80 : panel_tma ? 112 : 96);
   return cap > 0 ? std::min(cap, s) : s;
 }
 int select_accept_round() {

@@ -38,7 +38,7 @@ cudaError_t select_wcc_lsub(cudaStream_t st, const double* lr, long long ldl, in
 // certified greedy run): at most select_accept_cap, and a run that stops
 // between select_accept_round and the cap keeps select_accept_round — the
 // widths the tall-skinny GEMM tiles run best at.
-int select_accept_cap(int s, int n_r);
+int select_accept_cap(int s, int n_r, bool panel_tma = false);
 int select_accept_round();
 // d -= rowsum(L[:, kb:kb+b]^2) over unselected rows.
 cudaError_t select_downdate(cudaStream_t st, const double* L, int n_r, int kb, int b, const int* pos, double* d,
