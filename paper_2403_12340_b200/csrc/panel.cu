@@ -309,15 +309,15 @@ bool aligned16p(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) ==
 }  // namespace
 
 // LRGW_PANEL=0 / 1 forces the choice. By default the fused panel runs where
-// it beats the three TMA launches (measured, profiles/r02/): on the TMA
-// engine (panel4.cu) up to a Hadamard depth N_v + N_c of 1024 — Si64 select
-// 10.11 -> 9.40 ms, C60 41.9 -> 35.2 ms, Si216 229.5 -> 223.3 ms — but not
-// at Si512's 2048 (2799 vs 2739 ms); the cp.async panel (panel.cu) only up to
-// 512.
+// it beats the three launches (measured, profiles/r02/): on the TMA engine
+// (panel4.cu) at every Hadamard depth — Si64 select 10.11 -> 9.40 ms, C60
+// 41.9 -> 35.2 ms, Si216 229.5 -> 220 ms, Si512 2739 -> 2708 ms (the 96-wide
+// body loads its B halves one at a time to stay within the 2-CTA register
+// budget); the cp.async panel (panel.cu) only up to a depth of 512.
 bool select_panel_enabled(int n1, int n2) {
   static const int v = getenv("LRGW_PANEL") ? atoi(getenv("LRGW_PANEL")) : -1;
   if (v >= 0) return v != 0;
-  return n1 + n2 <= (select_panel_tma_enabled() ? 1024 : 512);
+  return select_panel_tma_enabled() || n1 + n2 <= 512;
 }
 
 cudaError_t select_panel(cudaStream_t st, int M, int N, const double* a1, long long lda1, const double* b1,

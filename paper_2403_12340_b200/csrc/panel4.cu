@@ -22,6 +22,20 @@ namespace lrgw_dev {
 
 namespace {
 
+// load_frag_swz for one k of the pair (h = 0: k = 8p + 2t, h = 1: k + 1): the
+// wide bodies load the B halves one at a time (fewer live registers)
+template <int FR, int BK>
+__device__ __forceinline__ void load_frag_swz1(const double* s, int w, int p, int h, int g, int t, double (&f)[FR]) {
+  const int k = 8 * p + 2 * t + h;
+#pragma unroll
+  for (int j = 0; j < FR / 2; ++j) {
+    const double* box = s + ((w >> 4) + j) * (BK * 16);
+    const double2 v = *reinterpret_cast<const double2*>(box + k * 16 + 2 * (g ^ (k & 7)));
+    f[2 * j] = v.x;
+    f[2 * j + 1] = v.y;
+  }
+}
+
 struct Panel4Params {
   int M, N, K1, K2, K3;
   double* C;
@@ -123,9 +137,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 2)
       const bool neg = kt >= e2;
 #pragma unroll
       for (int pp = 0; pp < BK / 8; ++pp) {
-        double a0[FM], a1_[FM], b0[FN], b1_[FN];
+        double a0[FM], a1_[FM];
         load_frag_swz<FM, BK>(sa, wm, pp, g, t, a0, a1_);
-        load_frag_swz<FN, BK>(sb, 0, pp, g, t, b0, b1_);
         if (neg) {
 #pragma unroll
           for (int i = 0; i < FM; ++i) {
@@ -133,23 +146,42 @@ __global__ void __launch_bounds__(Cfg::THREADS, 2)
             a1_[i] = -a1_[i];
           }
         }
-        dmma_block<FM, FN>(acc, a0, b0);
-        dmma_block<FM, FN>(acc, a1_, b1_);
+        if constexpr (FN > 10) {
+          double bf[FN];
+          load_frag_swz1<FN, BK>(sb, 0, pp, 0, g, t, bf);
+          dmma_block<FM, FN>(acc, a0, bf);
+          load_frag_swz1<FN, BK>(sb, 0, pp, 1, g, t, bf);
+          dmma_block<FM, FN>(acc, a1_, bf);
+        } else {
+          double b0[FN], b1_[FN];
+          load_frag_swz<FN, BK>(sb, 0, pp, g, t, b0, b1_);
+          dmma_block<FM, FN>(acc, a0, b0);
+          dmma_block<FM, FN>(acc, a1_, b1_);
+        }
       }
     } else {
       // phase 4, W columns 16 q .. 16 q + 15: k-step (pp, h) <- W column 16 q + 4 t + 2 pp + h
       const int q = kt - e3;
 #pragma unroll
       for (int pp = 0; pp < BK / 8; ++pp) {
-        double a0[FM], a1_[FM], b0[FN], b1_[FN];
-        load_frag_swz<FN, BK>(sb, 0, pp, g, t, b0, b1_);
+        double a0[FM], a1_[FM];
 #pragma unroll
         for (int i = 0; i < FM; ++i) {
           a0[i] = park[((i * FN + 2 * q) * 2 + pp) * CT];
           a1_[i] = park[((i * FN + 2 * q + 1) * 2 + pp) * CT];
         }
-        dmma_block<FM, FN>(acc, a0, b0);
-        dmma_block<FM, FN>(acc, a1_, b1_);
+        if constexpr (FN > 10) {
+          double bf[FN];
+          load_frag_swz1<FN, BK>(sb, 0, pp, 0, g, t, bf);
+          dmma_block<FM, FN>(acc, a0, bf);
+          load_frag_swz1<FN, BK>(sb, 0, pp, 1, g, t, bf);
+          dmma_block<FM, FN>(acc, a1_, bf);
+        } else {
+          double b0[FN], b1_[FN];
+          load_frag_swz<FN, BK>(sb, 0, pp, g, t, b0, b1_);
+          dmma_block<FM, FN>(acc, a0, b0);
+          dmma_block<FM, FN>(acc, a1_, b1_);
+        }
       }
     }
     __syncwarp();
