@@ -183,6 +183,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   const int wm = (warp % Cfg::WARPS_M) * Cfg::WM, wn = (warp / Cfg::WARPS_M) * Cfg::WN;
   const int g = lane >> 2, t = lane & 3;
   const bool live = n0 + wn < N;
+  // leading k-tiles that are zero for this warp's columns (triangular B)
+  const int kz = p.tri_b ? max(0, (n0 + wn - kb) / BK) : 0;
   double acc[FM][FN][2];
   double first[Cfg::HAD ? FM : 1][Cfg::HAD ? FN : 1][2];
 #pragma unroll
@@ -206,8 +208,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     // triangular B: a k-tile wholly left of the warp's first column is zero
     // for the whole warp (the tile-level skip only starts K at n0) — skip its
     // MMAs (exact: the skipped products are zeros)
-    const bool zero_k = p.tri_b && kt < kt1 && kb + (kt + 1) * BK <= n0 + wn;
-    if (live && !zero_k) {
+    if (live && kt >= kz) {
       const double* sa = ring + s * Cfg::STAGE_ELEMS;
       const double* sb = sa + Cfg::A_BOXES * Cfg::BOX;
 #pragma unroll
