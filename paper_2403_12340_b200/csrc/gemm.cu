@@ -392,6 +392,23 @@ cudaError_t dispatch2(cudaStream_t st, const Dgemm2Params& p, bool had) {
 
 }  // namespace
 
+cudaError_t dgemm_batched(cudaStream_t st, int batch, int M, int N, int K, const double* A, long long lda,
+                          long long bsa, Lay la, const double* B, long long ldb, long long bsb, Lay lb, double* C,
+                          long long ldc, long long bsc, double alpha, double beta, bool tri_b) {
+  if (M <= 0 || N <= 0 || batch <= 0) return cudaSuccess;
+  DgemmParams p{};
+  p.M = M, p.N = N, p.K = K, p.A = A, p.lda = lda, p.B = B, p.ldb = ldb, p.C = C, p.ldc = ldc;
+  p.alpha = alpha, p.beta = beta, p.tri_b = tri_b ? 1 : 0;
+  p.batch = batch, p.bsa = bsa, p.bsb = bsb, p.bsc = bsc;
+  const bool ak = la == Lay::K, bk = lb == Lay::K;
+  const bool va = aligned16(A) && lda % 2 == 0 && bsa % 2 == 0 && (ak ? K % 2 == 0 : (M % 2 == 0 || lda > M));
+  const bool vb = aligned16(B) && ldb % 2 == 0 && bsb % 2 == 0 && (bk ? K % 2 == 0 : (N % 2 == 0 || ldb > N));
+  if (!ak && !bk) return launch_layout<false, false>(st, p, Tile::S, va, vb, batch);
+  if (!ak && bk) return launch_layout<false, true>(st, p, Tile::S, va, vb, batch);
+  if (ak && !bk) return launch_layout<true, false>(st, p, Tile::S, va, vb, batch);
+  return launch_layout<true, true>(st, p, Tile::S, va, vb, batch);
+}
+
 cudaError_t gather_rows3(cudaStream_t st, const double* a, long long lda, int n1, const double* b, long long ldb,
                         int n2, const double* l, long long ldl, int nl, const int* rows, int n_rows, double* da,
                         double* db, double* dl, long long ldd, const int* nl_dev, const int* nrows_dev,

@@ -40,6 +40,8 @@ struct DgemmParams {
   const double* Cin;     // if set: the beta term reads Cin[m + cin_map[n] ldcin] instead of C
   long long ldcin;
   const int* cin_map;
+  int batch;             // > 1: gridDim.z runs independent products at A + z bsa, B + z bsb, C + z bsc
+  long long bsa, bsb, bsc;
 };
 
 // Tile loader for one operand. ROWS = BM or BN.
@@ -119,6 +121,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) dgemm_kernel(DgemmPar
     const int nd = *p.n_dev;
     if (nd < p.N) p.N = nd;
     if (n0 >= p.N) return;
+  }
+  if (p.batch > 1) {
+    p.A += blockIdx.z * p.bsa;
+    p.B += blockIdx.z * p.bsb;
+    p.C += blockIdx.z * p.bsc;
   }
   const int kb = p.k_chunk > 0 ? blockIdx.z * p.k_chunk : (p.tri_b ? (n0 / BK) * BK : 0);
   const int ke = p.k_chunk > 0 ? min(p.K, kb + p.k_chunk) : p.K;

@@ -26,6 +26,12 @@ cudaError_t dgemm(cudaStream_t st, int M, int N, int K, const double* A, long lo
                   const int* n_dev = nullptr, const double* cin = nullptr, long long ldcin = 0,
                   const int* cin_map = nullptr);
 
+// `batch` independent products C_z = alpha A_z B_z^T + beta C_z with A_z = A + z bsa
+// (likewise B, C), one launch (64 x 64 tiles): the small GEMMs of a recursion level.
+cudaError_t dgemm_batched(cudaStream_t st, int batch, int M, int N, int K, const double* A, long long lda,
+                          long long bsa, Lay la, const double* B, long long ldb, long long bsb, Lay lb, double* C,
+                          long long ldc, long long bsc, double alpha, double beta, bool tri_b);
+
 // TMA-fed engine (gemm4.cuh / gemm_tma.cu) for MN-contiguous operands:
 // cudaErrorNotSupported when a shape / alignment is not covered (callers fall
 // back to the cp.async engines). Enabled with LRGW_TMA=1.

@@ -107,7 +107,7 @@ __global__ void tril_copy_kernel(const double* src, long long lds, double* dst, 
 
 }  // namespace
 
-size_t trtri_work_elems(int n) { return (size_t)n * n + (size_t)n * n / 2 + 64; }
+size_t trtri_work_elems(int n) { return 2 * (size_t)n * n + 64; }
 
 cudaError_t trtri_lower(cudaStream_t st, double* a_in, int n, long long lda_in, double* work, int* bad,
                         int sm_count) {
@@ -124,18 +124,36 @@ cudaError_t trtri_lower(cudaStream_t st, double* a_in, int n, long long lda_in, 
   if (e != cudaSuccess) return e;
   trtri_leaf_kernel<<<leaves, LEAF_THREADS, smem, st>>>(a, n, lda, bad); count_launches(1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  // levels: pairs of inverted b-blocks become inverted 2b-blocks
+  // levels: pairs of inverted b-blocks become inverted 2b-blocks; the full
+  // pairs of a level are independent and run as ONE batched launch per
+  // product (the small levels are latency-bound: 8 + 4 launches of 12-19 us
+  // at N_mu 1024 become 2 + 2), a ragged last pair separately
   for (int b = LEAF; b < n; b *= 2) {
-    for (int r0 = 0; r0 + b < n; r0 += 2 * b) {
-      const int r1 = r0 + b, b2 = std::min(b, n - r1);
+    const long long step = 2LL * b * (lda + 1);  // pair to pair along the diagonal
+    int full = 0;
+    while ((full + 1) * 2 * b <= n) ++full;      // pairs with b2 == b
+    if (full > 0) {
+      double* x11 = a;
+      double* l21 = a + b;
+      double* x22 = a + b + (long long)b * lda;
+      // T_z = L21_z X11_z (b x b), X11 lower: B(n, k) = X11(k, n) is zero for k < n
+      e = dgemm_batched(st, full, b, b, b, l21, lda, step, Lay::MN, x11, lda, step, Lay::K, work, b, (long long)b * b,
+                        1.0, 0.0, true);
+      if (e != cudaSuccess) return e;
+      // X21_z = -X22_z T_z
+      e = dgemm_batched(st, full, b, b, b, x22, lda, step, Lay::MN, work, b, (long long)b * b, Lay::K, l21, lda, step,
+                        -1.0, 0.0, false);
+      if (e != cudaSuccess) return e;
+    }
+    const int r0 = full * 2 * b;
+    if (r0 + b < n) {  // the ragged pair (b2 < b)
+      const int r1 = r0 + b, b2 = n - r1;
       double* x11 = a + r0 + (long long)r0 * lda;
       double* l21 = a + r1 + (long long)r0 * lda;
       double* x22 = a + r1 + (long long)r1 * lda;
-      // T = L21 X11 (b2 x b), X11 lower: B(n, k) = X11(k, n) is zero for k < n
       e = dgemm(st, b2, b, b, l21, lda, Lay::MN, x11, lda, Lay::K, work, b2, 1.0, 0.0, nullptr, false, sm_count,
                 nullptr, 0, true);
       if (e != cudaSuccess) return e;
-      // X21 = -X22 T (X22 lower: A(m, k) = 0 for k > m; the engine streams it densely)
       e = dgemm(st, b2, b, b2, x22, lda, Lay::MN, work, b2, Lay::K, l21, lda, -1.0, 0.0, nullptr, false, sm_count,
                 nullptr, 0);
       if (e != cudaSuccess) return e;
