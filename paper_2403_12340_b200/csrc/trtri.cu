@@ -4,10 +4,10 @@
 // Recursive 2 x 2 blocking on the DMMA GEMM engine:
 //   [L11  0 ]^-1   [ X11            0  ]
 //   [L21 L22]    = [ -X22 L21 X11   X22 ],
-// bottom-up from 128 x 128 diagonal leaves inverted one CTA each (32 x 32
+// bottom-up from 64 x 64 diagonal leaves inverted one CTA each (32 x 32
 // diagonal blocks by one warp per block — lane = column, unrolled forward
 // substitution with reciprocal pivots — then the leaf's block rows), then
-// levels 128, 256, ... with two GEMMs per block pair. log2(N / 128) levels,
+// levels 64, 128, ... with two (batched) GEMMs per level. log2(N / 64) levels,
 // all compute on tensor cores; replaces cuSOLVER's trsm / trmm cascade.
 #include <cfloat>
 
@@ -18,7 +18,7 @@ namespace lrgw_dev {
 
 namespace {
 
-constexpr int LEAF = 128;
+constexpr int LEAF = 64;
 constexpr int LEAF_THREADS = 512;
 
 // One CTA per diagonal leaf q: a[q LEAF + i, q LEAF + j] (size nb <= LEAF).
