@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_trtri.py tests/test_gpu_build.py tests/test_gpu_implicit.py -x -q 2>&1 | tail -2
-( SWEEP_REPS=3 timeout 900 python tools/env_sweep.py si64 ''
-  SWEEP_REPS=2 timeout 900 python tools/env_sweep.py c60 '' ) 2>&1 | grep -v Warn | cut -c1-160
+timeout 1200 python -m pytest tests/test_gpu_dist.py -x -q -rf 2>&1 | tail -2
+timeout 600 python bench.py --config si64 --mode sharded --steps 10 --warmup 3 --no-cpu-baseline 2>&1 | grep '^{' | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('sharded x1', d['value'], d['stages_ms'])"

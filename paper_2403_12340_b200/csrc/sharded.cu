@@ -236,7 +236,8 @@ PanelSelect select_panel(lrgw_ctx c, lrgw_comm m, const Panels& pn, const double
   ps.L = dalloc(c, (size_t)rows * std::max(steps, 1));
   const int wmax = n1 + n2 + steps;
   DBuf rowbuf = dalloc(c, (size_t)lds * wmax), pick = dalloc(c, (size_t)lds * wmax);
-  DBuf wsel = dalloc(c, (size_t)rows * s), wcc = dalloc(c, (size_t)s * s), xcol = dalloc(c, (size_t)s * s);
+  DBuf wcc = dalloc(c, (size_t)s * s), xcol = dalloc(c, (size_t)s * s);
+  DBuf wsel, xperm;  // the three-launch fallback's W columns / the TMA panel's permuted X (allocated on use)
   const size_t eb = select_ent_bytes();
   DBuf top_loc(c, eb * (s + 1)), gathered(c, eb * (s + 1) * world), top(c, eb * (s + 1));
   DBuf tmp(c, select_topk_tmp_bytes(rows, s + 1));
@@ -262,9 +263,12 @@ PanelSelect select_panel(lrgw_ctx c, lrgw_comm m, const Panels& pn, const double
     ck(hadamard_gemm(c->stream, se, se, amu, lds, amu, lds, n1, bmu, lds, bmu, lds, n2, wcc.d(), se, 1.0, 0.0),
        "hadamard_gemm(W_CC)");
     if (k > 0) gemm(c, se, se, k, lrow, lds, Lay::MN, lrow, lds, Lay::MN, wcc.d(), se, -1.0, 1.0, nullptr, false, &w);
+    const bool use_panel = fused_downdate_enabled() && select_panel_enabled(n1, n2);
+    const bool use_p4 = use_panel && select_panel_tma_enabled();
+    if (use_p4 && !xperm.p) xperm = dalloc(c, (size_t)s * s);
     ck(select_cand_greedy(c->stream, n_r, se, steps, k, top.p, wcc.d(), pos.i(), perm.i(), xcol.d(), order.i(),
-                          margin.d(), bout.i(), select_accept_cap(se, n_r),
-                          select_accept_round()),
+                          margin.d(), bout.i(), select_accept_cap(se, n_r, use_p4), select_accept_round(), nullptr,
+                          nullptr, use_p4 ? xperm.d() : nullptr),
        "cand_greedy");
     int nb = 0;
     download(c, &nb, bout.p, sizeof(int));  // the one host sync per block
@@ -276,10 +280,28 @@ PanelSelect select_panel(lrgw_ctx c, lrgw_comm m, const Panels& pn, const double
     const double* asel = pick.d();
     const double* bsel = asel + (size_t)ldp * n1;
     const double* lsel = bsel + (size_t)ldp * n2;
+    double* lblk = ps.L.d() + (size_t)k * rows;
+    // the fused panel (panel4.cu / panel.cu) on this rank's rows, as in the one-GPU loop
+    cudaError_t pe = cudaErrorNotSupported;
+    if (use_p4)
+      pe = select_panel_tma(c->stream, rows, nb, a, lda, asel, ldp, n1, b, ldb, bsel, ldp, n2, ps.L.d(), rows, lsel,
+                            ldp, k, xperm.d(), se, lblk, rows, d.d(), pos.i() + row0, k + nb);
+    if (pe == cudaErrorNotSupported && use_panel) {
+      cudaGetLastError();
+      pe = lrgw_dev::select_panel(c->stream, rows, nb, a, lda, asel, ldp, n1, b, ldb, bsel, ldp, n2, ps.L.d(), rows,
+                                  lsel, ldp, k, xcol.d(), se, lblk, rows, d.d(), pos.i() + row0, k + nb);
+    }
+    if (pe != cudaErrorNotSupported) {
+      ck(pe, "select_panel");
+      k += nb;
+      ++ps.blocks;
+      continue;
+    }
+    cudaGetLastError();
+    if (!wsel.p) wsel = dalloc(c, (size_t)rows * s);
     ck(hadamard_gemm(c->stream, rows, nb, a, lda, asel, ldp, n1, b, ldb, bsel, ldp, n2, wsel.d(), rows, 1.0, 0.0),
        "hadamard_gemm");
     if (k > 0) gemm(c, rows, nb, k, ps.L.d(), rows, Lay::MN, lsel, ldp, Lay::MN, wsel.d(), rows, -1.0, 1.0);
-    double* lblk = ps.L.d() + (size_t)k * rows;
     cudaError_t fe = fused_downdate_enabled() ? dgemm_tall_downdate(c->stream, rows, nb, nb, wsel.d(), rows, xcol.d(),
                                                                     se, lblk, rows, d.d(), pos.i() + row0, k + nb)
                                               : cudaErrorNotSupported;
