@@ -8,5 +8,5 @@ timeout 600 python bench.py --config si64 --steps 20 --warmup 5 > gpurun_out/ben
 timeout 600 python bench.py --config c60 --steps 5 --warmup 3 > gpurun_out/bench_c60.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_c60.log
 timeout 900 python bench.py --config si216 --steps 5 --warmup 3 > gpurun_out/bench_si216.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_si216.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_si64.csv python bench.py --config si64 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:panel_kernel -s 6 -c 1 -o gpurun_out/ncu_panel_si64 python tools/trace_build.py si64 2 > gpurun_out/ncu_panel.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:panel4_kernel -s 6 -c 1 -o gpurun_out/ncu_panel4_si64 python tools/trace_build.py si64 2 > gpurun_out/ncu_panel4.log 2>&1
 tail -n 3 gpurun_out/gpu_tests.log; tail -n 2 gpurun_out/smoke.log; grep -h '"value"' gpurun_out/bench_*.log | cut -c1-150
