@@ -1,2 +1,4 @@
-timeout 1200 python -m pytest tests/test_gpu_dist.py -x -q -rf 2>&1 | tail -2
-timeout 600 python bench.py --config si64 --mode sharded --steps 10 --warmup 3 --no-cpu-baseline 2>&1 | grep '^{' | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('sharded x1', d['value'], d['stages_ms'])"
+( SWEEP_REPS=3 timeout 900 python tools/env_sweep.py si64 '' 'LRGW_TMA_PERSIST=0'
+  SWEEP_REPS=2 timeout 900 python tools/env_sweep.py c60 ''
+  SWEEP_REPS=2 timeout 900 python tools/env_sweep.py si216 ''
+  SWEEP_REPS=2 timeout 1200 python tools/env_sweep.py si512 '' ) 2>&1 | grep -v Warn | cut -c1-110

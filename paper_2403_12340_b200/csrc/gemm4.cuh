@@ -266,6 +266,124 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     }
 }
 
+// Persistent form of dgemm4_kernel (no Hadamard phase, no device N): each CTA
+// walks a contiguous run of tiles (N tiles fastest), and the TMA
+// warp's ring runs on across tile boundaries (global k-tile count g for the
+// stage and phase), so the next tile's first boxes load during this tile's
+// epilogue — the per-tile fill / drain the one-tile-per-CTA grid pays on
+// short K (the Si64 fit: K 128..1024 by the triangular skip).
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
+    dgemm4p_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   Dgemm4Params p, int tiles_m, int tiles_n) {
+  static_assert(Cfg::PROD && !Cfg::HAD, "persistent: TMA warp, single phase");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
+  constexpr int FM = Cfg::FM, FN = Cfg::FN;
+  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * Cfg::STAGE_ELEMS);
+  uint64_t* empty = full + STAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, Cfg::CWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int ntiles = tiles_m * tiles_n, N = p.N;
+  // a contiguous run of tiles per CTA (N fastest): whole tile rows, so the
+  // triangular-B work per CTA balances and a row's A panel stays in L2
+  const int t_begin = static_cast<int>((long long)ntiles * blockIdx.x / gridDim.x);
+  const int t_end = static_cast<int>((long long)ntiles * (blockIdx.x + 1) / gridDim.x);
+  if (warp == Cfg::CWARPS) {  // ===== TMA producer =====
+    if (lane != 0) return;
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    long long gk = 0;
+    for (int tile = t_begin; tile < t_end; ++tile) {
+      const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+      const int kb = p.tri_b ? (n0 / BK) * BK : 0;
+      const int kt1 = p.K > kb ? (p.K - kb + BK - 1) / BK : 0;
+      for (int kt = 0; kt < kt1; ++kt, ++gk) {
+        const int s = static_cast<int>(gk % STAGES);
+        if (gk >= STAGES) mbar_wait(empty + s, static_cast<unsigned>(((gk / STAGES) - 1) & 1));
+        double* sa = ring + s * Cfg::STAGE_ELEMS;
+        double* sb = sa + Cfg::A_BOXES * Cfg::BOX;
+        mbar_arrive_expect_tx(full + s, Cfg::STAGE_BYTES);
+        const int k0 = kb + kt * BK;
+#pragma unroll
+        for (int b = 0; b < Cfg::A_BOXES; ++b) tma_load_2d(sa + b * Cfg::BOX, &map_a, full + s, m0 + 16 * b, k0);
+#pragma unroll
+        for (int b = 0; b < Cfg::B_BOXES; ++b) tma_load_2d(sb + b * Cfg::BOX, &map_b, full + s, n0 + 16 * b, k0);
+      }
+    }
+    return;
+  }
+  // ===== consumers =====
+  const int wm = (warp % Cfg::WARPS_M) * Cfg::WM, wn = (warp / Cfg::WARPS_M) * Cfg::WN;
+  const int g = lane >> 2, t = lane & 3;
+  long long gk = 0;
+  for (int tile = t_begin; tile < t_end; ++tile) {
+    const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+    const int kb = p.tri_b ? (n0 / BK) * BK : 0;
+    const int kt1 = p.K > kb ? (p.K - kb + BK - 1) / BK : 0;
+    const bool live = n0 + wn < N;
+    const int kz = p.tri_b ? max(0, (n0 + wn - kb) / BK) : 0;
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < kt1; ++kt, ++gk) {
+      const int s = static_cast<int>(gk % STAGES);
+      mbar_wait(full + s, static_cast<unsigned>((gk / STAGES) & 1));
+      if (live && kt >= kz) {
+        const double* sa = ring + s * Cfg::STAGE_ELEMS;
+        const double* sb = sa + Cfg::A_BOXES * Cfg::BOX;
+#pragma unroll
+        for (int pp = 0; pp < BK / 8; ++pp) {
+          double a0[FM], a1[FM], b0[FN], b1[FN];
+          load_frag_swz<FM, BK>(sa, wm, pp, g, t, a0, a1);
+          load_frag_swz<FN, BK>(sb, wn, pp, g, t, b0, b1);
+          dmma_block<FM, FN>(acc, a0, b0);
+          dmma_block<FM, FN>(acc, a1, b1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+    }
+    if (!live) continue;
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = n0 + wn + 16 * (j / 2) + 4 * t + 2 * h + (j & 1);
+        if (n >= N) continue;
+        const long long nc = p.colmap ? __ldg(p.colmap + n) : n;
+        double* col = p.C + nc * p.ldc;
+#pragma unroll
+        for (int ii = 0; ii < FM / 2; ++ii) {
+          const int m = m0 + wm + 16 * ii + 2 * g;
+          double v0 = p.alpha * acc[2 * ii][j][h], v1 = p.alpha * acc[2 * ii + 1][j][h];
+          if (p.vec_store && m + 1 < p.M) {
+            double2* c2 = reinterpret_cast<double2*>(col + m);
+            if (p.beta != 0.0) {
+              const double2 o = *c2;
+              v0 += p.beta * o.x;
+              v1 += p.beta * o.y;
+            }
+            *c2 = make_double2(v0, v1);
+          } else {
+            if (m < p.M) col[m] = p.beta != 0.0 ? v0 + p.beta * col[m] : v0;
+            if (m + 1 < p.M) col[m + 1] = p.beta != 0.0 ? v1 + p.beta * col[m + 1] : v1;
+          }
+        }
+      }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K-contiguous operands (the G-space SYRK Theta^T V Theta over the half
 // spectrum: X is 2K x n_mu with each column's k contiguous):

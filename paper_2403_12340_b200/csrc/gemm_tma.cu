@@ -160,6 +160,12 @@ cudaError_t dgemm_tma_k(cudaStream_t st, int M, int N, int K, const double* A, l
   }
 }
 
+// Persistent MN engine (dgemm4p_kernel): LRGW_TMA_PERSIST=0 / 1.
+bool persist_enabled() {
+  static const bool on = !(getenv("LRGW_TMA_PERSIST") && atoi(getenv("LRGW_TMA_PERSIST")) == 0);
+  return on;
+}
+
 bool tma_tall_enabled() {
   static const bool on = !(getenv("LRGW_TMA_TALL") && atoi(getenv("LRGW_TMA_TALL")) == 0);
   return on;
@@ -195,6 +201,19 @@ cudaError_t dgemm_tma(cudaStream_t st, int M, int N, int K, const double* A, lon
   }
   if (n_dev) return cudaErrorNotSupported;
   if (mncfg() == 1) return launch4<T4S>(st, ma, mb, ma, mb, p);
+  if (persist_enabled()) {
+    using C = T4<128>;
+    auto kern = dgemm4p_kernel<C>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    const int tm = (M + C::BM - 1) / C::BM, tn = (N + C::BN - 1) / C::BN;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int grid = std::min(tm * tn, sms * C::MINB);
+    kern<<<grid, C::THREADS, C::SMEM_BYTES, st>>>(ma, mb, p, tm, tn);
+    count_launches(1);
+    return cudaGetLastError();
+  }
   return launch4<T4<128>>(st, ma, mb, ma, mb, p);
 }
 
