@@ -1,4 +1,2 @@
-( SWEEP_REPS=3 timeout 900 python tools/env_sweep.py si64 '' 'LRGW_TMA_PERSIST=0'
-  SWEEP_REPS=2 timeout 900 python tools/env_sweep.py c60 ''
-  SWEEP_REPS=2 timeout 900 python tools/env_sweep.py si216 ''
-  SWEEP_REPS=2 timeout 1200 python tools/env_sweep.py si512 '' ) 2>&1 | grep -v Warn | cut -c1-110
+timeout 300 python tools/trace_apply2.py si64 2>&1 | grep -E "tn_|nn_|span"
+timeout 600 python -m pytest tests/test_gpu_build.py tests/test_gpu_parity.py -k "apply or build" -q -x 2>&1 | tail -1
