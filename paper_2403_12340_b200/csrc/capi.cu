@@ -667,6 +667,40 @@ int* select_pinned(lrgw_ctx c, size_t n) {
   return c->sel_pinned;
 }
 
+// The per-block read of the accepted count b: the greedy writes b into a
+// host-mapped pinned slot before its triangular-inverse tail and the host
+// spins on it, so the panel's launches are queued while the greedy is still
+// running (a cudaMemcpy + stream sync left the device idle ~30 us per block:
+// D2H, the host wake-up and the first launch after it).
+int* select_flag_arm(lrgw_ctx c) {
+  if (!c->sel_flag) {
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&c->sel_flag), 64, cudaHostAllocMapped | cudaHostAllocPortable),
+       "cudaHostAlloc");
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->sel_flag_dev), c->sel_flag, 0),
+       "cudaHostGetDevicePointer");
+  }
+  *reinterpret_cast<volatile int*>(c->sel_flag) = -1;
+  return c->sel_flag_dev;
+}
+
+int select_wait_b(lrgw_ctx c, const int* b_dev) {
+  volatile int* f = c->sel_flag;
+  for (unsigned it = 1;; ++it) {
+    const int v = *f;
+    if (v >= 0) return v;
+    if ((it & 1023u) == 0) {
+      const cudaError_t q = cudaStreamQuery(c->stream);
+      if (q == cudaErrorNotReady) continue;
+      if (q != cudaSuccess) ck(q, "select greedy");
+      // the stream drained without the slot changing: read b the slow way
+      if (*f >= 0) return *f;
+      int nb = 0;
+      download(c, &nb, b_dev, sizeof(int));
+      return nb;
+    }
+  }
+}
+
 cudaEvent_t select_event(lrgw_ctx c, int j) {
   constexpr int R = sizeof(c->sel_ev) / sizeof(c->sel_ev[0]);
   cudaEvent_t& e = c->sel_ev[j % R];
@@ -786,10 +820,10 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
     if (use_p4 && !xperm.p) xperm = dalloc(c, (size_t)s * s);
     ck(select_cand_greedy(c->stream, n_r, se, steps, k, top.p, wcc.d(), pos.i(), perm.i(), xcol.d(), order.i(),
                           min_margin ? margin.d() : nullptr, bout, select_accept_cap(se, n_r, use_p4),
-                          select_accept_round(), nullptr, nullptr, use_p4 ? xperm.d() : nullptr),
+                          select_accept_round(), nullptr, nullptr, use_p4 ? xperm.d() : nullptr,
+                          select_flag_arm(c)),
        "cand_greedy");
-    int nb = 0;
-    download(c, &nb, bout, sizeof(int));  // the one host sync per block
+    const int nb = select_wait_b(c, bout);  // the one host wait per block
     if (nb <= 0) fail(LRGW_ERR_INTERNAL, "select: no progress (non-finite residuals?)");
     if (select_trace()) fprintf(stderr, "select block k=%d se=%d b=%d\n", k, se, nb);
     // Full-length W columns of the nb accepted pivots only (grid rows
@@ -1211,6 +1245,7 @@ int lrgw_ctx_destroy(lrgw_ctx c) {
   for (auto& kv : c->plans_many) cufftDestroy(kv.second);
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->sel_pinned) cudaFreeHost(c->sel_pinned);
+  if (c->sel_flag) cudaFreeHost(c->sel_flag);
   for (auto e : c->sel_ev)
     if (e) cudaEventDestroy(e);
   if (c->side) {

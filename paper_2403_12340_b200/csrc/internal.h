@@ -56,6 +56,8 @@ struct lrgw_ctx_s {
   cudaEvent_t ev_side = nullptr, ev_join = nullptr;
   int* sel_pinned = nullptr;  // the selection's device-loop read-back slots (pinned)
   size_t sel_pinned_n = 0;
+  int* sel_flag = nullptr;      // host-mapped slot the greedy writes b into (select_wait_b)
+  int* sel_flag_dev = nullptr;  // its device address
   cudaEvent_t sel_ev[4] = {};
   int sm_count = 148;
   cusolverDnHandle_t solver = nullptr;
@@ -248,6 +250,9 @@ struct HostEnt {
   int pos, row;
 };
 bool fused_downdate_enabled();
+// the selection's per-block read of the greedy's accepted count (capi.cu)
+int* select_flag_arm(lrgw_ctx c);
+int select_wait_b(lrgw_ctx c, const int* b_dev);
 struct SelectKeep {
   DBuf L;
   std::vector<int> order;

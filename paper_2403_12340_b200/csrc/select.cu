@@ -411,6 +411,10 @@ struct CandParams {
   // *kb_dev, the next block start kb + b written to *k_next
   const int* kb_dev;
   int* k_next;
+  // optional: host-mapped pinned slot that receives b as soon as the run is
+  // decided (before the triangular inverse), so the host can enqueue the
+  // panel while this kernel finishes
+  int* b_host;
 };
 
 __device__ __forceinline__ double pick8(const double (&x)[CG_ROWS], int r) {
@@ -716,6 +720,10 @@ __global__ void __launch_bounds__(CG_THREADS, 1) cand_greedy_kernel(CandParams p
   // of bmax keeps a tile-friendly bround steps (the rest are re-found next
   // block)
   const int b = (t < tmax_s && p.bround > 0 && t >= p.bround) ? p.bround : t;
+  if (threadIdx.x == 0 && p.b_host) {
+    *reinterpret_cast<volatile int*>(p.b_host) = b;
+    __threadfence_system();
+  }
   if (threadIdx.x == 0) {
     for (int q = 0; q < b; ++q) {  // the swaps in step order
       const int k = kb + q, gp = rec_gp[q], occ = rec_occ[q], pp = rec_pp[q];
@@ -820,10 +828,10 @@ int select_accept_round() {
 
 cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* wcc,
                                int* pos, int* perm, double* xcol, int* piv_order, double* margin, int* b_out,
-                               int bmax, int bround, const int* kb_dev, int* k_next, double* xperm) {
+                               int bmax, int bround, const int* kb_dev, int* k_next, double* xperm, int* b_host) {
   const Ent* tp = static_cast<const Ent*>(top);
   CandParams p{n_r,  s,    steps,     kb,     std::max(1, bmax), bround, tp,     wcc,   pos,
-               perm, xcol, xperm, piv_order, margin,            b_out,  kb_dev, k_next};
+               perm, xcol, xperm, piv_order, margin,            b_out,  kb_dev, k_next, b_host};
   const size_t smem = select_cand_smem_bytes(s);
   cudaError_t e = cudaFuncSetAttribute(cand_greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

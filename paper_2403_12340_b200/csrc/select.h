@@ -28,7 +28,7 @@ size_t select_cand_smem_bytes(int s);
 cudaError_t select_cand_greedy(cudaStream_t st, int n_r, int s, int steps, int kb, const void* top, const double* wcc,
                                int* pos, int* perm, double* xcol, int* piv_order, double* margin, int* b_out,
                                int bmax, int bround, const int* kb_dev = nullptr, int* k_next = nullptr,
-                               double* xperm = nullptr);
+                               double* xperm = nullptr, int* b_host = nullptr);
 // W[C, C] -= Lr Lr^T over the device-side pivot count *k_dev (Lr: s x k, ld
 // ldl; s <= 128); work: select_wcc_work_elems() doubles.
 size_t select_wcc_work_elems();

@@ -268,10 +268,9 @@ PanelSelect select_panel(lrgw_ctx c, lrgw_comm m, const Panels& pn, const double
     if (use_p4 && !xperm.p) xperm = dalloc(c, (size_t)s * s);
     ck(select_cand_greedy(c->stream, n_r, se, steps, k, top.p, wcc.d(), pos.i(), perm.i(), xcol.d(), order.i(),
                           margin.d(), bout.i(), select_accept_cap(se, n_r, use_p4), select_accept_round(), nullptr,
-                          nullptr, use_p4 ? xperm.d() : nullptr),
+                          nullptr, use_p4 ? xperm.d() : nullptr, select_flag_arm(c)),
        "cand_greedy");
-    int nb = 0;
-    download(c, &nb, bout.p, sizeof(int));  // the one host sync per block
+    const int nb = select_wait_b(c, bout.i());  // the one host wait per block
     if (nb <= 0) fail(LRGW_ERR_INTERNAL, "select: no progress (non-finite residuals?)");
     // the accepted pivots' rows (they are candidates: already exchanged)
     const int ldp = nb + (nb & 1);
