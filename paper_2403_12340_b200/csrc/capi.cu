@@ -527,6 +527,18 @@ struct SmwState {
   }
 };
 
+// Device status of the fused fit, read back with the SMW status (one host
+// wait per build after the selection): diag = {min |L_ii|, max |L_ii|, ok}
+// of L_P, bad = trtri's first zero pivot + 1 (0x7f7f7f7f: none).
+struct FusedFit {
+  DBuf diag, bad;
+  double h[3] = {0.0, 0.0, 0.0};
+  int hbad = 0;
+  bool ok() const { return h[2] == 1.0 && hbad == 0x7f7f7f7f; }
+  // (max |L_ii| / min |L_ii|)^2 is a lower bound on cond(G(P, P)) = cond(L_P)^2
+  double ratio() const { return h[0] > 0.0 ? (h[1] / h[0]) * (h[1] / h[0]) : HUGE_VAL; }
+};
+
 void smw_factor_t(lrgw_ctx c, cudaStream_t st, const double* t, int n, SmwState& s) {
   const size_t nn = (size_t)n * n;
   s.stat = ialloc(c, SMW_NSTAT);
@@ -560,7 +572,9 @@ void smw_join(lrgw_ctx c, SmwState& s) {
   s.pending = nullptr;
 }
 
-void smw_finish(lrgw_ctx c, SmwState& s, const double* pvp, int n, double* k) {
+// false (and no SMW check raised): the fused fit's status in ff failed —
+// Theta, and so pvp and K, must be rebuilt on the explicit path.
+bool smw_finish(lrgw_ctx c, SmwState& s, const double* pvp, int n, double* k, FusedFit* ff = nullptr) {
   const size_t nn = (size_t)n * n;
   int* sd = s.stat.i();
   double* r = s.r.d();
@@ -594,6 +608,10 @@ void smw_finish(lrgw_ctx c, SmwState& s, const double* pvp, int n, double* k) {
   gemm(c, n, n, n, y.d(), n, Lay::MN, y.d(), n, Lay::MN, k, n, -1.0, 0.0, nullptr, true, &w);
   ck(mirror_lower(c->stream, k, n, n, false), "mirror");
   int h[SMW_NSTAT];
+  if (ff) {
+    ck(cudaMemcpyAsync(ff->h, ff->diag.p, sizeof(ff->h), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaMemcpyAsync(&ff->hbad, ff->bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  }
   download(c, h, sd, sizeof(h));
   if (c->timing) {
     float ms = 0.0f;
@@ -602,6 +620,7 @@ void smw_finish(lrgw_ctx c, SmwState& s, const double* pvp, int n, double* k) {
     if (cudaEventElapsedTime(&ms, c->ev_lib[2], c->ev_lib[3]) == cudaSuccess) lib += ms;
     c->lib_ms += lib;
   }
+  if (ff && !ff->ok()) return false;
   const int unset = 0x7f7f7f7f;
   if (h[SMW_INFO_T] != 0)
     fail(LRGW_ERR_NUMERIC, "assemble_K: T is not negative definite (gapless or rank-deficient input)");
@@ -609,6 +628,7 @@ void smw_finish(lrgw_ctx c, SmwState& s, const double* pvp, int n, double* k) {
   if (h[SMW_INFO_M] != 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", 0);
   if (h[SMW_TINY_M] >= 0) fail(LRGW_ERR_SINGULAR, "assemble_K: middle matrix singular", h[SMW_TINY_M]);
   if (h[SMW_TRTRI_BAD] != unset) fail(LRGW_ERR_SINGULAR, "trtri: singular factor", h[SMW_TRTRI_BAD] - 1);
+  return true;
 }
 
 cudaStream_t side_stream(lrgw_ctx c) {
@@ -870,18 +890,24 @@ std::vector<int32_t> select_impl(lrgw_ctx c, const double* a, long long lda, int
     k += nb;
     if (keep) ++keep->blocks;
   }
-  std::vector<int32_t> pts(n_mu);
-  download(c, pts.data(), perm.p, sizeof(int) * n_mu);
+  // one read-back (pinned) of the points, the pivot order and the margins
+  const size_t n_ord = keep ? (size_t)steps : 0, n_mg = min_margin ? (size_t)std::max(steps, 1) : 0;
+  const size_t o_ord = (size_t)n_mu, o_mg = (o_ord + n_ord + 1) / 2 * 2;  // margins 8-byte aligned
+  int* hp = select_pinned(c, o_mg + 2 * n_mg + 2);
+  ck(cudaMemcpyAsync(hp, perm.p, sizeof(int) * n_mu, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  if (n_ord) ck(cudaMemcpyAsync(hp + o_ord, order.p, sizeof(int) * n_ord, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  if (n_mg) ck(cudaMemcpyAsync(hp + o_mg, margin.p, sizeof(double) * n_mg, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  std::vector<int32_t> pts(hp, hp + n_mu);
   std::sort(pts.begin(), pts.end());
   if (keep) {
     keep->steps = steps;
-    keep->order.resize(steps);
-    download(c, keep->order.data(), order.p, sizeof(int) * steps);
+    keep->order.assign(hp + o_ord, hp + o_ord + n_ord);
     keep->L = std::move(L);
   }
   if (min_margin) {
-    std::vector<double> mg(std::max(steps, 1));
-    download(c, mg.data(), margin.p, sizeof(double) * std::max(steps, 1));
+    const double* hm = reinterpret_cast<const double*>(hp + o_mg);
+    std::vector<double> mg(hm, hm + n_mg);
     double mn = 1.0;
     int at = -1;
     for (int i = 0; i < steps; ++i)
@@ -997,48 +1023,35 @@ void fit_impl(lrgw_ctx c, const double* a, long long lda, int n1, const double* 
 // of L_P^-1 and scatters the pivot-ordered columns into sorted-point order.
 // Returns false (caller falls back to the explicit path) when L_P has a pivot
 // below the LU singularity threshold of linalg.hpp:128, 137.
+// Theta = L L_P^-1 from the selection's factor, enqueued without a host wait:
+// the singularity rule of the LU the reference solves (1e-14 max G(p, p) on
+// L_ii^2, linalg.hpp:128) and trtri's zero-pivot flag land in ff and are
+// checked when the SMW status is read (smw_finish); a failed check rebuilds
+// Theta on the explicit path there. false: not applicable (steps != N_mu).
 bool fused_fit(lrgw_ctx c, const SelectKeep& keep, int n_r, const std::vector<int32_t>& pts_sorted, int n_mu,
-               double* theta, long long ldt, double* diag_ratio) {
+               double* theta, long long ldt, FusedFit& ff) {
   if (keep.steps != n_mu) return false;
-  std::vector<int> order(keep.order.begin(), keep.order.end());
-  DBuf dorder = upload_i(c, order.data(), n_mu);
-  DBuf lp = dalloc(c, (size_t)n_mu * n_mu);
-  ck(gather_rows(c->stream, keep.L.d(), n_r, n_mu, dorder.i(), n_mu, lp.d(), n_mu), "gather");
-  // zero the (numerically tiny) strict upper triangle and check the diagonal
-  ck(zero_strict_upper(c->stream, lp.d(), n_mu, n_mu), "zero_upper");
-  std::vector<double> diag(n_mu);
-  ck(cudaMemcpy2DAsync(diag.data(), sizeof(double), lp.d(), (size_t)(n_mu + 1) * sizeof(double), sizeof(double),
-                       n_mu, cudaMemcpyDeviceToHost, c->stream),
-     "D2H diag");
-  ck(cudaStreamSynchronize(c->stream), "sync");
-  double gmax = 0.0, dmin = HUGE_VAL, dmax = 0.0;
-  for (double v : diag) {
-    gmax = std::max(gmax, v * v);  // G(p_i, p_i) >= L_ii^2; the LU scale
-    dmin = std::min(dmin, std::abs(v));
-    dmax = std::max(dmax, std::abs(v));
-  }
-  // (max |L_ii| / min |L_ii|)^2 is a lower bound on cond(G(P, P)) = cond(L_P)^2
-  if (diag_ratio) *diag_ratio = dmin > 0.0 ? (dmax / dmin) * (dmax / dmin) : HUGE_VAL;
-  const double tiny = 1e-14 * (gmax > 0.0 ? gmax : 1.0);
-  for (double v : diag)
-    if (!(v * v >= tiny)) return false;
-  // X = L_P^-1 in place (trtri.cu: recursive 2 x 2 blocking on the DMMA engine)
-  {
-    DBuf work = dalloc(c, trtri_work_elems(n_mu));
-    DBuf bad = ialloc(c, 1);
-    const int big = 0x7fffffff;
-    ck(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D");
-    ck(lrgw_dev::trtri_lower(c->stream, lp.d(), n_mu, n_mu, work.d(), bad.i(), c->sm_count), "trtri");
-    int h = 0;
-    download(c, &h, bad.p, sizeof(int));
-    if (h != big) return false;
-  }
-  mark(c, 3);  // FIT_SOLVE = gather L_P + trtri; FIT_GEMM = L L_P^-1 below
+  const std::vector<int>& order = keep.order;
   // output column of pivot-ordered column q: its rank among the sorted points
   std::vector<int> colmap(n_mu);
   for (int q = 0; q < n_mu; ++q)
     colmap[q] = (int)(std::lower_bound(pts_sorted.begin(), pts_sorted.end(), order[q]) - pts_sorted.begin());
+  DBuf dorder = upload_i(c, order.data(), n_mu);
   DBuf dmap = upload_i(c, colmap.data(), n_mu);
+  ff.diag = dalloc(c, 4);
+  ff.bad = ialloc(c, 1);
+  DBuf lp = dalloc(c, (size_t)n_mu * n_mu);
+  ck(gather_rows(c->stream, keep.L.d(), n_r, n_mu, dorder.i(), n_mu, lp.d(), n_mu), "gather");
+  // zero the (numerically tiny) strict upper triangle and check the diagonal
+  ck(zero_strict_upper(c->stream, lp.d(), n_mu, n_mu), "zero_upper");
+  ck(diag_stats(c->stream, lp.d(), n_mu, n_mu, ff.diag.d()), "diag_stats");
+  // X = L_P^-1 in place (trtri.cu: recursive 2 x 2 blocking on the DMMA engine)
+  {
+    DBuf work = dalloc(c, trtri_work_elems(n_mu));
+    ck(cudaMemsetAsync(ff.bad.p, 0x7f, sizeof(int), c->stream), "memset");  // 0x7f7f7f7f: no zero pivot
+    ck(lrgw_dev::trtri_lower(c->stream, lp.d(), n_mu, n_mu, work.d(), ff.bad.i(), c->sm_count), "trtri");
+  }
+  mark(c, 3);  // FIT_SOLVE = gather L_P + trtri; FIT_GEMM = L L_P^-1 below
   // B(n, k) = X(k, n) stored n-contiguous (X^T): both operands MN-contiguous
   // for the paired-fragment engine
   DBuf xt = dalloc(c, (size_t)n_mu * n_mu);
@@ -1930,8 +1943,8 @@ lrgw_eps_s* build_one(lrgw_ctx c, const lrgw_build_params& P, const BuildSetup& 
   // stage 2: fused fit from the selection's factor (explicit path otherwise)
   DBuf theta = dalloc(c, (size_t)n_r * n_mu);
   mark(c, 2);  // FIT_LHS is empty on the fused path (lhs lives in L)
-  double lp_ratio = 0.0;
-  const bool fused = fused_fit(c, keep, n_r, pts, n_mu, theta.d(), n_r, &lp_ratio);
+  FusedFit ff;
+  bool fused = fused_fit(c, keep, n_r, pts, n_mu, theta.d(), n_r, ff);
   keep.L.release();
   if (!fused) {  // explicit path re-marks its own lhs / solve boundaries
     fit_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, pts.data(), n_mu, theta.d(), n_r);
@@ -1962,7 +1975,15 @@ lrgw_eps_s* build_one(lrgw_ctx c, const lrgw_build_params& P, const BuildSetup& 
   pvp_impl(c, P.dims, P.cell, P.zero_kernel, theta.d(), n_r, n_mu, pvp.d());
   mark(c, 7);
   smw_join(c, smw);
-  smw_finish(c, smw, pvp.d(), n_mu, k.d());
+  double lp_ratio = 0.0;
+  if (smw_finish(c, smw, pvp.d(), n_mu, k.d(), fused ? &ff : nullptr)) {
+    if (fused) lp_ratio = ff.ratio();
+  } else {  // L_P failed the LU rule: the reference's explicit fit, then stages 4-5 again
+    fused = false;
+    fit_impl(c, phi_v, ldv, n_v, phi_c, ldc, n_c, n_r, pts.data(), n_mu, theta.d(), n_r);
+    pvp_impl(c, P.dims, P.cell, P.zero_kernel, theta.d(), n_r, n_mu, pvp.d());
+    smw_core(c, t.d(), pvp.d(), n_mu, k.d());
+  }
   mark(c, 8);
   timing_end(c);
   auto* e = new_eps(c);

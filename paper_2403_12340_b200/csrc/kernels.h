@@ -164,6 +164,7 @@ cudaError_t axpby(cudaStream_t st, int rows, int cols, double alpha, const doubl
                   double beta, double* y, long long ldy);
 cudaError_t max_abs(cudaStream_t st, const double* x, size_t n, double* d_out);
 // first i with chol(i, i)^2 < 1e-14 max(*max_abs_a, 1 if 0) (or NaN), else -1 -> *out
+cudaError_t diag_stats(cudaStream_t st, const double* a, int n, long long ld, double* out);
 cudaError_t tiny_pivot_dev(cudaStream_t st, const double* chol, int n, long long ld, const double* max_abs_a,
                            int* out);
 // sigma.cu: m = h o m (n x n); out[j] = alpha * a(:, j) . b(:, j).

@@ -1,4 +1,5 @@
 // misc.cu — small elementwise / reduction kernels used around the hot path.
+#include <cfloat>
 #include <climits>
 #include "kernels.h"
 
@@ -185,6 +186,45 @@ __global__ void tiny_pivot_kernel(const double* chol, int n, long long ld, const
   if (mine != INT_MAX) atomicMin(&best, mine);
   __syncthreads();
   if (threadIdx.x == 0) *out = best == INT_MAX ? -1 : best;
+}
+
+// Diagonal of a triangular factor: out = {min |d_i|, max |d_i|, all(d_i^2 >=
+// 1e-14 max d^2) ? 1 : 0}. One CTA (the fused fit's singularity rule, decided
+// on the device so the fit never waits on the host).
+__global__ void diag_stats_kernel(const double* a, int n, long long ld, double* out) {
+  __shared__ double smin[256], smax[256];
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  double mn = HUGE_VAL, mx = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double d = fabs(a[(long long)i * (ld + 1)]);
+    if (!(d <= DBL_MAX)) bad = 1;  // NaN / Inf
+    mn = fmin(mn, d);
+    mx = fmax(mx, d);
+  }
+  smin[threadIdx.x] = mn;
+  smax[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + o]);
+      smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double gmax = smax[0] * smax[0];
+    const double tiny = 1e-14 * (gmax > 0.0 ? gmax : 1.0);
+    out[0] = smin[0];
+    out[1] = smax[0];
+    out[2] = (!bad && smin[0] * smin[0] >= tiny) ? 1.0 : 0.0;
+  }
+}
+
+cudaError_t diag_stats(cudaStream_t st, const double* a, int n, long long ld, double* out) {
+  diag_stats_kernel<<<1, 256, 0, st>>>(a, n, ld, out); count_launches(1);
+  return cudaGetLastError();
 }
 
 cudaError_t tiny_pivot_dev(cudaStream_t st, const double* chol, int n, long long ld, const double* max_abs_a,

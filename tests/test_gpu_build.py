@@ -79,3 +79,34 @@ def test_handles_survive_their_context(L):
     c3.close()
     with pytest.raises(L.InvalidInput):
         L.epsilon_inverse_apply(eps, np.zeros((64, 1)))
+
+
+def test_build_fused_fit_rejected_then_context_reusable(L, ctx):
+    """A pair set of rank 10 < N_mu = 12 (psi_c = psi_v: f g = g f) makes the
+    selection's last pivots numerically zero, so L_P fails the LU rule the
+    fused fit checks on the device (read back with the SMW status): the build
+    falls back to the explicit fit (pinv, isdf.hpp:143-160) and T at the
+    points is singular — the error the reference raises (smw.hpp:49-53). The
+    context must stay usable: the next build equals one on a fresh context."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    n_r = 512
+    f = np.linalg.qr(rng.standard_normal((n_r, 4)))[0]
+    psi = np.concatenate([f, f], axis=1)
+    e = np.array([-0.5, -0.4, -0.3, -0.1, 0.05, 0.2, 0.4, 0.8])
+    d = torch.from_numpy(np.asfortranarray(psi)).cuda().t().contiguous().t()
+    with pytest.raises(L.NumericError):
+        L.build(d[:, :4], d[:, 4:], e, (8, 8, 8), (6.0, 6.0, 6.0), k_mu=3.0, n_lambda=16, ctx=ctx)
+    psi2 = np.linalg.qr(rng.standard_normal((n_r, 32)))[0]
+    e2 = np.concatenate([np.sort(rng.uniform(-0.5, -0.1, 16)), np.sort(rng.uniform(0.05, 0.8, 16))])
+    d2 = torch.from_numpy(np.asfortranarray(psi2)).cuda().t().contiguous().t()
+    ep = L.build(d2[:, :16], d2[:, 16:], e2, (8, 8, 8), (6.0, 6.0, 6.0), k_mu=8.0, n_lambda=16, ctx=ctx)
+    fresh = L.Context(0)
+    ep2 = L.build(d2[:, :16], d2[:, 16:], e2, (8, 8, 8), (6.0, 6.0, 6.0), k_mu=8.0, n_lambda=16, ctx=fresh)
+    assert np.array_equal(ep.point_indices, ep2.point_indices)
+    assert np.array_equal(ep.k, ep2.k) and np.array_equal(ep.p_vc, ep2.p_vc)
+    assert ep.info()["fit_path"] == 0
+    ep.close()
+    ep2.close()
+    fresh.close()
