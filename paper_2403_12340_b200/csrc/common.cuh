@@ -39,6 +39,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// The 1024-byte aligned start of a TMA ring inside the dynamic shared memory
+// (128-byte swizzle keys on shared-address bits 7-9). The pad is added to the
+// array itself: rounding the pointer through an integer makes every later
+// access a generic load (LD.E) instead of LDS.
+__device__ __forceinline__ double* smem_ring_1024(unsigned char* smem_raw) {
+  return reinterpret_cast<double*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+}
+
 // 16-byte async copy global->shared, zero-filled when !pred.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
   const int n = pred ? 16 : 0;

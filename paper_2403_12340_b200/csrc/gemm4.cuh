@@ -84,6 +84,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
+// Releasing a ring slot. A consumer warp must not arrive on a slot's empty
+// barrier while its own shared-memory loads from that slot can still be in
+// flight: ptxas schedules the arrive right behind the last LDS (the MMAs that
+// consume the loaded registers follow it), and a producer blocked on that
+// barrier refills the slot at once — measured on the B200 as run-to-run
+// differences of ~1e-6 (tools/stress_quad.py, tools/bench_quad.py). Every
+// consumer therefore releases k-tile j - 1 right after its wait for k-tile j:
+// the wait's spin loop ends the basic block, so every MMA of tile j - 1 — and
+// with it every load it depends on — has issued. The last k-tile of a kernel
+// is never refilled and needs no release.
+__device__ __forceinline__ void release_prev(uint64_t* empty_prev, int lane) {
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty_prev);
+}
+
 // 2-D TMA load of box (c0 = row, c1 = k) into shared memory, completing on bar.
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
@@ -124,7 +139,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
   constexpr int FM = Cfg::FM, FN = Cfg::FN;
-  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* ring = smem_ring_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * Cfg::STAGE_ELEMS);
   uint64_t* empty = full + STAGES;
 
@@ -205,6 +220,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
         }
     }
     mbar_wait(full + s, (kt / STAGES) & 1);
+    if (kt > 0) {
+      release_prev(empty + (kt - 1) % STAGES, lane);
+      if (!Cfg::PROD && tid == 0 && kt - 1 + STAGES < nkt) {
+        mbar_wait(empty + (kt - 1) % STAGES, ((kt - 1) / STAGES) & 1);
+        issue(kt - 1 + STAGES);
+      }
+    }
     // triangular B: a k-tile wholly left of the warp's first column is zero
     // for the whole warp (the tile-level skip only starts K at n0) — skip its
     // MMAs (exact: the skipped products are zeros)
@@ -219,12 +241,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
         dmma_block<FM, FN>(acc, a0, b0);
         dmma_block<FM, FN>(acc, a1, b1);
       }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + s);
-    if (!Cfg::PROD && tid == 0 && kt + STAGES < nkt) {
-      mbar_wait(empty + s, (kt / STAGES) & 1);
-      issue(kt + STAGES);
     }
   }
   if (!live) return;
@@ -280,7 +296,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
   constexpr int FM = Cfg::FM, FN = Cfg::FN;
-  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* ring = smem_ring_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * Cfg::STAGE_ELEMS);
   uint64_t* empty = full + STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -339,6 +355,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     for (int kt = 0; kt < kt1; ++kt, ++gk) {
       const int s = static_cast<int>(gk % STAGES);
       mbar_wait(full + s, static_cast<unsigned>((gk / STAGES) & 1));
+      if (gk > 0) release_prev(empty + static_cast<int>((gk - 1) % STAGES), lane);
       if (live && kt >= kz) {
         const double* sa = ring + s * Cfg::STAGE_ELEMS;
         const double* sb = sa + Cfg::A_BOXES * Cfg::BOX;
@@ -351,8 +368,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
           dmma_block<FM, FN>(acc, a1, b1);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + s);
     }
     if (!live) continue;
 #pragma unroll
@@ -447,7 +462,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
                    Dgemm4kParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int BM = Cfg::BM, BN = Cfg::BN, STAGES = Cfg::STAGES, FM = Cfg::FM, FN = Cfg::FN;
-  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* ring = smem_ring_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * Cfg::STAGE_ELEMS);
   uint64_t* empty = full + STAGES;
   int tm, tn;
@@ -510,6 +525,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
       }
     }
     mbar_wait(full + s, (kt / STAGES) & 1);
+    if (kt > 0) {
+      release_prev(empty + (kt - 1) % STAGES, lane);
+      if (!Cfg::PROD && tid == 0 && kt - 1 + STAGES < nkt) {
+        mbar_wait(empty + (kt - 1) % STAGES, ((kt - 1) / STAGES) & 1);
+        issue(kt - 1 + STAGES);
+      }
+    }
     if (live) {
       const double* sa = ring + s * Cfg::STAGE_ELEMS;
       const double* sb = sa + BM * 16;
@@ -528,12 +550,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
         dmma_block<FM, FN>(acc, a0, b0);
         dmma_block<FM, FN>(acc, a1, b1);
       }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + s);
-    if (!Cfg::PROD && tid == 0 && kt + STAGES < nkt) {
-      mbar_wait(empty + s, (kt / STAGES) & 1);
-      issue(kt + STAGES);
     }
   }
   if (!live) return;

@@ -123,6 +123,14 @@ cudaError_t quad_nodes(cudaStream_t st, int n_mu, int n_v, int n_c, const double
                        double* running, double beta, double pref, double* t, long long ldt,
                        cudaEvent_t k_begin = nullptr, cudaEvent_t k_end = nullptr);
 
+// The node kernel on the TMA feed (quad4.cu); cudaErrorNotSupported when the
+// panels do not qualify for a tensor map. LRGW_QUAD_TMA=0 keeps the cp.async kernel.
+bool quad_tma_enabled();
+cudaError_t quad_nodes_tma(cudaStream_t st, int n_mu, int n_v, int n_c, const double* pv, long long ldv,
+                           const double* pc, long long ldc, int n_nodes, long long units, const double* dv,
+                           const double* dc, const double* gw, const int* seg_base, int ctas,
+                           double* partial);
+
 // The batched 3-D D2Z of m columns (fft.cu; cuFFT's layout and sign):
 // cudaErrorNotSupported for axes that do not factor into 2, 3, 5 or an odd
 // dims[0] / dims[1] (callers use the cuFFT leaf). LRGW_FFT_OWN=0: always cuFFT.

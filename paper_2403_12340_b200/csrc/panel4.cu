@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 2)
                   const __grid_constant__ CUtensorMap xm, Panel4Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES, FM = Cfg::FM, FN = Cfg::FN, CT = Cfg::CT;
-  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* ring = smem_ring_1024(smem_raw);
   double* park_base = ring + STAGES * Cfg::STAGE_ELEMS;
   uint64_t* full = reinterpret_cast<uint64_t*>(park_base + Cfg::PARK_ELEMS);
   uint64_t* empty = full + STAGES;
@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 2)
   for (int kt = 0; kt < nkt; ++kt) {
     const int s = kt % STAGES;
     mbar_wait(full + s, (kt / STAGES) & 1);
+    if (kt > 0) release_prev(empty + (kt - 1) % STAGES, lane);  // gemm4.cuh: never right behind the slot's own loads
     const double* sa = ring + s * Cfg::STAGE_ELEMS;
     const double* sb = sa + Cfg::A_BOXES * Cfg::BOX;
     if (kt < e3) {
@@ -184,8 +185,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 2)
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + s);
     if (kt == e1 - 1) park_acc();
     if (kt == e2 - 1) {
 #pragma unroll

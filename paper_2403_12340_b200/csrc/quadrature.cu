@@ -321,6 +321,16 @@ cudaError_t quad_nodes(cudaStream_t st, int n_mu, int n_v, int n_c, const double
                    (reinterpret_cast<uintptr_t>(pv) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(pc) % 16 == 0);
   if (k_begin) cudaEventRecord(k_begin, st);
+  // the TMA feed (quad4.cu) wherever the Phi_mu panels qualify for a tensor map
+  bool done = false;
+  if (quad_tma_enabled()) {
+    e = quad_nodes_tma(st, n_mu, n_v, n_c, pv, ldv, pc, ldc, n_nodes, p.units, dv, dc, gw, seg_base, q.ctas,
+                       partial);
+    if (e == cudaSuccess)
+      done = true;
+    else if (e != cudaErrorNotSupported)
+      return e;
+  }
   auto go = [&](auto vec_c, auto bk_c) {
     constexpr int V = decltype(vec_c)::value, B = decltype(bk_c)::value;
     cudaFuncSetAttribute(quad_kernel<V, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, QK<B>::QSMEM);
@@ -337,7 +347,8 @@ cudaError_t quad_nodes(cudaStream_t st, int n_mu, int n_v, int n_c, const double
   if (nb >= 40)
     for (int cand : {48, 40})
       if (waste(cand) < waste(bk)) bk = cand;
-  if (nb >= 64 && bk == 64) {
+  if (done) {
+  } else if (nb >= 64 && bk == 64) {
     using B = std::integral_constant<int, 64>;
     vec ? go(V2{}, B{}) : go(V1{}, B{});
   } else if (nb >= 48 && bk == 48) {

@@ -166,6 +166,12 @@ __global__ void __launch_bounds__(TN_THREADS + 32) tn_bulk_kernel(const double* 
     const int nrow = min(C::R, r1 - (r0 + k * C::R));
     const double* buf = tb_smem + s * C::ST;
     mbar_wait(full + s, (unsigned)((k / TB_S) & 1));
+    // the previous stage goes back only now: an arrive right behind the
+    // stage's own loads lets the refill race them (gemm4.cuh:release_prev)
+    if (k > 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + (k - 1) % TB_S);
+    }
     for (int q = 2 * lane + 64 * part; q < nrow; q += 64 * TB_PARTS) {
       double2 tv[TB_W];
 #pragma unroll
@@ -178,8 +184,6 @@ __global__ void __launch_bounds__(TN_THREADS + 32) tn_bulk_kernel(const double* 
         for (int i = 0; i < TB_W; ++i) acc[i][c] = fma(tv[i].y, xv.y, fma(tv[i].x, xv.x, acc[i][c]));
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + s);
   }
 #pragma unroll
   for (int i = 0; i < TB_W; ++i)
@@ -290,6 +294,10 @@ __global__ void __launch_bounds__(NB_CONS + 32) nn_bulk_kernel(const double* the
     const int s = k % NB_S, mu0 = k * C::CN, ncol = min(C::CN, n_mu - mu0);
     const double* buf = nb_smem + s * C::ST;
     mbar_wait(full + s, (unsigned)((k / NB_S) & 1));
+    if (k > 0) {  // deferred release, as in tn_bulk_kernel
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + (k - 1) % NB_S);
+    }
     if (q < nrow) {
 #pragma unroll 8
       for (int j = 0; j < ncol; ++j) {
@@ -299,8 +307,6 @@ __global__ void __launch_bounds__(NB_CONS + 32) nn_bulk_kernel(const double* the
         for (int c = 0; c < M; ++c) a0[c] = fma(tv, wv[c], a0[c]);
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + s);
   }
   if (q < nrow) {
 #pragma unroll

@@ -90,6 +90,32 @@ def test_quadrature_ragged_shapes(L, ctx, ref, n_mu, n_v, n_c):
         assert rel(L.sum_node_terms(pv, pc, e, spec, nodes, w, ctx=ctx), 0.5 * (acc_ref + acc_ref.T)) <= TOL
 
 
+# the k-tile depths of the TMA feed (quad4.cu: 16 / 24 / 32 / 40 / 48 / 64 by band padding), band
+# tails, ragged row tiles; odd n_mu keeps the cp.async feed
+@pytest.mark.parametrize("n_mu,n_v,n_c", [(130, 17, 33), (192, 120, 120), (256, 48, 96), (320, 64, 128),
+                                          (96, 24, 72), (200, 40, 80), (258, 32, 100), (131, 16, 16)])
+def test_quadrature_feeds_agree(L, ctx, ref, monkeypatch, n_mu, n_v, n_c):
+    rng = np.random.default_rng(n_mu + n_v)
+    pv = rng.standard_normal((n_mu, n_v))
+    pc = rng.standard_normal((n_mu, n_c))
+    e = np.concatenate([np.sort(rng.uniform(-1, -0.2, n_v)), np.sort(rng.uniform(0.1, 2.0, n_c))])
+    s7 = ref.elliptic_params(e, n_v, n_c)
+    assert s7[6] == 0
+    spec = L.elliptic_params(e, n_v, n_c, 1e-7)
+    nodes = np.linspace(-s7[3], s7[3], 11)
+    w = np.linspace(0.2, 0.7, 11)
+    acc_ref = ref.sum_node_terms(pv, pc, e, s7, nodes, w)
+    acc_ref = 0.5 * (acc_ref + acc_ref.T)
+    out = {}
+    for feed in ("0", "1"):
+        monkeypatch.setenv("LRGW_QUAD_TMA", feed)
+        out[feed] = L.sum_node_terms(pv, pc, e, spec, nodes, w, ctx=ctx)
+        assert rel(out[feed], acc_ref) <= TOL
+        again = L.sum_node_terms(pv, pc, e, spec, nodes, w, ctx=ctx)
+        assert np.array_equal(out[feed], again)  # fixed summation order, no staging race
+    assert rel(out["1"], out["0"]) <= 1e-13
+
+
 def test_contour_toy_and_errors(L, ctx):
     # test_contour.cpp:84-95 (T = -0.75), 175-200 (bypass, max_nodes)
     e = [0.0, 2.0, 4.0]
