@@ -509,18 +509,25 @@ def reference_arm(args, cfg, world, workload, metric):
     its Gram LU, the quadrature, sym_eig / LU of the SMW core) are timed once
     per run; every step times the sampled pieces (selection steps,
     apply_coulomb columns, a matmul_tn block) and reports the extrapolated
-    full-build time. Si512 is timed on Si216 through the N^3 model."""
+    full-build time. Si512 is timed on Si216 through the N^3 model; there the
+    once-per-run pieces are bounded too (8 of the 33 nodes, sym_eig on the
+    leading N_mu / 2 block x8, half the per-step samples) so the default
+    --steps 5 --warmup 3 run ends in ~5 minutes instead of 12.5
+    (profiles/r02/bench_reference_si512_session4*.json)."""
     from oracle import cpu_baseline
 
     cores = os.cpu_count() or 1
     ccfg, scale = cpu_config(cfg)
     t_run = time.perf_counter()
-    fixed, fs = cpu_baseline.fixed_pieces(ccfg, cores=cores)
+    big = ccfg.name == "si216"
+    fixed, fs = cpu_baseline.fixed_pieces(ccfg, cores=cores, node_sample=8 if big else None,
+                                          eig_size="half" if big else None)
     t_fixed = time.perf_counter() - t_run
     vals, measured = [], []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        samp, ss = cpu_baseline.sampled_pieces(ccfg, cores=cores, sel_steps=16, cols=32, seed=5 + i)
+        samp, ss = cpu_baseline.sampled_pieces(ccfg, cores=cores, sel_steps=8 if big else 16,
+                                               cols=16 if big else 32, seed=5 + i)
         if i >= args.warmup:
             measured.append(time.perf_counter() - t0)
             vals.append((sum(fixed.values()) + sum(samp.values())) * scale)

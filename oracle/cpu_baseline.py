@@ -50,14 +50,21 @@ def _inputs(cfg, psi, energies, rng):
     return psi, e
 
 
-def fixed_pieces(cfg, psi=None, energies=None, cores=None, fit_rows=(2048, 4096), seed=5, points=None):
+def fixed_pieces(cfg, psi=None, energies=None, cores=None, fit_rows=(2048, 4096), seed=5, points=None,
+                 node_sample=None, eig_size=None):
     """The pieces timed once per run: the reference fit on two row samples
     (each with the full N_mu^3 Gram LU; linear in N_r), the quadrature over
-    all nodes, and the N_mu^3 SMW factorisations (sym_eig, lu_solve, lu_invert)."""
+    all nodes, and the N_mu^3 SMW factorisations (sym_eig, lu_solve, lu_invert).
+    Bounded variants for the large configs: `node_sample` times that many
+    evenly spaced nodes of the trapezoid and scales by (N_lambda + 1) / sample
+    (the node terms cost the same); `eig_size` times sym_eig on the leading
+    block of that size and scales by (N_mu / size)^3 (Householder + QL, cubic)."""
     cores = cores or os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     n_r, n_v, n_c = cfg.n_r, cfg.n_v, cfg.n_c
     n_mu = min(max(R.num_aux(cfg.k_mu, n_v, n_c), 1), n_r)
+    if eig_size == "half":
+        eig_size = n_mu // 2
     rng = np.random.default_rng(seed)
     psi, e = _inputs(cfg, psi, energies, rng)
     a, b = psi[:, :n_v], psi[:, n_v:n_v + n_c]
@@ -84,18 +91,34 @@ def fixed_pieces(cfg, psi=None, energies=None, cores=None, fit_rows=(2048, 4096)
     h = 2 * s7[3] / cfg.n_lambda
     nodes = [-s7[3] + i * h for i in range(cfg.n_lambda + 1)]
     wts = [0.5 * h if i in (0, cfg.n_lambda) else h for i in range(cfg.n_lambda + 1)]
-    t_quad, acc = _t(lambda: ref.sum_node_terms(pv, pc, e, s7, nodes, wts, threads=cores))
-    stages["contour"] = t_quad
+    n_nodes = cfg.n_lambda + 1
+    if node_sample and node_sample < n_nodes:
+        # the timed subset only feeds the timing; the matrix the factorisations
+        # below are timed on is that subset's sum (same structure, negative definite)
+        idx = np.unique(np.linspace(0, n_nodes - 1, node_sample).round().astype(int))
+        nodes_t, wts_t = [nodes[i] for i in idx], [wts[i] * n_nodes / len(idx) for i in idx]
+    else:
+        idx = np.arange(n_nodes)
+        nodes_t, wts_t = nodes, wts
+    t_quad, acc = _t(lambda: ref.sum_node_terms(pv, pc, e, s7, nodes_t, wts_t, threads=cores))
+    stages["contour"] = t_quad * n_nodes / len(idx)
     t_mat = 2 * np.sqrt(s7[0] * s7[1]) / (np.pi * s7[2]) * acc
     t_mat = 0.5 * (t_mat + t_mat.T)
-    t_eig, _ = _t(lambda: ref.sym_eig_values(t_mat))
+    if eig_size and eig_size < n_mu:
+        blk = np.asfortranarray(t_mat[:eig_size, :eig_size])
+        t_eig, _ = _t(lambda: ref.sym_eig_values(blk))
+        t_eig *= (n_mu / eig_size) ** 3
+    else:
+        t_eig, _ = _t(lambda: ref.sym_eig_values(t_mat))
     t_half, half = _t(lambda: ref.lu_solve(t_mat, 0.5 * np.eye(n_mu)))
     mid = 0.5 * (half + half.T) - 1e-3 * np.eye(n_mu)
     t_inv, _ = _t(lambda: ref.lu_solve(mid, np.eye(n_mu)))
     stages["smw_eig"] = t_eig
     stages["smw_lu"] = t_half + t_inv
-    sample = (f"fit on {fit_rows} rows -> linear in N_r={n_r}; all {cfg.n_lambda + 1} nodes; sym_eig / 2 LU at "
-              f"N_mu={n_mu}")
+    nodes_txt = f"all {n_nodes} nodes" if len(idx) == n_nodes else f"{len(idx)}/{n_nodes} nodes x{n_nodes / len(idx):.2f}"
+    eig_txt = (f"sym_eig at {eig_size} x{(n_mu / eig_size) ** 3:.1f}, 2 LU at N_mu={n_mu}"
+               if eig_size and eig_size < n_mu else f"sym_eig / 2 LU at N_mu={n_mu}")
+    sample = f"fit on {fit_rows} rows -> linear in N_r={n_r}; {nodes_txt}; {eig_txt}"
     return stages, sample
 
 

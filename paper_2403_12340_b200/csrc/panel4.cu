@@ -36,6 +36,21 @@ __device__ __forceinline__ void load_frag_swz1(const double* s, int w, int p, in
   }
 }
 
+// dmma_block over the column fragments j >= j0 only (warp-uniform j0): phase 4
+// multiplies by X = L_sel^-1, lower triangular, so k-tile q (W columns
+// 16 q .. 16 q + 15) contributes nothing to output columns below 16 q — the
+// skipped products are exact zeros, the results stay bit for bit.
+template <int FM, int FN>
+__device__ __forceinline__ void dmma_block_from(double (&acc)[FM][FN][2], const double (&af)[FM],
+                                                const double (&bf)[FN], int j0) {
+#pragma unroll
+  for (int j = 0; j < FN; ++j)
+    if (j >= j0) {
+#pragma unroll
+      for (int i = 0; i < FM; ++i) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+}
+
 struct Panel4Params {
   int M, N, K1, K2, K3;
   double* C;
@@ -174,14 +189,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 2)
         if constexpr (FN > 10) {
           double bf[FN];
           load_frag_swz1<FN, BK>(sb, 0, pp, 0, g, t, bf);
-          dmma_block<FM, FN>(acc, a0, bf);
+          dmma_block_from<FM, FN>(acc, a0, bf, 2 * q);
           load_frag_swz1<FN, BK>(sb, 0, pp, 1, g, t, bf);
-          dmma_block<FM, FN>(acc, a1_, bf);
+          dmma_block_from<FM, FN>(acc, a1_, bf, 2 * q);
         } else {
           double b0[FN], b1_[FN];
           load_frag_swz<FN, BK>(sb, 0, pp, g, t, b0, b1_);
-          dmma_block<FM, FN>(acc, a0, b0);
-          dmma_block<FM, FN>(acc, a1_, b1_);
+          dmma_block_from<FM, FN>(acc, a0, b0, 2 * q);
+          dmma_block_from<FM, FN>(acc, a1_, b1_, 2 * q);
         }
       }
     }
