@@ -510,24 +510,29 @@ def reference_arm(args, cfg, world, workload, metric):
     per run; every step times the sampled pieces (selection steps,
     apply_coulomb columns, a matmul_tn block) and reports the extrapolated
     full-build time. Si512 is timed on Si216 through the N^3 model; there the
-    once-per-run pieces are bounded too (8 of the 33 nodes, sym_eig on the
-    leading N_mu / 2 block x8, half the per-step samples) so the default
-    --steps 5 --warmup 3 run ends in ~5 minutes instead of 12.5
-    (profiles/r02/bench_reference_si512_session4*.json)."""
+    quadrature is timed on 8 of its 33 nodes (the node terms cost the same),
+    and the seeded orbitals are generated once per run, not per step (that
+    QR alone was ~25 s of every step: 12.5 min for --steps 5 --warmup 3,
+    profiles/r02/bench_reference_si512_session4_full_pieces.json). Bounding
+    sym_eig by a half-size block or halving the per-step samples was tried
+    and dropped: the N^3 model under-predicts sym_eig 2.7x at 3456 and the
+    smaller samples moved the fit / pvp extrapolations by +20..+140 %."""
     from oracle import cpu_baseline
 
     cores = os.cpu_count() or 1
     ccfg, scale = cpu_config(cfg)
     t_run = time.perf_counter()
     big = ccfg.name == "si216"
-    fixed, fs = cpu_baseline.fixed_pieces(ccfg, cores=cores, node_sample=8 if big else None,
-                                          eig_size="half" if big else None)
+    # the seeded inputs once per run (the QR of the N_r x (N_v + N_c) Gaussian is ~20 s at Si216)
+    rng = np.random.default_rng(5)
+    psi, e_in = cpu_baseline._inputs(ccfg, None, None, rng)
+    fixed, fs = cpu_baseline.fixed_pieces(ccfg, psi=psi, energies=e_in, cores=cores,
+                                          node_sample=8 if big else None)
     t_fixed = time.perf_counter() - t_run
     vals, measured = [], []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        samp, ss = cpu_baseline.sampled_pieces(ccfg, cores=cores, sel_steps=8 if big else 16,
-                                               cols=16 if big else 32, seed=5 + i)
+        samp, ss = cpu_baseline.sampled_pieces(ccfg, psi=psi, cores=cores, sel_steps=16, cols=32, seed=5 + i)
         if i >= args.warmup:
             measured.append(time.perf_counter() - t0)
             vals.append((sum(fixed.values()) + sum(samp.values())) * scale)

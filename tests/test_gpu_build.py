@@ -110,3 +110,34 @@ def test_build_fused_fit_rejected_then_context_reusable(L, ctx):
     ep.close()
     ep2.close()
     fresh.close()
+
+
+@pytest.mark.parametrize("name,reps", [("si8", 6), ("si64", 4)])
+def test_repeated_builds_are_bit_identical(L, ctx, name, reps):
+    """Every reduction of the build has a fixed order (segment partials,
+    split-K slots, per-band column sums), so repeated builds of the same
+    inputs must agree bit for bit in the points, Theta, T and K. A mismatch
+    is a staging race in a ring engine (the class found in the TMA K3 kernel:
+    a slot released right behind its own shared-memory loads;
+    gemm4.cuh:release_prev, tools/stress_build.py runs the long version)."""
+    import torch
+
+    from paper_2403_12340_b200 import synth
+
+    cfg = synth.CONFIGS[name]
+    psi = synth.orbitals_device(cfg)
+    e = synth.energies(cfg)
+    first = None
+    for _ in range(reps):
+        ep = L.build(psi[:, :cfg.n_v], psi[:, cfg.n_v:], e, cfg.dims, cfg.cell3, k_mu=cfg.k_mu,
+                     n_lambda=cfg.n_lambda, ctx=ctx)
+        th_p, k_p, t_p = ep.device_ptrs()
+        cur = (np.array(ep.point_indices), L_tensor(th_p, (cfg.n_r, ep.n_mu)).clone(),
+               L_tensor(t_p, (ep.n_mu, ep.n_mu)).clone(), L_tensor(k_p, (ep.n_mu, ep.n_mu)).clone())
+        ep.close()
+        if first is None:
+            first = cur
+            continue
+        assert np.array_equal(cur[0], first[0])
+        for got, want in zip(cur[1:], first[1:]):
+            assert torch.equal(got, want)
