@@ -527,7 +527,8 @@ def reference_arm(args, cfg, world, workload, metric):
     rng = np.random.default_rng(5)
     psi, e_in = cpu_baseline._inputs(ccfg, None, None, rng)
     fixed, fs = cpu_baseline.fixed_pieces(ccfg, psi=psi, energies=e_in, cores=cores,
-                                          node_sample=8 if big else None)
+                                          node_sample=8 if big else None,
+                                          fit_rows="wide" if big else (2048, 4096))
     t_fixed = time.perf_counter() - t_run
     vals, measured = [], []
     for i in range(args.warmup + args.steps):

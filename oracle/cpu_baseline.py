@@ -65,6 +65,11 @@ def fixed_pieces(cfg, psi=None, energies=None, cores=None, fit_rows=(2048, 4096)
     n_mu = min(max(R.num_aux(cfg.k_mu, n_v, n_c), 1), n_r)
     if eig_size == "half":
         eig_size = n_mu // 2
+    if fit_rows == "wide":
+        # two row counts 2048 apart: with N_mu = 3456 the default (2048, 4096) clamps to
+        # (3457, 4096), and a 639-row difference extrapolated to 373 248 rows turned +-2 s of
+        # timing noise into +-45 % of the fit stage (33 000 .. 88 000 s across three runs)
+        fit_rows = (n_mu + 1, n_mu + 1 + 2048)
     rng = np.random.default_rng(seed)
     psi, e = _inputs(cfg, psi, energies, rng)
     a, b = psi[:, :n_v], psi[:, n_v:n_v + n_c]
