@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-for r in 1 2; do
-( time timeout 1790 python bench.py --impl reference --gpus 1 --steps 5 --warmup 3 > gpurun_out/bench_reference_wide_$r.log 2>&1 ) 2> gpurun_out/bench_reference_wide_time_$r.log; tail -3 gpurun_out/bench_reference_wide_time_$r.log | head -1; cut -c1-160 gpurun_out/bench_reference_wide_$r.log | tail -1
-done
+timeout 900 python tools/stress_build.py si64 150 2>&1 | tail -1
+timeout 900 python tools/stress_build.py c60 30 2>&1 | tail -1
+timeout 900 python tools/stress_build.py si216 12 2>&1 | tail -1
+timeout 1200 python tools/stress_build.py si512 3 2>&1 | tail -1
