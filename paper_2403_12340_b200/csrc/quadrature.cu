@@ -16,6 +16,12 @@
 // sequence (the pipeline never drains at node or tile boundaries) and writes
 // one 64 x 64 partial per tile segment it touches; a fixed-order reduction
 // sums the segments of each tile. Phi_mu panels are L2-resident (2 MB at Si64).
+//
+// This file holds the schedule (quad_plan), the reduction and the cp.async
+// feed of the node kernel; quad_nodes runs the node kernel on the TMA feed
+// (quad4.cu: same schedule, partial layout and node order) whenever the
+// Phi_mu panels qualify for a tensor map (16-byte aligned base, even leading
+// dimension) and keeps the cp.async kernel below for the rest.
 #include <algorithm>
 #include <type_traits>
 #include <vector>
