@@ -156,7 +156,15 @@ cudaError_t dgemm_tma_k(cudaStream_t st, int M, int N, int K, const double* A, l
   switch (kcfg(M)) {
     case 1: return launch4k<K4P>(st, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, scale, lower, splits, k_chunk, partial);
     case 2: return launch4k<K4S>(st, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, scale, lower, splits, k_chunk, partial);
-    default: return launch4k<K4>(st, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, scale, lower, splits, k_chunk, partial);
+    default: {
+      // ring depth of the 128 x 128 configuration (LRGW_TMA_KSTAGES = 5 / 6 / 7; 32 KB per stage)
+      static const int stages = getenv("LRGW_TMA_KSTAGES") ? atoi(getenv("LRGW_TMA_KSTAGES")) : 5;
+      if (stages == 7)
+        return launch4k<Gemm4kCfg<128, 128, 64, 32, 7, 1>>(st, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, scale, lower, splits, k_chunk, partial);
+      if (stages == 6)
+        return launch4k<Gemm4kCfg<128, 128, 64, 32, 6, 1>>(st, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, scale, lower, splits, k_chunk, partial);
+      return launch4k<K4>(st, M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, scale, lower, splits, k_chunk, partial);
+    }
   }
 }
 
@@ -203,14 +211,17 @@ cudaError_t dgemm_tma(cudaStream_t st, int M, int N, int K, const double* A, lon
   if (mncfg() == 1) return launch4<T4S>(st, ma, mb, ma, mb, p);
   if (persist_enabled()) {
     using C = T4<128>;
-    auto kern = dgemm4p_kernel<C>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    using C6 = Gemm4Cfg<128, 128, 64, 32, kBK, 6, false, 1>;  // LRGW_TMA_MNSTAGES=6: a 6-deep ring (192 KB)
+    static const int stages = getenv("LRGW_TMA_MNSTAGES") ? atoi(getenv("LRGW_TMA_MNSTAGES")) : 4;
+    auto kern = stages == 6 ? dgemm4p_kernel<C6> : dgemm4p_kernel<C>;
+    const int smem = stages == 6 ? C6::SMEM_BYTES : C::SMEM_BYTES;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     const int tm = (M + C::BM - 1) / C::BM, tn = (N + C::BN - 1) / C::BN;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int grid = std::min(tm * tn, sms * C::MINB);
-    kern<<<grid, C::THREADS, C::SMEM_BYTES, st>>>(ma, mb, p, tm, tn);
+    kern<<<grid, C::THREADS, smem, st>>>(ma, mb, p, tm, tn);
     count_launches(1);
     return cudaGetLastError();
   }
