@@ -1,4 +1,11 @@
 mkdir -p gpurun_out
-timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "quadrature_feeds or quadrature_ragged or node_terms" > gpurun_out/sanitizer_memcheck_quad.log 2>&1; echo "memcheck quad rc=$?"; tail -4 gpurun_out/sanitizer_memcheck_quad.log
-timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 9 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/sanitizer_memcheck_smoke.log 2>&1; echo "memcheck smoke rc=$?"; tail -3 gpurun_out/sanitizer_memcheck_smoke.log | cut -c1-200
-timeout 1500 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "quadrature_feeds" > gpurun_out/sanitizer_racecheck_quad.log 2>&1; echo "racecheck quad rc=$?"; tail -6 gpurun_out/sanitizer_racecheck_quad.log | cut -c1-200
+timeout 600 python bench.py --config si64 --mode sharded --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_si64_sharded1.log 2>&1; echo "rc=$?"
+timeout 900 python bench.py --config si216 --mode sharded --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_si216_sharded1.log 2>&1; echo "rc=$?"
+python - <<'PY'
+import json
+for f in ['gpurun_out/bench_si64_sharded1.log','gpurun_out/bench_si216_sharded1.log']:
+  for l in open(f):
+    if l.startswith('{'):
+        d=json.loads(l); print(d['value'], d['config'].get('parallelism'), {k:round(v,2) for k,v in d.get('stages_ms',{}).items() if k in ('select','fit_gemm','contour','fft','pvp','smw','total')})
+PY
+tail -2 gpurun_out/bench_si64_sharded1.log | cut -c1-300
