@@ -1,3 +1,4 @@
-mkdir -p gpurun_out
-timeout 2700 python -m pytest tests -m gpu -x -q -rf > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log; tail -3 gpurun_out/gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log | cut -c1-120
+for bk in 16 24 32 40 48 64; do LRGW_QUAD_BK=$bk timeout 600 python tools/stress_quad.py si216 60 2>&1 | tail -1; done
+for bk in 16 32 64; do LRGW_QUAD_BK=$bk timeout 600 python tools/stress_quad.py si512 6 2>&1 | tail -1; done
+timeout 600 python tools/stress_quad.py si64 500 2>&1 | tail -1
+timeout 600 python tools/stress_quad.py c60 300 2>&1 | tail -1
